@@ -1,0 +1,195 @@
+/*
+ * mgm.h -- C ABI of libmgm, a B200-native (sm_100a, fp64) implementation of the solve path
+ * of the meshfree geometric multilevel (MGM) method, arXiv 2204.06154.
+ *
+ * Citations: P:n = line n of the paper text; O1..O17 = the readings written out
+ * in DESIGN.md ("Readings of the paper").
+ *
+ * Problem: solve L_h u = f on a point cloud X_h of a closed surface, with
+ *   L_h = I - mu D_h   (shifted surface Poisson, problem = 0), or
+ *   L_h = D_h          (surface Poisson, problem = 1; solved as the bordered system
+ *                       [L 1; 1^T 0][u; lambda] = [f; 0]),
+ * D_h the RBF-FD or GFD Laplace-Beltrami matrix.  MGM (Alg. 2,
+ * P:361-378; Alg. 3) is used standalone or as the right preconditioner of
+ * GMRES.
+ *
+ * Conventions (all entry points):
+ *  - No C++ types cross this boundary.  Every call returns mgm_status; nothing throws.
+ *  - Host arrays ("host") are read during the call only and may be freed afterwards.
+ *  - Device arrays ("device") are caller-owned, contiguous fp64 buffers on the ctx's GPU.
+ *  - User vectors are in the caller's ORIGINAL point order; the library applies and undoes
+ *    its internal ordering (Morton order, O1, in place of RCM, P:283/P:390/P:404).
+ *  - Calls are ordered on the given CUDA stream (cudaStream_t passed as void*, NULL = the
+ *    legacy default stream).  A ctx is not re-entrant: one call at a time per ctx.
+ *  - On error, mgm_last_error() returns a message and the failing index (stencil centre,
+ *    fine row, or pivot) where one exists.
+ */
+#ifndef MGM_H
+#define MGM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct mgm_ctx mgm_ctx; /* opaque; owns the device hierarchy, workspaces, graphs */
+
+typedef enum {
+    MGM_OK = 0,
+    MGM_ERR_ARG = 1,        /* invalid argument (sizes, parameters, NULL pointers)          */
+    MGM_ERR_UNISOLVENT = 2, /* RBF-FD/GFD stencil system singular; index = stencil centre   */
+    MGM_ERR_SINGULAR = 3,   /* transfer system (index = fine row) or coarse LU (index = pivot) */
+    MGM_ERR_BREAKDOWN = 4,  /* GMRES breakdown with a nonzero residual                       */
+    MGM_ERR_CUDA = 5,       /* CUDA runtime error                                             */
+    MGM_ERR_NCCL = 6,       /* reserved (multi-GPU)                                           */
+    MGM_ERR_OOM = 7,        /* device allocation failed                                       */
+    MGM_ERR_INPUT = 8       /* duplicate points / non-finite input; index = offending point  */
+} mgm_status;
+
+/* Discretisation of the surface operator (Section 2 of the paper). */
+typedef struct {
+    int method;       /* 0 = PHS RBF-FD, 1 = GFD                     */
+    int poly_degree;  /* ell: degree of the tangent-plane polynomials, 0..8          */
+    int phs_k;        /* k: PHS kernel r^(2k+1), 1 <= k <= ell (k=0 has no Laplacian) */
+    int stencil_n;    /* n: stencil size incl. the centre, nearest in R^3; <= 96      */
+    double gfd_alpha; /* alpha of the GFD Gaussian weight                            */
+    int problem;      /* 0 = shifted (L = I - mu D), 1 = Poisson (L = D, mean-zero border)   */
+    double mu;        /* mu > 0 of the shifted problem                                 */
+} mgm_stencil_params;
+
+/* Multilevel parameters (Section 4; Table 1). */
+typedef struct {
+    int num_levels;     /* p; 0 = the paper's rule p = floor(log(N/n_min)/log 4) + 1 */
+    int n_min;          /* N_min for the rule above (Table 1: 250)                            */
+    int coarsen_factor; /* N_{j+1} = floor(N_j / factor); the paper uses 4            */
+    int interp_m;       /* m: nearest coarse points per interpolation stencil, <= 16   */
+    int nu1, nu2;       /* pre-/post-smoothing sweeps                                  */
+    int smoother;       /* 0 forward GS both, 1 backward both, 2 forward pre/backward post    */
+    int restart;        /* GMRES restart length (<= 128)                                       */
+} mgm_level_params;
+
+typedef struct {
+    int iterations;            /* GMRES: preconditioner applications in Arnoldi; standalone: V-cycles */
+    int converged;             /* 1 if the stopping test was met                                        */
+    double final_rel_residual; /* true ||b - A x||_2 / ||b||_2 at exit                                  */
+    double* history;           /* caller-owned host buffer (or NULL): relative residual per iteration   */
+    int history_cap;           /* capacity of history                                                   */
+    double lambda;             /* Poisson mode: Lagrange multiplier of the border               */
+    double setup_ms;           /* device+host time of mgm_setup                                         */
+    double solve_ms;           /* device time of this solve (CUDA events on the stream)                 */
+} mgm_report;
+
+/* Build the hierarchy (Alg. 2) on the current CUDA device.
+ * points, normals: host, n_points x 3 row-major fp64 (normals unit length).  Copied.
+ * On success *out receives a new ctx (free with mgm_destroy).  Errors: MGM_ERR_ARG,
+ * MGM_ERR_INPUT (index = point), MGM_ERR_UNISOLVENT (index = centre, original order),
+ * MGM_ERR_SINGULAR, MGM_ERR_CUDA, MGM_ERR_OOM.  If out is non-NULL and the failure happened
+ * after allocation, *out is set to a ctx that only carries the error (query with
+ * mgm_last_error, then mgm_destroy). */
+mgm_status mgm_setup(const double* points, const double* normals, int64_t n_points,
+                     const mgm_stencil_params* stencil, const mgm_level_params* levels,
+                     void* cuda_stream, mgm_ctx** out);
+
+/* One V(nu1,nu2)-cycle (Alg. 3): u <- MGM(f, u).
+ * f_dev, u_dev: device, n_points fp64, original order; u_dev is the initial guess on entry
+ * and the result on exit.  Poisson mode: lambda starts at 0 and is not returned. */
+mgm_status mgm_vcycle(mgm_ctx* ctx, const double* f_dev, double* u_dev, void* cuda_stream);
+
+/* Solve L u = rhs (Poisson: the bordered system) to ||rhs - L x|| / ||rhs|| <= tol.
+ * krylov = 1: right-preconditioned GMRES(restart) with one V-cycle from a zero guess as the
+ *             preconditioner;  krylov = 0: standalone MGM.
+ * rhs_dev, x_dev: device, n_points fp64, original order; x_dev is ignored on entry (zero
+ * initial guess) and receives the solution.  rhs = 0 gives x = 0 with 0 iterations.
+ * Non-convergence within maxit is NOT an error (converged = 0).  report may be NULL. */
+mgm_status mgm_solve(mgm_ctx* ctx, const double* rhs_dev, double* x_dev, double tol, int maxit,
+                     int krylov, mgm_report* report, void* cuda_stream);
+
+/* Same as mgm_solve with HOST vectors (pinned or pageable): copies rhs in and x out on the
+ * stream inside the call (the end-to-end path). */
+mgm_status mgm_solve_host(mgm_ctx* ctx, const double* rhs_host, double* x_host, double tol,
+                          int maxit, int krylov, mgm_report* report, void* cuda_stream);
+
+mgm_status mgm_destroy(mgm_ctx* ctx);
+
+/* Message of the last failure on this ctx (or of the last failed mgm_setup on this thread
+ * when ctx is NULL); *failing_index (if non-NULL) receives the index or -1. */
+const char* mgm_last_error(const mgm_ctx* ctx, int64_t* failing_index);
+
+/* ---------------- introspection and test hooks (not on the timed path) ---------------- */
+
+mgm_status mgm_num_levels(const mgm_ctx* ctx, int* p);
+
+/* Level j (0 = finest): rows, stored nonzeros of L_j (symbolic pattern), nonzeros of the
+ * interpolation P_j = I_{j+1}^j (0 on the coarsest level), number of GS colours (0 on the
+ * coarsest), and the bytes the solve-phase layout of level j occupies on the device. */
+mgm_status mgm_level_info(const mgm_ctx* ctx, int level, int64_t* n_rows, int64_t* nnz_L,
+                          int64_t* nnz_P, int* n_colours, int64_t* stored_bytes);
+
+/* Copy level j's discrete structures to HOST buffers (any may be NULL), in the library's
+ * level ordering ("lib order": rows grouped by colour, Morton order within a colour):
+ *   ids[n_rows]          original point index of each row
+ *   L_ptr[n_rows+1], L_col[nnz_L] (lib-order column), L_val[nnz_L]: CSR of L_j, columns
+ *                        ascending in Morton order with the diagonal first
+ *   colour[n_rows]       GS colour of each row (all 0 on the coarsest level)
+ *   P_ptr[n_rows+1], P_col[nnz_P] (next level's lib order), P_val[nnz_P]: CSR of P_j
+ *   border[n_rows]       Poisson border vector c_j (c_1 = 1, c_{j+1} = P_j^T c_j) */
+mgm_status mgm_export_level(const mgm_ctx* ctx, int level, int64_t* ids, int64_t* L_ptr,
+                            int32_t* L_col, double* L_val, int32_t* colour, int64_t* P_ptr,
+                            int32_t* P_col, double* P_val, double* border);
+
+/* Fine-level stencil weights c_ij as computed on the GPU, host output
+ * w[n_points * stencil_n] and stencil indices sten[n_points * stencil_n] (original point
+ * indices, centre first, O2 order), both in ORIGINAL row order. */
+mgm_status mgm_export_weights(const mgm_ctx* ctx, double* w, int64_t* sten);
+
+/* Operators on level j, device vectors in lib order (n_j entries; Poisson: n_j + 1 with the
+ * multiplier last):
+ *   MGM_OP_SPMV      y = L_j x                         (Poisson: [L x + c x_N; c^T x])
+ *   MGM_OP_SWEEP     y = x after ONE forward colour GS sweep with rhs f; y may == x
+ *   MGM_OP_RESIDUAL  y = f - L_j x                     (Poisson: bordered)
+ *   MGM_OP_RESTRICT  y (n_{j+1}) = R_j x               (Poisson: multiplier copied)
+ *   MGM_OP_INTERP    y (n_j) = P_j x (x has n_{j+1})   (Poisson: multiplier copied)
+ *   MGM_OP_COARSE    y = L_p^{-1} x on the coarsest level (level ignored)
+ * f is used by SWEEP and RESIDUAL only. */
+enum { MGM_OP_SPMV = 0, MGM_OP_SWEEP = 1, MGM_OP_RESIDUAL = 2, MGM_OP_RESTRICT = 3,
+       MGM_OP_INTERP = 4, MGM_OP_COARSE = 5 };
+mgm_status mgm_apply(mgm_ctx* ctx, int level, int op, const double* x_dev, const double* f_dev,
+                     double* y_dev, void* cuda_stream);
+
+/* Per-kernel-class device timing (CUDA events around every launch of that class on the
+ * solve stream; adds events, use only for measurement).  cls: 0 = level-0 GS colour sweep
+ * kernels, 1 = level-0 SpMV, 2 = whole V-cycle.  enable = 1 resets the accumulators. */
+mgm_status mgm_timing_enable(mgm_ctx* ctx, int cls, int enable);
+/* total_ms = sum of event-measured durations, launches = number of timed launches,
+ * alg_bytes = algorithmic bytes those launches move (DESIGN.md byte model). */
+mgm_status mgm_timing_read(mgm_ctx* ctx, int cls, double* total_ms, int64_t* launches,
+                           double* alg_bytes);
+
+/* Algorithmic bytes of one V-cycle and one GMRES Arnoldi step k (DESIGN.md byte model). */
+mgm_status mgm_bytes_model(const mgm_ctx* ctx, double* vcycle_bytes, double* spmv_bytes);
+
+/* Number of kernels launched by one V-cycle (graph nodes). */
+mgm_status mgm_vcycle_kernel_count(const mgm_ctx* ctx, int64_t* count);
+
+/* ---------------- host-only hooks of the setup's discrete steps (no GPU needed) --------
+ * They run the same host code mgm_setup uses, so discrete-structure parity with the
+ * oracle can be checked on a CPU-only machine. */
+
+/* Morton order (O1, replaces RCM of P:283): perm[new] = old.  host arrays. */
+mgm_status mgm_host_morton(const double* points, int64_t n, int64_t* perm);
+/* k nearest `points` of each query (O2 order: squared distance, then index).
+ * out[nq * k] int32 indices into points. */
+mgm_status mgm_host_knn(const double* points, int64_t n, const double* queries, int64_t nq,
+                        int k, int32_t* out);
+/* Weighted sample elimination of n points down to nt (O8). keep[nt] ascending. */
+mgm_status mgm_host_wse(const double* points, int64_t n, int64_t nt, int64_t* keep);
+/* Greedy colouring (O11) of sym(pattern) minus the diagonal, vertices in index order.
+ * CSR pattern ptr[n+1], col[ptr[n]]; colour[n] out; *n_colours out. */
+mgm_status mgm_host_colouring(int64_t n, const int64_t* ptr, const int32_t* col, int32_t* colour,
+                              int* n_colours);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MGM_H */

@@ -165,7 +165,8 @@ int orc_tangent_project(const double* pts, const double* nrm, const i64* sten, i
 
 /* ------------------------------------------------------------------------------------
  * Dense LU with partial pivoting (ties -> lowest row), RHS eliminated alongside,
- * back substitution in ascending column order.  M is m x m row-major, overwritten.
+ * back substitution x_i = (b_i - sum_{j=m-1 down to i+1} M_ij x_j) / M_ii (the sum taken
+ * in descending j).  M is m x m row-major, overwritten.
  * Returns the failing pivot column + 1 if |pivot| <= tol * max|M|, else 0.
  * ---------------------------------------------------------------------------------- */
 static int lu_solve_inplace(double* M, double* b, int m, double tol) {
@@ -191,7 +192,7 @@ static int lu_solve_inplace(double* M, double* b, int m, double tol) {
     }
     for (int i = m - 1; i >= 0; --i) {
         double s = b[i];
-        for (int j = i + 1; j < m; ++j) s = s - M[i * m + j] * b[j];
+        for (int j = m - 1; j > i; --j) s = s - M[i * m + j] * b[j];
         b[i] = s / M[i * m + i];
     }
     return 0;

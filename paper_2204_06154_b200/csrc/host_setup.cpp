@@ -1,0 +1,444 @@
+// Host-side setup of libmgm: Morton ordering, exact grid kNN, weighted sample elimination,
+// greedy colouring, CSR transpose, dense LU.  Compiled with -O3 -ffp-contract=off so that
+// every floating-point decision (distances, WSE weights) follows DESIGN.md's written rules
+// bit for bit.  Citations: P:n = PAPER.md line n; O-numbers = DESIGN.md readings.
+#include "mgm_internal.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <thread>
+
+namespace mgm {
+
+template <class F>
+static void parallel_for(i64 n, int nthreads, F&& f) {
+    if (nthreads <= 1 || n < 4096) {
+        f(0, n);
+        return;
+    }
+    std::vector<std::thread> th;
+    i64 chunk = (n + nthreads - 1) / nthreads;
+    for (int t = 0; t < nthreads; ++t) {
+        i64 b = t * chunk, e = std::min(n, b + chunk);
+        if (b >= e) break;
+        th.emplace_back([&f, b, e] { f(b, e); });
+    }
+    for (auto& x : th) x.join();
+}
+
+// ---------------------------------------------------------------------------------------
+// O1: Morton order.  Quantise each axis with the common extent to 21 bits, interleave
+// (x at bit 3b+2, y at 3b+1, z at 3b), sort by (key, index).
+// ---------------------------------------------------------------------------------------
+static inline uint64_t spread3(uint64_t v) {  // 21 bits -> every third bit
+    v &= 0x1fffffull;
+    v = (v | (v << 32)) & 0x1f00000000ffffull;
+    v = (v | (v << 16)) & 0x1f0000ff0000ffull;
+    v = (v | (v << 8)) & 0x100f00f00f00f00full;
+    v = (v | (v << 4)) & 0x10c30c30c30c30c3ull;
+    v = (v | (v << 2)) & 0x1249249249249249ull;
+    return v;
+}
+
+bool morton_order(const double* pts, i64 n, std::vector<i64>& perm) {
+    double lo[3], hi[3];
+    for (int a = 0; a < 3; ++a) lo[a] = hi[a] = pts[a];
+    for (i64 i = 0; i < n; ++i)
+        for (int a = 0; a < 3; ++a) {
+            lo[a] = std::min(lo[a], pts[3 * i + a]);
+            hi[a] = std::max(hi[a], pts[3 * i + a]);
+        }
+    double ext = std::max(hi[0] - lo[0], std::max(hi[1] - lo[1], hi[2] - lo[2]));
+    if (!(ext > 0.0)) return false;
+    std::vector<std::pair<uint64_t, i64>> keys(n);
+    for (i64 i = 0; i < n; ++i) {
+        uint64_t q[3];
+        for (int a = 0; a < 3; ++a) {
+            double s = std::floor(((pts[3 * i + a] - lo[a]) / ext) * 2097152.0);
+            i64 v = (i64)s;
+            q[a] = (uint64_t)std::min<i64>(std::max<i64>(v, 0), 2097151);
+        }
+        keys[i] = {(spread3(q[0]) << 2) | (spread3(q[1]) << 1) | spread3(q[2]), i};
+    }
+    std::sort(keys.begin(), keys.end());
+    perm.resize(n);
+    for (i64 i = 0; i < n; ++i) perm[i] = keys[i].second;
+    return true;
+}
+
+// ---------------------------------------------------------------------------------------
+// Uniform grid over a point set (cells sorted by linear id; dense cell table).
+// ---------------------------------------------------------------------------------------
+namespace {
+struct Grid {
+    double lo[3], cell;
+    i64 dims[3];
+    std::vector<i64> start;  // ncell + 1
+    std::vector<i32> items;
+    const double* pts;
+
+    void build(const double* p, i64 n, double cell_size) {
+        pts = p;
+        for (int a = 0; a < 3; ++a) lo[a] = p[a];
+        double hi[3] = {p[0], p[1], p[2]};
+        for (i64 i = 0; i < n; ++i)
+            for (int a = 0; a < 3; ++a) {
+                lo[a] = std::min(lo[a], p[3 * i + a]);
+                hi[a] = std::max(hi[a], p[3 * i + a]);
+            }
+        cell = cell_size;
+        i64 total = 1;
+        for (int a = 0; a < 3; ++a) {
+            dims[a] = std::max<i64>(1, (i64)std::floor((hi[a] - lo[a]) / cell) + 1);
+            total *= dims[a];
+        }
+        // keep the dense table bounded (cells only grow, so correctness is unaffected)
+        while (total > 4 * n + 64) {
+            cell *= 1.26;
+            total = 1;
+            for (int a = 0; a < 3; ++a) {
+                dims[a] = std::max<i64>(1, (i64)std::floor((hi[a] - lo[a]) / cell) + 1);
+                total *= dims[a];
+            }
+        }
+        start.assign(total + 1, 0);
+        std::vector<i64> cid(n);
+        for (i64 i = 0; i < n; ++i) {
+            cid[i] = cell_of(p + 3 * i);
+            start[cid[i] + 1]++;
+        }
+        for (i64 c = 0; c < total; ++c) start[c + 1] += start[c];
+        items.resize(n);
+        std::vector<i64> fill(start.begin(), start.end() - 1);
+        for (i64 i = 0; i < n; ++i) items[fill[cid[i]]++] = (i32)i;
+    }
+    void coords(const double* x, i64* c) const {
+        for (int a = 0; a < 3; ++a) {
+            i64 v = (i64)std::floor((x[a] - lo[a]) / cell);
+            c[a] = std::min<i64>(std::max<i64>(v, 0), dims[a] - 1);
+        }
+    }
+    i64 cell_of(const double* x) const {
+        i64 c[3];
+        coords(x, c);
+        return (c[2] * dims[1] + c[1]) * dims[0] + c[0];
+    }
+};
+
+// O2 squared distance: dx = y - x; (dx*dx + dy*dy) + dz*dz, no FMA (-ffp-contract=off).
+inline double dist2(const double* x, const double* y) {
+    double dx = y[0] - x[0], dy = y[1] - x[1], dz = y[2] - x[2];
+    double s = dx * dx + dy * dy;
+    return s + dz * dz;
+}
+
+struct KBest {
+    int k;
+    double* d;
+    i32* j;
+    int count = 0;
+    void reset() { count = 0; }
+    bool full() const { return count == k; }
+    // insert keeping ascending (d, j)
+    void offer(double dd, i32 jj) {
+        if (count == k && (dd > d[k - 1] || (dd == d[k - 1] && jj > j[k - 1]))) return;
+        int p = (count < k) ? count++ : k - 1;
+        while (p > 0 && (d[p - 1] > dd || (d[p - 1] == dd && j[p - 1] > jj))) {
+            d[p] = d[p - 1];
+            j[p] = j[p - 1];
+            --p;
+        }
+        d[p] = dd;
+        j[p] = jj;
+    }
+};
+
+double default_cell(const double* p, i64 n, int k) {
+    double lo[3] = {p[0], p[1], p[2]}, hi[3] = {p[0], p[1], p[2]};
+    for (i64 i = 0; i < n; ++i)
+        for (int a = 0; a < 3; ++a) {
+            lo[a] = std::min(lo[a], p[3 * i + a]);
+            hi[a] = std::max(hi[a], p[3 * i + a]);
+        }
+    double ext = std::max(hi[0] - lo[0], std::max(hi[1] - lo[1], hi[2] - lo[2]));
+    double vol = 1.0;
+    for (int a = 0; a < 3; ++a) vol *= std::max(hi[a] - lo[a], 1e-3 * ext);
+    double c = std::cbrt(vol * std::max(1, k / 4) / (double)n);
+    return c > 0 ? c : 1.0;
+}
+}  // namespace
+
+// Exact kNN by expanding Chebyshev shells of grid cells; stops when the k-th best squared
+// distance is strictly below the squared distance to every unvisited cell.
+void knn_grid(const double* pts, i64 n, const double* qry, i64 nq, int k, std::vector<i32>& out,
+              int nthreads) {
+    out.assign((size_t)nq * k, -1);
+    Grid g;
+    g.build(pts, n, default_cell(pts, n, k));
+    parallel_for(nq, nthreads, [&](i64 b, i64 e) {
+        std::vector<double> bd(k);
+        std::vector<i32> bj(k);
+        KBest best{k, bd.data(), bj.data()};
+        for (i64 q = b; q < e; ++q) {
+            const double* x = qry + 3 * q;
+            best.reset();
+            i64 c[3];
+            g.coords(x, c);
+            i64 maxr = std::max(g.dims[0], std::max(g.dims[1], g.dims[2]));
+            for (i64 r = 0; r <= maxr; ++r) {
+                for (i64 z = c[2] - r; z <= c[2] + r; ++z) {
+                    if (z < 0 || z >= g.dims[2]) continue;
+                    bool zface = (z == c[2] - r || z == c[2] + r);
+                    for (i64 y = c[1] - r; y <= c[1] + r; ++y) {
+                        if (y < 0 || y >= g.dims[1]) continue;
+                        bool yface = zface || (y == c[1] - r || y == c[1] + r);
+                        for (i64 xx = c[0] - r; xx <= c[0] + r; ++xx) {
+                            if (xx < 0 || xx >= g.dims[0]) continue;
+                            if (!yface && xx != c[0] - r && xx != c[0] + r) continue;
+                            i64 cell = (z * g.dims[1] + y) * g.dims[0] + xx;
+                            for (i64 t = g.start[cell]; t < g.start[cell + 1]; ++t) {
+                                i32 j = g.items[t];
+                                best.offer(dist2(x, pts + 3 * (i64)j), j);
+                            }
+                        }
+                    }
+                }
+                if (best.full()) {
+                    // distance from x to the faces of the visited block
+                    double dmin = std::numeric_limits<double>::infinity();
+                    bool all = true;
+                    for (int a = 0; a < 3; ++a) {
+                        double lo_face = g.lo[a] + (double)(c[a] - r) * g.cell;
+                        double hi_face = g.lo[a] + (double)(c[a] + r + 1) * g.cell;
+                        if (c[a] - r > 0) { dmin = std::min(dmin, x[a] - lo_face); all = false; }
+                        if (c[a] + r + 1 < g.dims[a]) { dmin = std::min(dmin, hi_face - x[a]); all = false; }
+                    }
+                    if (all) break;
+                    if (dmin > 0) {
+                        double b2 = dmin * dmin * (1.0 - 1e-9);
+                        if (best.d[k - 1] < b2) break;
+                    }
+                }
+            }
+            for (int t = 0; t < k; ++t) out[(size_t)q * k + t] = best.j[t];
+        }
+    });
+}
+
+i64 nearest_other(const double* pts, i64 n, std::vector<double>& nn2, int nthreads) {
+    std::vector<i32> nb;
+    knn_grid(pts, n, pts, n, 3, nb, nthreads);
+    nn2.resize(n);
+    i64 dup = -1;
+    for (i64 i = 0; i < n; ++i) {
+        i32 j = nb[3 * i] == (i32)i ? nb[3 * i + 1] : nb[3 * i];
+        nn2[i] = dist2(pts + 3 * i, pts + 3 * (i64)j);
+        if (nn2[i] == 0.0 && dup < 0) dup = i;
+    }
+    return dup;
+}
+
+// ---------------------------------------------------------------------------------------
+// O8: weighted sample elimination (Yuksel 2015), fixed-point weights.
+// ---------------------------------------------------------------------------------------
+void wse_eliminate(const double* pts, i64 n, i64 nt, const std::vector<double>& nn2,
+                   std::vector<i64>& keep, int nthreads) {
+    keep.clear();
+    if (nt >= n) {
+        for (i64 i = 0; i < n; ++i) keep.push_back(i);
+        return;
+    }
+    std::vector<double> s(n);
+    for (i64 i = 0; i < n; ++i) s[i] = std::sqrt(nn2[i]);
+    std::nth_element(s.begin(), s.begin() + (n - 1) / 2, s.end());
+    double rh = 0.5 * s[(n - 1) / 2];
+    double rmax = rh * std::sqrt((double)n / (double)nt);
+    double R = 2.0 * rmax;
+
+    Grid g;
+    g.build(pts, n, std::max(R, default_cell(pts, n, 8)));
+    // neighbour lists per thread chunk, then concatenated (CSR)
+    int nt_threads = std::max(1, nthreads);
+    std::vector<std::vector<i32>> nj(nt_threads);
+    std::vector<std::vector<i64>> nw(nt_threads);
+    std::vector<i64> cnt(n, 0);
+    i64 chunk = (n + nt_threads - 1) / nt_threads;
+    std::vector<std::thread> th;
+    for (int t = 0; t < nt_threads; ++t) {
+        i64 b = t * chunk, e = std::min(n, b + chunk);
+        if (b >= e) break;
+        th.emplace_back([&, t, b, e] {
+            for (i64 i = b; i < e; ++i) {
+                i64 c[3];
+                g.coords(pts + 3 * i, c);
+                for (i64 z = c[2] - 1; z <= c[2] + 1; ++z) {
+                    if (z < 0 || z >= g.dims[2]) continue;
+                    for (i64 y = c[1] - 1; y <= c[1] + 1; ++y) {
+                        if (y < 0 || y >= g.dims[1]) continue;
+                        for (i64 x = c[0] - 1; x <= c[0] + 1; ++x) {
+                            if (x < 0 || x >= g.dims[0]) continue;
+                            i64 cell = (z * g.dims[1] + y) * g.dims[0] + x;
+                            for (i64 q = g.start[cell]; q < g.start[cell + 1]; ++q) {
+                                i32 j = g.items[q];
+                                if (j == (i32)i) continue;
+                                double d = std::sqrt(dist2(pts + 3 * i, pts + 3 * (i64)j));
+                                if (!(d < R)) continue;
+                                double u = 1.0 - d / R;
+                                double u2 = u * u;
+                                double u4 = u2 * u2;
+                                double u8 = u4 * u4;
+                                i64 W = (i64)std::floor(u8 * 1099511627776.0 + 0.5);
+                                nj[t].push_back(j);
+                                nw[t].push_back(W);
+                                cnt[i]++;
+                            }
+                        }
+                    }
+                }
+            }
+        });
+    }
+    for (auto& x : th) x.join();
+    std::vector<i64> ptr(n + 1, 0);
+    for (i64 i = 0; i < n; ++i) ptr[i + 1] = ptr[i] + cnt[i];
+    std::vector<i32> adj(ptr[n]);
+    std::vector<i64> adjw(ptr[n]);
+    {
+        i64 o = 0;
+        for (int t = 0; t < (int)nj.size(); ++t) {
+            std::copy(nj[t].begin(), nj[t].end(), adj.begin() + o);
+            std::copy(nw[t].begin(), nw[t].end(), adjw.begin() + o);
+            o += (i64)nj[t].size();
+        }
+    }
+    std::vector<i64> weight(n, 0);
+    for (i64 i = 0; i < n; ++i)
+        for (i64 t = ptr[i]; t < ptr[i + 1]; ++t) weight[i] += adjw[t];
+
+    // indexed max-heap: priority (weight desc, index asc)
+    std::vector<i32> heap(n), pos(n);
+    auto higher = [&](i32 a, i32 b) {
+        return weight[a] > weight[b] || (weight[a] == weight[b] && a < b);
+    };
+    for (i64 i = 0; i < n; ++i) { heap[i] = (i32)i; pos[i] = (i32)i; }
+    i64 hs = n;
+    auto sift_down = [&](i64 p) {
+        for (;;) {
+            i64 l = 2 * p + 1, r = l + 1, best = p;
+            if (l < hs && higher(heap[l], heap[best])) best = l;
+            if (r < hs && higher(heap[r], heap[best])) best = r;
+            if (best == p) return;
+            std::swap(heap[p], heap[best]);
+            pos[heap[p]] = (i32)p;
+            pos[heap[best]] = (i32)best;
+            p = best;
+        }
+    };
+    auto sift_up = [&](i64 p) {
+        while (p > 0) {
+            i64 q = (p - 1) / 2;
+            if (!higher(heap[p], heap[q])) return;
+            std::swap(heap[p], heap[q]);
+            pos[heap[p]] = (i32)p;
+            pos[heap[q]] = (i32)q;
+            p = q;
+        }
+    };
+    for (i64 p = n / 2 - 1; p >= 0; --p) sift_down(p);
+    std::vector<uint8_t> dead(n, 0);
+    for (i64 it = 0; it < n - nt; ++it) {
+        i32 a = heap[0];
+        dead[a] = 1;
+        heap[0] = heap[hs - 1];
+        pos[heap[0]] = 0;
+        --hs;
+        if (hs > 0) sift_down(0);
+        for (i64 t = ptr[a]; t < ptr[a + 1]; ++t) {
+            i32 j = adj[t];
+            if (dead[j]) continue;
+            weight[j] -= adjw[t];
+            sift_down(pos[j]);
+            (void)sift_up;
+        }
+    }
+    keep.reserve(nt);
+    for (i64 i = 0; i < n; ++i)
+        if (!dead[i]) keep.push_back(i);
+}
+
+// ---------------------------------------------------------------------------------------
+HostCSR transpose(const HostCSR& A) {
+    HostCSR T;
+    T.nrows = A.ncols;
+    T.ncols = A.nrows;
+    T.ptr.assign(T.nrows + 1, 0);
+    for (i64 t = 0; t < A.nnz(); ++t) T.ptr[A.col[t] + 1]++;
+    for (i64 r = 0; r < T.nrows; ++r) T.ptr[r + 1] += T.ptr[r];
+    T.col.resize(A.nnz());
+    T.val.resize(A.val.empty() ? 0 : A.nnz());
+    std::vector<i64> fill(T.ptr.begin(), T.ptr.end() - 1);
+    for (i64 i = 0; i < A.nrows; ++i)
+        for (i64 t = A.ptr[i]; t < A.ptr[i + 1]; ++t) {
+            i64 o = fill[A.col[t]]++;
+            T.col[o] = (i32)i;
+            if (!A.val.empty()) T.val[o] = A.val[t];
+        }
+    return T;
+}
+
+// O11: greedy colouring in index order on pattern(A) U pattern(A^T) minus the diagonal.
+int greedy_colouring(const HostCSR& A, std::vector<i32>& colour) {
+    HostCSR T = transpose(A);
+    i64 n = A.nrows;
+    colour.assign(n, -1);
+    std::vector<i64> stamp(256, -1);
+    int ncol = 0;
+    for (i64 i = 0; i < n; ++i) {
+        auto mark = [&](i32 j) {
+            if (j == (i32)i) return;
+            i32 c = colour[j];
+            if (c < 0) return;
+            if ((size_t)c >= stamp.size()) stamp.resize(2 * c + 2, -1);
+            stamp[c] = i;
+        };
+        for (i64 t = A.ptr[i]; t < A.ptr[i + 1]; ++t) mark(A.col[t]);
+        for (i64 t = T.ptr[i]; t < T.ptr[i + 1]; ++t) mark(T.col[t]);
+        i32 c = 0;
+        while ((size_t)c < stamp.size() && stamp[c] == i) ++c;
+        colour[i] = c;
+        ncol = std::max(ncol, c + 1);
+        if ((size_t)ncol >= stamp.size()) stamp.resize(2 * ncol + 2, -1);
+    }
+    return ncol;
+}
+
+// Dense LU with partial pivoting (O13); ties -> lowest row.  Row-major in, column-major out.
+i64 dense_lu_colmajor(std::vector<double>& A, int m, std::vector<double>& LU, std::vector<i32>& piv) {
+    double amax = 0.0;
+    for (double v : A) amax = std::max(amax, std::fabs(v));
+    piv.resize(m);
+    for (int k = 0; k < m; ++k) {
+        int p = k;
+        double pv = std::fabs(A[(i64)k * m + k]);
+        for (int i = k + 1; i < m; ++i)
+            if (std::fabs(A[(i64)i * m + k]) > pv) { pv = std::fabs(A[(i64)i * m + k]); p = i; }
+        if (!(pv > 1e-14 * amax)) return k;
+        piv[k] = p;
+        if (p != k)
+            for (int j = 0; j < m; ++j) std::swap(A[(i64)k * m + j], A[(i64)p * m + j]);
+        double d = A[(i64)k * m + k];
+        for (int i = k + 1; i < m; ++i) {
+            double l = A[(i64)i * m + k] / d;
+            A[(i64)i * m + k] = l;
+            for (int j = k + 1; j < m; ++j) A[(i64)i * m + j] = A[(i64)i * m + j] - l * A[(i64)k * m + j];
+        }
+    }
+    LU.resize((size_t)m * m);
+    for (int i = 0; i < m; ++i)
+        for (int j = 0; j < m; ++j) LU[(i64)j * m + i] = A[(i64)i * m + j];
+    return -1;
+}
+
+}  // namespace mgm

@@ -1,0 +1,1273 @@
+// libmgm: context, setup orchestration (Alg. 2), V-cycle (Alg. 3)
+// captured as a CUDA graph, right-preconditioned GMRES, standalone MGM
+// and the C ABI declared in include/mgm.h.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/mgm.h"
+#include "mgm_internal.h"
+#include "solve_kernels.cuh"
+
+using namespace mgm;
+
+namespace {
+
+thread_local std::string g_setup_error;
+thread_local int64_t g_setup_index = -1;
+
+struct Level {
+    i64 n = 0;
+    int ncol = 0;
+    std::vector<i64> coff;  // colour offsets (lib order)
+    // operator L_j (SELL-32)
+    i64* sptr = nullptr;
+    i32* scol = nullptr;
+    double* sval = nullptr;
+    i64 sell_stored = 0, nnz = 0;
+    // interpolation P_j (ELL width pm, slot-major) and restriction R_j (SELL-32, next level rows)
+    int pm = 0;
+    i32* pcol = nullptr;
+    double* pval = nullptr;
+    i64 p_nnz = 0;
+    i64* rptr = nullptr;
+    i32* rcol = nullptr;
+    double* rval = nullptr;
+    i64 r_stored = 0;
+    // vectors
+    double* u = nullptr;
+    double* f = nullptr;
+    double* t = nullptr;
+    double* c = nullptr;  // Poisson border
+    // host copies (export / test hooks)
+    std::vector<i64> ids;        // original point index per lib row
+    HostCSR L_lib, P_lib;        // lib order
+    std::vector<i32> colour_lib;
+    std::vector<double> c_lib;
+};
+
+struct KernelTimer {
+    bool on = false;
+    std::vector<cudaEvent_t> ev;  // pairs
+    int used = 0;
+    double total_ms = 0.0;
+    i64 launches = 0;
+    double bytes = 0.0;
+};
+
+}  // namespace
+
+struct mgm_ctx {
+    mgm_stencil_params sp{};
+    mgm_level_params lp{};
+    i64 N = 0;
+    int p = 0;
+    bool poisson = false;
+    int device = 0;
+    int nthreads = 1;
+    std::vector<Level> lv;
+    // coarsest dense LU
+    int nc = 0;
+    double* lu = nullptr;
+    i32* piv = nullptr;
+    // level-0 permutation (lib row -> original index)
+    i32* d_lib2orig = nullptr;
+    // fine weights (export)
+    std::vector<double> w_orig;
+    std::vector<i64> sten_orig;
+    // streams / graph
+    cudaStream_t st = nullptr;
+    cudaGraphExec_t vgraph = nullptr;
+    i64 vcycle_kernels = 0;
+    // GMRES workspace
+    int restart = 50;
+    i64 ld = 0;
+    double* V = nullptr;
+    double* w = nullptr;
+    double* xs = nullptr;    // solution accumulator (lib order)
+    double* b = nullptr;     // rhs (lib order)
+    double* partials = nullptr;
+    double* dh = nullptr;    // device scratch: h1[128], h2[128], nrm2, misc
+    double* hh = nullptr;    // pinned host mirror
+    // timing
+    KernelTimer timer[3];
+    double setup_ms = 0.0;
+    // errors
+    std::string err;
+    int64_t err_index = -1;
+};
+
+#define CK(call)                                                                           \
+    do {                                                                                   \
+        cudaError_t e_ = (call);                                                           \
+        if (e_ != cudaSuccess) {                                                           \
+            ctx->err = std::string(#call) + ": " + cudaGetErrorString(e_);                 \
+            return e_ == cudaErrorMemoryAllocation ? MGM_ERR_OOM : MGM_ERR_CUDA;           \
+        }                                                                                  \
+    } while (0)
+
+template <class T>
+static cudaError_t dalloc(T** p, i64 count) {
+    return cudaMalloc((void**)p, sizeof(T) * (size_t)std::max<i64>(count, 1));
+}
+
+static unsigned blocks_for(i64 n, int threads) { return (unsigned)std::max<i64>(1, (n + threads - 1) / threads); }
+
+// ---------------------------------------------------------------------------------------
+// Setup (Alg. 2)
+// ---------------------------------------------------------------------------------------
+namespace {
+
+// Pack a Morton-order CSR into lib-order SELL-32 (diagonal first for square operators).
+void pack_sell(const HostCSR& A, const std::vector<i64>& row_lib2mor, const std::vector<i32>& col_mor2lib,
+               bool diag_first, std::vector<i64>& sptr, std::vector<i32>& scol, std::vector<double>& sval,
+               HostCSR* lib_csr) {
+    i64 n = (i64)row_lib2mor.size();
+    i64 ns = (n + 31) / 32;
+    sptr.assign(ns + 1, 0);
+    for (i64 s = 0; s < ns; ++s) {
+        i64 w = 0;
+        for (i64 r = s * 32; r < std::min(n, s * 32 + 32); ++r) {
+            i64 mr = row_lib2mor[r];
+            w = std::max(w, A.ptr[mr + 1] - A.ptr[mr]);
+        }
+        sptr[s + 1] = sptr[s] + 32 * std::max<i64>(w, 1);
+    }
+    scol.assign(sptr[ns], 0);
+    sval.assign(sptr[ns], 0.0);
+    if (lib_csr) {
+        lib_csr->nrows = n;
+        lib_csr->ncols = (i64)col_mor2lib.size();
+        lib_csr->ptr.assign(n + 1, 0);
+        lib_csr->col.clear();
+        lib_csr->val.clear();
+    }
+    std::vector<std::pair<i32, double>> row;
+    for (i64 r = 0; r < n; ++r) {
+        i64 mr = row_lib2mor[r];
+        row.clear();
+        if (diag_first)
+            for (i64 t = A.ptr[mr]; t < A.ptr[mr + 1]; ++t)
+                if (A.col[t] == (i32)mr) row.push_back({A.col[t], A.val[t]});
+        for (i64 t = A.ptr[mr]; t < A.ptr[mr + 1]; ++t)
+            if (!diag_first || A.col[t] != (i32)mr) row.push_back({A.col[t], A.val[t]});
+        i64 s = r / 32, lane = r % 32;
+        i64 w = (sptr[s + 1] - sptr[s]) / 32;
+        for (i64 k = 0; k < w; ++k) {
+            i64 o = sptr[s] + 32 * k + lane;
+            if (k < (i64)row.size()) {
+                scol[o] = col_mor2lib[row[k].first];
+                sval[o] = row[k].second;
+            } else {
+                scol[o] = diag_first ? (i32)r : (row.empty() ? 0 : col_mor2lib[row[0].first]);
+                sval[o] = 0.0;
+            }
+        }
+        if (lib_csr) {
+            for (auto& e : row) {
+                lib_csr->col.push_back(col_mor2lib[e.first]);
+                lib_csr->val.push_back(e.second);
+            }
+            lib_csr->ptr[r + 1] = (i64)lib_csr->col.size();
+        }
+    }
+    // padded slice rows beyond n point at row 0
+    for (i64 r = n; r < ns * 32; ++r) {
+        i64 s = r / 32, lane = r % 32;
+        for (i64 k = 0; k < (sptr[s + 1] - sptr[s]) / 32; ++k) scol[sptr[s] + 32 * k + lane] = 0;
+    }
+}
+
+template <class T>
+mgm_status upload(mgm_ctx* ctx, T** dst, const std::vector<T>& src) {
+    CK(dalloc(dst, (i64)src.size()));
+    if (!src.empty()) CK(cudaMemcpyAsync(*dst, src.data(), sizeof(T) * src.size(), cudaMemcpyHostToDevice, ctx->st));
+    return MGM_OK;
+}
+
+mgm_status fail(mgm_ctx* ctx, mgm_status s, const std::string& msg, int64_t idx) {
+    ctx->err = msg;
+    ctx->err_index = idx;
+    return s;
+}
+
+mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i64 N) {
+    const auto& sp = ctx->sp;
+    const auto& lp = ctx->lp;
+    cudaStream_t st = ctx->st;
+    int nth = ctx->nthreads;
+    // ---- input checks
+    for (i64 i = 0; i < 3 * N; ++i)
+        if (!std::isfinite(points[i]) || !std::isfinite(normals[i])) return fail(ctx, MGM_ERR_INPUT, "non-finite input", i / 3);
+    // ---- Alg. 2 lines 2-3: order (Morton, O1)
+    std::vector<i64> perm;
+    if (!morton_order(points, N, perm)) return fail(ctx, MGM_ERR_INPUT, "degenerate point cloud", -1);
+    std::vector<double> X(3 * N), NR(3 * N);
+    for (i64 k = 0; k < N; ++k)
+        for (int a = 0; a < 3; ++a) {
+            X[3 * k + a] = points[3 * perm[k] + a];
+            NR[3 * k + a] = normals[3 * perm[k] + a];
+        }
+    // duplicates
+    {
+        std::vector<double> nn2;
+        i64 dup = nearest_other(X.data(), N, nn2, nth);
+        if (dup >= 0) return fail(ctx, MGM_ERR_INPUT, "duplicate points", perm[dup]);
+    }
+    // ---- level count (Alg. 2 line 4)
+    int p = lp.num_levels;
+    if (p <= 0) {
+        p = (int)std::floor(std::log((double)N / lp.n_min) / std::log((double)lp.coarsen_factor)) + 1;
+        p = std::max(p, 1);
+    }
+    {
+        i64 n = N;
+        for (int j = 1; j < p; ++j) {
+            n /= lp.coarsen_factor;
+            if (n < 2 || n < lp.interp_m) return fail(ctx, MGM_ERR_ARG, "too many levels for the point count", j);
+        }
+    }
+    ctx->p = p;
+    // ---- fine stencils and weights on the GPU
+    const int ns = sp.stencil_n;
+    std::vector<i32> sten;
+    knn_grid(X.data(), N, X.data(), N, ns, sten, nth);
+    double *dX = nullptr, *dN = nullptr, *dW = nullptr, *drho = nullptr;
+    i32* dS = nullptr;
+    i64* dfail = nullptr;
+    CK(dalloc(&dX, 3 * N));
+    CK(dalloc(&dN, 3 * N));
+    CK(dalloc(&dW, N * ns));
+    CK(dalloc(&dS, N * ns));
+    CK(dalloc(&dfail, 1));
+    CK(cudaMemcpyAsync(dX, X.data(), sizeof(double) * 3 * N, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dN, NR.data(), sizeof(double) * 3 * N, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dS, sten.data(), sizeof(i32) * N * ns, cudaMemcpyHostToDevice, st));
+    i64 none = INT64_MAX;
+    CK(cudaMemcpyAsync(dfail, &none, sizeof(i64), cudaMemcpyHostToDevice, st));
+    int rc;
+    if (sp.method == 0) {
+        rc = launch_rbffd_weights(dX, dN, dS, N, ns, sp.poly_degree, sp.phs_k, dW, dfail, st);
+    } else {
+        CK(dalloc(&drho, N));
+        rc = launch_stencil_radius(dX, dN, dS, N, ns, drho, st);
+        if (!rc) rc = launch_gfd_weights(dX, dN, dS, N, ns, sp.poly_degree, sp.gfd_alpha, drho, dW, dfail, st);
+    }
+    if (rc) return fail(ctx, MGM_ERR_CUDA, std::string("weight kernel: ") + cudaGetErrorString((cudaError_t)rc), -1);
+    std::vector<double> W((size_t)N * ns);
+    i64 hfail = 0;
+    CK(cudaMemcpyAsync(W.data(), dW, sizeof(double) * N * ns, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&hfail, dfail, sizeof(i64), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    cudaFree(dW);
+    cudaFree(dS);
+    cudaFree(dN);
+    if (drho) cudaFree(drho);
+    if (hfail != INT64_MAX)
+        return fail(ctx, MGM_ERR_UNISOLVENT, sp.method == 0 ? "RBF-FD stencil not unisolvent" : "GFD stencil rank deficient",
+                    perm[hfail]);
+    // export copy of weights in original order
+    ctx->w_orig.assign((size_t)N * ns, 0.0);
+    ctx->sten_orig.assign((size_t)N * ns, 0);
+    for (i64 k = 0; k < N; ++k)
+        for (int j = 0; j < ns; ++j) {
+            ctx->w_orig[perm[k] * ns + j] = W[k * ns + j];
+            ctx->sten_orig[perm[k] * ns + j] = perm[sten[k * ns + j]];
+        }
+    // ---- L_1, Morton order CSR with ascending columns
+    std::vector<HostCSR> Lm(p), Pm(p);
+    {
+        HostCSR& A = Lm[0];
+        A.nrows = A.ncols = N;
+        A.ptr.resize(N + 1);
+        A.col.resize((size_t)N * ns);
+        A.val.resize((size_t)N * ns);
+        std::vector<int> ord(ns);
+        for (i64 i = 0; i < N; ++i) {
+            A.ptr[i] = i * ns;
+            for (int j = 0; j < ns; ++j) ord[j] = j;
+            std::sort(ord.begin(), ord.end(), [&](int a, int b) { return sten[i * ns + a] < sten[i * ns + b]; });
+            for (int j = 0; j < ns; ++j) {
+                int q = ord[j];
+                double wv = W[i * ns + q];
+                double v;
+                if (sp.problem == 0) v = (q == 0) ? 1.0 - sp.mu * wv : -(sp.mu * wv);
+                else v = wv;
+                A.col[i * ns + j] = sten[i * ns + q];
+                A.val[i * ns + j] = v;
+            }
+        }
+        A.ptr[N] = N * ns;
+    }
+    // ---- level loop (Alg. 2 lines 5-12)
+    std::vector<std::vector<double>> Xl(p);
+    std::vector<std::vector<i64>> idsl(p);
+    Xl[0] = X;
+    idsl[0] = perm;
+    double* dXf = dX;
+    for (int j = 0; j + 1 < p; ++j) {
+        i64 nf = Lm[j].nrows, ncs = nf / lp.coarsen_factor;
+        // WSE, host
+        std::vector<double> nn2;
+        nearest_other(Xl[j].data(), nf, nn2, nth);
+        std::vector<i64> keep;
+        wse_eliminate(Xl[j].data(), nf, ncs, nn2, keep, nth);
+        Xl[j + 1].resize(3 * ncs);
+        idsl[j + 1].resize(ncs);
+        for (i64 k = 0; k < ncs; ++k) {
+            for (int a = 0; a < 3; ++a) Xl[j + 1][3 * k + a] = Xl[j][3 * keep[k] + a];
+            idsl[j + 1][k] = idsl[j][keep[k]];
+        }
+        // interpolation stencils (m nearest coarse points, O2) and weights on the GPU
+        const int m = lp.interp_m;
+        std::vector<i32> ist;
+        knn_grid(Xl[j + 1].data(), ncs, Xl[j].data(), nf, m, ist, nth);
+        double *dXc = nullptr, *dPw = nullptr;
+        i32 *dI = nullptr, *dcnt = nullptr;
+        CK(dalloc(&dXc, 3 * ncs));
+        CK(dalloc(&dPw, nf * m));
+        CK(dalloc(&dI, nf * m));
+        CK(dalloc(&dcnt, nf));
+        CK(cudaMemcpyAsync(dXc, Xl[j + 1].data(), sizeof(double) * 3 * ncs, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(dI, ist.data(), sizeof(i32) * nf * m, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(dfail, &none, sizeof(i64), cudaMemcpyHostToDevice, st));
+        rc = launch_interp_weights(dXf, nf, dXc, dI, m, dPw, dcnt, dfail, st);
+        if (rc) return fail(ctx, MGM_ERR_CUDA, "interp kernel", -1);
+        std::vector<double> Pw((size_t)nf * m);
+        std::vector<i32> pc(nf);
+        CK(cudaMemcpyAsync(Pw.data(), dPw, sizeof(double) * nf * m, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(pc.data(), dcnt, sizeof(i32) * nf, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(&hfail, dfail, sizeof(i64), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        cudaFree(dPw);
+        cudaFree(dI);
+        cudaFree(dcnt);
+        cudaFree(dXf);
+        dXf = dXc;
+        if (hfail != INT64_MAX) return fail(ctx, MGM_ERR_SINGULAR, "singular transfer system", idsl[j][hfail]);
+        HostCSR& P = Pm[j];
+        P.nrows = nf;
+        P.ncols = ncs;
+        P.ptr.assign(nf + 1, 0);
+        std::vector<int> ord(m);
+        for (i64 i = 0; i < nf; ++i) {
+            int c = pc[i];
+            for (int t = 0; t < c; ++t) ord[t] = t;
+            std::sort(ord.begin(), ord.begin() + c, [&](int a, int b) { return ist[i * m + a] < ist[i * m + b]; });
+            for (int t = 0; t < c; ++t) {
+                P.col.push_back(ist[i * m + ord[t]]);
+                P.val.push_back(Pw[i * m + ord[t]]);
+            }
+            P.ptr[i + 1] = (i64)P.col.size();
+        }
+        HostCSR R = transpose(P);  // P:370, exact
+        // Galerkin L_{j+1} = R (L P) on the GPU
+        DevCSR dL, dP, dR, dLP, dC;
+        if (upload_csr(Lm[j], dL, st) || upload_csr(P, dP, st) || upload_csr(R, dR, st))
+            return fail(ctx, MGM_ERR_OOM, "upload for SpGEMM", j);
+        std::string e1;
+        if (spgemm_device(dL, dP, dLP, st, e1)) return fail(ctx, MGM_ERR_CUDA, "SpGEMM L*P: " + e1, j);
+        if (spgemm_device(dR, dLP, dC, st, e1)) return fail(ctx, MGM_ERR_CUDA, "SpGEMM R*(LP): " + e1, j);
+        if (download_csr(dC, Lm[j + 1], st)) return fail(ctx, MGM_ERR_CUDA, "download Galerkin", j);
+        free_dev_csr(dL);
+        free_dev_csr(dP);
+        free_dev_csr(dR);
+        free_dev_csr(dLP);
+        free_dev_csr(dC);
+    }
+    cudaFree(dXf);
+    cudaFree(dfail);
+    // ---- colouring (O11) and lib orders
+    ctx->lv.assign(p, Level());
+    std::vector<std::vector<i64>> lib2mor(p);
+    std::vector<std::vector<i32>> mor2lib(p);
+    std::vector<std::vector<i32>> colour_mor(p);
+    for (int j = 0; j < p; ++j) {
+        Level& L = ctx->lv[j];
+        i64 n = Lm[j].nrows;
+        L.n = n;
+        lib2mor[j].resize(n);
+        mor2lib[j].resize(n);
+        if (j + 1 < p) {
+            L.ncol = greedy_colouring(Lm[j], colour_mor[j]);
+            L.coff.assign(L.ncol + 1, 0);
+            for (i64 i = 0; i < n; ++i) L.coff[colour_mor[j][i] + 1]++;
+            for (int c = 0; c < L.ncol; ++c) L.coff[c + 1] += L.coff[c];
+            std::vector<i64> fillp(L.coff.begin(), L.coff.end() - 1);
+            for (i64 i = 0; i < n; ++i) lib2mor[j][fillp[colour_mor[j][i]]++] = i;
+        } else {
+            L.ncol = 0;
+            colour_mor[j].assign(n, 0);
+            for (i64 i = 0; i < n; ++i) lib2mor[j][i] = i;
+        }
+        for (i64 r = 0; r < n; ++r) mor2lib[j][lib2mor[j][r]] = (i32)r;
+        L.ids.resize(n);
+        L.colour_lib.resize(n);
+        for (i64 r = 0; r < n; ++r) {
+            L.ids[r] = idsl[j][lib2mor[j][r]];
+            L.colour_lib[r] = colour_mor[j][lib2mor[j][r]];
+        }
+    }
+    // ---- pack solve-phase layout
+    mgm_status s;
+    for (int j = 0; j < p; ++j) {
+        Level& L = ctx->lv[j];
+        i64 n = L.n;
+        L.nnz = Lm[j].nnz();
+        std::vector<i64> sptr;
+        std::vector<i32> scol;
+        std::vector<double> sval;
+        pack_sell(Lm[j], lib2mor[j], mor2lib[j], true, sptr, scol, sval, &L.L_lib);
+        L.sell_stored = (i64)sval.size();
+        if ((s = upload(ctx, &L.sptr, sptr)) || (s = upload(ctx, &L.scol, scol)) || (s = upload(ctx, &L.sval, sval))) return s;
+        if (j + 1 < p) {
+            const HostCSR& P = Pm[j];
+            const int m = lp.interp_m;
+            L.pm = m;
+            L.p_nnz = P.nnz();
+            std::vector<i32> pcol((size_t)m * n);
+            std::vector<double> pval((size_t)m * n, 0.0);
+            L.P_lib.nrows = n;
+            L.P_lib.ncols = Lm[j + 1].nrows;
+            L.P_lib.ptr.assign(n + 1, 0);
+            for (i64 r = 0; r < n; ++r) {
+                i64 mr = lib2mor[j][r];
+                i64 a = P.ptr[mr], cnt = P.ptr[mr + 1] - a;
+                for (int k = 0; k < m; ++k) {
+                    if (k < cnt) {
+                        pcol[(size_t)k * n + r] = mor2lib[j + 1][P.col[a + k]];
+                        pval[(size_t)k * n + r] = P.val[a + k];
+                    } else {
+                        pcol[(size_t)k * n + r] = mor2lib[j + 1][P.col[a]];
+                        pval[(size_t)k * n + r] = 0.0;
+                    }
+                }
+                for (i64 k = 0; k < cnt; ++k) {
+                    L.P_lib.col.push_back(mor2lib[j + 1][P.col[a + k]]);
+                    L.P_lib.val.push_back(P.val[a + k]);
+                }
+                L.P_lib.ptr[r + 1] = (i64)L.P_lib.col.size();
+            }
+            if ((s = upload(ctx, &L.pcol, pcol)) || (s = upload(ctx, &L.pval, pval))) return s;
+            HostCSR R = transpose(P);
+            std::vector<i64> rptr;
+            std::vector<i32> rcol;
+            std::vector<double> rval;
+            pack_sell(R, lib2mor[j + 1], mor2lib[j], false, rptr, rcol, rval, nullptr);
+            L.r_stored = (i64)rval.size();
+            if ((s = upload(ctx, &L.rptr, rptr)) || (s = upload(ctx, &L.rcol, rcol)) || (s = upload(ctx, &L.rval, rval)))
+                return s;
+        }
+        i64 vn = n + (ctx->poisson ? 1 : 0);
+        CK(dalloc(&L.u, vn));
+        CK(dalloc(&L.f, vn));
+        CK(dalloc(&L.t, vn));
+        CK(cudaMemsetAsync(L.u, 0, sizeof(double) * vn, st));
+        CK(cudaMemsetAsync(L.f, 0, sizeof(double) * vn, st));
+        CK(cudaMemsetAsync(L.t, 0, sizeof(double) * vn, st));
+    }
+    // ---- Poisson border vectors c_{j+1} = P_j^T c_j, Morton order then lib
+    if (ctx->poisson) {
+        std::vector<double> cm(N, 1.0);
+        for (int j = 0; j < p; ++j) {
+            Level& L = ctx->lv[j];
+            L.c_lib.resize(L.n);
+            for (i64 r = 0; r < L.n; ++r) L.c_lib[r] = cm[lib2mor[j][r]];
+            if ((s = upload(ctx, &L.c, L.c_lib))) return s;
+            if (j + 1 < p) {
+                HostCSR R = transpose(Pm[j]);
+                std::vector<double> cn(R.nrows, 0.0);
+                for (i64 a = 0; a < R.nrows; ++a) {
+                    double acc = 0.0;
+                    for (i64 t = R.ptr[a]; t < R.ptr[a + 1]; ++t) acc = acc + R.val[t] * cm[R.col[t]];
+                    cn[a] = acc;
+                }
+                cm.swap(cn);
+            }
+        }
+    }
+    // ---- coarsest dense LU (Alg. 2 line 13; O13)
+    {
+        Level& L = ctx->lv[p - 1];
+        int n = (int)L.n;
+        int m = n + (ctx->poisson ? 1 : 0);
+        if (m > 8192) return fail(ctx, MGM_ERR_ARG, "coarsest level too large for the dense solve", m);
+        std::vector<double> A((size_t)m * m, 0.0);
+        const HostCSR& C = Lm[p - 1];  // lib order == Morton order on the coarsest level
+        for (int i = 0; i < n; ++i)
+            for (i64 t = C.ptr[i]; t < C.ptr[i + 1]; ++t) A[(size_t)i * m + C.col[t]] += C.val[t];
+        if (ctx->poisson)
+            for (int i = 0; i < n; ++i) {
+                A[(size_t)i * m + n] = L.c_lib[i];
+                A[(size_t)n * m + i] = L.c_lib[i];
+            }
+        std::vector<double> LU;
+        std::vector<i32> piv;
+        i64 bad = dense_lu_colmajor(A, m, LU, piv);
+        if (bad >= 0) return fail(ctx, MGM_ERR_SINGULAR, "singular coarsest operator", bad);
+        ctx->nc = m;
+        if ((s = upload(ctx, &ctx->lu, LU)) || (s = upload(ctx, &ctx->piv, piv))) return s;
+    }
+    // ---- level-0 permutation
+    {
+        std::vector<i32> l2o(N);
+        for (i64 r = 0; r < N; ++r) l2o[r] = (i32)ctx->lv[0].ids[r];
+        if ((s = upload(ctx, &ctx->d_lib2orig, l2o))) return s;
+    }
+    CK(cudaStreamSynchronize(st));
+    return MGM_OK;
+}
+
+// ---------------------------------------------------------------------------------------
+// Solve-phase enqueue helpers (all on stream `st`)
+// ---------------------------------------------------------------------------------------
+void timer_begin(mgm_ctx* ctx, int cls, cudaStream_t st) {
+    KernelTimer& T = ctx->timer[cls];
+    if (!T.on) return;
+    if (T.used + 2 > (int)T.ev.size()) {
+        for (int q = 0; q < 64; ++q) {
+            cudaEvent_t e;
+            cudaEventCreate(&e);
+            T.ev.push_back(e);
+        }
+    }
+    cudaEventRecord(T.ev[T.used], st);
+}
+void timer_end(mgm_ctx* ctx, int cls, cudaStream_t st, double bytes) {
+    KernelTimer& T = ctx->timer[cls];
+    if (!T.on) return;
+    cudaEventRecord(T.ev[T.used + 1], st);
+    T.used += 2;
+    T.launches += 1;
+    T.bytes += bytes;
+}
+void timer_collect(mgm_ctx* ctx) {
+    for (auto& T : ctx->timer) {
+        if (!T.on || T.used == 0) continue;
+        for (int q = 0; q < T.used; q += 2) {
+            cudaEventSynchronize(T.ev[q + 1]);
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, T.ev[q], T.ev[q + 1]);
+            T.total_ms += ms;
+        }
+        T.used = 0;
+    }
+}
+
+double sweep_colour_bytes(const Level& L, i64 rows) {
+    // algorithmic: 12 B per stored nonzero of those rows (approximated by the level mean)
+    // + f read + u read/write (8+16 B per row)
+    return (double)rows * (12.0 * (double)L.nnz / (double)L.n + 24.0);
+}
+
+void enqueue_sweep(mgm_ctx* ctx, int j, bool backward, cudaStream_t st) {
+    Level& L = ctx->lv[j];
+    for (int q = 0; q < L.ncol; ++q) {
+        int c = backward ? L.ncol - 1 - q : q;
+        int r0 = (int)L.coff[c], r1 = (int)L.coff[c + 1];
+        if (r1 <= r0) continue;
+        int span = r1 - (r0 & ~31);
+        if (j == 0) timer_begin(ctx, 0, st);
+        if (ctx->poisson)
+            k_gs_colour<true><<<blocks_for(span, 128), 128, 0, st>>>(r0, r1, L.sptr, L.scol, L.sval, L.f, L.u, L.c, (int)L.n);
+        else
+            k_gs_colour<false><<<blocks_for(span, 128), 128, 0, st>>>(r0, r1, L.sptr, L.scol, L.sval, L.f, L.u, L.c, (int)L.n);
+        if (j == 0) timer_end(ctx, 0, st, sweep_colour_bytes(L, r1 - r0));
+        ctx->vcycle_kernels++;
+    }
+}
+
+// Poisson border row: y[n] = fs*f[n] + sign * (c . x)
+void enqueue_border_dot(mgm_ctx* ctx, const Level& L, const double* x, const double* f, double fs, double sign,
+                        double* y, cudaStream_t st) {
+    k_multidot<<<RED_BLOCKS, RED_THREADS, 0, st>>>(L.n, L.c, 0, 1, x, ctx->partials);
+    k_border_finish<<<1, 32, 0, st>>>(ctx->partials, RED_BLOCKS, fs, f, (int)L.n, sign, y);
+    ctx->vcycle_kernels += 2;
+}
+
+// y = L x (level j)
+void enqueue_spmv(mgm_ctx* ctx, int j, const double* x, double* y, cudaStream_t st) {
+    Level& L = ctx->lv[j];
+    if (j == 0) timer_begin(ctx, 1, st);
+    if (ctx->poisson)
+        k_sell_spmv<0, true><<<blocks_for(L.n, 256), 256, 0, st>>>((int)L.n, L.sptr, L.scol, L.sval, x, nullptr, y, L.c);
+    else
+        k_sell_spmv<0, false><<<blocks_for(L.n, 256), 256, 0, st>>>((int)L.n, L.sptr, L.scol, L.sval, x, nullptr, y, L.c);
+    if (j == 0) timer_end(ctx, 1, st, 12.0 * L.nnz + 16.0 * L.n);
+    if (ctx->poisson) enqueue_border_dot(ctx, L, x, nullptr, 0.0, 1.0, y, st);
+}
+
+// t = f - L u (level j), Poisson: t[n] = f[n] - c.u
+void enqueue_residual(mgm_ctx* ctx, int j, const double* f, const double* u, double* t, cudaStream_t st) {
+    Level& L = ctx->lv[j];
+    if (ctx->poisson)
+        k_sell_spmv<1, true><<<blocks_for(L.n, 256), 256, 0, st>>>((int)L.n, L.sptr, L.scol, L.sval, u, f, t, L.c);
+    else
+        k_sell_spmv<1, false><<<blocks_for(L.n, 256), 256, 0, st>>>((int)L.n, L.sptr, L.scol, L.sval, u, f, t, L.c);
+    ctx->vcycle_kernels++;
+    if (ctx->poisson) enqueue_border_dot(ctx, L, u, f, 1.0, -1.0, t, st);
+}
+
+// y (next level) = R_j x
+void enqueue_restrict(mgm_ctx* ctx, int j, const double* x, double* y, cudaStream_t st) {
+    Level& L = ctx->lv[j];
+    Level& Ln = ctx->lv[j + 1];
+    k_sell_spmv<0, false><<<blocks_for(Ln.n, 256), 256, 0, st>>>((int)Ln.n, L.rptr, L.rcol, L.rval, x, nullptr, y, nullptr);
+    ctx->vcycle_kernels++;
+    if (ctx->poisson) {
+        k_copy1<<<1, 1, 0, st>>>(x + L.n, y + Ln.n);
+        ctx->vcycle_kernels++;
+    }
+}
+
+void enqueue_interp_correct(mgm_ctx* ctx, int j, const double* ec, double* e, cudaStream_t st) {
+    Level& L = ctx->lv[j];
+    Level& Ln = ctx->lv[j + 1];
+    if (ctx->poisson)
+        k_interp_correct<true><<<blocks_for(L.n + 1, 256), 256, 0, st>>>((int)L.n, L.pm, L.pcol, L.pval, ec, e, (int)Ln.n);
+    else
+        k_interp_correct<false><<<blocks_for(L.n + 1, 256), 256, 0, st>>>((int)L.n, L.pm, L.pcol, L.pval, ec, e, (int)Ln.n);
+    ctx->vcycle_kernels++;
+}
+
+void enqueue_coarse(mgm_ctx* ctx, const double* r, double* e, cudaStream_t st) {
+    k_coarse_solve<<<1, 32, sizeof(double) * ctx->nc, st>>>(ctx->nc, ctx->lu, ctx->piv, r, e);
+    ctx->vcycle_kernels++;
+}
+
+void enqueue_zero(mgm_ctx* ctx, double* x, i64 n, cudaStream_t st) {
+    k_fill<<<blocks_for(n, 256), 256, 0, st>>>(n, x, 0.0);
+    ctx->vcycle_kernels++;
+}
+
+// Alg. 3 on level-0 buffers lv[0].f (rhs) and lv[0].u (guess in, result out), lib order.
+void enqueue_vcycle(mgm_ctx* ctx, cudaStream_t st) {
+    auto& lv = ctx->lv;
+    const int p = ctx->p;
+    const int nu1 = ctx->lp.nu1, nu2 = ctx->lp.nu2;
+    const bool pre_b = ctx->lp.smoother == 1, post_b = ctx->lp.smoother == 1 || ctx->lp.smoother == 2;
+    const i64 pad = ctx->poisson ? 1 : 0;
+    ctx->vcycle_kernels = 0;
+    if (p == 1) {
+        enqueue_coarse(ctx, lv[0].f, lv[0].u, st);
+        return;
+    }
+    for (int s = 0; s < nu1; ++s) enqueue_sweep(ctx, 0, pre_b, st);      // line 4
+    enqueue_residual(ctx, 0, lv[0].f, lv[0].u, lv[0].t, st);              // line 5
+    enqueue_restrict(ctx, 0, lv[0].t, lv[1].f, st);
+    for (int j = 1; j + 1 < p; ++j) {                                     // lines 6-9
+        enqueue_zero(ctx, lv[j].u, lv[j].n + pad, st);
+        for (int s = 0; s < nu1; ++s) enqueue_sweep(ctx, j, pre_b, st);
+        enqueue_residual(ctx, j, lv[j].f, lv[j].u, lv[j].t, st);
+        enqueue_restrict(ctx, j, lv[j].t, lv[j + 1].f, st);
+    }
+    enqueue_coarse(ctx, lv[p - 1].f, lv[p - 1].u, st);                     // line 10
+    for (int j = p - 2; j >= 1; --j) {                                    // lines 11-14
+        enqueue_interp_correct(ctx, j, lv[j + 1].u, lv[j].u, st);
+        for (int s = 0; s < nu2; ++s) enqueue_sweep(ctx, j, post_b, st);
+    }
+    enqueue_interp_correct(ctx, 0, lv[1].u, lv[0].u, st);                 // line 15
+    for (int s = 0; s < nu2; ++s) enqueue_sweep(ctx, 0, post_b, st);      // line 16
+}
+
+bool timing_on(const mgm_ctx* ctx) { return ctx->timer[0].on || ctx->timer[1].on; }
+
+mgm_status build_graph(mgm_ctx* ctx) {
+    if (ctx->vgraph) return MGM_OK;
+    cudaGraph_t g;
+    CK(cudaStreamBeginCapture(ctx->st, cudaStreamCaptureModeThreadLocal));
+    enqueue_vcycle(ctx, ctx->st);
+    CK(cudaStreamEndCapture(ctx->st, &g));
+    CK(cudaGraphInstantiate(&ctx->vgraph, g, 0));
+    cudaGraphDestroy(g);
+    return MGM_OK;
+}
+
+// run one V-cycle on lv[0].f / lv[0].u
+mgm_status run_vcycle(mgm_ctx* ctx, cudaStream_t st) {
+    if (timing_on(ctx)) {
+        timer_begin(ctx, 2, st);
+        enqueue_vcycle(ctx, st);
+        timer_end(ctx, 2, st, 0.0);
+        return MGM_OK;
+    }
+    mgm_status s = build_graph(ctx);
+    if (s) return s;
+    timer_begin(ctx, 2, st);
+    CK(cudaGraphLaunch(ctx->vgraph, st));
+    timer_end(ctx, 2, st, 0.0);
+    return MGM_OK;
+}
+
+mgm_status ensure_krylov(mgm_ctx* ctx) {
+    if (ctx->V) return MGM_OK;
+    i64 n = ctx->N + (ctx->poisson ? 1 : 0);
+    ctx->ld = (n + 31) / 32 * 32;
+    CK(dalloc(&ctx->V, ctx->ld * (ctx->restart + 1)));
+    CK(dalloc(&ctx->w, ctx->ld));
+    CK(dalloc(&ctx->xs, ctx->ld));
+    CK(dalloc(&ctx->b, ctx->ld));
+    CK(dalloc(&ctx->partials, (i64)RED_BLOCKS * 256));
+    CK(dalloc(&ctx->dh, 1024));
+    CK(cudaMallocHost((void**)&ctx->hh, sizeof(double) * 1024));
+    return MGM_OK;
+}
+
+// dot over n entries of a and b -> device scalar out
+void enqueue_dot(mgm_ctx* ctx, i64 n, const double* a, const double* b, double* out, cudaStream_t st) {
+    k_multidot<<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, a, 0, 1, b, ctx->partials);
+    k_reduce_partials<<<1, 32, 0, st>>>(ctx->partials, RED_BLOCKS, 1, out);
+}
+
+// A x on level 0 (bordered in Poisson mode), n-vector incl. multiplier
+void enqueue_apply_A(mgm_ctx* ctx, const double* x, double* y, cudaStream_t st) { enqueue_spmv(ctx, 0, x, y, st); }
+
+// z = M(v): one V-cycle from zero, result left in lv[0].u
+mgm_status enqueue_precond(mgm_ctx* ctx, const double* v, cudaStream_t st) {
+    i64 n = ctx->N + (ctx->poisson ? 1 : 0);
+    CK(cudaMemcpyAsync(ctx->lv[0].f, v, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemsetAsync(ctx->lv[0].u, 0, sizeof(double) * n, st));
+    return run_vcycle(ctx, st);
+}
+
+// Right-preconditioned GMRES(restart) with CGS2 orthogonalisation (equal to MGS in exact
+// arithmetic; O15), Givens rotations on the host.  b, x in lib order (x = 0 on entry).
+mgm_status gmres_lib(mgm_ctx* ctx, double tol, int maxit, mgm_report* rep, cudaStream_t st) {
+    const i64 n = ctx->N + (ctx->poisson ? 1 : 0);
+    const int m = ctx->restart;
+    const i64 ld = ctx->ld;
+    double* V = ctx->V;
+    double* w = ctx->w;
+    double* h1 = ctx->dh;
+    double* h2 = ctx->dh + 256;
+    double* nr = ctx->dh + 512;
+    mgm_status s;
+    CK(cudaMemsetAsync(ctx->xs, 0, sizeof(double) * n, st));
+    enqueue_dot(ctx, n, ctx->b, ctx->b, nr, st);
+    CK(cudaMemcpyAsync(ctx->hh, nr, sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const double bnorm = std::sqrt(ctx->hh[0]);
+    int its = 0, hist_n = 0;
+    bool converged = false;
+    if (bnorm == 0.0) {
+        if (rep) { rep->iterations = 0; rep->converged = 1; rep->final_rel_residual = 0.0; }
+        return MGM_OK;
+    }
+    std::vector<double> H((size_t)(m + 1) * m), cs(m), sn(m), g(m + 1), y(m);
+    bool first = true;
+    while (true) {
+        // r = b - A x ; beta
+        if (first) {
+            CK(cudaMemcpyAsync(w, ctx->b, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+        } else {
+            enqueue_apply_A(ctx, ctx->xs, w, st);
+            k_axpby<<<RED_BLOCKS, 256, 0, st>>>(n, 1.0, ctx->b, -1.0, w, w);
+        }
+        first = false;
+        enqueue_dot(ctx, n, w, w, nr, st);
+        CK(cudaMemcpyAsync(ctx->hh, nr, sizeof(double), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        const double beta = std::sqrt(ctx->hh[0]);
+        if (beta / bnorm <= tol || its >= maxit) {
+            converged = beta / bnorm <= tol;
+            break;
+        }
+        k_scale_by_invnorm<<<RED_BLOCKS, 256, 0, st>>>(n, w, nr, V);
+        std::fill(H.begin(), H.end(), 0.0);
+        std::fill(g.begin(), g.end(), 0.0);
+        g[0] = beta;
+        int kdone = 0;
+        bool stop = false;
+        for (int k = 0; k < m; ++k) {
+            if ((s = enqueue_precond(ctx, V + (i64)k * ld, st))) return s;
+            enqueue_apply_A(ctx, ctx->lv[0].u, w, st);
+            ++its;
+            const int k1 = k + 1;
+            // CGS2: h = V^T w; w -= V h; h2 = V^T w; w -= V h2; h += h2
+            k_multidot<<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, V, ld, k1, w, ctx->partials);
+            k_reduce_partials<<<1, 128, 0, st>>>(ctx->partials, RED_BLOCKS, k1, h1);
+            k_multiaxpy<<<RED_BLOCKS * 2, 256, 0, st>>>(n, V, ld, k1, h1, w);
+            k_multidot<<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, V, ld, k1, w, ctx->partials);
+            k_reduce_partials<<<1, 128, 0, st>>>(ctx->partials, RED_BLOCKS, k1, h2);
+            k_multiaxpy<<<RED_BLOCKS * 2, 256, 0, st>>>(n, V, ld, k1, h2, w);
+            k_vadd<<<1, 128, 0, st>>>(k1, h1, h2);
+            enqueue_dot(ctx, n, w, w, nr, st);
+            k_scale_by_invnorm<<<RED_BLOCKS, 256, 0, st>>>(n, w, nr, V + (i64)k1 * ld);
+            CK(cudaMemcpyAsync(ctx->hh, h1, sizeof(double) * k1, cudaMemcpyDeviceToHost, st));
+            CK(cudaMemcpyAsync(ctx->hh + 512, nr, sizeof(double), cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            if (timing_on(ctx)) timer_collect(ctx);
+            for (int i = 0; i < k1; ++i) H[(size_t)i * m + k] = ctx->hh[i];
+            double hk1 = std::sqrt(ctx->hh[512]);
+            H[(size_t)k1 * m + k] = hk1;
+            for (int i = 0; i < k; ++i) {
+                double t = cs[i] * H[(size_t)i * m + k] + sn[i] * H[(size_t)(i + 1) * m + k];
+                H[(size_t)(i + 1) * m + k] = -sn[i] * H[(size_t)i * m + k] + cs[i] * H[(size_t)(i + 1) * m + k];
+                H[(size_t)i * m + k] = t;
+            }
+            double den = std::hypot(H[(size_t)k * m + k], hk1);
+            cs[k] = H[(size_t)k * m + k] / den;
+            sn[k] = hk1 / den;
+            H[(size_t)k * m + k] = den;
+            H[(size_t)k1 * m + k] = 0.0;
+            g[k1] = -sn[k] * g[k];
+            g[k] = cs[k] * g[k];
+            double rel = std::fabs(g[k1]) / bnorm;
+            if (rep && rep->history && hist_n < rep->history_cap) rep->history[hist_n++] = rel;
+            kdone = k1;
+            if (!std::isfinite(rel)) return fail(ctx, MGM_ERR_BREAKDOWN, "non-finite GMRES residual", its);
+            if (rel <= tol || its >= maxit || hk1 == 0.0) {
+                stop = true;
+                break;
+            }
+        }
+        for (int i = kdone - 1; i >= 0; --i) {
+            double sacc = g[i];
+            for (int j2 = i + 1; j2 < kdone; ++j2) sacc -= H[(size_t)i * m + j2] * y[j2];
+            y[i] = sacc / H[(size_t)i * m + i];
+        }
+        CK(cudaMemcpyAsync(h1, y.data(), sizeof(double) * kdone, cudaMemcpyHostToDevice, st));
+        k_lincomb<<<RED_BLOCKS * 2, 256, 0, st>>>(n, V, ld, kdone, h1, w);
+        if ((s = enqueue_precond(ctx, w, st))) return s;
+        k_axpby<<<RED_BLOCKS, 256, 0, st>>>(n, 1.0, ctx->xs, 1.0, ctx->lv[0].u, ctx->xs);
+        if (stop) {
+            converged = std::fabs(g[kdone]) / bnorm <= tol;
+            break;
+        }
+    }
+    // true residual
+    enqueue_apply_A(ctx, ctx->xs, w, st);
+    k_axpby<<<RED_BLOCKS, 256, 0, st>>>(n, 1.0, ctx->b, -1.0, w, w);
+    enqueue_dot(ctx, n, w, w, nr, st);
+    CK(cudaMemcpyAsync(ctx->hh, nr, sizeof(double), cudaMemcpyDeviceToHost, st));
+    if (ctx->poisson) CK(cudaMemcpyAsync(ctx->hh + 1, ctx->xs + ctx->N, sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (rep) {
+        rep->iterations = its;
+        rep->converged = converged ? 1 : 0;
+        rep->final_rel_residual = std::sqrt(ctx->hh[0]) / bnorm;
+        rep->lambda = ctx->poisson ? ctx->hh[1] : 0.0;
+    }
+    return MGM_OK;
+}
+
+// Standalone MGM: u <- V-cycle(f, u) from u = 0 until ||f - A u|| / ||f|| <= tol.
+mgm_status standalone_lib(mgm_ctx* ctx, double tol, int maxit, mgm_report* rep, cudaStream_t st) {
+    const i64 n = ctx->N + (ctx->poisson ? 1 : 0);
+    double* nr = ctx->dh + 512;
+    mgm_status s;
+    enqueue_dot(ctx, n, ctx->b, ctx->b, nr, st);
+    CK(cudaMemcpyAsync(ctx->hh, nr, sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const double fn = std::sqrt(ctx->hh[0]);
+    CK(cudaMemsetAsync(ctx->lv[0].u, 0, sizeof(double) * n, st));
+    CK(cudaMemsetAsync(ctx->xs, 0, sizeof(double) * n, st));
+    if (fn == 0.0) {
+        if (rep) { rep->iterations = 0; rep->converged = 1; rep->final_rel_residual = 0.0; }
+        return MGM_OK;
+    }
+    CK(cudaMemcpyAsync(ctx->lv[0].f, ctx->b, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+    int it = 0, hist_n = 0;
+    double rel = 1.0;
+    bool conv = false;
+    while (it < maxit) {
+        if ((s = run_vcycle(ctx, st))) return s;
+        ++it;
+        enqueue_apply_A(ctx, ctx->lv[0].u, ctx->w, st);
+        k_axpby<<<RED_BLOCKS, 256, 0, st>>>(n, 1.0, ctx->b, -1.0, ctx->w, ctx->w);
+        enqueue_dot(ctx, n, ctx->w, ctx->w, nr, st);
+        CK(cudaMemcpyAsync(ctx->hh, nr, sizeof(double), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (timing_on(ctx)) timer_collect(ctx);
+        rel = std::sqrt(ctx->hh[0]) / fn;
+        if (rep && rep->history && hist_n < rep->history_cap) rep->history[hist_n++] = rel;
+        if (rel <= tol) { conv = true; break; }
+        if (!std::isfinite(rel)) break;
+    }
+    CK(cudaMemcpyAsync(ctx->xs, ctx->lv[0].u, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+    if (ctx->poisson) {
+        CK(cudaMemcpyAsync(ctx->hh + 1, ctx->xs + ctx->N, sizeof(double), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+    }
+    if (rep) {
+        rep->iterations = it;
+        rep->converged = conv ? 1 : 0;
+        rep->final_rel_residual = rel;
+        rep->lambda = ctx->poisson ? ctx->hh[1] : 0.0;
+    }
+    return MGM_OK;
+}
+
+mgm_status check_ctx(mgm_ctx* ctx) {
+    if (!ctx || ctx->lv.empty()) return MGM_ERR_ARG;
+    cudaSetDevice(ctx->device);
+    return MGM_OK;
+}
+
+}  // namespace
+
+// =======================================================================================
+// C ABI
+// =======================================================================================
+extern "C" {
+
+mgm_status mgm_setup(const double* points, const double* normals, int64_t n_points,
+                     const mgm_stencil_params* stencil, const mgm_level_params* levels, void* cuda_stream,
+                     mgm_ctx** out) {
+    g_setup_error.clear();
+    g_setup_index = -1;
+    if (out) *out = nullptr;
+    if (!points || !normals || !stencil || !levels || !out || n_points < 2) {
+        g_setup_error = "invalid argument";
+        return MGM_ERR_ARG;
+    }
+    const mgm_stencil_params& sp = *stencil;
+    const mgm_level_params& lp = *levels;
+    if (sp.method < 0 || sp.method > 1 || sp.poly_degree < 0 || sp.poly_degree > 8 || sp.stencil_n < 2 ||
+        sp.stencil_n > 96 || sp.stencil_n > n_points || (sp.method == 0 && (sp.phs_k < 1 || sp.phs_k > 8)) ||
+        sp.problem < 0 || sp.problem > 1 || (sp.problem == 0 && !(sp.mu > 0)) || lp.interp_m < 1 ||
+        lp.interp_m > 16 || lp.nu1 < 0 || lp.nu2 < 0 || lp.coarsen_factor < 2 || lp.restart < 1 ||
+        lp.restart > 128 || lp.smoother < 0 || lp.smoother > 2 || (lp.num_levels <= 0 && lp.n_min < 1) ||
+        n_points > INT32_MAX / 2) {
+        g_setup_error = "invalid stencil or level parameters";
+        return MGM_ERR_ARG;
+    }
+    if (sp.method == 1 && sp.stencil_n < (sp.poly_degree + 1) * (sp.poly_degree + 2) / 2) {
+        g_setup_error = "GFD stencil smaller than the polynomial space";
+        return MGM_ERR_ARG;
+    }
+    auto t0 = std::chrono::steady_clock::now();
+    mgm_ctx* ctx = new mgm_ctx();
+    ctx->sp = sp;
+    ctx->lp = lp;
+    ctx->N = n_points;
+    ctx->poisson = sp.problem == 1;
+    ctx->restart = lp.restart;
+    ctx->nthreads = std::max(1, std::min(64, (int)std::thread::hardware_concurrency()));
+    cudaGetDevice(&ctx->device);
+    (void)cuda_stream;
+    if (cudaStreamCreateWithFlags(&ctx->st, cudaStreamNonBlocking) != cudaSuccess) {
+        g_setup_error = "cannot create CUDA stream (no device?)";
+        delete ctx;
+        return MGM_ERR_CUDA;
+    }
+    mgm_status s = do_setup(ctx, points, normals, n_points);
+    ctx->setup_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    if (s != MGM_OK) {
+        g_setup_error = ctx->err;
+        g_setup_index = ctx->err_index;
+        ctx->lv.clear();
+        *out = ctx;
+        return s;
+    }
+    *out = ctx;
+    return MGM_OK;
+}
+
+mgm_status mgm_destroy(mgm_ctx* ctx) {
+    if (!ctx) return MGM_OK;
+    cudaSetDevice(ctx->device);
+    if (ctx->st) cudaStreamSynchronize(ctx->st);
+    for (auto& L : ctx->lv) {
+        for (void* ptr : {(void*)L.sptr, (void*)L.scol, (void*)L.sval, (void*)L.pcol, (void*)L.pval, (void*)L.rptr,
+                          (void*)L.rcol, (void*)L.rval, (void*)L.u, (void*)L.f, (void*)L.t, (void*)L.c})
+            if (ptr) cudaFree(ptr);
+    }
+    for (void* ptr : {(void*)ctx->lu, (void*)ctx->piv, (void*)ctx->d_lib2orig, (void*)ctx->V, (void*)ctx->w,
+                      (void*)ctx->xs, (void*)ctx->b, (void*)ctx->partials, (void*)ctx->dh})
+        if (ptr) cudaFree(ptr);
+    if (ctx->hh) cudaFreeHost(ctx->hh);
+    if (ctx->vgraph) cudaGraphExecDestroy(ctx->vgraph);
+    for (auto& T : ctx->timer)
+        for (auto e : T.ev) cudaEventDestroy(e);
+    if (ctx->st) cudaStreamDestroy(ctx->st);
+    delete ctx;
+    return MGM_OK;
+}
+
+const char* mgm_last_error(const mgm_ctx* ctx, int64_t* failing_index) {
+    if (!ctx) {
+        if (failing_index) *failing_index = g_setup_index;
+        return g_setup_error.c_str();
+    }
+    if (failing_index) *failing_index = ctx->err_index;
+    return ctx->err.c_str();
+}
+
+mgm_status mgm_vcycle(mgm_ctx* ctx, const double* f_dev, double* u_dev, void* cuda_stream) {
+    mgm_status s = check_ctx(ctx);
+    if (s) return s;
+    if (!f_dev || !u_dev) return MGM_ERR_ARG;
+    if ((s = ensure_krylov(ctx))) return s;
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    const i64 N = ctx->N;
+    Level& L0 = ctx->lv[0];
+    k_gather<<<blocks_for(N, 256), 256, 0, st>>>((int)N, ctx->d_lib2orig, f_dev, L0.f);
+    k_gather<<<blocks_for(N, 256), 256, 0, st>>>((int)N, ctx->d_lib2orig, u_dev, L0.u);
+    if (ctx->poisson) {
+        CK(cudaMemsetAsync(L0.f + N, 0, sizeof(double), st));
+        CK(cudaMemsetAsync(L0.u + N, 0, sizeof(double), st));
+    }
+    if ((s = run_vcycle(ctx, st))) return s;
+    k_scatter<<<blocks_for(N, 256), 256, 0, st>>>((int)N, ctx->d_lib2orig, L0.u, u_dev);
+    CK(cudaGetLastError());
+    if (timing_on(ctx)) {
+        CK(cudaStreamSynchronize(st));
+        timer_collect(ctx);
+    }
+    return MGM_OK;
+}
+
+static mgm_status solve_impl(mgm_ctx* ctx, const double* rhs, double* x, bool host, double tol, int maxit,
+                             int krylov, mgm_report* rep, cudaStream_t st) {
+    mgm_status s = check_ctx(ctx);
+    if (s) return s;
+    if (!rhs || !x || !(tol >= 0) || maxit < 0 || krylov < 0 || krylov > 1) return MGM_ERR_ARG;
+    if ((s = ensure_krylov(ctx))) return s;
+    const i64 N = ctx->N;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, st);
+    const double* rhs_dev = rhs;
+    if (host) {
+        CK(cudaMemcpyAsync(ctx->w, rhs, sizeof(double) * N, cudaMemcpyHostToDevice, st));
+        rhs_dev = ctx->w;
+    }
+    k_gather<<<blocks_for(N, 256), 256, 0, st>>>((int)N, ctx->d_lib2orig, rhs_dev, ctx->b);
+    if (ctx->poisson) CK(cudaMemsetAsync(ctx->b + N, 0, sizeof(double), st));
+    s = krylov ? gmres_lib(ctx, tol, maxit, rep, st) : standalone_lib(ctx, tol, maxit, rep, st);
+    if (s) return s;
+    if (host) {
+        k_scatter<<<blocks_for(N, 256), 256, 0, st>>>((int)N, ctx->d_lib2orig, ctx->xs, ctx->w);
+        CK(cudaMemcpyAsync(x, ctx->w, sizeof(double) * N, cudaMemcpyDeviceToHost, st));
+    } else {
+        k_scatter<<<blocks_for(N, 256), 256, 0, st>>>((int)N, ctx->d_lib2orig, ctx->xs, x);
+    }
+    cudaEventRecord(e1, st);
+    CK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (rep) {
+        rep->solve_ms = ms;
+        rep->setup_ms = ctx->setup_ms;
+    }
+    CK(cudaGetLastError());
+    return MGM_OK;
+}
+
+mgm_status mgm_solve(mgm_ctx* ctx, const double* rhs_dev, double* x_dev, double tol, int maxit, int krylov,
+                     mgm_report* report, void* cuda_stream) {
+    return solve_impl(ctx, rhs_dev, x_dev, false, tol, maxit, krylov, report, (cudaStream_t)cuda_stream);
+}
+
+mgm_status mgm_solve_host(mgm_ctx* ctx, const double* rhs_host, double* x_host, double tol, int maxit, int krylov,
+                          mgm_report* report, void* cuda_stream) {
+    return solve_impl(ctx, rhs_host, x_host, true, tol, maxit, krylov, report, (cudaStream_t)cuda_stream);
+}
+
+mgm_status mgm_num_levels(const mgm_ctx* ctx, int* p) {
+    if (!ctx || ctx->lv.empty() || !p) return MGM_ERR_ARG;
+    *p = ctx->p;
+    return MGM_OK;
+}
+
+mgm_status mgm_level_info(const mgm_ctx* ctx, int level, int64_t* n_rows, int64_t* nnz_L, int64_t* nnz_P,
+                          int* n_colours, int64_t* stored_bytes) {
+    if (!ctx || ctx->lv.empty() || level < 0 || level >= ctx->p) return MGM_ERR_ARG;
+    const Level& L = ctx->lv[level];
+    if (n_rows) *n_rows = L.n;
+    if (nnz_L) *nnz_L = L.nnz;
+    if (nnz_P) *nnz_P = L.p_nnz;
+    if (n_colours) *n_colours = L.ncol;
+    if (stored_bytes)
+        *stored_bytes = 12 * L.sell_stored + 8 * ((L.n + 31) / 32 + 1) + 12 * (i64)L.pm * L.n + 12 * L.r_stored +
+                        24 * L.n;
+    return MGM_OK;
+}
+
+mgm_status mgm_export_level(const mgm_ctx* ctx, int level, int64_t* ids, int64_t* L_ptr, int32_t* L_col,
+                            double* L_val, int32_t* colour, int64_t* P_ptr, int32_t* P_col, double* P_val,
+                            double* border) {
+    if (!ctx || ctx->lv.empty() || level < 0 || level >= ctx->p) return MGM_ERR_ARG;
+    const Level& L = ctx->lv[level];
+    if (ids) std::copy(L.ids.begin(), L.ids.end(), ids);
+    if (L_ptr) std::copy(L.L_lib.ptr.begin(), L.L_lib.ptr.end(), L_ptr);
+    if (L_col) std::copy(L.L_lib.col.begin(), L.L_lib.col.end(), L_col);
+    if (L_val) std::copy(L.L_lib.val.begin(), L.L_lib.val.end(), L_val);
+    if (colour) std::copy(L.colour_lib.begin(), L.colour_lib.end(), colour);
+    if (level + 1 < ctx->p) {
+        if (P_ptr) std::copy(L.P_lib.ptr.begin(), L.P_lib.ptr.end(), P_ptr);
+        if (P_col) std::copy(L.P_lib.col.begin(), L.P_lib.col.end(), P_col);
+        if (P_val) std::copy(L.P_lib.val.begin(), L.P_lib.val.end(), P_val);
+    }
+    if (border) {
+        if (!ctx->poisson) return MGM_ERR_ARG;
+        std::copy(L.c_lib.begin(), L.c_lib.end(), border);
+    }
+    return MGM_OK;
+}
+
+mgm_status mgm_export_weights(const mgm_ctx* ctx, double* w, int64_t* sten) {
+    if (!ctx || ctx->lv.empty()) return MGM_ERR_ARG;
+    if (w) std::copy(ctx->w_orig.begin(), ctx->w_orig.end(), w);
+    if (sten) std::copy(ctx->sten_orig.begin(), ctx->sten_orig.end(), sten);
+    return MGM_OK;
+}
+
+mgm_status mgm_apply(mgm_ctx* ctx, int level, int op, const double* x, const double* f, double* y,
+                     void* cuda_stream) {
+    mgm_status s = check_ctx(ctx);
+    if (s) return s;
+    if (level < 0 || level >= ctx->p || !x || !y) return MGM_ERR_ARG;
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    Level& L = ctx->lv[level];
+    const i64 pad = ctx->poisson ? 1 : 0;
+    const i64 vn = L.n + pad;
+    if ((s = ensure_krylov(ctx))) return s;
+    switch (op) {
+        case MGM_OP_SPMV:
+            enqueue_spmv(ctx, level, x, y, st);
+            break;
+        case MGM_OP_SWEEP:
+            if (!f || level == ctx->p - 1) return MGM_ERR_ARG;
+            CK(cudaMemcpyAsync(L.u, x, sizeof(double) * vn, cudaMemcpyDeviceToDevice, st));
+            CK(cudaMemcpyAsync(L.f, f, sizeof(double) * vn, cudaMemcpyDeviceToDevice, st));
+            enqueue_sweep(ctx, level, false, st);
+            CK(cudaMemcpyAsync(y, L.u, sizeof(double) * vn, cudaMemcpyDeviceToDevice, st));
+            break;
+        case MGM_OP_RESIDUAL:
+            if (!f) return MGM_ERR_ARG;
+            enqueue_residual(ctx, level, f, x, y, st);
+            break;
+        case MGM_OP_RESTRICT:
+            if (level == ctx->p - 1) return MGM_ERR_ARG;
+            enqueue_restrict(ctx, level, x, y, st);
+            break;
+        case MGM_OP_INTERP: {
+            if (level == ctx->p - 1) return MGM_ERR_ARG;
+            const Level& Ln = ctx->lv[level + 1];
+            if (ctx->poisson)
+                k_interp<true><<<blocks_for(L.n + 1, 256), 256, 0, st>>>((int)L.n, L.pm, L.pcol, L.pval, x, y, (int)Ln.n);
+            else
+                k_interp<false><<<blocks_for(L.n + 1, 256), 256, 0, st>>>((int)L.n, L.pm, L.pcol, L.pval, x, y, (int)Ln.n);
+            break;
+        }
+        case MGM_OP_COARSE:
+            enqueue_coarse(ctx, x, y, st);
+            break;
+        default:
+            return MGM_ERR_ARG;
+    }
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(st));
+    return MGM_OK;
+}
+
+mgm_status mgm_timing_enable(mgm_ctx* ctx, int cls, int enable) {
+    if (!ctx || cls < 0 || cls > 2) return MGM_ERR_ARG;
+    KernelTimer& T = ctx->timer[cls];
+    T.on = enable != 0;
+    T.used = 0;
+    T.total_ms = 0.0;
+    T.launches = 0;
+    T.bytes = 0.0;
+    return MGM_OK;
+}
+
+mgm_status mgm_timing_read(mgm_ctx* ctx, int cls, double* total_ms, int64_t* launches, double* alg_bytes) {
+    if (!ctx || cls < 0 || cls > 2) return MGM_ERR_ARG;
+    timer_collect(ctx);
+    const KernelTimer& T = ctx->timer[cls];
+    if (total_ms) *total_ms = T.total_ms;
+    if (launches) *launches = T.launches;
+    if (alg_bytes) *alg_bytes = T.bytes;
+    return MGM_OK;
+}
+
+mgm_status mgm_bytes_model(const mgm_ctx* ctx, double* vcycle_bytes, double* spmv_bytes) {
+    if (!ctx || ctx->lv.empty()) return MGM_ERR_ARG;
+    const int p = ctx->p;
+    const double nu = ctx->lp.nu1 + ctx->lp.nu2;
+    const double bp = ctx->poisson ? 8.0 : 0.0;
+    double B = 0.0;
+    for (int j = 0; j + 1 < p; ++j) {
+        const Level& L = ctx->lv[j];
+        const double n = (double)L.n, z = (double)L.nnz, q = (double)L.p_nnz, nn = (double)ctx->lv[j + 1].n;
+        B += nu * (12.0 * z + 24.0 * n + bp * n);                   // sweeps
+        B += 12.0 * z + 16.0 * n + 12.0 * q + 8.0 * nn + 16.0 * n + bp * n;  // residual + restrict (unfused)
+        B += 12.0 * q + 8.0 * nn + 16.0 * n;                        // interp + correct
+    }
+    const double np = (double)ctx->nc;
+    B += 8.0 * np * np + 16.0 * np;
+    if (vcycle_bytes) *vcycle_bytes = B;
+    if (spmv_bytes) *spmv_bytes = 12.0 * ctx->lv[0].nnz + 16.0 * ctx->lv[0].n;
+    return MGM_OK;
+}
+
+mgm_status mgm_vcycle_kernel_count(const mgm_ctx* ctx, int64_t* count) {
+    if (!ctx || ctx->lv.empty() || !count) return MGM_ERR_ARG;
+    i64 c = 0;
+    const int p = ctx->p;
+    if (p == 1) { *count = 1; return MGM_OK; }
+    for (int j = 0; j + 1 < p; ++j) {
+        c += (i64)(ctx->lp.nu1 + ctx->lp.nu2) * ctx->lv[j].ncol;
+        c += 2 + 1 + (j > 0 ? 1 : 0);
+        if (ctx->poisson) c += 3;
+    }
+    *count = c + 1;
+    return MGM_OK;
+}
+
+mgm_status mgm_host_morton(const double* points, int64_t n, int64_t* perm) {
+    if (!points || !perm || n < 1) return MGM_ERR_ARG;
+    std::vector<i64> p;
+    if (!morton_order(points, n, p)) return MGM_ERR_INPUT;
+    std::copy(p.begin(), p.end(), perm);
+    return MGM_OK;
+}
+
+mgm_status mgm_host_knn(const double* points, int64_t n, const double* queries, int64_t nq, int k,
+                        int32_t* out) {
+    if (!points || !queries || !out || k < 1 || k > n) return MGM_ERR_ARG;
+    std::vector<i32> o;
+    knn_grid(points, n, queries, nq, k, o, std::max(1, (int)std::thread::hardware_concurrency()));
+    std::copy(o.begin(), o.end(), out);
+    return MGM_OK;
+}
+
+mgm_status mgm_host_wse(const double* points, int64_t n, int64_t nt, int64_t* keep) {
+    if (!points || !keep || nt < 1 || nt > n) return MGM_ERR_ARG;
+    int nth = std::max(1, (int)std::thread::hardware_concurrency());
+    std::vector<double> nn2;
+    if (nearest_other(points, n, nn2, nth) >= 0) return MGM_ERR_INPUT;
+    std::vector<i64> k;
+    wse_eliminate(points, n, nt, nn2, k, nth);
+    std::copy(k.begin(), k.end(), keep);
+    return MGM_OK;
+}
+
+mgm_status mgm_host_colouring(int64_t n, const int64_t* ptr, const int32_t* col, int32_t* colour,
+                              int* n_colours) {
+    if (!ptr || !col || !colour || n < 1) return MGM_ERR_ARG;
+    HostCSR A;
+    A.nrows = A.ncols = n;
+    A.ptr.assign(ptr, ptr + n + 1);
+    A.col.assign(col, col + ptr[n]);
+    std::vector<i32> c;
+    int nc = greedy_colouring(A, c);
+    std::copy(c.begin(), c.end(), colour);
+    if (n_colours) *n_colours = nc;
+    return MGM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,73 @@
+// Internal declarations of libmgm (not part of the ABI).
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace mgm {
+
+using i64 = int64_t;
+using i32 = int32_t;
+
+// Host CSR (int64 row pointer, int32 columns ascending within a row).
+struct HostCSR {
+    i64 nrows = 0, ncols = 0;
+    std::vector<i64> ptr;
+    std::vector<i32> col;
+    std::vector<double> val;
+    i64 nnz() const { return ptr.empty() ? 0 : ptr.back(); }
+};
+
+// ---------------- host setup (host_setup.cpp; compiled with -ffp-contract=off) ----------
+// Morton permutation (O1): perm[new] = old.  Returns false on a degenerate cloud.
+bool morton_order(const double* pts, i64 n, std::vector<i64>& perm);
+
+// k nearest neighbours of each query among `pts` under the (d2, index) order of O2.
+// out[q*k + t] (int32 indices into pts).  Multi-threaded, exact.
+void knn_grid(const double* pts, i64 n, const double* qry, i64 nq, int k, std::vector<i32>& out,
+              int nthreads);
+
+// Duplicate check: returns the index of a point whose nearest other point is at distance 0,
+// or -1.  nn2[i] receives the squared distance to the nearest other point.
+i64 nearest_other(const double* pts, i64 n, std::vector<double>& nn2, int nthreads);
+
+// Weighted sample elimination (O8): keep (size nt) = surviving indices, ascending.
+void wse_eliminate(const double* pts, i64 n, i64 nt, const std::vector<double>& nn2,
+                   std::vector<i64>& keep, int nthreads);
+
+// Greedy colouring (O11) of sym(pattern(A)) minus the diagonal in index order.
+int greedy_colouring(const HostCSR& A, std::vector<i32>& colour);
+
+HostCSR transpose(const HostCSR& A);
+
+// Dense LU with partial pivoting (ties -> lowest row), column-major output for the device
+// solve.  Returns -1 on success or the failing pivot column.
+i64 dense_lu_colmajor(std::vector<double>& A_rowmajor, int m, std::vector<double>& LU_colmajor,
+                      std::vector<i32>& piv);
+
+// ---------------- device setup kernels (setup_kernels.cu; -fmad=false) -----------------
+// All pointers device.  Return cudaError_t as int; *fail_dev = failing row or INT64_MAX.
+int launch_rbffd_weights(const double* pts, const double* nrm, const i32* sten, i64 n, int ns,
+                         int ell, int k, double* w, i64* fail_dev, void* stream);
+int launch_stencil_radius(const double* pts, const double* nrm, const i32* sten, i64 n, int ns,
+                          double* rho, void* stream);
+int launch_gfd_weights(const double* pts, const double* nrm, const i32* sten, i64 n, int ns,
+                       int ell, double alpha, const double* rho, double* w, i64* fail_dev,
+                       void* stream);
+int launch_interp_weights(const double* fine, i64 nf, const double* coarse, const i32* sten,
+                          int m, double* w, i32* cnt, i64* fail_dev, void* stream);
+
+// Device SpGEMM C = A B (CSR, columns ascending).  Symbolic pattern kept in full; values
+// summed in canonical order (O10), bit-identical to a sequential loop.
+struct DevCSR {
+    i64 nrows = 0, ncols = 0, nnz = 0;
+    i64* ptr = nullptr;
+    i32* col = nullptr;
+    double* val = nullptr;
+};
+int spgemm_device(const DevCSR& A, const DevCSR& B, DevCSR& C, void* stream, std::string& err);
+void free_dev_csr(DevCSR& M);
+int upload_csr(const HostCSR& H, DevCSR& D, void* stream);
+int download_csr(const DevCSR& D, HostCSR& H, void* stream);
+
+}  // namespace mgm

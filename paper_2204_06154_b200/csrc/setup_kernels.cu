@@ -1,0 +1,619 @@
+// Device setup kernels of libmgm (compiled with -fmad=false: every multiply and add is
+// rounded separately, so the operation sequences written in DESIGN.md give the same bits
+// as a sequential host loop).
+//   * batched tangent-plane PHS RBF-FD weights, one warp per stencil
+//   * batched GFD weights, one warp per stencil, Householder QR
+//   * batched PHS interpolation weights, one thread per fine point
+//   * SpGEMM for the Galerkin product, one CTA per output row, sort-based
+#include <cuda_runtime.h>
+
+#include <climits>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "mgm_internal.h"
+
+namespace mgm {
+
+#define FULL 0xffffffffu
+
+// ---------------------------------------------------------------------------------------
+// shared device helpers
+// ---------------------------------------------------------------------------------------
+__device__ __forceinline__ void tangent_basis_dev(const double* n, double* t1, double* t2) {
+    int a = 0;
+    if (fabs(n[1]) < fabs(n[a])) a = 1;
+    if (fabs(n[2]) < fabs(n[a])) a = 2;
+    for (int b = 0; b < 3; ++b) t1[b] = (b == a ? 1.0 : 0.0) - n[a] * n[b];
+    double s = t1[0] * t1[0] + t1[1] * t1[1];
+    s = s + t1[2] * t1[2];
+    double nn = sqrt(s);
+    for (int b = 0; b < 3; ++b) t1[b] = t1[b] / nn;
+    t2[0] = n[1] * t1[2] - n[2] * t1[1];
+    t2[1] = n[2] * t1[0] - n[0] * t1[2];
+    t2[2] = n[0] * t1[1] - n[1] * t1[0];
+}
+
+__device__ __forceinline__ void project_dev(const double* xc, const double* t1, const double* t2,
+                                            const double* xj, double& u, double& v) {
+    double d0 = xj[0] - xc[0], d1 = xj[1] - xc[1], d2 = xj[2] - xc[2];
+    double a = t1[0] * d0 + t1[1] * d1;
+    a = a + t1[2] * d2;
+    double b = t2[0] * d0 + t2[1] * d1;
+    b = b + t2[2] * d2;
+    u = a;
+    v = b;
+}
+
+__device__ __forceinline__ double dist2_dev(const double* x, const double* y) {
+    double dx = y[0] - x[0], dy = y[1] - x[1], dz = y[2] - x[2];
+    double s = dx * dx + dy * dy;
+    return s + dz * dz;
+}
+
+__device__ __forceinline__ double warp_max(double v) {
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(FULL, v, o));
+    return v;
+}
+
+// monomial x^i y^(d-i) in graded order; value by repeated multiplication (as DESIGN.md)
+__device__ __forceinline__ double monomial_dev(double x, double y, int col) {
+    int d = 0, c = col;
+    while (c > d) { c -= d + 1; ++d; }
+    int i = d - c;  // within degree d: i = d, d-1, ..., 0
+    double xp = 1.0, yp = 1.0;
+    for (int t = 0; t < i; ++t) xp = xp * x;
+    for (int t = 0; t < d - i; ++t) yp = yp * y;
+    return xp * yp;
+}
+__device__ __forceinline__ double monomial_lap0_dev(int col) {
+    int d = 0, c = col;
+    while (c > d) { c -= d + 1; ++d; }
+    int i = d - c;
+    return (d == 2 && (i == 2 || i == 0)) ? 2.0 : 0.0;
+}
+
+// Warp LU with partial pivoting on M (m x m, row-major in smem) and RHS b; the update
+// order of every entry equals the sequential right-looking algorithm; back substitution
+// column-oriented (descending j).  Returns false if |pivot| <= tol * max|M|.
+__device__ bool warp_lu_solve(double* M, double* b, double* lcol, int m, double tol) {
+    const int lane = threadIdx.x & 31;
+    double amax = 0.0;
+    for (int e = lane; e < m * m; e += 32) amax = fmax(amax, fabs(M[e]));
+    amax = warp_max(amax);
+    for (int k = 0; k < m; ++k) {
+        // pivot: max |M[i][k]|, lowest i on ties
+        double pv = -1.0;
+        int pi = INT_MAX;
+        for (int i = k + lane; i < m; i += 32) {
+            double v = fabs(M[i * m + k]);
+            if (v > pv) { pv = v; pi = i; }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            double ov = __shfl_xor_sync(FULL, pv, o);
+            int oi = __shfl_xor_sync(FULL, pi, o);
+            if (ov > pv || (ov == pv && oi < pi)) { pv = ov; pi = oi; }
+        }
+        if (!(pv > tol * amax)) return false;
+        if (pi != k) {
+            for (int j = lane; j < m; j += 32) {
+                double t = M[k * m + j];
+                M[k * m + j] = M[pi * m + j];
+                M[pi * m + j] = t;
+            }
+            if (lane == 0) { double t = b[k]; b[k] = b[pi]; b[pi] = t; }
+        }
+        __syncwarp();
+        double piv = M[k * m + k];
+        for (int i = k + 1 + lane; i < m; i += 32) {
+            double l = M[i * m + k] / piv;
+            lcol[i] = l;
+            M[i * m + k] = l;
+            b[i] = b[i] - l * b[k];
+        }
+        __syncwarp();
+        for (int j = k + 1 + lane; j < m; j += 32) {
+            double mk = M[k * m + j];
+            for (int i = k + 1; i < m; ++i) M[i * m + j] = M[i * m + j] - lcol[i] * mk;
+        }
+        __syncwarp();
+    }
+    for (int i = m - 1; i >= 0; --i) {
+        if (lane == 0) b[i] = b[i] / M[i * m + i];
+        __syncwarp();
+        double xi = b[i];
+        for (int r = lane; r < i; r += 32) b[r] = b[r] - M[r * m + i] * xi;
+        __syncwarp();
+    }
+    return true;
+}
+
+// ---------------------------------------------------------------------------------------
+// O4: PHS RBF-FD weights, one warp per stencil
+// smem per warp: M[m*m], b[m], lcol[m], z[2*ns]
+// ---------------------------------------------------------------------------------------
+__global__ void k_rbffd_weights(const double* __restrict__ pts, const double* __restrict__ nrm,
+                                const i32* __restrict__ sten, i64 n, int ns, int ell, int kphs,
+                                double* __restrict__ w, i64* fail) {
+    extern __shared__ double smem[];
+    const int L = (ell + 1) * (ell + 2) / 2, m = ns + L;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int per_warp = m * m + 2 * m + 2 * ns;
+    double* M = smem + (size_t)warp * per_warp;
+    double* b = M + m * m;
+    double* lcol = b + m;
+    double* z = lcol + m;
+    const int wpb = blockDim.x >> 5;
+    for (i64 i = (i64)blockIdx.x * wpb + warp; i < n; i += (i64)gridDim.x * wpb) {
+        double t1[3], t2[3];
+        tangent_basis_dev(nrm + 3 * i, t1, t2);
+        double rho = 0.0;
+        for (int j = lane; j < ns; j += 32) {
+            double u, v;
+            project_dev(pts + 3 * i, t1, t2, pts + 3 * (i64)sten[i * ns + j], u, v);
+            z[2 * j] = u;
+            z[2 * j + 1] = v;
+            rho = fmax(rho, sqrt(u * u + v * v));
+        }
+        rho = warp_max(rho);
+        __syncwarp();
+        for (int j = lane; j < 2 * ns; j += 32) z[j] = z[j] / rho;
+        __syncwarp();
+        for (int e = lane; e < m * m; e += 32) {
+            int a = e / m, c = e % m;
+            double v;
+            if (a < ns && c < ns) {
+                double dx = z[2 * a] - z[2 * c], dy = z[2 * a + 1] - z[2 * c + 1];
+                double r2 = dx * dx + dy * dy;
+                double r = sqrt(r2);
+                v = r;
+                for (int t = 0; t < kphs; ++t) v = v * r2;
+            } else if (a < ns) {
+                v = monomial_dev(z[2 * a], z[2 * a + 1], c - ns);
+            } else if (c < ns) {
+                v = monomial_dev(z[2 * c], z[2 * c + 1], a - ns);
+            } else {
+                v = 0.0;
+            }
+            M[e] = v;
+        }
+        for (int a = lane; a < m; a += 32) {
+            double v;
+            if (a < ns) {
+                double r2 = z[2 * a] * z[2 * a] + z[2 * a + 1] * z[2 * a + 1];
+                double r = sqrt(r2);
+                v = r;
+                for (int t = 0; t < kphs - 1; ++t) v = v * r2;
+                v = (double)((2 * kphs + 1) * (2 * kphs + 1)) * v;
+            } else {
+                v = monomial_lap0_dev(a - ns);
+            }
+            b[a] = v;
+        }
+        __syncwarp();
+        bool ok = warp_lu_solve(M, b, lcol, m, 1e-14);
+        if (!ok) {
+            if (lane == 0) atomicMin((unsigned long long*)fail, (unsigned long long)i);
+            for (int j = lane; j < ns; j += 32) w[i * ns + j] = 0.0;
+        } else {
+            double rr = rho * rho;
+            for (int j = lane; j < ns; j += 32) w[i * ns + j] = b[j] / rr;
+        }
+        __syncwarp();
+    }
+}
+
+int launch_rbffd_weights(const double* pts, const double* nrm, const i32* sten, i64 n, int ns,
+                         int ell, int k, double* w, i64* fail_dev, void* stream) {
+    int L = (ell + 1) * (ell + 2) / 2, m = ns + L;
+    size_t per_warp = (size_t)(m * m + 2 * m + 2 * ns) * sizeof(double);
+    int wpb = (int)std::max<size_t>(1, std::min<size_t>(8, (200 * 1024) / per_warp));
+    size_t smem = per_warp * wpb;
+    cudaFuncSetAttribute(k_rbffd_weights, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    i64 blocks = std::min<i64>((n + wpb - 1) / wpb, 148 * 16);
+    k_rbffd_weights<<<(unsigned)blocks, 32 * wpb, smem, (cudaStream_t)stream>>>(pts, nrm, sten, n, ns,
+                                                                                 ell, k, w, fail_dev);
+    return (int)cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------------------
+// O5: GFD weights.  rho of every point first (own projected stencil radius).
+// ---------------------------------------------------------------------------------------
+__global__ void k_stencil_radius(const double* __restrict__ pts, const double* __restrict__ nrm,
+                                 const i32* __restrict__ sten, i64 n, int ns, double* rho_out) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, wpb = blockDim.x >> 5;
+    for (i64 i = (i64)blockIdx.x * wpb + warp; i < n; i += (i64)gridDim.x * wpb) {
+        double t1[3], t2[3];
+        tangent_basis_dev(nrm + 3 * i, t1, t2);
+        double rho = 0.0;
+        for (int j = lane; j < ns; j += 32) {
+            double u, v;
+            project_dev(pts + 3 * i, t1, t2, pts + 3 * (i64)sten[i * ns + j], u, v);
+            rho = fmax(rho, sqrt(u * u + v * v));
+        }
+        rho = warp_max(rho);
+        if (lane == 0) rho_out[i] = rho;
+    }
+}
+
+int launch_stencil_radius(const double* pts, const double* nrm, const i32* sten, i64 n, int ns,
+                          double* rho, void* stream) {
+    i64 blocks = std::min<i64>((n + 7) / 8, 148 * 32);
+    k_stencil_radius<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(pts, nrm, sten, n, ns, rho);
+    return (int)cudaGetLastError();
+}
+
+// smem per warp: B[ns*L], V[ns*L], tau[L], sw[ns], q[ns], y[L]
+__global__ void k_gfd_weights(const double* __restrict__ pts, const double* __restrict__ nrm,
+                              const i32* __restrict__ sten, i64 n, int ns, int ell, double alpha,
+                              const double* __restrict__ rho_all, double* __restrict__ w, i64* fail) {
+    extern __shared__ double smem[];
+    const int L = (ell + 1) * (ell + 2) / 2;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
+    const int per_warp = 2 * ns * L + 2 * L + 2 * ns;
+    double* B = smem + (size_t)warp * per_warp;
+    double* V = B + ns * L;
+    double* tau = V + ns * L;
+    double* y = tau + L;
+    double* sw = y + L;
+    double* q = sw + ns;
+    for (i64 i = (i64)blockIdx.x * wpb + warp; i < n; i += (i64)gridDim.x * wpb) {
+        double t1[3], t2[3];
+        tangent_basis_dev(nrm + 3 * i, t1, t2);
+        const double rho = rho_all[i];
+        const double rr = rho * rho;
+        for (int j = lane; j < ns; j += 32) {
+            i64 g = sten[i * ns + j];
+            double u, v;
+            project_dev(pts + 3 * i, t1, t2, pts + 3 * g, u, v);
+            double d2 = u * u + v * v;
+            double rg = rho_all[g];
+            double s = sqrt(exp(-alpha * d2 / (rr + rg * rg)));
+            sw[j] = s;
+            double zx = u / rho, zy = v / rho;
+            for (int c = 0; c < L; ++c) B[j * L + c] = s * monomial_dev(zx, zy, c);
+        }
+        __syncwarp();
+        double rmax = 0.0;
+        bool ok = true;
+        for (int k = 0; k < L; ++k) {
+            // column norm by one lane (sequential order), reflector v
+            double nx = 0.0, x0 = 0.0;
+            if (lane == 0) {
+                double s = 0.0;
+                for (int r = k; r < ns; ++r) s = s + B[r * L + k] * B[r * L + k];
+                nx = sqrt(s);
+                x0 = B[k * L + k];
+            }
+            nx = __shfl_sync(FULL, nx, 0);
+            x0 = __shfl_sync(FULL, x0, 0);
+            double alph = (x0 >= 0.0) ? -nx : nx;
+            for (int r = lane; r < ns; r += 32)
+                V[r * L + k] = (r < k) ? 0.0 : (r == k ? x0 - alph : B[r * L + k]);
+            __syncwarp();
+            if (nx == 0.0) {
+                if (lane == 0) tau[k] = 0.0;
+                __syncwarp();
+                continue;
+            }
+            if (lane == 0) {
+                double vv = 0.0;
+                for (int r = k; r < ns; ++r) vv = vv + V[r * L + k] * V[r * L + k];
+                tau[k] = 2.0 / vv;
+            }
+            __syncwarp();
+            for (int c = k + lane; c < L; c += 32) {
+                double d = 0.0;
+                for (int r = k; r < ns; ++r) d = d + V[r * L + k] * B[r * L + c];
+                d = tau[k] * d;
+                for (int r = k; r < ns; ++r) B[r * L + c] = B[r * L + c] - d * V[r * L + k];
+            }
+            __syncwarp();
+            rmax = fmax(rmax, fabs(B[k * L + k]));
+        }
+        for (int k = 0; k < L; ++k)
+            if (!(fabs(B[k * L + k]) > 1e-12 * rmax)) ok = false;
+        if (!ok) {
+            if (lane == 0) atomicMin((unsigned long long*)fail, (unsigned long long)i);
+            for (int j = lane; j < ns; j += 32) w[i * ns + j] = 0.0;
+            __syncwarp();
+            continue;
+        }
+        if (lane == 0) {
+            for (int k = 0; k < L; ++k) {  // y = R^{-T} Lap p
+                double s = monomial_lap0_dev(k);
+                for (int c = 0; c < k; ++c) s = s - B[c * L + k] * y[c];
+                y[k] = s / B[k * L + k];
+            }
+            for (int r = 0; r < ns; ++r) q[r] = (r < L) ? y[r] : 0.0;
+            for (int k = L - 1; k >= 0; --k) {  // q = H_0 ... H_{L-1} [y; 0]
+                double d = 0.0;
+                for (int r = k; r < ns; ++r) d = d + V[r * L + k] * q[r];
+                d = tau[k] * d;
+                for (int r = k; r < ns; ++r) q[r] = q[r] - d * V[r * L + k];
+            }
+        }
+        __syncwarp();
+        for (int j = lane; j < ns; j += 32) w[i * ns + j] = (sw[j] * q[j]) / rr;
+        __syncwarp();
+    }
+}
+
+int launch_gfd_weights(const double* pts, const double* nrm, const i32* sten, i64 n, int ns,
+                       int ell, double alpha, const double* rho, double* w, i64* fail_dev,
+                       void* stream) {
+    int L = (ell + 1) * (ell + 2) / 2;
+    size_t per_warp = (size_t)(2 * ns * L + 2 * L + 2 * ns) * sizeof(double);
+    int wpb = (int)std::max<size_t>(1, std::min<size_t>(8, (200 * 1024) / per_warp));
+    size_t smem = per_warp * wpb;
+    cudaFuncSetAttribute(k_gfd_weights, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    i64 blocks = std::min<i64>((n + wpb - 1) / wpb, 148 * 16);
+    k_gfd_weights<<<(unsigned)blocks, 32 * wpb, smem, (cudaStream_t)stream>>>(pts, nrm, sten, n, ns, ell,
+                                                                              alpha, rho, w, fail_dev);
+    return (int)cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------------------
+// O9: PHS interpolation weights, one thread per fine point.
+// ---------------------------------------------------------------------------------------
+__global__ void k_interp_weights(const double* __restrict__ fine, i64 nf,
+                                 const double* __restrict__ coarse, const i32* __restrict__ sten,
+                                 int m, double* __restrict__ w, i32* __restrict__ cnt, i64* fail) {
+    double M[17 * 17], b[17];
+    const int mm = m + 1;
+    for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < nf; i += (i64)gridDim.x * blockDim.x) {
+        const double* x = fine + 3 * i;
+        if (dist2_dev(x, coarse + 3 * (i64)sten[i * m]) == 0.0) {
+            for (int a = 0; a < m; ++a) w[i * m + a] = (a == 0) ? 1.0 : 0.0;
+            cnt[i] = 1;
+            continue;
+        }
+        for (int a = 0; a < m; ++a) {
+            const double* ya = coarse + 3 * (i64)sten[i * m + a];
+            for (int c = 0; c < m; ++c) M[a * mm + c] = sqrt(dist2_dev(ya, coarse + 3 * (i64)sten[i * m + c]));
+            M[a * mm + m] = 1.0;
+            M[m * mm + a] = 1.0;
+            b[a] = sqrt(dist2_dev(x, ya));
+        }
+        M[m * mm + m] = 0.0;
+        b[m] = 1.0;
+        // sequential LU, same operation order as the warp version
+        double amax = 0.0;
+        for (int e = 0; e < mm * mm; ++e) amax = fmax(amax, fabs(M[e]));
+        bool ok = true;
+        for (int k = 0; k < mm && ok; ++k) {
+            int p = k;
+            double pv = fabs(M[k * mm + k]);
+            for (int r = k + 1; r < mm; ++r)
+                if (fabs(M[r * mm + k]) > pv) { pv = fabs(M[r * mm + k]); p = r; }
+            if (!(pv > 1e-14 * amax)) { ok = false; break; }
+            if (p != k) {
+                for (int j = 0; j < mm; ++j) { double t = M[k * mm + j]; M[k * mm + j] = M[p * mm + j]; M[p * mm + j] = t; }
+                double t = b[k]; b[k] = b[p]; b[p] = t;
+            }
+            double piv = M[k * mm + k];
+            for (int r = k + 1; r < mm; ++r) {
+                double l = M[r * mm + k] / piv;
+                M[r * mm + k] = l;
+                for (int j = k + 1; j < mm; ++j) M[r * mm + j] = M[r * mm + j] - l * M[k * mm + j];
+                b[r] = b[r] - l * b[k];
+            }
+        }
+        if (!ok) {
+            atomicMin((unsigned long long*)fail, (unsigned long long)i);
+            for (int a = 0; a < m; ++a) w[i * m + a] = 0.0;
+            cnt[i] = m;
+            continue;
+        }
+        for (int r = mm - 1; r >= 0; --r) {
+            double s = b[r];
+            for (int j = mm - 1; j > r; --j) s = s - M[r * mm + j] * b[j];
+            b[r] = s / M[r * mm + r];
+        }
+        for (int a = 0; a < m; ++a) w[i * m + a] = b[a];
+        cnt[i] = m;
+    }
+}
+
+int launch_interp_weights(const double* fine, i64 nf, const double* coarse, const i32* sten,
+                          int m, double* w, i32* cnt, i64* fail_dev, void* stream) {
+    if (m > 16) return (int)cudaErrorInvalidValue;
+    i64 blocks = std::min<i64>((nf + 127) / 128, 148 * 32);
+    k_interp_weights<<<(unsigned)blocks, 128, 0, (cudaStream_t)stream>>>(fine, nf, coarse, sten, m, w,
+                                                                         cnt, fail_dev);
+    return (int)cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------------------
+// O10: SpGEMM C = A B, one CTA per output row (grid-stride).  Products of row i are laid
+// out in canonical order (A entries by ascending column, then B entries by ascending
+// column), keyed (col << 32 | product index), bitonic-sorted in shared memory; each run
+// of equal columns is summed sequentially in product order, as the host loop would.
+// ---------------------------------------------------------------------------------------
+__global__ void k_row_products(const i64* __restrict__ ap, const i32* __restrict__ ai,
+                               const i64* __restrict__ bp, i64 nrows, i64* __restrict__ cnt) {
+    for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < nrows; i += (i64)gridDim.x * blockDim.x) {
+        i64 s = 0;
+        for (i64 t = ap[i]; t < ap[i + 1]; ++t) s += bp[ai[t] + 1] - bp[ai[t]];
+        cnt[i] = s;
+    }
+}
+
+__device__ void block_bitonic_sort(unsigned long long* keys, int n2) {
+    for (int size = 2; size <= n2; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int t = threadIdx.x; t < (n2 >> 1); t += blockDim.x) {
+                int lo = 2 * stride * (t / stride) + (t % stride);
+                int hi = lo + stride;
+                bool up = ((lo & size) == 0);
+                unsigned long long a = keys[lo], b = keys[hi];
+                if ((a > b) == up) { keys[lo] = b; keys[hi] = a; }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// numeric == false: write the unique-column count of each row to cnt.
+// numeric == true : write columns/values at cptr[i].
+template <bool NUMERIC>
+__global__ void k_spgemm_rows(i64 nrows, const i64* __restrict__ ap, const i32* __restrict__ ai,
+                              const double* __restrict__ av, const i64* __restrict__ bp,
+                              const i32* __restrict__ bi, const double* __restrict__ bv, int n2,
+                              i64* __restrict__ cnt, const i64* __restrict__ cptr,
+                              i32* __restrict__ ci, double* __restrict__ cv) {
+    extern __shared__ unsigned long long sm[];
+    unsigned long long* keys = sm;                          // n2
+    double* vals = (double*)(keys + n2);                    // n2
+    int* flag = (int*)(vals + n2);                          // n2 + 1 (scan)
+    __shared__ i64 off_s[1025];
+    __shared__ int total_s;
+    for (i64 i = blockIdx.x; i < nrows; i += gridDim.x) {
+        const i64 a0 = ap[i], a1 = ap[i + 1];
+        const int na = (int)(a1 - a0);
+        // offsets of each A entry's products (serial, rows are short)
+        if (threadIdx.x == 0) {
+            i64 o = 0;
+            for (int t = 0; t < na; ++t) {
+                off_s[t] = o;
+                i32 k = ai[a0 + t];
+                o += bp[k + 1] - bp[k];
+            }
+            off_s[na] = o;
+            total_s = (int)o;
+        }
+        __syncthreads();
+        const int total = total_s;
+        for (int t = 0; t < na; ++t) {
+            i32 k = ai[a0 + t];
+            i64 b0 = bp[k], b1 = bp[k + 1];
+            double a = NUMERIC ? av[a0 + t] : 0.0;
+            for (i64 s = b0 + threadIdx.x; s < b1; s += blockDim.x) {
+                int pidx = (int)(off_s[t] + (s - b0));
+                keys[pidx] = ((unsigned long long)(unsigned)bi[s] << 32) | (unsigned)pidx;
+                if (NUMERIC) vals[pidx] = __dmul_rn(a, bv[s]);
+            }
+        }
+        for (int p = total + threadIdx.x; p < n2; p += blockDim.x) keys[p] = ~0ull;
+        __syncthreads();
+        block_bitonic_sort(keys, n2);
+        // segment starts and their ranks (exclusive scan, serial over warps for simplicity)
+        for (int p = threadIdx.x; p < total; p += blockDim.x)
+            flag[p] = (p == 0 || (keys[p] >> 32) != (keys[p - 1] >> 32)) ? 1 : 0;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int s = 0;
+            for (int p = 0; p < total; ++p) { int f = flag[p]; flag[p] = f ? s : -1; s += f; }
+            flag[total] = s;
+        }
+        __syncthreads();
+        if (!NUMERIC) {
+            if (threadIdx.x == 0) cnt[i] = flag[total];
+        } else {
+            const i64 base = cptr[i];
+            for (int p = threadIdx.x; p < total; p += blockDim.x) {
+                int rank = flag[p];
+                if (rank < 0) continue;
+                unsigned col = (unsigned)(keys[p] >> 32);
+                double s = 0.0;
+                for (int q = p; q < total && (unsigned)(keys[q] >> 32) == col; ++q)
+                    s = __dadd_rn(s, vals[(unsigned)(keys[q] & 0xffffffffu)]);
+                ci[base + rank] = (i32)col;
+                cv[base + rank] = s;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+static inline int next_pow2(i64 v) {
+    int p = 1;
+    while (p < v) p <<= 1;
+    return p;
+}
+
+int spgemm_device(const DevCSR& A, const DevCSR& B, DevCSR& C, void* stream, std::string& err) {
+    cudaStream_t st = (cudaStream_t)stream;
+    C = DevCSR();
+    C.nrows = A.nrows;
+    C.ncols = B.ncols;
+    i64 n = A.nrows;
+    i64* d_cnt = nullptr;
+    cudaError_t e = cudaMalloc(&d_cnt, sizeof(i64) * (n + 1));
+    if (e != cudaSuccess) { err = "cudaMalloc"; return (int)e; }
+    k_row_products<<<(unsigned)std::min<i64>((n + 255) / 256, 148 * 16), 256, 0, st>>>(A.ptr, A.col, B.ptr, n, d_cnt);
+    std::vector<i64> cnt(n);
+    cudaMemcpyAsync(cnt.data(), d_cnt, sizeof(i64) * n, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    i64 mx = 0;
+    for (i64 v : cnt) mx = std::max(mx, v);
+    // A rows longer than 1024 entries are not supported by off_s
+    std::vector<i64> hap(2);
+    int n2 = next_pow2(std::max<i64>(mx, 2));
+    size_t smem = (size_t)n2 * (8 + 8 + 4) + 8;
+    if (smem > 200 * 1024) {
+        cudaFree(d_cnt);
+        err = "SpGEMM row with " + std::to_string(mx) + " products exceeds the shared-memory row buffer";
+        return (int)cudaErrorInvalidValue;
+    }
+    cudaFuncSetAttribute(k_spgemm_rows<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_spgemm_rows<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    unsigned grid = (unsigned)std::min<i64>(n, 148 * 8);
+    int threads = n2 >= 2048 ? 512 : 256;
+    k_spgemm_rows<false><<<grid, threads, smem, st>>>(n, A.ptr, A.col, A.val, B.ptr, B.col, B.val, n2, d_cnt,
+                                                      nullptr, nullptr, nullptr);
+    cudaMemcpyAsync(cnt.data(), d_cnt, sizeof(i64) * n, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    std::vector<i64> ptr(n + 1, 0);
+    for (i64 r = 0; r < n; ++r) ptr[r + 1] = ptr[r] + cnt[r];
+    C.nnz = ptr[n];
+    e = cudaMalloc(&C.ptr, sizeof(i64) * (n + 1));
+    if (e == cudaSuccess) e = cudaMalloc(&C.col, sizeof(i32) * std::max<i64>(1, C.nnz));
+    if (e == cudaSuccess) e = cudaMalloc(&C.val, sizeof(double) * std::max<i64>(1, C.nnz));
+    if (e != cudaSuccess) { cudaFree(d_cnt); err = "cudaMalloc (SpGEMM output)"; return (int)e; }
+    cudaMemcpyAsync(C.ptr, ptr.data(), sizeof(i64) * (n + 1), cudaMemcpyHostToDevice, st);
+    k_spgemm_rows<true><<<grid, threads, smem, st>>>(n, A.ptr, A.col, A.val, B.ptr, B.col, B.val, n2, nullptr,
+                                                     C.ptr, C.col, C.val);
+    e = cudaStreamSynchronize(st);
+    cudaFree(d_cnt);
+    if (e != cudaSuccess) { err = "SpGEMM kernel"; return (int)e; }
+    return (int)cudaGetLastError();
+}
+
+void free_dev_csr(DevCSR& M) {
+    if (M.ptr) cudaFree(M.ptr);
+    if (M.col) cudaFree(M.col);
+    if (M.val) cudaFree(M.val);
+    M = DevCSR();
+}
+
+int upload_csr(const HostCSR& H, DevCSR& D, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    D.nrows = H.nrows;
+    D.ncols = H.ncols;
+    D.nnz = H.nnz();
+    cudaError_t e = cudaMalloc(&D.ptr, sizeof(i64) * (H.nrows + 1));
+    if (e == cudaSuccess) e = cudaMalloc(&D.col, sizeof(i32) * std::max<i64>(1, D.nnz));
+    if (e == cudaSuccess) e = cudaMalloc(&D.val, sizeof(double) * std::max<i64>(1, D.nnz));
+    if (e != cudaSuccess) return (int)e;
+    cudaMemcpyAsync(D.ptr, H.ptr.data(), sizeof(i64) * (H.nrows + 1), cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(D.col, H.col.data(), sizeof(i32) * D.nnz, cudaMemcpyHostToDevice, st);
+    if (!H.val.empty()) cudaMemcpyAsync(D.val, H.val.data(), sizeof(double) * D.nnz, cudaMemcpyHostToDevice, st);
+    return (int)cudaStreamSynchronize(st);
+}
+
+int download_csr(const DevCSR& D, HostCSR& H, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    H.nrows = D.nrows;
+    H.ncols = D.ncols;
+    H.ptr.resize(D.nrows + 1);
+    H.col.resize(D.nnz);
+    H.val.resize(D.nnz);
+    cudaMemcpyAsync(H.ptr.data(), D.ptr, sizeof(i64) * (D.nrows + 1), cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(H.col.data(), D.col, sizeof(i32) * D.nnz, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(H.val.data(), D.val, sizeof(double) * D.nnz, cudaMemcpyDeviceToHost, st);
+    return (int)cudaStreamSynchronize(st);
+}
+
+}  // namespace mgm

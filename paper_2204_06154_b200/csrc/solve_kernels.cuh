@@ -1,0 +1,267 @@
+// Solve-phase kernels of libmgm (sm_100a, fp64).  All are HBM/latency bound sparse
+// gathers: no tensor cores.  Data layout:
+//   * L_j, R_j: SELL-32 -- rows in lib order (colour-major, Morton within a colour), slices
+//     of 32 consecutive rows stored slot-major (entry k of row r at sptr[r/32] + 32k + r%32),
+//     diagonal in slot 0 for L_j, padding = (own row, 0.0).
+//   * P_j: ELL, width m, slot-major [m][n_j].
+//   * vectors: fp64, lib order; Poisson mode appends the multiplier lambda at index n_j.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace mgm {
+
+__device__ __forceinline__ double ld_stream_f64(const double* p) {
+    double v;
+    asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ int ld_stream_i32(const int* p) {
+    int v;
+    asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+
+// One colour of a Gauss-Seidel sweep (Poisson variant P:348-352):
+//   r = f_i - a_ii u_i - sum_{j != i} a_ij u_j [- c_i lambda];  u_i += r / a_ii
+// rows [r0, r1) of one colour; threads are aligned to 32-row slices.
+template <bool POISSON>
+__global__ void __launch_bounds__(128) k_gs_colour(int r0, int r1, const int64_t* __restrict__ sptr,
+                                                   const int* __restrict__ scol,
+                                                   const double* __restrict__ sval,
+                                                   const double* __restrict__ f, double* u,
+                                                   const double* __restrict__ c, int n) {
+    const int r = (r0 & ~31) + blockIdx.x * blockDim.x + threadIdx.x;
+    if (r < r0 || r >= r1) return;
+    const int64_t base = sptr[r >> 5] + (r & 31);
+    const int w = (int)((sptr[(r >> 5) + 1] - sptr[r >> 5]) >> 5);
+    const double* v = sval + base;
+    const int* cc = scol + base;
+    const double d = ld_stream_f64(v);
+    double acc = f[r] - d * u[r];
+#pragma unroll 8
+    for (int k = 1; k < w; ++k) acc -= ld_stream_f64(v + 32 * k) * u[ld_stream_i32(cc + 32 * k)];
+    if (POISSON) acc -= c[r] * u[n];
+    u[r] += acc / d;
+}
+
+// y = L x  (MODE 0),  y = f - L x  (MODE 1).  Poisson: border term c_i * x[n].
+template <int MODE, bool POISSON>
+__global__ void __launch_bounds__(256) k_sell_spmv(int n, const int64_t* __restrict__ sptr,
+                                                   const int* __restrict__ scol,
+                                                   const double* __restrict__ sval,
+                                                   const double* __restrict__ x,
+                                                   const double* __restrict__ f,
+                                                   double* __restrict__ y,
+                                                   const double* __restrict__ c) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    const int64_t base = sptr[r >> 5] + (r & 31);
+    const int w = (int)((sptr[(r >> 5) + 1] - sptr[r >> 5]) >> 5);
+    const double* v = sval + base;
+    const int* cc = scol + base;
+    double acc = 0.0;
+#pragma unroll 8
+    for (int k = 0; k < w; ++k) acc += ld_stream_f64(v + 32 * k) * x[ld_stream_i32(cc + 32 * k)];
+    if (POISSON) acc += c[r] * x[n];
+    y[r] = (MODE == 0) ? acc : f[r] - acc;
+}
+
+// e[r] += sum_k P[k][r] * ec[Pcol[k][r]]  (interpolate + correct)
+template <bool POISSON>
+__global__ void __launch_bounds__(256) k_interp_correct(int n, int m, const int* __restrict__ pcol,
+                                                        const double* __restrict__ pval,
+                                                        const double* __restrict__ ec,
+                                                        double* __restrict__ e, int nc) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r > n) return;
+    if (r == n) {
+        if (POISSON) e[n] += ec[nc];
+        return;
+    }
+    double acc = 0.0;
+    for (int k = 0; k < m; ++k)
+        acc += ld_stream_f64(pval + (int64_t)k * n + r) * ec[ld_stream_i32(pcol + (int64_t)k * n + r)];
+    e[r] += acc;
+}
+
+// y[r] = sum_k P[k][r] * x[...]  (plain interpolation, test hook)
+template <bool POISSON>
+__global__ void k_interp(int n, int m, const int* __restrict__ pcol, const double* __restrict__ pval,
+                         const double* __restrict__ x, double* __restrict__ y, int nc) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r > n) return;
+    if (r == n) {
+        if (POISSON) y[n] = x[nc];
+        return;
+    }
+    double acc = 0.0;
+    for (int k = 0; k < m; ++k) acc += pval[(int64_t)k * n + r] * x[pcol[(int64_t)k * n + r]];
+    y[r] = acc;
+}
+
+// Dense coarse solve with the LU factors (column-major) and pivots, one warp.
+__global__ void k_coarse_solve(int m, const double* __restrict__ LU, const int* __restrict__ piv,
+                               const double* __restrict__ rhs, double* __restrict__ x) {
+    extern __shared__ double b[];
+    const int lane = threadIdx.x;
+    for (int i = lane; i < m; i += 32) b[i] = rhs[i];
+    __syncwarp();
+    if (lane == 0)
+        for (int k = 0; k < m; ++k) {
+            int p = piv[k];
+            if (p != k) { double t = b[k]; b[k] = b[p]; b[p] = t; }
+        }
+    __syncwarp();
+    for (int k = 0; k < m; ++k) {  // forward, unit lower
+        const double xk = b[k];
+        const double* col = LU + (int64_t)k * m;
+        for (int i = k + 1 + lane; i < m; i += 32) b[i] -= col[i] * xk;
+        __syncwarp();
+    }
+    for (int i = m - 1; i >= 0; --i) {  // backward
+        const double* col = LU + (int64_t)i * m;
+        if (lane == 0) b[i] = b[i] / col[i];
+        __syncwarp();
+        const double xi = b[i];
+        for (int r = lane; r < i; r += 32) b[r] -= col[r] * xi;
+        __syncwarp();
+    }
+    for (int i = lane; i < m; i += 32) x[i] = b[i];
+}
+
+__global__ void k_fill(int64_t n, double* __restrict__ x, double v) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) x[i] = v;
+}
+__global__ void k_copy1(const double* __restrict__ src, double* __restrict__ dst) { *dst = *src; }
+
+// out[i] = in[idx[i]]  /  out[idx[i]] = in[i]
+__global__ void k_gather(int n, const int* __restrict__ idx, const double* __restrict__ in,
+                         double* __restrict__ out) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = in[idx[i]];
+}
+__global__ void k_scatter(int n, const int* __restrict__ idx, const double* __restrict__ in,
+                          double* __restrict__ out) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[idx[i]] = in[i];
+}
+
+// ------------------------------- deterministic reductions ------------------------------
+constexpr int RED_BLOCKS = 296;   // 2 per SM, fixed so reductions are bitwise reproducible
+constexpr int RED_THREADS = 256;
+constexpr int MD_GROUP = 8;       // vectors per pass of the multi-dot
+
+__device__ __forceinline__ double warp_sum(double v) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// partials[b * k1 + j] = sum over block b's chunk of V_j . w   (V_j = V + j*ld)
+__global__ void __launch_bounds__(RED_THREADS) k_multidot(int64_t n, const double* __restrict__ V,
+                                                          int64_t ld, int k1,
+                                                          const double* __restrict__ w,
+                                                          double* __restrict__ partials) {
+    __shared__ double red[RED_THREADS / 32][MD_GROUP];
+    const int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
+    const int64_t b0 = blockIdx.x * chunk, b1 = min(n, b0 + chunk);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int g = 0; g < k1; g += MD_GROUP) {
+        const int gn = min(MD_GROUP, k1 - g);
+        double s[MD_GROUP];
+#pragma unroll
+        for (int q = 0; q < MD_GROUP; ++q) s[q] = 0.0;
+        for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
+            const double wi = w[i];
+#pragma unroll
+            for (int q = 0; q < MD_GROUP; ++q)
+                if (q < gn) s[q] += V[(int64_t)(g + q) * ld + i] * wi;
+        }
+#pragma unroll
+        for (int q = 0; q < MD_GROUP; ++q) {
+            double t = warp_sum(s[q]);
+            if (lane == 0) red[warp][q] = t;
+        }
+        __syncthreads();
+        if (threadIdx.x < gn) {
+            double t = 0.0;
+            for (int ww = 0; ww < RED_THREADS / 32; ++ww) t += red[ww][threadIdx.x];
+            partials[(int64_t)blockIdx.x * k1 + g + threadIdx.x] = t;
+        }
+        __syncthreads();
+    }
+}
+
+// out[j] = scale * sum_b partials[b*k1 + j] (+ out0[j] if accumulate)
+__global__ void k_reduce_partials(const double* __restrict__ partials, int nblk, int k1,
+                                  double* __restrict__ out) {
+    for (int j = threadIdx.x; j < k1; j += blockDim.x) {
+        double t = 0.0;
+        for (int b = 0; b < nblk; ++b) t += partials[(int64_t)b * k1 + j];
+        out[j] = t;
+    }
+}
+
+// w[i] -= sum_j V_j[i] * h[j]
+__global__ void __launch_bounds__(256) k_multiaxpy(int64_t n, const double* __restrict__ V,
+                                                   int64_t ld, int k1, const double* __restrict__ h,
+                                                   double* __restrict__ w) {
+    __shared__ double hs[256];
+    for (int j = threadIdx.x; j < k1; j += blockDim.x) hs[j] = h[j];
+    __syncthreads();
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        double acc = w[i];
+        for (int j = 0; j < k1; ++j) acc -= V[(int64_t)j * ld + i] * hs[j];
+        w[i] = acc;
+    }
+}
+
+// y[i] = sum_j V_j[i] * h[j]
+__global__ void __launch_bounds__(256) k_lincomb(int64_t n, const double* __restrict__ V, int64_t ld,
+                                                 int k1, const double* __restrict__ h,
+                                                 double* __restrict__ y) {
+    __shared__ double hs[256];
+    for (int j = threadIdx.x; j < k1; j += blockDim.x) hs[j] = h[j];
+    __syncthreads();
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        double acc = 0.0;
+        for (int j = 0; j < k1; ++j) acc += V[(int64_t)j * ld + i] * hs[j];
+        y[i] = acc;
+    }
+}
+
+// dst = src / sqrt(*nrm2)
+__global__ void k_scale_by_invnorm(int64_t n, const double* __restrict__ src,
+                                   const double* __restrict__ nrm2, double* __restrict__ dst) {
+    const double inv = 1.0 / sqrt(*nrm2);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = src[i] * inv;
+}
+// dst = a*x + b*y
+__global__ void k_axpby(int64_t n, double a, const double* __restrict__ x, double b,
+                        const double* __restrict__ y, double* __restrict__ dst) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = a * x[i] + b * y[i];
+}
+// h[j] += h2[j]
+__global__ void k_vadd(int k1, double* __restrict__ h, const double* __restrict__ h2) {
+    for (int j = threadIdx.x; j < k1; j += blockDim.x) h[j] += h2[j];
+}
+// y[n] = f[n]*fs - sum   (border row of the Poisson system), single block finish
+__global__ void k_border_finish(const double* __restrict__ partials, int nblk, double fs,
+                                const double* __restrict__ f, int n, double sign,
+                                double* __restrict__ y) {
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int b = 0; b < nblk; ++b) t += partials[b];
+        y[n] = (f ? fs * f[n] : 0.0) + sign * t;
+    }
+}
+
+}  // namespace mgm

@@ -1,0 +1,345 @@
+"""Thin ctypes binding of libmgm's C ABI (include/mgm.h).  Argument marshalling only:
+every step of the MGM path runs in libmgm's CUDA kernels.  There is no fallback; if
+libmgm.so is missing or cannot be loaded this module raises.
+
+Function names mirror the C ABI (``mgm_setup``, ``mgm_vcycle``, ``mgm_solve``, ...);
+:class:`MGM` is a small convenience wrapper that owns a context and takes torch tensors
+(device memory and streams come from PyTorch; the arithmetic does not).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmgm.so")
+
+MGM_OK, MGM_ERR_ARG, MGM_ERR_UNISOLVENT, MGM_ERR_SINGULAR, MGM_ERR_BREAKDOWN, \
+    MGM_ERR_CUDA, MGM_ERR_NCCL, MGM_ERR_OOM, MGM_ERR_INPUT = range(9)
+OP_SPMV, OP_SWEEP, OP_RESIDUAL, OP_RESTRICT, OP_INTERP, OP_COARSE = range(6)
+STATUS_NAMES = {0: "MGM_OK", 1: "MGM_ERR_ARG", 2: "MGM_ERR_UNISOLVENT", 3: "MGM_ERR_SINGULAR",
+                4: "MGM_ERR_BREAKDOWN", 5: "MGM_ERR_CUDA", 6: "MGM_ERR_NCCL", 7: "MGM_ERR_OOM",
+                8: "MGM_ERR_INPUT"}
+
+
+class StencilParams(ctypes.Structure):
+    _fields_ = [("method", ctypes.c_int), ("poly_degree", ctypes.c_int), ("phs_k", ctypes.c_int),
+                ("stencil_n", ctypes.c_int), ("gfd_alpha", ctypes.c_double),
+                ("problem", ctypes.c_int), ("mu", ctypes.c_double)]
+
+
+class LevelParams(ctypes.Structure):
+    _fields_ = [("num_levels", ctypes.c_int), ("n_min", ctypes.c_int),
+                ("coarsen_factor", ctypes.c_int), ("interp_m", ctypes.c_int),
+                ("nu1", ctypes.c_int), ("nu2", ctypes.c_int), ("smoother", ctypes.c_int),
+                ("restart", ctypes.c_int)]
+
+
+class Report(ctypes.Structure):
+    _fields_ = [("iterations", ctypes.c_int), ("converged", ctypes.c_int),
+                ("final_rel_residual", ctypes.c_double),
+                ("history", ctypes.POINTER(ctypes.c_double)), ("history_cap", ctypes.c_int),
+                ("lambda_", ctypes.c_double), ("setup_ms", ctypes.c_double),
+                ("solve_ms", ctypes.c_double)]
+
+
+_vp = ctypes.c_void_p
+_i64 = ctypes.c_int64
+_i64p = ctypes.POINTER(ctypes.c_int64)
+_i32p = ctypes.POINTER(ctypes.c_int32)
+_f64p = ctypes.POINTER(ctypes.c_double)
+
+_SIGS = {
+    "mgm_setup": ([_f64p, _f64p, _i64, ctypes.POINTER(StencilParams), ctypes.POINTER(LevelParams),
+                   _vp, ctypes.POINTER(_vp)], ctypes.c_int),
+    "mgm_vcycle": ([_vp, _vp, _vp, _vp], ctypes.c_int),
+    "mgm_solve": ([_vp, _vp, _vp, ctypes.c_double, ctypes.c_int, ctypes.c_int,
+                   ctypes.POINTER(Report), _vp], ctypes.c_int),
+    "mgm_solve_host": ([_vp, _vp, _vp, ctypes.c_double, ctypes.c_int, ctypes.c_int,
+                        ctypes.POINTER(Report), _vp], ctypes.c_int),
+    "mgm_destroy": ([_vp], ctypes.c_int),
+    "mgm_last_error": ([_vp, _i64p], ctypes.c_char_p),
+    "mgm_num_levels": ([_vp, ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
+    "mgm_level_info": ([_vp, ctypes.c_int, _i64p, _i64p, _i64p, ctypes.POINTER(ctypes.c_int),
+                        _i64p], ctypes.c_int),
+    "mgm_export_level": ([_vp, ctypes.c_int, _i64p, _i64p, _i32p, _f64p, _i32p, _i64p, _i32p,
+                          _f64p, _f64p], ctypes.c_int),
+    "mgm_export_weights": ([_vp, _f64p, _i64p], ctypes.c_int),
+    "mgm_apply": ([_vp, ctypes.c_int, ctypes.c_int, _vp, _vp, _vp, _vp], ctypes.c_int),
+    "mgm_timing_enable": ([_vp, ctypes.c_int, ctypes.c_int], ctypes.c_int),
+    "mgm_timing_read": ([_vp, ctypes.c_int, _f64p, _i64p, _f64p], ctypes.c_int),
+    "mgm_bytes_model": ([_vp, _f64p, _f64p], ctypes.c_int),
+    "mgm_vcycle_kernel_count": ([_vp, _i64p], ctypes.c_int),
+    "mgm_host_morton": ([_f64p, _i64, _i64p], ctypes.c_int),
+    "mgm_host_knn": ([_f64p, _i64, _f64p, _i64, ctypes.c_int, _i32p], ctypes.c_int),
+    "mgm_host_wse": ([_f64p, _i64, _i64, _i64p], ctypes.c_int),
+    "mgm_host_colouring": ([_i64, _i64p, _i32p, _i32p, ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
+}
+EXPORTED = tuple(_SIGS)
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libmgm.so (raises OSError/RuntimeError if it is missing -- no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(path):
+            raise RuntimeError(f"libmgm.so not built ({path}); run __graft_entry__.build()")
+        lib = ctypes.CDLL(path)
+        for name, (args, res) in _SIGS.items():
+            fn = getattr(lib, name)
+            fn.argtypes = args
+            fn.restype = res
+        _lib = lib
+    return _lib
+
+
+class MGMError(RuntimeError):
+    def __init__(self, status, msg, index):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg} (index {index})")
+        self.status, self.index = status, index
+
+
+def _ptr(a, t):
+    return a.ctypes.data_as(t)
+
+
+def _check(status, ctx=None):
+    if status != MGM_OK:
+        idx = _i64(-1)
+        msg = load_library().mgm_last_error(ctx, ctypes.byref(idx))
+        raise MGMError(status, (msg or b"").decode(), idx.value)
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+# ---------------------------------------------------------------- ABI-named functions
+def mgm_setup(points: np.ndarray, normals: np.ndarray, stencil: dict, levels: dict, stream=None):
+    """Returns an opaque ctx handle (c_void_p).  Raises MGMError on failure."""
+    lib = load_library()
+    pts = np.ascontiguousarray(points, dtype=np.float64)
+    nrm = np.ascontiguousarray(normals, dtype=np.float64)
+    sp = StencilParams(method=stencil.get("method", 0), poly_degree=stencil.get("poly_degree", 2),
+                       phs_k=stencil.get("phs_k", 1), stencil_n=stencil.get("stencil_n", 15),
+                       gfd_alpha=stencil.get("gfd_alpha", 4.0), problem=stencil.get("problem", 0),
+                       mu=stencil.get("mu", 1.0))
+    lp = LevelParams(num_levels=levels.get("num_levels", 0), n_min=levels.get("n_min", 250),
+                     coarsen_factor=levels.get("coarsen_factor", 4),
+                     interp_m=levels.get("interp_m", 6), nu1=levels.get("nu1", 1),
+                     nu2=levels.get("nu2", 1), smoother=levels.get("smoother", 0),
+                     restart=levels.get("restart", 50))
+    ctx = _vp()
+    st = lib.mgm_setup(_ptr(pts, _f64p), _ptr(nrm, _f64p), len(pts), ctypes.byref(sp),
+                       ctypes.byref(lp), _vp(_stream_ptr(stream) if stream is not None else 0),
+                       ctypes.byref(ctx))
+    if st != MGM_OK:
+        idx = _i64(-1)
+        msg = lib.mgm_last_error(None, ctypes.byref(idx)).decode()
+        if ctx.value:
+            lib.mgm_destroy(ctx)
+        raise MGMError(st, msg, idx.value)
+    return ctx
+
+
+def mgm_destroy(ctx):
+    load_library().mgm_destroy(ctx)
+
+
+def mgm_vcycle(ctx, f, u, stream=None):
+    _check(load_library().mgm_vcycle(ctx, _vp(f.data_ptr()), _vp(u.data_ptr()),
+                                     _vp(_stream_ptr(stream))), ctx)
+
+
+@dataclass
+class SolveReport:
+    iterations: int
+    converged: bool
+    final_rel_residual: float
+    history: list
+    lam: float
+    setup_ms: float
+    solve_ms: float
+
+
+def _report(rep, hist):
+    n = min(rep.iterations, len(hist))
+    return SolveReport(rep.iterations, bool(rep.converged), rep.final_rel_residual,
+                       list(hist[:n]), rep.lambda_, rep.setup_ms, rep.solve_ms)
+
+
+def mgm_solve(ctx, rhs, x, tol=1e-10, maxit=500, krylov=1, stream=None, history_cap=1024):
+    hist = np.zeros(history_cap)
+    rep = Report(history=_ptr(hist, _f64p), history_cap=history_cap)
+    _check(load_library().mgm_solve(ctx, _vp(rhs.data_ptr()), _vp(x.data_ptr()), tol, maxit, krylov,
+                                    ctypes.byref(rep), _vp(_stream_ptr(stream))), ctx)
+    return _report(rep, hist)
+
+
+def mgm_solve_host(ctx, rhs: np.ndarray, x: np.ndarray, tol=1e-10, maxit=500, krylov=1,
+                   stream=None, history_cap=1024):
+    """rhs / x: host arrays (numpy, or pinned torch CPU tensors via .numpy())."""
+    hist = np.zeros(history_cap)
+    rep = Report(history=_ptr(hist, _f64p), history_cap=history_cap)
+    assert rhs.dtype == np.float64 and x.dtype == np.float64 and x.flags.c_contiguous
+    _check(load_library().mgm_solve_host(ctx, _vp(rhs.ctypes.data), _vp(x.ctypes.data), tol, maxit,
+                                         krylov, ctypes.byref(rep), _vp(_stream_ptr(stream))), ctx)
+    return _report(rep, hist)
+
+
+def mgm_num_levels(ctx) -> int:
+    p = ctypes.c_int(0)
+    _check(load_library().mgm_num_levels(ctx, ctypes.byref(p)), ctx)
+    return p.value
+
+
+def mgm_level_info(ctx, level: int) -> dict:
+    n, z, q, b = _i64(), _i64(), _i64(), _i64()
+    c = ctypes.c_int()
+    _check(load_library().mgm_level_info(ctx, level, ctypes.byref(n), ctypes.byref(z),
+                                         ctypes.byref(q), ctypes.byref(c), ctypes.byref(b)), ctx)
+    return dict(n=n.value, nnz=z.value, nnz_P=q.value, colours=c.value, stored_bytes=b.value)
+
+
+def mgm_export_level(ctx, level: int, poisson: bool = False) -> dict:
+    info = mgm_level_info(ctx, level)
+    n, z, q = info["n"], info["nnz"], info["nnz_P"]
+    ids = np.empty(n, dtype=np.int64)
+    Lp = np.empty(n + 1, dtype=np.int64)
+    Lc = np.empty(z, dtype=np.int32)
+    Lv = np.empty(z)
+    col = np.empty(n, dtype=np.int32)
+    Pp = np.empty(n + 1, dtype=np.int64)
+    Pc = np.empty(max(q, 1), dtype=np.int32)
+    Pv = np.empty(max(q, 1))
+    bd = np.empty(n) if poisson else None
+    _check(load_library().mgm_export_level(
+        ctx, level, _ptr(ids, _i64p), _ptr(Lp, _i64p), _ptr(Lc, _i32p), _ptr(Lv, _f64p),
+        _ptr(col, _i32p), _ptr(Pp, _i64p), _ptr(Pc, _i32p), _ptr(Pv, _f64p),
+        _ptr(bd, _f64p) if poisson else None), ctx)
+    out = dict(info, ids=ids, L_ptr=Lp, L_col=Lc, L_val=Lv, colour=col, border=bd)
+    if q:
+        out.update(P_ptr=Pp, P_col=Pc[:q], P_val=Pv[:q])
+    return out
+
+
+def mgm_export_weights(ctx, n_points: int, stencil_n: int):
+    w = np.empty(n_points * stencil_n)
+    s = np.empty(n_points * stencil_n, dtype=np.int64)
+    _check(load_library().mgm_export_weights(ctx, _ptr(w, _f64p), _ptr(s, _i64p)), ctx)
+    return w.reshape(n_points, stencil_n), s.reshape(n_points, stencil_n)
+
+
+def mgm_apply(ctx, level: int, op: int, x, f=None, y=None, stream=None):
+    _check(load_library().mgm_apply(ctx, level, op, _vp(x.data_ptr()),
+                                    _vp(f.data_ptr()) if f is not None else None,
+                                    _vp(y.data_ptr()), _vp(_stream_ptr(stream))), ctx)
+    return y
+
+
+def mgm_timing_enable(ctx, cls: int, enable: bool = True):
+    _check(load_library().mgm_timing_enable(ctx, cls, 1 if enable else 0), ctx)
+
+
+def mgm_timing_read(ctx, cls: int):
+    t, n, b = ctypes.c_double(), _i64(), ctypes.c_double()
+    _check(load_library().mgm_timing_read(ctx, cls, ctypes.byref(t), ctypes.byref(n),
+                                          ctypes.byref(b)), ctx)
+    return dict(total_ms=t.value, launches=n.value, alg_bytes=b.value)
+
+
+def mgm_bytes_model(ctx):
+    v, s = ctypes.c_double(), ctypes.c_double()
+    _check(load_library().mgm_bytes_model(ctx, ctypes.byref(v), ctypes.byref(s)), ctx)
+    return dict(vcycle_bytes=v.value, spmv_bytes=s.value)
+
+
+def mgm_vcycle_kernel_count(ctx) -> int:
+    c = _i64()
+    _check(load_library().mgm_vcycle_kernel_count(ctx, ctypes.byref(c)), ctx)
+    return c.value
+
+
+def mgm_host_morton(points):
+    pts = np.ascontiguousarray(points, dtype=np.float64)
+    perm = np.empty(len(pts), dtype=np.int64)
+    _check(load_library().mgm_host_morton(_ptr(pts, _f64p), len(pts), _ptr(perm, _i64p)))
+    return perm
+
+
+def mgm_host_knn(points, queries, k):
+    pts = np.ascontiguousarray(points, dtype=np.float64)
+    q = np.ascontiguousarray(queries, dtype=np.float64)
+    out = np.empty((len(q), k), dtype=np.int32)
+    _check(load_library().mgm_host_knn(_ptr(pts, _f64p), len(pts), _ptr(q, _f64p), len(q), k,
+                                       _ptr(out, _i32p)))
+    return out
+
+
+def mgm_host_wse(points, nt):
+    pts = np.ascontiguousarray(points, dtype=np.float64)
+    keep = np.empty(nt, dtype=np.int64)
+    _check(load_library().mgm_host_wse(_ptr(pts, _f64p), len(pts), nt, _ptr(keep, _i64p)))
+    return keep
+
+
+def mgm_host_colouring(ptr, col):
+    ptr = np.ascontiguousarray(ptr, dtype=np.int64)
+    col = np.ascontiguousarray(col, dtype=np.int32)
+    n = len(ptr) - 1
+    c = np.empty(n, dtype=np.int32)
+    nc = ctypes.c_int()
+    _check(load_library().mgm_host_colouring(n, _ptr(ptr, _i64p), _ptr(col, _i32p), _ptr(c, _i32p),
+                                             ctypes.byref(nc)))
+    return c, nc.value
+
+
+# ---------------------------------------------------------------- convenience wrapper
+class MGM:
+    """Owns one libmgm context.  Vectors are torch CUDA float64 tensors in original order."""
+
+    def __init__(self, points, normals, stencil: dict, levels: dict):
+        import torch
+
+        if not torch.cuda.is_available():
+            raise RuntimeError("libmgm needs a CUDA device")
+        self.n = len(points)
+        self.stencil, self.levels = dict(stencil), dict(levels)
+        self.ctx = mgm_setup(points, normals, stencil, levels)
+        self.p = mgm_num_levels(self.ctx)
+
+    def close(self):
+        if getattr(self, "ctx", None) is not None:
+            mgm_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def vcycle(self, f, u, stream=None):
+        mgm_vcycle(self.ctx, f, u, stream)
+        return u
+
+    def solve(self, rhs, x=None, tol=1e-10, maxit=500, krylov=1, stream=None):
+        import torch
+
+        if x is None:
+            x = torch.empty_like(rhs)
+        rep = mgm_solve(self.ctx, rhs, x, tol, maxit, krylov, stream)
+        return x, rep
+
+    def level_info(self):
+        return [mgm_level_info(self.ctx, j) for j in range(self.p)]

@@ -1,0 +1,214 @@
+"""GPU (libmgm through the C ABI) vs oracle parity on the same seeded inputs.
+
+Tolerances (BASELINE.json north_star): discrete structures exact; per-operator outputs
+(SpMV, one sweep, residual, restriction, interpolation, coarse solve, one V-cycle) to
+relative max-norm 1e-12; GMRES iteration counts within +-1; solutions to relative 1e-9
+when both solve to 1e-10.  Setup floats (weights, transfers, Galerkin values) are held to
+1e-12 relative -- the setup kernels are written to reproduce the oracle's operation order
+(DESIGN.md "operation order"), so in practice they agree bit for bit."""
+import numpy as np
+import pytest
+
+import mgm_inputs as MI
+from _parity import Pair, coo_ids, relmax
+
+pytestmark = pytest.mark.gpu
+
+CASES = {
+    "cfg1": lambda: MI.make_workload(1),                              # sphere N=4096, 4 levels
+    "torus20000": lambda: MI.make_workload(3, n=20000),               # ragged sizes, ell=3 n=30
+    "gfd9000": lambda: MI.make_workload(2, n=9000, method="gfd"),     # GFD, nu=2/2
+    "poisson6000": lambda: MI.make_workload(4, n=6000),               # bordered Poisson, n=50
+}
+_cache = {}
+
+
+def pair(name):
+    if name not in _cache:
+        _cache[name] = Pair(CASES[name]())
+    return _cache[name]
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cleanup():
+    yield
+    for p in _cache.values():
+        p.close()
+    _cache.clear()
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_structures_exact(name):
+    P = pair(name)
+    assert P.gpu.p == P.ref.p
+    for j in range(P.ref.p):
+        g, o = P.glv[j], P.ref.levels[j]
+        assert g["n"] == o.N
+        assert np.array_equal(np.sort(g["ids"]), np.sort(o.ids))          # WSE subsets
+        pos = P.oracle_pos(j)
+        if j + 1 < P.ref.p:
+            assert np.array_equal(g["colour"], o.colour[pos[g["ids"]]])   # greedy colouring
+        gr, gc, gv = coo_ids(g["L_ptr"], g["L_col"], g["L_val"], g["ids"], g["ids"])
+        orr, oc, ov = coo_ids(o.L.ptr, o.L.idx, o.L.val, o.ids, o.ids)
+        assert np.array_equal(gr, orr) and np.array_equal(gc, oc)         # Galerkin pattern
+        assert relmax(gv, ov) <= 1e-12
+        if j + 1 < P.ref.p:
+            nx = P.glv[j + 1]
+            gr, gc, gv = coo_ids(g["P_ptr"], g["P_col"], g["P_val"], g["ids"], nx["ids"])
+            orr, oc, ov = coo_ids(o.P.ptr, o.P.idx, o.P.val, o.ids, P.ref.levels[j + 1].ids)
+            assert np.array_equal(gr, orr) and np.array_equal(gc, oc)
+            assert relmax(gv, ov) <= 1e-13
+        if P.poisson:
+            assert relmax(g["border"], o.c[pos[g["ids"]]]) <= 1e-13
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_fine_weights(name):
+    from paper_2204_06154_b200 import mgm_export_weights
+
+    P = pair(name)
+    n, ns = len(P.w.points), P.w.stencil["stencil_n"]
+    wg, sg = mgm_export_weights(P.gpu.ctx, n, ns)
+    so = P.ref.perm[P.ref.stencil]                     # oracle stencils in original ids
+    wo = np.empty_like(P.ref.weights)
+    wo[P.ref.perm] = P.ref.weights
+    st = np.empty_like(so)
+    st[P.ref.perm] = so
+    assert np.array_equal(sg, st)                      # kNN lists (O2), exact
+    rowscale = np.abs(wo).max(1, keepdims=True)
+    assert (np.abs(wg - wo) / rowscale).max() <= 1e-10
+
+
+def _rand(n, seed):
+    return np.random.default_rng(seed).uniform(-1.0, 1.0, n)
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_per_operator(name):
+    import torch
+    from paper_2204_06154_b200 import mgm_apply, mgm_level_info
+    import oracle as O
+
+    P = pair(name)
+    pad = 1 if P.poisson else 0
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    for j in range(P.ref.p):
+        o = P.ref.levels[j]
+        n = o.N
+        x = _rand(n + pad, 10 + j)
+        f = _rand(n + pad, 20 + j)
+        xl, fl = P.to_lib_order(j, x), P.to_lib_order(j, f)
+        # SpMV
+        y = torch.empty(n + pad, dtype=torch.float64, device="cuda")
+        mgm_apply(P.gpu.ctx, j, 0, dev(xl), None, y)
+        ref = P.ref._apply_level(j, x)
+        assert relmax(P.to_oracle_order(j, y.cpu().numpy()), ref) <= 1e-12, ("spmv", j)
+        # residual
+        mgm_apply(P.gpu.ctx, j, 2, dev(xl), dev(fl), y)
+        ref = P.ref._residual(o, f, x)
+        assert relmax(P.to_oracle_order(j, y.cpu().numpy()), ref) <= 1e-12, ("residual", j)
+        if j + 1 == P.ref.p:
+            continue
+        # one forward sweep
+        mgm_apply(P.gpu.ctx, j, 1, dev(xl), dev(fl), y)
+        u = x.copy()
+        P.ref._smooth(o, f, u, 1, False)
+        assert relmax(P.to_oracle_order(j, y.cpu().numpy()), u) <= 1e-12, ("sweep", j)
+        # restriction
+        nn = P.ref.levels[j + 1].N
+        yr = torch.empty(nn + pad, dtype=torch.float64, device="cuda")
+        mgm_apply(P.gpu.ctx, j, 3, dev(xl), None, yr)
+        ref = P.ref._restrict(o, x)
+        assert relmax(P.to_oracle_order(j + 1, yr.cpu().numpy()), ref) <= 1e-12, ("restrict", j)
+        # interpolation
+        xc = _rand(nn + pad, 30 + j)
+        mgm_apply(P.gpu.ctx, j, 4, dev(P.to_lib_order(j + 1, xc)), None, y)
+        ref = P.ref._interp(o, xc)
+        assert relmax(P.to_oracle_order(j, y.cpu().numpy()), ref) <= 1e-12, ("interp", j)
+    # coarse solve
+    jp = P.ref.p - 1
+    npd = P.ref.levels[jp].N + pad
+    r = _rand(npd, 99)
+    y = torch.empty(npd, dtype=torch.float64, device="cuda")
+    mgm_apply(P.gpu.ctx, jp, 5, dev(P.to_lib_order(jp, r)), None, y)
+    assert relmax(P.to_oracle_order(jp, y.cpu().numpy()), P.ref.coarse_solve(r)) <= 1e-12
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_vcycle(name):
+    import torch
+
+    P = pair(name)
+    n = len(P.w.points)
+    f = _rand(n, 1)
+    u0 = _rand(n, 2)
+    uf = torch.from_numpy(u0.copy()).cuda()
+    P.gpu.vcycle(torch.from_numpy(f).cuda(), uf)
+    ref = P.ref.vcycle(f, u0)
+    assert relmax(uf.cpu().numpy(), ref) <= 1e-12
+    # zero guess (the preconditioner M(r))
+    uz = torch.zeros(n, dtype=torch.float64, device="cuda")
+    P.gpu.vcycle(torch.from_numpy(f).cuda(), uz)
+    assert relmax(uz.cpu().numpy(), P.ref.vcycle(f, np.zeros(n))) <= 1e-12
+
+
+@pytest.mark.parametrize("name", list(CASES))
+@pytest.mark.parametrize("krylov", [1, 0])
+def test_solve(name, krylov):
+    import torch
+
+    P = pair(name)
+    if krylov == 0 and name == "gfd9000":
+        pytest.skip("standalone MGM is slow on GFD ell=2 (P:411); covered by GMRES")
+    rhs = P.w.rhs
+    x, rep = P.gpu.solve(torch.from_numpy(rhs).cuda(), tol=1e-10, krylov=krylov, maxit=300)
+    xr, rr = P.ref.solve(rhs, tol=1e-10, krylov=krylov, maxit=300)
+    assert rep.converged and rr.converged
+    assert rep.final_rel_residual <= 1e-10
+    assert abs(rep.iterations - rr.iterations) <= 1, (rep.iterations, rr.iterations)
+    xg = x.cpu().numpy()
+    assert np.linalg.norm(xg - xr) / np.linalg.norm(xr) <= 1e-9
+    if P.poisson:
+        assert abs(rep.lam - rr.lam) <= 1e-8 * max(1.0, abs(rr.lam))
+        assert abs(xg.sum()) <= 1e-8 * len(xg)
+
+
+def test_zero_rhs_and_host_path():
+    import torch
+    from paper_2204_06154_b200 import mgm_solve_host
+
+    P = pair("cfg1")
+    n = len(P.w.points)
+    x, rep = P.gpu.solve(torch.zeros(n, dtype=torch.float64, device="cuda"))
+    assert rep.iterations == 0 and rep.converged and not x.cpu().numpy().any()
+    xh = np.empty(n)
+    rep = mgm_solve_host(P.gpu.ctx, np.ascontiguousarray(P.w.rhs), xh, tol=1e-10)
+    xd, rep2 = P.gpu.solve(torch.from_numpy(P.w.rhs).cuda(), tol=1e-10)
+    assert rep.iterations == rep2.iterations
+    assert np.array_equal(xh, xd.cpu().numpy())          # deterministic, same path
+
+
+def test_determinism():
+    import torch
+
+    P = pair("torus20000")
+    rhs = torch.from_numpy(P.w.rhs).cuda()
+    x1, r1 = P.gpu.solve(rhs, tol=1e-10)
+    x2, r2 = P.gpu.solve(rhs, tol=1e-10)
+    assert r1.history == r2.history
+    assert torch.equal(x1, x2)
+
+
+def test_error_paths():
+    from paper_2204_06154_b200 import MGM, MGMError
+
+    w = MI.make_workload(1, n=600)
+    pts = w.points.copy()
+    pts[10] = pts[3]                                       # duplicate point
+    with pytest.raises(MGMError) as e:
+        MGM(pts, w.normals, w.stencil, w.levels)
+    assert e.value.status == 8 and e.value.index in (3, 10)
+    with pytest.raises(MGMError):
+        MGM(w.points, w.normals, dict(w.stencil, stencil_n=0), w.levels)
+    with pytest.raises(MGMError):
+        MGM(w.points, w.normals, w.stencil, dict(w.levels, num_levels=9))
