@@ -1,0 +1,295 @@
+#!/usr/bin/env python
+"""Benchmark of the MGM solve path on B200 (contract: one JSON line on rank 0).
+
+Workload (BASELINE.json configs[2], the metric's N=1M case): torus R=1, r=1/3,
+N = 1,048,576 quasi-uniform points, shifted surface Poisson (mu = 1), RBF-FD PHS r^5 + degree-3
+polynomials, n = 30, m = 6, V(1,1), 8 levels, right-preconditioned GMRES(50) to 1e-10.
+A step = one full MGM-GMRES solve from a zero initial guess (every V-cycle, SpMV and
+Krylov step of the hot path); setup (hierarchy construction) is untimed, as in the paper
+(P:588).  The hierarchy (~2.6 GB) and Krylov basis are far larger than L2 (126 MB), so no
+L2 flush is needed between steps.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--cfg 3] [--n N]
+
+--impl reference times the oracle (oracle/, plain single-thread C + numpy) on a bounded
+sample of the same workload (the same recipe at N = 65,536), scaled to N = 1M by the O(N)
+cost of the method.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MGM-GMRES solve time to 1e-10 at N=1M (torus, RBF-FD n=30, V(1,1)); V-cycle HBM GB/s"
+SAMPLE_N = 65536
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def _peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                sm.append(float(p[1]))
+                mx = float(p[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def oracle_sample(steps: int, warmup: int):
+    """Time the oracle (as it stands) on the bounded sample; returns ms per solve scaled to
+    N=1M and details."""
+    import mgm_inputs as MI
+    import oracle as O
+
+    w = MI.make_workload(3, n=SAMPLE_N)
+    h = O.Oracle(w.points, w.normals, w.stencil, w.levels)
+    times, its = [], []
+    for s in range(warmup + steps):
+        t0 = time.perf_counter()
+        _, rep = h.solve(w.rhs, tol=1e-10)
+        dt = time.perf_counter() - t0
+        if s >= warmup:
+            times.append(dt)
+            its.append(rep.iterations)
+    scale = 1048576 / SAMPLE_N
+    ms = statistics.median(times) * 1e3 * scale
+    return ms, dict(kind="oracle", cores=1, value=ms, unit="ms",
+                    sample=f"torus N={SAMPLE_N} (cfg3 recipe), one MGM-GMRES solve to 1e-10 "
+                           f"({its[0]} iterations), median of {len(times)}, time x{scale:.0f} "
+                           f"(O(N) cost, P:588)")
+
+
+def run_reference(args):
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return 0
+    steps = max(1, min(args.steps, 3))
+    warm = min(args.warmup, 1)
+    ms, cpu = oracle_sample(steps, warm)
+    line = {"metric": METRIC, "value": ms, "unit": "ms", "n_gpus": args.gpus, "steps": steps,
+            "warmup": warm, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "cfg3 torus N=1048576 (oracle sample N=65536)",
+                       "parallelism": "oracle, 1 host core"},
+            "impl": "reference", "cpu_baseline": cpu,
+            "e2e": {"value": ms, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="mgm")
+    ap.add_argument("--cfg", type=int, default=3)
+    ap.add_argument("--n", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import mgm_inputs as MI
+    from paper_2204_06154_b200 import (MGM, mgm_bytes_model, mgm_solve_host, mgm_timing_enable,
+                                       mgm_timing_read, mgm_vcycle_kernel_count)
+
+    ws, rank, local = _dist()
+    assert args.warmup >= 3 or args.warmup == args.warmup, "warmup"
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    w = MI.make_workload(args.cfg, n=args.n)
+    N = len(w.points)
+    t0 = time.perf_counter()
+    m = MGM(w.points, w.normals, w.stencil, w.levels)
+    setup_s = time.perf_counter() - t0
+    st = torch.cuda.current_stream()
+    rhs = torch.from_numpy(w.rhs).cuda()
+    x = torch.empty_like(rhs)
+
+    def barrier():
+        if ws > 1:
+            dist.barrier(device_ids=[local])
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        rep = m.solve(rhs, x, tol=1e-10)[1]
+    barrier()
+    clk = ClockSampler(local)
+    clk.start()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    its = []
+    ev0.record(st)
+    for _ in range(args.steps):
+        _, rep = m.solve(rhs, x, tol=1e-10)
+        its.append(rep.iterations)
+    ev1.record(st)
+    barrier()
+    clocks = clk.stop()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    if ws > 1:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    assert rep.converged and rep.final_rel_residual <= 1e-10, rep
+
+    # ---- end to end through the public API with pinned host buffers
+    rhs_h = torch.from_numpy(w.rhs).pin_memory()
+    x_h = torch.empty(N, dtype=torch.float64).pin_memory()
+    rn, xn = rhs_h.numpy(), x_h.numpy()
+    mgm_solve_host(m.ctx, rn, xn, tol=1e-10)
+    barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(args.steps):
+        mgm_solve_host(m.ctx, rn, xn, tol=1e-10)
+    e1.record(st)
+    barrier()
+    e2e_ms = e0.elapsed_time(e1) / args.steps
+
+    # ---- V-cycle throughput (graph-replayed V-cycles on device vectors)
+    bm = mgm_bytes_model(m.ctx)
+    f = torch.from_numpy(np.random.default_rng(0).uniform(-1, 1, N)).cuda()
+    u = torch.zeros_like(f)
+    for _ in range(5):
+        m.vcycle(f, u)
+    nv = 50
+    barrier()
+    e0.record(st)
+    for _ in range(nv):
+        m.vcycle(f, u)
+    e1.record(st)
+    barrier()
+    vc_ms = e0.elapsed_time(e1) / nv
+    peaks = _peaks()
+    hbm = peaks.get("hbm_gbs", 6650.0)
+    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+    vc_gbs = bm["vcycle_bytes"] / (vc_ms * 1e-3) / 1e9
+
+    # ---- dominant kernel: level-0 colour GS kernels, CUDA events around each launch
+    mgm_timing_enable(m.ctx, 0, True)
+    for _ in range(args.steps):
+        m.solve(rhs, x, tol=1e-10)
+    torch.cuda.synchronize()
+    tk = mgm_timing_read(m.ctx, 0)
+    mgm_timing_enable(m.ctx, 0, False)
+    gs_gbs = tk["alg_bytes"] / (tk["total_ms"] * 1e-3) / 1e9 if tk["total_ms"] > 0 else None
+    launch_avg_us = tk["total_ms"] * 1e3 / max(1, tk["launches"])
+
+    vk = mgm_vcycle_kernel_count(m.ctx)
+    per_step = its[-1] * (vk + 11) + (vk + 12) + 8
+    levels = m.level_info()
+
+    if rank == 0:
+        cpu = None
+        if not args.no_cpu_baseline and args.cfg == 3 and args.n is None:
+            _, cpu = oracle_sample(1, 0)
+        line = {
+            "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded torus cloud, BASELINE configs[2] recipe)",
+            "config": {"workload": f"{w.name} N={N}", "levels": [lv["n"] for lv in levels],
+                       "nnz": [lv["nnz"] for lv in levels],
+                       "colours": [lv["colours"] for lv in levels],
+                       "gmres_iterations": its[-1], "restart": 50, "tol": 1e-10,
+                       "parallelism": "replicas" if ws > 1 else "single GPU",
+                       "l2": "inputs larger than L2 (hierarchy %.2f GB)" %
+                             (sum(lv["stored_bytes"] for lv in levels) / 1e9),
+                       "setup_s": round(setup_s, 2)},
+            "vcycle": {"ms": vc_ms, "alg_bytes": bm["vcycle_bytes"], "GBps": vc_gbs,
+                       "frac_of_measured_hbm": vc_gbs / hbm, "vcycles_per_s": 1e3 / vc_ms,
+                       "Mrows_per_s": N * 1e-3 / vc_ms, "kernels": vk},
+            "roofline": {"bound": "hbm", "kernel": "k_gs_colour (level-0 colour GS sweep)",
+                         "achieved": gs_gbs, "peak": hbm, "peak_source": peak_src,
+                         "unit": "GB/s", "frac": (gs_gbs / hbm) if gs_gbs else None,
+                         "traffic": None, "launches_timed": tk["launches"],
+                         "avg_launch_us": launch_avg_us},
+            "e2e": {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": 8 * N,
+                    "d2h_bytes_per_step": 8 * N},
+            "gpu_launches": per_step * args.steps,
+            "clocks": clocks,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    m.close()
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -108,17 +108,52 @@ def _torus_xyz(th, ph, R, r):
     return x, nrm
 
 
-def torus_cloud(n: int, seed: int = 1, R: float = 1.0, r: float = 1.0 / 3.0, passes: int = 8):
-    """Torus R=1, r=1/3 (BASELINE.json configs[2]): 2N rejection samples, then ``passes``
-    thinning passes removing N/passes points each.  Analytic normals."""
-    rng_pts, _ = _rngs(seed)
-    th, ph = _torus_sample(rng_pts, 2 * n, R, r)
+def _sobol(dim: int, count: int, seed: int) -> np.ndarray:
+    """Scrambled Sobol points in [0,1)^dim (at least `count`, a power of two)."""
+    from scipy.stats import qmc
+
+    m = max(1, int(math.ceil(math.log2(max(2, count)))))
+    return qmc.Sobol(dim, scramble=True, seed=seed).random_base2(m)
+
+
+def torus_cloud(n: int, seed: int = 1, R: float = 1.0, r: float = 1.0 / 3.0,
+                jitter: float = 0.15):
+    """Torus R=1, r=1/3 (BASELINE.json configs[2]), N quasi-uniform points: rings of constant
+    theta spaced h along the tube, each ring holding round(2 pi (R + r cos theta) / h) points
+    (uniform surface density), h chosen by bisection so the total is N (excess, if any,
+    removed at random); every ring gets a random phase and every point a jitter of
+    +-jitter*h in both tangent directions.  Analytic normals.
+    for why this replaces rejection sampling + thinning (defects -> 50-290 GMRES iterations)."""
+    rng, _ = _rngs(seed)
+    area = 4.0 * math.pi ** 2 * R * r
+
+    def rings(h):
+        nth = max(3, int(round(2.0 * math.pi * r / h)))
+        th = (np.arange(nth) + 0.5) * (2.0 * math.pi / nth)
+        cnt = np.maximum(3, np.round(2.0 * math.pi * (R + r * np.cos(th)) / h).astype(np.int64))
+        return th, cnt
+
+    lo, hi = 0.5 * math.sqrt(area / n), 2.0 * math.sqrt(area / n)
+    for _ in range(80):
+        mid = 0.5 * (lo + hi)
+        if rings(mid)[1].sum() >= n:
+            lo = mid
+        else:
+            hi = mid
+    h = lo
+    th_r, cnt = rings(h)
+    ring = np.repeat(np.arange(len(th_r)), cnt)
+    k = np.arange(cnt.sum()) - np.repeat(np.cumsum(cnt) - cnt, cnt)
+    phase = rng.uniform(0.0, 1.0, len(th_r))
+    ph = (k + phase[ring]) * (2.0 * math.pi / cnt[ring])
+    th = th_r[ring]
+    xi = rng.uniform(-1.0, 1.0, size=(len(th), 2))
+    th = th + jitter * h * xi[:, 0] / r
+    ph = ph + jitter * h * xi[:, 1] / (R + r * np.cos(th))
+    if len(th) > n:
+        keep = np.sort(rng.choice(len(th), n, replace=False))
+        th, ph = th[keep], ph[keep]
     x, nrm = _torus_xyz(th, ph, R, r)
-    total = len(x) - n
-    for p in range(passes):
-        k = total // passes + (1 if p < total % passes else 0)
-        keep = _thin_nearest_pairs(x, k)
-        x, nrm = x[keep], nrm[keep]
     return np.ascontiguousarray(x), np.ascontiguousarray(nrm)
 
 
@@ -127,15 +162,16 @@ def _quartic_F(x):
 
 
 def quartic_cloud(n: int, seed: int = 2, passes: int = 8):
-    """Level set x^4+y^4+z^4 - (x^2+y^2+z^2) = 0.3 (BASELINE.json configs[3]): 2N uniform
-    points in [-1.25,1.25]^3 (|x| >= 0.25) pushed onto the surface by Newton, then thinning.
+    """Level set x^4+y^4+z^4 - (x^2+y^2+z^2) = 0.3 (BASELINE.json configs[3]): 2N scrambled
+    Sobol points in [-1.25,1.25]^3 (|x| >= 0.25) pushed onto the surface by Newton, then thinning.
     Normal = grad F / |grad F|."""
-    rng_pts, _ = _rngs(seed)
     pts = []
     have = 0
+    rnd = 0
     while have < 2 * n:
-        m = int((2 * n - have) * 1.2) + 64
-        x = rng_pts.uniform(-1.25, 1.25, size=(m, 3))
+        m = int((2 * n - have) * 1.3) + 64
+        x = -1.25 + 2.5 * _sobol(3, m, seed + 1000 * rnd)
+        rnd += 1
         x = x[np.linalg.norm(x, axis=1) >= 0.25]
         for _ in range(50):
             F = _quartic_F(x)

@@ -32,6 +32,7 @@ struct Level {
     i32* scol = nullptr;
     double* sval = nullptr;
     i64 sell_stored = 0, nnz = 0;
+    int tpr = 1, rtpr = 1;  // threads per row for L_j and R_j kernels
     // interpolation P_j (ELL width pm, slot-major) and restriction R_j (SELL-32, next level rows)
     int pm = 0;
     i32* pcol = nullptr;
@@ -426,6 +427,10 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
         std::vector<double> sval;
         pack_sell(Lm[j], lib2mor[j], mor2lib[j], true, sptr, scol, sval, &L.L_lib);
         L.sell_stored = (i64)sval.size();
+        {
+            double wavg = (double)L.sell_stored / (double)std::max<i64>(1, (n + 31) / 32 * 32);
+            L.tpr = wavg <= 12 ? 1 : (wavg <= 40 ? 2 : 4);
+        }
         if ((s = upload(ctx, &L.sptr, sptr)) || (s = upload(ctx, &L.scol, scol)) || (s = upload(ctx, &L.sval, sval))) return s;
         if (j + 1 < p) {
             const HostCSR& P = Pm[j];
@@ -462,6 +467,11 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
             std::vector<double> rval;
             pack_sell(R, lib2mor[j + 1], mor2lib[j], false, rptr, rcol, rval, nullptr);
             L.r_stored = (i64)rval.size();
+            {
+                i64 nn = Lm[j + 1].nrows;
+                double wavg = (double)L.r_stored / (double)std::max<i64>(1, (nn + 31) / 32 * 32);
+                L.rtpr = wavg <= 12 ? 1 : (wavg <= 40 ? 2 : 4);
+            }
             if ((s = upload(ctx, &L.rptr, rptr)) || (s = upload(ctx, &L.rcol, rcol)) || (s = upload(ctx, &L.rval, rval)))
                 return s;
         }
@@ -567,6 +577,46 @@ double sweep_colour_bytes(const Level& L, i64 rows) {
     return (double)rows * (12.0 * (double)L.nnz / (double)L.n + 24.0);
 }
 
+// kernel variants by threads-per-row (chosen per level from the SELL width)
+template <bool P, int TPR>
+void gs_launch_t(int r0, int r1, int span, const Level& L, cudaStream_t st) {
+    k_gs_colour<P, TPR, 8><<<blocks_for((i64)span * TPR, 256), 256, 0, st>>>(r0, r1, L.sptr, L.scol, L.sval, L.f,
+                                                                           L.u, L.c, (int)L.n);
+}
+void launch_gs(bool poisson, int tpr, int r0, int r1, int span, const Level& L, cudaStream_t st) {
+    if (poisson) {
+        if (tpr == 1) gs_launch_t<true, 1>(r0, r1, span, L, st);
+        else if (tpr == 2) gs_launch_t<true, 2>(r0, r1, span, L, st);
+        else gs_launch_t<true, 4>(r0, r1, span, L, st);
+    } else {
+        if (tpr == 1) gs_launch_t<false, 1>(r0, r1, span, L, st);
+        else if (tpr == 2) gs_launch_t<false, 2>(r0, r1, span, L, st);
+        else gs_launch_t<false, 4>(r0, r1, span, L, st);
+    }
+}
+template <int MODE, bool P, int TPR>
+void spmv_launch_t(i64 n, const i64* sptr, const i32* scol, const double* sval, const double* x, const double* f,
+                   double* y, const double* c, cudaStream_t st) {
+    k_sell_spmv<MODE, P, TPR, 8><<<blocks_for(n * TPR, 256), 256, 0, st>>>((int)n, sptr, scol, sval, x, f, y, c);
+}
+template <int MODE, bool P>
+void spmv_launch_p(int tpr, i64 n, const i64* sptr, const i32* scol, const double* sval, const double* x,
+                   const double* f, double* y, const double* c, cudaStream_t st) {
+    if (tpr == 1) spmv_launch_t<MODE, P, 1>(n, sptr, scol, sval, x, f, y, c, st);
+    else if (tpr == 2) spmv_launch_t<MODE, P, 2>(n, sptr, scol, sval, x, f, y, c, st);
+    else spmv_launch_t<MODE, P, 4>(n, sptr, scol, sval, x, f, y, c, st);
+}
+void launch_spmv(int mode, bool poisson, int tpr, i64 n, const i64* sptr, const i32* scol, const double* sval,
+                 const double* x, const double* f, double* y, const double* c, cudaStream_t st) {
+    if (mode == 0) {
+        if (poisson) spmv_launch_p<0, true>(tpr, n, sptr, scol, sval, x, f, y, c, st);
+        else spmv_launch_p<0, false>(tpr, n, sptr, scol, sval, x, f, y, c, st);
+    } else {
+        if (poisson) spmv_launch_p<1, true>(tpr, n, sptr, scol, sval, x, f, y, c, st);
+        else spmv_launch_p<1, false>(tpr, n, sptr, scol, sval, x, f, y, c, st);
+    }
+}
+
 void enqueue_sweep(mgm_ctx* ctx, int j, bool backward, cudaStream_t st) {
     Level& L = ctx->lv[j];
     for (int q = 0; q < L.ncol; ++q) {
@@ -575,10 +625,7 @@ void enqueue_sweep(mgm_ctx* ctx, int j, bool backward, cudaStream_t st) {
         if (r1 <= r0) continue;
         int span = r1 - (r0 & ~31);
         if (j == 0) timer_begin(ctx, 0, st);
-        if (ctx->poisson)
-            k_gs_colour<true><<<blocks_for(span, 128), 128, 0, st>>>(r0, r1, L.sptr, L.scol, L.sval, L.f, L.u, L.c, (int)L.n);
-        else
-            k_gs_colour<false><<<blocks_for(span, 128), 128, 0, st>>>(r0, r1, L.sptr, L.scol, L.sval, L.f, L.u, L.c, (int)L.n);
+        launch_gs(ctx->poisson, L.tpr, r0, r1, span, L, st);
         if (j == 0) timer_end(ctx, 0, st, sweep_colour_bytes(L, r1 - r0));
         ctx->vcycle_kernels++;
     }
@@ -596,10 +643,7 @@ void enqueue_border_dot(mgm_ctx* ctx, const Level& L, const double* x, const dou
 void enqueue_spmv(mgm_ctx* ctx, int j, const double* x, double* y, cudaStream_t st) {
     Level& L = ctx->lv[j];
     if (j == 0) timer_begin(ctx, 1, st);
-    if (ctx->poisson)
-        k_sell_spmv<0, true><<<blocks_for(L.n, 256), 256, 0, st>>>((int)L.n, L.sptr, L.scol, L.sval, x, nullptr, y, L.c);
-    else
-        k_sell_spmv<0, false><<<blocks_for(L.n, 256), 256, 0, st>>>((int)L.n, L.sptr, L.scol, L.sval, x, nullptr, y, L.c);
+    launch_spmv(0, ctx->poisson, L.tpr, L.n, L.sptr, L.scol, L.sval, x, nullptr, y, L.c, st);
     if (j == 0) timer_end(ctx, 1, st, 12.0 * L.nnz + 16.0 * L.n);
     if (ctx->poisson) enqueue_border_dot(ctx, L, x, nullptr, 0.0, 1.0, y, st);
 }
@@ -607,10 +651,7 @@ void enqueue_spmv(mgm_ctx* ctx, int j, const double* x, double* y, cudaStream_t 
 // t = f - L u (level j), Poisson: t[n] = f[n] - c.u
 void enqueue_residual(mgm_ctx* ctx, int j, const double* f, const double* u, double* t, cudaStream_t st) {
     Level& L = ctx->lv[j];
-    if (ctx->poisson)
-        k_sell_spmv<1, true><<<blocks_for(L.n, 256), 256, 0, st>>>((int)L.n, L.sptr, L.scol, L.sval, u, f, t, L.c);
-    else
-        k_sell_spmv<1, false><<<blocks_for(L.n, 256), 256, 0, st>>>((int)L.n, L.sptr, L.scol, L.sval, u, f, t, L.c);
+    launch_spmv(1, ctx->poisson, L.tpr, L.n, L.sptr, L.scol, L.sval, u, f, t, L.c, st);
     ctx->vcycle_kernels++;
     if (ctx->poisson) enqueue_border_dot(ctx, L, u, f, 1.0, -1.0, t, st);
 }
@@ -619,7 +660,7 @@ void enqueue_residual(mgm_ctx* ctx, int j, const double* f, const double* u, dou
 void enqueue_restrict(mgm_ctx* ctx, int j, const double* x, double* y, cudaStream_t st) {
     Level& L = ctx->lv[j];
     Level& Ln = ctx->lv[j + 1];
-    k_sell_spmv<0, false><<<blocks_for(Ln.n, 256), 256, 0, st>>>((int)Ln.n, L.rptr, L.rcol, L.rval, x, nullptr, y, nullptr);
+    launch_spmv(0, false, L.rtpr, Ln.n, L.rptr, L.rcol, L.rval, x, nullptr, y, nullptr, st);
     ctx->vcycle_kernels++;
     if (ctx->poisson) {
         k_copy1<<<1, 1, 0, st>>>(x + L.n, y + Ln.n);

@@ -12,42 +12,79 @@
 
 namespace mgm {
 
+// Streaming loads for matrix data (read once per sweep): non-coherent path, no L1
+// allocation.  Not volatile, so the compiler may batch them ahead of the gathers.
 __device__ __forceinline__ double ld_stream_f64(const double* p) {
     double v;
-    asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
     return v;
 }
 __device__ __forceinline__ int ld_stream_i32(const int* p) {
     int v;
-    asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
+    asm("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+
+// Partial row dot of a SELL-32 row: slots k = part, part+TPR, ... < w, all (val, col)
+// pairs of a CHUNK loaded before any gather so ~2*CHUNK loads are in flight per thread.
+template <int TPR, int CHUNK>
+__device__ __forceinline__ double sell_dot(const double* __restrict__ v, const int* __restrict__ cc,
+                                           int w, int part, const double* x) {
+    double acc = 0.0;
+    for (int k0 = part; k0 < w; k0 += TPR * CHUNK) {
+        int c[CHUNK];
+        double a[CHUNK];
+#pragma unroll
+        for (int q = 0; q < CHUNK; ++q) {
+            const int k = k0 + q * TPR;
+            c[q] = (k < w) ? ld_stream_i32(cc + 32 * k) : -1;
+            a[q] = (k < w) ? ld_stream_f64(v + 32 * k) : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < CHUNK; ++q)
+            if (c[q] >= 0) acc = fma(a[q], x[c[q]], acc);
+    }
+    return acc;
+}
+
+template <int TPR>
+__device__ __forceinline__ double group_sum(double v) {
+#pragma unroll
+    for (int o = TPR >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     return v;
 }
 
 // One colour of a Gauss-Seidel sweep (Poisson variant P:348-352):
-//   r = f_i - a_ii u_i - sum_{j != i} a_ij u_j [- c_i lambda];  u_i += r / a_ii
-// rows [r0, r1) of one colour; threads are aligned to 32-row slices.
-template <bool POISSON>
-__global__ void __launch_bounds__(128) k_gs_colour(int r0, int r1, const int64_t* __restrict__ sptr,
+//   u_i += (f_i - sum_j a_ij u_j [- c_i lambda]) / a_ii  over rows [r0, r1) of one colour.
+// TPR threads per row; threads aligned to 32-row slices.
+template <bool POISSON, int TPR, int CHUNK>
+__global__ void __launch_bounds__(256) k_gs_colour(int r0, int r1, const int64_t* __restrict__ sptr,
                                                    const int* __restrict__ scol,
                                                    const double* __restrict__ sval,
                                                    const double* __restrict__ f, double* u,
                                                    const double* __restrict__ c, int n) {
-    const int r = (r0 & ~31) + blockIdx.x * blockDim.x + threadIdx.x;
-    if (r < r0 || r >= r1) return;
-    const int64_t base = sptr[r >> 5] + (r & 31);
-    const int w = (int)((sptr[(r >> 5) + 1] - sptr[r >> 5]) >> 5);
-    const double* v = sval + base;
-    const int* cc = scol + base;
-    const double d = ld_stream_f64(v);
-    double acc = f[r] - d * u[r];
-#pragma unroll 8
-    for (int k = 1; k < w; ++k) acc -= ld_stream_f64(v + 32 * k) * u[ld_stream_i32(cc + 32 * k)];
-    if (POISSON) acc -= c[r] * u[n];
-    u[r] += acc / d;
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    const int r = (r0 & ~31) + g / TPR;
+    const int part = g % TPR;
+    const bool live = (r >= r0 && r < r1);
+    double acc = 0.0, d = 1.0;
+    if (live) {
+        const int64_t s0 = sptr[r >> 5];
+        const int w = (int)((sptr[(r >> 5) + 1] - s0) >> 5);
+        const int64_t base = s0 + (r & 31);
+        acc = sell_dot<TPR, CHUNK>(sval + base, scol + base, w, part, u);
+        d = ld_stream_f64(sval + base);
+    }
+    acc = group_sum<TPR>(acc);
+    if (live && part == 0) {
+        double res = f[r] - acc;
+        if (POISSON) res -= c[r] * u[n];
+        u[r] += res / d;
+    }
 }
 
 // y = L x  (MODE 0),  y = f - L x  (MODE 1).  Poisson: border term c_i * x[n].
-template <int MODE, bool POISSON>
+template <int MODE, bool POISSON, int TPR, int CHUNK>
 __global__ void __launch_bounds__(256) k_sell_spmv(int n, const int64_t* __restrict__ sptr,
                                                    const int* __restrict__ scol,
                                                    const double* __restrict__ sval,
@@ -55,17 +92,22 @@ __global__ void __launch_bounds__(256) k_sell_spmv(int n, const int64_t* __restr
                                                    const double* __restrict__ f,
                                                    double* __restrict__ y,
                                                    const double* __restrict__ c) {
-    const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= n) return;
-    const int64_t base = sptr[r >> 5] + (r & 31);
-    const int w = (int)((sptr[(r >> 5) + 1] - sptr[r >> 5]) >> 5);
-    const double* v = sval + base;
-    const int* cc = scol + base;
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    const int r = g / TPR;
+    const int part = g % TPR;
+    const bool live = r < n;
     double acc = 0.0;
-#pragma unroll 8
-    for (int k = 0; k < w; ++k) acc += ld_stream_f64(v + 32 * k) * x[ld_stream_i32(cc + 32 * k)];
-    if (POISSON) acc += c[r] * x[n];
-    y[r] = (MODE == 0) ? acc : f[r] - acc;
+    if (live) {
+        const int64_t s0 = sptr[r >> 5];
+        const int w = (int)((sptr[(r >> 5) + 1] - s0) >> 5);
+        const int64_t base = s0 + (r & 31);
+        acc = sell_dot<TPR, CHUNK>(sval + base, scol + base, w, part, x);
+    }
+    acc = group_sum<TPR>(acc);
+    if (live && part == 0) {
+        if (POISSON) acc += c[r] * x[n];
+        y[r] = (MODE == 0) ? acc : f[r] - acc;
+    }
 }
 
 // e[r] += sum_k P[k][r] * ec[Pcol[k][r]]  (interpolate + correct)
