@@ -7,6 +7,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <thread>
@@ -15,6 +16,7 @@
 #include "../../include/mgm.h"
 #include "mgm_internal.h"
 #include "solve_kernels.cuh"
+#include "tail_kernel.cuh"
 
 using namespace mgm;
 
@@ -86,6 +88,12 @@ struct mgm_ctx {
     // streams / graph
     cudaStream_t st = nullptr;
     cudaGraphExec_t vgraph = nullptr;
+    bool pdl = false;  // set while enqueueing the V-cycle (PDL launches)
+    // cluster tail (levels tailJ..p-1 in one thread-block-cluster kernel), tailJ < 0 = off
+    int tailJ = -1;
+    int tail_cluster = 16;
+    size_t tail_smem = 0;
+    TailParams tail{};
     i64 vcycle_kernels = 0;
     // GMRES workspace
     int restart = 50;
@@ -120,6 +128,24 @@ static cudaError_t dalloc(T** p, i64 count) {
 }
 
 static unsigned blocks_for(i64 n, int threads) { return (unsigned)std::max<i64>(1, (n + threads - 1) / threads); }
+
+// Kernel launch with optional programmatic dependent launch (PDL, see solve_kernels.cuh).
+static bool g_use_pdl = std::getenv("MGM_NO_PDL") == nullptr;
+template <typename... KArgs, typename... Args>
+static void launch(bool pdl, void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t st,
+                   Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = (pdl && g_use_pdl) ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
 
 // ---------------------------------------------------------------------------------------
 // Setup (Alg. 2)
@@ -197,6 +223,73 @@ mgm_status fail(mgm_ctx* ctx, mgm_status s, const std::string& msg, int64_t idx)
     ctx->err = msg;
     ctx->err_index = idx;
     return s;
+}
+
+// Choose the first level J >= 1 with N_J <= MGM_TAIL_MAX (default 65536) and prepare the
+// cluster kernel that runs levels J..p-1 (tail_kernel.cuh).  Disabled by MGM_NO_TAIL.
+void setup_tail(mgm_ctx* ctx) {
+    ctx->tailJ = -1;
+    if (std::getenv("MGM_NO_TAIL") || ctx->p < 3) return;
+    i64 tmax = 65536;
+    if (const char* e = std::getenv("MGM_TAIL_MAX")) tmax = std::atoll(e);
+    int J = -1;
+    for (int j = 1; j + 1 < ctx->p; ++j)
+        if (ctx->lv[j].n <= tmax) { J = j; break; }
+    if (J < 0 || ctx->p - J > TAIL_MAX_LEVELS) return;
+    for (int j = J; j + 1 < ctx->p; ++j)
+        if (ctx->lv[j].ncol > TAIL_MAX_COLOURS) return;
+    TailParams& T = ctx->tail;
+    T.J = J;
+    T.p = ctx->p;
+    T.nu1 = ctx->lp.nu1;
+    T.nu2 = ctx->lp.nu2;
+    T.pre_b = ctx->lp.smoother == 1;
+    T.post_b = ctx->lp.smoother == 1 || ctx->lp.smoother == 2;
+    T.poisson = ctx->poisson;
+    T.nc = ctx->nc;
+    T.lu = ctx->lu;
+    T.piv = ctx->piv;
+    for (int j = J; j < ctx->p; ++j) {
+        const Level& L = ctx->lv[j];
+        TailLevel& D = T.lv[j - J];
+        D.n = (int)L.n;
+        D.ncol = L.ncol;
+        D.tpr = L.tpr;
+        D.rtpr = L.rtpr;
+        D.pm = L.pm;
+        D.nnext = j + 1 < ctx->p ? (int)ctx->lv[j + 1].n : 0;
+        D.sptr = L.sptr; D.scol = L.scol; D.sval = L.sval;
+        D.pcol = L.pcol; D.pval = L.pval;
+        D.rptr = L.rptr; D.rcol = L.rcol; D.rval = L.rval;
+        D.u = L.u; D.f = L.f; D.t = L.t; D.c = L.c;
+        for (int c = 0; c <= L.ncol; ++c) D.coff[c] = (int)L.coff[c];
+    }
+    const size_t lu_bytes = (size_t)ctx->nc * ctx->nc * sizeof(double);
+    T.lu_smem = lu_bytes + ctx->nc * sizeof(double) <= 160 * 1024 ? 1 : 0;
+    ctx->tail_smem = (T.lu_smem ? lu_bytes : 0) + ctx->nc * sizeof(double);
+    if (cudaMalloc(&T.partials, 64 * sizeof(double)) != cudaSuccess) return;
+    cudaFuncSetAttribute(k_vcycle_tail, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(k_vcycle_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->tail_smem);
+    for (int cs : {16, 8}) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(cs);
+        cfg.blockDim = dim3(512);
+        cfg.dynamicSmemBytes = ctx->tail_smem;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = cs;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        int nclusters = 0;
+        if (cudaOccupancyMaxActiveClusters(&nclusters, k_vcycle_tail, &cfg) == cudaSuccess && nclusters > 0) {
+            ctx->tail_cluster = cs;
+            ctx->tailJ = J;
+            break;
+        }
+        cudaGetLastError();
+    }
 }
 
 mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i64 N) {
@@ -532,6 +625,7 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
         if ((s = upload(ctx, &ctx->d_lib2orig, l2o))) return s;
     }
     CK(cudaStreamSynchronize(st));
+    setup_tail(ctx);
     return MGM_OK;
 }
 
@@ -578,42 +672,44 @@ double sweep_colour_bytes(const Level& L, i64 rows) {
 }
 
 // kernel variants by threads-per-row (chosen per level from the SELL width)
+constexpr int CHUNK = 16;
 template <bool P, int TPR>
-void gs_launch_t(int r0, int r1, int span, const Level& L, cudaStream_t st) {
-    k_gs_colour<P, TPR, 8><<<blocks_for((i64)span * TPR, 256), 256, 0, st>>>(r0, r1, L.sptr, L.scol, L.sval, L.f,
-                                                                           L.u, L.c, (int)L.n);
+void gs_launch_t(bool pdl, int r0, int r1, int span, const Level& L, cudaStream_t st) {
+    launch(pdl, k_gs_colour<P, TPR, CHUNK>, blocks_for((i64)span * TPR, 256), 256, 0, st, r0, r1, L.sptr, L.scol,
+           L.sval, L.f, L.u, L.c, (int)L.n);
 }
-void launch_gs(bool poisson, int tpr, int r0, int r1, int span, const Level& L, cudaStream_t st) {
+void launch_gs(bool pdl, bool poisson, int tpr, int r0, int r1, int span, const Level& L, cudaStream_t st) {
     if (poisson) {
-        if (tpr == 1) gs_launch_t<true, 1>(r0, r1, span, L, st);
-        else if (tpr == 2) gs_launch_t<true, 2>(r0, r1, span, L, st);
-        else gs_launch_t<true, 4>(r0, r1, span, L, st);
+        if (tpr == 1) gs_launch_t<true, 1>(pdl, r0, r1, span, L, st);
+        else if (tpr == 2) gs_launch_t<true, 2>(pdl, r0, r1, span, L, st);
+        else gs_launch_t<true, 4>(pdl, r0, r1, span, L, st);
     } else {
-        if (tpr == 1) gs_launch_t<false, 1>(r0, r1, span, L, st);
-        else if (tpr == 2) gs_launch_t<false, 2>(r0, r1, span, L, st);
-        else gs_launch_t<false, 4>(r0, r1, span, L, st);
+        if (tpr == 1) gs_launch_t<false, 1>(pdl, r0, r1, span, L, st);
+        else if (tpr == 2) gs_launch_t<false, 2>(pdl, r0, r1, span, L, st);
+        else gs_launch_t<false, 4>(pdl, r0, r1, span, L, st);
     }
 }
 template <int MODE, bool P, int TPR>
-void spmv_launch_t(i64 n, const i64* sptr, const i32* scol, const double* sval, const double* x, const double* f,
-                   double* y, const double* c, cudaStream_t st) {
-    k_sell_spmv<MODE, P, TPR, 8><<<blocks_for(n * TPR, 256), 256, 0, st>>>((int)n, sptr, scol, sval, x, f, y, c);
+void spmv_launch_t(bool pdl, i64 n, const i64* sptr, const i32* scol, const double* sval, const double* x,
+                   const double* f, double* y, const double* c, cudaStream_t st) {
+    launch(pdl, k_sell_spmv<MODE, P, TPR, CHUNK>, blocks_for(n * TPR, 256), 256, 0, st, (int)n, sptr, scol, sval, x,
+           f, y, c);
 }
 template <int MODE, bool P>
-void spmv_launch_p(int tpr, i64 n, const i64* sptr, const i32* scol, const double* sval, const double* x,
+void spmv_launch_p(bool pdl, int tpr, i64 n, const i64* sptr, const i32* scol, const double* sval, const double* x,
                    const double* f, double* y, const double* c, cudaStream_t st) {
-    if (tpr == 1) spmv_launch_t<MODE, P, 1>(n, sptr, scol, sval, x, f, y, c, st);
-    else if (tpr == 2) spmv_launch_t<MODE, P, 2>(n, sptr, scol, sval, x, f, y, c, st);
-    else spmv_launch_t<MODE, P, 4>(n, sptr, scol, sval, x, f, y, c, st);
+    if (tpr == 1) spmv_launch_t<MODE, P, 1>(pdl, n, sptr, scol, sval, x, f, y, c, st);
+    else if (tpr == 2) spmv_launch_t<MODE, P, 2>(pdl, n, sptr, scol, sval, x, f, y, c, st);
+    else spmv_launch_t<MODE, P, 4>(pdl, n, sptr, scol, sval, x, f, y, c, st);
 }
-void launch_spmv(int mode, bool poisson, int tpr, i64 n, const i64* sptr, const i32* scol, const double* sval,
-                 const double* x, const double* f, double* y, const double* c, cudaStream_t st) {
+void launch_spmv(bool pdl, int mode, bool poisson, int tpr, i64 n, const i64* sptr, const i32* scol,
+                 const double* sval, const double* x, const double* f, double* y, const double* c, cudaStream_t st) {
     if (mode == 0) {
-        if (poisson) spmv_launch_p<0, true>(tpr, n, sptr, scol, sval, x, f, y, c, st);
-        else spmv_launch_p<0, false>(tpr, n, sptr, scol, sval, x, f, y, c, st);
+        if (poisson) spmv_launch_p<0, true>(pdl, tpr, n, sptr, scol, sval, x, f, y, c, st);
+        else spmv_launch_p<0, false>(pdl, tpr, n, sptr, scol, sval, x, f, y, c, st);
     } else {
-        if (poisson) spmv_launch_p<1, true>(tpr, n, sptr, scol, sval, x, f, y, c, st);
-        else spmv_launch_p<1, false>(tpr, n, sptr, scol, sval, x, f, y, c, st);
+        if (poisson) spmv_launch_p<1, true>(pdl, tpr, n, sptr, scol, sval, x, f, y, c, st);
+        else spmv_launch_p<1, false>(pdl, tpr, n, sptr, scol, sval, x, f, y, c, st);
     }
 }
 
@@ -625,7 +721,7 @@ void enqueue_sweep(mgm_ctx* ctx, int j, bool backward, cudaStream_t st) {
         if (r1 <= r0) continue;
         int span = r1 - (r0 & ~31);
         if (j == 0) timer_begin(ctx, 0, st);
-        launch_gs(ctx->poisson, L.tpr, r0, r1, span, L, st);
+        launch_gs(ctx->pdl, ctx->poisson, L.tpr, r0, r1, span, L, st);
         if (j == 0) timer_end(ctx, 0, st, sweep_colour_bytes(L, r1 - r0));
         ctx->vcycle_kernels++;
     }
@@ -634,8 +730,10 @@ void enqueue_sweep(mgm_ctx* ctx, int j, bool backward, cudaStream_t st) {
 // Poisson border row: y[n] = fs*f[n] + sign * (c . x)
 void enqueue_border_dot(mgm_ctx* ctx, const Level& L, const double* x, const double* f, double fs, double sign,
                         double* y, cudaStream_t st) {
-    k_multidot<<<RED_BLOCKS, RED_THREADS, 0, st>>>(L.n, L.c, 0, 1, x, ctx->partials);
-    k_border_finish<<<1, 32, 0, st>>>(ctx->partials, RED_BLOCKS, fs, f, (int)L.n, sign, y);
+    launch(ctx->pdl, k_multidot, RED_BLOCKS, RED_THREADS, 0, st, (i64)L.n, (const double*)L.c, (i64)0, 1, x,
+           ctx->partials);
+    launch(ctx->pdl, k_border_finish, 1, 32, 0, st, (const double*)ctx->partials, (int)RED_BLOCKS, fs, f, (int)L.n,
+           sign, y);
     ctx->vcycle_kernels += 2;
 }
 
@@ -643,7 +741,7 @@ void enqueue_border_dot(mgm_ctx* ctx, const Level& L, const double* x, const dou
 void enqueue_spmv(mgm_ctx* ctx, int j, const double* x, double* y, cudaStream_t st) {
     Level& L = ctx->lv[j];
     if (j == 0) timer_begin(ctx, 1, st);
-    launch_spmv(0, ctx->poisson, L.tpr, L.n, L.sptr, L.scol, L.sval, x, nullptr, y, L.c, st);
+    launch_spmv(ctx->pdl, 0, ctx->poisson, L.tpr, L.n, L.sptr, L.scol, L.sval, x, nullptr, y, L.c, st);
     if (j == 0) timer_end(ctx, 1, st, 12.0 * L.nnz + 16.0 * L.n);
     if (ctx->poisson) enqueue_border_dot(ctx, L, x, nullptr, 0.0, 1.0, y, st);
 }
@@ -651,7 +749,7 @@ void enqueue_spmv(mgm_ctx* ctx, int j, const double* x, double* y, cudaStream_t 
 // t = f - L u (level j), Poisson: t[n] = f[n] - c.u
 void enqueue_residual(mgm_ctx* ctx, int j, const double* f, const double* u, double* t, cudaStream_t st) {
     Level& L = ctx->lv[j];
-    launch_spmv(1, ctx->poisson, L.tpr, L.n, L.sptr, L.scol, L.sval, u, f, t, L.c, st);
+    launch_spmv(ctx->pdl, 1, ctx->poisson, L.tpr, L.n, L.sptr, L.scol, L.sval, u, f, t, L.c, st);
     ctx->vcycle_kernels++;
     if (ctx->poisson) enqueue_border_dot(ctx, L, u, f, 1.0, -1.0, t, st);
 }
@@ -660,10 +758,10 @@ void enqueue_residual(mgm_ctx* ctx, int j, const double* f, const double* u, dou
 void enqueue_restrict(mgm_ctx* ctx, int j, const double* x, double* y, cudaStream_t st) {
     Level& L = ctx->lv[j];
     Level& Ln = ctx->lv[j + 1];
-    launch_spmv(0, false, L.rtpr, Ln.n, L.rptr, L.rcol, L.rval, x, nullptr, y, nullptr, st);
+    launch_spmv(ctx->pdl, 0, false, L.rtpr, Ln.n, L.rptr, L.rcol, L.rval, x, nullptr, y, nullptr, st);
     ctx->vcycle_kernels++;
     if (ctx->poisson) {
-        k_copy1<<<1, 1, 0, st>>>(x + L.n, y + Ln.n);
+        launch(ctx->pdl, k_copy1, 1, 1, 0, st, (const double*)(x + L.n), y + Ln.n);
         ctx->vcycle_kernels++;
     }
 }
@@ -671,20 +769,24 @@ void enqueue_restrict(mgm_ctx* ctx, int j, const double* x, double* y, cudaStrea
 void enqueue_interp_correct(mgm_ctx* ctx, int j, const double* ec, double* e, cudaStream_t st) {
     Level& L = ctx->lv[j];
     Level& Ln = ctx->lv[j + 1];
-    if (ctx->poisson)
-        k_interp_correct<true><<<blocks_for(L.n + 1, 256), 256, 0, st>>>((int)L.n, L.pm, L.pcol, L.pval, ec, e, (int)Ln.n);
-    else
-        k_interp_correct<false><<<blocks_for(L.n + 1, 256), 256, 0, st>>>((int)L.n, L.pm, L.pcol, L.pval, ec, e, (int)Ln.n);
+    auto kern = ctx->poisson ? (L.pm <= 8 ? k_interp_correct<true, 8> : k_interp_correct<true, 16>)
+                             : (L.pm <= 8 ? k_interp_correct<false, 8> : k_interp_correct<false, 16>);
+    launch(ctx->pdl, kern, blocks_for(L.n + 1, 256), 256, 0, st, (int)L.n, L.pm, (const i32*)L.pcol,
+           (const double*)L.pval, ec, e, (int)Ln.n);
     ctx->vcycle_kernels++;
 }
 
 void enqueue_coarse(mgm_ctx* ctx, const double* r, double* e, cudaStream_t st) {
-    k_coarse_solve<<<1, 32, sizeof(double) * ctx->nc, st>>>(ctx->nc, ctx->lu, ctx->piv, r, e);
+    const int m = ctx->nc;
+    const int in_smem = (size_t)(m + m * m) * sizeof(double) <= 200 * 1024 ? 1 : 0;
+    const size_t smem = sizeof(double) * (m + (in_smem ? (size_t)m * m : 0));
+    cudaFuncSetAttribute(k_coarse_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    launch(ctx->pdl, k_coarse_solve, 1, 256, smem, st, m, in_smem, (const double*)ctx->lu, (const i32*)ctx->piv, r, e);
     ctx->vcycle_kernels++;
 }
 
 void enqueue_zero(mgm_ctx* ctx, double* x, i64 n, cudaStream_t st) {
-    k_fill<<<blocks_for(n, 256), 256, 0, st>>>(n, x, 0.0);
+    launch(ctx->pdl, k_fill, blocks_for(n, 256), 256, 0, st, n, x, 0.0);
     ctx->vcycle_kernels++;
 }
 
@@ -696,21 +798,44 @@ void enqueue_vcycle(mgm_ctx* ctx, cudaStream_t st) {
     const bool pre_b = ctx->lp.smoother == 1, post_b = ctx->lp.smoother == 1 || ctx->lp.smoother == 2;
     const i64 pad = ctx->poisson ? 1 : 0;
     ctx->vcycle_kernels = 0;
+    ctx->pdl = true;
+    struct Reset { mgm_ctx* c; ~Reset() { c->pdl = false; } } reset_{ctx};
     if (p == 1) {
         enqueue_coarse(ctx, lv[0].f, lv[0].u, st);
         return;
     }
+    // levels >= D are handled by the cluster tail kernel (if enabled), else D = p - 1
+    const int D = ctx->tailJ > 0 ? ctx->tailJ : p - 1;
     for (int s = 0; s < nu1; ++s) enqueue_sweep(ctx, 0, pre_b, st);      // line 4
     enqueue_residual(ctx, 0, lv[0].f, lv[0].u, lv[0].t, st);              // line 5
     enqueue_restrict(ctx, 0, lv[0].t, lv[1].f, st);
-    for (int j = 1; j + 1 < p; ++j) {                                     // lines 6-9
+    for (int j = 1; j < D; ++j) {                                         // lines 6-9
         enqueue_zero(ctx, lv[j].u, lv[j].n + pad, st);
         for (int s = 0; s < nu1; ++s) enqueue_sweep(ctx, j, pre_b, st);
         enqueue_residual(ctx, j, lv[j].f, lv[j].u, lv[j].t, st);
         enqueue_restrict(ctx, j, lv[j].t, lv[j + 1].f, st);
     }
-    enqueue_coarse(ctx, lv[p - 1].f, lv[p - 1].u, st);                     // line 10
-    for (int j = p - 2; j >= 1; --j) {                                    // lines 11-14
+    if (ctx->tailJ > 0) {                                                 // lines 6-14 for j >= J
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(ctx->tail_cluster);
+        cfg.blockDim = dim3(512);
+        cfg.dynamicSmemBytes = ctx->tail_smem;
+        cfg.stream = st;
+        cudaLaunchAttribute at[2];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = ctx->tail_cluster;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[1].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = g_use_pdl ? 2 : 1;
+        cudaLaunchKernelEx(&cfg, k_vcycle_tail, ctx->tail);
+        ctx->vcycle_kernels++;
+    } else {
+        enqueue_coarse(ctx, lv[p - 1].f, lv[p - 1].u, st);                 // line 10
+    }
+    for (int j = D - 1; j >= 1; --j) {                                    // lines 11-14
         enqueue_interp_correct(ctx, j, lv[j + 1].u, lv[j].u, st);
         for (int s = 0; s < nu2; ++s) enqueue_sweep(ctx, j, post_b, st);
     }
@@ -1025,6 +1150,7 @@ mgm_status mgm_destroy(mgm_ctx* ctx) {
                       (void*)ctx->xs, (void*)ctx->b, (void*)ctx->partials, (void*)ctx->dh})
         if (ptr) cudaFree(ptr);
     if (ctx->hh) cudaFreeHost(ctx->hh);
+    if (ctx->tail.partials) cudaFree(ctx->tail.partials);
     if (ctx->vgraph) cudaGraphExecDestroy(ctx->vgraph);
     for (auto& T : ctx->timer)
         for (auto e : T.ev) cudaEventDestroy(e);
@@ -1257,6 +1383,7 @@ mgm_status mgm_bytes_model(const mgm_ctx* ctx, double* vcycle_bytes, double* spm
 
 mgm_status mgm_vcycle_kernel_count(const mgm_ctx* ctx, int64_t* count) {
     if (!ctx || ctx->lv.empty() || !count) return MGM_ERR_ARG;
+    if (ctx->vcycle_kernels > 0) { *count = ctx->vcycle_kernels; return MGM_OK; }
     i64 c = 0;
     const int p = ctx->p;
     if (p == 1) { *count = 1; return MGM_OK; }

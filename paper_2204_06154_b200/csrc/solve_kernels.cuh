@@ -5,12 +5,21 @@
 //     diagonal in slot 0 for L_j, padding = (own row, 0.0).
 //   * P_j: ELL, width m, slot-major [m][n_j].
 //   * vectors: fp64, lib order; Poisson mode appends the multiplier lambda at index n_j.
+//
+// Programmatic dependent launch (PDL): inside the V-cycle graph every kernel is launched with
+// programmatic stream serialisation.  Each kernel first calls pdl_trigger() so its successor
+// can be scheduled, loads the immutable operator data it needs (prologue), then pdl_wait()s
+// for its predecessor before reading any vector or writing anything.  Launched without the
+// attribute, both instructions are no-ops.
 #pragma once
 #include <cuda_runtime.h>
 
 #include <cstdint>
 
 namespace mgm {
+
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 // Streaming loads for matrix data (read once per sweep): non-coherent path, no L1
 // allocation.  Not volatile, so the compiler may batch them ahead of the gathers.
@@ -25,27 +34,26 @@ __device__ __forceinline__ int ld_stream_i32(const int* p) {
     return v;
 }
 
-// Partial row dot of a SELL-32 row: slots k = part, part+TPR, ... < w, all (val, col)
-// pairs of a CHUNK loaded before any gather so ~2*CHUNK loads are in flight per thread.
-template <int TPR, int CHUNK>
-__device__ __forceinline__ double sell_dot(const double* __restrict__ v, const int* __restrict__ cc,
-                                           int w, int part, const double* x) {
-    double acc = 0.0;
-    for (int k0 = part; k0 < w; k0 += TPR * CHUNK) {
-        int c[CHUNK];
-        double a[CHUNK];
+// A chunk of one SELL-32 row held in registers: slots k0, k0+TPR, ..., k0+(CH-1)*TPR.
+template <int TPR, int CH>
+struct RowFrag {
+    int c[CH];
+    double a[CH];
+    __device__ __forceinline__ void load(const double* __restrict__ v, const int* __restrict__ cc, int w, int k0) {
 #pragma unroll
-        for (int q = 0; q < CHUNK; ++q) {
+        for (int q = 0; q < CH; ++q) {
             const int k = k0 + q * TPR;
             c[q] = (k < w) ? ld_stream_i32(cc + 32 * k) : -1;
             a[q] = (k < w) ? ld_stream_f64(v + 32 * k) : 0.0;
         }
-#pragma unroll
-        for (int q = 0; q < CHUNK; ++q)
-            if (c[q] >= 0) acc = fma(a[q], x[c[q]], acc);
     }
-    return acc;
-}
+    __device__ __forceinline__ double dot(const double* x, double acc) const {
+#pragma unroll
+        for (int q = 0; q < CH; ++q)
+            if (c[q] >= 0) acc = fma(a[q], x[c[q]], acc);
+        return acc;
+    }
+};
 
 template <int TPR>
 __device__ __forceinline__ double group_sum(double v) {
@@ -57,23 +65,35 @@ __device__ __forceinline__ double group_sum(double v) {
 // One colour of a Gauss-Seidel sweep (Poisson variant P:348-352):
 //   u_i += (f_i - sum_j a_ij u_j [- c_i lambda]) / a_ii  over rows [r0, r1) of one colour.
 // TPR threads per row; threads aligned to 32-row slices.
-template <bool POISSON, int TPR, int CHUNK>
+template <bool POISSON, int TPR, int CH>
 __global__ void __launch_bounds__(256) k_gs_colour(int r0, int r1, const int64_t* __restrict__ sptr,
                                                    const int* __restrict__ scol,
                                                    const double* __restrict__ sval,
                                                    const double* __restrict__ f, double* u,
                                                    const double* __restrict__ c, int n) {
+    pdl_trigger();
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
     const int r = (r0 & ~31) + g / TPR;
     const int part = g % TPR;
     const bool live = (r >= r0 && r < r1);
-    double acc = 0.0, d = 1.0;
+    RowFrag<TPR, CH> fr;
+    int w = 0;
+    int64_t base = 0;
+    double d = 1.0;
     if (live) {
         const int64_t s0 = sptr[r >> 5];
-        const int w = (int)((sptr[(r >> 5) + 1] - s0) >> 5);
-        const int64_t base = s0 + (r & 31);
-        acc = sell_dot<TPR, CHUNK>(sval + base, scol + base, w, part, u);
+        w = (int)((sptr[(r >> 5) + 1] - s0) >> 5);
+        base = s0 + (r & 31);
+        fr.load(sval + base, scol + base, w, part);
         d = ld_stream_f64(sval + base);
+    } else {
+        fr.load(sval, scol, 0, 0);
+    }
+    pdl_wait();
+    double acc = fr.dot(u, 0.0);
+    for (int k0 = part + TPR * CH; k0 < w; k0 += TPR * CH) {
+        fr.load(sval + base, scol + base, w, k0);
+        acc = fr.dot(u, acc);
     }
     acc = group_sum<TPR>(acc);
     if (live && part == 0) {
@@ -84,7 +104,7 @@ __global__ void __launch_bounds__(256) k_gs_colour(int r0, int r1, const int64_t
 }
 
 // y = L x  (MODE 0),  y = f - L x  (MODE 1).  Poisson: border term c_i * x[n].
-template <int MODE, bool POISSON, int TPR, int CHUNK>
+template <int MODE, bool POISSON, int TPR, int CH>
 __global__ void __launch_bounds__(256) k_sell_spmv(int n, const int64_t* __restrict__ sptr,
                                                    const int* __restrict__ scol,
                                                    const double* __restrict__ sval,
@@ -92,16 +112,27 @@ __global__ void __launch_bounds__(256) k_sell_spmv(int n, const int64_t* __restr
                                                    const double* __restrict__ f,
                                                    double* __restrict__ y,
                                                    const double* __restrict__ c) {
+    pdl_trigger();
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
     const int r = g / TPR;
     const int part = g % TPR;
     const bool live = r < n;
-    double acc = 0.0;
+    RowFrag<TPR, CH> fr;
+    int w = 0;
+    int64_t base = 0;
     if (live) {
         const int64_t s0 = sptr[r >> 5];
-        const int w = (int)((sptr[(r >> 5) + 1] - s0) >> 5);
-        const int64_t base = s0 + (r & 31);
-        acc = sell_dot<TPR, CHUNK>(sval + base, scol + base, w, part, x);
+        w = (int)((sptr[(r >> 5) + 1] - s0) >> 5);
+        base = s0 + (r & 31);
+        fr.load(sval + base, scol + base, w, part);
+    } else {
+        fr.load(sval, scol, 0, 0);
+    }
+    pdl_wait();
+    double acc = fr.dot(x, 0.0);
+    for (int k0 = part + TPR * CH; k0 < w; k0 += TPR * CH) {
+        fr.load(sval + base, scol + base, w, k0);
+        acc = fr.dot(x, acc);
     }
     acc = group_sum<TPR>(acc);
     if (live && part == 0) {
@@ -111,20 +142,31 @@ __global__ void __launch_bounds__(256) k_sell_spmv(int n, const int64_t* __restr
 }
 
 // e[r] += sum_k P[k][r] * ec[Pcol[k][r]]  (interpolate + correct)
-template <bool POISSON>
+template <bool POISSON, int M>
 __global__ void __launch_bounds__(256) k_interp_correct(int n, int m, const int* __restrict__ pcol,
                                                         const double* __restrict__ pval,
                                                         const double* __restrict__ ec,
                                                         double* __restrict__ e, int nc) {
+    pdl_trigger();
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    int cidx[M];
+    double a[M];
+#pragma unroll
+    for (int k = 0; k < M; ++k) {
+        const bool ok = r < n && k < m;
+        cidx[k] = ok ? ld_stream_i32(pcol + (int64_t)k * n + r) : -1;
+        a[k] = ok ? ld_stream_f64(pval + (int64_t)k * n + r) : 0.0;
+    }
+    pdl_wait();
     if (r > n) return;
     if (r == n) {
         if (POISSON) e[n] += ec[nc];
         return;
     }
     double acc = 0.0;
-    for (int k = 0; k < m; ++k)
-        acc += ld_stream_f64(pval + (int64_t)k * n + r) * ec[ld_stream_i32(pcol + (int64_t)k * n + r)];
+#pragma unroll
+    for (int k = 0; k < M; ++k)
+        if (cidx[k] >= 0) acc = fma(a[k], ec[cidx[k]], acc);
     e[r] += acc;
 }
 
@@ -143,13 +185,25 @@ __global__ void k_interp(int n, int m, const int* __restrict__ pcol, const doubl
     y[r] = acc;
 }
 
-// Dense coarse solve with the LU factors (column-major) and pivots, one warp.
-__global__ void k_coarse_solve(int m, const double* __restrict__ LU, const int* __restrict__ piv,
-                               const double* __restrict__ rhs, double* __restrict__ x) {
-    extern __shared__ double b[];
+// Dense coarse solve with the LU factors (column-major) and pivots.  The factors
+// are staged in shared memory by the whole CTA (prologue), then one warp solves.
+// smem: LU[m*m] (if it fits, else read from global), b[m]
+__global__ void __launch_bounds__(256) k_coarse_solve(int m, int lu_in_smem, const double* __restrict__ LU,
+                                                      const int* __restrict__ piv,
+                                                      const double* __restrict__ rhs,
+                                                      double* __restrict__ x) {
+    extern __shared__ double sm[];
+    pdl_trigger();
+    double* b = sm;
+    double* L = lu_in_smem ? sm + m : nullptr;
+    const double* A = lu_in_smem ? L : LU;
+    if (lu_in_smem)
+        for (int i = threadIdx.x; i < m * m; i += blockDim.x) L[i] = LU[i];
+    pdl_wait();
+    for (int i = threadIdx.x; i < m; i += blockDim.x) b[i] = rhs[i];
+    __syncthreads();
+    if (threadIdx.x >= 32) return;
     const int lane = threadIdx.x;
-    for (int i = lane; i < m; i += 32) b[i] = rhs[i];
-    __syncwarp();
     if (lane == 0)
         for (int k = 0; k < m; ++k) {
             int p = piv[k];
@@ -158,12 +212,12 @@ __global__ void k_coarse_solve(int m, const double* __restrict__ LU, const int* 
     __syncwarp();
     for (int k = 0; k < m; ++k) {  // forward, unit lower
         const double xk = b[k];
-        const double* col = LU + (int64_t)k * m;
+        const double* col = A + (int64_t)k * m;
         for (int i = k + 1 + lane; i < m; i += 32) b[i] -= col[i] * xk;
         __syncwarp();
     }
     for (int i = m - 1; i >= 0; --i) {  // backward
-        const double* col = LU + (int64_t)i * m;
+        const double* col = A + (int64_t)i * m;
         if (lane == 0) b[i] = b[i] / col[i];
         __syncwarp();
         const double xi = b[i];
@@ -174,10 +228,16 @@ __global__ void k_coarse_solve(int m, const double* __restrict__ LU, const int* 
 }
 
 __global__ void k_fill(int64_t n, double* __restrict__ x, double v) {
+    pdl_trigger();
+    pdl_wait();
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) x[i] = v;
 }
-__global__ void k_copy1(const double* __restrict__ src, double* __restrict__ dst) { *dst = *src; }
+__global__ void k_copy1(const double* __restrict__ src, double* __restrict__ dst) {
+    pdl_trigger();
+    pdl_wait();
+    *dst = *src;
+}
 
 // out[i] = in[idx[i]]  /  out[idx[i]] = in[i]
 __global__ void k_gather(int n, const int* __restrict__ idx, const double* __restrict__ in,
@@ -206,6 +266,8 @@ __global__ void __launch_bounds__(RED_THREADS) k_multidot(int64_t n, const doubl
                                                           int64_t ld, int k1,
                                                           const double* __restrict__ w,
                                                           double* __restrict__ partials) {
+    pdl_trigger();
+    pdl_wait();
     __shared__ double red[RED_THREADS / 32][MD_GROUP];
     const int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
     const int64_t b0 = blockIdx.x * chunk, b1 = min(n, b0 + chunk);
@@ -299,6 +361,8 @@ __global__ void k_vadd(int k1, double* __restrict__ h, const double* __restrict_
 __global__ void k_border_finish(const double* __restrict__ partials, int nblk, double fs,
                                 const double* __restrict__ f, int n, double sign,
                                 double* __restrict__ y) {
+    pdl_trigger();
+    pdl_wait();
     if (threadIdx.x == 0) {
         double t = 0.0;
         for (int b = 0; b < nblk; ++b) t += partials[b];

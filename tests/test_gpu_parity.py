@@ -213,3 +213,24 @@ def test_error_paths():
         MGM(w.points, w.normals, dict(w.stencil, stencil_n=0), w.levels)
     with pytest.raises(MGMError):
         MGM(w.points, w.normals, w.stencil, dict(w.levels, num_levels=9))
+
+
+@pytest.mark.parametrize("name", ["cfg1", "torus20000", "poisson6000"])
+def test_cluster_tail_equals_kernel_path(name, monkeypatch):
+    """The one-kernel cluster tail (levels J..p-1) computes the same V-cycle as one kernel
+    per colour / operator (MGM_NO_TAIL)."""
+    import torch
+    from paper_2204_06154_b200 import MGM
+
+    P = pair(name)
+    monkeypatch.setenv("MGM_NO_TAIL", "1")
+    m2 = MGM(P.w.points, P.w.normals, P.w.stencil, P.w.levels)
+    monkeypatch.delenv("MGM_NO_TAIL")
+    n = len(P.w.points)
+    f = torch.from_numpy(_rand(n, 5)).cuda()
+    u1 = torch.from_numpy(_rand(n, 6)).cuda()
+    u2 = u1.clone()
+    P.gpu.vcycle(f, u1)
+    m2.vcycle(f, u2)
+    assert relmax(u1.cpu().numpy(), u2.cpu().numpy()) <= 1e-14
+    m2.close()
