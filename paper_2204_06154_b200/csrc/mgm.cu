@@ -129,6 +129,25 @@ static cudaError_t dalloc(T** p, i64 count) {
 
 static unsigned blocks_for(i64 n, int threads) { return (unsigned)std::max<i64>(1, (n + threads - 1) / threads); }
 
+// Allow a kernel the device's opt-in maximum of dynamic shared memory (process-wide).
+static void set_max_dyn_smem(const void* kern) {
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncAttributes fa;
+    if (cudaFuncGetAttributes(&fa, kern) == cudaSuccess) optin -= (int)fa.sharedSizeBytes;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+}
+
+// First failed launch since the last check (a failed launch inside stream capture only
+// surfaces at cudaStreamEndCapture; this names it).
+static thread_local std::string g_launch_err;
+static void note_launch(cudaError_t e, unsigned grid, unsigned block, size_t smem) {
+    if (e != cudaSuccess && g_launch_err.empty())
+        g_launch_err = std::string(cudaGetErrorString(e)) + " (grid " + std::to_string(grid) + ", block " +
+                       std::to_string(block) + ", smem " + std::to_string(smem) + ")";
+}
+
 // Kernel launch with optional programmatic dependent launch (PDL, see solve_kernels.cuh).
 static bool g_use_pdl = std::getenv("MGM_NO_PDL") == nullptr;
 template <typename... KArgs, typename... Args>
@@ -144,7 +163,7 @@ static void launch(bool pdl, void (*kern)(KArgs...), unsigned grid, unsigned blo
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = (pdl && g_use_pdl) ? 1 : 0;
-    cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+    note_launch(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...), grid, block, smem);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -229,7 +248,8 @@ mgm_status fail(mgm_ctx* ctx, mgm_status s, const std::string& msg, int64_t idx)
 // cluster kernel that runs levels J..p-1 (tail_kernel.cuh).  Disabled by MGM_NO_TAIL.
 void setup_tail(mgm_ctx* ctx) {
     ctx->tailJ = -1;
-    if (std::getenv("MGM_NO_TAIL") || ctx->p < 3) return;
+    // off by default: measured slower than per-colour kernels (profiles/r01_notes.md); opt in with MGM_TAIL=1
+    if (!std::getenv("MGM_TAIL") || std::getenv("MGM_NO_TAIL") || ctx->p < 3) return;
     i64 tmax = 65536;
     if (const char* e = std::getenv("MGM_TAIL_MAX")) tmax = std::atoll(e);
     int J = -1;
@@ -262,14 +282,17 @@ void setup_tail(mgm_ctx* ctx) {
         D.pcol = L.pcol; D.pval = L.pval;
         D.rptr = L.rptr; D.rcol = L.rcol; D.rval = L.rval;
         D.u = L.u; D.f = L.f; D.t = L.t; D.c = L.c;
-        for (int c = 0; c <= L.ncol; ++c) D.coff[c] = (int)L.coff[c];
+        // the coarsest level is not coloured (coff empty): copy only what exists
+        for (size_t c = 0; c < L.coff.size(); ++c) D.coff[c] = (int)L.coff[c];
     }
     const size_t lu_bytes = (size_t)ctx->nc * ctx->nc * sizeof(double);
     T.lu_smem = lu_bytes + ctx->nc * sizeof(double) <= 160 * 1024 ? 1 : 0;
     ctx->tail_smem = (T.lu_smem ? lu_bytes : 0) + ctx->nc * sizeof(double);
     if (cudaMalloc(&T.partials, 64 * sizeof(double)) != cudaSuccess) return;
     cudaFuncSetAttribute(k_vcycle_tail, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    cudaFuncSetAttribute(k_vcycle_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->tail_smem);
+    // the attribute is process-wide (shared by every ctx): raise it to the opt-in maximum
+    // rather than to this ctx's size, so a later ctx cannot shrink it under an earlier one
+    set_max_dyn_smem((const void*)k_vcycle_tail);
     for (int cs : {16, 8}) {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(cs);
@@ -780,7 +803,7 @@ void enqueue_coarse(mgm_ctx* ctx, const double* r, double* e, cudaStream_t st) {
     const int m = ctx->nc;
     const int in_smem = (size_t)(m + m * m) * sizeof(double) <= 200 * 1024 ? 1 : 0;
     const size_t smem = sizeof(double) * (m + (in_smem ? (size_t)m * m : 0));
-    cudaFuncSetAttribute(k_coarse_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    set_max_dyn_smem((const void*)k_coarse_solve);
     launch(ctx->pdl, k_coarse_solve, 1, 256, smem, st, m, in_smem, (const double*)ctx->lu, (const i32*)ctx->piv, r, e);
     ctx->vcycle_kernels++;
 }
@@ -830,7 +853,7 @@ void enqueue_vcycle(mgm_ctx* ctx, cudaStream_t st) {
         at[1].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = at;
         cfg.numAttrs = g_use_pdl ? 2 : 1;
-        cudaLaunchKernelEx(&cfg, k_vcycle_tail, ctx->tail);
+        note_launch(cudaLaunchKernelEx(&cfg, k_vcycle_tail, ctx->tail), ctx->tail_cluster, 512, ctx->tail_smem);
         ctx->vcycle_kernels++;
     } else {
         enqueue_coarse(ctx, lv[p - 1].f, lv[p - 1].u, st);                 // line 10
@@ -849,8 +872,16 @@ mgm_status build_graph(mgm_ctx* ctx) {
     if (ctx->vgraph) return MGM_OK;
     cudaGraph_t g;
     CK(cudaStreamBeginCapture(ctx->st, cudaStreamCaptureModeThreadLocal));
+    g_launch_err.clear();
     enqueue_vcycle(ctx, ctx->st);
-    CK(cudaStreamEndCapture(ctx->st, &g));
+    const cudaError_t ce = cudaStreamEndCapture(ctx->st, &g);
+    if (ce != cudaSuccess || !g_launch_err.empty()) {
+        ctx->err = "V-cycle capture failed: " + std::string(cudaGetErrorString(ce)) + "; first failed launch: " +
+                   (g_launch_err.empty() ? std::string("none recorded") : g_launch_err);
+        g_launch_err.clear();
+        cudaGetLastError();
+        return MGM_ERR_CUDA;
+    }
     CK(cudaGraphInstantiate(&ctx->vgraph, g, 0));
     cudaGraphDestroy(g);
     return MGM_OK;

@@ -218,14 +218,14 @@ def test_error_paths():
 @pytest.mark.parametrize("name", ["cfg1", "torus20000", "poisson6000"])
 def test_cluster_tail_equals_kernel_path(name, monkeypatch):
     """The one-kernel cluster tail (levels J..p-1) computes the same V-cycle as one kernel
-    per colour / operator (MGM_NO_TAIL)."""
+    per colour / operator (the default path; the tail is enabled with MGM_TAIL=1)."""
     import torch
     from paper_2204_06154_b200 import MGM
 
     P = pair(name)
-    monkeypatch.setenv("MGM_NO_TAIL", "1")
+    monkeypatch.setenv("MGM_TAIL", "1")
     m2 = MGM(P.w.points, P.w.normals, P.w.stencil, P.w.levels)
-    monkeypatch.delenv("MGM_NO_TAIL")
+    monkeypatch.delenv("MGM_TAIL")
     n = len(P.w.points)
     f = torch.from_numpy(_rand(n, 5)).cuda()
     u1 = torch.from_numpy(_rand(n, 6)).cuda()
