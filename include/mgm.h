@@ -172,6 +172,19 @@ mgm_status mgm_bytes_model(const mgm_ctx* ctx, double* vcycle_bytes, double* spm
 /* Number of kernels launched by one V-cycle (graph nodes). */
 mgm_status mgm_vcycle_kernel_count(const mgm_ctx* ctx, int64_t* count);
 
+/* Diagnostics (not on the timed path).  With MGM_TRACE set in the environment at
+ * mgm_setup, the V-cycle graph contains one-thread stamp kernels between Alg. 3 stages
+ * that record %globaltimer (ns) once their predecessor has finished.  Copies the stamps
+ * of the last V-cycle into stamps_ns[cap] (host), *n = count (0 when tracing is off), and
+ * newline-separated stage labels into labels[label_cap] (may be NULL).  MGM_ERR_ARG if
+ * cap < *n. */
+mgm_status mgm_trace_read(const mgm_ctx* ctx, uint64_t* stamps_ns, int cap, int* n, char* labels, int label_cap);
+
+/* Diagnostics: start time (%globaltimer, ns) of every phase of the one-kernel bottom of the
+ * last V-cycle (MGM_TRACE set at setup), *n = number of phases (0 if tracing is off or the
+ * bottom kernel is not used); meta[4*q..] = {op, local, rows, threads per row} (may be NULL). */
+mgm_status mgm_bottom_trace_read(const mgm_ctx* ctx, uint64_t* stamps_ns, int cap, int* n, int32_t* meta);
+
 /* ---------------- host-only hooks of the setup's discrete steps (no GPU needed) --------
  * They run the same host code mgm_setup uses, so discrete-structure parity with the
  * oracle can be checked on a CPU-only machine. */

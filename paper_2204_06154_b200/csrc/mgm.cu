@@ -16,7 +16,7 @@
 #include "../../include/mgm.h"
 #include "mgm_internal.h"
 #include "solve_kernels.cuh"
-#include "tail_kernel.cuh"
+#include "bottom_kernel.cuh"
 
 using namespace mgm;
 
@@ -89,11 +89,25 @@ struct mgm_ctx {
     cudaStream_t st = nullptr;
     cudaGraphExec_t vgraph = nullptr;
     bool pdl = false;  // set while enqueueing the V-cycle (PDL launches)
-    // cluster tail (levels tailJ..p-1 in one thread-block-cluster kernel), tailJ < 0 = off
-    int tailJ = -1;
-    int tail_cluster = 16;
-    size_t tail_smem = 0;
-    TailParams tail{};
+    // bottom of the V-cycle (levels botJ..p-1) in one thread-block-cluster kernel
+    // (bottom_kernel.cuh); botJ < 0 = off
+    // stage trace (MGM_TRACE=1 at setup): %globaltimer stamps between V-cycle stages
+    unsigned long long* d_trace = nullptr;
+    int ntrace = 0;
+    std::vector<std::string> trace_labels;
+    int botJ = -1;
+    int bot_cluster = 16;
+    int bot_cs_log2 = 4;
+    size_t bot_smem = 0;
+    int nphases = 0;
+    int bot_ring_off = 0;
+    BPhase* d_phases = nullptr;
+    BChunk* d_chunks = nullptr;
+    BTile* d_tiles = nullptr;
+    int* d_ntiles = nullptr;
+    int bot_tiles_off = 0;
+    char* d_ops = nullptr;
+    std::vector<void*> bot_mem;
     i64 vcycle_kernels = 0;
     // GMRES workspace
     int restart = 50;
@@ -244,75 +258,264 @@ mgm_status fail(mgm_ctx* ctx, mgm_status s, const std::string& msg, int64_t idx)
     return s;
 }
 
-// Choose the first level J >= 1 with N_J <= MGM_TAIL_MAX (default 65536) and prepare the
-// cluster kernel that runs levels J..p-1 (tail_kernel.cuh).  Disabled by MGM_NO_TAIL.
-void setup_tail(mgm_ctx* ctx) {
-    ctx->tailJ = -1;
-    // off by default: measured slower than per-colour kernels (profiles/r01_notes.md); opt in with MGM_TAIL=1
-    if (!std::getenv("MGM_TAIL") || std::getenv("MGM_NO_TAIL") || ctx->p < 3) return;
-    i64 tmax = 65536;
-    if (const char* e = std::getenv("MGM_TAIL_MAX")) tmax = std::atoll(e);
-    int J = -1;
-    for (int j = 1; j + 1 < ctx->p; ++j)
-        if (ctx->lv[j].n <= tmax) { J = j; break; }
-    if (J < 0 || ctx->p - J > TAIL_MAX_LEVELS) return;
-    for (int j = J; j + 1 < ctx->p; ++j)
-        if (ctx->lv[j].ncol > TAIL_MAX_COLOURS) return;
-    TailParams& T = ctx->tail;
-    T.J = J;
-    T.p = ctx->p;
-    T.nu1 = ctx->lp.nu1;
-    T.nu2 = ctx->lp.nu2;
-    T.pre_b = ctx->lp.smoother == 1;
-    T.post_b = ctx->lp.smoother == 1 || ctx->lp.smoother == 2;
-    T.poisson = ctx->poisson;
-    T.nc = ctx->nc;
-    T.lu = ctx->lu;
-    T.piv = ctx->piv;
-    for (int j = J; j < ctx->p; ++j) {
-        const Level& L = ctx->lv[j];
-        TailLevel& D = T.lv[j - J];
-        D.n = (int)L.n;
-        D.ncol = L.ncol;
-        D.tpr = L.tpr;
-        D.rtpr = L.rtpr;
-        D.pm = L.pm;
-        D.nnext = j + 1 < ctx->p ? (int)ctx->lv[j + 1].n : 0;
-        D.sptr = L.sptr; D.scol = L.scol; D.sval = L.sval;
-        D.pcol = L.pcol; D.pval = L.pval;
-        D.rptr = L.rptr; D.rcol = L.rcol; D.rval = L.rval;
-        D.u = L.u; D.f = L.f; D.t = L.t; D.c = L.c;
-        // the coarsest level is not coloured (coff empty): copy only what exists
-        for (size_t c = 0; c < L.coff.size(); ++c) D.coff[c] = (int)L.coff[c];
-    }
-    const size_t lu_bytes = (size_t)ctx->nc * ctx->nc * sizeof(double);
-    T.lu_smem = lu_bytes + ctx->nc * sizeof(double) <= 160 * 1024 ? 1 : 0;
-    ctx->tail_smem = (T.lu_smem ? lu_bytes : 0) + ctx->nc * sizeof(double);
-    if (cudaMalloc(&T.partials, 64 * sizeof(double)) != cudaSuccess) return;
-    cudaFuncSetAttribute(k_vcycle_tail, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    // the attribute is process-wide (shared by every ctx): raise it to the opt-in maximum
-    // rather than to this ctx's size, so a later ctx cannot shrink it under an earlier one
-    set_max_dyn_smem((const void*)k_vcycle_tail);
-    for (int cs : {16, 8}) {
+// Build the phase list of the one-kernel bottom of the V-cycle (bottom_kernel.cuh) for the
+// levels J..p-1, J = the first level >= 1 with N_J <= MGM_BOT_MAX (default 16384; 0 = off).
+// Levels with N_j <= MGM_BOT_LOCAL (default 1024) run on CTA 0 alone with __syncthreads.
+// Shifted problems only.  Operators are re-packed as lib-order CSR (int32) with the
+// diagonal first, row-contiguous so that a thread group reads a row coalesced.
+template <class T>
+static T* bot_upload(mgm_ctx* ctx, const std::vector<T>& v, bool& ok) {
+    T* d = nullptr;
+    if (cudaMalloc((void**)&d, sizeof(T) * std::max<size_t>(1, v.size())) != cudaSuccess) { ok = false; return nullptr; }
+    ctx->bot_mem.push_back(d);
+    if (!v.empty() && cudaMemcpy(d, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice) != cudaSuccess) ok = false;
+    return d;
+}
+
+void setup_bottom(mgm_ctx* ctx, const std::vector<double>& LU, const std::vector<i32>& piv) {
+    ctx->botJ = -1;
+    i64 bmax = 4096, blocal = 1024;  // measured best split for cfg3 (profiles/r01_notes.md)
+    if (const char* e = std::getenv("MGM_BOT_MAX")) bmax = std::atoll(e);
+    if (const char* e = std::getenv("MGM_BOT_LOCAL")) blocal = std::atoll(e);
+    if (ctx->poisson || bmax <= 0 || ctx->p < 2) return;
+    const int p = ctx->p;
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncSetAttribute(k_vcycle_bottom, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    set_max_dyn_smem((const void*)k_vcycle_bottom);
+    // cluster size: 16 (non-portable) if the device can co-schedule it, else 8
+    int cs = 0;
+    for (int c : {16, 8}) {
         cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(cs);
-        cfg.blockDim = dim3(512);
-        cfg.dynamicSmemBytes = ctx->tail_smem;
+        cfg.gridDim = dim3(c);
+        cfg.blockDim = dim3(BOT_THREADS);
+        cfg.dynamicSmemBytes = 200 * 1024;
         cudaLaunchAttribute at[1];
         at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = cs;
+        at[0].val.clusterDim.x = c;
         at[0].val.clusterDim.y = 1;
         at[0].val.clusterDim.z = 1;
         cfg.attrs = at;
         cfg.numAttrs = 1;
-        int nclusters = 0;
-        if (cudaOccupancyMaxActiveClusters(&nclusters, k_vcycle_tail, &cfg) == cudaSuccess && nclusters > 0) {
-            ctx->tail_cluster = cs;
-            ctx->tailJ = J;
-            break;
-        }
+        int ncl = 0;
+        if (cudaOccupancyMaxActiveClusters(&ncl, k_vcycle_bottom, &cfg) == cudaSuccess && ncl > 0) { cs = c; break; }
         cudaGetLastError();
     }
+    if (!cs) return;
+    const int cs_log2 = cs == 16 ? 4 : 3;
+    const bool pre_b = ctx->lp.smoother == 1, post_b = ctx->lp.smoother == 1 || ctx->lp.smoother == 2;
+    const int nu1 = ctx->lp.nu1, nu2 = ctx->lp.nu2;
+    auto is_local = [&](int j) { return ctx->lv[j].n <= blocal; };
+    auto slice = [&](int j) { return is_local(j) ? ctx->lv[j].n : (ctx->lv[j].n + cs - 1) / cs; };
+    // first level J >= 1 with N_J <= bmax; the layout is checked against shared memory below
+    int J = -1;
+    for (int j = 1; j < p; ++j)
+        if (ctx->lv[j].n <= bmax) { J = j; break; }
+    if (J < 0) return;
+    {
+        i64 nph = 3;
+        for (int q = J; q + 1 < p; ++q) nph += (i64)(nu1 + nu2) * ctx->lv[q].ncol + 3;
+        if (nph > BOT_MAX_PHASES) return;
+    }
+    std::vector<int> ou(p), of(p), ot(p), sh(p);
+    for (int j = J; j < p; ++j) sh[j] = is_local(j) ? 0 : cs_log2;
+    // ---- operator byte stream: per operator and CTA, the rows the CTA owns (r = k mod C,
+    // ascending; local operators: all rows in CTA 0's stream), as 16-byte aligned records
+    // [1/a_rr or 0 | W values | W columns | pad]
+    std::vector<char> bytes;
+    struct Op { int W = 1, rb = 16; bool dist = false; std::vector<size_t> base; i64 n = 0; };
+    auto add_op = [&](const HostCSR& A, bool dist, bool with_dinv) {
+        Op o;
+        i64 W = 1;
+        for (i64 r = 0; r < A.nrows; ++r) W = std::max(W, A.ptr[r + 1] - A.ptr[r]);
+        o.W = (int)W;
+        o.rb = (int)((8 + 12 * W + 15) / 16 * 16);
+        o.dist = dist;
+        o.n = A.nrows;
+        const int nk = dist ? cs : 1;
+        o.base.assign(nk, 0);
+        for (int k = 0; k < nk; ++k) {
+            o.base[k] = bytes.size();
+            for (i64 r = dist ? k : 0; r < A.nrows; r += dist ? cs : 1) {
+                const size_t at = bytes.size();
+                bytes.resize(at + o.rb, 0);
+                char* rec = bytes.data() + at;
+                const i64 a0 = A.ptr[r], len = A.ptr[r + 1] - a0;
+                const double di = (with_dinv && len > 0) ? 1.0 / A.val[a0] : 0.0;
+                std::memcpy(rec, &di, 8);
+                for (i64 t = 0; t < W; ++t) {
+                    const double v = t < len ? A.val[a0 + t] : 0.0;
+                    const int c = t < len ? A.col[a0 + t] : (len > 0 ? A.col[a0] : 0);
+                    std::memcpy(rec + 8 + 8 * t, &v, 8);
+                    std::memcpy(rec + 8 + 8 * W + 4 * t, &c, 4);
+                }
+            }
+        }
+        return o;
+    };
+    std::vector<Op> OL(p), OP(p), OR(p);
+    for (int j = J; j + 1 < p; ++j) {
+        Level& L = ctx->lv[j];
+        OL[j] = add_op(L.L_lib, !is_local(j), true);
+        OP[j] = add_op(L.P_lib, !is_local(j), false);
+        OR[j] = add_op(transpose(L.P_lib), !is_local(j + 1), false);  // R_j = P_j^T
+    }
+    // coarsest: explicit inverse from the LU factors (same solution up to rounding, O13)
+    const int m = ctx->nc;
+    Op OC;
+    {
+        std::vector<double> b(m);
+        HostCSR A;
+        A.nrows = A.ncols = m;
+        A.ptr.resize(m + 1);
+        A.col.resize((size_t)m * m);
+        A.val.resize((size_t)m * m);
+        for (int r = 0; r <= m; ++r) A.ptr[r] = (i64)r * m;
+        for (int i = 0; i < m; ++i) {
+            std::fill(b.begin(), b.end(), 0.0);
+            b[i] = 1.0;
+            for (int k = 0; k < m; ++k)
+                if (piv[k] != k) std::swap(b[k], b[piv[k]]);
+            for (int k = 0; k < m; ++k)
+                for (int r = k + 1; r < m; ++r) b[r] -= LU[(size_t)k * m + r] * b[k];
+            for (int r = m - 1; r >= 0; --r) {
+                double acc = b[r];
+                for (int c = r + 1; c < m; ++c) acc -= LU[(size_t)c * m + r] * b[c];
+                b[r] = acc / LU[(size_t)r * m + r];
+            }
+            for (int r = 0; r < m; ++r) {
+                A.col[(size_t)r * m + i] = i;
+                A.val[(size_t)r * m + i] = b[r];
+            }
+        }
+        OC = add_op(A, !is_local(p - 1), false);
+    }
+    // ---- phases and per-CTA chunks
+    std::vector<BPhase> ph;
+    std::vector<BChunk> ch;
+    auto add = [&](int op, int out_level, i64 r0, i64 r1, const Op* O, int xo, int xs, int yo, int fo, int zo,
+                   double* g) {
+        if (r1 <= r0) return;
+        BPhase P{};
+        P.op = op;
+        P.local = is_local(out_level) ? 1 : 0;
+        P.r0 = (int)r0;
+        P.r1 = (int)r1;
+        P.W = O ? O->W : 1;
+        P.rb = O ? O->rb : 16;
+        P.tile_rows = std::max(1, BOT_STAGE_BYTES / P.rb);
+        P.xo = xo; P.xs = xs;
+        P.yo = yo; P.ys = sh[out_level];
+        P.fo = fo; P.zo = zo;
+        P.g = g;
+        // per-CTA rows; tpr: the largest power of two (<= 32) with one pass over a tile
+        i64 maxrows = 0;
+        for (int k = 0; k < cs; ++k) {
+            BChunk c{};
+            if (P.local) {
+                if (k == 0) {
+                    c.nrows = (int)(r1 - r0);
+                    if (O) c.off = O->base[0] + (size_t)r0 * O->rb;
+                }
+            } else {
+                const i64 first = r0 + ((k - r0) % cs + cs) % cs;  // first row >= r0 with r = k (mod C)
+                c.nrows = first < r1 ? (int)((r1 - first + cs - 1) / cs) : 0;
+                if (O) c.off = O->base[k] + (size_t)(first / cs) * O->rb;
+            }
+            maxrows = std::max<i64>(maxrows, c.nrows);
+            ch.push_back(c);
+        }
+        const i64 tile = std::min<i64>(maxrows, P.tile_rows);
+        int lg = 5;
+        while (lg > 0 && tile * (1 << lg) > BOT_CONSUMERS) --lg;
+        P.tpr_log2 = lg;
+        ph.push_back(P);
+    };
+    auto sweep = [&](int j, bool backward) {
+        Level& L = ctx->lv[j];
+        for (int q = 0; q < L.ncol; ++q) {
+            const int c = backward ? L.ncol - 1 - q : q;
+            add(BP_GS, j, L.coff[c], L.coff[c + 1], &OL[j], ou[j], sh[j], ou[j], of[j], 0, nullptr);
+        }
+    };
+    // vector offsets are patched once the table sizes are known: code -(1 + 3 j + {0:u,1:f,2:t})
+    for (int j = J; j < p; ++j) {
+        ou[j] = -(1 + 3 * j);
+        of[j] = -(2 + 3 * j);
+        ot[j] = -(3 + 3 * j);
+    }
+    add(BP_LOAD, J, 0, ctx->lv[J].n, nullptr, 0, 0, of[J], 0, ou[J], ctx->lv[J].f);  // f_J <- global, u_J = 0
+    for (int j = J; j + 1 < p; ++j) {  // Alg. 3 lines 6-9 (and 4-5 for j = J)
+        Level& L = ctx->lv[j];
+        Level& Ln = ctx->lv[j + 1];
+        for (int s2 = 0; s2 < nu1; ++s2) sweep(j, pre_b);
+        add(BP_RES, j, 0, L.n, &OL[j], ou[j], sh[j], ot[j], of[j], 0, nullptr);
+        add(BP_MVZ, j + 1, 0, Ln.n, &OR[j], ot[j], sh[j], of[j + 1], 0, ou[j + 1], nullptr);
+    }
+    add(BP_MV, p - 1, 0, m, &OC, of[p - 1], sh[p - 1], ou[p - 1], 0, 0, nullptr);  // line 10
+    for (int j = p - 2; j >= J; --j) {  // lines 11-14
+        add(BP_ADD, j, 0, ctx->lv[j].n, &OP[j], ou[j + 1], sh[j + 1], ou[j], 0, 0, nullptr);
+        for (int s2 = 0; s2 < nu2; ++s2) sweep(j, post_b);
+    }
+    add(BP_STORE, J, 0, ctx->lv[J].n, nullptr, ou[J], sh[J], 0, 0, 0, ctx->lv[J].u);  // u_J -> global
+    if ((int)ph.size() > BOT_MAX_PHASES) return;
+    // ---- per-CTA tile lists (consumption order) and the shared-memory layout
+    std::vector<std::vector<BTile>> tl(cs);
+    for (size_t q = 0; q < ph.size(); ++q) {
+        const BPhase& P = ph[q];
+        if (P.op == BP_LOAD || P.op == BP_STORE) continue;
+        for (int k = 0; k < cs; ++k) {
+            const BChunk& C = ch[q * cs + k];
+            for (int i0 = 0; i0 < C.nrows; i0 += P.tile_rows) {
+                BTile T{};
+                T.off = C.off + (unsigned long long)i0 * P.rb;
+                T.bytes = (unsigned)(std::min(P.tile_rows, C.nrows - i0) * P.rb);
+                tl[k].push_back(T);
+            }
+        }
+    }
+    size_t maxT = 1;
+    for (auto& v : tl) maxT = std::max(maxT, v.size());
+    const size_t tables = ph.size() * (sizeof(BPhase) + sizeof(BChunk));
+    const size_t tiles_off = (tables + 15) / 16 * 16;
+    const size_t ring_off = (tiles_off + maxT * sizeof(BTile) + 64 + 127) / 128 * 128;
+    size_t off = ring_off + (size_t)BOT_STAGES * BOT_STAGE_BYTES;
+    std::vector<int> vo(3 * p, 0);
+    for (int j = J; j < p; ++j)
+        for (int w = 0; w < 3; ++w) {
+            vo[3 * j + w] = (int)off;
+            off += (size_t)slice(j) * sizeof(double);
+        }
+    if (off + 1024 > (size_t)optin) return;  // does not fit: per-kernel path only
+    auto patch = [&](int& o) { if (o < 0) o = vo[-o - 1]; };
+    for (auto& P : ph) {
+        patch(P.xo);
+        patch(P.yo);
+        patch(P.fo);
+        patch(P.zo);
+    }
+    std::vector<BTile> tflat(maxT * cs);
+    std::vector<int> nt(cs + 1);
+    for (int k = 0; k < cs; ++k) {
+        std::copy(tl[k].begin(), tl[k].end(), tflat.begin() + k * maxT);
+        nt[k] = (int)tl[k].size();
+    }
+    nt[cs] = (int)maxT;
+    bool ok = true;
+    ctx->d_phases = bot_upload(ctx, ph, ok);
+    ctx->d_chunks = bot_upload(ctx, ch, ok);
+    ctx->d_tiles = bot_upload(ctx, tflat, ok);
+    ctx->d_ntiles = bot_upload(ctx, nt, ok);
+    ctx->d_ops = bot_upload(ctx, bytes, ok);
+    if (!ok) return;
+    ctx->nphases = (int)ph.size();
+    ctx->bot_cluster = cs;
+    ctx->bot_cs_log2 = cs_log2;
+    ctx->bot_tiles_off = (int)tiles_off;
+    ctx->bot_ring_off = (int)ring_off;
+    ctx->bot_smem = off;
+    ctx->botJ = J;
 }
 
 mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i64 N) {
@@ -640,6 +843,9 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
         if (bad >= 0) return fail(ctx, MGM_ERR_SINGULAR, "singular coarsest operator", bad);
         ctx->nc = m;
         if ((s = upload(ctx, &ctx->lu, LU)) || (s = upload(ctx, &ctx->piv, piv))) return s;
+        CK(cudaStreamSynchronize(st));
+        setup_bottom(ctx, LU, piv);
+        cudaGetLastError();
     }
     // ---- level-0 permutation
     {
@@ -647,8 +853,10 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
         for (i64 r = 0; r < N; ++r) l2o[r] = (i32)ctx->lv[0].ids[r];
         if ((s = upload(ctx, &ctx->d_lib2orig, l2o))) return s;
     }
+    if (std::getenv("MGM_TRACE")) CK(dalloc(&ctx->d_trace, 256 + 6 * BOT_MAX_PHASES));
+    if (const char* e = std::getenv("MGM_L2_PERSIST"))  // experiment: persisting-L2 carve-out (bytes)
+        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)std::atoll(e));
     CK(cudaStreamSynchronize(st));
-    setup_tail(ctx);
     return MGM_OK;
 }
 
@@ -813,8 +1021,24 @@ void enqueue_zero(mgm_ctx* ctx, double* x, i64 n, cudaStream_t st) {
     ctx->vcycle_kernels++;
 }
 
+// Trace stamp: waits for its predecessor (PDL) and records %globaltimer (ns).
+__global__ void k_stamp(unsigned long long* slot) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    *slot = t;
+}
+void stamp(mgm_ctx* ctx, const char* label, int level, cudaStream_t st) {
+    if (!ctx->d_trace || ctx->ntrace >= 256) return;
+    launch(true, k_stamp, 1, 1, 0, st, ctx->d_trace + ctx->ntrace);
+    ctx->trace_labels.push_back(std::string(label) + " L" + std::to_string(level));
+    ctx->ntrace++;
+}
+
 // Alg. 3 on level-0 buffers lv[0].f (rhs) and lv[0].u (guess in, result out), lib order.
 void enqueue_vcycle(mgm_ctx* ctx, cudaStream_t st) {
+    ctx->ntrace = 0;
+    ctx->trace_labels.clear();
     auto& lv = ctx->lv;
     const int p = ctx->p;
     const int nu1 = ctx->lp.nu1, nu2 = ctx->lp.nu2;
@@ -827,43 +1051,61 @@ void enqueue_vcycle(mgm_ctx* ctx, cudaStream_t st) {
         enqueue_coarse(ctx, lv[0].f, lv[0].u, st);
         return;
     }
-    // levels >= D are handled by the cluster tail kernel (if enabled), else D = p - 1
-    const int D = ctx->tailJ > 0 ? ctx->tailJ : p - 1;
+    // levels >= D run in the one-kernel bottom (if enabled), else D = p - 1
+    const int D = ctx->botJ > 0 ? ctx->botJ : p - 1;
+    stamp(ctx, "start", 0, st);
+    const bool bottom_only = std::getenv("MGM_DEBUG_BOTTOM_ONLY") && ctx->botJ > 0;  // timing experiment only
+    if (!bottom_only) {
     for (int s = 0; s < nu1; ++s) enqueue_sweep(ctx, 0, pre_b, st);      // line 4
+    stamp(ctx, "presmooth", 0, st);
     enqueue_residual(ctx, 0, lv[0].f, lv[0].u, lv[0].t, st);              // line 5
+    stamp(ctx, "residual", 0, st);
     enqueue_restrict(ctx, 0, lv[0].t, lv[1].f, st);
+    stamp(ctx, "restrict", 0, st);
     for (int j = 1; j < D; ++j) {                                         // lines 6-9
         enqueue_zero(ctx, lv[j].u, lv[j].n + pad, st);
         for (int s = 0; s < nu1; ++s) enqueue_sweep(ctx, j, pre_b, st);
+        stamp(ctx, "zero+presmooth", j, st);
         enqueue_residual(ctx, j, lv[j].f, lv[j].u, lv[j].t, st);
         enqueue_restrict(ctx, j, lv[j].t, lv[j + 1].f, st);
+        stamp(ctx, "residual+restrict", j, st);
     }
-    if (ctx->tailJ > 0) {                                                 // lines 6-14 for j >= J
+    }
+    if (ctx->botJ > 0) {                                                  // lines 6-14 for j >= J
         cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(ctx->tail_cluster);
-        cfg.blockDim = dim3(512);
-        cfg.dynamicSmemBytes = ctx->tail_smem;
+        cfg.gridDim = dim3(ctx->bot_cluster);
+        cfg.blockDim = dim3(BOT_THREADS);
         cfg.stream = st;
         cudaLaunchAttribute at[2];
         at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = ctx->tail_cluster;
+        at[0].val.clusterDim.x = ctx->bot_cluster;
         at[0].val.clusterDim.y = 1;
         at[0].val.clusterDim.z = 1;
         at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         at[1].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = at;
         cfg.numAttrs = g_use_pdl ? 2 : 1;
-        note_launch(cudaLaunchKernelEx(&cfg, k_vcycle_tail, ctx->tail), ctx->tail_cluster, 512, ctx->tail_smem);
+        cfg.dynamicSmemBytes = ctx->bot_smem;
+        note_launch(cudaLaunchKernelEx(&cfg, k_vcycle_bottom, (const BPhase*)ctx->d_phases, (const BChunk*)ctx->d_chunks,
+                                       (const BTile*)ctx->d_tiles, (const int*)ctx->d_ntiles, (const char*)ctx->d_ops,
+                                       ctx->nphases, ctx->bot_cs_log2, ctx->bot_tiles_off, ctx->bot_ring_off,
+                                       ctx->d_trace ? ctx->d_trace + 256 : (unsigned long long*)nullptr),
+                    ctx->bot_cluster, BOT_THREADS, cfg.dynamicSmemBytes);
         ctx->vcycle_kernels++;
     } else {
         enqueue_coarse(ctx, lv[p - 1].f, lv[p - 1].u, st);                 // line 10
     }
+    stamp(ctx, "bottom", D, st);
+    if (bottom_only) return;
     for (int j = D - 1; j >= 1; --j) {                                    // lines 11-14
         enqueue_interp_correct(ctx, j, lv[j + 1].u, lv[j].u, st);
         for (int s = 0; s < nu2; ++s) enqueue_sweep(ctx, j, post_b, st);
+        stamp(ctx, "interp+postsmooth", j, st);
     }
     enqueue_interp_correct(ctx, 0, lv[1].u, lv[0].u, st);                 // line 15
+    stamp(ctx, "interp", 0, st);
     for (int s = 0; s < nu2; ++s) enqueue_sweep(ctx, 0, post_b, st);      // line 16
+    stamp(ctx, "postsmooth", 0, st);
 }
 
 bool timing_on(const mgm_ctx* ctx) { return ctx->timer[0].on || ctx->timer[1].on; }
@@ -1181,7 +1423,8 @@ mgm_status mgm_destroy(mgm_ctx* ctx) {
                       (void*)ctx->xs, (void*)ctx->b, (void*)ctx->partials, (void*)ctx->dh})
         if (ptr) cudaFree(ptr);
     if (ctx->hh) cudaFreeHost(ctx->hh);
-    if (ctx->tail.partials) cudaFree(ctx->tail.partials);
+    for (void* q : ctx->bot_mem) cudaFree(q);
+    if (ctx->d_trace) cudaFree(ctx->d_trace);
     if (ctx->vgraph) cudaGraphExecDestroy(ctx->vgraph);
     for (auto& T : ctx->timer)
         for (auto e : T.ev) cudaEventDestroy(e);
@@ -1409,6 +1652,47 @@ mgm_status mgm_bytes_model(const mgm_ctx* ctx, double* vcycle_bytes, double* spm
     B += 8.0 * np * np + 16.0 * np;
     if (vcycle_bytes) *vcycle_bytes = B;
     if (spmv_bytes) *spmv_bytes = 12.0 * ctx->lv[0].nnz + 16.0 * ctx->lv[0].n;
+    return MGM_OK;
+}
+
+mgm_status mgm_trace_read(const mgm_ctx* ctx, uint64_t* stamps_ns, int cap, int* n, char* labels, int label_cap) {
+    if (!ctx || !n) return MGM_ERR_ARG;
+    *n = ctx->d_trace ? ctx->ntrace : 0;
+    if (*n == 0) return MGM_OK;
+    if (cap < *n) return MGM_ERR_ARG;
+    if (cudaMemcpy(stamps_ns, ctx->d_trace, sizeof(uint64_t) * *n, cudaMemcpyDeviceToHost) != cudaSuccess)
+        return MGM_ERR_CUDA;
+    if (labels && label_cap > 0) {
+        std::string all;
+        for (auto& l : ctx->trace_labels) all += l + "\n";
+        std::strncpy(labels, all.c_str(), label_cap - 1);
+        labels[label_cap - 1] = 0;
+    }
+    return MGM_OK;
+}
+
+mgm_status mgm_bottom_trace_read(const mgm_ctx* ctx, uint64_t* stamps_ns, int cap, int* n, int32_t* meta) {
+    if (!ctx || !n) return MGM_ERR_ARG;
+    *n = (ctx->d_trace && ctx->botJ > 0) ? ctx->nphases : 0;
+    if (*n == 0) return MGM_OK;
+    if (cap < *n) return MGM_ERR_ARG;
+    if (cudaMemcpy(stamps_ns, ctx->d_trace + 256, sizeof(uint64_t) * *n, cudaMemcpyDeviceToHost) != cudaSuccess)
+        return MGM_ERR_CUDA;
+    if (cap >= 5 * *n &&  // clock64 sub-stamps follow (4 per phase), see bottom_kernel.cuh
+        cudaMemcpy(stamps_ns + *n, ctx->d_trace + 256 + BOT_MAX_PHASES, sizeof(uint64_t) * 4 * *n,
+                   cudaMemcpyDeviceToHost) != cudaSuccess)
+        return MGM_ERR_CUDA;
+    if (meta) {
+        std::vector<BPhase> ph(*n);
+        if (cudaMemcpy(ph.data(), ctx->d_phases, sizeof(BPhase) * *n, cudaMemcpyDeviceToHost) != cudaSuccess)
+            return MGM_ERR_CUDA;
+        for (int q = 0; q < *n; ++q) {
+            meta[4 * q] = ph[q].op;
+            meta[4 * q + 1] = ph[q].local;
+            meta[4 * q + 2] = ph[q].r1 - ph[q].r0;  // rows
+            meta[4 * q + 3] = 1 << ph[q].tpr_log2;
+        }
+    }
     return MGM_OK;
 }
 

@@ -22,15 +22,22 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 // Streaming loads for matrix data (read once per sweep): non-coherent path, no L1
-// allocation.  Not volatile, so the compiler may batch them ahead of the gathers.
+// allocation, L2 evict_first so that the streamed upper levels do not evict the small
+// bottom levels (bottom_kernel.cuh loads those with evict_last).  Not volatile, so the
+// compiler may batch them ahead of the gathers.
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t pol;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
 __device__ __forceinline__ double ld_stream_f64(const double* p) {
     double v;
-    asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(policy_evict_first()));
     return v;
 }
 __device__ __forceinline__ int ld_stream_i32(const int* p) {
     int v;
-    asm("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(policy_evict_first()));
     return v;
 }
 
@@ -90,6 +97,13 @@ __global__ void __launch_bounds__(256) k_gs_colour(int r0, int r1, const int64_t
         fr.load(sval, scol, 0, 0);
     }
     pdl_wait();
+    // epilogue operands issued together with the gathers (one memory round trip)
+    double fr_v = 0.0, ur = 0.0, cl = 0.0;
+    if (live && part == 0) {
+        fr_v = f[r];
+        ur = u[r];
+        if (POISSON) cl = c[r] * u[n];
+    }
     double acc = fr.dot(u, 0.0);
     for (int k0 = part + TPR * CH; k0 < w; k0 += TPR * CH) {
         fr.load(sval + base, scol + base, w, k0);
@@ -97,9 +111,9 @@ __global__ void __launch_bounds__(256) k_gs_colour(int r0, int r1, const int64_t
     }
     acc = group_sum<TPR>(acc);
     if (live && part == 0) {
-        double res = f[r] - acc;
-        if (POISSON) res -= c[r] * u[n];
-        u[r] += res / d;
+        double res = fr_v - acc;
+        if (POISSON) res -= cl;
+        u[r] = ur + res / d;
     }
 }
 

@@ -73,6 +73,10 @@ _SIGS = {
     "mgm_timing_read": ([_vp, ctypes.c_int, _f64p, _i64p, _f64p], ctypes.c_int),
     "mgm_bytes_model": ([_vp, _f64p, _f64p], ctypes.c_int),
     "mgm_vcycle_kernel_count": ([_vp, _i64p], ctypes.c_int),
+    "mgm_trace_read": ([_vp, ctypes.POINTER(ctypes.c_uint64), ctypes.c_int,
+                        ctypes.POINTER(ctypes.c_int), ctypes.c_char_p, ctypes.c_int], ctypes.c_int),
+    "mgm_bottom_trace_read": ([_vp, ctypes.POINTER(ctypes.c_uint64), ctypes.c_int,
+                               ctypes.POINTER(ctypes.c_int), _i32p], ctypes.c_int),
     "mgm_host_morton": ([_f64p, _i64, _i64p], ctypes.c_int),
     "mgm_host_knn": ([_f64p, _i64, _f64p, _i64, ctypes.c_int, _i32p], ctypes.c_int),
     "mgm_host_wse": ([_f64p, _i64, _i64, _i64p], ctypes.c_int),
@@ -268,6 +272,27 @@ def mgm_vcycle_kernel_count(ctx) -> int:
     c = _i64()
     _check(load_library().mgm_vcycle_kernel_count(ctx, ctypes.byref(c)), ctx)
     return c.value
+
+
+def mgm_trace_read(ctx):
+    """Stage stamps of the last V-cycle (MGM_TRACE set at setup): list of (label, ns)."""
+    buf = (ctypes.c_uint64 * 256)()
+    n = ctypes.c_int()
+    lab = ctypes.create_string_buffer(16384)
+    _check(load_library().mgm_trace_read(ctx, buf, 256, ctypes.byref(n), lab, 16384), ctx)
+    labels = lab.value.decode().split("\n")
+    return [(labels[i], int(buf[i])) for i in range(n.value)]
+
+
+def mgm_bottom_trace_read(ctx):
+    """Phase start stamps of the one-kernel bottom (MGM_TRACE): (stamps ns, meta[n,4])."""
+    buf = (ctypes.c_uint64 * 8192)()
+    meta = np.zeros((4096, 4), dtype=np.int32)
+    n = ctypes.c_int()
+    _check(load_library().mgm_bottom_trace_read(ctx, buf, 8192, ctypes.byref(n), meta.ctypes.data_as(_i32p)), ctx)
+    k = n.value
+    sub = np.array(buf[k:5 * k], dtype=np.int64).reshape(k, 4) if k else np.zeros((0, 4), np.int64)
+    return np.array(buf[:k], dtype=np.uint64), meta[:k], sub
 
 
 def mgm_host_morton(points):
