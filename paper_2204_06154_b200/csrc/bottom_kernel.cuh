@@ -49,7 +49,7 @@ enum : int { BP_LOAD = 0, BP_GS = 1, BP_RES = 2, BP_MVZ = 3, BP_ADD = 4, BP_MV =
 constexpr int BOT_THREADS = 512;
 constexpr int BOT_MAX_PHASES = 1024;
 constexpr int BOT_STAGES = 4;
-constexpr int BOT_STAGE_BYTES = 24 * 1024;
+constexpr int BOT_STAGE_BYTES = 24 * 1024;  // default ring stage (MGM_BOT_STAGE overrides)
 
 // Vectors in distributed shared memory: byte offset of the slice (same in every CTA) and
 // distribution shift s: entry r is in CTA (r & (2^s - 1)) at slot r >> s (s = 0: CTA 0).
@@ -226,7 +226,8 @@ struct BTile {
 __global__ void __launch_bounds__(BOT_THREADS, 1)
     k_vcycle_bottom(const BPhase* __restrict__ gphases, const BChunk* __restrict__ gchunks,
                     const BTile* __restrict__ gtiles, const int* __restrict__ gntiles, const char* __restrict__ ops,
-                    int nph, int cs_log2, int tiles_off, int ring_off, unsigned long long* __restrict__ trace) {
+                    int nph, int cs_log2, int tiles_off, int ring_off, int stage_bytes,
+                    unsigned long long* __restrict__ trace) {
     extern __shared__ __align__(128) char smem[];
     BPhase* phases = reinterpret_cast<BPhase*>(smem);
     BChunk* chunks = reinterpret_cast<BChunk*>(smem + nph * sizeof(BPhase));
@@ -261,7 +262,7 @@ __global__ void __launch_bounds__(BOT_THREADS, 1)
             const int stage = issued % BOT_STAGES;
             const BTile T = tiles[issued];
             mbar_expect_tx(bars + 8 * stage, T.bytes);
-            tma_load(ring + stage * BOT_STAGE_BYTES, ops + T.off, T.bytes, bars + 8 * stage, pol);
+            tma_load(ring + stage * stage_bytes, ops + T.off, T.bytes, bars + 8 * stage, pol);
         }
     };
     if (producer) issue(BOT_STAGES - 1);  // operators are immutable: stream before the dependency wait
@@ -288,7 +289,7 @@ __global__ void __launch_bounds__(BOT_THREADS, 1)
                     if (threadIdx.x < BOT_CONSUMERS) {
                         mbar_wait(bars + 8 * stage, (unsigned)(consumed / BOT_STAGES) & 1u);
                         if (st && i0 == 0) st[1] = clock64();
-                        consume_tile_any(P, smem + ring_off + stage * BOT_STAGE_BYTES, min(P.tile_rows, nrows - i0),
+                        consume_tile_any(P, smem + ring_off + stage * stage_bytes, min(P.tile_rows, nrows - i0),
                                          i0, rank, cs_log2, smem, sbase);
                     }
                     ++consumed;

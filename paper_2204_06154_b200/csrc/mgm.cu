@@ -17,6 +17,7 @@
 #include "mgm_internal.h"
 #include "solve_kernels.cuh"
 #include "bottom_kernel.cuh"
+#include "sweep_kernel.cuh"
 
 using namespace mgm;
 
@@ -54,6 +55,13 @@ struct Level {
     HostCSR L_lib, P_lib;        // lib order
     std::vector<i32> colour_lib;
     std::vector<double> c_lib;
+    std::vector<i64> lib2mor;  // Morton index of each lib row
+    // one-kernel sweep with CTA-to-CTA dependencies (sweep_kernel.cuh); swB = 0: off
+    int swB = 0;
+    int* sw_cstart = nullptr;
+    int* sw_nbr_ptr = nullptr;
+    int* sw_nbr = nullptr;
+    unsigned* sw_prog = nullptr;
 };
 
 struct KernelTimer {
@@ -106,6 +114,7 @@ struct mgm_ctx {
     BTile* d_tiles = nullptr;
     int* d_ntiles = nullptr;
     int bot_tiles_off = 0;
+    int bot_stage = 0;
     char* d_ops = nullptr;
     std::vector<void*> bot_mem;
     i64 vcycle_kernels = 0;
@@ -117,6 +126,7 @@ struct mgm_ctx {
     double* xs = nullptr;    // solution accumulator (lib order)
     double* b = nullptr;     // rhs (lib order)
     double* partials = nullptr;
+    unsigned* tickets = nullptr;  // last-block counters of the fused reductions (reset by the finisher)
     double* dh = nullptr;    // device scratch: h1[128], h2[128], nrm2, misc
     double* hh = nullptr;    // pinned host mirror
     // timing
@@ -392,6 +402,10 @@ void setup_bottom(mgm_ctx* ctx, const std::vector<double>& LU, const std::vector
         OC = add_op(A, !is_local(p - 1), false);
     }
     // ---- phases and per-CTA chunks
+    int stage_bytes = BOT_STAGE_BYTES;
+    if (const char* e = std::getenv("MGM_BOT_STAGE")) stage_bytes = std::atoi(e);
+  for (;; stage_bytes /= 2) {  // shrink the ring until the layout fits shared memory
+    if (stage_bytes < 2048) return;
     std::vector<BPhase> ph;
     std::vector<BChunk> ch;
     auto add = [&](int op, int out_level, i64 r0, i64 r1, const Op* O, int xo, int xs, int yo, int fo, int zo,
@@ -404,7 +418,7 @@ void setup_bottom(mgm_ctx* ctx, const std::vector<double>& LU, const std::vector
         P.r1 = (int)r1;
         P.W = O ? O->W : 1;
         P.rb = O ? O->rb : 16;
-        P.tile_rows = std::max(1, BOT_STAGE_BYTES / P.rb);
+        P.tile_rows = std::max(1, stage_bytes / P.rb);
         P.xo = xo; P.xs = xs;
         P.yo = yo; P.ys = sh[out_level];
         P.fo = fo; P.zo = zo;
@@ -480,14 +494,14 @@ void setup_bottom(mgm_ctx* ctx, const std::vector<double>& LU, const std::vector
     const size_t tables = ph.size() * (sizeof(BPhase) + sizeof(BChunk));
     const size_t tiles_off = (tables + 15) / 16 * 16;
     const size_t ring_off = (tiles_off + maxT * sizeof(BTile) + 64 + 127) / 128 * 128;
-    size_t off = ring_off + (size_t)BOT_STAGES * BOT_STAGE_BYTES;
+    size_t off = ring_off + (size_t)BOT_STAGES * stage_bytes;
     std::vector<int> vo(3 * p, 0);
     for (int j = J; j < p; ++j)
         for (int w = 0; w < 3; ++w) {
             vo[3 * j + w] = (int)off;
             off += (size_t)slice(j) * sizeof(double);
         }
-    if (off + 1024 > (size_t)optin) return;  // does not fit: per-kernel path only
+    if (off + 1024 > (size_t)optin) continue;  // does not fit: smaller ring stages
     auto patch = [&](int& o) { if (o < 0) o = vo[-o - 1]; };
     for (auto& P : ph) {
         patch(P.xo);
@@ -515,7 +529,81 @@ void setup_bottom(mgm_ctx* ctx, const std::vector<double>& LU, const std::vector
     ctx->bot_tiles_off = (int)tiles_off;
     ctx->bot_ring_off = (int)ring_off;
     ctx->bot_smem = off;
+    ctx->bot_stage = stage_bytes;
     ctx->botJ = J;
+    return;
+  }
+}
+
+// Build the CTA-dependency sweep (sweep_kernel.cuh) for level j: B Morton-block owners,
+// per-colour row ranges, symmetric neighbour lists, progress counters.  Off for Poisson
+// problems (border terms) or with MGM_NO_SWEEP.
+template <int TPR>
+static int sweep_max_blocks() {
+    int dev = 0, nsm = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_gs_sweep<TPR, 16>, SW_THREADS, 0) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return per * nsm;
+}
+
+void setup_sweep(mgm_ctx* ctx, int j) {
+    Level& L = ctx->lv[j];
+    L.swB = 0;
+    // opt-in (MGM_SWEEP=1): measured slower than one kernel per colour (profiles/r01_notes.md)
+    if (ctx->poisson || !std::getenv("MGM_SWEEP") || std::getenv("MGM_NO_SWEEP") || L.ncol <= 1) return;
+    i64 rows_min = 16;
+    if (const char* e = std::getenv("MGM_SWEEP_ROWS")) rows_min = std::max<i64>(1, std::atoll(e));
+    const int bmax = L.tpr == 1 ? sweep_max_blocks<1>() : L.tpr == 2 ? sweep_max_blocks<2>() : sweep_max_blocks<4>();
+    if (bmax <= 0) return;
+    const i64 n = L.n;
+    const int B = (int)std::max<i64>(1, std::min<i64>(bmax, n / ((i64)L.ncol * rows_min)));
+    std::vector<i64> mstart(B + 1);
+    for (int b = 0; b <= B; ++b) mstart[b] = (i64)b * n / B;
+    std::vector<int> owner_m(n);
+    for (int b = 0; b < B; ++b)
+        for (i64 m = mstart[b]; m < mstart[b + 1]; ++m) owner_m[m] = b;
+    std::vector<int> cstart((size_t)L.ncol * (B + 1));
+    for (int c = 0; c < L.ncol; ++c) {
+        const i64 a0 = L.coff[c], a1 = L.coff[c + 1];
+        for (int b = 0; b <= B; ++b) {
+            // first row of colour c with Morton index >= mstart[b] (Morton-sorted inside a colour)
+            i64 lo = a0, hi = a1;
+            while (lo < hi) {
+                const i64 mid = (lo + hi) / 2;
+                if (L.lib2mor[mid] < mstart[b]) lo = mid + 1; else hi = mid;
+            }
+            cstart[(size_t)c * (B + 1) + b] = (int)lo;
+        }
+    }
+    std::vector<std::vector<int>> nb(B);
+    for (i64 r = 0; r < n; ++r) {
+        const int ob = owner_m[L.lib2mor[r]];
+        for (i64 t = L.L_lib.ptr[r]; t < L.L_lib.ptr[r + 1]; ++t) {
+            const int oc = owner_m[L.lib2mor[L.L_lib.col[t]]];
+            if (oc != ob) {
+                nb[ob].push_back(oc);
+                nb[oc].push_back(ob);
+            }
+        }
+    }
+    std::vector<int> nptr(B + 1, 0), nidx;
+    for (int b = 0; b < B; ++b) {
+        std::sort(nb[b].begin(), nb[b].end());
+        nb[b].erase(std::unique(nb[b].begin(), nb[b].end()), nb[b].end());
+        nidx.insert(nidx.end(), nb[b].begin(), nb[b].end());
+        nptr[b + 1] = (int)nidx.size();
+    }
+    bool ok = true;
+    L.sw_cstart = bot_upload(ctx, cstart, ok);
+    L.sw_nbr_ptr = bot_upload(ctx, nptr, ok);
+    L.sw_nbr = bot_upload(ctx, nidx, ok);
+    L.sw_prog = bot_upload(ctx, std::vector<unsigned>((size_t)B * SW_PROG_STRIDE, 0u), ok);
+    if (!ok) return;
+    L.swB = B;
 }
 
 mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i64 N) {
@@ -728,6 +816,7 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
             for (i64 i = 0; i < n; ++i) lib2mor[j][i] = i;
         }
         for (i64 r = 0; r < n; ++r) mor2lib[j][lib2mor[j][r]] = (i32)r;
+        L.lib2mor = lib2mor[j];
         L.ids.resize(n);
         L.colour_lib.resize(n);
         for (i64 r = 0; r < n; ++r) {
@@ -802,6 +891,7 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
         CK(cudaMemsetAsync(L.f, 0, sizeof(double) * vn, st));
         CK(cudaMemsetAsync(L.t, 0, sizeof(double) * vn, st));
     }
+    for (int j = 0; j + 1 < p; ++j) setup_sweep(ctx, j);
     // ---- Poisson border vectors c_{j+1} = P_j^T c_j, Morton order then lib
     if (ctx->poisson) {
         std::vector<double> cm(N, 1.0);
@@ -944,8 +1034,25 @@ void launch_spmv(bool pdl, int mode, bool poisson, int tpr, i64 n, const i64* sp
     }
 }
 
+bool timing_on(const mgm_ctx* ctx);
 void enqueue_sweep(mgm_ctx* ctx, int j, bool backward, cudaStream_t st) {
     Level& L = ctx->lv[j];
+    if (L.swB > 0 && !timing_on(ctx)) {  // one persistent kernel for the whole sweep
+        SweepParams P{};
+        P.n = (int)L.n;
+        P.ncol = L.ncol;
+        P.nsweep = 1;
+        P.backward = backward ? 1 : 0;
+        P.sptr = L.sptr; P.scol = L.scol; P.sval = L.sval;
+        P.f = L.f; P.u = L.u;
+        P.cstart = L.sw_cstart; P.nbr_ptr = L.sw_nbr_ptr; P.nbr = L.sw_nbr; P.prog = L.sw_prog;
+        // no PDL: every CTA must be co-resident, so the predecessor must have drained
+        if (L.tpr == 1) launch(false, k_gs_sweep<1, 16>, L.swB, SW_THREADS, 0, st, P);
+        else if (L.tpr == 2) launch(false, k_gs_sweep<2, 16>, L.swB, SW_THREADS, 0, st, P);
+        else launch(false, k_gs_sweep<4, 16>, L.swB, SW_THREADS, 0, st, P);
+        ctx->vcycle_kernels++;
+        return;
+    }
     for (int q = 0; q < L.ncol; ++q) {
         int c = backward ? L.ncol - 1 - q : q;
         int r0 = (int)L.coff[c], r1 = (int)L.coff[c + 1];
@@ -1088,7 +1195,7 @@ void enqueue_vcycle(mgm_ctx* ctx, cudaStream_t st) {
         cfg.dynamicSmemBytes = ctx->bot_smem;
         note_launch(cudaLaunchKernelEx(&cfg, k_vcycle_bottom, (const BPhase*)ctx->d_phases, (const BChunk*)ctx->d_chunks,
                                        (const BTile*)ctx->d_tiles, (const int*)ctx->d_ntiles, (const char*)ctx->d_ops,
-                                       ctx->nphases, ctx->bot_cs_log2, ctx->bot_tiles_off, ctx->bot_ring_off,
+                                       ctx->nphases, ctx->bot_cs_log2, ctx->bot_tiles_off, ctx->bot_ring_off, ctx->bot_stage,
                                        ctx->d_trace ? ctx->d_trace + 256 : (unsigned long long*)nullptr),
                     ctx->bot_cluster, BOT_THREADS, cfg.dynamicSmemBytes);
         ctx->vcycle_kernels++;
@@ -1154,6 +1261,8 @@ mgm_status ensure_krylov(mgm_ctx* ctx) {
     CK(dalloc(&ctx->xs, ctx->ld));
     CK(dalloc(&ctx->b, ctx->ld));
     CK(dalloc(&ctx->partials, (i64)RED_BLOCKS * 256));
+    CK(cudaMalloc((void**)&ctx->tickets, 64 * sizeof(unsigned)));
+    CK(cudaMemset(ctx->tickets, 0, 64 * sizeof(unsigned)));
     CK(dalloc(&ctx->dh, 1024));
     CK(cudaMallocHost((void**)&ctx->hh, sizeof(double) * 1024));
     return MGM_OK;
@@ -1161,8 +1270,7 @@ mgm_status ensure_krylov(mgm_ctx* ctx) {
 
 // dot over n entries of a and b -> device scalar out
 void enqueue_dot(mgm_ctx* ctx, i64 n, const double* a, const double* b, double* out, cudaStream_t st) {
-    k_multidot<<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, a, 0, 1, b, ctx->partials);
-    k_reduce_partials<<<1, 32, 0, st>>>(ctx->partials, RED_BLOCKS, 1, out);
+    k_multidot_fin<<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, a, 0, 1, b, ctx->partials, ctx->tickets, out, nullptr);
 }
 
 // A x on level 0 (bordered in Poisson mode), n-vector incl. multiplier
@@ -1230,14 +1338,13 @@ mgm_status gmres_lib(mgm_ctx* ctx, double tol, int maxit, mgm_report* rep, cudaS
             ++its;
             const int k1 = k + 1;
             // CGS2: h = V^T w; w -= V h; h2 = V^T w; w -= V h2; h += h2
-            k_multidot<<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, V, ld, k1, w, ctx->partials);
-            k_reduce_partials<<<1, 128, 0, st>>>(ctx->partials, RED_BLOCKS, k1, h1);
+            // CGS2 in 5 launches: h1 = V^T w; w -= V h1; h2 = V^T w (h1 += h2); w -= V h2 with
+            // ||w||^2; v_{k+1} = w / ||w||.  Reductions finish in the last block (deterministic).
+            k_multidot_fin<<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, V, ld, k1, w, ctx->partials, ctx->tickets, h1,
+                                                               nullptr);
             k_multiaxpy<<<RED_BLOCKS * 2, 256, 0, st>>>(n, V, ld, k1, h1, w);
-            k_multidot<<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, V, ld, k1, w, ctx->partials);
-            k_reduce_partials<<<1, 128, 0, st>>>(ctx->partials, RED_BLOCKS, k1, h2);
-            k_multiaxpy<<<RED_BLOCKS * 2, 256, 0, st>>>(n, V, ld, k1, h2, w);
-            k_vadd<<<1, 128, 0, st>>>(k1, h1, h2);
-            enqueue_dot(ctx, n, w, w, nr, st);
+            k_multidot_fin<<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, V, ld, k1, w, ctx->partials, ctx->tickets, h2, h1);
+            k_multiaxpy_norm<<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, V, ld, k1, h2, w, ctx->partials, ctx->tickets, nr);
             k_scale_by_invnorm<<<RED_BLOCKS, 256, 0, st>>>(n, w, nr, V + (i64)k1 * ld);
             CK(cudaMemcpyAsync(ctx->hh, h1, sizeof(double) * k1, cudaMemcpyDeviceToHost, st));
             CK(cudaMemcpyAsync(ctx->hh + 512, nr, sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -1420,7 +1527,7 @@ mgm_status mgm_destroy(mgm_ctx* ctx) {
             if (ptr) cudaFree(ptr);
     }
     for (void* ptr : {(void*)ctx->lu, (void*)ctx->piv, (void*)ctx->d_lib2orig, (void*)ctx->V, (void*)ctx->w,
-                      (void*)ctx->xs, (void*)ctx->b, (void*)ctx->partials, (void*)ctx->dh})
+                      (void*)ctx->xs, (void*)ctx->b, (void*)ctx->partials, (void*)ctx->dh, (void*)ctx->tickets})
         if (ptr) cudaFree(ptr);
     if (ctx->hh) cudaFreeHost(ctx->hh);
     for (void* q : ctx->bot_mem) cudaFree(q);

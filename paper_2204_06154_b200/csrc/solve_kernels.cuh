@@ -312,6 +312,97 @@ __global__ void __launch_bounds__(RED_THREADS) k_multidot(int64_t n, const doubl
     }
 }
 
+// Last-block finish of a deterministic reduction: every block has written its partials
+// (partials[b * k1 + j]); the block that takes the last ticket sums them in block order
+// (lanes stride over blocks, then a fixed shuffle tree), so the result is bitwise
+// reproducible whichever block finishes last.  out[j] = sum; acc[j] += sum if acc.
+__device__ __forceinline__ void finish_partials(const double* partials, int k1, unsigned* ticket, double* out,
+                                                double* acc) {
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int j = warp; j < k1; j += nw) {
+        double t = 0.0;
+        for (int b = lane; b < (int)gridDim.x; b += 32) t += __ldcg(partials + (int64_t)b * k1 + j);
+        t = warp_sum(t);
+        if (lane == 0) {
+            out[j] = t;
+            if (acc) acc[j] += t;
+        }
+    }
+    if (threadIdx.x == 0) *ticket = 0u;
+}
+
+// out[j] = V_j . w for j < k1 (V_j = V + j*ld), one launch (block partials + last-block finish)
+__global__ void __launch_bounds__(RED_THREADS) k_multidot_fin(int64_t n, const double* __restrict__ V, int64_t ld,
+                                                              int k1, const double* __restrict__ w,
+                                                              double* __restrict__ partials, unsigned* ticket,
+                                                              double* out, double* acc) {
+    __shared__ double red[RED_THREADS / 32][MD_GROUP];
+    const int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
+    const int64_t b0 = blockIdx.x * chunk, b1 = min(n, b0 + chunk);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int g = 0; g < k1; g += MD_GROUP) {
+        const int gn = min(MD_GROUP, k1 - g);
+        double s[MD_GROUP];
+#pragma unroll
+        for (int q = 0; q < MD_GROUP; ++q) s[q] = 0.0;
+        for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
+            const double wi = w[i];
+#pragma unroll
+            for (int q = 0; q < MD_GROUP; ++q)
+                if (q < gn) s[q] = fma(V[(int64_t)(g + q) * ld + i], wi, s[q]);
+        }
+#pragma unroll
+        for (int q = 0; q < MD_GROUP; ++q) {
+            double t = warp_sum(s[q]);
+            if (lane == 0) red[warp][q] = t;
+        }
+        __syncthreads();
+        if (threadIdx.x < gn) {
+            double t = 0.0;
+            for (int ww = 0; ww < RED_THREADS / 32; ++ww) t += red[ww][threadIdx.x];
+            partials[(int64_t)blockIdx.x * k1 + g + threadIdx.x] = t;
+        }
+        __syncthreads();
+    }
+    finish_partials(partials, k1, ticket, out, acc);
+}
+
+// w[i] -= sum_j V_j[i] h[j]; nrm2[0] = ||w||^2 (block partials + last-block finish)
+__global__ void __launch_bounds__(RED_THREADS) k_multiaxpy_norm(int64_t n, const double* __restrict__ V, int64_t ld,
+                                                                int k1, const double* __restrict__ h,
+                                                                double* __restrict__ w, double* __restrict__ partials,
+                                                                unsigned* ticket, double* nrm2) {
+    __shared__ double hs[256];
+    __shared__ double red[RED_THREADS / 32];
+    for (int j = threadIdx.x; j < k1; j += blockDim.x) hs[j] = h[j];
+    __syncthreads();
+    const int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
+    const int64_t b0 = blockIdx.x * chunk, b1 = min(n, b0 + chunk);
+    double s = 0.0;
+    for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
+        double a = w[i];
+        for (int j = 0; j < k1; ++j) a -= V[(int64_t)j * ld + i] * hs[j];
+        w[i] = a;
+        s = fma(a, a, s);
+    }
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int ww = 0; ww < RED_THREADS / 32; ++ww) t += red[ww];
+        partials[blockIdx.x] = t;
+    }
+    finish_partials(partials, 1, ticket, nrm2, nullptr);
+}
+
 // out[j] = scale * sum_b partials[b*k1 + j] (+ out0[j] if accumulate)
 __global__ void k_reduce_partials(const double* __restrict__ partials, int nblk, int k1,
                                   double* __restrict__ out) {
