@@ -965,12 +965,12 @@ void timer_begin(mgm_ctx* ctx, int cls, cudaStream_t st) {
     }
     cudaEventRecord(T.ev[T.used], st);
 }
-void timer_end(mgm_ctx* ctx, int cls, cudaStream_t st, double bytes) {
+void timer_end(mgm_ctx* ctx, int cls, cudaStream_t st, double bytes, int nlaunch = 1) {
     KernelTimer& T = ctx->timer[cls];
     if (!T.on) return;
     cudaEventRecord(T.ev[T.used + 1], st);
     T.used += 2;
-    T.launches += 1;
+    T.launches += nlaunch;
     T.bytes += bytes;
 }
 void timer_collect(mgm_ctx* ctx) {
@@ -1053,16 +1053,22 @@ void enqueue_sweep(mgm_ctx* ctx, int j, bool backward, cudaStream_t st) {
         ctx->vcycle_kernels++;
         return;
     }
+    // timing class 0: CUDA events around the whole level-0 sweep (the colour kernels keep
+    // their PDL overlap inside it); launches and algorithmic bytes are summed over colours
+    if (j == 0) timer_begin(ctx, 0, st);
+    double bytes = 0.0;
+    int nl = 0;
     for (int q = 0; q < L.ncol; ++q) {
         int c = backward ? L.ncol - 1 - q : q;
         int r0 = (int)L.coff[c], r1 = (int)L.coff[c + 1];
         if (r1 <= r0) continue;
         int span = r1 - (r0 & ~31);
-        if (j == 0) timer_begin(ctx, 0, st);
         launch_gs(ctx->pdl, ctx->poisson, L.tpr, r0, r1, span, L, st);
-        if (j == 0) timer_end(ctx, 0, st, sweep_colour_bytes(L, r1 - r0));
+        bytes += sweep_colour_bytes(L, r1 - r0);
+        ++nl;
         ctx->vcycle_kernels++;
     }
+    if (j == 0) timer_end(ctx, 0, st, bytes, nl);
 }
 
 // Poisson border row: y[n] = fs*f[n] + sign * (c . x)
