@@ -151,6 +151,9 @@ def main():
     ap.add_argument("--cfg", type=int, default=3)
     ap.add_argument("--n", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--parallel", choices=["replicas", "dist"], default="replicas",
+                    help="N>1: independent replicas of the solve (weak scaling) or one solve "
+                         "split across the ranks (mgm_dist_attach, strong scaling)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -174,6 +177,9 @@ def main():
     t0 = time.perf_counter()
     m = MGM(w.points, w.normals, w.stencil, w.levels)
     setup_s = time.perf_counter() - t0
+    dist_mode = ws > 1 and args.parallel == "dist"
+    if dist_mode:
+        m.attach_dist()
     st = torch.cuda.current_stream()
     rhs = torch.from_numpy(w.rhs).cuda()
     x = torch.empty_like(rhs)
@@ -277,13 +283,14 @@ def main():
         line = {
             "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "strong" if dist_mode else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded torus cloud, BASELINE configs[2] recipe)",
             "config": {"workload": f"{w.name} N={N}", "levels": [lv["n"] for lv in levels],
                        "nnz": [lv["nnz"] for lv in levels],
                        "colours": [lv["colours"] for lv in levels],
                        "gmres_iterations": its[-1], "restart": 50, "tol": 1e-10,
-                       "parallelism": "replicas" if ws > 1 else "single GPU",
+                       "parallelism": (f"dist{ws} (level-0 row pieces + NCCL)" if dist_mode else
+                                       f"replicas{ws}" if ws > 1 else "single GPU"),
                        "l2": "inputs larger than L2 (hierarchy %.2f GB)" %
                              (sum(lv["stored_bytes"] for lv in levels) / 1e9),
                        "setup_s": round(setup_s, 2)},

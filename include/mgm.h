@@ -42,7 +42,7 @@ typedef enum {
     MGM_ERR_SINGULAR = 3,   /* transfer system (index = fine row) or coarse LU (index = pivot) */
     MGM_ERR_BREAKDOWN = 4,  /* GMRES breakdown with a nonzero residual                       */
     MGM_ERR_CUDA = 5,       /* CUDA runtime error                                             */
-    MGM_ERR_NCCL = 6,       /* reserved (multi-GPU)                                           */
+    MGM_ERR_NCCL = 6,       /* NCCL missing or failed (multi-GPU)                             */
     MGM_ERR_OOM = 7,        /* device allocation failed                                       */
     MGM_ERR_INPUT = 8       /* duplicate points / non-finite input; index = offending point  */
 } mgm_status;
@@ -111,6 +111,31 @@ mgm_status mgm_solve_host(mgm_ctx* ctx, const double* rhs_host, double* x_host, 
                           int maxit, int krylov, mgm_report* report, void* cuda_stream);
 
 mgm_status mgm_destroy(mgm_ctx* ctx);
+
+/* ---- multi-GPU ----------------------------------
+ * One process per GPU.  Every rank calls mgm_setup with the SAME cloud and parameters (the
+ * setup is deterministic, so all ranks hold identical hierarchies), then mgm_dist_attach.
+ * From then on mgm_vcycle / mgm_solve are collective: on levels 0 .. D-1 (D from the
+ * environment variable MGM_DIST_LEVELS at mgm_setup, default 1) every operator application
+ * of Alg. 3 and of the Krylov loop (each colour of the Gauss-Seidel sweep, the residual,
+ * the restriction, the interpolation, the GMRES SpMV) is split into nranks contiguous row
+ * pieces (a colour's rows are in Morton order, so each piece is a Morton block of that
+ * colour); each rank computes its piece and the pieces are exchanged with in-place NCCL
+ * broadcasts (one grouped call per application), captured in the V-cycle's CUDA graph.
+ * Levels >= D are computed redundantly on every rank.  Krylov inner products: each rank
+ * reduces its own piece, then ncclAllReduce(sum).  Vectors stay replicated, so every
+ * rank's result is the same; the V-cycle is bitwise the single-GPU one, the GMRES
+ * iterates agree with it to rounding (the inner products are summed in another order).
+ * Shifted problems only (MGM_ERR_ARG for the Poisson problem with nranks > 1).
+ *
+ * mgm_nccl_unique_id: rank 0 creates the 128-byte NCCL id (host buffer id128); the caller
+ * broadcasts it to the other ranks (e.g. torch.distributed).  MGM_ERR_NCCL if
+ * libnccl.so.2 cannot be loaded.
+ * mgm_dist_attach: rank in [0, nranks); id128 = that id (host, 128 bytes, copied).  The
+ * communicator is created on the ctx's device and destroyed by mgm_destroy.  Errors:
+ * MGM_ERR_ARG (bad rank / already attached / Poisson), MGM_ERR_NCCL. */
+mgm_status mgm_nccl_unique_id(void* id128);
+mgm_status mgm_dist_attach(mgm_ctx* ctx, int rank, int nranks, const void* id128);
 
 /* Message of the last failure on this ctx (or of the last failed mgm_setup on this thread
  * when ctx is NULL); *failing_index (if non-NULL) receives the index or -1. */

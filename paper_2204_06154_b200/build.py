@@ -45,7 +45,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
                 raise RuntimeError(f"compilation of {src} failed")
     if force or _newer(objs, LIB):
         tmp = LIB + ".tmp%d" % os.getpid()
-        full = [NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-lpthread"]
+        full = [NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-lpthread", "-ldl"]
         r = subprocess.run(full, capture_output=True, text=True)
         if r.returncode:
             sys.stderr.write(" ".join(full) + "\n" + r.stdout + r.stderr)

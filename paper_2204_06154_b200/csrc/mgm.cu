@@ -2,6 +2,8 @@
 // captured as a CUDA graph, right-preconditioned GMRES, standalone MGM
 // and the C ABI declared in include/mgm.h.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <chrono>
@@ -20,6 +22,54 @@
 #include "sweep_kernel.cuh"
 
 using namespace mgm;
+
+// ---------------------------------------------------------------------------------------
+// NCCL, loaded at run time (dlopen "libnccl.so.2": inside a PyTorch process this resolves
+// to the NCCL torch already loaded), so libmgm has no link-time NCCL dependency.
+// ---------------------------------------------------------------------------------------
+namespace {
+struct NcclApi {
+    bool tried = false, ok = false;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) =
+        nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+NcclApi& nccl() {
+    static NcclApi api;
+    if (!api.tried) {
+        api.tried = true;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (h) {
+            api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+            api.CommInitRank = (decltype(api.CommInitRank))dlsym(h, "ncclCommInitRank");
+            api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
+            api.Broadcast = (decltype(api.Broadcast))dlsym(h, "ncclBroadcast");
+            api.AllReduce = (decltype(api.AllReduce))dlsym(h, "ncclAllReduce");
+            api.GroupStart = (decltype(api.GroupStart))dlsym(h, "ncclGroupStart");
+            api.GroupEnd = (decltype(api.GroupEnd))dlsym(h, "ncclGroupEnd");
+            api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
+            api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.Broadcast && api.AllReduce &&
+                     api.GroupStart && api.GroupEnd && api.GetErrorString;
+        }
+    }
+    return api;
+}
+void nccl_group_start() { nccl().GroupStart(); }
+void nccl_group_end() { nccl().GroupEnd(); }
+void nccl_bcast(double* p, size_t n, int root, ncclComm_t comm, cudaStream_t st) {
+    nccl().Broadcast(p, p, n, ncclFloat64, root, comm, st);
+}
+void nccl_allreduce_sum(double* p, size_t n, ncclComm_t comm, cudaStream_t st) {
+    nccl().AllReduce(p, p, n, ncclFloat64, ncclSum, comm, st);
+}
+}  // namespace
 
 namespace {
 
@@ -118,6 +168,11 @@ struct mgm_ctx {
     char* d_ops = nullptr;
     std::vector<void*> bot_mem;
     i64 vcycle_kernels = 0;
+    // multi-GPU (mgm_dist_attach)
+    int rank = 0, nranks = 1;
+    ncclComm_t comm = nullptr;
+    int dist_levels = 1;   // levels 0..dist_levels-1 are split across ranks (MGM_DIST_LEVELS)
+    int fake_ranks = 0;    // MGM_DIST_FAKE_RANKS: split into pieces on one GPU (test hook)
     // GMRES workspace
     int restart = 50;
     i64 ld = 0;
@@ -1011,27 +1066,75 @@ void launch_gs(bool pdl, bool poisson, int tpr, int r0, int r1, int span, const 
     }
 }
 template <int MODE, bool P, int TPR>
-void spmv_launch_t(bool pdl, i64 n, const i64* sptr, const i32* scol, const double* sval, const double* x,
-                   const double* f, double* y, const double* c, cudaStream_t st) {
-    launch(pdl, k_sell_spmv<MODE, P, TPR, CHUNK>, blocks_for(n * TPR, 256), 256, 0, st, (int)n, sptr, scol, sval, x,
-           f, y, c);
+void spmv_launch_t(bool pdl, i64 r0, i64 r1, i64 nl, const i64* sptr, const i32* scol, const double* sval,
+                   const double* x, const double* f, double* y, const double* c, cudaStream_t st) {
+    launch(pdl, k_sell_spmv<MODE, P, TPR, CHUNK>, blocks_for((r1 - (r0 & ~31)) * TPR, 256), 256, 0, st, (int)r0,
+           (int)r1, (int)nl, sptr, scol, sval, x, f, y, c);
 }
 template <int MODE, bool P>
-void spmv_launch_p(bool pdl, int tpr, i64 n, const i64* sptr, const i32* scol, const double* sval, const double* x,
-                   const double* f, double* y, const double* c, cudaStream_t st) {
-    if (tpr == 1) spmv_launch_t<MODE, P, 1>(pdl, n, sptr, scol, sval, x, f, y, c, st);
-    else if (tpr == 2) spmv_launch_t<MODE, P, 2>(pdl, n, sptr, scol, sval, x, f, y, c, st);
-    else spmv_launch_t<MODE, P, 4>(pdl, n, sptr, scol, sval, x, f, y, c, st);
+void spmv_launch_p(bool pdl, int tpr, i64 r0, i64 r1, i64 nl, const i64* sptr, const i32* scol, const double* sval,
+                   const double* x, const double* f, double* y, const double* c, cudaStream_t st) {
+    if (tpr == 1) spmv_launch_t<MODE, P, 1>(pdl, r0, r1, nl, sptr, scol, sval, x, f, y, c, st);
+    else if (tpr == 2) spmv_launch_t<MODE, P, 2>(pdl, r0, r1, nl, sptr, scol, sval, x, f, y, c, st);
+    else spmv_launch_t<MODE, P, 4>(pdl, r0, r1, nl, sptr, scol, sval, x, f, y, c, st);
 }
-void launch_spmv(bool pdl, int mode, bool poisson, int tpr, i64 n, const i64* sptr, const i32* scol,
-                 const double* sval, const double* x, const double* f, double* y, const double* c, cudaStream_t st) {
+// rows [r0, r1) of a SELL operator whose level has nl rows
+void launch_spmv(bool pdl, int mode, bool poisson, int tpr, i64 r0, i64 r1, i64 nl, const i64* sptr,
+                 const i32* scol, const double* sval, const double* x, const double* f, double* y, const double* c,
+                 cudaStream_t st) {
+    if (r1 <= r0) return;
     if (mode == 0) {
-        if (poisson) spmv_launch_p<0, true>(pdl, tpr, n, sptr, scol, sval, x, f, y, c, st);
-        else spmv_launch_p<0, false>(pdl, tpr, n, sptr, scol, sval, x, f, y, c, st);
+        if (poisson) spmv_launch_p<0, true>(pdl, tpr, r0, r1, nl, sptr, scol, sval, x, f, y, c, st);
+        else spmv_launch_p<0, false>(pdl, tpr, r0, r1, nl, sptr, scol, sval, x, f, y, c, st);
     } else {
-        if (poisson) spmv_launch_p<1, true>(pdl, tpr, n, sptr, scol, sval, x, f, y, c, st);
-        else spmv_launch_p<1, false>(pdl, tpr, n, sptr, scol, sval, x, f, y, c, st);
+        if (poisson) spmv_launch_p<1, true>(pdl, tpr, r0, r1, nl, sptr, scol, sval, x, f, y, c, st);
+        else spmv_launch_p<1, false>(pdl, tpr, r0, r1, nl, sptr, scol, sval, x, f, y, c, st);
     }
+}
+
+// ---------------------------------------------------------------------------------------
+// Multi-GPU (mgm_dist_attach): every rank holds the full hierarchy
+// and full vectors; on the distributed levels (j < dist_levels) each operator application
+// is split into nranks contiguous row pieces (a colour's rows are Morton-ordered, so a
+// piece is a Morton block of that colour), each rank computes its piece and the pieces are
+// exchanged with in-place NCCL broadcasts (one grouped call), after which every rank's
+// vector is bitwise what one GPU computes.  Krylov inner products: own piece + allreduce.
+// MGM_DIST_FAKE_RANKS=R (debug, 1 GPU): split into R pieces, all computed locally.
+// ---------------------------------------------------------------------------------------
+static void piece(i64 lo, i64 hi, int R, int q, i64& a, i64& b) {
+    const i64 len = hi - lo;
+    a = lo + len * q / R;
+    b = lo + len * (q + 1) / R;
+}
+// distributed once a communicator is attached (also with nranks = 1: one piece, the
+// broadcasts are then no-ops but the exchange path is exercised), or with fake ranks
+static bool dist_level(const mgm_ctx* ctx, int j) {
+    return (ctx->comm || ctx->fake_ranks > 1) && j < ctx->dist_levels;
+}
+static int dist_pieces(const mgm_ctx* ctx) { return ctx->comm ? ctx->nranks : ctx->fake_ranks; }
+// run f(a, b) on this rank's piece(s) of [lo, hi)
+template <class F>
+static void for_my_pieces(const mgm_ctx* ctx, int j, i64 lo, i64 hi, F f) {
+    if (!dist_level(ctx, j)) { f(lo, hi); return; }
+    const int R = dist_pieces(ctx);
+    for (int q = 0; q < R; ++q) {
+        if (ctx->comm && q != ctx->rank) continue;
+        i64 a, b;
+        piece(lo, hi, R, q, a, b);
+        f(a, b);
+    }
+}
+// exchange the pieces of y[lo, hi) after a distributed application
+static void dist_exchange(mgm_ctx* ctx, int j, double* y, i64 lo, i64 hi, cudaStream_t st) {
+    if (!dist_level(ctx, j) || !ctx->comm) return;
+    nccl_group_start();
+    for (int q = 0; q < ctx->nranks; ++q) {
+        i64 a, b;
+        piece(lo, hi, ctx->nranks, q, a, b);
+        if (b > a) nccl_bcast(y + a, (size_t)(b - a), q, ctx->comm, st);
+    }
+    nccl_group_end();
+    ctx->vcycle_kernels++;
 }
 
 bool timing_on(const mgm_ctx* ctx);
@@ -1060,13 +1163,16 @@ void enqueue_sweep(mgm_ctx* ctx, int j, bool backward, cudaStream_t st) {
     int nl = 0;
     for (int q = 0; q < L.ncol; ++q) {
         int c = backward ? L.ncol - 1 - q : q;
-        int r0 = (int)L.coff[c], r1 = (int)L.coff[c + 1];
-        if (r1 <= r0) continue;
-        int span = r1 - (r0 & ~31);
-        launch_gs(ctx->pdl, ctx->poisson, L.tpr, r0, r1, span, L, st);
-        bytes += sweep_colour_bytes(L, r1 - r0);
-        ++nl;
-        ctx->vcycle_kernels++;
+        const i64 c0 = L.coff[c], c1 = L.coff[c + 1];
+        if (c1 <= c0) continue;
+        for_my_pieces(ctx, j, c0, c1, [&](i64 a, i64 b) {
+            if (b <= a) return;
+            launch_gs(ctx->pdl, ctx->poisson, L.tpr, (int)a, (int)b, (int)(b - (a & ~31)), L, st);
+            bytes += sweep_colour_bytes(L, b - a);
+            ++nl;
+            ctx->vcycle_kernels++;
+        });
+        dist_exchange(ctx, j, L.u, c0, c1, st);
     }
     if (j == 0) timer_end(ctx, 0, st, bytes, nl);
 }
@@ -1085,7 +1191,10 @@ void enqueue_border_dot(mgm_ctx* ctx, const Level& L, const double* x, const dou
 void enqueue_spmv(mgm_ctx* ctx, int j, const double* x, double* y, cudaStream_t st) {
     Level& L = ctx->lv[j];
     if (j == 0) timer_begin(ctx, 1, st);
-    launch_spmv(ctx->pdl, 0, ctx->poisson, L.tpr, L.n, L.sptr, L.scol, L.sval, x, nullptr, y, L.c, st);
+    for_my_pieces(ctx, j, 0, L.n, [&](i64 a, i64 b) {
+        launch_spmv(ctx->pdl, 0, ctx->poisson, L.tpr, a, b, L.n, L.sptr, L.scol, L.sval, x, nullptr, y, L.c, st);
+    });
+    dist_exchange(ctx, j, y, 0, L.n, st);
     if (j == 0) timer_end(ctx, 1, st, 12.0 * L.nnz + 16.0 * L.n);
     if (ctx->poisson) enqueue_border_dot(ctx, L, x, nullptr, 0.0, 1.0, y, st);
 }
@@ -1093,8 +1202,11 @@ void enqueue_spmv(mgm_ctx* ctx, int j, const double* x, double* y, cudaStream_t 
 // t = f - L u (level j), Poisson: t[n] = f[n] - c.u
 void enqueue_residual(mgm_ctx* ctx, int j, const double* f, const double* u, double* t, cudaStream_t st) {
     Level& L = ctx->lv[j];
-    launch_spmv(ctx->pdl, 1, ctx->poisson, L.tpr, L.n, L.sptr, L.scol, L.sval, u, f, t, L.c, st);
-    ctx->vcycle_kernels++;
+    for_my_pieces(ctx, j, 0, L.n, [&](i64 a, i64 b) {
+        launch_spmv(ctx->pdl, 1, ctx->poisson, L.tpr, a, b, L.n, L.sptr, L.scol, L.sval, u, f, t, L.c, st);
+        ctx->vcycle_kernels++;
+    });
+    dist_exchange(ctx, j, t, 0, L.n, st);
     if (ctx->poisson) enqueue_border_dot(ctx, L, u, f, 1.0, -1.0, t, st);
 }
 
@@ -1102,8 +1214,11 @@ void enqueue_residual(mgm_ctx* ctx, int j, const double* f, const double* u, dou
 void enqueue_restrict(mgm_ctx* ctx, int j, const double* x, double* y, cudaStream_t st) {
     Level& L = ctx->lv[j];
     Level& Ln = ctx->lv[j + 1];
-    launch_spmv(ctx->pdl, 0, false, L.rtpr, Ln.n, L.rptr, L.rcol, L.rval, x, nullptr, y, nullptr, st);
-    ctx->vcycle_kernels++;
+    for_my_pieces(ctx, j, 0, Ln.n, [&](i64 a, i64 b) {
+        launch_spmv(ctx->pdl, 0, false, L.rtpr, a, b, Ln.n, L.rptr, L.rcol, L.rval, x, nullptr, y, nullptr, st);
+        ctx->vcycle_kernels++;
+    });
+    dist_exchange(ctx, j, y, 0, Ln.n, st);
     if (ctx->poisson) {
         launch(ctx->pdl, k_copy1, 1, 1, 0, st, (const double*)(x + L.n), y + Ln.n);
         ctx->vcycle_kernels++;
@@ -1115,9 +1230,13 @@ void enqueue_interp_correct(mgm_ctx* ctx, int j, const double* ec, double* e, cu
     Level& Ln = ctx->lv[j + 1];
     auto kern = ctx->poisson ? (L.pm <= 8 ? k_interp_correct<true, 8> : k_interp_correct<true, 16>)
                              : (L.pm <= 8 ? k_interp_correct<false, 8> : k_interp_correct<false, 16>);
-    launch(ctx->pdl, kern, blocks_for(L.n + 1, 256), 256, 0, st, (int)L.n, L.pm, (const i32*)L.pcol,
-           (const double*)L.pval, ec, e, (int)Ln.n);
-    ctx->vcycle_kernels++;
+    for_my_pieces(ctx, j, 0, L.n, [&](i64 a, i64 b) {
+        const i64 extra = (ctx->poisson && b == L.n) ? 1 : 0;  // multiplier thread
+        launch(ctx->pdl, kern, blocks_for(b - a + extra, 256), 256, 0, st, (int)a, (int)b, (int)L.n, L.pm,
+               (const i32*)L.pcol, (const double*)L.pval, ec, e, (int)Ln.n);
+        ctx->vcycle_kernels++;
+    });
+    dist_exchange(ctx, j, e, 0, L.n, st);
 }
 
 void enqueue_coarse(mgm_ctx* ctx, const double* r, double* e, cudaStream_t st) {
@@ -1275,8 +1394,23 @@ mgm_status ensure_krylov(mgm_ctx* ctx) {
 }
 
 // dot over n entries of a and b -> device scalar out
+// Krylov inner products: on nranks > 1 each rank reduces its own row piece (deterministic
+// in-kernel finish) and the pieces are summed with ncclAllReduce (identical on every rank).
+void enqueue_multidot(mgm_ctx* ctx, i64 n, const double* V, i64 ld, int k1, const double* w, double* out,
+                      double* acc, cudaStream_t st) {
+    if (!ctx->comm) {
+        k_multidot_fin<<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, V, ld, k1, w, ctx->partials, ctx->tickets, out, acc);
+        return;
+    }
+    i64 a, b;
+    piece(0, n, ctx->nranks, ctx->rank, a, b);
+    k_multidot_fin<<<RED_BLOCKS, RED_THREADS, 0, st>>>(b - a, V + a, ld, k1, w + a, ctx->partials, ctx->tickets, out,
+                                                       nullptr);
+    nccl_allreduce_sum(out, (size_t)k1, ctx->comm, st);
+    if (acc) k_vadd<<<1, 128, 0, st>>>(k1, acc, out);
+}
 void enqueue_dot(mgm_ctx* ctx, i64 n, const double* a, const double* b, double* out, cudaStream_t st) {
-    k_multidot_fin<<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, a, 0, 1, b, ctx->partials, ctx->tickets, out, nullptr);
+    enqueue_multidot(ctx, n, a, 0, 1, b, out, nullptr, st);
 }
 
 // A x on level 0 (bordered in Poisson mode), n-vector incl. multiplier
@@ -1346,11 +1480,16 @@ mgm_status gmres_lib(mgm_ctx* ctx, double tol, int maxit, mgm_report* rep, cudaS
             // CGS2: h = V^T w; w -= V h; h2 = V^T w; w -= V h2; h += h2
             // CGS2 in 5 launches: h1 = V^T w; w -= V h1; h2 = V^T w (h1 += h2); w -= V h2 with
             // ||w||^2; v_{k+1} = w / ||w||.  Reductions finish in the last block (deterministic).
-            k_multidot_fin<<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, V, ld, k1, w, ctx->partials, ctx->tickets, h1,
-                                                               nullptr);
+            enqueue_multidot(ctx, n, V, ld, k1, w, h1, nullptr, st);
             k_multiaxpy<<<RED_BLOCKS * 2, 256, 0, st>>>(n, V, ld, k1, h1, w);
-            k_multidot_fin<<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, V, ld, k1, w, ctx->partials, ctx->tickets, h2, h1);
-            k_multiaxpy_norm<<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, V, ld, k1, h2, w, ctx->partials, ctx->tickets, nr);
+            enqueue_multidot(ctx, n, V, ld, k1, w, h2, h1, st);
+            if (!ctx->comm) {
+                k_multiaxpy_norm<<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, V, ld, k1, h2, w, ctx->partials, ctx->tickets,
+                                                                     nr);
+            } else {  // full (replicated) update, distributed norm
+                k_multiaxpy<<<RED_BLOCKS * 2, 256, 0, st>>>(n, V, ld, k1, h2, w);
+                enqueue_dot(ctx, n, w, w, nr, st);
+            }
             k_scale_by_invnorm<<<RED_BLOCKS, 256, 0, st>>>(n, w, nr, V + (i64)k1 * ld);
             CK(cudaMemcpyAsync(ctx->hh, h1, sizeof(double) * k1, cudaMemcpyDeviceToHost, st));
             CK(cudaMemcpyAsync(ctx->hh + 512, nr, sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -1503,6 +1642,8 @@ mgm_status mgm_setup(const double* points, const double* normals, int64_t n_poin
     ctx->poisson = sp.problem == 1;
     ctx->restart = lp.restart;
     ctx->nthreads = std::max(1, std::min(64, (int)std::thread::hardware_concurrency()));
+    if (const char* e = std::getenv("MGM_DIST_LEVELS")) ctx->dist_levels = std::max(0, std::atoi(e));
+    if (const char* e = std::getenv("MGM_DIST_FAKE_RANKS")) ctx->fake_ranks = ctx->poisson ? 0 : std::max(0, std::atoi(e));
     cudaGetDevice(&ctx->device);
     (void)cuda_stream;
     if (cudaStreamCreateWithFlags(&ctx->st, cudaStreamNonBlocking) != cudaSuccess) {
@@ -1523,6 +1664,45 @@ mgm_status mgm_setup(const double* points, const double* normals, int64_t n_poin
     return MGM_OK;
 }
 
+mgm_status mgm_nccl_unique_id(void* id128) {
+    if (!id128) return MGM_ERR_ARG;
+    if (!nccl().ok) return MGM_ERR_NCCL;
+    ncclUniqueId id;
+    if (nccl().GetUniqueId(&id) != ncclSuccess) return MGM_ERR_NCCL;
+    std::memcpy(id128, &id, sizeof(id));
+    return MGM_OK;
+}
+
+mgm_status mgm_dist_attach(mgm_ctx* ctx, int rank, int nranks, const void* id128) {
+    if (!ctx || ctx->lv.empty() || nranks < 1 || rank < 0 || rank >= nranks || !id128) return MGM_ERR_ARG;
+    if (ctx->poisson && nranks > 1) {
+        ctx->err = "multi-GPU solve supports the shifted problem only";
+        return MGM_ERR_ARG;
+    }
+    if (ctx->comm) return MGM_ERR_ARG;
+    if (!nccl().ok) {
+        ctx->err = "libnccl.so.2 not found";
+        return MGM_ERR_NCCL;
+    }
+    cudaSetDevice(ctx->device);
+    ncclUniqueId id;
+    std::memcpy(&id, id128, sizeof(id));
+    ncclComm_t comm;
+    const ncclResult_t r = nccl().CommInitRank(&comm, nranks, id, rank);
+    if (r != ncclSuccess) {
+        ctx->err = std::string("ncclCommInitRank: ") + nccl().GetErrorString(r);
+        return MGM_ERR_NCCL;
+    }
+    ctx->comm = comm;
+    ctx->rank = rank;
+    ctx->nranks = nranks;
+    if (ctx->vgraph) {  // re-capture with the exchanges
+        cudaGraphExecDestroy(ctx->vgraph);
+        ctx->vgraph = nullptr;
+    }
+    return MGM_OK;
+}
+
 mgm_status mgm_destroy(mgm_ctx* ctx) {
     if (!ctx) return MGM_OK;
     cudaSetDevice(ctx->device);
@@ -1539,6 +1719,7 @@ mgm_status mgm_destroy(mgm_ctx* ctx) {
     for (void* q : ctx->bot_mem) cudaFree(q);
     if (ctx->d_trace) cudaFree(ctx->d_trace);
     if (ctx->vgraph) cudaGraphExecDestroy(ctx->vgraph);
+    if (ctx->comm) nccl().CommDestroy(ctx->comm);
     for (auto& T : ctx->timer)
         for (auto e : T.ev) cudaEventDestroy(e);
     if (ctx->st) cudaStreamDestroy(ctx->st);

@@ -117,9 +117,10 @@ __global__ void __launch_bounds__(256) k_gs_colour(int r0, int r1, const int64_t
     }
 }
 
-// y = L x  (MODE 0),  y = f - L x  (MODE 1).  Poisson: border term c_i * x[n].
+// y = L x  (MODE 0),  y = f - L x  (MODE 1) on the rows [r0, r1).  Poisson: border term
+// c_i * x[nl] (nl = the level's row count; the multiplier sits after the rows).
 template <int MODE, bool POISSON, int TPR, int CH>
-__global__ void __launch_bounds__(256) k_sell_spmv(int n, const int64_t* __restrict__ sptr,
+__global__ void __launch_bounds__(256) k_sell_spmv(int r0, int r1, int nl, const int64_t* __restrict__ sptr,
                                                    const int* __restrict__ scol,
                                                    const double* __restrict__ sval,
                                                    const double* __restrict__ x,
@@ -128,9 +129,9 @@ __global__ void __launch_bounds__(256) k_sell_spmv(int n, const int64_t* __restr
                                                    const double* __restrict__ c) {
     pdl_trigger();
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
-    const int r = g / TPR;
+    const int r = (r0 & ~31) + g / TPR;
     const int part = g % TPR;
-    const bool live = r < n;
+    const bool live = r >= r0 && r < r1;
     RowFrag<TPR, CH> fr;
     int w = 0;
     int64_t base = 0;
@@ -150,31 +151,32 @@ __global__ void __launch_bounds__(256) k_sell_spmv(int n, const int64_t* __restr
     }
     acc = group_sum<TPR>(acc);
     if (live && part == 0) {
-        if (POISSON) acc += c[r] * x[n];
+        if (POISSON) acc += c[r] * x[nl];
         y[r] = (MODE == 0) ? acc : f[r] - acc;
     }
 }
 
-// e[r] += sum_k P[k][r] * ec[Pcol[k][r]]  (interpolate + correct)
+// e[r] += sum_k P[k][r] * ec[Pcol[k][r]] on the rows [r0, r1) of a level with n rows
+// (interpolate + correct); Poisson: the multiplier e[n] += ec[nc] is added by
+// the thread of row n when r1 == n.
 template <bool POISSON, int M>
-__global__ void __launch_bounds__(256) k_interp_correct(int n, int m, const int* __restrict__ pcol,
+__global__ void __launch_bounds__(256) k_interp_correct(int r0, int r1, int n, int m, const int* __restrict__ pcol,
                                                         const double* __restrict__ pval,
                                                         const double* __restrict__ ec,
                                                         double* __restrict__ e, int nc) {
     pdl_trigger();
-    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    const int r = r0 + blockIdx.x * blockDim.x + threadIdx.x;
     int cidx[M];
     double a[M];
 #pragma unroll
     for (int k = 0; k < M; ++k) {
-        const bool ok = r < n && k < m;
+        const bool ok = r < r1 && k < m;
         cidx[k] = ok ? ld_stream_i32(pcol + (int64_t)k * n + r) : -1;
         a[k] = ok ? ld_stream_f64(pval + (int64_t)k * n + r) : 0.0;
     }
     pdl_wait();
-    if (r > n) return;
-    if (r == n) {
-        if (POISSON) e[n] += ec[nc];
+    if (r >= r1) {
+        if (POISSON && r == n && r1 == n) e[n] += ec[nc];
         return;
     }
     double acc = 0.0;

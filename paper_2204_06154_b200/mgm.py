@@ -61,6 +61,8 @@ _SIGS = {
     "mgm_solve_host": ([_vp, _vp, _vp, ctypes.c_double, ctypes.c_int, ctypes.c_int,
                         ctypes.POINTER(Report), _vp], ctypes.c_int),
     "mgm_destroy": ([_vp], ctypes.c_int),
+    "mgm_nccl_unique_id": ([_vp], ctypes.c_int),
+    "mgm_dist_attach": ([_vp, ctypes.c_int, ctypes.c_int, _vp], ctypes.c_int),
     "mgm_last_error": ([_vp, _i64p], ctypes.c_char_p),
     "mgm_num_levels": ([_vp, ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
     "mgm_level_info": ([_vp, ctypes.c_int, _i64p, _i64p, _i64p, ctypes.POINTER(ctypes.c_int),
@@ -274,6 +276,18 @@ def mgm_vcycle_kernel_count(ctx) -> int:
     return c.value
 
 
+def mgm_nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id (rank 0 creates it; broadcast it to the other ranks)."""
+    buf = ctypes.create_string_buffer(128)
+    _check(load_library().mgm_nccl_unique_id(buf), None)
+    return buf.raw
+
+
+def mgm_dist_attach(ctx, rank: int, nranks: int, nccl_id: bytes):
+    buf = ctypes.create_string_buffer(bytes(nccl_id), 128)
+    _check(load_library().mgm_dist_attach(ctx, rank, nranks, buf), ctx)
+
+
 def mgm_trace_read(ctx):
     """Stage stamps of the last V-cycle (MGM_TRACE set at setup): list of (label, ns)."""
     buf = (ctypes.c_uint64 * 256)()
@@ -368,3 +382,15 @@ class MGM:
 
     def level_info(self):
         return [mgm_level_info(self.ctx, j) for j in range(self.p)]
+
+    def attach_dist(self, group=None):
+        """Make vcycle/solve collective over the torch.distributed process group (one rank
+        per GPU; every rank built this MGM from the same cloud).  Rank 0 creates the NCCL id,
+        torch.distributed broadcasts it (marshalling only), libmgm creates the communicator."""
+        import torch.distributed as dist
+
+        rank, nranks = dist.get_rank(group), dist.get_world_size(group)
+        obj = [mgm_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        mgm_dist_attach(self.ctx, rank, nranks, obj[0])
+        self.rank, self.nranks = rank, nranks

@@ -244,3 +244,67 @@ def test_bottom_kernel_equals_kernel_path(name, knobs, monkeypatch):
     ref.close()
     if knobs:
         m2.close()
+
+
+# ------------------------------------------------------------------ multi-GPU path (8(e))
+@pytest.mark.parametrize("name", ["torus20000", "gfd9000"])
+def test_dist_fake_ranks_bitwise(name, monkeypatch):
+    """MGM_DIST_FAKE_RANKS=R splits every level-0..2 operator application into R row pieces
+    (the multi-GPU decomposition) computed on one GPU: the V-cycle and the GMRES solve must be
+    bitwise identical to the unsplit path (each output row is computed by the same arithmetic)."""
+    import torch
+    from paper_2204_06154_b200 import MGM
+
+    P = pair(name)
+    monkeypatch.setenv("MGM_DIST_FAKE_RANKS", "3")
+    monkeypatch.setenv("MGM_DIST_LEVELS", "3")
+    m2 = MGM(P.w.points, P.w.normals, P.w.stencil, P.w.levels)
+    n = len(P.w.points)
+    f = torch.from_numpy(_rand(n, 7)).cuda()
+    u1 = torch.from_numpy(_rand(n, 8)).cuda()
+    u2 = u1.clone()
+    P.gpu.vcycle(f, u1)
+    m2.vcycle(f, u2)
+    assert torch.equal(u1, u2)
+    rhs = torch.from_numpy(P.w.rhs).cuda()
+    x1, r1 = P.gpu.solve(rhs, tol=1e-10)
+    x2, r2 = m2.solve(rhs, tol=1e-10)
+    assert r1.iterations == r2.iterations and torch.equal(x1, x2)
+    m2.close()
+
+
+def test_dist_nccl_single_rank():
+    """The NCCL path (mgm_dist_attach, grouped in-place broadcasts captured in the V-cycle
+    graph, allreduce of the Krylov inner products) with one rank: same solve as without."""
+    import os
+    import socket
+
+    import torch
+    import torch.distributed as dist
+    from paper_2204_06154_b200 import MGM
+
+    P = pair("torus20000")
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        m2 = MGM(P.w.points, P.w.normals, P.w.stencil, P.w.levels)
+        m2.attach_dist()
+        n = len(P.w.points)
+        f = torch.from_numpy(_rand(n, 9)).cuda()
+        u1 = torch.from_numpy(_rand(n, 10)).cuda()
+        u2 = u1.clone()
+        P.gpu.vcycle(f, u1)
+        m2.vcycle(f, u2)
+        assert torch.equal(u1, u2)
+        rhs = torch.from_numpy(P.w.rhs).cuda()
+        x1, r1 = P.gpu.solve(rhs, tol=1e-10)
+        x2, r2 = m2.solve(rhs, tol=1e-10)
+        assert abs(r1.iterations - r2.iterations) <= 1
+        assert (x1 - x2).norm().item() <= 1e-12 * x1.norm().item()
+        m2.close()
+    finally:
+        dist.destroy_process_group()
