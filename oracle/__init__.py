@@ -552,11 +552,21 @@ class Oracle:
             rep.lam = float(u[-1])
         return u, rep
 
+    def bicgstab(self, b, tol=1e-10, maxit=500):
+        """MGM-preconditioned BiCGSTAB on the fine operator, level order."""
+        x, rep = bicgstab(self.apply_A, self.precondition, b, tol=tol, maxit=maxit)
+        if self.poisson:
+            rep.lam = float(x[-1])
+        return x, rep
+
     def solve(self, rhs, tol=1e-10, maxit=500, krylov=1):
-        """Public solve on original-order vectors (mirrors mgm_solve)."""
+        """Public solve on original-order vectors (mirrors mgm_solve: krylov 0 standalone,
+        1 GMRES, 2 BiCGSTAB)."""
         b = self.to_level(rhs)
         if krylov == 1:
             x, rep = self.gmres(b, tol=tol, maxit=maxit)
+        elif krylov == 2:
+            x, rep = self.bicgstab(b, tol=tol, maxit=maxit)
         else:
             x, rep = self.standalone(b, tol=tol, maxit=maxit)
         return self.from_level(x), rep
@@ -624,6 +634,72 @@ def gmres(apply_A, precond, b, tol=1e-10, restart=50, maxit=500, x0=None):
         if stop:
             rep.converged = abs(g[k_done]) / bnorm <= tol
             break
+    rep.iterations = its
+    rep.final_rel_residual = float(np.linalg.norm(b - apply_A(x))) / bnorm
+    return x, rep
+
+
+def bicgstab(apply_A, precond, b, tol=1e-10, maxit=500, x0=None):
+    """Right-preconditioned BiCGSTAB ([Saad] Alg. 7.7 applied to A M, x = M z), in the
+    algorithm's order.  Iterations are counted as preconditioner applications, two per full
+    step; the relative residual ||r||/||b|| is recorded after each half step (||s||)
+    and full step (||r||), and the iteration stops at the first one <= tol.  Breakdown
+    (|rho| or |omega| < 1e-30 relative): restart once from the current iterate with
+    r_hat = r, then report non-convergence (SPEC S:508-516 reading, O18)."""
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    x = np.zeros_like(b) if x0 is None else np.array(x0, dtype=np.float64)
+    rep = Report()
+    bnorm = float(np.linalg.norm(b))
+    if bnorm == 0.0:
+        rep.converged, rep.final_rel_residual = True, 0.0
+        return np.zeros_like(b), rep
+    its = 0
+    restarts = 0
+    r = b - apply_A(x)
+    while True:
+        r_hat = r.copy()
+        rho_prev = alpha = omega = 1.0
+        v = np.zeros_like(b)
+        p = np.zeros_like(b)
+        broke = False
+        while its < maxit:
+            rho = float(r_hat @ r)
+            if abs(rho) < 1e-30 * bnorm * bnorm:
+                broke = True
+                break
+            beta = (rho / rho_prev) * (alpha / omega)
+            p = r + beta * (p - omega * v)
+            p_hat = precond(p)
+            its += 1
+            v = apply_A(p_hat)
+            alpha = rho / float(r_hat @ v)
+            s = r - alpha * v
+            rel_s = float(np.linalg.norm(s)) / bnorm
+            rep.history.append(rel_s)
+            if rel_s <= tol:
+                x = x + alpha * p_hat
+                r = s
+                rep.converged = True
+                break
+            s_hat = precond(s)
+            its += 1
+            t = apply_A(s_hat)
+            tt = float(t @ t)
+            omega = float(t @ s) / tt if tt > 0.0 else 0.0
+            x = x + alpha * p_hat + omega * s_hat
+            r = s - omega * t
+            rel = float(np.linalg.norm(r)) / bnorm
+            rep.history.append(rel)
+            if rel <= tol:
+                rep.converged = True
+                break
+            if abs(omega) < 1e-30:
+                broke = True
+                break
+            rho_prev = rho
+        if rep.converged or its >= maxit or not broke or restarts >= 1:
+            break
+        restarts += 1
     rep.iterations = its
     rep.final_rel_residual = float(np.linalg.norm(b - apply_A(x))) / bnorm
     return x, rep

@@ -197,3 +197,53 @@ def test_gfd_hierarchy_solves():
     x, rep = h.solve(f, tol=1e-10)
     assert rep.converged
     assert rep.final_rel_residual <= 1e-10
+
+
+# ------------------------------------------------------------------ BiCGSTAB
+def test_bicgstab_dense_cases():
+    """A = I converges at the first half step; a diagonally dominant SPD 20x20 system with
+    M = I matches the dense solve; an exact preconditioner converges in one
+    application; iterations count preconditioner applications."""
+    rng = np.random.default_rng(3)
+    b = rng.normal(size=20)
+    x, rep = O.bicgstab(lambda v: v, lambda v: v, b, tol=1e-12)
+    assert rep.converged and rep.iterations == 1 and np.allclose(x, b, atol=1e-14)
+    B = rng.normal(size=(20, 20))
+    A = B @ B.T / 20 + 4 * np.eye(20)
+    x, rep = O.bicgstab(lambda v: A @ v, lambda v: v, b, tol=1e-13)
+    assert rep.converged
+    assert np.linalg.norm(x - np.linalg.solve(A, b)) / np.linalg.norm(x) < 1e-10
+    assert len(rep.history) == rep.iterations              # one residual per application
+    Ai = np.linalg.inv(A)
+    x, rep = O.bicgstab(lambda v: A @ v, lambda v: Ai @ v, b, tol=1e-10)
+    assert rep.converged and rep.iterations == 1
+    x, rep = O.bicgstab(lambda v: A @ v, lambda v: v, np.zeros(20))
+    assert rep.iterations == 0 and not x.any()
+    # non-symmetric, non-normal: still the dense solution
+    C = rng.normal(size=(20, 20)) + 8 * np.eye(20)
+    x, rep = O.bicgstab(lambda v: C @ v, lambda v: v, b, tol=1e-13, maxit=400)
+    assert rep.converged and np.linalg.norm(x - np.linalg.solve(C, b)) / np.linalg.norm(x) < 1e-10
+
+
+def test_mgm_bicgstab_matches_dense_direct_solve_and_gmres():
+    """MGM-BiCGSTAB (shifted and bordered Poisson) reaches the dense direct solution, and
+    needs about as many preconditioner applications as MGM-GMRES."""
+    for problem in (0, 1):
+        h = _hier(problem=problem, N=900, p=3)
+        rng = np.random.default_rng(5)
+        f = rng.uniform(-1, 1, 900)
+        if problem:
+            f -= f.mean()
+        x, rep = h.solve(f, tol=1e-12, krylov=2)
+        xg, repg = h.solve(f, tol=1e-12, krylov=1)
+        assert rep.converged and rep.final_rel_residual <= 1e-11
+        assert rep.iterations <= 2 * repg.iterations + 2
+        A = h.levels[0].L.dense()
+        if problem:
+            n = 900
+            M = np.zeros((n + 1, n + 1)); M[:n, :n] = A; M[:n, n] = 1.0; M[n, :n] = 1.0
+            ref = np.linalg.solve(M, np.concatenate([f[h.perm], [0.0]]))[:n]
+            xr = np.empty(n); xr[h.perm] = ref
+        else:
+            xr = np.empty(900); xr[h.perm] = np.linalg.solve(A, f[h.perm])
+        assert np.linalg.norm(x - xr) / np.linalg.norm(xr) < 1e-9
