@@ -232,6 +232,21 @@ def main():
     barrier()
     e2e_ms = e0.elapsed_time(e1) / args.steps
 
+    # ---- the other solvers of the path on the same system (context, not the metric):
+    # MGM-BiCGSTAB (iterations = preconditioner applications) and standalone MGM
+    others = {}
+    for name, kr in (("bicgstab", 2), ("standalone", 0)):
+        m.solve(rhs, x, tol=1e-10, krylov=kr, maxit=300)
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        _, rk = m.solve(rhs, x, tol=1e-10, krylov=kr, maxit=300)
+        e1.record(st)
+        barrier()
+        others[name] = {"ms": e0.elapsed_time(e1), "iterations": rk.iterations, "converged": bool(rk.converged),
+                        "final_rel_residual": rk.final_rel_residual}
+
     # ---- V-cycle throughput (graph-replayed V-cycles on device vectors)
     bm = mgm_bytes_model(m.ctx)
     f = torch.from_numpy(np.random.default_rng(0).uniform(-1, 1, N)).cuda()
@@ -302,6 +317,7 @@ def main():
                          "unit": "GB/s", "frac": (gs_gbs / hbm) if gs_gbs else None,
                          "traffic": traffic, "alg_bytes_per_launch": alg_per_launch,
                          "launches_timed": tk["launches"], "avg_launch_us": launch_avg_us},
+            "other_solvers": others,
             "e2e": {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": 8 * N,
                     "d2h_bytes_per_step": 8 * N},
             "gpu_launches": per_step * args.steps,

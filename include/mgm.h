@@ -98,7 +98,11 @@ mgm_status mgm_vcycle(mgm_ctx* ctx, const double* f_dev, double* u_dev, void* cu
 
 /* Solve L u = rhs (Poisson: the bordered system) to ||rhs - L x|| / ||rhs|| <= tol.
  * krylov = 1: right-preconditioned GMRES(restart) with one V-cycle from a zero guess as the
- *             preconditioner;  krylov = 0: standalone MGM.
+ *             preconditioner;  krylov = 0: standalone MGM;
+ * krylov = 2: right-preconditioned BiCGSTAB: report.iterations counts
+ *             preconditioner applications (two per step) and report.history holds the
+ *             relative residual after every half step; on a rho/omega breakdown it restarts
+ *             once from the current iterate, then returns converged = 0.
  * rhs_dev, x_dev: device, n_points fp64, original order; x_dev is ignored on entry (zero
  * initial guess) and receives the solution.  rhs = 0 gives x = 0 with 0 iterations.
  * Non-convergence within maxit is NOT an error (converged = 0).  report may be NULL. */

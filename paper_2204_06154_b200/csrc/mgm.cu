@@ -1381,7 +1381,7 @@ mgm_status ensure_krylov(mgm_ctx* ctx) {
     if (ctx->V) return MGM_OK;
     i64 n = ctx->N + (ctx->poisson ? 1 : 0);
     ctx->ld = (n + 31) / 32 * 32;
-    CK(dalloc(&ctx->V, ctx->ld * (ctx->restart + 1)));
+    CK(dalloc(&ctx->V, ctx->ld * std::max(ctx->restart + 1, 8)));  // >= 8 BiCGSTAB vectors
     CK(dalloc(&ctx->w, ctx->ld));
     CK(dalloc(&ctx->xs, ctx->ld));
     CK(dalloc(&ctx->b, ctx->ld));
@@ -1545,6 +1545,112 @@ mgm_status gmres_lib(mgm_ctx* ctx, double tol, int maxit, mgm_report* rep, cudaS
         rep->converged = converged ? 1 : 0;
         rep->final_rel_residual = std::sqrt(ctx->hh[0]) / bnorm;
         rep->lambda = ctx->poisson ? ctx->hh[1] : 0.0;
+    }
+    return MGM_OK;
+}
+
+// Right-preconditioned BiCGSTAB (oracle.bicgstab, O18): Saad's
+// Alg. 7.7 on A M with x = M z; two V-cycles (preconditioner applications, counted as the
+// iterations) and two SpMVs per step; the relative residual after each half step.  b, x
+// in lib order (x = 0 on entry).  Workspace columns of V: r_hat, r, p, v, p_hat, s, t
+// (r_hat/r and s/t adjacent so that one multi-dot gives two inner products).
+mgm_status bicgstab_lib(mgm_ctx* ctx, double tol, int maxit, mgm_report* rep, cudaStream_t st) {
+    const i64 n = ctx->N + (ctx->poisson ? 1 : 0);
+    const i64 ld = ctx->ld;
+    double* rh = ctx->V;
+    double* r = ctx->V + ld;
+    double* p = ctx->V + 2 * ld;
+    double* v = ctx->V + 3 * ld;
+    double* ph = ctx->V + 4 * ld;
+    double* sv = ctx->V + 5 * ld;
+    double* t = ctx->V + 6 * ld;
+    double* dd = ctx->dh + 512;  // device scalars
+    double* hh = ctx->hh;
+    const unsigned nb = RED_BLOCKS, nt = 256;
+    mgm_status s;
+    auto fetch = [&](int k) -> mgm_status {
+        CK(cudaMemcpyAsync(hh, dd, sizeof(double) * k, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        return MGM_OK;
+    };
+    CK(cudaMemsetAsync(ctx->xs, 0, sizeof(double) * n, st));
+    enqueue_dot(ctx, n, ctx->b, ctx->b, dd, st);
+    if ((s = fetch(1))) return s;
+    const double bnorm = std::sqrt(hh[0]);
+    int its = 0, hist_n = 0, restarts = 0;
+    bool converged = false;
+    if (bnorm == 0.0) {
+        if (rep) { rep->iterations = 0; rep->converged = 1; rep->final_rel_residual = 0.0; rep->lambda = 0.0; }
+        return MGM_OK;
+    }
+    auto record = [&](double rel) {
+        if (rep && rep->history && hist_n < rep->history_cap) rep->history[hist_n++] = rel;
+    };
+    CK(cudaMemcpyAsync(r, ctx->b, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));  // r = b - A 0
+    while (true) {
+        CK(cudaMemcpyAsync(rh, r, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemsetAsync(p, 0, sizeof(double) * n, st));
+        CK(cudaMemsetAsync(v, 0, sizeof(double) * n, st));
+        double rho_prev = 1.0, alpha = 1.0, omega = 1.0;
+        enqueue_dot(ctx, n, rh, r, dd, st);
+        if ((s = fetch(1))) return s;
+        double rho = hh[0];
+        bool broke = false;
+        while (its < maxit) {
+            if (std::fabs(rho) < 1e-30 * bnorm * bnorm) { broke = true; break; }
+            const double beta = (rho / rho_prev) * (alpha / omega);
+            k_bicg_p<<<nb, nt, 0, st>>>(n, r, v, p, beta, omega);
+            if ((s = enqueue_precond(ctx, p, st))) return s;  // p_hat = M p
+            ++its;
+            CK(cudaMemcpyAsync(ph, ctx->lv[0].u, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+            enqueue_apply_A(ctx, ph, v, st);
+            enqueue_dot(ctx, n, rh, v, dd, st);
+            if ((s = fetch(1))) return s;
+            alpha = rho / hh[0];
+            k_axpby<<<nb, nt, 0, st>>>(n, 1.0, r, -alpha, v, sv);  // s = r - alpha v
+            enqueue_dot(ctx, n, sv, sv, dd, st);
+            if ((s = fetch(1))) return s;
+            const double rel_s = std::sqrt(hh[0]) / bnorm;
+            record(rel_s);
+            if (!std::isfinite(rel_s)) return fail(ctx, MGM_ERR_BREAKDOWN, "non-finite BiCGSTAB residual", its);
+            if (rel_s <= tol) {
+                k_axpby<<<nb, nt, 0, st>>>(n, 1.0, ctx->xs, alpha, ph, ctx->xs);
+                converged = true;
+                break;
+            }
+            if ((s = enqueue_precond(ctx, sv, st))) return s;  // s_hat = M s (in lv[0].u)
+            ++its;
+            enqueue_apply_A(ctx, ctx->lv[0].u, t, st);
+            enqueue_multidot(ctx, n, sv, ld, 2, t, dd, nullptr, st);  // (s, t), (t, t)
+            if ((s = fetch(2))) return s;
+            omega = hh[1] > 0.0 ? hh[0] / hh[1] : 0.0;
+            k_axpbypz<<<nb, nt, 0, st>>>(n, ctx->xs, alpha, ph, omega, ctx->lv[0].u);
+            k_axpby<<<nb, nt, 0, st>>>(n, 1.0, sv, -omega, t, r);  // r = s - omega t
+            enqueue_multidot(ctx, n, rh, ld, 2, r, dd, nullptr, st);  // (r_hat, r), (r, r)
+            if ((s = fetch(2))) return s;
+            const double rel = std::sqrt(hh[1]) / bnorm;
+            record(rel);
+            if (timing_on(ctx)) timer_collect(ctx);
+            if (rel <= tol) { converged = true; break; }
+            if (std::fabs(omega) < 1e-30) { broke = true; break; }
+            rho_prev = rho;
+            rho = hh[0];
+        }
+        if (converged || its >= maxit || !broke || restarts >= 1) break;
+        ++restarts;  // breakdown: restart once from the current iterate (r is current)
+    }
+    // true residual
+    enqueue_apply_A(ctx, ctx->xs, ctx->w, st);
+    k_axpby<<<nb, nt, 0, st>>>(n, 1.0, ctx->b, -1.0, ctx->w, ctx->w);
+    enqueue_dot(ctx, n, ctx->w, ctx->w, dd, st);
+    CK(cudaMemcpyAsync(hh, dd, sizeof(double), cudaMemcpyDeviceToHost, st));
+    if (ctx->poisson) CK(cudaMemcpyAsync(hh + 1, ctx->xs + ctx->N, sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (rep) {
+        rep->iterations = its;
+        rep->converged = converged ? 1 : 0;
+        rep->final_rel_residual = std::sqrt(hh[0]) / bnorm;
+        rep->lambda = ctx->poisson ? hh[1] : 0.0;
     }
     return MGM_OK;
 }
@@ -1764,7 +1870,7 @@ static mgm_status solve_impl(mgm_ctx* ctx, const double* rhs, double* x, bool ho
                              int krylov, mgm_report* rep, cudaStream_t st) {
     mgm_status s = check_ctx(ctx);
     if (s) return s;
-    if (!rhs || !x || !(tol >= 0) || maxit < 0 || krylov < 0 || krylov > 1) return MGM_ERR_ARG;
+    if (!rhs || !x || !(tol >= 0) || maxit < 0 || krylov < 0 || krylov > 2) return MGM_ERR_ARG;
     if ((s = ensure_krylov(ctx))) return s;
     const i64 N = ctx->N;
     cudaEvent_t e0, e1;
@@ -1778,7 +1884,9 @@ static mgm_status solve_impl(mgm_ctx* ctx, const double* rhs, double* x, bool ho
     }
     k_gather<<<blocks_for(N, 256), 256, 0, st>>>((int)N, ctx->d_lib2orig, rhs_dev, ctx->b);
     if (ctx->poisson) CK(cudaMemsetAsync(ctx->b + N, 0, sizeof(double), st));
-    s = krylov ? gmres_lib(ctx, tol, maxit, rep, st) : standalone_lib(ctx, tol, maxit, rep, st);
+    s = krylov == 1 ? gmres_lib(ctx, tol, maxit, rep, st)
+        : krylov == 2 ? bicgstab_lib(ctx, tol, maxit, rep, st)
+                      : standalone_lib(ctx, tol, maxit, rep, st);
     if (s) return s;
     if (host) {
         k_scatter<<<blocks_for(N, 256), 256, 0, st>>>((int)N, ctx->d_lib2orig, ctx->xs, ctx->w);

@@ -460,6 +460,18 @@ __global__ void k_axpby(int64_t n, double a, const double* __restrict__ x, doubl
          i += (int64_t)gridDim.x * blockDim.x)
         dst[i] = a * x[i] + b * y[i];
 }
+// BiCGSTAB direction update p = r + beta (p - omega v)
+__global__ void k_bicg_p(int64_t n, const double* __restrict__ r, const double* __restrict__ v, double* p,
+                         double beta, double omega) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = r[i] + beta * (p[i] - omega * v[i]);
+}
+// x += a y + b z
+__global__ void k_axpbypz(int64_t n, double* x, double a, const double* __restrict__ y, double b,
+                          const double* __restrict__ z) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        x[i] = x[i] + a * y[i] + b * z[i];
+}
 // h[j] += h2[j]
 __global__ void k_vadd(int k1, double* __restrict__ h, const double* __restrict__ h2) {
     for (int j = threadIdx.x; j < k1; j += blockDim.x) h[j] += h2[j];

@@ -153,8 +153,12 @@ def test_vcycle(name):
 
 
 @pytest.mark.parametrize("name", list(CASES))
-@pytest.mark.parametrize("krylov", [1, 0])
+@pytest.mark.parametrize("krylov", [1, 0, 2])
 def test_solve(name, krylov):
+    """Solves from the same seeded cloud and RHS: GMRES (1), standalone MGM (0) and BiCGSTAB (2).
+    Iteration counts within +-1 (GMRES, standalone, north_star) or +-2 for BiCGSTAB, whose
+    count is preconditioner applications, two per step (P:478), so one step of drift is +-2;
+    solutions to relative 1e-9 when both reach 1e-10."""
     import torch
 
     P = pair(name)
@@ -166,7 +170,7 @@ def test_solve(name, krylov):
     xr, rr = P.ref.solve(rhs, tol=1e-10, krylov=krylov, maxit=300)
     assert rep.converged and rr.converged
     assert rep.final_rel_residual <= 1e-10
-    assert abs(rep.iterations - rr.iterations) <= 1, (rep.iterations, rr.iterations)
+    assert abs(rep.iterations - rr.iterations) <= (2 if krylov == 2 else 1), (rep.iterations, rr.iterations)
     xg = x.cpu().numpy()
     assert np.linalg.norm(xg - xr) / np.linalg.norm(xr) <= 1e-9
     if P.poisson:
