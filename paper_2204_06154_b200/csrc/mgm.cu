@@ -155,17 +155,9 @@ struct mgm_ctx {
     std::vector<std::string> trace_labels;
     int botJ = -1;
     int bot_cluster = 16;
-    int bot_cs_log2 = 4;
     size_t bot_smem = 0;
     int nphases = 0;
-    int bot_ring_off = 0;
     BPhase* d_phases = nullptr;
-    BChunk* d_chunks = nullptr;
-    BTile* d_tiles = nullptr;
-    int* d_ntiles = nullptr;
-    int bot_tiles_off = 0;
-    int bot_stage = 0;
-    char* d_ops = nullptr;
     std::vector<void*> bot_mem;
     i64 vcycle_kernels = 0;
     // multi-GPU (mgm_dist_attach)
@@ -339,14 +331,20 @@ static T* bot_upload(mgm_ctx* ctx, const std::vector<T>& v, bool& ok) {
 
 void setup_bottom(mgm_ctx* ctx, const std::vector<double>& LU, const std::vector<i32>& piv) {
     ctx->botJ = -1;
-    i64 bmax = 4096, blocal = 1024;  // measured best split for cfg3 (profiles/r01_notes.md)
+    i64 bmax = 16384, blocal = 256;  // measured best split for cfg3 (profiles/r01_notes.md)
     if (const char* e = std::getenv("MGM_BOT_MAX")) bmax = std::atoll(e);
     if (const char* e = std::getenv("MGM_BOT_LOCAL")) blocal = std::atoll(e);
     if (ctx->poisson || bmax <= 0 || ctx->p < 2) return;
     const int p = ctx->p;
-    int dev = 0, optin = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    int J = -1;
+    for (int j = 1; j < p; ++j)
+        if (ctx->lv[j].n <= bmax) { J = j; break; }
+    if (J < 0) return;
+    {
+        i64 nph = 2;
+        for (int q = J; q + 1 < p; ++q) nph += (i64)(ctx->lp.nu1 + ctx->lp.nu2) * ctx->lv[q].ncol + 3;
+        if (nph > BOT_MAX_PHASES) return;
+    }
     cudaFuncSetAttribute(k_vcycle_bottom, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     set_max_dyn_smem((const void*)k_vcycle_bottom);
     // cluster size: 16 (non-portable) if the device can co-schedule it, else 8
@@ -355,7 +353,7 @@ void setup_bottom(mgm_ctx* ctx, const std::vector<double>& LU, const std::vector
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(c);
         cfg.blockDim = dim3(BOT_THREADS);
-        cfg.dynamicSmemBytes = 200 * 1024;
+        cfg.dynamicSmemBytes = sizeof(BPhase) * BOT_MAX_PHASES;
         cudaLaunchAttribute at[1];
         at[0].id = cudaLaunchAttributeClusterDimension;
         at[0].val.clusterDim.x = c;
@@ -368,75 +366,43 @@ void setup_bottom(mgm_ctx* ctx, const std::vector<double>& LU, const std::vector
         cudaGetLastError();
     }
     if (!cs) return;
-    const int cs_log2 = cs == 16 ? 4 : 3;
-    const bool pre_b = ctx->lp.smoother == 1, post_b = ctx->lp.smoother == 1 || ctx->lp.smoother == 2;
-    const int nu1 = ctx->lp.nu1, nu2 = ctx->lp.nu2;
-    auto is_local = [&](int j) { return ctx->lv[j].n <= blocal; };
-    auto slice = [&](int j) { return is_local(j) ? ctx->lv[j].n : (ctx->lv[j].n + cs - 1) / cs; };
-    // first level J >= 1 with N_J <= bmax; the layout is checked against shared memory below
-    int J = -1;
-    for (int j = 1; j < p; ++j)
-        if (ctx->lv[j].n <= bmax) { J = j; break; }
-    if (J < 0) return;
-    {
-        i64 nph = 3;
-        for (int q = J; q + 1 < p; ++q) nph += (i64)(nu1 + nu2) * ctx->lv[q].ncol + 3;
-        if (nph > BOT_MAX_PHASES) return;
-    }
-    std::vector<int> ou(p), of(p), ot(p), sh(p);
-    for (int j = J; j < p; ++j) sh[j] = is_local(j) ? 0 : cs_log2;
-    // ---- operator byte stream: per operator and CTA, the rows the CTA owns (r = k mod C,
-    // ascending; local operators: all rows in CTA 0's stream), as 16-byte aligned records
-    // [1/a_rr or 0 | W values | W columns | pad]
-    std::vector<char> bytes;
-    struct Op { int W = 1, rb = 16; bool dist = false; std::vector<size_t> base; i64 n = 0; };
-    auto add_op = [&](const HostCSR& A, bool dist, bool with_dinv) {
-        Op o;
+    bool ok = true;
+    // row-major ELL copy of a lib-order CSR (diagonal first for L, as stored in L_lib)
+    struct Ell { const int* col = nullptr; const double* val = nullptr; int W = 0; };
+    auto make_ell = [&](const HostCSR& A) {
+        Ell E;
         i64 W = 1;
         for (i64 r = 0; r < A.nrows; ++r) W = std::max(W, A.ptr[r + 1] - A.ptr[r]);
-        o.W = (int)W;
-        o.rb = (int)((8 + 12 * W + 15) / 16 * 16);
-        o.dist = dist;
-        o.n = A.nrows;
-        const int nk = dist ? cs : 1;
-        o.base.assign(nk, 0);
-        for (int k = 0; k < nk; ++k) {
-            o.base[k] = bytes.size();
-            for (i64 r = dist ? k : 0; r < A.nrows; r += dist ? cs : 1) {
-                const size_t at = bytes.size();
-                bytes.resize(at + o.rb, 0);
-                char* rec = bytes.data() + at;
-                const i64 a0 = A.ptr[r], len = A.ptr[r + 1] - a0;
-                const double di = (with_dinv && len > 0) ? 1.0 / A.val[a0] : 0.0;
-                std::memcpy(rec, &di, 8);
-                for (i64 t = 0; t < W; ++t) {
-                    const double v = t < len ? A.val[a0 + t] : 0.0;
-                    const int c = t < len ? A.col[a0 + t] : (len > 0 ? A.col[a0] : 0);
-                    std::memcpy(rec + 8 + 8 * t, &v, 8);
-                    std::memcpy(rec + 8 + 8 * W + 4 * t, &c, 4);
-                }
+        std::vector<int> c((size_t)A.nrows * W);
+        std::vector<double> v((size_t)A.nrows * W, 0.0);
+        for (i64 r = 0; r < A.nrows; ++r) {
+            const i64 a0 = A.ptr[r], len = A.ptr[r + 1] - a0;
+            for (i64 k = 0; k < W; ++k) {
+                c[(size_t)r * W + k] = k < len ? A.col[a0 + k] : (len > 0 ? A.col[a0] : 0);
+                v[(size_t)r * W + k] = k < len ? A.val[a0 + k] : 0.0;
             }
         }
-        return o;
+        E.col = bot_upload(ctx, c, ok);
+        E.val = bot_upload(ctx, v, ok);
+        E.W = (int)W;
+        return E;
     };
-    std::vector<Op> OL(p), OP(p), OR(p);
+    std::vector<Ell> EL(p), EP(p), ER(p);
+    std::vector<const double*> dinv(p, nullptr);
     for (int j = J; j + 1 < p; ++j) {
         Level& L = ctx->lv[j];
-        OL[j] = add_op(L.L_lib, !is_local(j), true);
-        OP[j] = add_op(L.P_lib, !is_local(j), false);
-        OR[j] = add_op(transpose(L.P_lib), !is_local(j + 1), false);  // R_j = P_j^T
+        EL[j] = make_ell(L.L_lib);
+        EP[j] = make_ell(L.P_lib);
+        ER[j] = make_ell(transpose(L.P_lib));  // R_j = P_j^T, rows = coarse lib order
+        std::vector<double> di(L.n);
+        for (i64 r = 0; r < L.n; ++r) di[r] = 1.0 / L.L_lib.val[L.L_lib.ptr[r]];
+        dinv[j] = bot_upload(ctx, di, ok);
     }
     // coarsest: explicit inverse from the LU factors (same solution up to rounding, O13)
     const int m = ctx->nc;
-    Op OC;
+    Ell EC;
     {
-        std::vector<double> b(m);
-        HostCSR A;
-        A.nrows = A.ncols = m;
-        A.ptr.resize(m + 1);
-        A.col.resize((size_t)m * m);
-        A.val.resize((size_t)m * m);
-        for (int r = 0; r <= m; ++r) A.ptr[r] = (i64)r * m;
+        std::vector<double> Ainv((size_t)m * m), b(m);
         for (int i = 0; i < m; ++i) {
             std::fill(b.begin(), b.end(), 0.0);
             b[i] = 1.0;
@@ -449,145 +415,82 @@ void setup_bottom(mgm_ctx* ctx, const std::vector<double>& LU, const std::vector
                 for (int c = r + 1; c < m; ++c) acc -= LU[(size_t)c * m + r] * b[c];
                 b[r] = acc / LU[(size_t)r * m + r];
             }
-            for (int r = 0; r < m; ++r) {
-                A.col[(size_t)r * m + i] = i;
-                A.val[(size_t)r * m + i] = b[r];
-            }
+            for (int r = 0; r < m; ++r) Ainv[(size_t)r * m + i] = b[r];
         }
-        OC = add_op(A, !is_local(p - 1), false);
+        std::vector<int> ccol((size_t)m * m);
+        for (int r = 0; r < m; ++r)
+            for (int c = 0; c < m; ++c) ccol[(size_t)r * m + c] = c;
+        EC.col = bot_upload(ctx, ccol, ok);
+        EC.val = bot_upload(ctx, Ainv, ok);
+        EC.W = m;
     }
-    // ---- phases and per-CTA chunks
-    int stage_bytes = BOT_STAGE_BYTES;
-    if (const char* e = std::getenv("MGM_BOT_STAGE")) stage_bytes = std::atoi(e);
-  for (;; stage_bytes /= 2) {  // shrink the ring until the layout fits shared memory
-    if (stage_bytes < 2048) return;
+    if (!ok) return;
+    const int nthr_cl = cs * BOT_THREADS;
     std::vector<BPhase> ph;
-    std::vector<BChunk> ch;
-    auto add = [&](int op, int out_level, i64 r0, i64 r1, const Op* O, int xo, int xs, int yo, int fo, int zo,
-                   double* g) {
+    auto add = [&](int op, bool local, i64 r0, i64 r1, const Ell& E, const double* x, double* y, const double* f,
+                   double* z, const double* di) {
         if (r1 <= r0) return;
         BPhase P{};
         P.op = op;
-        P.local = is_local(out_level) ? 1 : 0;
+        P.local = local ? 1 : 0;
         P.r0 = (int)r0;
         P.r1 = (int)r1;
-        P.W = O ? O->W : 1;
-        P.rb = O ? O->rb : 16;
-        P.tile_rows = std::max(1, stage_bytes / P.rb);
-        P.xo = xo; P.xs = xs;
-        P.yo = yo; P.ys = sh[out_level];
-        P.fo = fo; P.zo = zo;
-        P.g = g;
-        // per-CTA rows; tpr: the largest power of two (<= 32) with one pass over a tile
-        i64 maxrows = 0;
-        for (int k = 0; k < cs; ++k) {
-            BChunk c{};
-            if (P.local) {
-                if (k == 0) {
-                    c.nrows = (int)(r1 - r0);
-                    if (O) c.off = O->base[0] + (size_t)r0 * O->rb;
-                }
-            } else {
-                const i64 first = r0 + ((k - r0) % cs + cs) % cs;  // first row >= r0 with r = k (mod C)
-                c.nrows = first < r1 ? (int)((r1 - first + cs - 1) / cs) : 0;
-                if (O) c.off = O->base[k] + (size_t)(first / cs) * O->rb;
+        P.W = std::max(E.W, 1);
+        const i64 nthr = local ? BOT_THREADS : nthr_cl;
+        int best = -1;
+        if (op == BP_ZERO) {
+            best = 0;
+        } else {
+            int smallest_valid = -1;
+            for (int lg = 5; lg >= 0; --lg) {  // largest tpr that covers W and fits one pass
+                const int tpr = 1 << lg;
+                if (bot_ch(tpr) * tpr < P.W) continue;
+                smallest_valid = lg;
+                if (best < 0 && (r1 - r0) * tpr <= nthr) best = lg;
             }
-            maxrows = std::max<i64>(maxrows, c.nrows);
-            ch.push_back(c);
+            if (best < 0) best = smallest_valid >= 0 ? smallest_valid : 5;
         }
-        const i64 tile = std::min<i64>(maxrows, P.tile_rows);
-        int lg = 5;
-        while (lg > 0 && tile * (1 << lg) > BOT_CONSUMERS) --lg;
-        P.tpr_log2 = lg;
+        P.tpr_log2 = best;
+        P.col = E.col;
+        P.val = E.val;
+        P.x = x; P.y = y; P.f = f; P.z = z; P.dinv = di;
         ph.push_back(P);
     };
+    auto is_local = [&](int j) { return ctx->lv[j].n <= blocal; };
+    const bool pre_b = ctx->lp.smoother == 1, post_b = ctx->lp.smoother == 1 || ctx->lp.smoother == 2;
     auto sweep = [&](int j, bool backward) {
         Level& L = ctx->lv[j];
         for (int q = 0; q < L.ncol; ++q) {
             const int c = backward ? L.ncol - 1 - q : q;
-            add(BP_GS, j, L.coff[c], L.coff[c + 1], &OL[j], ou[j], sh[j], ou[j], of[j], 0, nullptr);
+            add(BP_GS, is_local(j), L.coff[c], L.coff[c + 1], EL[j], L.u, L.u, L.f, nullptr, dinv[j]);
         }
     };
-    // vector offsets are patched once the table sizes are known: code -(1 + 3 j + {0:u,1:f,2:t})
-    for (int j = J; j < p; ++j) {
-        ou[j] = -(1 + 3 * j);
-        of[j] = -(2 + 3 * j);
-        ot[j] = -(3 + 3 * j);
-    }
-    add(BP_LOAD, J, 0, ctx->lv[J].n, nullptr, 0, 0, of[J], 0, ou[J], ctx->lv[J].f);  // f_J <- global, u_J = 0
+    const Ell none;
+    if (J < p - 1) add(BP_ZERO, is_local(J), 0, ctx->lv[J].n, none, nullptr, ctx->lv[J].u, nullptr, nullptr, nullptr);
     for (int j = J; j + 1 < p; ++j) {  // Alg. 3 lines 6-9 (and 4-5 for j = J)
         Level& L = ctx->lv[j];
         Level& Ln = ctx->lv[j + 1];
-        for (int s2 = 0; s2 < nu1; ++s2) sweep(j, pre_b);
-        add(BP_RES, j, 0, L.n, &OL[j], ou[j], sh[j], ot[j], of[j], 0, nullptr);
-        add(BP_MVZ, j + 1, 0, Ln.n, &OR[j], ot[j], sh[j], of[j + 1], 0, ou[j + 1], nullptr);
+        for (int s2 = 0; s2 < ctx->lp.nu1; ++s2) sweep(j, pre_b);
+        add(BP_RES, is_local(j), 0, L.n, EL[j], L.u, L.t, L.f, nullptr, nullptr);
+        add(BP_MVZ, is_local(j), 0, Ln.n, ER[j], L.t, Ln.f, nullptr, Ln.u, nullptr);
     }
-    add(BP_MV, p - 1, 0, m, &OC, of[p - 1], sh[p - 1], ou[p - 1], 0, 0, nullptr);  // line 10
+    {  // line 10
+        Level& C = ctx->lv[p - 1];
+        add(BP_MV, is_local(p - 1), 0, m, EC, C.f, C.u, nullptr, nullptr, nullptr);
+    }
     for (int j = p - 2; j >= J; --j) {  // lines 11-14
-        add(BP_ADD, j, 0, ctx->lv[j].n, &OP[j], ou[j + 1], sh[j + 1], ou[j], 0, 0, nullptr);
-        for (int s2 = 0; s2 < nu2; ++s2) sweep(j, post_b);
+        Level& L = ctx->lv[j];
+        Level& Ln = ctx->lv[j + 1];
+        add(BP_ADD, is_local(j), 0, L.n, EP[j], Ln.u, L.u, nullptr, nullptr, nullptr);
+        for (int s2 = 0; s2 < ctx->lp.nu2; ++s2) sweep(j, post_b);
     }
-    add(BP_STORE, J, 0, ctx->lv[J].n, nullptr, ou[J], sh[J], 0, 0, 0, ctx->lv[J].u);  // u_J -> global
     if ((int)ph.size() > BOT_MAX_PHASES) return;
-    // ---- per-CTA tile lists (consumption order) and the shared-memory layout
-    std::vector<std::vector<BTile>> tl(cs);
-    for (size_t q = 0; q < ph.size(); ++q) {
-        const BPhase& P = ph[q];
-        if (P.op == BP_LOAD || P.op == BP_STORE) continue;
-        for (int k = 0; k < cs; ++k) {
-            const BChunk& C = ch[q * cs + k];
-            for (int i0 = 0; i0 < C.nrows; i0 += P.tile_rows) {
-                BTile T{};
-                T.off = C.off + (unsigned long long)i0 * P.rb;
-                T.bytes = (unsigned)(std::min(P.tile_rows, C.nrows - i0) * P.rb);
-                tl[k].push_back(T);
-            }
-        }
-    }
-    size_t maxT = 1;
-    for (auto& v : tl) maxT = std::max(maxT, v.size());
-    const size_t tables = ph.size() * (sizeof(BPhase) + sizeof(BChunk));
-    const size_t tiles_off = (tables + 15) / 16 * 16;
-    const size_t ring_off = (tiles_off + maxT * sizeof(BTile) + 64 + 127) / 128 * 128;
-    size_t off = ring_off + (size_t)BOT_STAGES * stage_bytes;
-    std::vector<int> vo(3 * p, 0);
-    for (int j = J; j < p; ++j)
-        for (int w = 0; w < 3; ++w) {
-            vo[3 * j + w] = (int)off;
-            off += (size_t)slice(j) * sizeof(double);
-        }
-    if (off + 1024 > (size_t)optin) continue;  // does not fit: smaller ring stages
-    auto patch = [&](int& o) { if (o < 0) o = vo[-o - 1]; };
-    for (auto& P : ph) {
-        patch(P.xo);
-        patch(P.yo);
-        patch(P.fo);
-        patch(P.zo);
-    }
-    std::vector<BTile> tflat(maxT * cs);
-    std::vector<int> nt(cs + 1);
-    for (int k = 0; k < cs; ++k) {
-        std::copy(tl[k].begin(), tl[k].end(), tflat.begin() + k * maxT);
-        nt[k] = (int)tl[k].size();
-    }
-    nt[cs] = (int)maxT;
-    bool ok = true;
     ctx->d_phases = bot_upload(ctx, ph, ok);
-    ctx->d_chunks = bot_upload(ctx, ch, ok);
-    ctx->d_tiles = bot_upload(ctx, tflat, ok);
-    ctx->d_ntiles = bot_upload(ctx, nt, ok);
-    ctx->d_ops = bot_upload(ctx, bytes, ok);
     if (!ok) return;
     ctx->nphases = (int)ph.size();
     ctx->bot_cluster = cs;
-    ctx->bot_cs_log2 = cs_log2;
-    ctx->bot_tiles_off = (int)tiles_off;
-    ctx->bot_ring_off = (int)ring_off;
-    ctx->bot_smem = off;
-    ctx->bot_stage = stage_bytes;
+    ctx->bot_smem = sizeof(BPhase) * ph.size();
     ctx->botJ = J;
-    return;
-  }
 }
 
 // Build the CTA-dependency sweep (sweep_kernel.cuh) for level j: B Morton-block owners,
@@ -1318,11 +1221,9 @@ void enqueue_vcycle(mgm_ctx* ctx, cudaStream_t st) {
         cfg.attrs = at;
         cfg.numAttrs = g_use_pdl ? 2 : 1;
         cfg.dynamicSmemBytes = ctx->bot_smem;
-        note_launch(cudaLaunchKernelEx(&cfg, k_vcycle_bottom, (const BPhase*)ctx->d_phases, (const BChunk*)ctx->d_chunks,
-                                       (const BTile*)ctx->d_tiles, (const int*)ctx->d_ntiles, (const char*)ctx->d_ops,
-                                       ctx->nphases, ctx->bot_cs_log2, ctx->bot_tiles_off, ctx->bot_ring_off, ctx->bot_stage,
+        note_launch(cudaLaunchKernelEx(&cfg, k_vcycle_bottom, (const BPhase*)ctx->d_phases, ctx->nphases,
                                        ctx->d_trace ? ctx->d_trace + 256 : (unsigned long long*)nullptr),
-                    ctx->bot_cluster, BOT_THREADS, cfg.dynamicSmemBytes);
+                    ctx->bot_cluster, BOT_THREADS, ctx->bot_smem);
         ctx->vcycle_kernels++;
     } else {
         enqueue_coarse(ctx, lv[p - 1].f, lv[p - 1].u, st);                 // line 10
@@ -2079,10 +1980,6 @@ mgm_status mgm_bottom_trace_read(const mgm_ctx* ctx, uint64_t* stamps_ns, int ca
     if (*n == 0) return MGM_OK;
     if (cap < *n) return MGM_ERR_ARG;
     if (cudaMemcpy(stamps_ns, ctx->d_trace + 256, sizeof(uint64_t) * *n, cudaMemcpyDeviceToHost) != cudaSuccess)
-        return MGM_ERR_CUDA;
-    if (cap >= 5 * *n &&  // clock64 sub-stamps follow (4 per phase), see bottom_kernel.cuh
-        cudaMemcpy(stamps_ns + *n, ctx->d_trace + 256 + BOT_MAX_PHASES, sizeof(uint64_t) * 4 * *n,
-                   cudaMemcpyDeviceToHost) != cudaSuccess)
         return MGM_ERR_CUDA;
     if (meta) {
         std::vector<BPhase> ph(*n);

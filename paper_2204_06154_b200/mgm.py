@@ -305,8 +305,7 @@ def mgm_bottom_trace_read(ctx):
     n = ctypes.c_int()
     _check(load_library().mgm_bottom_trace_read(ctx, buf, 8192, ctypes.byref(n), meta.ctypes.data_as(_i32p)), ctx)
     k = n.value
-    sub = np.array(buf[k:5 * k], dtype=np.int64).reshape(k, 4) if k else np.zeros((0, 4), np.int64)
-    return np.array(buf[:k], dtype=np.uint64), meta[:k], sub
+    return np.array(buf[:k], dtype=np.uint64), meta[:k]
 
 
 def mgm_host_morton(points):

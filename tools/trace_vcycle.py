@@ -49,22 +49,16 @@ if os.environ.get("BOTTOM_PHASES"):
     for _ in range(10):
         m.vcycle(f, u)
         torch.cuda.synchronize()
-        st, meta, sub = mgm_bottom_trace_read(m.ctx)
+        st, meta = mgm_bottom_trace_read(m.ctx)
         d = np.diff(st.astype(np.float64)) / 1e3
         acc = d if acc is None else acc + d
     acc /= 10
-    names = ["LOAD", "GS", "RES", "MVZ", "ADD", "MV", "STORE"]
+    names = ["ZERO", "GS", "RES", "MVZ", "ADD", "MV"]
     print("bottom phases:", len(st), "sum of phase gaps", acc.sum(), "us")
     rows = {}
     for q, dt in enumerate(acc):
         k = (names[meta[q, 0]], int(meta[q, 1]), int(meta[q, 2]) if meta[q, 0] != 1 else -1, int(meta[q, 3]))
         rows.setdefault(k, []).append(dt)
-    subd = {}
-    for q in range(len(st) - 1):
-        k = (names[meta[q, 0]], int(meta[q, 1]), int(meta[q, 2]) if meta[q, 0] != 1 else -1, int(meta[q, 3]))
-        subd.setdefault(k, []).append(np.diff(sub[q]))
     for k, v in sorted(rows.items(), key=lambda kv: -sum(kv[1])):
-        sd = np.median(subd.get(k, [np.zeros(3)]), axis=0)
-        print(f"  {k}: n={len(v)} mean {np.mean(v):.2f} us total {np.sum(v):.1f} us | median cycles: tile wait "
-              f"{sd[0]:.0f}, compute {sd[1]:.0f}, barrier {sd[2]:.0f}")
+        print(f"  {k}: n={len(v)} mean {np.mean(v):.2f} us total {np.sum(v):.1f} us")
     m.close()
