@@ -312,3 +312,85 @@ def test_dist_nccl_single_rank():
         m2.close()
     finally:
         dist.destroy_process_group()
+
+
+# ------------------------------------------------------------------ degenerate hierarchies
+@pytest.mark.parametrize("levels", [
+    dict(num_levels=1),                              # p = 1: the V-cycle is the direct solve
+    dict(num_levels=2),                              # p = 2: the two-grid cycle (Alg. 1)
+    dict(num_levels=3, nu1=0, nu2=1),                # post-smoothing only
+    dict(num_levels=3, nu1=2, nu2=0),                # pre-smoothing only
+    dict(num_levels=4, smoother=1),                  # backward colour order
+    dict(num_levels=4, smoother=2),                  # forward pre, backward post
+])
+def test_degenerate_hierarchies(levels):
+    """Edge cases of Alg. 3 (O14): V-cycle to 1e-12 and GMRES within +-1 iteration
+    and 1e-9 of the oracle on a small ragged cloud (N = 1500, not a multiple of 4 or 32)."""
+    import torch
+    import oracle as O
+    from paper_2204_06154_b200 import MGM
+
+    w = MI.make_workload(1, n=1500)
+    lv = dict(w.levels, nu1=1, nu2=1, smoother=0)
+    lv.update(levels)
+    g = MGM(w.points, w.normals, w.stencil, lv)
+    o = O.Oracle(w.points, w.normals, w.stencil, lv)
+    n = len(w.points)
+    f, u0 = _rand(n, 41), _rand(n, 42)
+    uf = torch.from_numpy(u0.copy()).cuda()
+    g.vcycle(torch.from_numpy(f).cuda(), uf)
+    assert relmax(uf.cpu().numpy(), o.vcycle(f, u0)) <= 1e-12
+    x, rep = g.solve(torch.from_numpy(w.rhs).cuda(), tol=1e-10)
+    xr, rr = o.solve(w.rhs, tol=1e-10)
+    assert rep.converged and rr.converged
+    assert abs(rep.iterations - rr.iterations) <= 1
+    assert np.linalg.norm(x.cpu().numpy() - xr) / np.linalg.norm(xr) <= 1e-9
+    g.close()
+
+
+# ------------------------------------------------------------------ BASELINE full size (cfg3)
+def test_full_size_cfg3_sampled():
+    """BASELINE configs[2] at its full size (torus, N = 1,048,576, 8 levels) in the launch
+    configuration bench.py times.  The oracle cannot build this hierarchy in seconds, so:
+    (1) sampled rows -- kNN stencils (O2) and RBF-FD weights (O4) of 256 seeded rows computed
+    by the oracle from the raw cloud must equal the GPU's (stencils exactly, weights to
+    1e-10 per row); (2) the sampled rows of the GPU solution's residual b - L x, evaluated with
+    the ORACLE's weights, are bounded by the reported 2-norm residual (<= 1e-10 ||b||);
+    (3) properties of the V-cycle that hold at any size: M(0) = 0 and linearity to 1e-12."""
+    import torch
+    import oracle as O
+    from paper_2204_06154_b200 import MGM, mgm_export_weights
+
+    w = MI.make_workload(3)
+    n, ns = len(w.points), w.stencil["stencil_n"]
+    g = MGM(w.points, w.normals, w.stencil, w.levels)
+    assert g.p == 8
+    rows = np.sort(np.random.default_rng(123).choice(n, 256, replace=False))
+    sten = O.knn(w.points, w.points[rows], ns)
+    # the oracle's weight routine takes stencil row i centred at point i: put the sampled
+    # centres first and shift the neighbour indices
+    k0 = len(rows)
+    pts2 = np.concatenate([w.points[rows], w.points])
+    nrm2 = np.concatenate([w.normals[rows], w.normals])
+    wo = O.rbffd_weights(pts2, nrm2, sten + k0, w.stencil["poly_degree"], w.stencil["phs_k"])
+    wg, sg = mgm_export_weights(g.ctx, n, ns)
+    assert np.array_equal(sg[rows], sten)
+    assert (np.abs(wg[rows] - wo) / np.abs(wo).max(1, keepdims=True)).max() <= 1e-10
+    b = torch.from_numpy(w.rhs).cuda()
+    x, rep = g.solve(b, tol=1e-10)
+    assert rep.converged and rep.final_rel_residual <= 1e-10
+    xh = x.cpu().numpy()
+    mu = w.stencil["mu"]
+    Lx = xh[rows] - mu * (wo * xh[sten]).sum(1)          # L = I - mu D (O6), oracle weights
+    r = w.rhs[rows] - Lx
+    assert np.abs(r).max() <= 1.01e-10 * np.linalg.norm(w.rhs)
+    z = torch.zeros(n, dtype=torch.float64, device="cuda")
+    g.vcycle(torch.zeros_like(z), z)
+    assert not z.any()
+    a, c = torch.from_numpy(_rand(n, 5)).cuda(), torch.from_numpy(_rand(n, 6)).cuda()
+    ua, uc, us = torch.zeros_like(a), torch.zeros_like(a), torch.zeros_like(a)
+    g.vcycle(a, ua)
+    g.vcycle(c, uc)
+    g.vcycle(a + 2 * c, us)
+    assert ((us - (ua + 2 * uc)).abs().max() / us.abs().max()).item() <= 1e-12
+    g.close()
