@@ -85,7 +85,9 @@ struct Level {
     i32* scol = nullptr;
     double* sval = nullptr;
     i64 sell_stored = 0, nnz = 0;
-    int tpr = 1, rtpr = 1;  // threads per row for L_j and R_j kernels
+    int tpr = 1, rtpr = 1;  // threads per row for L_j (colour sweeps) and R_j kernels
+    int stpr = 1;           // threads per row for full-level SpMV / residual on L_j
+    int gs_block = 256;     // threads per block of the colour kernels
     // interpolation P_j (ELL width pm, slot-major) and restriction R_j (SELL-32, next level rows)
     int pm = 0;
     i32* pcol = nullptr;
@@ -349,7 +351,9 @@ void setup_bottom(mgm_ctx* ctx, const std::vector<double>& LU, const std::vector
     set_max_dyn_smem((const void*)k_vcycle_bottom);
     // cluster size: 16 (non-portable) if the device can co-schedule it, else 8
     int cs = 0;
-    for (int c : {16, 8}) {
+    std::vector<int> sizes = {16, 8};
+    if (const char* e = std::getenv("MGM_BOT_CS")) sizes = {std::atoi(e)};  // tuning experiment
+    for (int c : sizes) {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(c);
         cfg.blockDim = dim3(BOT_THREADS);
@@ -795,7 +799,31 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
         L.sell_stored = (i64)sval.size();
         {
             double wavg = (double)L.sell_stored / (double)std::max<i64>(1, (n + 31) / 32 * 32);
+            // threads per row: colour sweeps (short kernels) want more threads per row, the
+            // full-level SpMV / residual fewer (measured, profiles/r01_notes.md)
             L.tpr = wavg <= 12 ? 1 : (wavg <= 40 ? 2 : 4);
+            // small colours: more threads per row (shorter per-thread chains; L2 of cfg3:
+            // 112.8 -> 87.6 us per sweep with 8 instead of 4)
+            if (L.ncol > 0 && (double)n / L.ncol * L.tpr < 16384.0 && L.tpr < 8) L.tpr *= 2;
+            L.stpr = 1;
+            // colours with fewer threads than one 256-thread block per SM run 64-thread blocks
+            // (cfg3 L1+L2: -19 us per V-cycle, profiles/r01_notes.md)
+            {
+                int b = 64;
+                if (const char* e = std::getenv("MGM_GS_BLOCK_SMALL")) b = std::atoi(e);
+                if ((b == 64 || b == 128 || b == 256) && L.ncol > 0 && (double)n / L.ncol * L.tpr < 148.0 * 256)
+                    L.gs_block = b;
+                if (const char* e = std::getenv("MGM_GS_BLOCK_L0"))
+                    if (j == 0) L.gs_block = std::atoi(e);
+            }
+            if (const char* e = std::getenv(j == 0 ? "MGM_L0_TPR" : "MGM_LJ_TPR")) {  // tuning experiments
+                const int t = std::atoi(e);
+                if (t == 1 || t == 2 || t == 4 || t == 8) L.tpr = t;
+            }
+            if (const char* e = std::getenv(j == 0 ? "MGM_L0_STPR" : "MGM_LJ_STPR")) {
+                const int t = std::atoi(e);
+                if (t == 1 || t == 2 || t == 4 || t == 8) L.stpr = t;
+            }
         }
         if ((s = upload(ctx, &L.sptr, sptr)) || (s = upload(ctx, &L.scol, scol)) || (s = upload(ctx, &L.sval, sval))) return s;
         if (j + 1 < p) {
@@ -954,18 +982,23 @@ double sweep_colour_bytes(const Level& L, i64 rows) {
 constexpr int CHUNK = 16;
 template <bool P, int TPR>
 void gs_launch_t(bool pdl, int r0, int r1, int span, const Level& L, cudaStream_t st) {
-    launch(pdl, k_gs_colour<P, TPR, CHUNK>, blocks_for((i64)span * TPR, 256), 256, 0, st, r0, r1, L.sptr, L.scol,
+    // block size: colours too small to give every SM a 256-thread block use smaller blocks
+    // (spreads the gathers over more SMs)
+    const int bs = L.gs_block;
+    launch(pdl, k_gs_colour<P, TPR, CHUNK>, blocks_for((i64)span * TPR, bs), bs, 0, st, r0, r1, L.sptr, L.scol,
            L.sval, L.f, L.u, L.c, (int)L.n);
 }
 void launch_gs(bool pdl, bool poisson, int tpr, int r0, int r1, int span, const Level& L, cudaStream_t st) {
     if (poisson) {
         if (tpr == 1) gs_launch_t<true, 1>(pdl, r0, r1, span, L, st);
         else if (tpr == 2) gs_launch_t<true, 2>(pdl, r0, r1, span, L, st);
-        else gs_launch_t<true, 4>(pdl, r0, r1, span, L, st);
+        else if (tpr == 4) gs_launch_t<true, 4>(pdl, r0, r1, span, L, st);
+        else gs_launch_t<true, 8>(pdl, r0, r1, span, L, st);
     } else {
         if (tpr == 1) gs_launch_t<false, 1>(pdl, r0, r1, span, L, st);
         else if (tpr == 2) gs_launch_t<false, 2>(pdl, r0, r1, span, L, st);
-        else gs_launch_t<false, 4>(pdl, r0, r1, span, L, st);
+        else if (tpr == 4) gs_launch_t<false, 4>(pdl, r0, r1, span, L, st);
+        else gs_launch_t<false, 8>(pdl, r0, r1, span, L, st);
     }
 }
 template <int MODE, bool P, int TPR>
@@ -979,7 +1012,8 @@ void spmv_launch_p(bool pdl, int tpr, i64 r0, i64 r1, i64 nl, const i64* sptr, c
                    const double* x, const double* f, double* y, const double* c, cudaStream_t st) {
     if (tpr == 1) spmv_launch_t<MODE, P, 1>(pdl, r0, r1, nl, sptr, scol, sval, x, f, y, c, st);
     else if (tpr == 2) spmv_launch_t<MODE, P, 2>(pdl, r0, r1, nl, sptr, scol, sval, x, f, y, c, st);
-    else spmv_launch_t<MODE, P, 4>(pdl, r0, r1, nl, sptr, scol, sval, x, f, y, c, st);
+    else if (tpr == 4) spmv_launch_t<MODE, P, 4>(pdl, r0, r1, nl, sptr, scol, sval, x, f, y, c, st);
+    else spmv_launch_t<MODE, P, 8>(pdl, r0, r1, nl, sptr, scol, sval, x, f, y, c, st);
 }
 // rows [r0, r1) of a SELL operator whose level has nl rows
 void launch_spmv(bool pdl, int mode, bool poisson, int tpr, i64 r0, i64 r1, i64 nl, const i64* sptr,
@@ -1095,7 +1129,7 @@ void enqueue_spmv(mgm_ctx* ctx, int j, const double* x, double* y, cudaStream_t 
     Level& L = ctx->lv[j];
     if (j == 0) timer_begin(ctx, 1, st);
     for_my_pieces(ctx, j, 0, L.n, [&](i64 a, i64 b) {
-        launch_spmv(ctx->pdl, 0, ctx->poisson, L.tpr, a, b, L.n, L.sptr, L.scol, L.sval, x, nullptr, y, L.c, st);
+        launch_spmv(ctx->pdl, 0, ctx->poisson, L.stpr, a, b, L.n, L.sptr, L.scol, L.sval, x, nullptr, y, L.c, st);
     });
     dist_exchange(ctx, j, y, 0, L.n, st);
     if (j == 0) timer_end(ctx, 1, st, 12.0 * L.nnz + 16.0 * L.n);
@@ -1106,7 +1140,7 @@ void enqueue_spmv(mgm_ctx* ctx, int j, const double* x, double* y, cudaStream_t 
 void enqueue_residual(mgm_ctx* ctx, int j, const double* f, const double* u, double* t, cudaStream_t st) {
     Level& L = ctx->lv[j];
     for_my_pieces(ctx, j, 0, L.n, [&](i64 a, i64 b) {
-        launch_spmv(ctx->pdl, 1, ctx->poisson, L.tpr, a, b, L.n, L.sptr, L.scol, L.sval, u, f, t, L.c, st);
+        launch_spmv(ctx->pdl, 1, ctx->poisson, L.stpr, a, b, L.n, L.sptr, L.scol, L.sval, u, f, t, L.c, st);
         ctx->vcycle_kernels++;
     });
     dist_exchange(ctx, j, t, 0, L.n, st);
