@@ -988,7 +988,32 @@ void gs_launch_t(bool pdl, int r0, int r1, int span, const Level& L, cudaStream_
     launch(pdl, k_gs_colour<P, TPR, CHUNK>, blocks_for((i64)span * TPR, bs), bs, 0, st, r0, r1, L.sptr, L.scol,
            L.sval, L.f, L.u, L.c, (int)L.n);
 }
+// Threads one wave of colour kernels can hold (all SMs, register-limited occupancy).
+static i64 gs_wave_threads(int tpr, int block) {
+    static i64 cache[4][4] = {};
+    const int ti = tpr == 1 ? 0 : tpr == 2 ? 1 : tpr == 4 ? 2 : 3;
+    const int bi = block == 64 ? 0 : block == 128 ? 1 : block == 256 ? 2 : 3;
+    if (cache[ti][bi]) return cache[ti][bi];
+    int dev = 0, nsm = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const void* k = tpr == 1 ? (const void*)k_gs_colour<false, 1, CHUNK>
+                  : tpr == 2 ? (const void*)k_gs_colour<false, 2, CHUNK>
+                  : tpr == 4 ? (const void*)k_gs_colour<false, 4, CHUNK>
+                             : (const void*)k_gs_colour<false, 8, CHUNK>;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, block, 0) != cudaSuccess) {
+        cudaGetLastError();
+        per = 1;
+    }
+    return cache[ti][bi] = (i64)per * nsm * block;
+}
+
 void launch_gs(bool pdl, bool poisson, int tpr, int r0, int r1, int span, const Level& L, cudaStream_t st) {
+    // a colour slightly larger than one wave would run a nearly empty second wave (ncu:
+    // "1.04 waves" on the largest level-0 colours): halve the threads per row instead
+    while (tpr > 1 && (i64)span * tpr > gs_wave_threads(tpr, L.gs_block) &&
+           (i64)span * (tpr / 2) <= gs_wave_threads(tpr / 2, L.gs_block))
+        tpr /= 2;
     if (poisson) {
         if (tpr == 1) gs_launch_t<true, 1>(pdl, r0, r1, span, L, st);
         else if (tpr == 2) gs_launch_t<true, 2>(pdl, r0, r1, span, L, st);
