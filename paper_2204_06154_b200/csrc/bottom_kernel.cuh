@@ -6,35 +6,35 @@
 // kernel boundary (~0.7-1 us with PDL inside a graph, measured: tools/micro/sync_costs.cu)
 // plus the kernel's own dependent load chain (~2 us) dwarfs its work.  Here the barrier
 // between two colours is barrier.cluster (~0.25 us measured) or, for levels small enough
-// for one CTA ("local" phases, run by CTA 0 only), __syncthreads (~0.03 us).  Each thread
-// prefetches the immutable operator row of its NEXT phase (values, columns, 1/a_rr) into
-// registers between the barrier's arrive and wait, so that after a barrier only the
-// vector gathers (L2 hits) remain.
+// for one CTA ("local" phases, run by CTA 0 only), __syncthreads (~0.03 us).
 //
-// Vector loads are plain (L1-cacheable): barrier.cluster.wait.acquire invalidates L1
-// (CCTL.IVALL in the SASS) and local phases stay inside one SM, so L1 never serves a stale
-// value; L1 hits matter on the small levels, where neighbouring rows share gathers.
+// The gathered vectors -- the iterates u_J .. u_p -- are REPLICATED in every CTA's shared
+// memory (21.8k doubles = 175 KB for cfg3's levels 3..7): every gather is a local
+// ld.shared (~30 cycles instead of an L2 round trip of ~300-600 cycles with a 32-byte sector
+// per 8-byte value), and every update is stored into all C copies with st.shared::cluster
+// (fire-and-forget; the barrier's release orders them).  The right-hand sides f_j and the
+// residuals t_j stay in HBM/L2: f_j[row] is read once per row (prefetched with the
+// operator row when the previous phase did not write it), t_j is written by the residual
+// phase and gathered only by the restriction.  u_J is stored back to HBM at the end for
+// the per-kernel up-path.  Each thread prefetches the immutable operator row of its NEXT
+// phase (values, columns, 1/a_rr) into registers between the barrier's arrive and wait.
 //
-// Design history (profiles/r01_notes.md): vectors in distributed shared memory and a
-// TMA-fed shared-memory operator ring were both measured SLOWER on the cluster levels
-// (ld.shared::cluster gathers and the ring's tile waits cost more than L2-resident global
-// vectors with a register prefetch), so this is the L2 design.
-//
-// Layout (built by setup_bottom): every operator row-major ELL in global memory, row r at
-// val[r*W .. r*W+W), padded with (col = own first column, val = 0), L_j with its diagonal
-// first; so the address of a thread's entries is known without a row-pointer load.  Loads
-// of the bottom operators carry an L2 evict_last policy (the upper levels stream with
-// evict_first).  GS phases multiply by a stored 1/a_rr instead of dividing (the same
-// update up to one rounding).
+// Operators (built by setup_bottom): row-major ELL in global memory, row r at
+// val[r*W .. r*W+W), padded with (own first column, 0.0), L_j with its diagonal first; so
+// the address of a thread's entries is known without a row-pointer load.  Loads carry an
+// L2 evict_last policy (the upper levels stream with evict_first).  GS phases multiply by a
+// stored 1/a_rr instead of dividing (the same update up to one rounding).
 //
 // A phase applies one operator to the rows [r0, r1) with one of these epilogues
-// (acc = sum_k val_k x[col_k]):
-//   BP_ZERO  y[r] = 0                                  (e_J = 0, Alg. 3 line 7)
-//   BP_GS    y[r] = x[r] + (f[r] - acc) * dinv[r]      (one colour of the sweep; y = x = u)
-//   BP_RES   y[r] = f[r] - acc                         (t_j = r_j - L_j e_j)
-//   BP_MVZ   y[r] = acc, z[r] = 0                      (r_{j+1} = R_j t_j, and e_{j+1} = 0)
-//   BP_ADD   y[r] += acc                               (e_j += P_j e_{j+1})
-//   BP_MV    y[r] = acc                                (coarsest: e_p = L_p^{-1} r_p, dense rows)
+// (acc = sum_k val_k x[col_k]; x is a replicated shared vector or, for the restriction and
+// the coarsest solve, a global one):
+//   BP_ZERO  y[r] = 0 (own copy, all rows)                 (e_J = 0, Alg. 3 line 7)
+//   BP_GS    y[r] = x[r] + (f[r] - acc) * dinv[r]          (one colour; y = x = u_j)
+//   BP_RES   t[r] = f[r] - acc                             (t_j = r_j - L_j e_j; global)
+//   BP_MVZ   f'[r] = acc (global), z[r] = 0                (r_{j+1} = R_j t_j, e_{j+1} = 0)
+//   BP_ADD   y[r] += acc                                   (e_j += P_j e_{j+1})
+//   BP_MV    y[r] = acc                                    (coarsest: e_p = L_p^{-1} r_p)
+//   BP_STORE g[r] = y[r]                                   (e_J back to HBM)
 // Every output element is produced by one thread group with a fixed summation order, so
 // the kernel is deterministic.  Shifted problems only (the Poisson border terms run on the
 // per-kernel path).
@@ -47,7 +47,7 @@
 
 namespace mgm {
 
-enum : int { BP_ZERO = 0, BP_GS = 1, BP_RES = 2, BP_MVZ = 3, BP_ADD = 4, BP_MV = 5 };
+enum : int { BP_ZERO = 0, BP_GS = 1, BP_RES = 2, BP_MVZ = 3, BP_ADD = 4, BP_MV = 5, BP_STORE = 6 };
 constexpr int BOT_THREADS = 512;
 constexpr int BOT_MAX_PHASES = 1024;
 constexpr int BOT_FRAG = 9;  // max operator entries per thread held in registers
@@ -56,12 +56,15 @@ struct BPhase {
     int op, local, r0, r1;
     int tpr_log2;  // threads per row = 1 << tpr_log2 (<= 32)
     int W;         // ELL row stride
+    int xo;        // shared byte offset of the gathered vector, or -1: global x
+    int yo;        // shared byte offset of the output vector (replicated), or -1: global y
+    int zo;        // shared byte offset of the vector zeroed by BP_MVZ
+    int fpre;      // 1: f may be prefetched with the operator row (not written by the previous phase)
     const int* col;
     const double* val;
-    const double* x;
-    double* y;
+    const double* x;  // global gathered vector (xo < 0)
+    double* y;        // global output (yo < 0) / BP_STORE destination
     const double* f;
-    double* z;
     const double* dinv;
 };
 
@@ -80,18 +83,24 @@ __device__ __forceinline__ double ld_keep_f64(const double* p, uint64_t pol) {
     asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
     return v;
 }
+__device__ __forceinline__ void dsm_st_rank(uint32_t local_addr, unsigned rank, double v) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local_addr), "r"(rank));
+    asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(r), "d"(v) : "memory");
+}
 
 // The operator entries of one thread's first row of a phase, held in registers.
 struct BFrag {
     int c[BOT_FRAG];
     double a[BOT_FRAG];
     double dinv;  // 1/a_rr (GS phases, lane 0)
+    double f;     // f[row] when the phase allows the prefetch (lane 0)
 };
 
 template <int TPR>
 __device__ __forceinline__ void bfrag_load(BFrag& fr, const BPhase& P, int row, int lane, uint64_t pol) {
     constexpr int CH = bot_ch(TPR);
-    const bool live = row < P.r1 && P.op != BP_ZERO;  // BP_ZERO has no operator
+    const bool live = row < P.r1 && P.op != BP_ZERO && P.op != BP_STORE;  // no operator
     const int64_t base = (int64_t)row * P.W;
 #pragma unroll
     for (int q = 0; q < CH; ++q) {
@@ -101,51 +110,72 @@ __device__ __forceinline__ void bfrag_load(BFrag& fr, const BPhase& P, int row, 
         fr.a[q] = ok ? ld_keep_f64(P.val + base + k, pol) : 0.0;
     }
     fr.dinv = (live && lane == 0 && P.op == BP_GS) ? ld_keep_f64(P.dinv + row, pol) : 0.0;
+    fr.f = (live && lane == 0 && P.fpre && (P.op == BP_GS || P.op == BP_RES)) ? P.f[row] : 0.0;
+}
+
+// store v at byte offset off + 8*row of every CTA's copy (lanes of the row group share the
+// C stores)
+__device__ __forceinline__ void bcast_store(uint32_t sbase, int off, int row, double v, int lane, int tpr, int cs) {
+    const uint32_t a = sbase + (uint32_t)off + ((uint32_t)row << 3);
+    for (int k = lane; k < cs; k += tpr) dsm_st_rank(a, (unsigned)k, v);
 }
 
 template <int TPR>
-__device__ __forceinline__ void bottom_phase(const BPhase& P, const BFrag& fr0, int g, int nthr, uint64_t pol) {
+__device__ __forceinline__ void bottom_phase(const BPhase& P, const BFrag& fr0, int g, int nthr, const char* smem,
+                                             uint32_t sbase, int cs, uint64_t pol) {
     constexpr int CH = bot_ch(TPR);
     const int lane = g & (TPR - 1);
     const int ngroups = nthr / TPR;
     const int nrows = P.r1 - P.r0;
+    const double* xs = reinterpret_cast<const double*>(smem + (P.xo >= 0 ? P.xo : 0));
+    const double* ys = reinterpret_cast<const double*>(smem + (P.yo >= 0 ? P.yo : 0));
     for (int base = 0; base < nrows; base += ngroups) {  // uniform trip count across threads
         const int row = P.r0 + base + g / TPR;
         const bool live = row < P.r1;
-        if (P.op == BP_ZERO) {
-            if (live && lane == 0) P.y[row] = 0.0;
-            continue;
-        }
         BFrag fr = fr0;  // register copy; rows after the first are loaded here
         if (base != 0) bfrag_load<TPR>(fr, P, row, lane, pol);
-        // epilogue operands issued together with the gathers
+        // epilogue operand issued together with the gathers
         double ev = 0.0;
         if (live && lane == 0) {
-            if (P.op == BP_GS || P.op == BP_RES) ev = P.f[row];
-            else if (P.op == BP_ADD) ev = P.y[row];
+            if (P.op == BP_GS || P.op == BP_RES) ev = P.fpre && base == 0 ? fr.f : P.f[row];
+            else if (P.op == BP_ADD) ev = ys[row];
         }
         double xv[CH];
+        if (P.xo >= 0) {
 #pragma unroll
-        for (int q = 0; q < CH; ++q) xv[q] = fr.c[q] >= 0 ? P.x[fr.c[q]] : 0.0;  // L1-cacheable (see below)
+            for (int q = 0; q < CH; ++q) xv[q] = fr.c[q] >= 0 ? xs[fr.c[q]] : 0.0;
+        } else {
+#pragma unroll
+            for (int q = 0; q < CH; ++q) xv[q] = fr.c[q] >= 0 ? P.x[fr.c[q]] : 0.0;
+        }
         double acc = 0.0;
 #pragma unroll
         for (int q = 0; q < CH; ++q) acc = fma(fr.a[q], xv[q], acc);
-        for (int k = lane + CH * TPR; k < P.W; k += TPR)  // rows wider than TPR*CH (rare)
-            if (live) acc = fma(ld_keep_f64(P.val + (int64_t)row * P.W + k, pol),
-                                P.x[ld_keep_i32(P.col + (int64_t)row * P.W + k, pol)], acc);
+        for (int k = lane + CH * TPR; k < P.W; k += TPR) {  // rows wider than TPR*CH (rare)
+            if (!live) break;
+            const int c = ld_keep_i32(P.col + (int64_t)row * P.W + k, pol);
+            acc = fma(ld_keep_f64(P.val + (int64_t)row * P.W + k, pol), P.xo >= 0 ? xs[c] : P.x[c], acc);
+        }
 #pragma unroll
         for (int o = TPR >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        // every lane of the group holds acc; lane 0 computes the row's value, the group stores
+        double out = 0.0;
         if (live && lane == 0) {
             switch (P.op) {
-                case BP_GS: P.y[row] = xv[0] + (ev - acc) * fr.dinv; break;  // xv[0] = x[row] (diagonal first)
-                case BP_RES: P.y[row] = ev - acc; break;
-                case BP_MVZ:
-                    P.y[row] = acc;
-                    P.z[row] = 0.0;
-                    break;
-                case BP_ADD: P.y[row] = ev + acc; break;
-                default: P.y[row] = acc; break;
+                case BP_GS: out = xv[0] + (ev - acc) * fr.dinv; break;  // xv[0] = x[row] (diagonal first)
+                case BP_RES: out = ev - acc; break;
+                case BP_ADD: out = ev + acc; break;
+                default: out = acc; break;  // BP_MVZ, BP_MV
             }
+        }
+        out = __shfl_sync(0xffffffffu, out, (int)(threadIdx.x & 31) & ~(TPR - 1));
+        if (live) {
+            if (P.yo >= 0) {
+                bcast_store(sbase, P.yo, row, out, lane, TPR, cs);
+            } else if (lane == 0) {
+                P.y[row] = out;
+            }
+            if (P.op == BP_MVZ) bcast_store(sbase, P.zo, row, 0.0, lane, TPR, cs);
         }
     }
 }
@@ -162,14 +192,15 @@ __device__ __forceinline__ void bfrag_load_any(BFrag& fr, const BPhase& P, int g
         default: bfrag_load<32>(fr, P, row, lane, pol); break;
     }
 }
-__device__ __forceinline__ void bottom_phase_any(const BPhase& P, const BFrag& fr, int g, int nthr, uint64_t pol) {
+__device__ __forceinline__ void bottom_phase_any(const BPhase& P, const BFrag& fr, int g, int nthr, const char* smem,
+                                                 uint32_t sbase, int cs, uint64_t pol) {
     switch (P.tpr_log2) {
-        case 0: bottom_phase<1>(P, fr, g, nthr, pol); break;
-        case 1: bottom_phase<2>(P, fr, g, nthr, pol); break;
-        case 2: bottom_phase<4>(P, fr, g, nthr, pol); break;
-        case 3: bottom_phase<8>(P, fr, g, nthr, pol); break;
-        case 4: bottom_phase<16>(P, fr, g, nthr, pol); break;
-        default: bottom_phase<32>(P, fr, g, nthr, pol); break;
+        case 0: bottom_phase<1>(P, fr, g, nthr, smem, sbase, cs, pol); break;
+        case 1: bottom_phase<2>(P, fr, g, nthr, smem, sbase, cs, pol); break;
+        case 2: bottom_phase<4>(P, fr, g, nthr, smem, sbase, cs, pol); break;
+        case 3: bottom_phase<8>(P, fr, g, nthr, smem, sbase, cs, pol); break;
+        case 4: bottom_phase<16>(P, fr, g, nthr, smem, sbase, cs, pol); break;
+        default: bottom_phase<32>(P, fr, g, nthr, smem, sbase, cs, pol); break;
     }
 }
 
@@ -191,21 +222,25 @@ __device__ __forceinline__ unsigned long long gtimer() {
     return t;
 }
 
+// smem: [phase table (nph x BPhase)][replicated vectors at the offsets in the phases]
 __global__ void __launch_bounds__(BOT_THREADS, 1)
     k_vcycle_bottom(const BPhase* __restrict__ gphases, int nph, unsigned long long* __restrict__ trace) {
-    extern __shared__ __align__(16) BPhase phases[];  // the phase list, staged once (immutable)
+    extern __shared__ __align__(16) char smem[];
+    const BPhase* phases = reinterpret_cast<const BPhase*>(smem);
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
     pdl_trigger();
     uint64_t pol;
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
     {
         const int nw = nph * (int)(sizeof(BPhase) / 8);
         const unsigned long long* src = reinterpret_cast<const unsigned long long*>(gphases);
-        unsigned long long* dst = reinterpret_cast<unsigned long long*>(phases);
+        unsigned long long* dst = reinterpret_cast<unsigned long long*>(smem);
         for (int i = threadIdx.x; i < nw; i += BOT_THREADS) dst[i] = src[i];
         __syncthreads();
     }
     const int rank = (int)cluster_rank();
-    const int nthr_cl = (int)cluster_nctas() * BOT_THREADS;
+    const int cs = (int)cluster_nctas();
+    const int nthr_cl = cs * BOT_THREADS;
     const int g_cl = rank * BOT_THREADS + (int)threadIdx.x;
     // prologue (immutable data only): phase 0's operator rows
     BFrag fr;
@@ -214,13 +249,24 @@ __global__ void __launch_bounds__(BOT_THREADS, 1)
         if (!P.local || rank == 0) bfrag_load_any(fr, P, P.local ? (int)threadIdx.x : g_cl, pol);
     }
     pdl_wait();
+    cluster_arrive();  // every CTA's shared memory is live before any remote store
+    cluster_wait();
     for (int q = 0; q < nph; ++q) {
         if (trace && rank == 0 && threadIdx.x == 0) trace[q] = gtimer();  // diagnostics (MGM_TRACE)
         const BPhase P = phases[q];
-        const bool part = !P.local || rank == 0;
-        if (part) bottom_phase_any(P, fr, P.local ? (int)threadIdx.x : g_cl, P.local ? BOT_THREADS : nthr_cl, pol);
+        if (P.op == BP_ZERO) {  // every CTA zeroes its own copy
+            double* y = reinterpret_cast<double*>(smem + P.yo);
+            for (int r = P.r0 + threadIdx.x; r < P.r1; r += BOT_THREADS) y[r] = 0.0;
+        } else if (P.op == BP_STORE) {  // copy back to HBM, split over the cluster
+            const double* y = reinterpret_cast<const double*>(smem + P.yo);
+            for (int r = P.r0 + g_cl; r < P.r1; r += nthr_cl) P.y[r] = y[r];
+        } else if (!P.local || rank == 0) {
+            bottom_phase_any(P, fr, P.local ? (int)threadIdx.x : g_cl, P.local ? BOT_THREADS : nthr_cl, smem, sbase,
+                             cs, pol);
+        }
         if (q + 1 == nph) break;
         const BPhase& N = phases[q + 1];
+        const bool part = !P.local || rank == 0;
         const bool npart = !N.local || rank == 0;
         if (P.local && N.local) {  // CTA 0 only; the other CTAs skip local phases
             if (npart) bfrag_load_any(fr, N, (int)threadIdx.x, pol);
@@ -231,6 +277,8 @@ __global__ void __launch_bounds__(BOT_THREADS, 1)
             cluster_wait();
         }
     }
+    cluster_arrive();  // no CTA exits while others may still store into its shared memory
+    cluster_wait();
 }
 
 }  // namespace mgm

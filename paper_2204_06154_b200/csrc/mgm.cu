@@ -338,18 +338,36 @@ void setup_bottom(mgm_ctx* ctx, const std::vector<double>& LU, const std::vector
     if (const char* e = std::getenv("MGM_BOT_LOCAL")) blocal = std::atoll(e);
     if (ctx->poisson || bmax <= 0 || ctx->p < 2) return;
     const int p = ctx->p;
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    // first level J >= 1 with N_J <= bmax whose phase table + replicated iterates fit
     int J = -1;
-    for (int j = 1; j < p; ++j)
-        if (ctx->lv[j].n <= bmax) { J = j; break; }
-    if (J < 0) return;
-    {
-        i64 nph = 2;
-        for (int q = J; q + 1 < p; ++q) nph += (i64)(ctx->lp.nu1 + ctx->lp.nu2) * ctx->lv[q].ncol + 3;
-        if (nph > BOT_MAX_PHASES) return;
+    size_t table = 0;
+    for (int j = 1; j < p; ++j) {
+        if (ctx->lv[j].n > bmax) continue;
+        i64 nph = 3, vb = 0;
+        for (int q = j; q < p; ++q) {
+            vb += ctx->lv[q].n * (i64)sizeof(double);
+            if (q + 1 < p) nph += (i64)(ctx->lp.nu1 + ctx->lp.nu2) * ctx->lv[q].ncol + 3;
+        }
+        const size_t tb = (size_t)nph * sizeof(BPhase);
+        if (nph <= BOT_MAX_PHASES && (tb + 15) / 16 * 16 + (size_t)vb + 1024 <= (size_t)optin) {
+            J = j;
+            table = (tb + 15) / 16 * 16;
+            break;
+        }
     }
+    if (J < 0) return;
     cudaFuncSetAttribute(k_vcycle_bottom, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     set_max_dyn_smem((const void*)k_vcycle_bottom);
     // cluster size: 16 (non-portable) if the device can co-schedule it, else 8
+    size_t smem = table;
+    std::vector<int> ou(p, -1);
+    for (int j = J; j < p; ++j) {
+        ou[j] = (int)smem;
+        smem += (size_t)ctx->lv[j].n * sizeof(double);
+    }
     int cs = 0;
     std::vector<int> sizes = {16, 8};
     if (const char* e = std::getenv("MGM_BOT_CS")) sizes = {std::atoi(e)};  // tuning experiment
@@ -357,7 +375,7 @@ void setup_bottom(mgm_ctx* ctx, const std::vector<double>& LU, const std::vector
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(c);
         cfg.blockDim = dim3(BOT_THREADS);
-        cfg.dynamicSmemBytes = sizeof(BPhase) * BOT_MAX_PHASES;
+        cfg.dynamicSmemBytes = smem;
         cudaLaunchAttribute at[1];
         at[0].id = cudaLaunchAttributeClusterDimension;
         at[0].val.clusterDim.x = c;
@@ -431,18 +449,28 @@ void setup_bottom(mgm_ctx* ctx, const std::vector<double>& LU, const std::vector
     if (!ok) return;
     const int nthr_cl = cs * BOT_THREADS;
     std::vector<BPhase> ph;
-    auto add = [&](int op, bool local, i64 r0, i64 r1, const Ell& E, const double* x, double* y, const double* f,
-                   double* z, const double* di) {
+    auto is_local = [&](int j) { return ctx->lv[j].n <= blocal; };
+    // op on rows [r0, r1); x: smem offset xo (>= 0) or global xg; y: smem offset yo or global yg
+    auto add = [&](int op, bool local, i64 r0, i64 r1, const Ell* E, int xo, const double* xg, int yo, double* yg,
+                   const double* f, int zo, const double* di) {
         if (r1 <= r0) return;
         BPhase P{};
         P.op = op;
         P.local = local ? 1 : 0;
         P.r0 = (int)r0;
         P.r1 = (int)r1;
-        P.W = std::max(E.W, 1);
+        P.W = E ? std::max(E->W, 1) : 1;
+        P.xo = xo; P.yo = yo; P.zo = zo;
+        P.x = xg; P.y = yg; P.f = f; P.dinv = di;
+        P.col = E ? E->col : nullptr;
+        P.val = E ? E->val : nullptr;
+        // f may ride with the operator prefetch unless the previous phase wrote it (the
+        // restriction writes f_{j+1}; a GS or residual phase after a GS phase of the
+        // same level reads an f that is already final)
+        P.fpre = (!ph.empty() && ph.back().op == BP_GS && ph.back().f == f && (op == BP_GS || op == BP_RES)) ? 1 : 0;
         const i64 nthr = local ? BOT_THREADS : nthr_cl;
         int best = -1;
-        if (op == BP_ZERO) {
+        if (op == BP_ZERO || op == BP_STORE) {
             best = 0;
         } else {
             int smallest_valid = -1;
@@ -455,45 +483,40 @@ void setup_bottom(mgm_ctx* ctx, const std::vector<double>& LU, const std::vector
             if (best < 0) best = smallest_valid >= 0 ? smallest_valid : 5;
         }
         P.tpr_log2 = best;
-        P.col = E.col;
-        P.val = E.val;
-        P.x = x; P.y = y; P.f = f; P.z = z; P.dinv = di;
         ph.push_back(P);
     };
-    auto is_local = [&](int j) { return ctx->lv[j].n <= blocal; };
     const bool pre_b = ctx->lp.smoother == 1, post_b = ctx->lp.smoother == 1 || ctx->lp.smoother == 2;
     auto sweep = [&](int j, bool backward) {
         Level& L = ctx->lv[j];
         for (int q = 0; q < L.ncol; ++q) {
             const int c = backward ? L.ncol - 1 - q : q;
-            add(BP_GS, is_local(j), L.coff[c], L.coff[c + 1], EL[j], L.u, L.u, L.f, nullptr, dinv[j]);
+            add(BP_GS, is_local(j), L.coff[c], L.coff[c + 1], &EL[j], ou[j], nullptr, ou[j], nullptr, L.f, -1, dinv[j]);
         }
     };
-    const Ell none;
-    if (J < p - 1) add(BP_ZERO, is_local(J), 0, ctx->lv[J].n, none, nullptr, ctx->lv[J].u, nullptr, nullptr, nullptr);
+    add(BP_ZERO, false, 0, ctx->lv[J].n, nullptr, -1, nullptr, ou[J], nullptr, nullptr, -1, nullptr);  // u_J = 0
     for (int j = J; j + 1 < p; ++j) {  // Alg. 3 lines 6-9 (and 4-5 for j = J)
         Level& L = ctx->lv[j];
         Level& Ln = ctx->lv[j + 1];
         for (int s2 = 0; s2 < ctx->lp.nu1; ++s2) sweep(j, pre_b);
-        add(BP_RES, is_local(j), 0, L.n, EL[j], L.u, L.t, L.f, nullptr, nullptr);
-        add(BP_MVZ, is_local(j), 0, Ln.n, ER[j], L.t, Ln.f, nullptr, Ln.u, nullptr);
+        add(BP_RES, is_local(j), 0, L.n, &EL[j], ou[j], nullptr, -1, L.t, L.f, -1, nullptr);
+        add(BP_MVZ, is_local(j), 0, Ln.n, &ER[j], -1, L.t, -1, Ln.f, nullptr, ou[j + 1], nullptr);
     }
     {  // line 10
         Level& C = ctx->lv[p - 1];
-        add(BP_MV, is_local(p - 1), 0, m, EC, C.f, C.u, nullptr, nullptr, nullptr);
+        add(BP_MV, is_local(p - 1), 0, m, &EC, -1, C.f, ou[p - 1], nullptr, nullptr, -1, nullptr);
     }
     for (int j = p - 2; j >= J; --j) {  // lines 11-14
         Level& L = ctx->lv[j];
-        Level& Ln = ctx->lv[j + 1];
-        add(BP_ADD, is_local(j), 0, L.n, EP[j], Ln.u, L.u, nullptr, nullptr, nullptr);
+        add(BP_ADD, is_local(j), 0, L.n, &EP[j], ou[j + 1], nullptr, ou[j], nullptr, nullptr, -1, nullptr);
         for (int s2 = 0; s2 < ctx->lp.nu2; ++s2) sweep(j, post_b);
     }
-    if ((int)ph.size() > BOT_MAX_PHASES) return;
+    add(BP_STORE, false, 0, ctx->lv[J].n, nullptr, -1, nullptr, ou[J], ctx->lv[J].u, nullptr, -1, nullptr);
+    if ((int)ph.size() * sizeof(BPhase) > table) return;
     ctx->d_phases = bot_upload(ctx, ph, ok);
     if (!ok) return;
     ctx->nphases = (int)ph.size();
     ctx->bot_cluster = cs;
-    ctx->bot_smem = sizeof(BPhase) * ph.size();
+    ctx->bot_smem = smem;
     ctx->botJ = J;
 }
 

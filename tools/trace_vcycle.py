@@ -53,7 +53,7 @@ if os.environ.get("BOTTOM_PHASES"):
         d = np.diff(st.astype(np.float64)) / 1e3
         acc = d if acc is None else acc + d
     acc /= 10
-    names = ["ZERO", "GS", "RES", "MVZ", "ADD", "MV"]
+    names = ["ZERO", "GS", "RES", "MVZ", "ADD", "MV", "STORE"]
     print("bottom phases:", len(st), "sum of phase gaps", acc.sum(), "us")
     rows = {}
     for q, dt in enumerate(acc):
