@@ -150,6 +150,7 @@ def main():
     ap.add_argument("--impl", default="mgm")
     ap.add_argument("--cfg", type=int, default=3)
     ap.add_argument("--n", type=int, default=None)
+    ap.add_argument("--method", default="rbffd", choices=["rbffd", "gfd"], help="cfg 2 only: RBF-FD or GFD")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--parallel", choices=["replicas", "dist"], default="replicas",
                     help="N>1: independent replicas of the solve (weak scaling) or one solve "
@@ -172,7 +173,7 @@ def main():
     if ws > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    w = MI.make_workload(args.cfg, n=args.n)
+    w = MI.make_workload(args.cfg, n=args.n, method=args.method)
     N = len(w.points)
     t0 = time.perf_counter()
     m = MGM(w.points, w.normals, w.stencil, w.levels)

@@ -7,6 +7,9 @@
 //   * SpGEMM for the Galerkin product, one CTA per output row, sort-based
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cstdlib>
+
 #include <climits>
 #include <cstdint>
 #include <string>
@@ -462,7 +465,8 @@ __global__ void k_spgemm_rows(i64 nrows, const i64* __restrict__ ap, const i32* 
                               const double* __restrict__ av, const i64* __restrict__ bp,
                               const i32* __restrict__ bi, const double* __restrict__ bv, int n2,
                               i64* __restrict__ cnt, const i64* __restrict__ cptr,
-                              i32* __restrict__ ci, double* __restrict__ cv) {
+                              i32* __restrict__ ci, double* __restrict__ cv,
+                              const unsigned char* __restrict__ skip) {
     extern __shared__ unsigned long long sm[];
     unsigned long long* keys = sm;                          // n2
     double* vals = (double*)(keys + n2);                    // n2
@@ -470,6 +474,7 @@ __global__ void k_spgemm_rows(i64 nrows, const i64* __restrict__ ap, const i32* 
     __shared__ i64 off_s[1025];
     __shared__ int total_s;
     for (i64 i = blockIdx.x; i < nrows; i += gridDim.x) {
+        if (skip[i]) continue;  // long rows: computed on the host (spgemm_long_row)
         const i64 a0 = ap[i], a1 = ap[i + 1];
         const int na = (int)(a1 - a0);
         // offsets of each A entry's products (serial, rows are short)
@@ -533,6 +538,51 @@ static inline int next_pow2(i64 v) {
     return p;
 }
 
+// A row whose products do not fit the shared-memory buffer (or with more than 1024 A
+// entries) is computed on the host in exactly the device's canonical order: products
+// (A entries by ascending column, then B entries by ascending column) keyed (column,
+// product index), each column's products summed sequentially in product order, with the
+// same correctly rounded multiply and add -- so the result is bit-identical.
+static int spgemm_long_row(const DevCSR& A, const DevCSR& B, const std::vector<i64>& bptr, i64 i,
+                           std::vector<i32>& cols, std::vector<double>& vals, cudaStream_t st) {
+    i64 ar[2];
+    cudaMemcpy(ar, A.ptr + i, sizeof(i64) * 2, cudaMemcpyDeviceToHost);
+    const i64 na = ar[1] - ar[0];
+    std::vector<i32> ac(na);
+    std::vector<double> av(na);
+    cudaMemcpy(ac.data(), A.col + ar[0], sizeof(i32) * na, cudaMemcpyDeviceToHost);
+    cudaMemcpy(av.data(), A.val + ar[0], sizeof(double) * na, cudaMemcpyDeviceToHost);
+    std::vector<std::pair<unsigned long long, double>> prod;  // (col << 32 | pidx, a*b)
+    std::vector<i32> bc;
+    std::vector<double> bv;
+    for (i64 t = 0; t < na; ++t) {
+        const i64 b0 = bptr[ac[t]], b1 = bptr[ac[t] + 1];
+        bc.resize(b1 - b0);
+        bv.resize(b1 - b0);
+        cudaMemcpy(bc.data(), B.col + b0, sizeof(i32) * (b1 - b0), cudaMemcpyDeviceToHost);
+        cudaMemcpy(bv.data(), B.val + b0, sizeof(double) * (b1 - b0), cudaMemcpyDeviceToHost);
+        for (i64 s = 0; s < b1 - b0; ++s) {
+            const unsigned long long pidx = prod.size();
+            prod.push_back({((unsigned long long)(unsigned)bc[s] << 32) | pidx, av[t] * bv[s]});
+        }
+    }
+    std::sort(prod.begin(), prod.end(),
+              [](const std::pair<unsigned long long, double>& x, const std::pair<unsigned long long, double>& y) {
+                  return x.first < y.first;
+              });
+    cols.clear();
+    vals.clear();
+    for (size_t p = 0; p < prod.size();) {
+        const unsigned col = (unsigned)(prod[p].first >> 32);
+        double sum = 0.0;
+        for (; p < prod.size() && (unsigned)(prod[p].first >> 32) == col; ++p) sum = sum + prod[p].second;
+        cols.push_back((i32)col);
+        vals.push_back(sum);
+    }
+    (void)st;
+    return (int)cudaGetLastError();
+}
+
 int spgemm_device(const DevCSR& A, const DevCSR& B, DevCSR& C, void* stream, std::string& err) {
     cudaStream_t st = (cudaStream_t)stream;
     C = DevCSR();
@@ -540,43 +590,69 @@ int spgemm_device(const DevCSR& A, const DevCSR& B, DevCSR& C, void* stream, std
     C.ncols = B.ncols;
     i64 n = A.nrows;
     i64* d_cnt = nullptr;
+    unsigned char* d_skip = nullptr;
     cudaError_t e = cudaMalloc(&d_cnt, sizeof(i64) * (n + 1));
+    if (e == cudaSuccess) e = cudaMalloc(&d_skip, std::max<i64>(1, n));
     if (e != cudaSuccess) { err = "cudaMalloc"; return (int)e; }
     k_row_products<<<(unsigned)std::min<i64>((n + 255) / 256, 148 * 16), 256, 0, st>>>(A.ptr, A.col, B.ptr, n, d_cnt);
-    std::vector<i64> cnt(n);
+    std::vector<i64> cnt(n), aptr(n + 1);
     cudaMemcpyAsync(cnt.data(), d_cnt, sizeof(i64) * n, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(aptr.data(), A.ptr, sizeof(i64) * (n + 1), cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
-    i64 mx = 0;
-    for (i64 v : cnt) mx = std::max(mx, v);
-    // A rows longer than 1024 entries are not supported by off_s
-    std::vector<i64> hap(2);
-    int n2 = next_pow2(std::max<i64>(mx, 2));
-    size_t smem = (size_t)n2 * (8 + 8 + 4) + 8;
-    if (smem > 200 * 1024) {
-        cudaFree(d_cnt);
-        err = "SpGEMM row with " + std::to_string(mx) + " products exceeds the shared-memory row buffer";
-        return (int)cudaErrorInvalidValue;
+    // shared-memory row buffer: the largest power of two <= 8192 covering the typical rows;
+    // longer rows (and rows with > 1024 A entries) go to spgemm_long_row
+    i64 cap = 8192;
+    if (const char* e = std::getenv("MGM_SPGEMM_CAP")) cap = std::max<i64>(2, std::atoll(e));  // test hook
+    i64 mx = 2;
+    std::vector<unsigned char> skip(n, 0);
+    std::vector<i64> longs;
+    for (i64 r = 0; r < n; ++r) {
+        if (cnt[r] > cap || aptr[r + 1] - aptr[r] > 1024) {
+            skip[r] = 1;
+            longs.push_back(r);
+        } else {
+            mx = std::max(mx, cnt[r]);
+        }
     }
+    cudaMemcpyAsync(d_skip, skip.data(), std::max<i64>(1, n), cudaMemcpyHostToDevice, st);
+    int n2 = next_pow2(mx);
+    size_t smem = (size_t)n2 * (8 + 8 + 4) + 8;
     cudaFuncSetAttribute(k_spgemm_rows<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(k_spgemm_rows<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     unsigned grid = (unsigned)std::min<i64>(n, 148 * 8);
     int threads = n2 >= 2048 ? 512 : 256;
     k_spgemm_rows<false><<<grid, threads, smem, st>>>(n, A.ptr, A.col, A.val, B.ptr, B.col, B.val, n2, d_cnt,
-                                                      nullptr, nullptr, nullptr);
+                                                      nullptr, nullptr, nullptr, d_skip);
     cudaMemcpyAsync(cnt.data(), d_cnt, sizeof(i64) * n, cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
+    std::vector<std::vector<i32>> lcols(longs.size());
+    std::vector<std::vector<double>> lvals(longs.size());
+    if (!longs.empty()) {
+        std::vector<i64> bptr(B.nrows + 1);
+        cudaMemcpy(bptr.data(), B.ptr, sizeof(i64) * (B.nrows + 1), cudaMemcpyDeviceToHost);
+        for (size_t q = 0; q < longs.size(); ++q) {
+            spgemm_long_row(A, B, bptr, longs[q], lcols[q], lvals[q], st);
+            cnt[longs[q]] = (i64)lcols[q].size();
+        }
+    }
     std::vector<i64> ptr(n + 1, 0);
     for (i64 r = 0; r < n; ++r) ptr[r + 1] = ptr[r] + cnt[r];
     C.nnz = ptr[n];
     e = cudaMalloc(&C.ptr, sizeof(i64) * (n + 1));
     if (e == cudaSuccess) e = cudaMalloc(&C.col, sizeof(i32) * std::max<i64>(1, C.nnz));
     if (e == cudaSuccess) e = cudaMalloc(&C.val, sizeof(double) * std::max<i64>(1, C.nnz));
-    if (e != cudaSuccess) { cudaFree(d_cnt); err = "cudaMalloc (SpGEMM output)"; return (int)e; }
+    if (e != cudaSuccess) { cudaFree(d_cnt); cudaFree(d_skip); err = "cudaMalloc (SpGEMM output)"; return (int)e; }
     cudaMemcpyAsync(C.ptr, ptr.data(), sizeof(i64) * (n + 1), cudaMemcpyHostToDevice, st);
     k_spgemm_rows<true><<<grid, threads, smem, st>>>(n, A.ptr, A.col, A.val, B.ptr, B.col, B.val, n2, nullptr,
-                                                     C.ptr, C.col, C.val);
+                                                     C.ptr, C.col, C.val, d_skip);
+    for (size_t q = 0; q < longs.size(); ++q) {
+        const i64 o = ptr[longs[q]];
+        cudaMemcpyAsync(C.col + o, lcols[q].data(), sizeof(i32) * lcols[q].size(), cudaMemcpyHostToDevice, st);
+        cudaMemcpyAsync(C.val + o, lvals[q].data(), sizeof(double) * lvals[q].size(), cudaMemcpyHostToDevice, st);
+    }
     e = cudaStreamSynchronize(st);
     cudaFree(d_cnt);
+    cudaFree(d_skip);
     if (e != cudaSuccess) { err = "SpGEMM kernel"; return (int)e; }
     return (int)cudaGetLastError();
 }
