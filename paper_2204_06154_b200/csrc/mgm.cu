@@ -88,6 +88,8 @@ struct Level {
     int tpr = 1, rtpr = 1;  // threads per row for L_j (colour sweeps) and R_j kernels
     int stpr = 1;           // threads per row for full-level SpMV / residual on L_j
     int gs_block = 256;     // threads per block of the colour kernels
+    int pipe_ctas = 0;      // > 0: colours with >= pipe_ctas*128 rows use k_gs_colour_pipe on this many CTAs
+    int uniform_w = 0;      // > 0: every SELL slice has this width
     // interpolation P_j (ELL width pm, slot-major) and restriction R_j (SELL-32, next level rows)
     int pm = 0;
     i32* pcol = nullptr;
@@ -829,6 +831,18 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
             // 112.8 -> 87.6 us per sweep with 8 instead of 4)
             if (L.ncol > 0 && (double)n / L.ncol * L.tpr < 16384.0 && L.tpr < 8) L.tpr *= 2;
             L.stpr = 1;
+            {   // streamed colour kernel for large colours: opt-in (MGM_PIPE=1), measured slower
+                // than the one-wave kernel (level-0 sweep 174 us vs 122 us, profiles/r01_notes.md)
+                int dev = 0, nsm = 148;
+                cudaGetDevice(&dev);
+                cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+                L.pipe_ctas = (std::getenv("MGM_PIPE") && !std::getenv("MGM_NO_PIPE")) ? nsm : 0;
+                if (const char* e = std::getenv("MGM_PIPE_CTAS")) L.pipe_ctas = std::atoi(e);
+                const i64 ns = (n + 31) / 32;
+                bool uni = ns > 0;
+                for (i64 q = 0; q < ns && uni; ++q) uni = sptr[q + 1] - sptr[q] == sptr[1] - sptr[0];
+                L.uniform_w = uni ? (int)((sptr[1] - sptr[0]) / 32) : 0;
+            }
             // colours with fewer threads than one 256-thread block per SM run 64-thread blocks
             // (cfg3 L1+L2: -19 us per V-cycle, profiles/r01_notes.md)
             {
@@ -1152,7 +1166,15 @@ void enqueue_sweep(mgm_ctx* ctx, int j, bool backward, cudaStream_t st) {
         if (c1 <= c0) continue;
         for_my_pieces(ctx, j, c0, c1, [&](i64 a, i64 b) {
             if (b <= a) return;
-            launch_gs(ctx->pdl, ctx->poisson, L.tpr, (int)a, (int)b, (int)(b - (a & ~31)), L, st);
+            if (L.pipe_ctas > 0 && !ctx->poisson && b - a >= (i64)L.pipe_ctas * 128) {
+                // large colour: streamed kernel, one CTA per SM (k_gs_colour_pipe)
+                const int rpc = (int)((b - a + L.pipe_ctas - 1) / L.pipe_ctas);
+                launch(ctx->pdl, k_gs_colour_pipe<2, CHUNK>, (unsigned)((b - a + rpc - 1) / rpc), 256, 0, st, (int)a,
+                       (int)b, rpc, L.uniform_w, (const i64*)L.sptr, (const i32*)L.scol, (const double*)L.sval,
+                       (const double*)L.f, L.u);
+            } else {
+                launch_gs(ctx->pdl, ctx->poisson, L.tpr, (int)a, (int)b, (int)(b - (a & ~31)), L, st);
+            }
             bytes += sweep_colour_bytes(L, b - a);
             ++nl;
             ctx->vcycle_kernels++;
