@@ -1022,7 +1022,7 @@ void gs_launch_t(bool pdl, int r0, int r1, int span, const Level& L, cudaStream_
     // block size: colours too small to give every SM a 256-thread block use smaller blocks
     // (spreads the gathers over more SMs)
     const int bs = L.gs_block;
-    launch(pdl, k_gs_colour<P, TPR, CHUNK>, blocks_for((i64)span * TPR, bs), bs, 0, st, r0, r1, L.sptr, L.scol,
+    launch(pdl, k_gs_colour<P, TPR, CHUNK>, blocks_for((i64)span * TPR, bs), bs, 0, st, r0, r1, L.uniform_w, L.sptr, L.scol,
            L.sval, L.f, L.u, L.c, (int)L.n);
 }
 // Threads one wave of colour kernels can hold (all SMs, register-limited occupancy).

@@ -73,7 +73,7 @@ __device__ __forceinline__ double group_sum(double v) {
 //   u_i += (f_i - sum_j a_ij u_j [- c_i lambda]) / a_ii  over rows [r0, r1) of one colour.
 // TPR threads per row; threads aligned to 32-row slices.
 template <bool POISSON, int TPR, int CH>
-__global__ void __launch_bounds__(256) k_gs_colour(int r0, int r1, const int64_t* __restrict__ sptr,
+__global__ void __launch_bounds__(256) k_gs_colour(int r0, int r1, int Wu, const int64_t* __restrict__ sptr,
                                                    const int* __restrict__ scol,
                                                    const double* __restrict__ sval,
                                                    const double* __restrict__ f, double* u,
@@ -88,9 +88,14 @@ __global__ void __launch_bounds__(256) k_gs_colour(int r0, int r1, const int64_t
     int64_t base = 0;
     double d = 1.0;
     if (live) {
-        const int64_t s0 = sptr[r >> 5];
-        w = (int)((sptr[(r >> 5) + 1] - s0) >> 5);
-        base = s0 + (r & 31);
+        if (Wu > 0) {  // every slice has width Wu (level 0): the slice offset needs no load
+            w = Wu;
+            base = (int64_t)(r >> 5) * 32 * Wu + (r & 31);
+        } else {
+            const int64_t s0 = sptr[r >> 5];
+            w = (int)((sptr[(r >> 5) + 1] - s0) >> 5);
+            base = s0 + (r & 31);
+        }
         fr.load(sval + base, scol + base, w, part);
         d = ld_stream_f64(sval + base);
     } else {
