@@ -124,6 +124,80 @@ def oracle_sample(steps: int, warmup: int):
                            f"(O(N) cost, P:588)")
 
 
+def stage_breakdown(w, f, hbm):
+    """Stage times of the V-cycle graph (MGM_TRACE instance, 20 cycles averaged) with the
+    algorithmic bytes of each stage (DESIGN.md section 6 byte model) and the one-kernel
+    bottom's share; the bottom is latency-bound, its GB/s is reported against HBM anyway."""
+    import numpy as np
+    import torch
+    from paper_2204_06154_b200 import MGM, mgm_trace_read
+
+    os.environ["MGM_TRACE"] = "1"
+    try:
+        mt = MGM(w.points, w.normals, w.stencil, w.levels)
+    finally:
+        os.environ.pop("MGM_TRACE", None)
+    lv = mt.level_info()
+    u = torch.zeros_like(f)
+    for _ in range(3):
+        mt.vcycle(f, u)
+    acc = None
+    for _ in range(20):
+        mt.vcycle(f, u)
+        torch.cuda.synchronize()
+        tr = mgm_trace_read(mt.ctx)
+        d = np.diff([t for _, t in tr]) / 1e3
+        acc = d if acc is None else acc + d
+    acc = acc / 20
+    labels = [lab for lab, _ in tr[1:]]
+    nu1, nu2 = w.levels.get("nu1", 1), w.levels.get("nu2", 1)
+
+    def sweep_b(j, nsw):
+        return nsw * (12.0 * lv[j]["nnz"] + 24.0 * lv[j]["n"])
+
+    def bytes_of(lab):
+        name, jl = lab.rsplit(" L", 1)
+        j = int(jl)
+        if name == "presmooth":
+            return sweep_b(j, nu1)
+        if name == "residual":
+            return 12.0 * lv[j]["nnz"] + 32.0 * lv[j]["n"]
+        if name == "restrict":
+            return 12.0 * lv[j]["nnz_P"] + 8.0 * lv[j]["n"] + 8.0 * lv[j + 1]["n"]
+        if name == "zero+presmooth":
+            return 8.0 * lv[j]["n"] + sweep_b(j, nu1)
+        if name == "residual+restrict":
+            return 12.0 * lv[j]["nnz"] + 32.0 * lv[j]["n"] + 12.0 * lv[j]["nnz_P"] + 8.0 * lv[j]["n"] + 8.0 * lv[j + 1]["n"]
+        if name == "interp":
+            return 12.0 * lv[j]["nnz_P"] + 8.0 * lv[j + 1]["n"] + 16.0 * lv[j]["n"]
+        if name == "interp+postsmooth":
+            return 12.0 * lv[j]["nnz_P"] + 8.0 * lv[j + 1]["n"] + 16.0 * lv[j]["n"] + sweep_b(j, nu2)
+        if name == "postsmooth":
+            return sweep_b(j, nu2)
+        if name == "bottom":  # levels j..p-1: sweeps, residuals, transfers, dense coarse solve
+            b = 0.0
+            for q in range(j, len(lv) - 1):
+                b += sweep_b(q, nu1 + nu2) + 12.0 * lv[q]["nnz"] + 32.0 * lv[q]["n"]
+                b += 2 * (12.0 * lv[q]["nnz_P"] + 8.0 * lv[q + 1]["n"]) + 24.0 * lv[q]["n"]
+            nc = lv[-1]["n"]
+            return b + 12.0 * nc * nc + 16.0 * nc
+        return 0.0
+
+    total = float(acc.sum())
+    out, bottom = [], None
+    for lab, us in zip(labels, acc):
+        b = bytes_of(lab)
+        gbs = b / (us * 1e-6) / 1e9 if us > 0 else None
+        out.append({"stage": lab, "us": round(float(us), 2), "share": round(float(us) / total, 4),
+                    "alg_MB": round(b / 1e6, 2), "GBps": round(gbs, 1) if gbs else None})
+        if lab.startswith("bottom"):
+            bottom = {"bound": "latency (cluster barrier per colour step)", "kernel": "k_vcycle_bottom",
+                      "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm if gbs else None,
+                      "share_of_vcycle": float(us) / total, "us": float(us)}
+    mt.close()
+    return out, bottom
+
+
 def run_reference(args):
     ws, rank, _ = _dist()
     if rank != 0:
@@ -152,6 +226,7 @@ def main():
     ap.add_argument("--n", type=int, default=None)
     ap.add_argument("--method", default="rbffd", choices=["rbffd", "gfd"], help="cfg 2 only: RBF-FD or GFD")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-stages", action="store_true", help="skip the traced per-stage V-cycle breakdown")
     ap.add_argument("--parallel", choices=["replicas", "dist"], default="replicas",
                     help="N>1: independent replicas of the solve (weak scaling) or one solve "
                          "split across the ranks (mgm_dist_attach, strong scaling)")
@@ -286,6 +361,12 @@ def main():
     except Exception:
         pass
 
+    # ---- per-stage V-cycle breakdown (a second, traced instance: %globaltimer stamps between
+    # the stages of Alg. 3 inside the graph), with each stage's algorithmic bytes
+    stages, bottom = None, None
+    if not args.no_stages and ws == 1:
+        stages, bottom = stage_breakdown(w, f, hbm)
+
     vk = mgm_vcycle_kernel_count(m.ctx)
     # kernels per solve: per Arnoldi step the V-cycle graph (vk) + SpMV + 5 CGS2 kernels;
     # start: dot + scale; end: lincomb + V-cycle + axpby, true residual SpMV + axpby + dot
@@ -319,6 +400,8 @@ def main():
                          "traffic": traffic, "alg_bytes_per_launch": alg_per_launch,
                          "launches_timed": tk["launches"], "avg_launch_us": launch_avg_us},
             "other_solvers": others,
+            "vcycle_stages": stages,
+            "roofline_bottom": bottom,
             "e2e": {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": 8 * N,
                     "d2h_bytes_per_step": 8 * N},
             "gpu_launches": per_step * args.steps,

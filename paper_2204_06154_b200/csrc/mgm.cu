@@ -902,6 +902,10 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
                 i64 nn = Lm[j + 1].nrows;
                 double wavg = (double)L.r_stored / (double)std::max<i64>(1, (nn + 31) / 32 * 32);
                 L.rtpr = wavg <= 12 ? 1 : (wavg <= 40 ? 2 : 4);
+                if (const char* e = std::getenv("MGM_RTPR")) {  // tuning experiment
+                    const int t = std::atoi(e);
+                    if (t == 1 || t == 2 || t == 4 || t == 8) L.rtpr = t;
+                }
             }
             if ((s = upload(ctx, &L.rptr, rptr)) || (s = upload(ctx, &L.rcol, rcol)) || (s = upload(ctx, &L.rval, rval)))
                 return s;
