@@ -55,6 +55,38 @@ def fibonacci_sphere(n: int, jitter: float = 0.0, seed: int = 0):
     return np.ascontiguousarray(x), np.ascontiguousarray(x.copy())
 
 
+def icosahedral_sphere(level: int):
+    """Icosahedral node set on the unit sphere (the paper's sphere clouds): the 12
+    vertices of an icosahedron, each triangle recursively split into four by edge midpoints
+    projected to the sphere, `level` times: N = 10 * 4**level + 2.  Normals are the points.
+    Deterministic; no method arithmetic."""
+    t = (1.0 + math.sqrt(5.0)) / 2.0
+    v = [(-1, t, 0), (1, t, 0), (-1, -t, 0), (1, -t, 0), (0, -1, t), (0, 1, t), (0, -1, -t), (0, 1, -t),
+         (t, 0, -1), (t, 0, 1), (-t, 0, -1), (-t, 0, 1)]
+    verts = [np.array(p, dtype=np.float64) / np.linalg.norm(p) for p in v]
+    faces = [(0, 11, 5), (0, 5, 1), (0, 1, 7), (0, 7, 10), (0, 10, 11), (1, 5, 9), (5, 11, 4), (11, 10, 2),
+             (10, 7, 6), (7, 1, 8), (3, 9, 4), (3, 4, 2), (3, 2, 6), (3, 6, 8), (3, 8, 9), (4, 9, 5),
+             (2, 4, 11), (6, 2, 10), (8, 6, 7), (9, 8, 1)]
+    for _ in range(level):
+        cache = {}
+
+        def mid(a, b):
+            key = (min(a, b), max(a, b))
+            if key not in cache:
+                m = verts[a] + verts[b]
+                verts.append(m / np.linalg.norm(m))
+                cache[key] = len(verts) - 1
+            return cache[key]
+
+        nf = []
+        for a, b, c in faces:
+            ab, bc, ca = mid(a, b), mid(b, c), mid(c, a)
+            nf += [(a, ab, ca), (b, bc, ab), (c, ca, bc), (ab, bc, ca)]
+        faces = nf
+    x = np.ascontiguousarray(np.array(verts))
+    return x, x.copy()
+
+
 def _thin_nearest_pairs(x: np.ndarray, n_remove: int) -> np.ndarray:
     """Remove ``n_remove`` points, walking points by ascending nearest-neighbour distance
     and removing a point unless it is protected; removing a point protects its nearest

@@ -286,6 +286,17 @@ def greedy_colour(A: CSR):
     return col, int(nc.value)
 
 
+def rcm_order(A: CSR) -> np.ndarray:
+    """Reverse Cuthill-McKee ordering of sym(pattern(A)) (scipy's implementation):
+    the row order of the paper's lexicographic Gauss-Seidel (calibration variant)."""
+    import scipy.sparse as sps
+    from scipy.sparse.csgraph import reverse_cuthill_mckee
+
+    n = A.shape[0]
+    M = sps.csr_matrix((np.ones(len(A.idx)), A.idx, A.ptr), shape=(n, n))
+    return np.ascontiguousarray(reverse_cuthill_mckee((M + M.T).tocsr(), symmetric_mode=True), dtype=np.int64)
+
+
 def gs_sweep(A: CSR, order: np.ndarray, f, u, backward=False, c=None, lam=0.0):
     """O12 one GS sweep in the given row order, in place on u."""
     fail = ctypes.c_int64(-1)
@@ -365,7 +376,8 @@ class Oracle:
     """Reference MGM hierarchy + solvers.  Vectors at the public API are in the caller's
     original point order (like the C ABI); internally level order is Morton (O1)."""
 
-    def __init__(self, points, normals, stencil: dict | None = None, levels: dict | None = None):
+    def __init__(self, points, normals, stencil: dict | None = None, levels: dict | None = None,
+                 fine_weights=None):
         sp = dict(DEFAULT_STENCIL, **(stencil or {}))
         lp = dict(DEFAULT_LEVELS, **(levels or {}))
         self.sp, self.lp = sp, lp
@@ -386,7 +398,9 @@ class Oracle:
         ns = sp["stencil_n"]
         sten = knn(X, X, ns)
         self.stencil = sten
-        if sp["method"] == 0:
+        if fine_weights is not None:  # experiments with other weight readings (Morton order rows)
+            W = np.ascontiguousarray(fine_weights(X, nrm, sten), dtype=np.float64)
+        elif sp["method"] == 0:
             W = rbffd_weights(X, nrm, sten, sp["poly_degree"], sp["phs_k"])
         else:
             W = gfd_weights(X, nrm, sten, sp["poly_degree"], sp["gfd_alpha"])
@@ -410,7 +424,12 @@ class Oracle:
             self.levels.append(nxt)
         for lv in self.levels[:-1]:
             lv.colour, lv.ncolours = greedy_colour(lv.L)
-            lv.order = np.lexsort((np.arange(lv.N), lv.colour)).astype(np.int64)
+            if lp.get("gs_order", "colour") == "rcm":
+                # the paper's own smoother (Alg. 2 lines 2-3 and 11-12):
+                # lexicographic Gauss-Seidel in reverse Cuthill-McKee order of L_j
+                lv.order = rcm_order(lv.L)
+            else:
+                lv.order = np.lexsort((np.arange(lv.N), lv.colour)).astype(np.int64)
         # coarsest factorisation (Alg. 2 line 13, P:293 / P:354-355), dense (O13)
         last = self.levels[-1]
         Ad = last.L.dense()

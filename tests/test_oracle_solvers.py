@@ -247,3 +247,39 @@ def test_mgm_bicgstab_matches_dense_direct_solve_and_gmres():
         else:
             xr = np.empty(900); xr[h.perm] = np.linalg.solve(A, f[h.perm])
         assert np.linalg.norm(x - xr) / np.linalg.norm(xr) < 1e-9
+
+
+# ------------------------------------------------------------------ paper calibration (Table 2)
+@pytest.mark.parametrize("level,ell,paper_gmres,paper_bicgstab", [
+    (5, 3, 18, 19),     # N = 10242
+    (5, 5, 18, 18),
+    (6, 3, 19, 19),     # N = 40962
+])
+def test_paper_table2_iteration_counts(level, ell, paper_gmres, paper_bicgstab):
+    """The oracle with the paper's OWN settings (Table 1):
+    icosahedral sphere nodes, RBF-FD with k = l and n = (l+1)(l+2),
+    m = 3, N_min = 250, one forward Gauss-Seidel sweep pre and post in RCM
+    order, shifted Poisson (mu = 1, O6), tolerance 1e-12 --
+    reproduces the MGM columns of Table 2, GMRES iterations and BiCGSTAB
+    preconditioner applications, within one iteration (the right-hand side is not stated;
+    a seeded uniform one is used)."""
+    x, nrm = MI.icosahedral_sphere(level)
+    n = (ell + 1) * (ell + 2)
+    st = dict(method=0, poly_degree=ell, phs_k=ell, stencil_n=n, problem=0, mu=1.0)
+    lv = dict(num_levels=0, n_min=250, interp_m=3, nu1=1, nu2=1, smoother=0, gs_order="rcm")
+    h = O.Oracle(x, nrm, st, lv)
+    f = np.random.default_rng(0).uniform(-1, 1, len(x))
+    _, rg = h.solve(f, tol=1e-12, krylov=1)
+    _, rb = h.solve(f, tol=1e-12, krylov=2)
+    assert rg.converged and rb.converged
+    assert abs(rg.iterations - paper_gmres) <= 1, rg.iterations
+    assert abs(rb.iterations - paper_bicgstab) <= 1, rb.iterations
+
+
+def test_icosahedral_nodes():
+    """N = 10 * 4^level + 2 distinct unit vectors."""
+    for level in (0, 1, 3):
+        x, nrm = MI.icosahedral_sphere(level)
+        assert len(x) == 10 * 4 ** level + 2
+        assert np.allclose(np.linalg.norm(x, axis=1), 1.0, atol=1e-15)
+        assert len(np.unique(np.round(x, 12), axis=0)) == len(x)
