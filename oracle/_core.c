@@ -411,7 +411,8 @@ static int cmp_double(const void* a, const void* b) {
     double x = *(const double*)a, y = *(const double*)b;
     return (x < y) ? -1 : (x > y);
 }
-typedef struct { i64 w; i64 idx; } heapent;
+typedef int64_t wse_w;  /* O8: fixed-point weights, 2^40 per unit */
+typedef struct { wse_w w; i64 idx; } heapent;
 /* max-heap on (w desc, idx asc) */
 static int he_less(heapent a, heapent b) {  /* a has lower priority than b */
     if (a.w != b.w) return a.w < b.w;
@@ -438,16 +439,10 @@ static heapent heap_pop(heapent* h, i64* sz) {
     }
     return top;
 }
-int orc_wse(const double* pts, i64 n, i64 nt, const double* nn2, i64* keep /* nt */) {
-    if (nt <= 0 || nt > n) return -1;
-    if (nt == n) { for (i64 i = 0; i < n; ++i) keep[i] = i; return 0; }
-    double* s = (double*)malloc(sizeof(double) * n);
-    for (i64 i = 0; i < n; ++i) s[i] = sqrt(nn2[i]);
-    qsort(s, (size_t)n, sizeof(double), cmp_double);
-    double rh = 0.5 * s[(n - 1) / 2];
-    free(s);
-    double rmax = rh * sqrt((double)n / (double)nt);
-    double R = 2.0 * rmax;
+/* One elimination pass with weight radius R.  Returns 0 (keep filled), 1 if the pass had to
+ * eliminate a point of zero weight (no live neighbour within R: the weight no longer ranks
+ * the points and index ties would decide, wiping out the lowest-index region), -3 on error. */
+static int wse_pass(const double* pts, i64 n, i64 nt, double R, i64* keep) {
     /* uniform grid with cell size >= R: all pairs with d < R lie in adjacent cells */
     double lo[3] = {pts[0], pts[1], pts[2]}, hi[3] = {pts[0], pts[1], pts[2]};
     for (i64 i = 0; i < n; ++i)
@@ -489,8 +484,8 @@ int orc_wse(const double* pts, i64 n, i64 nt, const double* nn2, i64* keep /* nt
     i64 cap = 32 * n, nnz = 0;
     i64* nptr = (i64*)malloc(sizeof(i64) * (n + 1));
     i64* nidx = (i64*)malloc(sizeof(i64) * cap);
-    i64* nw = (i64*)malloc(sizeof(i64) * cap);
-    i64* weight = (i64*)calloc((size_t)n, sizeof(i64));
+    wse_w* nw = (wse_w*)malloc(sizeof(wse_w) * cap);
+    wse_w* weight = (wse_w*)calloc((size_t)n, sizeof(wse_w));
     for (i64 i = 0; i < n; ++i) {
         nptr[i] = nnz;
         i64 cx = cell[i] % dims[0], cy = (cell[i] / dims[0]) % dims[1], cz = cell[i] / (dims[0] * dims[1]);
@@ -508,11 +503,11 @@ int orc_wse(const double* pts, i64 n, i64 nt, const double* nn2, i64* keep /* nt
                         if (!(d < R)) continue;
                         double u = 1.0 - d / R;
                         double u2 = u * u, u4 = u2 * u2, u8 = u4 * u4;
-                        i64 W = (i64)floor(u8 * 1099511627776.0 + 0.5);
+                        wse_w W = (wse_w)floor(u8 * 1099511627776.0 + 0.5);  /* 2^40 */
                         if (nnz == cap) {
                             cap *= 2;
                             nidx = (i64*)realloc(nidx, sizeof(i64) * cap);
-                            nw = (i64*)realloc(nw, sizeof(i64) * cap);
+                            nw = (wse_w*)realloc(nw, sizeof(wse_w) * cap);
                         }
                         nidx[nnz] = j; nw[nnz] = W; ++nnz;
                         weight[i] += W;
@@ -532,6 +527,10 @@ int orc_wse(const double* pts, i64 n, i64 nt, const double* nn2, i64* keep /* nt
     while (removed < n - nt) {
         heapent e = heap_pop(h, &hs);
         if (dead[e.idx] || e.w != weight[e.idx]) continue;  /* stale entry */
+        if (e.w == 0) {  /* degenerate: R too small for this cloud (O8) */
+            free(h); free(dead); free(nptr); free(nidx); free(nw); free(weight);
+            return 1;
+        }
         dead[e.idx] = 1;
         ++removed;
         for (i64 t = nptr[e.idx]; t < nptr[e.idx + 1]; ++t) {
@@ -546,6 +545,24 @@ int orc_wse(const double* pts, i64 n, i64 nt, const double* nn2, i64* keep /* nt
     for (i64 i = 0; i < n; ++i) if (!dead[i]) keep[c++] = i;
     free(h); free(dead); free(nptr); free(nidx); free(nw); free(weight);
     return (c == nt) ? 0 : -3;
+}
+
+int orc_wse(const double* pts, i64 n, i64 nt, const double* nn2, i64* keep /* nt */) {
+    if (nt <= 0 || nt > n) return -1;
+    if (nt == n) { for (i64 i = 0; i < n; ++i) keep[i] = i; return 0; }
+    double* s = (double*)malloc(sizeof(double) * n);
+    for (i64 i = 0; i < n; ++i) s[i] = sqrt(nn2[i]);
+    qsort(s, (size_t)n, sizeof(double), cmp_double);
+    double rh = 0.5 * s[(n - 1) / 2];
+    free(s);
+    double rmax = rh * sqrt((double)n / (double)nt);
+    /* O8: R = 2 r_max; if a pass degenerates (zero-weight elimination), R *= 1.25 and restart */
+    double R = 2.0 * rmax;
+    for (int attempt = 0; attempt < 16; ++attempt, R *= 1.25) {
+        int rc = wse_pass(pts, n, nt, R, keep);
+        if (rc != 1) return rc;
+    }
+    return -4;
 }
 
 /* ------------------------------------------------------------------------------------

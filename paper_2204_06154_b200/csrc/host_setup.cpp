@@ -243,26 +243,18 @@ i64 nearest_other(const double* pts, i64 n, std::vector<double>& nn2, int nthrea
 // ---------------------------------------------------------------------------------------
 // O8: weighted sample elimination (Yuksel 2015), fixed-point weights.
 // ---------------------------------------------------------------------------------------
-void wse_eliminate(const double* pts, i64 n, i64 nt, const std::vector<double>& nn2,
-                   std::vector<i64>& keep, int nthreads) {
+// One elimination pass with weight radius R; false if it would have to eliminate a point of
+// zero weight (no live neighbour within R: index ties would then decide and wipe out the
+// lowest-index region), in which case the caller enlarges R.
+static bool wse_pass(const double* pts, i64 n, i64 nt, double R, std::vector<i64>& keep, int nthreads) {
     keep.clear();
-    if (nt >= n) {
-        for (i64 i = 0; i < n; ++i) keep.push_back(i);
-        return;
-    }
-    std::vector<double> s(n);
-    for (i64 i = 0; i < n; ++i) s[i] = std::sqrt(nn2[i]);
-    std::nth_element(s.begin(), s.begin() + (n - 1) / 2, s.end());
-    double rh = 0.5 * s[(n - 1) / 2];
-    double rmax = rh * std::sqrt((double)n / (double)nt);
-    double R = 2.0 * rmax;
-
     Grid g;
     g.build(pts, n, std::max(R, default_cell(pts, n, 8)));
     // neighbour lists per thread chunk, then concatenated (CSR)
     int nt_threads = std::max(1, nthreads);
     std::vector<std::vector<i32>> nj(nt_threads);
-    std::vector<std::vector<i64>> nw(nt_threads);
+    using wse_w = i64;  // O8: fixed-point weights, 2^40 per unit
+    std::vector<std::vector<wse_w>> nw(nt_threads);
     std::vector<i64> cnt(n, 0);
     i64 chunk = (n + nt_threads - 1) / nt_threads;
     std::vector<std::thread> th;
@@ -289,7 +281,7 @@ void wse_eliminate(const double* pts, i64 n, i64 nt, const std::vector<double>& 
                                 double u2 = u * u;
                                 double u4 = u2 * u2;
                                 double u8 = u4 * u4;
-                                i64 W = (i64)std::floor(u8 * 1099511627776.0 + 0.5);
+                                wse_w W = (wse_w)std::floor(u8 * 1099511627776.0 + 0.5);  // 2^40
                                 nj[t].push_back(j);
                                 nw[t].push_back(W);
                                 cnt[i]++;
@@ -304,7 +296,7 @@ void wse_eliminate(const double* pts, i64 n, i64 nt, const std::vector<double>& 
     std::vector<i64> ptr(n + 1, 0);
     for (i64 i = 0; i < n; ++i) ptr[i + 1] = ptr[i] + cnt[i];
     std::vector<i32> adj(ptr[n]);
-    std::vector<i64> adjw(ptr[n]);
+    std::vector<wse_w> adjw(ptr[n]);
     {
         i64 o = 0;
         for (int t = 0; t < (int)nj.size(); ++t) {
@@ -313,7 +305,7 @@ void wse_eliminate(const double* pts, i64 n, i64 nt, const std::vector<double>& 
             o += (i64)nj[t].size();
         }
     }
-    std::vector<i64> weight(n, 0);
+    std::vector<wse_w> weight(n, 0);
     for (i64 i = 0; i < n; ++i)
         for (i64 t = ptr[i]; t < ptr[i + 1]; ++t) weight[i] += adjw[t];
 
@@ -350,6 +342,7 @@ void wse_eliminate(const double* pts, i64 n, i64 nt, const std::vector<double>& 
     std::vector<uint8_t> dead(n, 0);
     for (i64 it = 0; it < n - nt; ++it) {
         i32 a = heap[0];
+        if (weight[a] == 0) return false;  // degenerate: R too small for this cloud (O8)
         dead[a] = 1;
         heap[0] = heap[hs - 1];
         pos[heap[0]] = 0;
@@ -366,6 +359,25 @@ void wse_eliminate(const double* pts, i64 n, i64 nt, const std::vector<double>& 
     keep.reserve(nt);
     for (i64 i = 0; i < n; ++i)
         if (!dead[i]) keep.push_back(i);
+    return true;
+}
+
+void wse_eliminate(const double* pts, i64 n, i64 nt, const std::vector<double>& nn2,
+                   std::vector<i64>& keep, int nthreads) {
+    keep.clear();
+    if (nt >= n) {
+        for (i64 i = 0; i < n; ++i) keep.push_back(i);
+        return;
+    }
+    std::vector<double> s(n);
+    for (i64 i = 0; i < n; ++i) s[i] = std::sqrt(nn2[i]);
+    std::nth_element(s.begin(), s.begin() + (n - 1) / 2, s.end());
+    double rh = 0.5 * s[(n - 1) / 2];
+    double rmax = rh * std::sqrt((double)n / (double)nt);
+    // O8: R = 2 r_max; a degenerate pass (zero-weight elimination) restarts with R *= 1.25
+    double R = 2.0 * rmax;
+    for (int attempt = 0; attempt < 16; ++attempt, R *= 1.25)
+        if (wse_pass(pts, n, nt, R, keep, nthreads)) return;
 }
 
 // ---------------------------------------------------------------------------------------

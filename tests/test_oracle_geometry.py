@@ -110,26 +110,39 @@ def test_tangent_projection_contracts_on_sphere():
 
 # ---------------------------------------------------------------- WSE (O8)
 def _wse_brute(pts, nt):
-    """Literal O(N^2) weighted sample elimination on tiny inputs (no grid, no heap)."""
+    """Literal O(N^2) weighted sample elimination on tiny inputs (no grid, no heap), O8:
+    integer weights (2^40 fixed point), ties to the lowest index, and a pass that would
+    eliminate a zero-weight point restarts with R * 1.25."""
     n = len(pts)
     d = np.sqrt(((pts[:, None, :] - pts[None, :, :]) ** 2).sum(2))
     dd = d + np.diag(np.full(n, np.inf))
     nn = np.sort(dd.min(1))
     rh = 0.5 * nn[(n - 1) // 2]
     R = 2.0 * rh * np.sqrt(n / nt)
-    W = np.zeros((n, n), dtype=np.int64)
-    for i in range(n):
-        for j in range(n):
-            if i != j and d[i, j] < R:
-                W[i, j] = int(np.floor((1.0 - d[i, j] / R) ** 8 * 2.0 ** 40 + 0.5))
-    weight = W.sum(1)
-    alive = np.ones(n, dtype=bool)
-    for _ in range(n - nt):
-        cand = np.flatnonzero(alive)
-        best = cand[np.argmax(weight[cand])]   # argmax returns the lowest index on ties
-        alive[best] = False
-        weight -= W[:, best]
-    return np.flatnonzero(alive)
+    for _ in range(16):
+        W = [[0] * n for _ in range(n)]
+        for i in range(n):
+            for j in range(n):
+                if i != j and d[i, j] < R:
+                    u = 1.0 - d[i, j] / R
+                    u2 = u * u
+                    u4 = u2 * u2
+                    W[i][j] = int(np.floor(u4 * u4 * 2.0 ** 40 + 0.5))
+        weight = [sum(row) for row in W]
+        alive = [True] * n
+        ok = True
+        for _ in range(n - nt):
+            best = max((i for i in range(n) if alive[i]), key=lambda i: (weight[i], -i))  # ties: lowest index
+            if weight[best] == 0:
+                ok = False
+                break
+            alive[best] = False
+            for i in range(n):
+                weight[i] -= W[i][best]
+        if ok:
+            return np.flatnonzero(alive)
+        R *= 1.25
+    raise RuntimeError("no pass")
 
 
 @pytest.mark.parametrize("n", [60, 157, 300])
@@ -176,3 +189,18 @@ def test_level_rule_examples():
         assert int(np.floor(np.log(N / nmin) / np.log(4))) + 1 == p
         Np = N // 4 ** (p - 1)
         assert nmin <= Np < 4 * nmin
+
+
+def test_wse_covers_irregular_cloud():
+    """O8 degenerate passes: on the quartic cloud (cfg4 recipe) the median-spacing radius is
+    too small, the elimination reaches points with no live neighbour (zero weight) and index
+    ties then wiped out the lowest-Morton corner (a 38-spacing hole).  The restart rule
+    (R *= 1.25) keeps the coarse set covering the surface (quasi-uniform subsets)."""
+    from scipy.spatial import cKDTree
+
+    w = MI.make_workload(4, n=16384)
+    x = w.points[O.morton_perm(w.points)]
+    keep = O.wse(x, len(x) // 4)
+    d, _ = cKDTree(x[keep]).query(x)
+    dn, _ = cKDTree(x).query(x, k=2)
+    assert d.max() < 5.0 * np.median(dn[:, 1])
