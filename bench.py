@@ -323,6 +323,36 @@ def main():
         others[name] = {"ms": e0.elapsed_time(e1), "iterations": rk.iterations, "converged": bool(rk.converged),
                         "final_rel_residual": rk.final_rel_residual}
 
+    # ---- multi-right-hand-side throughput: K columns per operator pass
+    multi = {}
+    if ws == 1 and not args.no_stages:
+        from paper_2204_06154_b200 import mgm_solve_batch, mgm_vcycle_batch
+
+        for K in (4, 8):
+            FK = torch.from_numpy(np.random.default_rng(K).uniform(-1, 1, (K, N))).cuda()
+            UK = torch.zeros_like(FK)
+            for _ in range(3):
+                mgm_vcycle_batch(m.ctx, K, FK, UK)
+            barrier()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            for _ in range(10):
+                mgm_vcycle_batch(m.ctx, K, FK, UK)
+            e1.record(st)
+            barrier()
+            vck = e0.elapsed_time(e1) / 10
+            RK = torch.from_numpy(np.stack([w.rhs] * K)).cuda()
+            XK = torch.zeros_like(RK)
+            e0.record(st)
+            reps = mgm_solve_batch(m.ctx, K, RK, XK, tol=1e-10, maxit=300)
+            e1.record(st)
+            barrier()
+            multi[K] = {"vcycle_ms": vck, "vcycle_ms_per_rhs": vck / K,
+                        "standalone_ms": e0.elapsed_time(e1), "standalone_ms_per_rhs": e0.elapsed_time(e1) / K,
+                        "iterations": max(r.iterations for r in reps),
+                        "all_converged": all(r.converged for r in reps)}
+
     # ---- V-cycle throughput (graph-replayed V-cycles on device vectors)
     bm = mgm_bytes_model(m.ctx)
     f = torch.from_numpy(np.random.default_rng(0).uniform(-1, 1, N)).cuda()
@@ -401,6 +431,7 @@ def main():
                          "launches_timed": tk["launches"], "avg_launch_us": launch_avg_us},
             "other_solvers": others,
             "vcycle_stages": stages,
+            "multi_rhs": multi,
             "roofline_bottom": bottom,
             "e2e": {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": 8 * N,
                     "d2h_bytes_per_step": 8 * N},

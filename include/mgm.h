@@ -116,6 +116,24 @@ mgm_status mgm_solve_host(mgm_ctx* ctx, const double* rhs_host, double* x_host, 
 
 mgm_status mgm_destroy(mgm_ctx* ctx);
 
+/* ---- multi-right-hand-side solves (the paper's applications solve
+ * many systems with one operator) ---------------------------------
+ * K right-hand sides share every pass over the operators: each colour kernel, SpMV and
+ * transfer reads its operator once for all K (vectors interleaved [row][K] inside; widths
+ * 2, 4, 8 -- K is padded with zero columns).  The per-(row, RHS) arithmetic is that of the
+ * single-RHS kernels, so each column of a batched V-cycle equals a single V-cycle (up to
+ * the coarsest solve, which uses the explicit inverse of L_p).  Shifted problems, one GPU,
+ * coarsest level <= 4096 rows; otherwise MGM_ERR_ARG.
+ * f_dev, u_dev, rhs_dev, x_dev: device, K column-major vectors of n_points fp64 in
+ * original order (column k at ptr + k*n_points).
+ * mgm_vcycle_batch: one V-cycle per column (u in: guess, out: result).
+ * mgm_solve_batch: standalone MGM on every column from x = 0 until every column's
+ * ||f - L x|| / ||f|| <= tol or maxit; reports[K] (may be NULL): iterations = the first
+ * cycle at which that column met tol, final_rel_residual after the last cycle. */
+mgm_status mgm_vcycle_batch(mgm_ctx* ctx, int K, const double* f_dev, double* u_dev, void* cuda_stream);
+mgm_status mgm_solve_batch(mgm_ctx* ctx, int K, const double* rhs_dev, double* x_dev, double tol, int maxit,
+                           mgm_report* reports, void* cuda_stream);
+
 /* ---- multi-GPU ----------------------------------
  * One process per GPU.  Every rank calls mgm_setup with the SAME cloud and parameters (the
  * setup is deterministic, so all ranks hold identical hierarchies), then mgm_dist_attach.

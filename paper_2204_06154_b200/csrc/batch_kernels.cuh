@@ -1,0 +1,217 @@
+// Multi-right-hand-side (batched) solve kernels: one pass over an
+// operator serves K right-hand sides.  Batched vectors are interleaved, row-major [row][K]
+// in lib order, so the K values a gather needs are contiguous (one 32-byte sector for K = 4).
+// The arithmetic per (row, right-hand side) is exactly that of the single-RHS kernels
+// (same threads-per-row split, same summation order), so a batched V-cycle reproduces K
+// single V-cycles.  Shifted problems only.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "solve_kernels.cuh"
+
+namespace mgm {
+
+// One colour of a Gauss-Seidel sweep for K right-hand sides (cf. k_gs_colour).
+template <int TPR, int CH, int K>
+__global__ void __launch_bounds__(256) k_gs_colour_b(int r0, int r1, int Wu, const int64_t* __restrict__ sptr,
+                                                     const int* __restrict__ scol, const double* __restrict__ sval,
+                                                     const double* __restrict__ f, double* u) {
+    pdl_trigger();
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    const int r = (r0 & ~31) + g / TPR;
+    const int part = g % TPR;
+    const bool live = (r >= r0 && r < r1);
+    RowFrag<TPR, CH> fr;
+    int w = 0;
+    int64_t base = 0;
+    double d = 1.0;
+    if (live) {
+        if (Wu > 0) {
+            w = Wu;
+            base = (int64_t)(r >> 5) * 32 * Wu + (r & 31);
+        } else {
+            const int64_t s0 = sptr[r >> 5];
+            w = (int)((sptr[(r >> 5) + 1] - s0) >> 5);
+            base = s0 + (r & 31);
+        }
+        fr.load(sval + base, scol + base, w, part);
+        d = ld_stream_f64(sval + base);
+    } else {
+        fr.load(sval, scol, 0, 0);
+    }
+    pdl_wait();
+    double fv[K], uv[K], acc[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        fv[k] = 0.0;
+        uv[k] = 0.0;
+        acc[k] = 0.0;
+    }
+    if (live && part == 0) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            fv[k] = f[(int64_t)r * K + k];
+            uv[k] = u[(int64_t)r * K + k];
+        }
+    }
+    for (int k0 = part;; k0 += TPR * CH) {
+        if (k0 != part) fr.load(sval + base, scol + base, w, k0);
+#pragma unroll
+        for (int q = 0; q < CH; ++q)
+            if (fr.c[q] >= 0) {
+                const double* xr = u + (int64_t)fr.c[q] * K;
+#pragma unroll
+                for (int k = 0; k < K; ++k) acc[k] = fma(fr.a[q], xr[k], acc[k]);
+            }
+        if (k0 + TPR * CH >= w) break;
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) acc[k] = group_sum<TPR>(acc[k]);
+    if (live && part == 0) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) u[(int64_t)r * K + k] = uv[k] + (fv[k] - acc[k]) / d;
+    }
+}
+
+// y = A x (MODE 0), y = f - A x (MODE 1) for K right-hand sides on the rows [r0, r1).
+template <int MODE, int TPR, int CH, int K>
+__global__ void __launch_bounds__(256) k_sell_spmv_b(int r0, int r1, const int64_t* __restrict__ sptr,
+                                                     const int* __restrict__ scol, const double* __restrict__ sval,
+                                                     const double* __restrict__ x, const double* __restrict__ f,
+                                                     double* __restrict__ y) {
+    pdl_trigger();
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    const int r = (r0 & ~31) + g / TPR;
+    const int part = g % TPR;
+    const bool live = r >= r0 && r < r1;
+    RowFrag<TPR, CH> fr;
+    int w = 0;
+    int64_t base = 0;
+    if (live) {
+        const int64_t s0 = sptr[r >> 5];
+        w = (int)((sptr[(r >> 5) + 1] - s0) >> 5);
+        base = s0 + (r & 31);
+        fr.load(sval + base, scol + base, w, part);
+    } else {
+        fr.load(sval, scol, 0, 0);
+    }
+    pdl_wait();
+    double acc[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) acc[k] = 0.0;
+    for (int k0 = part;; k0 += TPR * CH) {
+        if (k0 != part) fr.load(sval + base, scol + base, w, k0);
+#pragma unroll
+        for (int q = 0; q < CH; ++q)
+            if (fr.c[q] >= 0) {
+                const double* xr = x + (int64_t)fr.c[q] * K;
+#pragma unroll
+                for (int k = 0; k < K; ++k) acc[k] = fma(fr.a[q], xr[k], acc[k]);
+            }
+        if (k0 + TPR * CH >= w) break;
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) acc[k] = group_sum<TPR>(acc[k]);
+    if (live && part == 0) {
+#pragma unroll
+        for (int k = 0; k < K; ++k)
+            y[(int64_t)r * K + k] = (MODE == 0) ? acc[k] : f[(int64_t)r * K + k] - acc[k];
+    }
+}
+
+// e += P ec for K right-hand sides (interpolate + correct), rows [0, n)
+template <int M, int K>
+__global__ void __launch_bounds__(256) k_interp_correct_b(int n, int m, const int* __restrict__ pcol,
+                                                          const double* __restrict__ pval,
+                                                          const double* __restrict__ ec, double* __restrict__ e) {
+    pdl_trigger();
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    int cidx[M];
+    double a[M];
+#pragma unroll
+    for (int q = 0; q < M; ++q) {
+        const bool ok = r < n && q < m;
+        cidx[q] = ok ? ld_stream_i32(pcol + (int64_t)q * n + r) : -1;
+        a[q] = ok ? ld_stream_f64(pval + (int64_t)q * n + r) : 0.0;
+    }
+    pdl_wait();
+    if (r >= n) return;
+    double acc[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) acc[k] = 0.0;
+#pragma unroll
+    for (int q = 0; q < M; ++q)
+        if (cidx[q] >= 0) {
+            const double* xr = ec + (int64_t)cidx[q] * K;
+#pragma unroll
+            for (int k = 0; k < K; ++k) acc[k] = fma(a[q], xr[k], acc[k]);
+        }
+#pragma unroll
+    for (int k = 0; k < K; ++k) e[(int64_t)r * K + k] += acc[k];
+}
+
+// coarsest level: y = A^{-1} x for K right-hand sides with the explicit inverse (row-major)
+template <int K>
+__global__ void k_dense_mv_b(int m, const double* __restrict__ Ainv, const double* __restrict__ x,
+                             double* __restrict__ y) {
+    pdl_trigger();
+    pdl_wait();
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < m * K; t += gridDim.x * blockDim.x) {
+        const int i = t / K, k = t % K;
+        double acc = 0.0;
+        for (int j = 0; j < m; ++j) acc = fma(Ainv[(int64_t)i * m + j], x[(int64_t)j * K + k], acc);
+        y[t] = acc;
+    }
+}
+
+// column-major user vectors (K x N, original order) <-> interleaved lib order of width KK >= K
+// (columns K..KK-1 of the interleaved layout are zero)
+__global__ void k_gather_b(int n, int K, int KK, const int* __restrict__ idx, const double* __restrict__ in,
+                           double* __restrict__ out) {
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < (int64_t)n * KK;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = t / KK, k = t % KK;
+        out[t] = k < K ? in[k * n + idx[r]] : 0.0;
+    }
+}
+__global__ void k_scatter_b(int n, int K, int KK, const int* __restrict__ idx, const double* __restrict__ in,
+                            double* __restrict__ out) {
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < (int64_t)n * KK;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = t / KK, k = t % KK;
+        if (k < K) out[k * n + idx[r]] = in[t];
+    }
+}
+
+// out[k] = sum_r a[r*K+k] b[r*K+k], deterministic (block partials in fixed order, last-block finish)
+template <int K>
+__global__ void __launch_bounds__(RED_THREADS) k_bdot_fin(int64_t n, const double* __restrict__ a,
+                                                          const double* __restrict__ b, double* __restrict__ partials,
+                                                          unsigned* ticket, double* out) {
+    __shared__ double red[RED_THREADS / 32][K];
+    const int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
+    const int64_t b0 = blockIdx.x * chunk, b1 = min(n, b0 + chunk);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double s[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) s[k] = 0.0;
+    for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x)
+#pragma unroll
+        for (int k = 0; k < K; ++k) s[k] = fma(a[i * K + k], b[i * K + k], s[k]);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const double t = warp_sum(s[k]);
+        if (lane == 0) red[warp][k] = t;
+    }
+    __syncthreads();
+    if (threadIdx.x < K) {
+        double t = 0.0;
+        for (int ww = 0; ww < RED_THREADS / 32; ++ww) t += red[ww][threadIdx.x];
+        partials[(int64_t)blockIdx.x * K + threadIdx.x] = t;
+    }
+    finish_partials(partials, K, ticket, out, nullptr);
+}
+
+}  // namespace mgm

@@ -20,6 +20,7 @@
 #include "solve_kernels.cuh"
 #include "bottom_kernel.cuh"
 #include "sweep_kernel.cuh"
+#include "batch_kernels.cuh"
 
 using namespace mgm;
 
@@ -141,6 +142,7 @@ struct mgm_ctx {
     // coarsest dense LU
     int nc = 0;
     double* lu = nullptr;
+    double* ainv = nullptr;  // explicit inverse of the coarsest operator (batched solves), row-major
     i32* piv = nullptr;
     // level-0 permutation (lib row -> original index)
     i32* d_lib2orig = nullptr;
@@ -164,6 +166,11 @@ struct mgm_ctx {
     BPhase* d_phases = nullptr;
     std::vector<void*> bot_mem;
     i64 vcycle_kernels = 0;
+    // batched (multi-RHS) V-cycles: per level interleaved [n_j][bK] buffers, graph per K
+    int bK = 0;
+    std::vector<double*> bu, bf, bt;
+    cudaGraphExec_t bgraph[9] = {};
+    double* bres = nullptr;  // residual (n x K)
     // multi-GPU (mgm_dist_attach)
     int rank = 0, nranks = 1;
     ncclComm_t comm = nullptr;
@@ -962,6 +969,24 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
         if ((s = upload(ctx, &ctx->lu, LU)) || (s = upload(ctx, &ctx->piv, piv))) return s;
         CK(cudaStreamSynchronize(st));
         setup_bottom(ctx, LU, piv);
+        if (m <= 4096) {  // explicit inverse for the batched coarse solve (same solution up to rounding, O13)
+            std::vector<double> Ainv((size_t)m * m), bb(m);
+            for (int i = 0; i < m; ++i) {
+                std::fill(bb.begin(), bb.end(), 0.0);
+                bb[i] = 1.0;
+                for (int k = 0; k < m; ++k)
+                    if (piv[k] != k) std::swap(bb[k], bb[piv[k]]);
+                for (int k = 0; k < m; ++k)
+                    for (int r = k + 1; r < m; ++r) bb[r] -= LU[(size_t)k * m + r] * bb[k];
+                for (int r = m - 1; r >= 0; --r) {
+                    double acc = bb[r];
+                    for (int c = r + 1; c < m; ++c) acc -= LU[(size_t)c * m + r] * bb[c];
+                    bb[r] = acc / LU[(size_t)r * m + r];
+                }
+                for (int r = 0; r < m; ++r) Ainv[(size_t)r * m + i] = bb[r];
+            }
+            if ((s = upload(ctx, &ctx->ainv, Ainv))) return s;
+        }
         cudaGetLastError();
     }
     // ---- level-0 permutation
@@ -1665,6 +1690,134 @@ mgm_status bicgstab_lib(mgm_ctx* ctx, double tol, int maxit, mgm_report* rep, cu
 }
 
 // Standalone MGM: u <- V-cycle(f, u) from u = 0 until ||f - A u|| / ||f|| <= tol.
+// ---------------------------------------------------------------------------------------
+// Batched (multi-RHS) V-cycle and standalone MGM: K right-hand sides in
+// one pass over every operator; vectors interleaved [row][K] in lib order; the small levels
+// run the per-kernel path (the one-kernel bottom holds a single right-hand side).
+// ---------------------------------------------------------------------------------------
+template <int K>
+static void b_gs(mgm_ctx* ctx, const Level& L, int j, int r0, int r1, cudaStream_t st) {
+    const int span = r1 - (r0 & ~31);
+    const int bs = L.gs_block;
+    auto go = [&](auto kern, int tpr) {
+        launch(true, kern, blocks_for((i64)span * tpr, bs), bs, 0, st, r0, r1, L.uniform_w, (const i64*)L.sptr,
+               (const i32*)L.scol, (const double*)L.sval, (const double*)ctx->bf[j], ctx->bu[j]);
+    };
+    if (L.tpr == 1) go(k_gs_colour_b<1, CHUNK, K>, 1);
+    else if (L.tpr == 2) go(k_gs_colour_b<2, CHUNK, K>, 2);
+    else if (L.tpr == 4) go(k_gs_colour_b<4, CHUNK, K>, 4);
+    else go(k_gs_colour_b<8, CHUNK, K>, 8);
+}
+template <int MODE, int K>
+static void b_spmv(int tpr, i64 r1, const i64* sptr, const i32* scol, const double* sval, const double* x,
+                   const double* f, double* y, cudaStream_t st) {
+    auto go = [&](auto kern, int t) {
+        launch(true, kern, blocks_for(r1 * t, 256), 256, 0, st, 0, (int)r1, sptr, scol, sval, x, f, y);
+    };
+    if (tpr == 1) go(k_sell_spmv_b<MODE, 1, CHUNK, K>, 1);
+    else if (tpr == 2) go(k_sell_spmv_b<MODE, 2, CHUNK, K>, 2);
+    else if (tpr == 4) go(k_sell_spmv_b<MODE, 4, CHUNK, K>, 4);
+    else go(k_sell_spmv_b<MODE, 8, CHUNK, K>, 8);
+}
+template <int K>
+static void enqueue_vcycle_b(mgm_ctx* ctx, cudaStream_t st) {
+    auto& lv = ctx->lv;
+    const int p = ctx->p;
+    const int nu1 = ctx->lp.nu1, nu2 = ctx->lp.nu2;
+    const bool pre_b = ctx->lp.smoother == 1, post_b = ctx->lp.smoother == 1 || ctx->lp.smoother == 2;
+    auto sweep = [&](int j, bool backward) {
+        const Level& L = lv[j];
+        for (int q = 0; q < L.ncol; ++q) {
+            const int c = backward ? L.ncol - 1 - q : q;
+            if (L.coff[c + 1] > L.coff[c]) b_gs<K>(ctx, L, j, (int)L.coff[c], (int)L.coff[c + 1], st);
+        }
+    };
+    auto coarse = [&]() {
+        const int m = ctx->nc;
+        launch(true, k_dense_mv_b<K>, blocks_for((i64)m * K, 256), 256, 0, st, m, (const double*)ctx->ainv,
+               (const double*)ctx->bf[p - 1], ctx->bu[p - 1]);
+    };
+    if (p == 1) { coarse(); return; }
+    for (int s = 0; s < nu1; ++s) sweep(0, pre_b);                                  // line 4
+    for (int j = 0; j + 1 < p; ++j) {                                               // lines 5-9
+        const Level& L = lv[j];
+        if (j > 0) {
+            cudaMemsetAsync(ctx->bu[j], 0, sizeof(double) * L.n * K, st);
+            for (int s = 0; s < nu1; ++s) sweep(j, pre_b);
+        }
+        b_spmv<1, K>(L.stpr, L.n, L.sptr, L.scol, L.sval, ctx->bu[j], ctx->bf[j], ctx->bt[j], st);
+        b_spmv<0, K>(L.rtpr, lv[j + 1].n, L.rptr, L.rcol, L.rval, ctx->bt[j], nullptr, ctx->bf[j + 1], st);
+    }
+    coarse();                                                                        // line 10
+    for (int j = p - 2; j >= 0; --j) {                                              // lines 11-16
+        const Level& L = lv[j];
+        auto kern = L.pm <= 8 ? k_interp_correct_b<8, K> : k_interp_correct_b<16, K>;
+        launch(true, kern, blocks_for(L.n, 256), 256, 0, st, (int)L.n, L.pm, (const i32*)L.pcol,
+               (const double*)L.pval, (const double*)ctx->bu[j + 1], ctx->bu[j]);
+        for (int s = 0; s < nu2; ++s) sweep(j, post_b);
+    }
+}
+static void enqueue_vcycle_bk(mgm_ctx* ctx, int K, cudaStream_t st) {
+    switch (K) {
+        case 2: enqueue_vcycle_b<2>(ctx, st); break;
+        case 4: enqueue_vcycle_b<4>(ctx, st); break;
+        default: enqueue_vcycle_b<8>(ctx, st); break;
+    }
+}
+static mgm_status ensure_batch(mgm_ctx* ctx, int K) {
+    if (ctx->bK >= K) return MGM_OK;
+    for (auto* q : {&ctx->bu, &ctx->bf, &ctx->bt})
+        for (double* ptr : *q) cudaFree(ptr);
+    ctx->bu.assign(ctx->p, nullptr);
+    ctx->bf.assign(ctx->p, nullptr);
+    ctx->bt.assign(ctx->p, nullptr);
+    for (int j = 0; j < ctx->p; ++j) {
+        CK(dalloc(&ctx->bu[j], ctx->lv[j].n * K));
+        CK(dalloc(&ctx->bf[j], ctx->lv[j].n * K));
+        CK(dalloc(&ctx->bt[j], ctx->lv[j].n * K));
+    }
+    if (ctx->bres) cudaFree(ctx->bres);
+    CK(dalloc(&ctx->bres, ctx->N * K));
+    for (auto& gx : ctx->bgraph)
+        if (gx) { cudaGraphExecDestroy(gx); gx = nullptr; }
+    ctx->bK = K;
+    return MGM_OK;
+}
+static mgm_status run_vcycle_b(mgm_ctx* ctx, int K, cudaStream_t st) {
+    if (!ctx->bgraph[K]) {
+        cudaGraph_t g;
+        CK(cudaStreamBeginCapture(ctx->st, cudaStreamCaptureModeThreadLocal));
+        g_launch_err.clear();
+        enqueue_vcycle_bk(ctx, K, ctx->st);
+        const cudaError_t ce = cudaStreamEndCapture(ctx->st, &g);
+        if (ce != cudaSuccess || !g_launch_err.empty()) {
+            ctx->err = "batched V-cycle capture failed: " + std::string(cudaGetErrorString(ce)) + "; " + g_launch_err;
+            g_launch_err.clear();
+            cudaGetLastError();
+            return MGM_ERR_CUDA;
+        }
+        CK(cudaGraphInstantiate(&ctx->bgraph[K], g, 0));
+        cudaGraphDestroy(g);
+    }
+    CK(cudaGraphLaunch(ctx->bgraph[K], st));
+    return MGM_OK;
+}
+static void enqueue_bdot(mgm_ctx* ctx, int K, i64 n, const double* a, const double* b, double* out, cudaStream_t st) {
+    switch (K) {
+        case 2: k_bdot_fin<2><<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, a, b, ctx->partials, ctx->tickets, out); break;
+        case 4: k_bdot_fin<4><<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, a, b, ctx->partials, ctx->tickets, out); break;
+        default: k_bdot_fin<8><<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, a, b, ctx->partials, ctx->tickets, out); break;
+    }
+}
+static void enqueue_res_b(mgm_ctx* ctx, int K, cudaStream_t st) {  // bres = bf0 - L_1 bu0
+    const Level& L = ctx->lv[0];
+    switch (K) {
+        case 2: b_spmv<1, 2>(L.stpr, L.n, L.sptr, L.scol, L.sval, ctx->bu[0], ctx->bf[0], ctx->bres, st); break;
+        case 4: b_spmv<1, 4>(L.stpr, L.n, L.sptr, L.scol, L.sval, ctx->bu[0], ctx->bf[0], ctx->bres, st); break;
+        default: b_spmv<1, 8>(L.stpr, L.n, L.sptr, L.scol, L.sval, ctx->bu[0], ctx->bf[0], ctx->bres, st); break;
+    }
+}
+
 mgm_status standalone_lib(mgm_ctx* ctx, double tol, int maxit, mgm_report* rep, cudaStream_t st) {
     const i64 n = ctx->N + (ctx->poisson ? 1 : 0);
     double* nr = ctx->dh + 512;
@@ -1779,6 +1932,104 @@ mgm_status mgm_setup(const double* points, const double* normals, int64_t n_poin
     return MGM_OK;
 }
 
+// batch width used for K right-hand sides: 2, 4 or 8 (extra columns are zero)
+static int batch_width(int K) { return K <= 2 ? 2 : K <= 4 ? 4 : 8; }
+static mgm_status batch_check(mgm_ctx* ctx, int K) {
+    mgm_status s = check_ctx(ctx);
+    if (s) return s;
+    if (K < 1 || K > 8 || ctx->poisson || !ctx->ainv || ctx->comm) {
+        ctx->err = "batched solves: 1 <= K <= 8, shifted problem, coarsest level <= 4096 rows, one GPU";
+        return MGM_ERR_ARG;
+    }
+    if ((s = ensure_krylov(ctx))) return s;
+    return ensure_batch(ctx, batch_width(K));
+}
+
+mgm_status mgm_vcycle_batch(mgm_ctx* ctx, int K, const double* f_dev, double* u_dev, void* cuda_stream) {
+    if (K == 1) return mgm_vcycle(ctx, f_dev, u_dev, cuda_stream);
+    mgm_status s = batch_check(ctx, K);
+    if (s) return s;
+    if (!f_dev || !u_dev) return MGM_ERR_ARG;
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    const i64 N = ctx->N;
+    const int KK = batch_width(K);
+    k_gather_b<<<blocks_for(N * KK, 256), 256, 0, st>>>((int)N, K, KK, ctx->d_lib2orig, f_dev, ctx->bf[0]);
+    k_gather_b<<<blocks_for(N * KK, 256), 256, 0, st>>>((int)N, K, KK, ctx->d_lib2orig, u_dev, ctx->bu[0]);
+    if ((s = run_vcycle_b(ctx, KK, st))) return s;
+    k_scatter_b<<<blocks_for(N * KK, 256), 256, 0, st>>>((int)N, K, KK, ctx->d_lib2orig, ctx->bu[0], u_dev);
+    CK(cudaGetLastError());
+    return MGM_OK;
+}
+
+mgm_status mgm_solve_batch(mgm_ctx* ctx, int K, const double* rhs_dev, double* x_dev, double tol, int maxit,
+                           mgm_report* reports, void* cuda_stream) {
+    if (K == 1) return mgm_solve(ctx, rhs_dev, x_dev, tol, maxit, 0, reports, cuda_stream);
+    mgm_status s = batch_check(ctx, K);
+    if (s) return s;
+    if (!rhs_dev || !x_dev || !(tol >= 0) || maxit < 0) return MGM_ERR_ARG;
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    const i64 N = ctx->N;
+    const int KK = batch_width(K);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, st);
+    k_gather_b<<<blocks_for(N * KK, 256), 256, 0, st>>>((int)N, K, KK, ctx->d_lib2orig, rhs_dev, ctx->bf[0]);
+    CK(cudaMemsetAsync(ctx->bu[0], 0, sizeof(double) * N * KK, st));
+    double* dd = ctx->dh + 512;
+    enqueue_bdot(ctx, KK, N, ctx->bf[0], ctx->bf[0], dd, st);
+    CK(cudaMemcpyAsync(ctx->hh, dd, sizeof(double) * KK, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    std::vector<double> fn(KK), rel(KK, 1.0);
+    std::vector<int> its(KK, 0), hist(KK, 0);
+    std::vector<char> conv(KK, 0);
+    for (int k = 0; k < KK; ++k) {
+        fn[k] = std::sqrt(ctx->hh[k]);
+        if (fn[k] == 0.0) { conv[k] = 1; rel[k] = 0.0; }
+    }
+    int it = 0;
+    auto all = [&]() {
+        for (int k = 0; k < K; ++k)
+            if (!conv[k]) return false;
+        return true;
+    };
+    while (it < maxit && !all()) {
+        if ((s = run_vcycle_b(ctx, KK, st))) return s;
+        ++it;
+        enqueue_res_b(ctx, KK, st);
+        enqueue_bdot(ctx, KK, N, ctx->bres, ctx->bres, dd, st);
+        CK(cudaMemcpyAsync(ctx->hh, dd, sizeof(double) * KK, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        for (int k = 0; k < K; ++k) {
+            if (fn[k] == 0.0) continue;
+            rel[k] = std::sqrt(ctx->hh[k]) / fn[k];
+            if (reports && reports[k].history && hist[k] < reports[k].history_cap) reports[k].history[hist[k]++] = rel[k];
+            if (!conv[k]) {
+                its[k] = it;
+                if (rel[k] <= tol) conv[k] = 1;
+            }
+        }
+    }
+    k_scatter_b<<<blocks_for(N * KK, 256), 256, 0, st>>>((int)N, K, KK, ctx->d_lib2orig, ctx->bu[0], x_dev);
+    cudaEventRecord(e1, st);
+    CK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (reports)
+        for (int k = 0; k < K; ++k) {
+            reports[k].iterations = its[k];
+            reports[k].converged = conv[k];
+            reports[k].final_rel_residual = rel[k];
+            reports[k].lambda = 0.0;
+            reports[k].solve_ms = ms;
+            reports[k].setup_ms = ctx->setup_ms;
+        }
+    CK(cudaGetLastError());
+    return MGM_OK;
+}
+
 mgm_status mgm_nccl_unique_id(void* id128) {
     if (!id128) return MGM_ERR_ARG;
     if (!nccl().ok) return MGM_ERR_NCCL;
@@ -1835,6 +2086,12 @@ mgm_status mgm_destroy(mgm_ctx* ctx) {
     if (ctx->d_trace) cudaFree(ctx->d_trace);
     if (ctx->vgraph) cudaGraphExecDestroy(ctx->vgraph);
     if (ctx->comm) nccl().CommDestroy(ctx->comm);
+    for (auto* q : {&ctx->bu, &ctx->bf, &ctx->bt})
+        for (double* ptr : *q) cudaFree(ptr);
+    for (auto& gx : ctx->bgraph)
+        if (gx) cudaGraphExecDestroy(gx);
+    if (ctx->bres) cudaFree(ctx->bres);
+    if (ctx->ainv) cudaFree(ctx->ainv);
     for (auto& T : ctx->timer)
         for (auto e : T.ev) cudaEventDestroy(e);
     if (ctx->st) cudaStreamDestroy(ctx->st);

@@ -62,6 +62,9 @@ _SIGS = {
                         ctypes.POINTER(Report), _vp], ctypes.c_int),
     "mgm_destroy": ([_vp], ctypes.c_int),
     "mgm_nccl_unique_id": ([_vp], ctypes.c_int),
+    "mgm_vcycle_batch": ([_vp, ctypes.c_int, _vp, _vp, _vp], ctypes.c_int),
+    "mgm_solve_batch": ([_vp, ctypes.c_int, _vp, _vp, ctypes.c_double, ctypes.c_int,
+                         ctypes.POINTER(Report), _vp], ctypes.c_int),
     "mgm_dist_attach": ([_vp, ctypes.c_int, ctypes.c_int, _vp], ctypes.c_int),
     "mgm_last_error": ([_vp, _i64p], ctypes.c_char_p),
     "mgm_num_levels": ([_vp, ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
@@ -201,6 +204,26 @@ def mgm_solve_host(ctx, rhs: np.ndarray, x: np.ndarray, tol=1e-10, maxit=500, kr
     _check(load_library().mgm_solve_host(ctx, _vp(rhs.ctypes.data), _vp(x.ctypes.data), tol, maxit,
                                          krylov, ctypes.byref(rep), _vp(_stream_ptr(stream))), ctx)
     return _report(rep, hist)
+
+
+def mgm_vcycle_batch(ctx, K: int, f, u, stream=None):
+    """f, u: torch CUDA float64 tensors of shape (K, N) (original order), u in place."""
+    assert f.is_contiguous() and u.is_contiguous() and f.shape == u.shape and f.shape[0] == K
+    _check(load_library().mgm_vcycle_batch(ctx, K, _vp(f.data_ptr()), _vp(u.data_ptr()),
+                                           _vp(_stream_ptr(stream))), ctx)
+
+
+def mgm_solve_batch(ctx, K: int, rhs, x, tol=1e-10, maxit=500, stream=None, history_cap=512):
+    """Standalone MGM on K right-hand sides at once: rhs, x (K, N) CUDA float64 tensors."""
+    assert rhs.is_contiguous() and x.is_contiguous() and rhs.shape == x.shape and rhs.shape[0] == K
+    hists = [np.zeros(history_cap) for _ in range(K)]
+    reps = (Report * K)()
+    for k in range(K):
+        reps[k].history = _ptr(hists[k], _f64p)
+        reps[k].history_cap = history_cap
+    _check(load_library().mgm_solve_batch(ctx, K, _vp(rhs.data_ptr()), _vp(x.data_ptr()), tol, maxit,
+                                          reps, _vp(_stream_ptr(stream))), ctx)
+    return [_report(reps[k], hists[k]) for k in range(K)]
 
 
 def mgm_num_levels(ctx) -> int:
