@@ -483,7 +483,9 @@ void setup_bottom(mgm_ctx* ctx, const std::vector<double>& LU, const std::vector
             best = 0;
         } else {
             int smallest_valid = -1;
-            for (int lg = 5; lg >= 0; --lg) {  // largest tpr that covers W and fits one pass
+            int lgmax = 5;  // tuning experiment: MGM_BOT_TPR_MAX caps threads per row
+            if (const char* e = std::getenv("MGM_BOT_TPR_MAX")) lgmax = std::max(0, std::min(5, (int)std::log2(std::atoi(e))));
+            for (int lg = lgmax; lg >= 0; --lg) {  // largest tpr that covers W and fits one pass
                 const int tpr = 1 << lg;
                 if (bot_ch(tpr) * tpr < P.W) continue;
                 smallest_valid = lg;
