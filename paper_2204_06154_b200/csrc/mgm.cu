@@ -602,7 +602,21 @@ void setup_sweep(mgm_ctx* ctx, int j) {
     L.swB = B;
 }
 
+// Setup phase timer (MGM_SETUP_TIMING=1 prints host wall time per phase to stderr).
+struct SetupTimer {
+    bool on = std::getenv("MGM_SETUP_TIMING") != nullptr;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    void mark(const char* what, int level = -1) {
+        if (!on) return;
+        auto t1 = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[mgm setup] %-22s L%-2d %9.1f ms\n", what, level,
+                     std::chrono::duration<double, std::milli>(t1 - t0).count());
+        t0 = t1;
+    }
+};
+
 mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i64 N) {
+    SetupTimer tm;
     const auto& sp = ctx->sp;
     const auto& lp = ctx->lp;
     cudaStream_t st = ctx->st;
@@ -625,6 +639,7 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
         i64 dup = nearest_other(X.data(), N, nn2, nth);
         if (dup >= 0) return fail(ctx, MGM_ERR_INPUT, "duplicate points", perm[dup]);
     }
+    tm.mark("morton+duplicates");
     // ---- level count (Alg. 2 line 4)
     int p = lp.num_levels;
     if (p <= 0) {
@@ -643,6 +658,7 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
     const int ns = sp.stencil_n;
     std::vector<i32> sten;
     knn_grid(X.data(), N, X.data(), N, ns, sten, nth);
+    tm.mark("fine kNN");
     double *dX = nullptr, *dN = nullptr, *dW = nullptr, *drho = nullptr;
     i32* dS = nullptr;
     i64* dfail = nullptr;
@@ -677,6 +693,7 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
     if (hfail != INT64_MAX)
         return fail(ctx, MGM_ERR_UNISOLVENT, sp.method == 0 ? "RBF-FD stencil not unisolvent" : "GFD stencil rank deficient",
                     perm[hfail]);
+    tm.mark("fine weights (GPU)");
     // export copy of weights in original order
     ctx->w_orig.assign((size_t)N * ns, 0.0);
     ctx->sten_orig.assign((size_t)N * ns, 0);
@@ -710,6 +727,7 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
         }
         A.ptr[N] = N * ns;
     }
+    tm.mark("assemble L1");
     // ---- level loop (Alg. 2 lines 5-12)
     std::vector<std::vector<double>> Xl(p);
     std::vector<std::vector<i64>> idsl(p);
@@ -723,6 +741,7 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
         nearest_other(Xl[j].data(), nf, nn2, nth);
         std::vector<i64> keep;
         wse_eliminate(Xl[j].data(), nf, ncs, nn2, keep, nth);
+        tm.mark("WSE", j);
         Xl[j + 1].resize(3 * ncs);
         idsl[j + 1].resize(ncs);
         for (i64 k = 0; k < ncs; ++k) {
@@ -733,6 +752,7 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
         const int m = lp.interp_m;
         std::vector<i32> ist;
         knn_grid(Xl[j + 1].data(), ncs, Xl[j].data(), nf, m, ist, nth);
+        tm.mark("interp kNN", j);
         double *dXc = nullptr, *dPw = nullptr;
         i32 *dI = nullptr, *dcnt = nullptr;
         CK(dalloc(&dXc, 3 * ncs));
@@ -771,6 +791,7 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
             }
             P.ptr[i + 1] = (i64)P.col.size();
         }
+        tm.mark("interp weights", j);
         HostCSR R = transpose(P);  // P:370, exact
         // Galerkin L_{j+1} = R (L P) on the GPU
         DevCSR dL, dP, dR, dLP, dC;
@@ -785,6 +806,7 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
         free_dev_csr(dR);
         free_dev_csr(dLP);
         free_dev_csr(dC);
+        tm.mark("Galerkin RAP", j);
     }
     cudaFree(dXf);
     cudaFree(dfail);
@@ -820,6 +842,7 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
             L.colour_lib[r] = colour_mor[j][lib2mor[j][r]];
         }
     }
+    tm.mark("colouring");
     // ---- pack solve-phase layout
     mgm_status s;
     for (int j = 0; j < p; ++j) {
@@ -927,6 +950,7 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
         CK(cudaMemsetAsync(L.f, 0, sizeof(double) * vn, st));
         CK(cudaMemsetAsync(L.t, 0, sizeof(double) * vn, st));
     }
+    tm.mark("pack + upload");
     for (int j = 0; j + 1 < p; ++j) setup_sweep(ctx, j);
     // ---- Poisson border vectors c_{j+1} = P_j^T c_j, Morton order then lib
     if (ctx->poisson) {
@@ -965,12 +989,15 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
             }
         std::vector<double> LU;
         std::vector<i32> piv;
+        tm.mark("border vectors");
         i64 bad = dense_lu_colmajor(A, m, LU, piv);
+        tm.mark("coarse LU", p - 1);
         if (bad >= 0) return fail(ctx, MGM_ERR_SINGULAR, "singular coarsest operator", bad);
         ctx->nc = m;
         if ((s = upload(ctx, &ctx->lu, LU)) || (s = upload(ctx, &ctx->piv, piv))) return s;
         CK(cudaStreamSynchronize(st));
         setup_bottom(ctx, LU, piv);
+        tm.mark("bottom kernel setup", p - 1);
         if (m <= 4096) {  // explicit inverse for the batched coarse solve (same solution up to rounding, O13)
             std::vector<double> Ainv((size_t)m * m), bb(m);
             for (int i = 0; i < m; ++i) {
@@ -988,6 +1015,7 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
                 for (int r = 0; r < m; ++r) Ainv[(size_t)r * m + i] = bb[r];
             }
             if ((s = upload(ctx, &ctx->ainv, Ainv))) return s;
+            tm.mark("coarse inverse", p - 1);
         }
         cudaGetLastError();
     }
