@@ -232,6 +232,13 @@ mgm_status mgm_trace_read(const mgm_ctx* ctx, uint64_t* stamps_ns, int cap, int*
  * bottom kernel is not used); meta[4*q..] = {op, local, rows, threads per row} (may be NULL). */
 mgm_status mgm_bottom_trace_read(const mgm_ctx* ctx, uint64_t* stamps_ns, int cap, int* n, int32_t* meta);
 
+/* Diagnostics: fine per-phase timeline of the bottom kernel (MGM_TRACE=2 at setup): for
+ * thread 0 of the first and of the last CTA of the cluster, 8 SM-clock readings per phase
+ * {phase start, operator row in registers, row sum ready, value broadcast, stores issued,
+ * cluster arrive done, next rows' loads issued, cluster wait done} (slots 0,7,1,2,3,4,5,6 in
+ * that order of the array: clk[cta][phase][slot]).  clk holds 2*8*cap int64; *n = phases. */
+mgm_status mgm_bottom_ftrace_read(const mgm_ctx* ctx, int64_t* clk, int cap, int* n);
+
 /* ---------------- host-only hooks of the setup's discrete steps (no GPU needed) --------
  * They run the same host code mgm_setup uses, so discrete-structure parity with the
  * oracle can be checked on a CPU-only machine. */

@@ -35,6 +35,21 @@
 //   BP_ADD   y[r] += acc                                   (e_j += P_j e_{j+1})
 //   BP_MV    y[r] = acc                                    (coarsest: e_p = L_p^{-1} r_p)
 //   BP_STORE g[r] = y[r]                                   (e_J back to HBM)
+// Synchronisation between phases:
+//   * local -> local: __syncthreads (CTA 0 only);
+//   * DATA-SYNCHRONISED phases (mb >= 0: GS / ADD / MV of a cluster level whose output is a
+//     replicated vector): every row value is sent to every CTA with st.async, which signals
+//     the receiver's mbarrier (complete_tx, 8 bytes); a CTA proceeds once its mbarrier has
+//     received the phase's 8*rows bytes.  No release fence and no cluster barrier: the
+//     sender does not wait for acknowledgements (MGM_TRACE=2 timeline: the release of
+//     barrier.cluster.arrive cost ~1000 cycles per phase).  Two mbarriers alternate
+//     (k & 1); each is re-armed for phase k + 2 as soon as phase k completed, which precedes
+//     any byte of phase k + 2 (a sender needs this CTA's phase k + 1 values first), so the
+//     tx-count never goes negative.  Write-after-read: a sender can write values of phase
+//     k + 1 into this CTA's copy only after receiving all of this CTA's phase-k values, and
+//     each value is sent after the reads of its row group;
+//   * everything else (outputs in global memory, zeroing, local <-> cluster transitions):
+//     barrier.cluster arrive.release / wait.acquire.
 // Every output element is produced by one thread group with a fixed summation order, so
 // the kernel is deterministic.  Shifted problems only (the Poisson border terms run on the
 // per-kernel path).
@@ -60,6 +75,8 @@ struct BPhase {
     int yo;        // shared byte offset of the output vector (replicated), or -1: global y
     int zo;        // shared byte offset of the vector zeroed by BP_MVZ
     int fpre;      // 1: f may be prefetched with the operator row (not written by the previous phase)
+    int mb;        // >= 0: "data-synchronised" phase number k (see below), -1: barrier phase
+    int arm;       // bytes every CTA receives in data-synchronised phase k + 2 (0: none)
     const int* col;
     const double* val;
     const double* x;  // global gathered vector (xo < 0)
@@ -87,6 +104,46 @@ __device__ __forceinline__ void dsm_st_rank(uint32_t local_addr, unsigned rank, 
     uint32_t r;
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local_addr), "r"(rank));
     asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(r), "d"(v) : "memory");
+}
+// remote store that signals the receiver's mbarrier with 8 transaction bytes
+__device__ __forceinline__ void dsm_st_async_rank(uint32_t local_addr, uint32_t local_bar, unsigned rank, double v) {
+    uint32_t r, b;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local_addr), "r"(rank));
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(b) : "r"(local_bar), "r"(rank));
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(r),
+                 "l"(__double_as_longlong(v)), "r"(b)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arm(uint32_t bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+// wait for the phase of the given parity; a bounded spin (seconds) traps instead of hanging
+__device__ __forceinline__ void mbar_wait(uint32_t bar, unsigned parity) {
+    for (long long it = 0;; ++it) {
+        uint32_t done;
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n"
+            " selp.u32 %0, 1, 0, p;\n}"
+            : "=r"(done)
+            : "r"(bar), "r"(parity)
+            : "memory");
+        if (done) return;
+        if (it > (1ll << 26)) asm volatile("trap;");
+    }
+}
+// fine-grained phase timeline (MGM_TRACE=2, diagnostics): SM clock after the named value
+__device__ __forceinline__ long long clk_after(double v) {
+    long long t;
+    asm volatile("{ .reg .f64 d; mov.f64 d, %1; mov.u64 %0, %%clock64; }" : "=l"(t) : "d"(v));
+    return t;
+}
+__device__ __forceinline__ long long clk_after_i(int v) {
+    long long t;
+    asm volatile("{ .reg .s32 q; mov.s32 q, %1; mov.u64 %0, %%clock64; }" : "=l"(t) : "r"(v));
+    return t;
 }
 
 // The operator entries of one thread's first row of a phase, held in registers.
@@ -119,10 +176,15 @@ __device__ __forceinline__ void bcast_store(uint32_t sbase, int off, int row, do
     const uint32_t a = sbase + (uint32_t)off + ((uint32_t)row << 3);
     for (int k = lane; k < cs; k += tpr) dsm_st_rank(a, (unsigned)k, v);
 }
+__device__ __forceinline__ void bcast_store_async(uint32_t sbase, int off, int row, double v, int lane, int tpr, int cs,
+                                                  uint32_t bar) {
+    const uint32_t a = sbase + (uint32_t)off + ((uint32_t)row << 3);
+    for (int k = lane; k < cs; k += tpr) dsm_st_async_rank(a, bar, (unsigned)k, v);
+}
 
 template <int TPR>
 __device__ __forceinline__ void bottom_phase(const BPhase& P, const BFrag& fr0, int g, int nthr, const char* smem,
-                                             uint32_t sbase, int cs, uint64_t pol) {
+                                             uint32_t sbase, int cs, uint64_t pol, long long* tr, uint32_t mbar) {
     constexpr int CH = bot_ch(TPR);
     const int lane = g & (TPR - 1);
     const int ngroups = nthr / TPR;
@@ -156,6 +218,7 @@ __device__ __forceinline__ void bottom_phase(const BPhase& P, const BFrag& fr0, 
             const int c = ld_keep_i32(P.col + (int64_t)row * P.W + k, pol);
             acc = fma(ld_keep_f64(P.val + (int64_t)row * P.W + k, pol), P.xo >= 0 ? xs[c] : P.x[c], acc);
         }
+        if (tr && base == 0) tr[1] = clk_after(acc);
 #pragma unroll
         for (int o = TPR >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
         // every lane of the group holds acc; lane 0 computes the row's value, the group stores
@@ -169,14 +232,17 @@ __device__ __forceinline__ void bottom_phase(const BPhase& P, const BFrag& fr0, 
             }
         }
         out = __shfl_sync(0xffffffffu, out, (int)(threadIdx.x & 31) & ~(TPR - 1));
+        if (tr && base == 0) tr[2] = clk_after(out);
         if (live) {
             if (P.yo >= 0) {
-                bcast_store(sbase, P.yo, row, out, lane, TPR, cs);
+                if (P.mb >= 0) bcast_store_async(sbase, P.yo, row, out, lane, TPR, cs, mbar + 8u * (unsigned)(P.mb & 1));
+                else bcast_store(sbase, P.yo, row, out, lane, TPR, cs);
             } else if (lane == 0) {
                 P.y[row] = out;
             }
             if (P.op == BP_MVZ) bcast_store(sbase, P.zo, row, 0.0, lane, TPR, cs);
         }
+        if (tr && base == 0) tr[3] = clock64();
     }
 }
 
@@ -193,14 +259,15 @@ __device__ __forceinline__ void bfrag_load_any(BFrag& fr, const BPhase& P, int g
     }
 }
 __device__ __forceinline__ void bottom_phase_any(const BPhase& P, const BFrag& fr, int g, int nthr, const char* smem,
-                                                 uint32_t sbase, int cs, uint64_t pol) {
+                                                 uint32_t sbase, int cs, uint64_t pol, long long* tr,
+                                                 uint32_t mbar) {
     switch (P.tpr_log2) {
-        case 0: bottom_phase<1>(P, fr, g, nthr, smem, sbase, cs, pol); break;
-        case 1: bottom_phase<2>(P, fr, g, nthr, smem, sbase, cs, pol); break;
-        case 2: bottom_phase<4>(P, fr, g, nthr, smem, sbase, cs, pol); break;
-        case 3: bottom_phase<8>(P, fr, g, nthr, smem, sbase, cs, pol); break;
-        case 4: bottom_phase<16>(P, fr, g, nthr, smem, sbase, cs, pol); break;
-        default: bottom_phase<32>(P, fr, g, nthr, smem, sbase, cs, pol); break;
+        case 0: bottom_phase<1>(P, fr, g, nthr, smem, sbase, cs, pol, tr, mbar); break;
+        case 1: bottom_phase<2>(P, fr, g, nthr, smem, sbase, cs, pol, tr, mbar); break;
+        case 2: bottom_phase<4>(P, fr, g, nthr, smem, sbase, cs, pol, tr, mbar); break;
+        case 3: bottom_phase<8>(P, fr, g, nthr, smem, sbase, cs, pol, tr, mbar); break;
+        case 4: bottom_phase<16>(P, fr, g, nthr, smem, sbase, cs, pol, tr, mbar); break;
+        default: bottom_phase<32>(P, fr, g, nthr, smem, sbase, cs, pol, tr, mbar); break;
     }
 }
 
@@ -224,11 +291,15 @@ __device__ __forceinline__ unsigned long long gtimer() {
 
 // smem: [phase table (nph x BPhase)][replicated vectors at the offsets in the phases]
 __global__ void __launch_bounds__(BOT_THREADS, 1)
-    k_vcycle_bottom(const BPhase* __restrict__ gphases, int nph, unsigned long long* __restrict__ trace) {
+    k_vcycle_bottom(const BPhase* __restrict__ gphases, int nph, unsigned long long* __restrict__ trace, PfList pf,
+                    int arm0, int arm1) {
     extern __shared__ __align__(16) char smem[];
+    __shared__ __align__(8) unsigned long long mbars[2];  // data-synchronised phases k & 1
+    const uint32_t mbar = (uint32_t)__cvta_generic_to_shared(mbars);
     const BPhase* phases = reinterpret_cast<const BPhase*>(smem);
     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
     pdl_trigger();
+    l2_prefetch_share(pf);  // (opt-in L2 prefetch pacing, off by default)
     uint64_t pol;
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
     {
@@ -236,6 +307,13 @@ __global__ void __launch_bounds__(BOT_THREADS, 1)
         const unsigned long long* src = reinterpret_cast<const unsigned long long*>(gphases);
         unsigned long long* dst = reinterpret_cast<unsigned long long*>(smem);
         for (int i = threadIdx.x; i < nw; i += BOT_THREADS) dst[i] = src[i];
+        if (threadIdx.x == 0) {
+            mbar_init(mbar, 1);
+            mbar_init(mbar + 8, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            if (arm0 > 0) mbar_arm(mbar, (unsigned)arm0);
+            if (arm1 > 0) mbar_arm(mbar + 8, (unsigned)arm1);
+        }
         __syncthreads();
     }
     const int rank = (int)cluster_rank();
@@ -251,8 +329,14 @@ __global__ void __launch_bounds__(BOT_THREADS, 1)
     pdl_wait();
     cluster_arrive();  // every CTA's shared memory is live before any remote store
     cluster_wait();
+    // fine timeline (diagnostics): thread 0 of CTA 0 and of the last CTA, 8 clocks per phase
+    long long* ftr = nullptr;
+    if (trace && trace[BOT_MAX_PHASES - 1] == 2ull && threadIdx.x == 0 && (rank == 0 || rank == cs - 1))
+        ftr = reinterpret_cast<long long*>(trace) + BOT_MAX_PHASES + (rank == 0 ? 0 : 8 * BOT_MAX_PHASES);
     for (int q = 0; q < nph; ++q) {
         if (trace && rank == 0 && threadIdx.x == 0) trace[q] = gtimer();  // diagnostics (MGM_TRACE)
+        long long* tr = ftr ? ftr + 8 * q : nullptr;
+        if (tr) { tr[0] = clock64(); tr[7] = clk_after_i(fr.c[0]); }
         const BPhase P = phases[q];
         if (P.op == BP_ZERO) {  // every CTA zeroes its own copy
             double* y = reinterpret_cast<double*>(smem + P.yo);
@@ -262,19 +346,34 @@ __global__ void __launch_bounds__(BOT_THREADS, 1)
             for (int r = P.r0 + g_cl; r < P.r1; r += nthr_cl) P.y[r] = y[r];
         } else if (!P.local || rank == 0) {
             bottom_phase_any(P, fr, P.local ? (int)threadIdx.x : g_cl, P.local ? BOT_THREADS : nthr_cl, smem, sbase,
-                             cs, pol);
+                             cs, pol, tr, mbar);
         }
         if (q + 1 == nph) break;
         const BPhase& N = phases[q + 1];
         const bool part = !P.local || rank == 0;
         const bool npart = !N.local || rank == 0;
-        if (P.local && N.local) {  // CTA 0 only; the other CTAs skip local phases
+        if (P.mb >= 0) {  // data-synchronised: wait for this phase's bytes, re-arm for phase mb + 2
+            if (npart) bfrag_load_any(fr, N, N.local ? (int)threadIdx.x : g_cl, pol);
+            if (tr) tr[4] = clock64();
+            const uint32_t b = mbar + 8u * (unsigned)(P.mb & 1);
+            mbar_wait(b, (unsigned)((P.mb >> 1) & 1));
+            if (tr) tr[5] = clock64();
+            if (threadIdx.x == 0 && P.arm > 0) mbar_arm(b, (unsigned)P.arm);
+            if (tr) tr[6] = clock64();
+        } else if (P.local && N.local) {  // CTA 0 only; the other CTAs skip local phases
             if (npart) bfrag_load_any(fr, N, (int)threadIdx.x, pol);
             if (part) __syncthreads();
         } else {
+            // zeroing / plain remote stores (generic proxy) before later st.async writes to the
+            // same words
+            if (P.op == BP_ZERO || P.op == BP_MVZ || P.local)
+                asm volatile("fence.proxy.async.shared::cluster;" ::: "memory");
             cluster_arrive();
+            if (tr) tr[4] = clock64();
             if (npart) bfrag_load_any(fr, N, N.local ? (int)threadIdx.x : g_cl, pol);
+            if (tr) tr[5] = clock64();
             cluster_wait();
+            if (tr) tr[6] = clock64();
         }
     }
     cluster_arrive();  // no CTA exits while others may still store into its shared memory

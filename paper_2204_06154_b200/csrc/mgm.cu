@@ -86,6 +86,7 @@ struct Level {
     i32* scol = nullptr;
     double* sval = nullptr;
     i64 sell_stored = 0, nnz = 0;
+    std::vector<i64> h_sptr, h_rptr;  // host copies of the slice offsets (L2 prefetch regions)
     int tpr = 1, rtpr = 1;  // threads per row for L_j (colour sweeps) and R_j kernels
     int stpr = 1;           // threads per row for full-level SpMV / residual on L_j
     int gs_block = 256;     // threads per block of the colour kernels
@@ -163,9 +164,26 @@ struct mgm_ctx {
     int bot_cluster = 16;
     size_t bot_smem = 0;
     int nphases = 0;
+    int bot_arm0 = 0, bot_arm1 = 0;  // bytes of the first two data-synchronised phases
     BPhase* d_phases = nullptr;
     std::vector<void*> bot_mem;
     i64 vcycle_kernels = 0;
+    // L2 prefetch pacing of the V-cycle graph (solve_kernels.cuh l2_prefetch_share): the
+    // schedule's operator regions ("targets") are recorded by a dry enqueue pass; kernel t
+    // of the schedule then prefetches targets (t, t + pf_dist], the bottom kernel the
+    // up-path targets within pf_bot_budget bytes.  MGM_PF_DIST=0 turns it off.
+    int pf_mode = 0;  // 0 off, 1 record, 2 emit
+    int pf_dist = 0;  // off by default: measured slower
+    i64 pf_cap = (i64)24 << 20;         // bytes prefetched per target (its prefix)
+    i64 pf_bot_budget = (i64)48 << 20;  // bytes the bottom kernel prefetches for the up-path
+    std::vector<std::vector<PfRegion>> pf_tg;
+    std::vector<PfRegion> pf_flat;
+    std::vector<int> pf_off;
+    PfRegion* d_pf = nullptr;
+    std::vector<void*> pf_old;  // earlier tables (graphs may still reference them)
+    int pf_pos = 0, pf_last = 0;
+    int pf_late = 0, pf_nof = 0, pf_l0only = 0;  // experiments (MGM_PF_LATE / _NOF / _L0ONLY)
+    std::vector<PfRegion> bot_pf;  // the bottom kernel's operator arrays
     // batched (multi-RHS) V-cycles: per level interleaved [n_j][bK] buffers, graph per K
     int bK = 0;
     std::vector<double*> bu, bf, bt;
@@ -232,9 +250,12 @@ static void note_launch(cudaError_t e, unsigned grid, unsigned block, size_t sme
 
 // Kernel launch with optional programmatic dependent launch (PDL, see solve_kernels.cuh).
 static bool g_use_pdl = std::getenv("MGM_NO_PDL") == nullptr;
+// dry enqueue pass (L2 prefetch target recording): nothing is launched or recorded
+static thread_local bool g_dry = false;
 template <typename... KArgs, typename... Args>
 static void launch(bool pdl, void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t st,
                    Args... args) {
+    if (g_dry) return;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(block);
@@ -336,6 +357,7 @@ static T* bot_upload(mgm_ctx* ctx, const std::vector<T>& v, bool& ok) {
     T* d = nullptr;
     if (cudaMalloc((void**)&d, sizeof(T) * std::max<size_t>(1, v.size())) != cudaSuccess) { ok = false; return nullptr; }
     ctx->bot_mem.push_back(d);
+    ctx->bot_pf.push_back(PfRegion{(const char*)d, (int64_t)(sizeof(T) * v.size())});
     if (!v.empty() && cudaMemcpy(d, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice) != cudaSuccess) ok = false;
     return d;
 }
@@ -494,6 +516,8 @@ void setup_bottom(mgm_ctx* ctx, const std::vector<double>& LU, const std::vector
             if (best < 0) best = smallest_valid >= 0 ? smallest_valid : 5;
         }
         P.tpr_log2 = best;
+        P.mb = -1;
+        P.arm = 0;
         ph.push_back(P);
     };
     const bool pre_b = ctx->lp.smoother == 1, post_b = ctx->lp.smoother == 1 || ctx->lp.smoother == 2;
@@ -522,6 +546,21 @@ void setup_bottom(mgm_ctx* ctx, const std::vector<double>& LU, const std::vector
         for (int s2 = 0; s2 < ctx->lp.nu2; ++s2) sweep(j, post_b);
     }
     add(BP_STORE, false, 0, ctx->lv[J].n, nullptr, -1, nullptr, ou[J], ctx->lv[J].u, nullptr, -1, nullptr);
+    // data-synchronised phases (bottom_kernel.cuh): cluster GS / ADD / MV phases whose output
+    // is a replicated vector; every CTA receives 8 bytes per row of such a phase
+    const bool mbar_on = std::getenv("MGM_BOT_NO_MBAR") == nullptr;
+    std::vector<int> mbq;
+    for (size_t q = 0; q + 1 < ph.size(); ++q) {
+        BPhase& P = ph[q];
+        if (mbar_on && !P.local && P.yo >= 0 && (P.op == BP_GS || P.op == BP_ADD || P.op == BP_MV)) {
+            P.mb = (int)mbq.size();
+            mbq.push_back((int)q);
+        }
+    }
+    auto mbytes = [&](size_t k) { return 8 * (ph[(size_t)mbq[k]].r1 - ph[(size_t)mbq[k]].r0); };
+    for (size_t k = 0; k + 2 < mbq.size(); ++k) ph[(size_t)mbq[k]].arm = mbytes(k + 2);
+    ctx->bot_arm0 = mbq.size() > 0 ? mbytes(0) : 0;
+    ctx->bot_arm1 = mbq.size() > 1 ? mbytes(1) : 0;
     if ((int)ph.size() * sizeof(BPhase) > table) return;
     ctx->d_phases = bot_upload(ctx, ph, ok);
     if (!ok) return;
@@ -895,6 +934,7 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
             }
         }
         if ((s = upload(ctx, &L.sptr, sptr)) || (s = upload(ctx, &L.scol, scol)) || (s = upload(ctx, &L.sval, sval))) return s;
+        L.h_sptr = sptr;
         if (j + 1 < p) {
             const HostCSR& P = Pm[j];
             const int m = lp.interp_m;
@@ -939,6 +979,7 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
                     if (t == 1 || t == 2 || t == 4 || t == 8) L.rtpr = t;
                 }
             }
+            L.h_rptr = rptr;
             if ((s = upload(ctx, &L.rptr, rptr)) || (s = upload(ctx, &L.rcol, rcol)) || (s = upload(ctx, &L.rval, rval)))
                 return s;
         }
@@ -1025,7 +1066,12 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
         for (i64 r = 0; r < N; ++r) l2o[r] = (i32)ctx->lv[0].ids[r];
         if ((s = upload(ctx, &ctx->d_lib2orig, l2o))) return s;
     }
-    if (std::getenv("MGM_TRACE")) CK(dalloc(&ctx->d_trace, 256 + 6 * BOT_MAX_PHASES));
+    if (std::getenv("MGM_TRACE")) {
+        CK(dalloc(&ctx->d_trace, 256 + 17 * BOT_MAX_PHASES));
+        // MGM_TRACE=2: the bottom kernel also records its fine per-phase clock timeline
+        const unsigned long long mode = std::atoi(std::getenv("MGM_TRACE")) == 2 ? 2ull : 0ull;
+        CK(cudaMemcpy(ctx->d_trace + 256 + BOT_MAX_PHASES - 1, &mode, 8, cudaMemcpyHostToDevice));
+    }
     if (const char* e = std::getenv("MGM_L2_PERSIST"))  // experiment: persisting-L2 carve-out (bytes)
         cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)std::atoll(e));
     CK(cudaStreamSynchronize(st));
@@ -1037,7 +1083,7 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
 // ---------------------------------------------------------------------------------------
 void timer_begin(mgm_ctx* ctx, int cls, cudaStream_t st) {
     KernelTimer& T = ctx->timer[cls];
-    if (!T.on) return;
+    if (!T.on || g_dry) return;
     if (T.used + 2 > (int)T.ev.size()) {
         for (int q = 0; q < 64; ++q) {
             cudaEvent_t e;
@@ -1049,7 +1095,7 @@ void timer_begin(mgm_ctx* ctx, int cls, cudaStream_t st) {
 }
 void timer_end(mgm_ctx* ctx, int cls, cudaStream_t st, double bytes, int nlaunch = 1) {
     KernelTimer& T = ctx->timer[cls];
-    if (!T.on) return;
+    if (!T.on || g_dry) return;
     cudaEventRecord(T.ev[T.used + 1], st);
     T.used += 2;
     T.launches += nlaunch;
@@ -1077,12 +1123,12 @@ double sweep_colour_bytes(const Level& L, i64 rows) {
 // kernel variants by threads-per-row (chosen per level from the SELL width)
 constexpr int CHUNK = 16;
 template <bool P, int TPR>
-void gs_launch_t(bool pdl, int r0, int r1, int span, const Level& L, cudaStream_t st) {
+void gs_launch_t(bool pdl, int r0, int r1, int span, const Level& L, cudaStream_t st, PfList pf) {
     // block size: colours too small to give every SM a 256-thread block use smaller blocks
     // (spreads the gathers over more SMs)
     const int bs = L.gs_block;
     launch(pdl, k_gs_colour<P, TPR, CHUNK>, blocks_for((i64)span * TPR, bs), bs, 0, st, r0, r1, L.uniform_w, L.sptr, L.scol,
-           L.sval, L.f, L.u, L.c, (int)L.n);
+           L.sval, L.f, L.u, L.c, (int)L.n, pf);
 }
 // Threads one wave of colour kernels can hold (all SMs, register-limited occupancy).
 static i64 gs_wave_threads(int tpr, int block) {
@@ -1104,49 +1150,50 @@ static i64 gs_wave_threads(int tpr, int block) {
     return cache[ti][bi] = (i64)per * nsm * block;
 }
 
-void launch_gs(bool pdl, bool poisson, int tpr, int r0, int r1, int span, const Level& L, cudaStream_t st) {
+void launch_gs(bool pdl, bool poisson, int tpr, int r0, int r1, int span, const Level& L, cudaStream_t st,
+               PfList pf = {}) {
     // a colour slightly larger than one wave would run a nearly empty second wave (ncu:
     // "1.04 waves" on the largest level-0 colours): halve the threads per row instead
     while (tpr > 1 && (i64)span * tpr > gs_wave_threads(tpr, L.gs_block) &&
            (i64)span * (tpr / 2) <= gs_wave_threads(tpr / 2, L.gs_block))
         tpr /= 2;
     if (poisson) {
-        if (tpr == 1) gs_launch_t<true, 1>(pdl, r0, r1, span, L, st);
-        else if (tpr == 2) gs_launch_t<true, 2>(pdl, r0, r1, span, L, st);
-        else if (tpr == 4) gs_launch_t<true, 4>(pdl, r0, r1, span, L, st);
-        else gs_launch_t<true, 8>(pdl, r0, r1, span, L, st);
+        if (tpr == 1) gs_launch_t<true, 1>(pdl, r0, r1, span, L, st, pf);
+        else if (tpr == 2) gs_launch_t<true, 2>(pdl, r0, r1, span, L, st, pf);
+        else if (tpr == 4) gs_launch_t<true, 4>(pdl, r0, r1, span, L, st, pf);
+        else gs_launch_t<true, 8>(pdl, r0, r1, span, L, st, pf);
     } else {
-        if (tpr == 1) gs_launch_t<false, 1>(pdl, r0, r1, span, L, st);
-        else if (tpr == 2) gs_launch_t<false, 2>(pdl, r0, r1, span, L, st);
-        else if (tpr == 4) gs_launch_t<false, 4>(pdl, r0, r1, span, L, st);
-        else gs_launch_t<false, 8>(pdl, r0, r1, span, L, st);
+        if (tpr == 1) gs_launch_t<false, 1>(pdl, r0, r1, span, L, st, pf);
+        else if (tpr == 2) gs_launch_t<false, 2>(pdl, r0, r1, span, L, st, pf);
+        else if (tpr == 4) gs_launch_t<false, 4>(pdl, r0, r1, span, L, st, pf);
+        else gs_launch_t<false, 8>(pdl, r0, r1, span, L, st, pf);
     }
 }
 template <int MODE, bool P, int TPR>
 void spmv_launch_t(bool pdl, i64 r0, i64 r1, i64 nl, const i64* sptr, const i32* scol, const double* sval,
-                   const double* x, const double* f, double* y, const double* c, cudaStream_t st) {
+                   const double* x, const double* f, double* y, const double* c, cudaStream_t st, PfList pf) {
     launch(pdl, k_sell_spmv<MODE, P, TPR, CHUNK>, blocks_for((r1 - (r0 & ~31)) * TPR, 256), 256, 0, st, (int)r0,
-           (int)r1, (int)nl, sptr, scol, sval, x, f, y, c);
+           (int)r1, (int)nl, sptr, scol, sval, x, f, y, c, pf);
 }
 template <int MODE, bool P>
 void spmv_launch_p(bool pdl, int tpr, i64 r0, i64 r1, i64 nl, const i64* sptr, const i32* scol, const double* sval,
-                   const double* x, const double* f, double* y, const double* c, cudaStream_t st) {
-    if (tpr == 1) spmv_launch_t<MODE, P, 1>(pdl, r0, r1, nl, sptr, scol, sval, x, f, y, c, st);
-    else if (tpr == 2) spmv_launch_t<MODE, P, 2>(pdl, r0, r1, nl, sptr, scol, sval, x, f, y, c, st);
-    else if (tpr == 4) spmv_launch_t<MODE, P, 4>(pdl, r0, r1, nl, sptr, scol, sval, x, f, y, c, st);
-    else spmv_launch_t<MODE, P, 8>(pdl, r0, r1, nl, sptr, scol, sval, x, f, y, c, st);
+                   const double* x, const double* f, double* y, const double* c, cudaStream_t st, PfList pf) {
+    if (tpr == 1) spmv_launch_t<MODE, P, 1>(pdl, r0, r1, nl, sptr, scol, sval, x, f, y, c, st, pf);
+    else if (tpr == 2) spmv_launch_t<MODE, P, 2>(pdl, r0, r1, nl, sptr, scol, sval, x, f, y, c, st, pf);
+    else if (tpr == 4) spmv_launch_t<MODE, P, 4>(pdl, r0, r1, nl, sptr, scol, sval, x, f, y, c, st, pf);
+    else spmv_launch_t<MODE, P, 8>(pdl, r0, r1, nl, sptr, scol, sval, x, f, y, c, st, pf);
 }
 // rows [r0, r1) of a SELL operator whose level has nl rows
 void launch_spmv(bool pdl, int mode, bool poisson, int tpr, i64 r0, i64 r1, i64 nl, const i64* sptr,
                  const i32* scol, const double* sval, const double* x, const double* f, double* y, const double* c,
-                 cudaStream_t st) {
+                 cudaStream_t st, PfList pf = {}) {
     if (r1 <= r0) return;
     if (mode == 0) {
-        if (poisson) spmv_launch_p<0, true>(pdl, tpr, r0, r1, nl, sptr, scol, sval, x, f, y, c, st);
-        else spmv_launch_p<0, false>(pdl, tpr, r0, r1, nl, sptr, scol, sval, x, f, y, c, st);
+        if (poisson) spmv_launch_p<0, true>(pdl, tpr, r0, r1, nl, sptr, scol, sval, x, f, y, c, st, pf);
+        else spmv_launch_p<0, false>(pdl, tpr, r0, r1, nl, sptr, scol, sval, x, f, y, c, st, pf);
     } else {
-        if (poisson) spmv_launch_p<1, true>(pdl, tpr, r0, r1, nl, sptr, scol, sval, x, f, y, c, st);
-        else spmv_launch_p<1, false>(pdl, tpr, r0, r1, nl, sptr, scol, sval, x, f, y, c, st);
+        if (poisson) spmv_launch_p<1, true>(pdl, tpr, r0, r1, nl, sptr, scol, sval, x, f, y, c, st, pf);
+        else spmv_launch_p<1, false>(pdl, tpr, r0, r1, nl, sptr, scol, sval, x, f, y, c, st, pf);
     }
 }
 
@@ -1184,7 +1231,7 @@ static void for_my_pieces(const mgm_ctx* ctx, int j, i64 lo, i64 hi, F f) {
 }
 // exchange the pieces of y[lo, hi) after a distributed application
 static void dist_exchange(mgm_ctx* ctx, int j, double* y, i64 lo, i64 hi, cudaStream_t st) {
-    if (!dist_level(ctx, j) || !ctx->comm) return;
+    if (!dist_level(ctx, j) || !ctx->comm || g_dry) return;
     nccl_group_start();
     for (int q = 0; q < ctx->nranks; ++q) {
         i64 a, b;
@@ -1193,6 +1240,57 @@ static void dist_exchange(mgm_ctx* ctx, int j, double* y, i64 lo, i64 hi, cudaSt
     }
     nccl_group_end();
     ctx->vcycle_kernels++;
+}
+
+// ---------------------------------------------------------------------------------------
+// L2 prefetch pacing (solve_kernels.cuh l2_prefetch_share)
+// ---------------------------------------------------------------------------------------
+using Regions = std::vector<PfRegion>;
+static PfRegion pf_region(const void* p, i64 bytes) { return PfRegion{(const char*)p, (int64_t)bytes}; }
+// rows [a, b) of a SELL-32 operator: its value and column slices
+static void pf_sell(Regions& R, const std::vector<i64>& hptr, const i32* col, const double* val, i64 a, i64 b) {
+    if (hptr.empty() || b <= a) return;
+    const i64 s0 = hptr[(size_t)(a >> 5)], s1 = hptr[(size_t)std::min<i64>((b + 31) >> 5, (i64)hptr.size() - 1)];
+    R.push_back(pf_region(val + s0, 8 * (s1 - s0)));
+    R.push_back(pf_region(col + s0, 4 * (s1 - s0)));
+}
+// Register the next kernel of the schedule as a prefetch target with the given operator
+// regions and return what this kernel (if it can issue prefetches) should prefetch.
+static PfList pf_take(mgm_ctx* ctx, const Regions& regs, bool issuer = true, i64 budget = 0) {
+    if (ctx->pf_mode == 1) {
+        Regions capped;
+        i64 left = ctx->pf_cap;
+        for (const PfRegion& r : regs) {
+            if (left <= 0) break;
+            const uintptr_t p0 = (uintptr_t)r.p & ~(uintptr_t)15;
+            i64 b = std::min<i64>((i64)((uintptr_t)r.p - p0) + r.bytes, left);
+            b = (b + 15) & ~(i64)15;
+            if (b > 0) capped.push_back(PfRegion{(const char*)p0, (int64_t)b});
+            left -= b;
+        }
+        ctx->pf_tg.push_back(capped);
+        return PfList{nullptr, 0, 0};
+    }
+    if (ctx->pf_mode != 2) return PfList{nullptr, 0, 0};
+    const int t = ctx->pf_pos++;
+    const int T = (int)ctx->pf_off.size() - 1;
+    if (!issuer || t + 1 >= T) return PfList{nullptr, 0, 0};
+    int hi = std::min(T - 1, t + ctx->pf_dist);
+    if (budget > 0) {  // as many following targets as fit the budget
+        i64 acc = 0;
+        hi = t;
+        while (hi + 1 < T) {
+            i64 tb = 0;
+            for (int q = ctx->pf_off[hi + 1]; q < ctx->pf_off[hi + 2]; ++q) tb += ctx->pf_flat[(size_t)q].bytes;
+            if (acc + tb > budget && hi > t) break;
+            acc += tb;
+            ++hi;
+        }
+    }
+    const int lo = std::max(ctx->pf_last + 1, t + 1);
+    if (hi < lo) return PfList{nullptr, 0, 0};
+    ctx->pf_last = hi;
+    return PfList{ctx->d_pf + ctx->pf_off[lo], ctx->pf_off[hi + 1] - ctx->pf_off[lo], ctx->pf_late};
 }
 
 bool timing_on(const mgm_ctx* ctx);
@@ -1232,7 +1330,13 @@ void enqueue_sweep(mgm_ctx* ctx, int j, bool backward, cudaStream_t st) {
                        (int)b, rpc, L.uniform_w, (const i64*)L.sptr, (const i32*)L.scol, (const double*)L.sval,
                        (const double*)L.f, L.u);
             } else {
-                launch_gs(ctx->pdl, ctx->poisson, L.tpr, (int)a, (int)b, (int)(b - (a & ~31)), L, st);
+                Regions rg;
+                if (!ctx->pf_l0only || j == 0) {
+                    pf_sell(rg, L.h_sptr, L.scol, L.sval, a, b);
+                    if (!ctx->pf_nof) rg.push_back(pf_region(L.f + a, 8 * (b - a)));
+                }
+                const PfList pf = pf_take(ctx, rg, !ctx->pf_l0only || j == 0);
+                launch_gs(ctx->pdl, ctx->poisson, L.tpr, (int)a, (int)b, (int)(b - (a & ~31)), L, st, pf);
             }
             bytes += sweep_colour_bytes(L, b - a);
             ++nl;
@@ -1269,7 +1373,10 @@ void enqueue_spmv(mgm_ctx* ctx, int j, const double* x, double* y, cudaStream_t 
 void enqueue_residual(mgm_ctx* ctx, int j, const double* f, const double* u, double* t, cudaStream_t st) {
     Level& L = ctx->lv[j];
     for_my_pieces(ctx, j, 0, L.n, [&](i64 a, i64 b) {
-        launch_spmv(ctx->pdl, 1, ctx->poisson, L.stpr, a, b, L.n, L.sptr, L.scol, L.sval, u, f, t, L.c, st);
+        Regions rg;
+        if (!ctx->pf_l0only) pf_sell(rg, L.h_sptr, L.scol, L.sval, a, b);
+        const PfList pf = pf_take(ctx, rg, !ctx->pf_l0only);
+        launch_spmv(ctx->pdl, 1, ctx->poisson, L.stpr, a, b, L.n, L.sptr, L.scol, L.sval, u, f, t, L.c, st, pf);
         ctx->vcycle_kernels++;
     });
     dist_exchange(ctx, j, t, 0, L.n, st);
@@ -1281,7 +1388,10 @@ void enqueue_restrict(mgm_ctx* ctx, int j, const double* x, double* y, cudaStrea
     Level& L = ctx->lv[j];
     Level& Ln = ctx->lv[j + 1];
     for_my_pieces(ctx, j, 0, Ln.n, [&](i64 a, i64 b) {
-        launch_spmv(ctx->pdl, 0, false, L.rtpr, a, b, Ln.n, L.rptr, L.rcol, L.rval, x, nullptr, y, nullptr, st);
+        Regions rg;
+        if (!ctx->pf_l0only) pf_sell(rg, L.h_rptr, L.rcol, L.rval, a, b);
+        const PfList pf = pf_take(ctx, rg, !ctx->pf_l0only);
+        launch_spmv(ctx->pdl, 0, false, L.rtpr, a, b, Ln.n, L.rptr, L.rcol, L.rval, x, nullptr, y, nullptr, st, pf);
         ctx->vcycle_kernels++;
     });
     dist_exchange(ctx, j, y, 0, Ln.n, st);
@@ -1298,8 +1408,14 @@ void enqueue_interp_correct(mgm_ctx* ctx, int j, const double* ec, double* e, cu
                              : (L.pm <= 8 ? k_interp_correct<false, 8> : k_interp_correct<false, 16>);
     for_my_pieces(ctx, j, 0, L.n, [&](i64 a, i64 b) {
         const i64 extra = (ctx->poisson && b == L.n) ? 1 : 0;  // multiplier thread
+        Regions rg;
+        for (int k = 0; k < L.pm && b > a && !ctx->pf_l0only; ++k) {  // slot-major [pm][n]
+            rg.push_back(pf_region(L.pval + (i64)k * L.n + a, 8 * (b - a)));
+            rg.push_back(pf_region(L.pcol + (i64)k * L.n + a, 4 * (b - a)));
+        }
+        const PfList pf = pf_take(ctx, rg, !ctx->pf_l0only);
         launch(ctx->pdl, kern, blocks_for(b - a + extra, 256), 256, 0, st, (int)a, (int)b, (int)L.n, L.pm,
-               (const i32*)L.pcol, (const double*)L.pval, ec, e, (int)Ln.n);
+               (const i32*)L.pcol, (const double*)L.pval, ec, e, (int)Ln.n, pf);
         ctx->vcycle_kernels++;
     });
     dist_exchange(ctx, j, e, 0, L.n, st);
@@ -1315,7 +1431,8 @@ void enqueue_coarse(mgm_ctx* ctx, const double* r, double* e, cudaStream_t st) {
 }
 
 void enqueue_zero(mgm_ctx* ctx, double* x, i64 n, cudaStream_t st) {
-    launch(ctx->pdl, k_fill, blocks_for(n, 256), 256, 0, st, n, x, 0.0);
+    const PfList pf = pf_take(ctx, Regions{}, !ctx->pf_l0only);
+    launch(ctx->pdl, k_fill, blocks_for(n, 256), 256, 0, st, n, x, 0.0, pf);
     ctx->vcycle_kernels++;
 }
 
@@ -1384,9 +1501,12 @@ void enqueue_vcycle(mgm_ctx* ctx, cudaStream_t st) {
         cfg.attrs = at;
         cfg.numAttrs = g_use_pdl ? 2 : 1;
         cfg.dynamicSmemBytes = ctx->bot_smem;
-        note_launch(cudaLaunchKernelEx(&cfg, k_vcycle_bottom, (const BPhase*)ctx->d_phases, ctx->nphases,
-                                       ctx->d_trace ? ctx->d_trace + 256 : (unsigned long long*)nullptr),
-                    ctx->bot_cluster, BOT_THREADS, ctx->bot_smem);
+        const PfList pf = pf_take(ctx, ctx->pf_l0only ? Regions{} : ctx->bot_pf, !ctx->pf_l0only, ctx->pf_bot_budget);
+        if (!g_dry)
+            note_launch(cudaLaunchKernelEx(&cfg, k_vcycle_bottom, (const BPhase*)ctx->d_phases, ctx->nphases,
+                                           ctx->d_trace ? ctx->d_trace + 256 : (unsigned long long*)nullptr, pf,
+                                           ctx->bot_arm0, ctx->bot_arm1),
+                        ctx->bot_cluster, BOT_THREADS, ctx->bot_smem);
         ctx->vcycle_kernels++;
     } else {
         enqueue_coarse(ctx, lv[p - 1].f, lv[p - 1].u, st);                 // line 10
@@ -1406,12 +1526,52 @@ void enqueue_vcycle(mgm_ctx* ctx, cudaStream_t st) {
 
 bool timing_on(const mgm_ctx* ctx) { return ctx->timer[0].on || ctx->timer[1].on; }
 
+// Record the V-cycle schedule's prefetch targets with a dry enqueue pass and upload the
+// region table (a new table only when the schedule changed: captured graphs keep theirs).
+mgm_status pf_prepare(mgm_ctx* ctx, cudaStream_t st) {
+    ctx->pf_mode = 0;
+    if (ctx->pf_dist <= 0) return MGM_OK;
+    ctx->pf_tg.clear();
+    ctx->pf_mode = 1;
+    g_dry = true;
+    enqueue_vcycle(ctx, st);
+    g_dry = false;
+    ctx->pf_mode = 0;
+    std::vector<PfRegion> flat;
+    std::vector<int> off{0};
+    for (const auto& t : ctx->pf_tg) {
+        flat.insert(flat.end(), t.begin(), t.end());
+        off.push_back((int)flat.size());
+    }
+    const bool same = ctx->d_pf && off == ctx->pf_off && flat.size() == ctx->pf_flat.size() &&
+                      std::equal(flat.begin(), flat.end(), ctx->pf_flat.begin(),
+                                 [](const PfRegion& a, const PfRegion& b) { return a.p == b.p && a.bytes == b.bytes; });
+    if (!same) {
+        if (ctx->d_pf) ctx->pf_old.push_back(ctx->d_pf);
+        ctx->d_pf = nullptr;
+        CK(cudaMalloc((void**)&ctx->d_pf, sizeof(PfRegion) * std::max<size_t>(1, flat.size())));
+        if (!flat.empty())
+            CK(cudaMemcpy(ctx->d_pf, flat.data(), sizeof(PfRegion) * flat.size(), cudaMemcpyHostToDevice));
+        ctx->pf_flat = flat;
+        ctx->pf_off = off;
+    }
+    ctx->pf_mode = 2;
+    ctx->pf_pos = 0;
+    ctx->pf_last = 0;
+    return MGM_OK;
+}
+
 mgm_status build_graph(mgm_ctx* ctx) {
     if (ctx->vgraph) return MGM_OK;
     cudaGraph_t g;
+    {
+        mgm_status ps = pf_prepare(ctx, ctx->st);
+        if (ps) return ps;
+    }
     CK(cudaStreamBeginCapture(ctx->st, cudaStreamCaptureModeThreadLocal));
     g_launch_err.clear();
     enqueue_vcycle(ctx, ctx->st);
+    ctx->pf_mode = 0;
     const cudaError_t ce = cudaStreamEndCapture(ctx->st, &g);
     if (ce != cudaSuccess || !g_launch_err.empty()) {
         ctx->err = "V-cycle capture failed: " + std::string(cudaGetErrorString(ce)) + "; first failed launch: " +
@@ -1428,8 +1588,11 @@ mgm_status build_graph(mgm_ctx* ctx) {
 // run one V-cycle on lv[0].f / lv[0].u
 mgm_status run_vcycle(mgm_ctx* ctx, cudaStream_t st) {
     if (timing_on(ctx)) {
+        mgm_status ps = pf_prepare(ctx, st);
+        if (ps) return ps;
         timer_begin(ctx, 2, st);
         enqueue_vcycle(ctx, st);
+        ctx->pf_mode = 0;
         timer_end(ctx, 2, st, 0.0);
         return MGM_OK;
     }
@@ -1942,6 +2105,12 @@ mgm_status mgm_setup(const double* points, const double* normals, int64_t n_poin
     ctx->nthreads = std::max(1, std::min(64, (int)std::thread::hardware_concurrency()));
     if (const char* e = std::getenv("MGM_DIST_LEVELS")) ctx->dist_levels = std::max(0, std::atoi(e));
     if (const char* e = std::getenv("MGM_DIST_FAKE_RANKS")) ctx->fake_ranks = ctx->poisson ? 0 : std::max(0, std::atoi(e));
+    if (const char* e = std::getenv("MGM_PF_DIST")) ctx->pf_dist = std::max(0, std::atoi(e));
+    if (const char* e = std::getenv("MGM_PF_CAP_MB")) ctx->pf_cap = (i64)std::max(0, std::atoi(e)) << 20;
+    if (std::getenv("MGM_PF_LATE")) ctx->pf_late = 1;
+    if (std::getenv("MGM_PF_NOF")) ctx->pf_nof = 1;
+    if (std::getenv("MGM_PF_L0ONLY")) ctx->pf_l0only = 1;
+    if (const char* e = std::getenv("MGM_PF_BOT_MB")) ctx->pf_bot_budget = (i64)std::max(0, std::atoi(e)) << 20;
     cudaGetDevice(&ctx->device);
     (void)cuda_stream;
     if (cudaStreamCreateWithFlags(&ctx->st, cudaStreamNonBlocking) != cudaSuccess) {
@@ -2113,6 +2282,8 @@ mgm_status mgm_destroy(mgm_ctx* ctx) {
         if (ptr) cudaFree(ptr);
     if (ctx->hh) cudaFreeHost(ctx->hh);
     for (void* q : ctx->bot_mem) cudaFree(q);
+    if (ctx->d_pf) cudaFree(ctx->d_pf);
+    for (void* q : ctx->pf_old) cudaFree(q);
     if (ctx->d_trace) cudaFree(ctx->d_trace);
     if (ctx->vgraph) cudaGraphExecDestroy(ctx->vgraph);
     if (ctx->comm) nccl().CommDestroy(ctx->comm);
@@ -2387,6 +2558,18 @@ mgm_status mgm_bottom_trace_read(const mgm_ctx* ctx, uint64_t* stamps_ns, int ca
             meta[4 * q + 3] = 1 << ph[q].tpr_log2;
         }
     }
+    return MGM_OK;
+}
+
+mgm_status mgm_bottom_ftrace_read(const mgm_ctx* ctx, int64_t* clk, int cap, int* n) {
+    if (!ctx || !n || !clk) return MGM_ERR_ARG;
+    *n = (ctx->d_trace && ctx->botJ > 0) ? ctx->nphases : 0;
+    if (*n == 0) return MGM_OK;
+    if (cap < *n) return MGM_ERR_ARG;
+    for (int c = 0; c < 2; ++c)
+        if (cudaMemcpy(clk + (size_t)c * 8 * cap, ctx->d_trace + 256 + BOT_MAX_PHASES + (size_t)c * 8 * BOT_MAX_PHASES,
+                       sizeof(int64_t) * 8 * (size_t)*n, cudaMemcpyDeviceToHost) != cudaSuccess)
+            return MGM_ERR_CUDA;
     return MGM_OK;
 }
 

@@ -21,6 +21,37 @@ namespace mgm {
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
+// L2 prefetch pacing ("L2 prefetch pacing").  Inside the V-cycle graph a
+// kernel is handed the operator regions (matrix values, columns, right-hand side block) of
+// the NEXT kernel(s) of the schedule; at start every CTA issues bulk L2 prefetches for its
+// share of those bytes.  Operator data is immutable during the solve, so the prefetch needs
+// no ordering: the HBM streams colour c+1's matrix block while colour c gathers and
+// updates out of L2, instead of each small colour kernel paying its own HBM ramp.
+// Regions are 16-byte aligned with sizes that are multiples of 16 (the host rounds).
+struct PfRegion {
+    const char* p;
+    int64_t bytes;
+};
+struct PfList {
+    const PfRegion* r;  // device table
+    int n;
+    int late;  // 1: issue after the kernel's own prologue loads (experiment, MGM_PF_LATE)
+};
+__device__ __forceinline__ void l2_prefetch_share(const PfList& pf) {
+    if (pf.n <= 0 || threadIdx.x != 0) return;
+    const int64_t G = gridDim.x, b = blockIdx.x;
+    for (int i = 0; i < pf.n; ++i) {
+        const PfRegion R = pf.r[i];
+        const int64_t lo = (R.bytes * b / G) & ~(int64_t)127;
+        const int64_t hi = (b + 1 == G) ? R.bytes : ((R.bytes * (b + 1) / G) & ~(int64_t)127);
+        for (int64_t o = lo; o < hi; o += 32768) {
+            const int64_t len = hi - o < 32768 ? hi - o : 32768;
+            const uint32_t sz = (uint32_t)((len + 15) & ~(int64_t)15);
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(R.p + o), "r"(sz) : "memory");
+        }
+    }
+}
+
 // Streaming loads for matrix data (read once per sweep): non-coherent path, no L1
 // allocation, L2 evict_first so that the streamed upper levels do not evict the small
 // bottom levels (bottom_kernel.cuh loads those with evict_last).  Not volatile, so the
@@ -77,8 +108,9 @@ __global__ void __launch_bounds__(256) k_gs_colour(int r0, int r1, int Wu, const
                                                    const int* __restrict__ scol,
                                                    const double* __restrict__ sval,
                                                    const double* __restrict__ f, double* u,
-                                                   const double* __restrict__ c, int n) {
+                                                   const double* __restrict__ c, int n, PfList pf) {
     pdl_trigger();
+    if (!pf.late) l2_prefetch_share(pf);
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
     const int r = (r0 & ~31) + g / TPR;
     const int part = g % TPR;
@@ -101,6 +133,7 @@ __global__ void __launch_bounds__(256) k_gs_colour(int r0, int r1, int Wu, const
     } else {
         fr.load(sval, scol, 0, 0);
     }
+    if (pf.late) l2_prefetch_share(pf);
     pdl_wait();
     // epilogue operands issued together with the gathers (one memory round trip)
     double fr_v = 0.0, ur = 0.0, cl = 0.0;
@@ -206,8 +239,9 @@ __global__ void __launch_bounds__(256) k_sell_spmv(int r0, int r1, int nl, const
                                                    const double* __restrict__ x,
                                                    const double* __restrict__ f,
                                                    double* __restrict__ y,
-                                                   const double* __restrict__ c) {
+                                                   const double* __restrict__ c, PfList pf) {
     pdl_trigger();
+    l2_prefetch_share(pf);
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
     const int r = (r0 & ~31) + g / TPR;
     const int part = g % TPR;
@@ -243,8 +277,9 @@ template <bool POISSON, int M>
 __global__ void __launch_bounds__(256) k_interp_correct(int r0, int r1, int n, int m, const int* __restrict__ pcol,
                                                         const double* __restrict__ pval,
                                                         const double* __restrict__ ec,
-                                                        double* __restrict__ e, int nc) {
+                                                        double* __restrict__ e, int nc, PfList pf) {
     pdl_trigger();
+    l2_prefetch_share(pf);
     const int r = r0 + blockIdx.x * blockDim.x + threadIdx.x;
     int cidx[M];
     double a[M];
@@ -323,8 +358,9 @@ __global__ void __launch_bounds__(256) k_coarse_solve(int m, int lu_in_smem, con
     for (int i = lane; i < m; i += 32) x[i] = b[i];
 }
 
-__global__ void k_fill(int64_t n, double* __restrict__ x, double v) {
+__global__ void k_fill(int64_t n, double* __restrict__ x, double v, PfList pf) {
     pdl_trigger();
+    l2_prefetch_share(pf);
     pdl_wait();
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) x[i] = v;

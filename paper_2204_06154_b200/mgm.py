@@ -82,6 +82,7 @@ _SIGS = {
                         ctypes.POINTER(ctypes.c_int), ctypes.c_char_p, ctypes.c_int], ctypes.c_int),
     "mgm_bottom_trace_read": ([_vp, ctypes.POINTER(ctypes.c_uint64), ctypes.c_int,
                                ctypes.POINTER(ctypes.c_int), _i32p], ctypes.c_int),
+    "mgm_bottom_ftrace_read": ([_vp, _i64p, ctypes.c_int, ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
     "mgm_host_morton": ([_f64p, _i64, _i64p], ctypes.c_int),
     "mgm_host_knn": ([_f64p, _i64, _f64p, _i64, ctypes.c_int, _i32p], ctypes.c_int),
     "mgm_host_wse": ([_f64p, _i64, _i64, _i64p], ctypes.c_int),
@@ -329,6 +330,15 @@ def mgm_bottom_trace_read(ctx):
     _check(load_library().mgm_bottom_trace_read(ctx, buf, 8192, ctypes.byref(n), meta.ctypes.data_as(_i32p)), ctx)
     k = n.value
     return np.array(buf[:k], dtype=np.uint64), meta[:k]
+
+
+def mgm_bottom_ftrace_read(ctx):
+    """Fine per-phase clock timeline of the bottom kernel (MGM_TRACE=2): int64 [2, n, 8]."""
+    cap = 1024
+    clk = np.zeros((2, cap, 8), dtype=np.int64)
+    n = ctypes.c_int()
+    _check(load_library().mgm_bottom_ftrace_read(ctx, clk.ctypes.data_as(_i64p), cap, ctypes.byref(n)), ctx)
+    return clk[:, :n.value]
 
 
 def mgm_host_morton(points):
