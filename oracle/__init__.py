@@ -274,13 +274,20 @@ def interp_operator(fine: np.ndarray, coarse: np.ndarray, m: int) -> CSR:
     return csr_from_rows(st, w, cnt.astype(np.int64), len(coarse))
 
 
-def greedy_colour(A: CSR):
-    """O11 greedy colouring of sym(pattern(A)) minus diagonal, vertices in index order."""
+COLOUR_PASSES = 10   # O11: iterated-greedy passes after the first greedy pass
+
+
+def greedy_colour(A: CSR, passes: int = COLOUR_PASSES):
+    """O11 colouring of sym(pattern(A)) minus diagonal: greedy with vertices in index (Morton)
+    order, then ``passes`` iterated-greedy passes (vertices by descending previous colour,
+    ties by index; each gives the smallest colour unused by neighbours coloured earlier in
+    the pass)."""
     T = A.transpose()
     col = np.empty(A.shape[0], dtype=np.int32)
     nc = ctypes.c_int32(0)
     rc = lib().orc_greedy_colour(ctypes.c_int64(A.shape[0]), _p(A.ptr, i64p), _p(A.idx, i64p),
-                                 _p(T.ptr, i64p), _p(T.idx, i64p), _p(col, i32p), ctypes.byref(nc))
+                                 _p(T.ptr, i64p), _p(T.idx, i64p), ctypes.c_int(passes), _p(col, i32p),
+                                 ctypes.byref(nc))
     if rc:
         raise OracleError(rc, -1, "too many colours")
     return col, int(nc.value)
@@ -423,7 +430,7 @@ class Oracle:
                 nxt.c = lv.R.matvec(lv.c)                          # border I_h^H b^T
             self.levels.append(nxt)
         for lv in self.levels[:-1]:
-            lv.colour, lv.ncolours = greedy_colour(lv.L)
+            lv.colour, lv.ncolours = greedy_colour(lv.L, lp.get("colour_passes", COLOUR_PASSES))
             if lp.get("gs_order", "colour") == "rcm":
                 # the paper's own smoother (Alg. 2 lines 2-3 and 11-12):
                 # lexicographic Gauss-Seidel in reverse Cuthill-McKee order of L_j

@@ -609,30 +609,58 @@ int orc_spgemm(i64 nra, const i64* ap, const i64* ai, const double* av,
 /* O11 greedy colouring of pattern(A) U pattern(A^T) minus the diagonal, vertices visited in
  * index order, colour = smallest non-negative integer unused by coloured neighbours.
  * at_p/at_i = transpose pattern.  Returns number of colours in *ncol. */
-int orc_greedy_colour(i64 n, const i64* ap, const i64* ai, const i64* tp, const i64* ti,
-                      int32_t* colour, int32_t* ncol) {
-    int32_t* used = (int32_t*)malloc(sizeof(int32_t) * 4096);
-    for (int c = 0; c < 4096; ++c) used[c] = -1;
+/* One greedy pass (O11): visit vertices in `order`, give each the smallest colour not used by
+ * a neighbour (sym(pattern) minus the diagonal) already coloured in this pass. */
+static int greedy_pass(i64 n, const i64* ap, const i64* ai, const i64* tp, const i64* ti, const i64* order,
+                       int32_t* colour, int32_t* used, int32_t* ncol) {
     int32_t maxc = 0;
     for (i64 i = 0; i < n; ++i) colour[i] = -1;
-    for (i64 i = 0; i < n; ++i) {
+    for (i64 q = 0; q < n; ++q) {
+        i64 i = order[q];
         for (i64 t = ap[i]; t < ap[i + 1]; ++t) {
             i64 j = ai[t];
-            if (j != i && colour[j] >= 0) used[colour[j]] = (int32_t)i;
+            if (j != i && colour[j] >= 0) used[colour[j]] = (int32_t)q;
         }
         for (i64 t = tp[i]; t < tp[i + 1]; ++t) {
             i64 j = ti[t];
-            if (j != i && colour[j] >= 0) used[colour[j]] = (int32_t)i;
+            if (j != i && colour[j] >= 0) used[colour[j]] = (int32_t)q;
         }
         int32_t c = 0;
-        while (used[c] == (int32_t)i) ++c;
-        if (c >= 4095) { free(used); return -1; }
+        while (used[c] == (int32_t)q) ++c;
+        if (c >= 4095) return -1;
         colour[i] = c;
         if (c + 1 > maxc) maxc = c + 1;
     }
     *ncol = maxc;
-    free(used);
     return 0;
+}
+
+/* O11: greedy colouring in index (Morton) order, then `passes` iterated-greedy passes
+ * (Culberson): each visits the vertices by descending colour of the previous pass, ties by
+ * index; a pass never increases the number of colours. */
+int orc_greedy_colour(i64 n, const i64* ap, const i64* ai, const i64* tp, const i64* ti, int passes,
+                      int32_t* colour, int32_t* ncol) {
+    int32_t* used = (int32_t*)malloc(sizeof(int32_t) * 4096);
+    i64* order = (i64*)malloc(sizeof(i64) * (size_t)(n > 0 ? n : 1));
+    i64* cnt = (i64*)malloc(sizeof(i64) * 4097);
+    int rc = 0;
+    for (int c = 0; c < 4096; ++c) used[c] = -1;
+    for (i64 i = 0; i < n; ++i) order[i] = i;
+    rc = greedy_pass(n, ap, ai, tp, ti, order, colour, used, ncol);
+    for (int r = 0; r < passes && rc == 0; ++r) {
+        /* vertices by descending colour, ascending index within a colour */
+        int32_t K = *ncol;
+        for (int32_t c = 0; c <= K; ++c) cnt[c] = 0;
+        for (i64 i = 0; i < n; ++i) cnt[K - 1 - colour[i] + 1]++;
+        for (int32_t c = 0; c < K; ++c) cnt[c + 1] += cnt[c];
+        for (i64 i = 0; i < n; ++i) order[cnt[K - 1 - colour[i]]++] = i;
+        for (int c = 0; c < 4096; ++c) used[c] = -1;
+        rc = greedy_pass(n, ap, ai, tp, ti, order, colour, used, ncol);
+    }
+    free(cnt);
+    free(order);
+    free(used);
+    return rc;
 }
 
 /* y = A x, row sums in stored (ascending column) order */

@@ -861,7 +861,7 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
         lib2mor[j].resize(n);
         mor2lib[j].resize(n);
         if (j + 1 < p) {
-            L.ncol = greedy_colouring(Lm[j], colour_mor[j]);
+            L.ncol = greedy_colouring(Lm[j], colour_mor[j], colour_passes());
             L.coff.assign(L.ncol + 1, 0);
             for (i64 i = 0; i < n; ++i) L.coff[colour_mor[j][i] + 1]++;
             for (int c = 0; c < L.ncol; ++c) L.coff[c + 1] += L.coff[c];
@@ -2624,7 +2624,7 @@ mgm_status mgm_host_colouring(int64_t n, const int64_t* ptr, const int32_t* col,
     A.ptr.assign(ptr, ptr + n + 1);
     A.col.assign(col, col + ptr[n]);
     std::vector<i32> c;
-    int nc = greedy_colouring(A, c);
+    int nc = greedy_colouring(A, c, colour_passes());
     std::copy(c.begin(), c.end(), colour);
     if (n_colours) *n_colours = nc;
     return MGM_OK;

@@ -36,7 +36,9 @@ void wse_eliminate(const double* pts, i64 n, i64 nt, const std::vector<double>& 
                    std::vector<i64>& keep, int nthreads);
 
 // Greedy colouring (O11) of sym(pattern(A)) minus the diagonal in index order.
-int greedy_colouring(const HostCSR& A, std::vector<i32>& colour);
+int greedy_colouring(const HostCSR& A, std::vector<i32>& colour, int passes);
+// O11 iterated-greedy passes: 10, or MGM_COLOUR_PASSES (experiments; the oracle must match)
+int colour_passes();
 
 HostCSR transpose(const HostCSR& A);
 

@@ -221,14 +221,22 @@ def test_colouring_proper_and_multicolour_gs_is_dense_gs():
         np.fill_diagonal(S, False)
         i, j = np.nonzero(S)
         assert not np.any(lv.colour[i] == lv.colour[j])          # proper
-        # greedy: every vertex's colour is the smallest not used by earlier neighbours
+        # any greedy colouring (in whatever visiting order) is complete: a vertex of colour c
+        # has neighbours of every colour 0..c-1 (it got c because those were taken)
+        for v in range(lv.N):
+            assert set(range(lv.colour[v])) <= set(lv.colour[S[v]].tolist())
+        # the first pass is greedy in index (Morton) order: each vertex takes the smallest
+        # colour not used by its lower-index neighbours
+        c0, n0 = O.greedy_colour(lv.L, passes=0)
         for v in range(0, lv.N, 37):
             nb = np.flatnonzero(S[v]); nb = nb[nb < v]
-            used = set(lv.colour[nb].tolist())
+            used = set(c0[nb].tolist())
             c = 0
             while c in used:
                 c += 1
-            assert lv.colour[v] == c
+            assert c0[v] == c
+        # iterated-greedy passes never add colours (Culberson's theorem)
+        assert lv.ncolours <= n0 and lv.ncolours == lv.colour.max() + 1
         # multicolour GS = forward GS on the colour-major permuted matrix (textbook form)
         rng = np.random.default_rng(1)
         f = rng.uniform(-1, 1, lv.N)
