@@ -206,7 +206,9 @@ mgm_status mgm_apply(mgm_ctx* ctx, int level, int op, const double* x_dev, const
 
 /* Per-kernel-class device timing (CUDA events around every launch of that class on the
  * solve stream; adds events, use only for measurement).  cls: 0 = level-0 GS colour sweep
- * kernels, 1 = level-0 SpMV, 2 = whole V-cycle.  enable = 1 resets the accumulators. */
+ * kernels (full sweeps), 1 = level-0 SpMV, 2 = whole V-cycle, 3 = level-0 GS colour kernels
+ * of the first presmooth from a zero guess (Krylov preconditioner; reads diagonal +
+ * earlier-colour entries only).  enable = 1 resets the accumulators. */
 mgm_status mgm_timing_enable(mgm_ctx* ctx, int cls, int enable);
 /* total_ms = sum of event-measured durations, launches = number of timed launches,
  * alg_bytes = algorithmic bytes those launches move (DESIGN.md byte model). */
@@ -226,6 +228,13 @@ mgm_status mgm_vcycle_kernel_count(const mgm_ctx* ctx, int64_t* count);
  * newline-separated stage labels into labels[label_cap] (may be NULL).  MGM_ERR_ARG if
  * cap < *n. */
 mgm_status mgm_trace_read(const mgm_ctx* ctx, uint64_t* stamps_ns, int cap, int* n, char* labels, int label_cap);
+
+/* Stored entries of level `level`'s operator that a forward Gauss-Seidel sweep from a zero
+ * guess reads (the diagonal and the earlier-colour columns of every row; k_gs_colour ZG,
+ * used for the first presmooth sweep on levels >= 1 and, inside the Krylov solvers, on
+ * level 0), or nnz(L_j) when zero-guess sweeps are not used (Poisson, backward presmooth,
+ * MGM_NO_ZG).  For byte models. */
+mgm_status mgm_level_zg_nnz(const mgm_ctx* ctx, int level, int64_t* nnz_zg);
 
 /* Diagnostics: start time (%globaltimer, ns) of every phase of the one-kernel bottom of the
  * last V-cycle (MGM_TRACE set at setup), *n = number of phases (0 if tracing is off or the

@@ -87,6 +87,9 @@ struct Level {
     double* sval = nullptr;
     i64 sell_stored = 0, nnz = 0;
     std::vector<i64> h_sptr, h_rptr;  // host copies of the slice offsets (L2 prefetch regions)
+    i32* slw = nullptr;                 // per slice: slots read by a sweep from a zero guess (pack_sell)
+    uint8_t* nlow = nullptr;            // per row: its earlier-colour entries (slots 1..nlow)
+    std::vector<i64> lower_per_colour;  // per colour: stored entries such a sweep reads (diag + earlier colours)
     int tpr = 1, rtpr = 1;  // threads per row for L_j (colour sweeps) and R_j kernels
     int stpr = 1;           // threads per row for full-level SpMV / residual on L_j
     int gs_block = 256;     // threads per block of the colour kernels
@@ -153,6 +156,9 @@ struct mgm_ctx {
     // streams / graph
     cudaStream_t st = nullptr;
     cudaGraphExec_t vgraph = nullptr;
+    cudaGraphExec_t vgraph0 = nullptr;  // the same V-cycle from a zero guess on level 0 (Krylov preconditioner)
+    bool vc_zero_guess = false;         // set while enqueueing vgraph0
+    bool no_zg = false;                 // MGM_NO_ZG: no zero-guess sweeps (comparison)
     bool pdl = false;  // set while enqueueing the V-cycle (PDL launches)
     // bottom of the V-cycle (levels botJ..p-1) in one thread-block-cluster kernel
     // (bottom_kernel.cuh); botJ < 0 = off
@@ -206,7 +212,7 @@ struct mgm_ctx {
     double* dh = nullptr;    // device scratch: h1[128], h2[128], nrm2, misc
     double* hh = nullptr;    // pinned host mirror
     // timing
-    KernelTimer timer[3];
+    KernelTimer timer[4];
     double setup_ms = 0.0;
     // errors
     std::string err;
@@ -275,9 +281,15 @@ static void launch(bool pdl, void (*kern)(KArgs...), unsigned grid, unsigned blo
 namespace {
 
 // Pack a Morton-order CSR into lib-order SELL-32 (diagonal first for square operators).
+// With a colouring (colour_lib: GS colour of each lib row), the stored row order is
+// [diagonal | earlier-colour columns | later-colour columns], each group in ascending Morton
+// column, and slw[s] = 1 + the largest earlier-colour count of slice s: a Gauss-Seidel sweep
+// from a zero guess reads only those first slw slots (the later-colour values are still 0).
+// lib_csr keeps the plain order (diagonal first, ascending column).
 void pack_sell(const HostCSR& A, const std::vector<i64>& row_lib2mor, const std::vector<i32>& col_mor2lib,
                bool diag_first, std::vector<i64>& sptr, std::vector<i32>& scol, std::vector<double>& sval,
-               HostCSR* lib_csr) {
+               HostCSR* lib_csr, const std::vector<i32>* colour_lib = nullptr, std::vector<i32>* slw = nullptr,
+               std::vector<i64>* lower_per_colour = nullptr, std::vector<uint8_t>* nlow_row = nullptr) {
     i64 n = (i64)row_lib2mor.size();
     i64 ns = (n + 31) / 32;
     sptr.assign(ns + 1, 0);
@@ -298,7 +310,14 @@ void pack_sell(const HostCSR& A, const std::vector<i64>& row_lib2mor, const std:
         lib_csr->col.clear();
         lib_csr->val.clear();
     }
-    std::vector<std::pair<i32, double>> row;
+    std::vector<std::pair<i32, double>> row, srow;
+    if (slw) slw->assign(ns, 1);
+    if (nlow_row) nlow_row->assign(n, 0);
+    if (lower_per_colour && colour_lib) {
+        i32 nc = 0;
+        for (i32 c : *colour_lib) nc = std::max(nc, c + 1);
+        lower_per_colour->assign(nc, 0);
+    }
     for (i64 r = 0; r < n; ++r) {
         i64 mr = row_lib2mor[r];
         row.clear();
@@ -309,11 +328,24 @@ void pack_sell(const HostCSR& A, const std::vector<i64>& row_lib2mor, const std:
             if (!diag_first || A.col[t] != (i32)mr) row.push_back({A.col[t], A.val[t]});
         i64 s = r / 32, lane = r % 32;
         i64 w = (sptr[s + 1] - sptr[s]) / 32;
+        srow = row;
+        if (colour_lib && diag_first && !row.empty()) {  // [diag | earlier colours | later colours]
+            const i32 cr = (*colour_lib)[r];
+            i64 o = 1;
+            for (size_t k = 1; k < row.size(); ++k)
+                if ((*colour_lib)[col_mor2lib[row[k].first]] < cr) srow[o++] = row[k];
+            const i64 nlow = o - 1;
+            for (size_t k = 1; k < row.size(); ++k)
+                if ((*colour_lib)[col_mor2lib[row[k].first]] >= cr) srow[o++] = row[k];
+            if (slw) (*slw)[s] = std::max<i32>((*slw)[s], (i32)(1 + nlow));
+            if (nlow_row) (*nlow_row)[r] = (uint8_t)std::min<i64>(nlow, 255);
+            if (lower_per_colour) (*lower_per_colour)[cr] += 1 + nlow;
+        }
         for (i64 k = 0; k < w; ++k) {
             i64 o = sptr[s] + 32 * k + lane;
-            if (k < (i64)row.size()) {
-                scol[o] = col_mor2lib[row[k].first];
-                sval[o] = row[k].second;
+            if (k < (i64)srow.size()) {
+                scol[o] = col_mor2lib[srow[k].first];
+                sval[o] = srow[k].second;
             } else {
                 scol[o] = diag_first ? (i32)r : (row.empty() ? 0 : col_mor2lib[row[0].first]);
                 sval[o] = 0.0;
@@ -891,7 +923,15 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
         std::vector<i64> sptr;
         std::vector<i32> scol;
         std::vector<double> sval;
-        pack_sell(Lm[j], lib2mor[j], mor2lib[j], true, sptr, scol, sval, &L.L_lib);
+        std::vector<i32> slw;
+        std::vector<uint8_t> nlow;
+        bool coloured = L.ncol > 0 && j + 1 < p;
+        pack_sell(Lm[j], lib2mor[j], mor2lib[j], true, sptr, scol, sval, &L.L_lib,
+                  coloured ? &L.colour_lib : nullptr, coloured ? &slw : nullptr,
+                  coloured ? &L.lower_per_colour : nullptr, coloured ? &nlow : nullptr);
+        for (i64 r = 0; r < n && coloured; ++r)
+            if (nlow[(size_t)r] == 255) coloured = false;  // (no zero-guess sweeps for such rows)
+        if (coloured && ((s = upload(ctx, &L.slw, slw)) || (s = upload(ctx, &L.nlow, nlow)))) return s;
         L.sell_stored = (i64)sval.size();
         {
             double wavg = (double)L.sell_stored / (double)std::max<i64>(1, (n + 31) / 32 * 32);
@@ -1123,12 +1163,17 @@ double sweep_colour_bytes(const Level& L, i64 rows) {
 // kernel variants by threads-per-row (chosen per level from the SELL width)
 constexpr int CHUNK = 16;
 template <bool P, int TPR>
-void gs_launch_t(bool pdl, int r0, int r1, int span, const Level& L, cudaStream_t st, PfList pf) {
+void gs_launch_t(bool pdl, int r0, int r1, int span, const Level& L, cudaStream_t st, PfList pf, bool zg) {
     // block size: colours too small to give every SM a 256-thread block use smaller blocks
     // (spreads the gathers over more SMs)
     const int bs = L.gs_block;
-    launch(pdl, k_gs_colour<P, TPR, CHUNK>, blocks_for((i64)span * TPR, bs), bs, 0, st, r0, r1, L.uniform_w, L.sptr, L.scol,
-           L.sval, L.f, L.u, L.c, (int)L.n, pf);
+    if (zg && !P)
+        launch(pdl, k_gs_colour<false, TPR, CHUNK, true>, blocks_for((i64)span * TPR, bs), bs, 0, st, r0, r1,
+               L.uniform_w, L.sptr, L.scol, L.sval, L.f, L.u, L.c, (int)L.n, pf, (const int*)L.slw,
+               (const uint8_t*)L.nlow);
+    else
+        launch(pdl, k_gs_colour<P, TPR, CHUNK>, blocks_for((i64)span * TPR, bs), bs, 0, st, r0, r1, L.uniform_w, L.sptr,
+               L.scol, L.sval, L.f, L.u, L.c, (int)L.n, pf, (const int*)nullptr, (const uint8_t*)nullptr);
 }
 // Threads one wave of colour kernels can hold (all SMs, register-limited occupancy).
 static i64 gs_wave_threads(int tpr, int block) {
@@ -1151,22 +1196,22 @@ static i64 gs_wave_threads(int tpr, int block) {
 }
 
 void launch_gs(bool pdl, bool poisson, int tpr, int r0, int r1, int span, const Level& L, cudaStream_t st,
-               PfList pf = {}) {
+               PfList pf = {}, bool zg = false) {
     // a colour slightly larger than one wave would run a nearly empty second wave (ncu:
     // "1.04 waves" on the largest level-0 colours): halve the threads per row instead
     while (tpr > 1 && (i64)span * tpr > gs_wave_threads(tpr, L.gs_block) &&
            (i64)span * (tpr / 2) <= gs_wave_threads(tpr / 2, L.gs_block))
         tpr /= 2;
     if (poisson) {
-        if (tpr == 1) gs_launch_t<true, 1>(pdl, r0, r1, span, L, st, pf);
-        else if (tpr == 2) gs_launch_t<true, 2>(pdl, r0, r1, span, L, st, pf);
-        else if (tpr == 4) gs_launch_t<true, 4>(pdl, r0, r1, span, L, st, pf);
-        else gs_launch_t<true, 8>(pdl, r0, r1, span, L, st, pf);
+        if (tpr == 1) gs_launch_t<true, 1>(pdl, r0, r1, span, L, st, pf, zg);
+        else if (tpr == 2) gs_launch_t<true, 2>(pdl, r0, r1, span, L, st, pf, zg);
+        else if (tpr == 4) gs_launch_t<true, 4>(pdl, r0, r1, span, L, st, pf, zg);
+        else gs_launch_t<true, 8>(pdl, r0, r1, span, L, st, pf, zg);
     } else {
-        if (tpr == 1) gs_launch_t<false, 1>(pdl, r0, r1, span, L, st, pf);
-        else if (tpr == 2) gs_launch_t<false, 2>(pdl, r0, r1, span, L, st, pf);
-        else if (tpr == 4) gs_launch_t<false, 4>(pdl, r0, r1, span, L, st, pf);
-        else gs_launch_t<false, 8>(pdl, r0, r1, span, L, st, pf);
+        if (tpr == 1) gs_launch_t<false, 1>(pdl, r0, r1, span, L, st, pf, zg);
+        else if (tpr == 2) gs_launch_t<false, 2>(pdl, r0, r1, span, L, st, pf, zg);
+        else if (tpr == 4) gs_launch_t<false, 4>(pdl, r0, r1, span, L, st, pf, zg);
+        else gs_launch_t<false, 8>(pdl, r0, r1, span, L, st, pf, zg);
     }
 }
 template <int MODE, bool P, int TPR>
@@ -1294,9 +1339,11 @@ static PfList pf_take(mgm_ctx* ctx, const Regions& regs, bool issuer = true, i64
 }
 
 bool timing_on(const mgm_ctx* ctx);
-void enqueue_sweep(mgm_ctx* ctx, int j, bool backward, cudaStream_t st) {
+// zg: first forward sweep from a zero guess (k_gs_colour ZG; shifted problems only)
+void enqueue_sweep(mgm_ctx* ctx, int j, bool backward, cudaStream_t st, bool zg = false) {
     Level& L = ctx->lv[j];
-    if (L.swB > 0 && !timing_on(ctx)) {  // one persistent kernel for the whole sweep
+    zg = zg && !backward && !ctx->poisson && L.slw;
+    if (L.swB > 0 && !timing_on(ctx) && !zg) {  // one persistent kernel for the whole sweep
         SweepParams P{};
         P.n = (int)L.n;
         P.ncol = L.ncol;
@@ -1314,7 +1361,8 @@ void enqueue_sweep(mgm_ctx* ctx, int j, bool backward, cudaStream_t st) {
     }
     // timing class 0: CUDA events around the whole level-0 sweep (the colour kernels keep
     // their PDL overlap inside it); launches and algorithmic bytes are summed over colours
-    if (j == 0) timer_begin(ctx, 0, st);
+    const int tcls = zg ? 3 : 0;  // zero-guess level-0 sweeps are their own timing class
+    if (j == 0) timer_begin(ctx, tcls, st);
     double bytes = 0.0;
     int nl = 0;
     for (int q = 0; q < L.ncol; ++q) {
@@ -1323,7 +1371,7 @@ void enqueue_sweep(mgm_ctx* ctx, int j, bool backward, cudaStream_t st) {
         if (c1 <= c0) continue;
         for_my_pieces(ctx, j, c0, c1, [&](i64 a, i64 b) {
             if (b <= a) return;
-            if (L.pipe_ctas > 0 && !ctx->poisson && b - a >= (i64)L.pipe_ctas * 128) {
+            if (L.pipe_ctas > 0 && !ctx->poisson && !zg && b - a >= (i64)L.pipe_ctas * 128) {
                 // large colour: streamed kernel, one CTA per SM (k_gs_colour_pipe)
                 const int rpc = (int)((b - a + L.pipe_ctas - 1) / L.pipe_ctas);
                 launch(ctx->pdl, k_gs_colour_pipe<2, CHUNK>, (unsigned)((b - a + rpc - 1) / rpc), 256, 0, st, (int)a,
@@ -1336,15 +1384,17 @@ void enqueue_sweep(mgm_ctx* ctx, int j, bool backward, cudaStream_t st) {
                     if (!ctx->pf_nof) rg.push_back(pf_region(L.f + a, 8 * (b - a)));
                 }
                 const PfList pf = pf_take(ctx, rg, !ctx->pf_l0only || j == 0);
-                launch_gs(ctx->pdl, ctx->poisson, L.tpr, (int)a, (int)b, (int)(b - (a & ~31)), L, st, pf);
+                launch_gs(ctx->pdl, ctx->poisson, L.tpr, (int)a, (int)b, (int)(b - (a & ~31)), L, st, pf, zg);
             }
-            bytes += sweep_colour_bytes(L, b - a);
+            // algorithmic bytes; a zero-guess sweep reads its stored entries and f, writes u
+            bytes += zg ? (12.0 * (double)L.lower_per_colour[c] * (double)(b - a) / (double)(c1 - c0) + 16.0 * (double)(b - a))
+                        : sweep_colour_bytes(L, b - a);
             ++nl;
             ctx->vcycle_kernels++;
         });
         dist_exchange(ctx, j, L.u, c0, c1, st);
     }
-    if (j == 0) timer_end(ctx, 0, st, bytes, nl);
+    if (j == 0) timer_end(ctx, tcls, st, bytes, nl);
 }
 
 // Poisson border row: y[n] = fs*f[n] + sign * (c . x)
@@ -1471,15 +1521,20 @@ void enqueue_vcycle(mgm_ctx* ctx, cudaStream_t st) {
     stamp(ctx, "start", 0, st);
     const bool bottom_only = std::getenv("MGM_DEBUG_BOTTOM_ONLY") && ctx->botJ > 0;  // timing experiment only
     if (!bottom_only) {
-    for (int s = 0; s < nu1; ++s) enqueue_sweep(ctx, 0, pre_b, st);      // line 4
+    // level 0 from a zero guess (preconditioner applications): the first sweep reads only
+    // the diagonal and earlier-colour entries (k_gs_colour ZG)
+    for (int s = 0; s < nu1; ++s) enqueue_sweep(ctx, 0, pre_b, st, s == 0 && ctx->vc_zero_guess);  // line 4
     stamp(ctx, "presmooth", 0, st);
     enqueue_residual(ctx, 0, lv[0].f, lv[0].u, lv[0].t, st);              // line 5
     stamp(ctx, "residual", 0, st);
     enqueue_restrict(ctx, 0, lv[0].t, lv[1].f, st);
     stamp(ctx, "restrict", 0, st);
     for (int j = 1; j < D; ++j) {                                         // lines 6-9
-        enqueue_zero(ctx, lv[j].u, lv[j].n + pad, st);
-        for (int s = 0; s < nu1; ++s) enqueue_sweep(ctx, j, pre_b, st);
+        // e_j = 0 then presmooth; the first forward sweep from the zero guess writes every row
+        // and reads only earlier-colour values, so the zero fill is not needed
+        const bool zg = nu1 >= 1 && !pre_b && !ctx->poisson && lv[j].slw && !ctx->no_zg;
+        if (!zg) enqueue_zero(ctx, lv[j].u, lv[j].n + pad, st);
+        for (int s = 0; s < nu1; ++s) enqueue_sweep(ctx, j, pre_b, st, s == 0 && zg);
         stamp(ctx, "zero+presmooth", j, st);
         enqueue_residual(ctx, j, lv[j].f, lv[j].u, lv[j].t, st);
         enqueue_restrict(ctx, j, lv[j].t, lv[j + 1].f, st);
@@ -1524,8 +1579,9 @@ void enqueue_vcycle(mgm_ctx* ctx, cudaStream_t st) {
     stamp(ctx, "postsmooth", 0, st);
 }
 
-bool timing_on(const mgm_ctx* ctx) { return ctx->timer[0].on || ctx->timer[1].on; }
+bool timing_on(const mgm_ctx* ctx) { return ctx->timer[0].on || ctx->timer[1].on || ctx->timer[3].on; }
 
+bool zg_capable(const mgm_ctx* ctx);
 // Record the V-cycle schedule's prefetch targets with a dry enqueue pass and upload the
 // region table (a new table only when the schedule changed: captured graphs keep theirs).
 mgm_status pf_prepare(mgm_ctx* ctx, cudaStream_t st) {
@@ -1561,8 +1617,11 @@ mgm_status pf_prepare(mgm_ctx* ctx, cudaStream_t st) {
     return MGM_OK;
 }
 
-mgm_status build_graph(mgm_ctx* ctx) {
-    if (ctx->vgraph) return MGM_OK;
+mgm_status build_graph(mgm_ctx* ctx, bool zero_guess = false) {
+    cudaGraphExec_t& gx = zero_guess ? ctx->vgraph0 : ctx->vgraph;
+    if (gx) return MGM_OK;
+    ctx->vc_zero_guess = zero_guess && zg_capable(ctx);
+    struct ResetZ { mgm_ctx* c; ~ResetZ() { c->vc_zero_guess = false; } } resetz_{ctx};
     cudaGraph_t g;
     {
         mgm_status ps = pf_prepare(ctx, ctx->st);
@@ -1580,26 +1639,35 @@ mgm_status build_graph(mgm_ctx* ctx) {
         cudaGetLastError();
         return MGM_ERR_CUDA;
     }
-    CK(cudaGraphInstantiate(&ctx->vgraph, g, 0));
+    CK(cudaGraphInstantiate(&gx, g, 0));
     cudaGraphDestroy(g);
     return MGM_OK;
 }
 
 // run one V-cycle on lv[0].f / lv[0].u
-mgm_status run_vcycle(mgm_ctx* ctx, cudaStream_t st) {
+// zero_guess: lv[0].u holds no guess (Krylov preconditioner): the level-0 presmooth starts
+// from 0 without reading u (see zg_capable)
+bool zg_capable(const mgm_ctx* ctx) {
+    return !ctx->no_zg && !ctx->poisson && ctx->lp.nu1 >= 1 && ctx->lp.smoother != 1 && ctx->p > 1 && ctx->lv[0].slw;
+}
+mgm_status run_vcycle(mgm_ctx* ctx, cudaStream_t st, bool zero_guess = false) {
+    zero_guess = zero_guess && zg_capable(ctx);
     if (timing_on(ctx)) {
+        ctx->vc_zero_guess = zero_guess;
         mgm_status ps = pf_prepare(ctx, st);
-        if (ps) return ps;
+        if (ps) { ctx->vc_zero_guess = false; return ps; }
+        ctx->vc_zero_guess = zero_guess;
         timer_begin(ctx, 2, st);
         enqueue_vcycle(ctx, st);
         ctx->pf_mode = 0;
+        ctx->vc_zero_guess = false;
         timer_end(ctx, 2, st, 0.0);
         return MGM_OK;
     }
-    mgm_status s = build_graph(ctx);
+    mgm_status s = build_graph(ctx, zero_guess);
     if (s) return s;
     timer_begin(ctx, 2, st);
-    CK(cudaGraphLaunch(ctx->vgraph, st));
+    CK(cudaGraphLaunch(zero_guess ? ctx->vgraph0 : ctx->vgraph, st));
     timer_end(ctx, 2, st, 0.0);
     return MGM_OK;
 }
@@ -1647,8 +1715,8 @@ void enqueue_apply_A(mgm_ctx* ctx, const double* x, double* y, cudaStream_t st) 
 mgm_status enqueue_precond(mgm_ctx* ctx, const double* v, cudaStream_t st) {
     i64 n = ctx->N + (ctx->poisson ? 1 : 0);
     CK(cudaMemcpyAsync(ctx->lv[0].f, v, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
-    CK(cudaMemsetAsync(ctx->lv[0].u, 0, sizeof(double) * n, st));
-    return run_vcycle(ctx, st);
+    if (!zg_capable(ctx)) CK(cudaMemsetAsync(ctx->lv[0].u, 0, sizeof(double) * n, st));
+    return run_vcycle(ctx, st, true);  // M v from the zero guess
 }
 
 // Right-preconditioned GMRES(restart) with CGS2 orthogonalisation (equal to MGS in exact
@@ -2107,6 +2175,7 @@ mgm_status mgm_setup(const double* points, const double* normals, int64_t n_poin
     if (const char* e = std::getenv("MGM_DIST_FAKE_RANKS")) ctx->fake_ranks = ctx->poisson ? 0 : std::max(0, std::atoi(e));
     if (const char* e = std::getenv("MGM_PF_DIST")) ctx->pf_dist = std::max(0, std::atoi(e));
     if (const char* e = std::getenv("MGM_PF_CAP_MB")) ctx->pf_cap = (i64)std::max(0, std::atoi(e)) << 20;
+    if (std::getenv("MGM_NO_ZG")) ctx->no_zg = true;
     if (std::getenv("MGM_PF_LATE")) ctx->pf_late = 1;
     if (std::getenv("MGM_PF_NOF")) ctx->pf_nof = 1;
     if (std::getenv("MGM_PF_L0ONLY")) ctx->pf_l0only = 1;
@@ -2261,10 +2330,11 @@ mgm_status mgm_dist_attach(mgm_ctx* ctx, int rank, int nranks, const void* id128
     ctx->comm = comm;
     ctx->rank = rank;
     ctx->nranks = nranks;
-    if (ctx->vgraph) {  // re-capture with the exchanges
-        cudaGraphExecDestroy(ctx->vgraph);
-        ctx->vgraph = nullptr;
-    }
+    for (cudaGraphExec_t* gx : {&ctx->vgraph, &ctx->vgraph0})  // re-capture with the exchanges
+        if (*gx) {
+            cudaGraphExecDestroy(*gx);
+            *gx = nullptr;
+        }
     return MGM_OK;
 }
 
@@ -2274,7 +2344,8 @@ mgm_status mgm_destroy(mgm_ctx* ctx) {
     if (ctx->st) cudaStreamSynchronize(ctx->st);
     for (auto& L : ctx->lv) {
         for (void* ptr : {(void*)L.sptr, (void*)L.scol, (void*)L.sval, (void*)L.pcol, (void*)L.pval, (void*)L.rptr,
-                          (void*)L.rcol, (void*)L.rval, (void*)L.u, (void*)L.f, (void*)L.t, (void*)L.c})
+                          (void*)L.rcol, (void*)L.rval, (void*)L.u, (void*)L.f, (void*)L.t, (void*)L.c, (void*)L.slw,
+                          (void*)L.nlow})
             if (ptr) cudaFree(ptr);
     }
     for (void* ptr : {(void*)ctx->lu, (void*)ctx->piv, (void*)ctx->d_lib2orig, (void*)ctx->V, (void*)ctx->w,
@@ -2286,6 +2357,7 @@ mgm_status mgm_destroy(mgm_ctx* ctx) {
     for (void* q : ctx->pf_old) cudaFree(q);
     if (ctx->d_trace) cudaFree(ctx->d_trace);
     if (ctx->vgraph) cudaGraphExecDestroy(ctx->vgraph);
+    if (ctx->vgraph0) cudaGraphExecDestroy(ctx->vgraph0);
     if (ctx->comm) nccl().CommDestroy(ctx->comm);
     for (auto* q : {&ctx->bu, &ctx->bf, &ctx->bt})
         for (double* ptr : *q) cudaFree(ptr);
@@ -2484,7 +2556,7 @@ mgm_status mgm_apply(mgm_ctx* ctx, int level, int op, const double* x, const dou
 }
 
 mgm_status mgm_timing_enable(mgm_ctx* ctx, int cls, int enable) {
-    if (!ctx || cls < 0 || cls > 2) return MGM_ERR_ARG;
+    if (!ctx || cls < 0 || cls > 3) return MGM_ERR_ARG;
     KernelTimer& T = ctx->timer[cls];
     T.on = enable != 0;
     T.used = 0;
@@ -2495,7 +2567,7 @@ mgm_status mgm_timing_enable(mgm_ctx* ctx, int cls, int enable) {
 }
 
 mgm_status mgm_timing_read(mgm_ctx* ctx, int cls, double* total_ms, int64_t* launches, double* alg_bytes) {
-    if (!ctx || cls < 0 || cls > 2) return MGM_ERR_ARG;
+    if (!ctx || cls < 0 || cls > 3) return MGM_ERR_ARG;
     timer_collect(ctx);
     const KernelTimer& T = ctx->timer[cls];
     if (total_ms) *total_ms = T.total_ms;
@@ -2514,6 +2586,11 @@ mgm_status mgm_bytes_model(const mgm_ctx* ctx, double* vcycle_bytes, double* spm
         const Level& L = ctx->lv[j];
         const double n = (double)L.n, z = (double)L.nnz, q = (double)L.p_nnz, nn = (double)ctx->lv[j + 1].n;
         B += nu * (12.0 * z + 24.0 * n + bp * n);                   // sweeps
+        if (j >= 1 && zg_capable(ctx)) {  // the first presmooth from e_j = 0 reads diag + earlier colours only
+            double low = 0.0;
+            for (i64 v : L.lower_per_colour) low += (double)v;
+            B -= (12.0 * z + 24.0 * n) - (12.0 * low + 16.0 * n);
+        }
         B += 12.0 * z + 16.0 * n + 12.0 * q + 8.0 * nn + 16.0 * n + bp * n;  // residual + restrict (unfused)
         B += 12.0 * q + 8.0 * nn + 16.0 * n;                        // interp + correct
     }
@@ -2521,6 +2598,14 @@ mgm_status mgm_bytes_model(const mgm_ctx* ctx, double* vcycle_bytes, double* spm
     B += 8.0 * np * np + 16.0 * np;
     if (vcycle_bytes) *vcycle_bytes = B;
     if (spmv_bytes) *spmv_bytes = 12.0 * ctx->lv[0].nnz + 16.0 * ctx->lv[0].n;
+    return MGM_OK;
+}
+
+mgm_status mgm_level_zg_nnz(const mgm_ctx* ctx, int level, int64_t* nnz_zg) {
+    if (!ctx || level < 0 || level >= ctx->p || !nnz_zg) return MGM_ERR_ARG;
+    i64 s = 0;
+    for (i64 v : ctx->lv[level].lower_per_colour) s += v;
+    *nnz_zg = zg_capable(ctx) ? s : ctx->lv[level].nnz;
     return MGM_OK;
 }
 

@@ -103,12 +103,19 @@ __device__ __forceinline__ double group_sum(double v) {
 // One colour of a Gauss-Seidel sweep (Poisson variant P:348-352):
 //   u_i += (f_i - sum_j a_ij u_j [- c_i lambda]) / a_ii  over rows [r0, r1) of one colour.
 // TPR threads per row; threads aligned to 32-row slices.
-template <bool POISSON, int TPR, int CH>
+// ZG (first forward sweep from a zero guess, shifted problems): the later-colour values are
+// still 0, so only the first slw[slice] slots of each row (diagonal + earlier-colour
+// columns, pack_sell's order) are read and u_i (= 0) is not: u_i = (f_i - sum_lower) / a_ii,
+// with the row's own earlier-colour count nlow[r] masking the slots a longer row of the same
+// slice needs (they hold this row's later-colour entries).  Skipping the zero products
+// leaves the remaining terms' order unchanged.
+template <bool POISSON, int TPR, int CH, bool ZG = false>
 __global__ void __launch_bounds__(256) k_gs_colour(int r0, int r1, int Wu, const int64_t* __restrict__ sptr,
                                                    const int* __restrict__ scol,
                                                    const double* __restrict__ sval,
                                                    const double* __restrict__ f, double* u,
-                                                   const double* __restrict__ c, int n, PfList pf) {
+                                                   const double* __restrict__ c, int n, PfList pf,
+                                                   const int* __restrict__ slw, const uint8_t* __restrict__ nlow) {
     pdl_trigger();
     if (!pf.late) l2_prefetch_share(pf);
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
@@ -128,7 +135,18 @@ __global__ void __launch_bounds__(256) k_gs_colour(int r0, int r1, int Wu, const
             w = (int)((sptr[(r >> 5) + 1] - s0) >> 5);
             base = s0 + (r & 31);
         }
+        int lim = 0;
+        if (ZG) {
+            w = slw[r >> 5];
+            lim = 1 + (int)nlow[r];
+        }
         fr.load(sval + base, scol + base, w, part);
+        if (ZG) {
+#pragma unroll
+            for (int q = 0; q < CH; ++q)  // the diagonal (u_i not yet written, term 0) and later colours
+                if (part + q * TPR == 0 || part + q * TPR >= lim) fr.c[q] = -1;
+            w = lim;  // (the tail loop below)
+        }
         d = ld_stream_f64(sval + base);
     } else {
         fr.load(sval, scol, 0, 0);
@@ -139,7 +157,7 @@ __global__ void __launch_bounds__(256) k_gs_colour(int r0, int r1, int Wu, const
     double fr_v = 0.0, ur = 0.0, cl = 0.0;
     if (live && part == 0) {
         fr_v = f[r];
-        ur = u[r];
+        if (!ZG) ur = u[r];
         if (POISSON) cl = c[r] * u[n];
     }
     double acc = fr.dot(u, 0.0);
