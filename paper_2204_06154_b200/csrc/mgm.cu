@@ -210,6 +210,13 @@ struct mgm_ctx {
     double* partials = nullptr;
     unsigned* tickets = nullptr;  // last-block counters of the fused reductions (reset by the finisher)
     double* dh = nullptr;    // device scratch: h1[128], h2[128], nrm2, misc
+    // device-side GMRES (gmres_dev): Arnoldi loop as a CUDA-graph WHILE node
+    cudaGraphExec_t ggraph = nullptr;
+    int* g_i = nullptr;       // {k, its, stop, maxit}
+    double* g_d = nullptr;    // {bnorm, tol, H, cs, sn, g, hist}
+    double* g_h = nullptr;    // pinned mirror of g_d
+    int* g_hi = nullptr;      // pinned mirror of g_i
+    int g_hist_cap = 4096;
     double* hh = nullptr;    // pinned host mirror
     // timing
     KernelTimer timer[4];
@@ -1844,6 +1851,180 @@ mgm_status gmres_lib(mgm_ctx* ctx, double tol, int maxit, mgm_report* rep, cudaS
     return MGM_OK;
 }
 
+// ---------------------------------------------------------------------------------------
+// Device-side GMRES: the Arnoldi steps of a restart cycle run as ONE graph launch, a WHILE
+// conditional node whose body is [V_k -> f_0, V-cycle from the zero guess, SpMV, CGS2 (5
+// kernels), V_{k+1} = w/||w||, Givens step] and whose condition the Givens kernel sets on the
+// device (solve_kernels.cuh k_gmres_givens).  The host synchronises once per restart cycle
+// instead of once per iteration.  Same arithmetic as gmres_lib (which remains the path for
+// Poisson problems, multi-GPU, kernel timing, restart > 128 and MGM_HOST_GMRES).
+// ---------------------------------------------------------------------------------------
+static size_t gmres_dev_doubles(const mgm_ctx* ctx) {
+    const size_t m = (size_t)ctx->restart;
+    return 2 + (m + 1) * m + 2 * m + (m + 1) + (size_t)ctx->g_hist_cap;
+}
+static bool gmres_dev_ok(const mgm_ctx* ctx) {
+    return !ctx->poisson && !ctx->comm && !timing_on(ctx) && ctx->restart <= 128 && ctx->p >= 1 &&
+           std::getenv("MGM_HOST_GMRES") == nullptr;
+}
+static mgm_status build_gmres_graph(mgm_ctx* ctx) {
+    if (ctx->ggraph) return MGM_OK;
+    const i64 n = ctx->N;
+    const int m = ctx->restart;
+    const i64 ld = ctx->ld;
+    cudaStream_t st = ctx->st;
+    if (!ctx->g_i) {
+        CK(dalloc(&ctx->g_i, 8));
+        CK(dalloc(&ctx->g_d, (i64)gmres_dev_doubles(ctx)));
+        CK(cudaMallocHost((void**)&ctx->g_h, sizeof(double) * gmres_dev_doubles(ctx)));
+        CK(cudaMallocHost((void**)&ctx->g_hi, sizeof(int) * 8));
+    }
+    GmresDev G{ctx->g_i, ctx->g_d, m, ctx->g_hist_cap};
+    double* V = ctx->V;
+    double* w = ctx->w;
+    double* h1 = ctx->dh;
+    double* h2 = ctx->dh + 256;
+    double* nr = ctx->dh + 512;
+    const int* kdev = ctx->g_i;
+    cudaGraph_t g;
+    CK(cudaGraphCreate(&g, 0));
+    struct GDel { cudaGraph_t g; ~GDel() { cudaGraphDestroy(g); } } gdel_{g};
+    cudaGraphConditionalHandle cond;
+    CK(cudaGraphConditionalHandleCreate(&cond, g, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = cond;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t cn;
+    CK(cudaGraphAddNode(&cn, g, nullptr, 0, &cp));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    CK(cudaStreamBeginCaptureToGraph(st, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    g_launch_err.clear();
+    k_copy_col<<<RED_BLOCKS, 256, 0, st>>>(n, V, ld, kdev, ctx->lv[0].f);  // f_0 = V_k
+    const bool zg = zg_capable(ctx);
+    if (!zg) cudaMemsetAsync(ctx->lv[0].u, 0, sizeof(double) * n, st);
+    ctx->vc_zero_guess = zg;
+    enqueue_vcycle(ctx, st);                                              // u = M V_k
+    ctx->vc_zero_guess = false;
+    enqueue_apply_A(ctx, ctx->lv[0].u, w, st);                            // w = A M V_k
+    // CGS2: h1 = V^T w; w -= V h1; h2 = V^T w (h1 += h2); w -= V h2, ||w||^2
+    k_multidot_fin<<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, V, ld, 0, w, ctx->partials, ctx->tickets, h1,
+                                                       (double*)nullptr, kdev);
+    k_multiaxpy<<<RED_BLOCKS * 2, 256, 0, st>>>(n, V, ld, 0, h1, w, kdev);
+    k_multidot_fin<<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, V, ld, 0, w, ctx->partials, ctx->tickets, h2, h1, kdev);
+    k_multiaxpy_norm<<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, V, ld, 0, h2, w, ctx->partials, ctx->tickets, nr, kdev);
+    k_scale_col<<<RED_BLOCKS, 256, 0, st>>>(n, w, nr, V, ld, kdev);         // V_{k+1}
+    k_gmres_givens<<<1, 32, 0, st>>>(G, h1, nr, cond);
+    cudaGraph_t cap = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(st, &cap);
+    if (ce != cudaSuccess || !g_launch_err.empty()) {
+        ctx->err = "GMRES graph capture failed: " + std::string(cudaGetErrorString(ce)) + "; first failed launch: " +
+                   (g_launch_err.empty() ? std::string("none recorded") : g_launch_err);
+        g_launch_err.clear();
+        cudaGetLastError();
+        return MGM_ERR_CUDA;
+    }
+    CK(cudaGraphInstantiate(&ctx->ggraph, g, 0));
+    return MGM_OK;
+}
+
+mgm_status gmres_dev(mgm_ctx* ctx, double tol, int maxit, mgm_report* rep, cudaStream_t st) {
+    const i64 n = ctx->N;
+    const int m = ctx->restart;
+    const i64 ld = ctx->ld;
+    double* V = ctx->V;
+    double* w = ctx->w;
+    double* h1 = ctx->dh;
+    double* nr = ctx->dh + 512;
+    mgm_status s;
+    if ((s = build_gmres_graph(ctx))) return s;
+    CK(cudaMemsetAsync(ctx->xs, 0, sizeof(double) * n, st));
+    enqueue_dot(ctx, n, ctx->b, ctx->b, nr, st);
+    CK(cudaMemcpyAsync(ctx->hh, nr, sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const double bnorm = std::sqrt(ctx->hh[0]);
+    int its = 0, hist_n = 0;
+    bool converged = false;
+    if (bnorm == 0.0) {
+        if (rep) { rep->iterations = 0; rep->converged = 1; rep->final_rel_residual = 0.0; }
+        return MGM_OK;
+    }
+    const size_t nd = gmres_dev_doubles(ctx);
+    double* gh = ctx->g_h;
+    double* Hh = gh + 2;
+    double* gg = Hh + (size_t)(m + 1) * m + 2 * (size_t)m;
+    double* hist = gg + (m + 1);
+    std::vector<double> y(m);
+    bool first = true;
+    while (true) {
+        if (first) {  // r = b - A x ; beta
+            CK(cudaMemcpyAsync(w, ctx->b, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+        } else {
+            enqueue_apply_A(ctx, ctx->xs, w, st);
+            k_axpby<<<RED_BLOCKS, 256, 0, st>>>(n, 1.0, ctx->b, -1.0, w, w);
+        }
+        first = false;
+        enqueue_dot(ctx, n, w, w, nr, st);
+        CK(cudaMemcpyAsync(ctx->hh, nr, sizeof(double), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        const double beta = std::sqrt(ctx->hh[0]);
+        if (beta / bnorm <= tol || its >= maxit) {
+            converged = beta / bnorm <= tol;
+            break;
+        }
+        k_scale_by_invnorm<<<RED_BLOCKS, 256, 0, st>>>(n, w, nr, V);
+        // cycle state: k = 0, its, stop = 0, maxit; bnorm, tol; H = cs = sn = 0; g = beta e_1
+        std::fill(gh, gh + nd - ctx->g_hist_cap, 0.0);
+        gh[0] = bnorm;
+        gh[1] = tol;
+        gg[0] = beta;
+        ctx->g_hi[0] = 0;
+        ctx->g_hi[1] = its;
+        ctx->g_hi[2] = 0;
+        ctx->g_hi[3] = maxit;
+        CK(cudaMemcpyAsync(ctx->g_d, gh, sizeof(double) * (nd - ctx->g_hist_cap), cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(ctx->g_i, ctx->g_hi, sizeof(int) * 4, cudaMemcpyHostToDevice, st));
+        CK(cudaGraphLaunch(ctx->ggraph, st));
+        CK(cudaMemcpyAsync(ctx->g_hi, ctx->g_i, sizeof(int) * 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(gh, ctx->g_d, sizeof(double) * nd, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        const int kdone = ctx->g_hi[0];
+        const int its0 = its;
+        its = ctx->g_hi[1];
+        const int stop = ctx->g_hi[2];
+        for (int q = its0; q < its && q < ctx->g_hist_cap; ++q)
+            if (rep && rep->history && hist_n < rep->history_cap) rep->history[hist_n++] = hist[q];
+        if (stop == 2) return fail(ctx, MGM_ERR_BREAKDOWN, "non-finite GMRES residual", its);
+        for (int i = kdone - 1; i >= 0; --i) {
+            double sacc = gg[i];
+            for (int j2 = i + 1; j2 < kdone; ++j2) sacc -= Hh[(size_t)i * m + j2] * y[j2];
+            y[i] = sacc / Hh[(size_t)i * m + i];
+        }
+        CK(cudaMemcpyAsync(h1, y.data(), sizeof(double) * kdone, cudaMemcpyHostToDevice, st));
+        k_lincomb<<<RED_BLOCKS * 2, 256, 0, st>>>(n, V, ld, kdone, h1, w);
+        if ((s = enqueue_precond(ctx, w, st))) return s;
+        k_axpby<<<RED_BLOCKS, 256, 0, st>>>(n, 1.0, ctx->xs, 1.0, ctx->lv[0].u, ctx->xs);
+        if (stop == 1) {
+            converged = std::fabs(gg[kdone]) / bnorm <= tol;
+            break;
+        }
+    }
+    // true residual
+    enqueue_apply_A(ctx, ctx->xs, w, st);
+    k_axpby<<<RED_BLOCKS, 256, 0, st>>>(n, 1.0, ctx->b, -1.0, w, w);
+    enqueue_dot(ctx, n, w, w, nr, st);
+    CK(cudaMemcpyAsync(ctx->hh, nr, sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (rep) {
+        rep->iterations = its;
+        rep->converged = converged ? 1 : 0;
+        rep->final_rel_residual = std::sqrt(ctx->hh[0]) / bnorm;
+        rep->lambda = 0.0;
+    }
+    return MGM_OK;
+}
+
 // Right-preconditioned BiCGSTAB (oracle.bicgstab, O18): Saad's
 // Alg. 7.7 on A M with x = M z; two V-cycles (preconditioner applications, counted as the
 // iterations) and two SpMVs per step; the relative residual after each half step.  b, x
@@ -2330,7 +2511,7 @@ mgm_status mgm_dist_attach(mgm_ctx* ctx, int rank, int nranks, const void* id128
     ctx->comm = comm;
     ctx->rank = rank;
     ctx->nranks = nranks;
-    for (cudaGraphExec_t* gx : {&ctx->vgraph, &ctx->vgraph0})  // re-capture with the exchanges
+    for (cudaGraphExec_t* gx : {&ctx->vgraph, &ctx->vgraph0, &ctx->ggraph})  // re-capture with the exchanges
         if (*gx) {
             cudaGraphExecDestroy(*gx);
             *gx = nullptr;
@@ -2352,6 +2533,11 @@ mgm_status mgm_destroy(mgm_ctx* ctx) {
                       (void*)ctx->xs, (void*)ctx->b, (void*)ctx->partials, (void*)ctx->dh, (void*)ctx->tickets})
         if (ptr) cudaFree(ptr);
     if (ctx->hh) cudaFreeHost(ctx->hh);
+    if (ctx->ggraph) cudaGraphExecDestroy(ctx->ggraph);
+    if (ctx->g_i) cudaFree(ctx->g_i);
+    if (ctx->g_d) cudaFree(ctx->g_d);
+    if (ctx->g_h) cudaFreeHost(ctx->g_h);
+    if (ctx->g_hi) cudaFreeHost(ctx->g_hi);
     for (void* q : ctx->bot_mem) cudaFree(q);
     if (ctx->d_pf) cudaFree(ctx->d_pf);
     for (void* q : ctx->pf_old) cudaFree(q);
@@ -2423,7 +2609,7 @@ static mgm_status solve_impl(mgm_ctx* ctx, const double* rhs, double* x, bool ho
     }
     k_gather<<<blocks_for(N, 256), 256, 0, st>>>((int)N, ctx->d_lib2orig, rhs_dev, ctx->b);
     if (ctx->poisson) CK(cudaMemsetAsync(ctx->b + N, 0, sizeof(double), st));
-    s = krylov == 1 ? gmres_lib(ctx, tol, maxit, rep, st)
+    s = krylov == 1 ? (gmres_dev_ok(ctx) ? gmres_dev(ctx, tol, maxit, rep, st) : gmres_lib(ctx, tol, maxit, rep, st))
         : krylov == 2 ? bicgstab_lib(ctx, tol, maxit, rep, st)
                       : standalone_lib(ctx, tol, maxit, rep, st);
     if (s) return s;

@@ -478,7 +478,8 @@ __device__ __forceinline__ void finish_partials(const double* partials, int k1, 
 __global__ void __launch_bounds__(RED_THREADS) k_multidot_fin(int64_t n, const double* __restrict__ V, int64_t ld,
                                                               int k1, const double* __restrict__ w,
                                                               double* __restrict__ partials, unsigned* ticket,
-                                                              double* out, double* acc) {
+                                                              double* out, double* acc, const int* kdev = nullptr) {
+    if (kdev) k1 = *kdev + 1;  // device-side GMRES: the Arnoldi step lives in device memory
     __shared__ double red[RED_THREADS / 32][MD_GROUP];
     const int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
     const int64_t b0 = blockIdx.x * chunk, b1 = min(n, b0 + chunk);
@@ -514,7 +515,8 @@ __global__ void __launch_bounds__(RED_THREADS) k_multidot_fin(int64_t n, const d
 __global__ void __launch_bounds__(RED_THREADS) k_multiaxpy_norm(int64_t n, const double* __restrict__ V, int64_t ld,
                                                                 int k1, const double* __restrict__ h,
                                                                 double* __restrict__ w, double* __restrict__ partials,
-                                                                unsigned* ticket, double* nrm2) {
+                                                                unsigned* ticket, double* nrm2, const int* kdev = nullptr) {
+    if (kdev) k1 = *kdev + 1;
     __shared__ double hs[256];
     __shared__ double red[RED_THREADS / 32];
     for (int j = threadIdx.x; j < k1; j += blockDim.x) hs[j] = h[j];
@@ -552,7 +554,8 @@ __global__ void k_reduce_partials(const double* __restrict__ partials, int nblk,
 // w[i] -= sum_j V_j[i] * h[j]
 __global__ void __launch_bounds__(256) k_multiaxpy(int64_t n, const double* __restrict__ V,
                                                    int64_t ld, int k1, const double* __restrict__ h,
-                                                   double* __restrict__ w) {
+                                                   double* __restrict__ w, const int* kdev = nullptr) {
+    if (kdev) k1 = *kdev + 1;
     __shared__ double hs[256];
     for (int j = threadIdx.x; j < k1; j += blockDim.x) hs[j] = h[j];
     __syncthreads();
@@ -577,6 +580,76 @@ __global__ void __launch_bounds__(256) k_lincomb(int64_t n, const double* __rest
         for (int j = 0; j < k1; ++j) acc += V[(int64_t)j * ld + i] * hs[j];
         y[i] = acc;
     }
+}
+
+// Device-side GMRES (mgm.cu gmres_dev): one CUDA graph per restart cycle whose WHILE node
+// runs Arnoldi steps until the device Givens kernel clears the condition.  State:
+// gi = {k, its, stop, maxit}; gd = {bnorm, tol, H[(m+1) x m] row-major, cs[m], sn[m],
+// g[m+1], hist[...]}.
+struct GmresDev {
+    int* gi;
+    double* gd;
+    int m;
+    int hist_cap;
+};
+__device__ __forceinline__ double* gmd_H(const GmresDev& G) { return G.gd + 2; }
+__device__ __forceinline__ double* gmd_cs(const GmresDev& G) { return G.gd + 2 + (G.m + 1) * G.m; }
+__device__ __forceinline__ double* gmd_sn(const GmresDev& G) { return gmd_cs(G) + G.m; }
+__device__ __forceinline__ double* gmd_g(const GmresDev& G) { return gmd_sn(G) + G.m; }
+__device__ __forceinline__ double* gmd_hist(const GmresDev& G) { return gmd_g(G) + G.m + 1; }
+
+// dst = V_k (k = gi[0]): the Arnoldi vector to precondition
+__global__ void k_copy_col(int64_t n, const double* __restrict__ V, int64_t ld, const int* __restrict__ kdev,
+                           double* __restrict__ dst) {
+    const double* src = V + (int64_t)(*kdev) * ld;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = src[i];
+}
+// V_{k+1} = w / sqrt(*nrm2)
+__global__ void k_scale_col(int64_t n, const double* __restrict__ w, const double* __restrict__ nrm2, double* V,
+                            int64_t ld, const int* __restrict__ kdev) {
+    const double inv = 1.0 / sqrt(*nrm2);
+    double* dst = V + (int64_t)(*kdev + 1) * ld;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = w[i] * inv;
+}
+// One Givens step of the Hessenberg least-squares problem (same operations as gmres_lib's
+// host loop), the relative residual history, and the loop condition.
+__global__ void k_gmres_givens(GmresDev G, const double* __restrict__ h, const double* __restrict__ nrm2,
+                               cudaGraphConditionalHandle cond) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const int m = G.m;
+    const int k = G.gi[0], k1 = k + 1;
+    double* H = gmd_H(G);
+    double* cs = gmd_cs(G);
+    double* sn = gmd_sn(G);
+    double* g = gmd_g(G);
+    for (int i = 0; i < k1; ++i) H[i * m + k] = h[i];
+    const double hk1 = sqrt(*nrm2);
+    H[k1 * m + k] = hk1;
+    for (int i = 0; i < k; ++i) {
+        const double t = cs[i] * H[i * m + k] + sn[i] * H[(i + 1) * m + k];
+        H[(i + 1) * m + k] = -sn[i] * H[i * m + k] + cs[i] * H[(i + 1) * m + k];
+        H[i * m + k] = t;
+    }
+    const double den = hypot(H[k * m + k], hk1);
+    cs[k] = H[k * m + k] / den;
+    sn[k] = hk1 / den;
+    H[k * m + k] = den;
+    H[k1 * m + k] = 0.0;
+    g[k1] = -sn[k] * g[k];
+    g[k] = cs[k] * g[k];
+    const double rel = fabs(g[k1]) / G.gd[0];
+    const int its = G.gi[1] + 1;
+    if (its - 1 < G.hist_cap) gmd_hist(G)[its - 1] = rel;
+    int stop = 0;  // 1: converged / maxit / happy breakdown, 2: non-finite, 3: restart
+    if (!isfinite(rel)) stop = 2;
+    else if (rel <= G.gd[1] || its >= G.gi[3] || hk1 == 0.0) stop = 1;
+    else if (k1 == m) stop = 3;
+    G.gi[0] = k1;
+    G.gi[1] = its;
+    G.gi[2] = stop;
+    cudaGraphSetConditional(cond, stop == 0 ? 1u : 0u);
 }
 
 // dst = src / sqrt(*nrm2)
