@@ -278,10 +278,11 @@ COLOUR_PASSES = 10   # O11: iterated-greedy passes after the first greedy pass
 
 
 def greedy_colour(A: CSR, passes: int = COLOUR_PASSES):
-    """O11 colouring of sym(pattern(A)) minus diagonal: greedy with vertices in index (Morton)
-    order, then ``passes`` iterated-greedy passes (vertices by descending previous colour,
-    ties by index; each gives the smallest colour unused by neighbours coloured earlier in
-    the pass)."""
+    """O11 colouring of sym(pattern(A)) minus diagonal: DSATUR (largest saturation first, ties
+    by larger degree then lower index; smallest free colour), then ``passes`` iterated-greedy
+    passes (vertices by descending previous colour, ties by index; each gives the smallest
+    colour unused by neighbours coloured earlier in the pass).  ``passes < 0``: plain greedy
+    in index (Morton) order."""
     T = A.transpose()
     col = np.empty(A.shape[0], dtype=np.int32)
     nc = ctypes.c_int32(0)

@@ -635,9 +635,79 @@ static int greedy_pass(i64 n, const i64* ap, const i64* ai, const i64* tp, const
     return 0;
 }
 
-/* O11: greedy colouring in index (Morton) order, then `passes` iterated-greedy passes
- * (Culberson): each visits the vertices by descending colour of the previous pass, ties by
- * index; a pass never increases the number of colours. */
+/* DSATUR (Brelaz 1979), O11: repeatedly colour the uncoloured vertex of largest saturation
+ * (number of distinct colours among its neighbours in sym(pattern) minus the diagonal), ties
+ * by larger degree (distinct neighbours), then lower index, with the smallest colour unused
+ * by its neighbours.  Returns -2 if a colour index reaches 256 (caller falls back). */
+typedef struct { int32_t sat, deg; i64 v; } ds_ent;
+static int cmp_i64(const void* a, const void* b) {
+    i64 x = *(const i64*)a, y = *(const i64*)b;
+    return (x > y) - (x < y);
+}
+static int ds_less(ds_ent a, ds_ent b) { /* a has lower priority than b */
+    if (a.sat != b.sat) return a.sat < b.sat;
+    if (a.deg != b.deg) return a.deg < b.deg;
+    return a.v > b.v;
+}
+static int dsatur(i64 n, const i64* ap, const i64* ai, const i64* tp, const i64* ti, int32_t* colour, int32_t* ncol) {
+    /* distinct-neighbour lists (merge of the row and column patterns) */
+    i64* np = (i64*)malloc(sizeof(i64) * (size_t)(n + 1));
+    i64 cap = (ap[n] + tp[n]) > 0 ? (ap[n] + tp[n]) : 1;
+    i64* nb = (i64*)malloc(sizeof(i64) * (size_t)cap);
+    np[0] = 0;
+    for (i64 i = 0; i < n; ++i) { /* row and column patterns, sorted, deduplicated, no diagonal */
+        i64 o = np[i], q = np[i];
+        for (i64 t = ap[i]; t < ap[i + 1]; ++t) if (ai[t] != i) nb[o++] = ai[t];
+        for (i64 t = tp[i]; t < tp[i + 1]; ++t) if (ti[t] != i) nb[o++] = ti[t];
+        qsort(nb + np[i], (size_t)(o - np[i]), sizeof(i64), cmp_i64);
+        for (i64 t = np[i]; t < o; ++t) if (q == np[i] || nb[q - 1] != nb[t]) nb[q++] = nb[t];
+        np[i + 1] = q;
+    }
+    uint64_t* bits = (uint64_t*)calloc((size_t)n * 4, sizeof(uint64_t));
+    int32_t* sat = (int32_t*)calloc((size_t)n, sizeof(int32_t));
+    i64 hcap = n + np[n] + 1, hn = 0;
+    ds_ent* h = (ds_ent*)malloc(sizeof(ds_ent) * (size_t)hcap);
+    int rc = 0;
+    int32_t maxc = 0;
+#define DS_PUSH(E) do { i64 k_ = hn++; h[k_] = (E); \
+        while (k_ > 0 && ds_less(h[(k_ - 1) / 2], h[k_])) { ds_ent t_ = h[k_]; h[k_] = h[(k_ - 1) / 2]; h[(k_ - 1) / 2] = t_; k_ = (k_ - 1) / 2; } } while (0)
+    for (i64 i = 0; i < n; ++i) { colour[i] = -1; ds_ent e = {0, (int32_t)(np[i + 1] - np[i]), i}; DS_PUSH(e); }
+    for (i64 done = 0; done < n;) {
+        ds_ent top = h[0];
+        h[0] = h[--hn];
+        for (i64 k = 0;;) { /* sift down */
+            i64 l = 2 * k + 1, r = l + 1, m = k;
+            if (l < hn && ds_less(h[m], h[l])) m = l;
+            if (r < hn && ds_less(h[m], h[r])) m = r;
+            if (m == k) break;
+            ds_ent t = h[k]; h[k] = h[m]; h[m] = t; k = m;
+        }
+        i64 v = top.v;
+        if (colour[v] >= 0 || top.sat != sat[v]) continue; /* stale entry */
+        int32_t c = 0;
+        while (c < 256 && (bits[v * 4 + (c >> 6)] >> (c & 63) & 1ull)) ++c;
+        if (c >= 256) { rc = -2; break; }
+        colour[v] = c;
+        if (c + 1 > maxc) maxc = c + 1;
+        ++done;
+        for (i64 t = np[v]; t < np[v + 1]; ++t) {
+            i64 w = nb[t];
+            if (colour[w] >= 0 || (bits[w * 4 + (c >> 6)] >> (c & 63) & 1ull)) continue;
+            bits[w * 4 + (c >> 6)] |= 1ull << (c & 63);
+            sat[w]++;
+            ds_ent e = {sat[w], (int32_t)(np[w + 1] - np[w]), w};
+            DS_PUSH(e);
+        }
+    }
+#undef DS_PUSH
+    *ncol = maxc;
+    free(h); free(sat); free(bits); free(nb); free(np);
+    return rc;
+}
+
+/* O11: DSATUR colouring, then `passes` iterated-greedy passes (Culberson): each visits the
+ * vertices by descending colour of the previous pass, ties by index; a pass never increases
+ * the number of colours.  passes < 0: plain greedy in index (Morton) order (reference). */
 int orc_greedy_colour(i64 n, const i64* ap, const i64* ai, const i64* tp, const i64* ti, int passes,
                       int32_t* colour, int32_t* ncol) {
     int32_t* used = (int32_t*)malloc(sizeof(int32_t) * 4096);
@@ -646,7 +716,10 @@ int orc_greedy_colour(i64 n, const i64* ap, const i64* ai, const i64* tp, const 
     int rc = 0;
     for (int c = 0; c < 4096; ++c) used[c] = -1;
     for (i64 i = 0; i < n; ++i) order[i] = i;
-    rc = greedy_pass(n, ap, ai, tp, ti, order, colour, used, ncol);
+    /* first colouring: DSATUR, or greedy in index order if DSATUR needed >= 256 colours
+       (passes < 0: plain greedy, no DSATUR and no iterated passes) */
+    if (passes < 0 || dsatur(n, ap, ai, tp, ti, colour, ncol) != 0)
+        rc = greedy_pass(n, ap, ai, tp, ti, order, colour, used, ncol);
     for (int r = 0; r < passes && rc == 0; ++r) {
         /* vertices by descending colour, ascending index within a colour */
         int32_t K = *ncol;

@@ -213,6 +213,38 @@ def test_gs_lower_triangular_one_sweep():
     assert np.allclose(u, np.linalg.solve(Ld, f), rtol=1e-13, atol=1e-13)
 
 
+def _pattern_csr(n, edges):
+    rows = [[i] for i in range(n)]
+    for a, b in edges:
+        rows[a].append(b)
+    ptr = np.zeros(n + 1, dtype=np.int64)
+    idx = []
+    for i, r in enumerate(rows):
+        r = sorted(set(r))
+        idx += r
+        ptr[i + 1] = len(idx)
+    return O.CSR(ptr, np.array(idx, dtype=np.int64), np.ones(len(idx)), (n, n))
+
+
+def test_dsatur_known_chromatic_numbers():
+    """DSATUR is exact on bipartite graphs (Brelaz 1979): a 7x9 grid takes 2 colours, as does
+    an even cycle; an odd cycle takes 3, the complete graph K_6 takes 6, a wheel with an odd
+    rim (W_7) takes 4.  The iterated passes keep these counts."""
+    grid = [(r * 9 + c, r * 9 + c + 1) for r in range(7) for c in range(8)] + \
+           [(r * 9 + c, (r + 1) * 9 + c) for r in range(6) for c in range(9)]
+    cases = [(63, grid, 2), (10, [(i, (i + 1) % 10) for i in range(10)], 2),
+             (9, [(i, (i + 1) % 9) for i in range(9)], 3),
+             (6, [(i, j) for i in range(6) for j in range(6) if i < j], 6),
+             (8, [(i, (i % 7) + 1 if i < 7 else 1) for i in range(1, 8)] + [(0, i) for i in range(1, 8)], 4)]
+    for n, edges, chi in cases:
+        A = _pattern_csr(n, edges)   # one direction only: the colouring symmetrises the pattern
+        for passes in (0, 10):
+            col, nc = O.greedy_colour(A, passes=passes)
+            assert nc == chi, (n, passes, nc)
+            for a, b in edges:
+                assert col[a] != col[b]
+
+
 def test_colouring_proper_and_multicolour_gs_is_dense_gs():
     h = _small_hierarchy()
     for lv in h.levels[:-1]:
@@ -225,9 +257,9 @@ def test_colouring_proper_and_multicolour_gs_is_dense_gs():
         # has neighbours of every colour 0..c-1 (it got c because those were taken)
         for v in range(lv.N):
             assert set(range(lv.colour[v])) <= set(lv.colour[S[v]].tolist())
-        # the first pass is greedy in index (Morton) order: each vertex takes the smallest
+        # plain greedy (passes < 0) in index (Morton) order: each vertex takes the smallest
         # colour not used by its lower-index neighbours
-        c0, n0 = O.greedy_colour(lv.L, passes=0)
+        c0, _ = O.greedy_colour(lv.L, passes=-1)
         for v in range(0, lv.N, 37):
             nb = np.flatnonzero(S[v]); nb = nb[nb < v]
             used = set(c0[nb].tolist())
@@ -235,8 +267,9 @@ def test_colouring_proper_and_multicolour_gs_is_dense_gs():
             while c in used:
                 c += 1
             assert c0[v] == c
-        # iterated-greedy passes never add colours (Culberson's theorem)
-        assert lv.ncolours <= n0 and lv.ncolours == lv.colour.max() + 1
+        # iterated-greedy passes never add colours to the DSATUR colouring (Culberson)
+        _, nd = O.greedy_colour(lv.L, passes=0)
+        assert lv.ncolours <= nd and lv.ncolours == lv.colour.max() + 1
         # multicolour GS = forward GS on the colour-major permuted matrix (textbook form)
         rng = np.random.default_rng(1)
         f = rng.uniform(-1, 1, lv.N)
