@@ -403,9 +403,21 @@ static T* bot_upload(mgm_ctx* ctx, const std::vector<T>& v, bool& ok) {
 
 void setup_bottom(mgm_ctx* ctx, const std::vector<double>& LU, const std::vector<i32>& piv) {
     ctx->botJ = -1;
-    i64 bmax = 16384, blocal = 256;  // measured best split for cfg3 (profiles/r01_notes.md)
+    // measured best split (profiles/r01_notes.md, session 3): the bottom starts at the first
+    // level with <= 4096 rows (cfg3: V-cycle 1270 -> 1165 us, cfg2: 1430 -> 1273 us against
+    // 16384 -- per-kernel colour steps of a 16k-row level beat its cluster phases now), and only
+    // levels <= 64 rows run on CTA 0 alone.  If that would leave only the coarsest level in the
+    // bottom (large coarsest, e.g. cfg5's 4096), the bottom starts at <= 16384 rows instead.
+    i64 bmax = 4096, blocal = 64;
+    const bool bmax_env = std::getenv("MGM_BOT_MAX") != nullptr;
     if (const char* e = std::getenv("MGM_BOT_MAX")) bmax = std::atoll(e);
     if (const char* e = std::getenv("MGM_BOT_LOCAL")) blocal = std::atoll(e);
+    if (!bmax_env) {
+        int first = -1;
+        for (int j = 1; j < ctx->p; ++j)
+            if (ctx->lv[j].n <= bmax) { first = j; break; }
+        if (first < 0 || first == ctx->p - 1) bmax = 16384;
+    }
     if (ctx->poisson || bmax <= 0 || ctx->p < 2) return;
     const int p = ctx->p;
     int dev = 0, optin = 0;
