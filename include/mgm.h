@@ -198,9 +198,16 @@ mgm_status mgm_export_weights(const mgm_ctx* ctx, double* w, int64_t* sten);
  *   MGM_OP_RESTRICT  y (n_{j+1}) = R_j x               (Poisson: multiplier copied)
  *   MGM_OP_INTERP    y (n_j) = P_j x (x has n_{j+1})   (Poisson: multiplier copied)
  *   MGM_OP_COARSE    y = L_p^{-1} x on the coarsest level (level ignored)
+ *   MGM_OP_SWEEP_ZG  y = ONE forward colour GS sweep from the zero guess with rhs f, by the
+ *                    zero-guess kernel (reads the diagonal and earlier-colour entries only;
+ *                    the level's u is filled with NaN first to show it is never read); x is
+ *                    ignored; shifted problems only
+ *   MGM_OP_PRECOND   y = M x, the V-cycle from the zero guess the Krylov solvers apply
+ *                    (level ignored; level-0 lib order; u starts as NaN when zero-guess
+ *                    sweeps are used)
  * f is used by SWEEP and RESIDUAL only. */
 enum { MGM_OP_SPMV = 0, MGM_OP_SWEEP = 1, MGM_OP_RESIDUAL = 2, MGM_OP_RESTRICT = 3,
-       MGM_OP_INTERP = 4, MGM_OP_COARSE = 5 };
+       MGM_OP_INTERP = 4, MGM_OP_COARSE = 5, MGM_OP_SWEEP_ZG = 6, MGM_OP_PRECOND = 7 };
 mgm_status mgm_apply(mgm_ctx* ctx, int level, int op, const double* x_dev, const double* f_dev,
                      double* y_dev, void* cuda_stream);
 

@@ -418,11 +418,14 @@ int colour_passes() {
 // its neighbours in sym(pattern) minus the diagonal), ties by larger degree (distinct
 // neighbours) then lower index, with the smallest colour unused by its neighbours.  Returns
 // the colour count, or -1 if a colour index would reach 256 (the caller falls back).
-static int dsatur_colouring(const HostCSR& A, const HostCSR& T, std::vector<i32>& colour) {
+// neighbours of each vertex in sym(pattern(A)) minus the diagonal: sorted, deduplicated
+static void sym_adjacency(const HostCSR& A, std::vector<i64>& np, std::vector<i64>& nb) {
+    const HostCSR T = transpose(A);
     const i64 n = A.nrows;
-    std::vector<i64> np(n + 1, 0), nb;
+    np.assign(n + 1, 0);
+    nb.clear();
     nb.reserve((size_t)(A.nnz() + T.nnz()));
-    for (i64 i = 0; i < n; ++i) {  // row and column patterns, sorted, deduplicated, no diagonal
+    for (i64 i = 0; i < n; ++i) {
         const size_t o0 = nb.size();
         for (i64 t = A.ptr[i]; t < A.ptr[i + 1]; ++t)
             if (A.col[t] != i) nb.push_back(A.col[t]);
@@ -432,6 +435,9 @@ static int dsatur_colouring(const HostCSR& A, const HostCSR& T, std::vector<i32>
         nb.erase(std::unique(nb.begin() + (i64)o0, nb.end()), nb.end());
         np[i + 1] = (i64)nb.size();
     }
+}
+
+static int dsatur_colouring(i64 n, const std::vector<i64>& np, const std::vector<i64>& nb, std::vector<i32>& colour) {
     struct Ent { i32 sat, deg; i64 v; };
     auto less = [](const Ent& x, const Ent& y) {  // x has lower priority than y
         if (x.sat != y.sat) return x.sat < y.sat;
@@ -487,14 +493,15 @@ static int dsatur_colouring(const HostCSR& A, const HostCSR& T, std::vector<i32>
 }
 
 int greedy_colouring(const HostCSR& A, std::vector<i32>& colour, int passes) {
-    HostCSR T = transpose(A);
     const i64 n = A.nrows;
+    std::vector<i64> np, nb;  // the symmetric adjacency, built once for every pass
+    sym_adjacency(A, np, nb);
     std::vector<i64> stamp(256, -1), order(n);
     for (i64 i = 0; i < n; ++i) order[i] = i;
     int ncol = 0;
     // first colouring: DSATUR (or greedy in Morton order if DSATUR needs >= 256 colours;
     // passes < 0: plain greedy in Morton order only)
-    const int pass0 = (passes >= 0 && (ncol = dsatur_colouring(A, T, colour)) > 0) ? 1 : 0;
+    const int pass0 = (passes >= 0 && (ncol = dsatur_colouring(n, np, nb, colour)) > 0) ? 1 : 0;
     if (pass0 == 0) ncol = 0;
     for (int pass = pass0; pass <= std::max(passes, 0); ++pass) {
         if (pass > 0) {  // descending previous colour, ascending index within a colour
@@ -515,8 +522,7 @@ int greedy_colouring(const HostCSR& A, std::vector<i32>& colour, int passes) {
                 if ((size_t)c >= stamp.size()) stamp.resize(2 * c + 2, -1);
                 stamp[c] = q;
             };
-            for (i64 t = A.ptr[i]; t < A.ptr[i + 1]; ++t) mark(A.col[t]);
-            for (i64 t = T.ptr[i]; t < T.ptr[i + 1]; ++t) mark(T.col[t]);
+            for (i64 t = np[i]; t < np[i + 1]; ++t) mark((i32)nb[t]);
             i32 c = 0;
             while ((size_t)c < stamp.size() && stamp[c] == q) ++c;
             colour[i] = c;

@@ -2745,6 +2745,24 @@ mgm_status mgm_apply(mgm_ctx* ctx, int level, int op, const double* x, const dou
         case MGM_OP_COARSE:
             enqueue_coarse(ctx, x, y, st);
             break;
+        case MGM_OP_SWEEP_ZG: {  // one forward sweep from the zero guess; u starts as NaN (never read)
+            if (!f || level == ctx->p - 1) return MGM_ERR_ARG;
+            if (!L.slw || ctx->poisson) return MGM_ERR_ARG;
+            k_fill<<<blocks_for(vn, 256), 256, 0, st>>>(vn, L.u, std::nan(""), PfList{nullptr, 0, 0});
+            CK(cudaMemcpyAsync(L.f, f, sizeof(double) * vn, cudaMemcpyDeviceToDevice, st));
+            enqueue_sweep(ctx, level, false, st, true);
+            CK(cudaMemcpyAsync(y, L.u, sizeof(double) * vn, cudaMemcpyDeviceToDevice, st));
+            break;
+        }
+        case MGM_OP_PRECOND: {  // y = M x, the Krylov preconditioner (level ignored, level-0 lib order)
+            Level& L0 = ctx->lv[0];
+            const i64 n0 = L0.n + pad;
+            k_fill<<<blocks_for(n0, 256), 256, 0, st>>>(n0, L0.u, zg_capable(ctx) ? std::nan("") : 0.0,
+                                                         PfList{nullptr, 0, 0});
+            if ((s = enqueue_precond(ctx, x, st))) return s;
+            CK(cudaMemcpyAsync(y, L0.u, sizeof(double) * n0, cudaMemcpyDeviceToDevice, st));
+            break;
+        }
         default:
             return MGM_ERR_ARG;
     }

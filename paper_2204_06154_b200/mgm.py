@@ -19,7 +19,7 @@ LIB_PATH = os.path.join(_HERE, "libmgm.so")
 
 MGM_OK, MGM_ERR_ARG, MGM_ERR_UNISOLVENT, MGM_ERR_SINGULAR, MGM_ERR_BREAKDOWN, \
     MGM_ERR_CUDA, MGM_ERR_NCCL, MGM_ERR_OOM, MGM_ERR_INPUT = range(9)
-OP_SPMV, OP_SWEEP, OP_RESIDUAL, OP_RESTRICT, OP_INTERP, OP_COARSE = range(6)
+OP_SPMV, OP_SWEEP, OP_RESIDUAL, OP_RESTRICT, OP_INTERP, OP_COARSE, OP_SWEEP_ZG, OP_PRECOND = range(8)
 STATUS_NAMES = {0: "MGM_OK", 1: "MGM_ERR_ARG", 2: "MGM_ERR_UNISOLVENT", 3: "MGM_ERR_SINGULAR",
                 4: "MGM_ERR_BREAKDOWN", 5: "MGM_ERR_CUDA", 6: "MGM_ERR_NCCL", 7: "MGM_ERR_OOM",
                 8: "MGM_ERR_INPUT"}

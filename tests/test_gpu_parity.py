@@ -134,6 +134,57 @@ def test_per_operator(name):
     assert relmax(P.to_oracle_order(jp, y.cpu().numpy()), P.ref.coarse_solve(r)) <= 1e-12
 
 
+@pytest.mark.parametrize("name", ["cfg1", "torus20000", "gfd9000"])
+def test_zero_guess_paths(name):
+    """The zero-guess kernels (first presmooth from e_j = 0; M v inside the Krylov solvers)
+    never read the iterate (it starts as NaN) and equal the oracle's sweep / V-cycle from 0."""
+    import torch
+    from paper_2204_06154_b200 import mgm_apply
+
+    P = pair(name)
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    for j in range(P.ref.p - 1):
+        o = P.ref.levels[j]
+        f = _rand(o.N, 40 + j)
+        y = torch.empty(o.N, dtype=torch.float64, device="cuda")
+        mgm_apply(P.gpu.ctx, j, 6, dev(np.zeros(o.N)), dev(P.to_lib_order(j, f)), y)
+        u = np.zeros(o.N)
+        P.ref._smooth(o, f, u, 1, False)
+        yo = P.to_oracle_order(j, y.cpu().numpy())
+        assert np.isfinite(yo).all() and relmax(yo, u) <= 1e-12, ("zero-guess sweep", j)
+    n = P.ref.levels[0].N
+    v = _rand(n, 50)
+    y = torch.empty(n, dtype=torch.float64, device="cuda")
+    mgm_apply(P.gpu.ctx, 0, 7, dev(P.to_lib_order(0, v)), None, y)
+    ref = P.ref.vcycle_level_order(v, np.zeros(n))
+    yo = P.to_oracle_order(0, y.cpu().numpy())
+    assert np.isfinite(yo).all() and relmax(yo, ref) <= 1e-12
+
+
+def test_device_gmres_equals_host_loop(monkeypatch):
+    """The device-side GMRES (WHILE graph node per restart cycle, Givens on the device) and the
+    host-driven loop run the same arithmetic: same iteration count and residual history, and
+    solutions to 1e-12; a restart (restart = 5) is crossed on the way."""
+    import torch
+    from paper_2204_06154_b200 import MGM
+
+    w = MI.make_workload(3, n=20000)
+    lv = dict(w.levels, restart=5)
+    rhs = torch.from_numpy(w.rhs).cuda()
+    out = []
+    for host in (False, True):
+        if host:
+            monkeypatch.setenv("MGM_HOST_GMRES", "1")
+        m = MGM(w.points, w.normals, w.stencil, lv)
+        x, rep = m.solve(rhs, tol=1e-10, krylov=1, maxit=300)
+        out.append((x.cpu().numpy(), rep))
+        m.close()
+    (xd, rd), (xh, rh) = out
+    assert rd.converged and rh.converged and rd.iterations == rh.iterations > 5
+    assert np.allclose(rd.history, rh.history, rtol=1e-9, atol=0)
+    assert np.linalg.norm(xd - xh) / np.linalg.norm(xh) <= 1e-12
+
+
 @pytest.mark.parametrize("name", list(CASES))
 def test_vcycle(name):
     import torch
