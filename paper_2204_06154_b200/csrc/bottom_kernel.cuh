@@ -183,7 +183,7 @@ __device__ __forceinline__ void bcast_store_async(uint32_t sbase, int off, int r
 }
 
 template <int TPR>
-__device__ __forceinline__ void bottom_phase(const BPhase& P, const BFrag& fr0, int g, int nthr, const char* smem,
+__device__ __forceinline__ void bottom_phase(const BPhase& P, BFrag& fr, int g, int nthr, const char* smem,
                                              uint32_t sbase, int cs, uint64_t pol, long long* tr, uint32_t mbar) {
     constexpr int CH = bot_ch(TPR);
     const int lane = g & (TPR - 1);
@@ -194,8 +194,8 @@ __device__ __forceinline__ void bottom_phase(const BPhase& P, const BFrag& fr0, 
     for (int base = 0; base < nrows; base += ngroups) {  // uniform trip count across threads
         const int row = P.r0 + base + g / TPR;
         const bool live = row < P.r1;
-        BFrag fr = fr0;  // register copy; rows after the first are loaded here
-        if (base != 0) bfrag_load<TPR>(fr, P, row, lane, pol);
+        if (base != 0) bfrag_load<TPR>(fr, P, row, lane, pol);  // rows after the first (in place:
+                                                                // fr is reloaded for the next phase anyway)
         // epilogue operand issued together with the gathers
         double ev = 0.0;
         if (live && lane == 0) {
@@ -246,27 +246,25 @@ __device__ __forceinline__ void bottom_phase(const BPhase& P, const BFrag& fr0, 
     }
 }
 
+// Threads per row: 2, 8 or 32 only (BOT_TPR_MASK; the host picks among these).  Fewer
+// specialisations keep the kernel's code smaller -- the phase loop is instruction-latency
+// bound and its code does not fit the instruction cache.
+constexpr unsigned BOT_TPR_MASK = (1u << 1) | (1u << 3) | (1u << 5);
 __device__ __forceinline__ void bfrag_load_any(BFrag& fr, const BPhase& P, int g, uint64_t pol) {
     const int row = P.r0 + (g >> P.tpr_log2);
     const int lane = g & ((1 << P.tpr_log2) - 1);
     switch (P.tpr_log2) {
-        case 0: bfrag_load<1>(fr, P, row, lane, pol); break;
         case 1: bfrag_load<2>(fr, P, row, lane, pol); break;
-        case 2: bfrag_load<4>(fr, P, row, lane, pol); break;
         case 3: bfrag_load<8>(fr, P, row, lane, pol); break;
-        case 4: bfrag_load<16>(fr, P, row, lane, pol); break;
         default: bfrag_load<32>(fr, P, row, lane, pol); break;
     }
 }
-__device__ __forceinline__ void bottom_phase_any(const BPhase& P, const BFrag& fr, int g, int nthr, const char* smem,
+__device__ __forceinline__ void bottom_phase_any(const BPhase& P, BFrag& fr, int g, int nthr, const char* smem,
                                                  uint32_t sbase, int cs, uint64_t pol, long long* tr,
                                                  uint32_t mbar) {
     switch (P.tpr_log2) {
-        case 0: bottom_phase<1>(P, fr, g, nthr, smem, sbase, cs, pol, tr, mbar); break;
         case 1: bottom_phase<2>(P, fr, g, nthr, smem, sbase, cs, pol, tr, mbar); break;
-        case 2: bottom_phase<4>(P, fr, g, nthr, smem, sbase, cs, pol, tr, mbar); break;
         case 3: bottom_phase<8>(P, fr, g, nthr, smem, sbase, cs, pol, tr, mbar); break;
-        case 4: bottom_phase<16>(P, fr, g, nthr, smem, sbase, cs, pol, tr, mbar); break;
         default: bottom_phase<32>(P, fr, g, nthr, smem, sbase, cs, pol, tr, mbar); break;
     }
 }
@@ -290,9 +288,13 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 
 // smem: [phase table (nph x BPhase)][replicated vectors at the offsets in the phases]
+// TRACE = false: the production instance, no diagnostics code in the phase loop (the trace
+// checks cost instructions in a loop that is instruction-latency bound); TRACE = true runs
+// when MGM_TRACE is set at setup.
+template <bool TRACE>
 __global__ void __launch_bounds__(BOT_THREADS, 1)
-    k_vcycle_bottom(const BPhase* __restrict__ gphases, int nph, unsigned long long* __restrict__ trace, PfList pf,
-                    int arm0, int arm1) {
+    k_vcycle_bottom_t(const BPhase* __restrict__ gphases, int nph, unsigned long long* __restrict__ trace, PfList pf,
+                      int arm0, int arm1) {
     extern __shared__ __align__(16) char smem[];
     __shared__ __align__(8) unsigned long long mbars[2];  // data-synchronised phases k & 1
     const uint32_t mbar = (uint32_t)__cvta_generic_to_shared(mbars);
@@ -331,12 +333,12 @@ __global__ void __launch_bounds__(BOT_THREADS, 1)
     cluster_wait();
     // fine timeline (diagnostics): thread 0 of CTA 0 and of the last CTA, 8 clocks per phase
     long long* ftr = nullptr;
-    if (trace && trace[BOT_MAX_PHASES - 1] == 2ull && threadIdx.x == 0 && (rank == 0 || rank == cs - 1))
+    if (TRACE && trace && trace[BOT_MAX_PHASES - 1] == 2ull && threadIdx.x == 0 && (rank == 0 || rank == cs - 1))
         ftr = reinterpret_cast<long long*>(trace) + BOT_MAX_PHASES + (rank == 0 ? 0 : 8 * BOT_MAX_PHASES);
     for (int q = 0; q < nph; ++q) {
-        if (trace && rank == 0 && threadIdx.x == 0) trace[q] = gtimer();  // diagnostics (MGM_TRACE)
-        long long* tr = ftr ? ftr + 8 * q : nullptr;
-        if (tr) { tr[0] = clock64(); tr[7] = clk_after_i(fr.c[0]); }
+        if (TRACE && trace && rank == 0 && threadIdx.x == 0) trace[q] = gtimer();  // diagnostics (MGM_TRACE)
+        long long* tr = TRACE && ftr ? ftr + 8 * q : nullptr;
+        if (TRACE && tr) { tr[0] = clock64(); tr[7] = clk_after_i(fr.c[0]); }
         const BPhase P = phases[q];
         if (P.op == BP_ZERO) {  // every CTA zeroes its own copy
             double* y = reinterpret_cast<double*>(smem + P.yo);
@@ -352,32 +354,37 @@ __global__ void __launch_bounds__(BOT_THREADS, 1)
         const BPhase& N = phases[q + 1];
         const bool part = !P.local || rank == 0;
         const bool npart = !N.local || rank == 0;
-        if (P.mb >= 0) {  // data-synchronised: wait for this phase's bytes, re-arm for phase mb + 2
-            if (npart) bfrag_load_any(fr, N, N.local ? (int)threadIdx.x : g_cl, pol);
-            if (tr) tr[4] = clock64();
-            const uint32_t b = mbar + 8u * (unsigned)(P.mb & 1);
-            mbar_wait(b, (unsigned)((P.mb >> 1) & 1));
-            if (tr) tr[5] = clock64();
-            if (threadIdx.x == 0 && P.arm > 0) mbar_arm(b, (unsigned)P.arm);
-            if (tr) tr[6] = clock64();
-        } else if (P.local && N.local) {  // CTA 0 only; the other CTAs skip local phases
-            if (npart) bfrag_load_any(fr, N, (int)threadIdx.x, pol);
-            if (part) __syncthreads();
-        } else {
+        const bool ll = P.local && N.local;  // CTA 0 only; the other CTAs skip local phases
+        if (P.mb < 0 && !ll) {
             // zeroing / plain remote stores (generic proxy) before later st.async writes to the
             // same words
             if (P.op == BP_ZERO || P.op == BP_MVZ || P.local)
                 asm volatile("fence.proxy.async.shared::cluster;" ::: "memory");
             cluster_arrive();
-            if (tr) tr[4] = clock64();
-            if (npart) bfrag_load_any(fr, N, N.local ? (int)threadIdx.x : g_cl, pol);
-            if (tr) tr[5] = clock64();
-            cluster_wait();
-            if (tr) tr[6] = clock64();
         }
+        if (TRACE && tr) tr[4] = clock64();
+        // the next phase's operator rows, overlapping the synchronisation (one call site: the
+        // loop is instruction-latency bound and its code size matters)
+        if (npart) bfrag_load_any(fr, N, N.local ? (int)threadIdx.x : g_cl, pol);
+        if (TRACE && tr) tr[5] = clock64();
+        if (P.mb >= 0) {  // data-synchronised: wait for this phase's bytes, re-arm for phase mb + 2
+            const uint32_t b = mbar + 8u * (unsigned)(P.mb & 1);
+            mbar_wait(b, (unsigned)((P.mb >> 1) & 1));
+            if (threadIdx.x == 0 && P.arm > 0) mbar_arm(b, (unsigned)P.arm);
+        } else if (ll) {
+            if (part) __syncthreads();
+        } else {
+            cluster_wait();
+        }
+        if (TRACE && tr) tr[6] = clock64();
     }
     cluster_arrive();  // no CTA exits while others may still store into its shared memory
     cluster_wait();
+}
+
+// the two instances (the host picks by MGM_TRACE)
+inline void* bottom_kernel_ptr(bool trace) {
+    return trace ? (void*)k_vcycle_bottom_t<true> : (void*)k_vcycle_bottom_t<false>;
 }
 
 }  // namespace mgm

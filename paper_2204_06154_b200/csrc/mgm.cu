@@ -441,8 +441,10 @@ void setup_bottom(mgm_ctx* ctx, const std::vector<double>& LU, const std::vector
         }
     }
     if (J < 0) return;
-    cudaFuncSetAttribute(k_vcycle_bottom, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    set_max_dyn_smem((const void*)k_vcycle_bottom);
+    for (bool tr : {false, true}) {
+        cudaFuncSetAttribute(bottom_kernel_ptr(tr), cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        set_max_dyn_smem(bottom_kernel_ptr(tr));
+    }
     // cluster size: 16 (non-portable) if the device can co-schedule it, else 8
     size_t smem = table;
     std::vector<int> ou(p, -1);
@@ -466,7 +468,7 @@ void setup_bottom(mgm_ctx* ctx, const std::vector<double>& LU, const std::vector
         cfg.attrs = at;
         cfg.numAttrs = 1;
         int ncl = 0;
-        if (cudaOccupancyMaxActiveClusters(&ncl, k_vcycle_bottom, &cfg) == cudaSuccess && ncl > 0) { cs = c; break; }
+        if (cudaOccupancyMaxActiveClusters(&ncl, bottom_kernel_ptr(false), &cfg) == cudaSuccess && ncl > 0) { cs = c; break; }
         cudaGetLastError();
     }
     if (!cs) return;
@@ -559,6 +561,7 @@ void setup_bottom(mgm_ctx* ctx, const std::vector<double>& LU, const std::vector
             int lgmax = 5;  // tuning experiment: MGM_BOT_TPR_MAX caps threads per row
             if (const char* e = std::getenv("MGM_BOT_TPR_MAX")) lgmax = std::max(0, std::min(5, (int)std::log2(std::atoi(e))));
             for (int lg = lgmax; lg >= 0; --lg) {  // largest tpr that covers W and fits one pass
+                if (!(BOT_TPR_MASK >> lg & 1u)) continue;  // compiled specialisations only
                 const int tpr = 1 << lg;
                 if (bot_ch(tpr) * tpr < P.W) continue;
                 smallest_valid = lg;
@@ -566,6 +569,7 @@ void setup_bottom(mgm_ctx* ctx, const std::vector<double>& LU, const std::vector
             }
             if (best < 0) best = smallest_valid >= 0 ? smallest_valid : 5;
         }
+        if (op == BP_ZERO || op == BP_STORE) best = 5;  // (no operator; any compiled value)
         P.tpr_log2 = best;
         P.mb = -1;
         P.arm = 0;
@@ -1577,9 +1581,12 @@ void enqueue_vcycle(mgm_ctx* ctx, cudaStream_t st) {
         cfg.dynamicSmemBytes = ctx->bot_smem;
         const PfList pf = pf_take(ctx, ctx->pf_l0only ? Regions{} : ctx->bot_pf, !ctx->pf_l0only, ctx->pf_bot_budget);
         if (!g_dry)
-            note_launch(cudaLaunchKernelEx(&cfg, k_vcycle_bottom, (const BPhase*)ctx->d_phases, ctx->nphases,
-                                           ctx->d_trace ? ctx->d_trace + 256 : (unsigned long long*)nullptr, pf,
-                                           ctx->bot_arm0, ctx->bot_arm1),
+            note_launch(ctx->d_trace
+                            ? cudaLaunchKernelEx(&cfg, k_vcycle_bottom_t<true>, (const BPhase*)ctx->d_phases,
+                                                 ctx->nphases, ctx->d_trace + 256, pf, ctx->bot_arm0, ctx->bot_arm1)
+                            : cudaLaunchKernelEx(&cfg, k_vcycle_bottom_t<false>, (const BPhase*)ctx->d_phases,
+                                                 ctx->nphases, (unsigned long long*)nullptr, pf, ctx->bot_arm0,
+                                                 ctx->bot_arm1),
                         ctx->bot_cluster, BOT_THREADS, ctx->bot_smem);
         ctx->vcycle_kernels++;
     } else {
