@@ -424,7 +424,7 @@ def main():
             "config": {"workload": f"{w.name} N={N}", "levels": [lv["n"] for lv in levels],
                        "nnz": [lv["nnz"] for lv in levels],
                        "colours": [lv["colours"] for lv in levels],
-                       "gmres_iterations": its[-1], "restart": 50, "tol": 1e-10,
+                       "gmres_iterations": its[-1], "restart": w.levels.get("restart", 50), "tol": 1e-10,
                        "parallelism": (f"dist{ws} (level-0 row pieces + NCCL)" if dist_mode else
                                        f"replicas{ws}" if ws > 1 else "single GPU"),
                        "l2": "inputs larger than L2 (hierarchy %.2f GB)" %
