@@ -169,7 +169,10 @@ def stage_breakdown(w, f, hbm):
                 return 12.0 * lv[j]["nnz_zg"] + 16.0 * lv[j]["n"] + sweep_b(j, nu1 - 1)
             return 8.0 * lv[j]["n"] + sweep_b(j, nu1)
         if name == "residual+restrict":
-            return 12.0 * lv[j]["nnz"] + 32.0 * lv[j]["n"] + 12.0 * lv[j]["nnz_P"] + 8.0 * lv[j]["n"] + 8.0 * lv[j + 1]["n"]
+            res = 12.0 * lv[j]["nnz"] + 32.0 * lv[j]["n"]
+            if lv[j]["nnz_zg"] < lv[j]["nnz"] and nu1 == 1 and lv[j]["n"] >= 131072:  # after the zero-guess sweep
+                res = 12.0 * (lv[j]["nnz"] - lv[j]["nnz_zg"]) + 24.0 * lv[j]["n"]
+            return res + 12.0 * lv[j]["nnz_P"] + 8.0 * lv[j]["n"] + 8.0 * lv[j + 1]["n"]
         if name == "interp":
             return 12.0 * lv[j]["nnz_P"] + 8.0 * lv[j + 1]["n"] + 16.0 * lv[j]["n"]
         if name == "interp+postsmooth":

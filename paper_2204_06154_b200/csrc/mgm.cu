@@ -89,6 +89,7 @@ struct Level {
     std::vector<i64> h_sptr, h_rptr;  // host copies of the slice offsets (L2 prefetch regions)
     i32* slw = nullptr;                 // per slice: slots read by a sweep from a zero guess (pack_sell)
     uint8_t* nlow = nullptr;            // per row: its earlier-colour entries (slots 1..nlow)
+    i32* sluw = nullptr;                // per slice: first later-colour slot of its rows (min 1 + nlow)
     std::vector<i64> lower_per_colour;  // per colour: stored entries such a sweep reads (diag + earlier colours)
     int tpr = 1, rtpr = 1;  // threads per row for L_j (colour sweeps) and R_j kernels
     int stpr = 1;           // threads per row for full-level SpMV / residual on L_j
@@ -159,6 +160,8 @@ struct mgm_ctx {
     cudaGraphExec_t vgraph0 = nullptr;  // the same V-cycle from a zero guess on level 0 (Krylov preconditioner)
     bool vc_zero_guess = false;         // set while enqueueing vgraph0
     bool no_zg = false;                 // MGM_NO_ZG: no zero-guess sweeps (comparison)
+    i64 upper_res_min = 131072;         // levels with at least this many rows use the later-colour
+                                        // residual after a zero-guess sweep (MGM_UPPER_RES_MIN)
     bool pdl = false;  // set while enqueueing the V-cycle (PDL launches)
     // bottom of the V-cycle (levels botJ..p-1) in one thread-block-cluster kernel
     // (bottom_kernel.cuh); botJ < 0 = off
@@ -296,7 +299,8 @@ namespace {
 void pack_sell(const HostCSR& A, const std::vector<i64>& row_lib2mor, const std::vector<i32>& col_mor2lib,
                bool diag_first, std::vector<i64>& sptr, std::vector<i32>& scol, std::vector<double>& sval,
                HostCSR* lib_csr, const std::vector<i32>* colour_lib = nullptr, std::vector<i32>* slw = nullptr,
-               std::vector<i64>* lower_per_colour = nullptr, std::vector<uint8_t>* nlow_row = nullptr) {
+               std::vector<i64>* lower_per_colour = nullptr, std::vector<uint8_t>* nlow_row = nullptr,
+               std::vector<i32>* sluw = nullptr) {
     i64 n = (i64)row_lib2mor.size();
     i64 ns = (n + 31) / 32;
     sptr.assign(ns + 1, 0);
@@ -320,6 +324,7 @@ void pack_sell(const HostCSR& A, const std::vector<i64>& row_lib2mor, const std:
     std::vector<std::pair<i32, double>> row, srow;
     if (slw) slw->assign(ns, 1);
     if (nlow_row) nlow_row->assign(n, 0);
+    if (sluw) sluw->assign(ns, 1 << 30);
     if (lower_per_colour && colour_lib) {
         i32 nc = 0;
         for (i32 c : *colour_lib) nc = std::max(nc, c + 1);
@@ -346,6 +351,7 @@ void pack_sell(const HostCSR& A, const std::vector<i64>& row_lib2mor, const std:
                 if ((*colour_lib)[col_mor2lib[row[k].first]] >= cr) srow[o++] = row[k];
             if (slw) (*slw)[s] = std::max<i32>((*slw)[s], (i32)(1 + nlow));
             if (nlow_row) (*nlow_row)[r] = (uint8_t)std::min<i64>(nlow, 255);
+            if (sluw) (*sluw)[s] = std::min<i32>((*sluw)[s], (i32)(1 + nlow));
             if (lower_per_colour) (*lower_per_colour)[cr] += 1 + nlow;
         }
         for (i64 k = 0; k < w; ++k) {
@@ -946,15 +952,18 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
         std::vector<i64> sptr;
         std::vector<i32> scol;
         std::vector<double> sval;
-        std::vector<i32> slw;
+        std::vector<i32> slw, sluw;
         std::vector<uint8_t> nlow;
         bool coloured = L.ncol > 0 && j + 1 < p;
         pack_sell(Lm[j], lib2mor[j], mor2lib[j], true, sptr, scol, sval, &L.L_lib,
                   coloured ? &L.colour_lib : nullptr, coloured ? &slw : nullptr,
-                  coloured ? &L.lower_per_colour : nullptr, coloured ? &nlow : nullptr);
+                  coloured ? &L.lower_per_colour : nullptr, coloured ? &nlow : nullptr,
+                  coloured ? &sluw : nullptr);
         for (i64 r = 0; r < n && coloured; ++r)
             if (nlow[(size_t)r] == 255) coloured = false;  // (no zero-guess sweeps for such rows)
-        if (coloured && ((s = upload(ctx, &L.slw, slw)) || (s = upload(ctx, &L.nlow, nlow)))) return s;
+        if (coloured && ((s = upload(ctx, &L.slw, slw)) || (s = upload(ctx, &L.nlow, nlow)) ||
+                         (s = upload(ctx, &L.sluw, sluw))))
+            return s;
         L.sell_stored = (i64)sval.size();
         {
             double wavg = (double)L.sell_stored / (double)std::max<i64>(1, (n + 31) / 32 * 32);
@@ -1237,11 +1246,15 @@ void launch_gs(bool pdl, bool poisson, int tpr, int r0, int r1, int span, const 
         else gs_launch_t<false, 8>(pdl, r0, r1, span, L, st, pf, zg);
     }
 }
+// (MODE 2 reads the level's later-colour slot tables g_sluw / g_nlow, set by enqueue_residual)
+static thread_local const int* g_sluw = nullptr;
+static thread_local const uint8_t* g_nlow = nullptr;
 template <int MODE, bool P, int TPR>
 void spmv_launch_t(bool pdl, i64 r0, i64 r1, i64 nl, const i64* sptr, const i32* scol, const double* sval,
                    const double* x, const double* f, double* y, const double* c, cudaStream_t st, PfList pf) {
     launch(pdl, k_sell_spmv<MODE, P, TPR, CHUNK>, blocks_for((r1 - (r0 & ~31)) * TPR, 256), 256, 0, st, (int)r0,
-           (int)r1, (int)nl, sptr, scol, sval, x, f, y, c, pf);
+           (int)r1, (int)nl, sptr, scol, sval, x, f, y, c, pf, MODE == 2 ? g_sluw : (const int*)nullptr,
+           MODE == 2 ? g_nlow : (const uint8_t*)nullptr);
 }
 template <int MODE, bool P>
 void spmv_launch_p(bool pdl, int tpr, i64 r0, i64 r1, i64 nl, const i64* sptr, const i32* scol, const double* sval,
@@ -1256,7 +1269,9 @@ void launch_spmv(bool pdl, int mode, bool poisson, int tpr, i64 r0, i64 r1, i64 
                  const i32* scol, const double* sval, const double* x, const double* f, double* y, const double* c,
                  cudaStream_t st, PfList pf = {}) {
     if (r1 <= r0) return;
-    if (mode == 0) {
+    if (mode == 2) {  // residual after a zero-guess sweep (shifted problems)
+        spmv_launch_p<2, false>(pdl, tpr, r0, r1, nl, sptr, scol, sval, x, f, y, c, st, pf);
+    } else if (mode == 0) {
         if (poisson) spmv_launch_p<0, true>(pdl, tpr, r0, r1, nl, sptr, scol, sval, x, f, y, c, st, pf);
         else spmv_launch_p<0, false>(pdl, tpr, r0, r1, nl, sptr, scol, sval, x, f, y, c, st, pf);
     } else {
@@ -1442,14 +1457,21 @@ void enqueue_spmv(mgm_ctx* ctx, int j, const double* x, double* y, cudaStream_t 
     if (ctx->poisson) enqueue_border_dot(ctx, L, x, nullptr, 0.0, 1.0, y, st);
 }
 
-// t = f - L u (level j), Poisson: t[n] = f[n] - c.u
-void enqueue_residual(mgm_ctx* ctx, int j, const double* f, const double* u, double* t, cudaStream_t st) {
+// t = f - L u (level j), Poisson: t[n] = f[n] - c.u.  after_zg: u is the result of ONE forward
+// sweep from a zero guess, so t = -(later-colour part of L) u (k_sell_spmv MODE 2)
+void enqueue_residual(mgm_ctx* ctx, int j, const double* f, const double* u, double* t, cudaStream_t st,
+                      bool after_zg = false) {
     Level& L = ctx->lv[j];
+    // (bandwidth-bound levels only: on the small latency-bound levels the extra per-row table
+    // loads cost more than the skipped entries save -- cfg3 L2/L3 17 -> 23 us)
+    const int mode = (after_zg && L.sluw && !ctx->poisson && !ctx->no_zg && L.n >= ctx->upper_res_min) ? 2 : 1;
+    g_sluw = L.sluw;
+    g_nlow = L.nlow;
     for_my_pieces(ctx, j, 0, L.n, [&](i64 a, i64 b) {
         Regions rg;
         if (!ctx->pf_l0only) pf_sell(rg, L.h_sptr, L.scol, L.sval, a, b);
         const PfList pf = pf_take(ctx, rg, !ctx->pf_l0only);
-        launch_spmv(ctx->pdl, 1, ctx->poisson, L.stpr, a, b, L.n, L.sptr, L.scol, L.sval, u, f, t, L.c, st, pf);
+        launch_spmv(ctx->pdl, mode, ctx->poisson, L.stpr, a, b, L.n, L.sptr, L.scol, L.sval, u, f, t, L.c, st, pf);
         ctx->vcycle_kernels++;
     });
     dist_exchange(ctx, j, t, 0, L.n, st);
@@ -1548,7 +1570,7 @@ void enqueue_vcycle(mgm_ctx* ctx, cudaStream_t st) {
     // the diagonal and earlier-colour entries (k_gs_colour ZG)
     for (int s = 0; s < nu1; ++s) enqueue_sweep(ctx, 0, pre_b, st, s == 0 && ctx->vc_zero_guess);  // line 4
     stamp(ctx, "presmooth", 0, st);
-    enqueue_residual(ctx, 0, lv[0].f, lv[0].u, lv[0].t, st);              // line 5
+    enqueue_residual(ctx, 0, lv[0].f, lv[0].u, lv[0].t, st, ctx->vc_zero_guess && nu1 == 1);  // line 5
     stamp(ctx, "residual", 0, st);
     enqueue_restrict(ctx, 0, lv[0].t, lv[1].f, st);
     stamp(ctx, "restrict", 0, st);
@@ -1559,7 +1581,7 @@ void enqueue_vcycle(mgm_ctx* ctx, cudaStream_t st) {
         if (!zg) enqueue_zero(ctx, lv[j].u, lv[j].n + pad, st);
         for (int s = 0; s < nu1; ++s) enqueue_sweep(ctx, j, pre_b, st, s == 0 && zg);
         stamp(ctx, "zero+presmooth", j, st);
-        enqueue_residual(ctx, j, lv[j].f, lv[j].u, lv[j].t, st);
+        enqueue_residual(ctx, j, lv[j].f, lv[j].u, lv[j].t, st, zg && nu1 == 1);
         enqueue_restrict(ctx, j, lv[j].t, lv[j + 1].f, st);
         stamp(ctx, "residual+restrict", j, st);
     }
@@ -2376,6 +2398,7 @@ mgm_status mgm_setup(const double* points, const double* normals, int64_t n_poin
     if (const char* e = std::getenv("MGM_PF_DIST")) ctx->pf_dist = std::max(0, std::atoi(e));
     if (const char* e = std::getenv("MGM_PF_CAP_MB")) ctx->pf_cap = (i64)std::max(0, std::atoi(e)) << 20;
     if (std::getenv("MGM_NO_ZG")) ctx->no_zg = true;
+    if (const char* e = std::getenv("MGM_UPPER_RES_MIN")) ctx->upper_res_min = std::atoll(e);
     if (std::getenv("MGM_PF_LATE")) ctx->pf_late = 1;
     if (std::getenv("MGM_PF_NOF")) ctx->pf_nof = 1;
     if (std::getenv("MGM_PF_L0ONLY")) ctx->pf_l0only = 1;
@@ -2545,7 +2568,7 @@ mgm_status mgm_destroy(mgm_ctx* ctx) {
     for (auto& L : ctx->lv) {
         for (void* ptr : {(void*)L.sptr, (void*)L.scol, (void*)L.sval, (void*)L.pcol, (void*)L.pval, (void*)L.rptr,
                           (void*)L.rcol, (void*)L.rval, (void*)L.u, (void*)L.f, (void*)L.t, (void*)L.c, (void*)L.slw,
-                          (void*)L.nlow})
+                          (void*)L.nlow, (void*)L.sluw})
             if (ptr) cudaFree(ptr);
     }
     for (void* ptr : {(void*)ctx->lu, (void*)ctx->piv, (void*)ctx->d_lib2orig, (void*)ctx->V, (void*)ctx->w,
@@ -2813,6 +2836,9 @@ mgm_status mgm_bytes_model(const mgm_ctx* ctx, double* vcycle_bytes, double* spm
             double low = 0.0;
             for (i64 v : L.lower_per_colour) low += (double)v;
             B -= (12.0 * z + 24.0 * n) - (12.0 * low + 16.0 * n);
+            // and with nu1 = 1 the residual reads only the later-colour entries, no f
+            if (ctx->lp.nu1 == 1 && L.n >= ctx->upper_res_min)
+                B -= (12.0 * z + 16.0 * n) - (12.0 * (z - low) + 8.0 * n);
         }
         B += 12.0 * z + 16.0 * n + 12.0 * q + 8.0 * nn + 16.0 * n + bp * n;  // residual + restrict (unfused)
         B += 12.0 * q + 8.0 * nn + 16.0 * n;                        // interp + correct

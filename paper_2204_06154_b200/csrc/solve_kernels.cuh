@@ -248,7 +248,13 @@ __global__ void __launch_bounds__(256) k_gs_colour_pipe(int r0, int r1, int rows
     }
 }
 
-// y = L x  (MODE 0),  y = f - L x  (MODE 1) on the rows [r0, r1).  Poisson: border term
+// y = L x  (MODE 0),  y = f - L x  (MODE 1) on the rows [r0, r1).
+// MODE 2: the residual right after a forward Gauss-Seidel sweep from a ZERO guess,
+// y = f - L u = -sum_{later colours} a_ij u_j: the sweep made every row's residual zero when
+// it updated the row (f_i = a_ii u_i + sum_{earlier colours} a_ij u_j), and only the later
+// colours changed since.  Reads the later-colour slots of pack_sell's [diag | earlier |
+// later] rows (from sluw[slice] = 1 + the slice's smallest earlier count, masked below
+// 1 + nlow[r]); equal to f - L u up to rounding.  Poisson: border term
 // c_i * x[nl] (nl = the level's row count; the multiplier sits after the rows).
 template <int MODE, bool POISSON, int TPR, int CH>
 __global__ void __launch_bounds__(256) k_sell_spmv(int r0, int r1, int nl, const int64_t* __restrict__ sptr,
@@ -257,7 +263,9 @@ __global__ void __launch_bounds__(256) k_sell_spmv(int r0, int r1, int nl, const
                                                    const double* __restrict__ x,
                                                    const double* __restrict__ f,
                                                    double* __restrict__ y,
-                                                   const double* __restrict__ c, PfList pf) {
+                                                   const double* __restrict__ c, PfList pf,
+                                                   const int* __restrict__ sluw = nullptr,
+                                                   const uint8_t* __restrict__ nlow = nullptr) {
     pdl_trigger();
     l2_prefetch_share(pf);
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
@@ -265,26 +273,40 @@ __global__ void __launch_bounds__(256) k_sell_spmv(int r0, int r1, int nl, const
     const int part = g % TPR;
     const bool live = r >= r0 && r < r1;
     RowFrag<TPR, CH> fr;
-    int w = 0;
+    int w = 0, k1 = part, lim = 0;
     int64_t base = 0;
     if (live) {
         const int64_t s0 = sptr[r >> 5];
         w = (int)((sptr[(r >> 5) + 1] - s0) >> 5);
         base = s0 + (r & 31);
-        fr.load(sval + base, scol + base, w, part);
+        if (MODE == 2) {  // later-colour slots only: from the slice's first one, masked per row
+            k1 = sluw[r >> 5] + part;
+            lim = 1 + (int)nlow[r];
+        }
+        fr.load(sval + base, scol + base, w, k1);
     } else {
         fr.load(sval, scol, 0, 0);
     }
+    if (MODE == 2) {
+#pragma unroll
+        for (int q = 0; q < CH; ++q)
+            if (k1 + q * TPR < lim) fr.c[q] = -1;
+    }
     pdl_wait();
     double acc = fr.dot(x, 0.0);
-    for (int k0 = part + TPR * CH; k0 < w; k0 += TPR * CH) {
+    for (int k0 = k1 + TPR * CH; k0 < w; k0 += TPR * CH) {
         fr.load(sval + base, scol + base, w, k0);
+        if (MODE == 2) {
+#pragma unroll
+            for (int q = 0; q < CH; ++q)
+                if (k0 + q * TPR < lim) fr.c[q] = -1;
+        }
         acc = fr.dot(x, acc);
     }
     acc = group_sum<TPR>(acc);
     if (live && part == 0) {
         if (POISSON) acc += c[r] * x[nl];
-        y[r] = (MODE == 0) ? acc : f[r] - acc;
+        y[r] = (MODE == 0) ? acc : (MODE == 1) ? f[r] - acc : -acc;
     }
 }
 

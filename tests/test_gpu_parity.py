@@ -161,6 +161,28 @@ def test_zero_guess_paths(name):
     assert np.isfinite(yo).all() and relmax(yo, ref) <= 1e-12
 
 
+def test_later_colour_residual_all_levels(monkeypatch):
+    """The residual after a zero-guess sweep as -(later-colour part of L) u (k_sell_spmv MODE 2),
+    forced onto every level (MGM_UPPER_RES_MIN=0; by default only levels >= 131072 rows use
+    it): V-cycle from the zero guess and MGM-GMRES equal the oracle's explicit f - L u path."""
+    import torch
+    from paper_2204_06154_b200 import MGM, mgm_apply
+
+    monkeypatch.setenv("MGM_UPPER_RES_MIN", "0")
+    P = pair("torus20000")
+    m = MGM(P.w.points, P.w.normals, P.w.stencil, P.w.levels)
+    n = P.ref.levels[0].N
+    v = _rand(n, 60)
+    y = torch.empty(n, dtype=torch.float64, device="cuda")
+    mgm_apply(m.ctx, 0, 7, torch.from_numpy(P.to_lib_order(0, v)).cuda(), None, y)
+    assert relmax(P.to_oracle_order(0, y.cpu().numpy()), P.ref.vcycle_level_order(v, np.zeros(n))) <= 1e-12
+    x, rep = m.solve(torch.from_numpy(P.w.rhs).cuda(), tol=1e-10, krylov=1)
+    xr, rr = P.ref.solve(P.w.rhs, tol=1e-10, krylov=1)
+    assert rep.converged and abs(rep.iterations - rr.iterations) <= 1
+    assert np.linalg.norm(x.cpu().numpy() - xr) / np.linalg.norm(xr) <= 1e-9
+    m.close()
+
+
 def test_device_gmres_equals_host_loop(monkeypatch):
     """The device-side GMRES (WHILE graph node per restart cycle, Givens on the device) and the
     host-driven loop run the same arithmetic: same iteration count, residual histories equal to
