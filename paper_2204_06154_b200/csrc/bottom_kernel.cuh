@@ -35,6 +35,7 @@
 //   BP_ADD   y[r] += acc                                   (e_j += P_j e_{j+1})
 //   BP_MV    y[r] = acc                                    (coarsest: e_p = L_p^{-1} r_p)
 //   BP_STORE g[r] = y[r]                                   (e_J back to HBM)
+//   BP_LOAD  y[r] = x[r] (own copy, all rows)              (after a grid-wide coarse solve)
 // Synchronisation between phases:
 //   * local -> local: __syncthreads (CTA 0 only);
 //   * DATA-SYNCHRONISED phases (mb >= 0: GS / ADD / MV of a cluster level whose output is a
@@ -62,7 +63,7 @@
 
 namespace mgm {
 
-enum : int { BP_ZERO = 0, BP_GS = 1, BP_RES = 2, BP_MVZ = 3, BP_ADD = 4, BP_MV = 5, BP_STORE = 6 };
+enum : int { BP_ZERO = 0, BP_GS = 1, BP_RES = 2, BP_MVZ = 3, BP_ADD = 4, BP_MV = 5, BP_STORE = 6, BP_LOAD = 7 };
 constexpr int BOT_THREADS = 512;
 constexpr int BOT_MAX_PHASES = 1024;
 constexpr int BOT_FRAG = 9;  // max operator entries per thread held in registers
@@ -157,7 +158,7 @@ struct BFrag {
 template <int TPR>
 __device__ __forceinline__ void bfrag_load(BFrag& fr, const BPhase& P, int row, int lane, uint64_t pol) {
     constexpr int CH = bot_ch(TPR);
-    const bool live = row < P.r1 && P.op != BP_ZERO && P.op != BP_STORE;  // no operator
+    const bool live = row < P.r1 && P.op != BP_ZERO && P.op != BP_STORE && P.op != BP_LOAD;  // no operator
     const int64_t base = (int64_t)row * P.W;
 #pragma unroll
     for (int q = 0; q < CH; ++q) {
@@ -346,6 +347,9 @@ __global__ void __launch_bounds__(BOT_THREADS, 1)
         } else if (P.op == BP_STORE) {  // copy back to HBM, split over the cluster
             const double* y = reinterpret_cast<const double*>(smem + P.yo);
             for (int r = P.r0 + g_cl; r < P.r1; r += nthr_cl) P.y[r] = y[r];
+        } else if (P.op == BP_LOAD) {  // every CTA fills its own copy from HBM
+            double* y = reinterpret_cast<double*>(smem + P.yo);
+            for (int r = P.r0 + threadIdx.x; r < P.r1; r += BOT_THREADS) y[r] = P.x[r];
         } else if (!P.local || rank == 0) {
             bottom_phase_any(P, fr, P.local ? (int)threadIdx.x : g_cl, P.local ? BOT_THREADS : nthr_cl, smem, sbase,
                              cs, pol, tr, mbar);
@@ -358,7 +362,7 @@ __global__ void __launch_bounds__(BOT_THREADS, 1)
         if (P.mb < 0 && !ll) {
             // zeroing / plain remote stores (generic proxy) before later st.async writes to the
             // same words
-            if (P.op == BP_ZERO || P.op == BP_MVZ || P.local)
+            if (P.op == BP_ZERO || P.op == BP_MVZ || P.op == BP_LOAD || P.local)
                 asm volatile("fence.proxy.async.shared::cluster;" ::: "memory");
             cluster_arrive();
         }
@@ -380,6 +384,31 @@ __global__ void __launch_bounds__(BOT_THREADS, 1)
     }
     cluster_arrive();  // no CTA exits while others may still store into its shared memory
     cluster_wait();
+}
+
+// y = A x for a dense row-major m x m A (the explicit coarsest inverse when the coarsest level
+// is large, e.g. cfg5's 4096 rows = 134 MB: a grid-wide GEMV between the two halves of the
+// bottom instead of the cluster's 16 SMs).  One warp per row, fixed reduction order.
+__global__ void __launch_bounds__(128) k_dense_gemv(int m, const double* __restrict__ A, const double* __restrict__ x,
+                                                    double* __restrict__ y) {
+    pdl_trigger();
+    const int row = blockIdx.x * 4 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    pdl_wait();
+    if (row >= m) return;
+    const double* a = A + (int64_t)row * m;
+    double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
+    int c = lane;
+    for (; c + 96 < m; c += 128) {
+        acc0 = fma(a[c], x[c], acc0);
+        acc1 = fma(a[c + 32], x[c + 32], acc1);
+        acc2 = fma(a[c + 64], x[c + 64], acc2);
+        acc3 = fma(a[c + 96], x[c + 96], acc3);
+    }
+    for (; c < m; c += 32) acc0 = fma(a[c], x[c], acc0);
+    double acc = (acc0 + acc1) + (acc2 + acc3);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) y[row] = acc;
 }
 
 // the two instances (the host picks by MGM_TRACE)

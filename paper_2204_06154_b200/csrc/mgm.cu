@@ -174,6 +174,9 @@ struct mgm_ctx {
     size_t bot_smem = 0;
     int nphases = 0;
     int bot_arm0 = 0, bot_arm1 = 0;  // bytes of the first two data-synchronised phases
+    int bot_arm0b = 0, bot_arm1b = 0;  // ... of the second launch when split
+    int bot_split = 0;                 // > 0: phases of the first launch; the coarse solve is a GEMV
+    const double* bot_ainv = nullptr;  // the coarsest inverse (row-major) for that GEMV
     BPhase* d_phases = nullptr;
     std::vector<void*> bot_mem;
     i64 vcycle_kernels = 0;
@@ -597,7 +600,21 @@ void setup_bottom(mgm_ctx* ctx, const std::vector<double>& LU, const std::vector
         add(BP_RES, is_local(j), 0, L.n, &EL[j], ou[j], nullptr, -1, L.t, L.f, -1, nullptr);
         add(BP_MVZ, is_local(j), 0, Ln.n, &ER[j], -1, L.t, -1, Ln.f, nullptr, ou[j + 1], nullptr);
     }
-    {  // line 10
+    // a large coarsest level (cfg5: 4096 rows, a 134 MB dense inverse) is solved by a
+    // grid-wide GEMV between two launches of the bottom kernel: the first stores the
+    // iterates e_J..e_{p-2} to HBM, the second loads them (and e_p) back
+    i64 gemv_min = 1024;
+    if (const char* e = std::getenv("MGM_BOT_GEMV_MIN")) gemv_min = std::atoll(e);
+    const bool split = m >= gemv_min && J < p - 1;
+    size_t qa = 0;  // phases of the first launch
+    if (split) {
+        for (int j = J; j + 1 < p; ++j)
+            add(BP_STORE, false, 0, ctx->lv[j].n, nullptr, -1, nullptr, ou[j], ctx->lv[j].u, nullptr, -1, nullptr);
+        qa = ph.size();
+        add(BP_LOAD, false, 0, m, nullptr, -1, ctx->lv[p - 1].u, ou[p - 1], nullptr, nullptr, -1, nullptr);
+        for (int j = J; j + 1 < p; ++j)
+            add(BP_LOAD, false, 0, ctx->lv[j].n, nullptr, -1, ctx->lv[j].u, ou[j], nullptr, nullptr, -1, nullptr);
+    } else {  // line 10
         Level& C = ctx->lv[p - 1];
         add(BP_MV, is_local(p - 1), 0, m, &EC, -1, C.f, ou[p - 1], nullptr, nullptr, -1, nullptr);
     }
@@ -609,19 +626,30 @@ void setup_bottom(mgm_ctx* ctx, const std::vector<double>& LU, const std::vector
     add(BP_STORE, false, 0, ctx->lv[J].n, nullptr, -1, nullptr, ou[J], ctx->lv[J].u, nullptr, -1, nullptr);
     // data-synchronised phases (bottom_kernel.cuh): cluster GS / ADD / MV phases whose output
     // is a replicated vector; every CTA receives 8 bytes per row of such a phase
+    // (numbered per launch: each launch initialises its own mbarriers)
     const bool mbar_on = std::getenv("MGM_BOT_NO_MBAR") == nullptr;
-    std::vector<int> mbq;
-    for (size_t q = 0; q + 1 < ph.size(); ++q) {
-        BPhase& P = ph[q];
-        if (mbar_on && !P.local && P.yo >= 0 && (P.op == BP_GS || P.op == BP_ADD || P.op == BP_MV)) {
-            P.mb = (int)mbq.size();
-            mbq.push_back((int)q);
+    auto number = [&](size_t q0, size_t q1, int& arm0, int& arm1) {
+        std::vector<int> mbq;
+        for (size_t q = q0; q + 1 < q1; ++q) {
+            BPhase& P = ph[q];
+            if (mbar_on && !P.local && P.yo >= 0 && (P.op == BP_GS || P.op == BP_ADD || P.op == BP_MV)) {
+                P.mb = (int)mbq.size();
+                mbq.push_back((int)q);
+            }
         }
+        auto mbytes = [&](size_t k) { return 8 * (ph[(size_t)mbq[k]].r1 - ph[(size_t)mbq[k]].r0); };
+        for (size_t k = 0; k + 2 < mbq.size(); ++k) ph[(size_t)mbq[k]].arm = mbytes(k + 2);
+        arm0 = mbq.size() > 0 ? mbytes(0) : 0;
+        arm1 = mbq.size() > 1 ? mbytes(1) : 0;
+    };
+    if (split) {
+        number(0, qa, ctx->bot_arm0, ctx->bot_arm1);
+        number(qa, ph.size(), ctx->bot_arm0b, ctx->bot_arm1b);
+    } else {
+        number(0, ph.size(), ctx->bot_arm0, ctx->bot_arm1);
     }
-    auto mbytes = [&](size_t k) { return 8 * (ph[(size_t)mbq[k]].r1 - ph[(size_t)mbq[k]].r0); };
-    for (size_t k = 0; k + 2 < mbq.size(); ++k) ph[(size_t)mbq[k]].arm = mbytes(k + 2);
-    ctx->bot_arm0 = mbq.size() > 0 ? mbytes(0) : 0;
-    ctx->bot_arm1 = mbq.size() > 1 ? mbytes(1) : 0;
+    ctx->bot_split = split ? (int)qa : 0;
+    ctx->bot_ainv = split ? EC.val : nullptr;
     if ((int)ph.size() * sizeof(BPhase) > table) return;
     ctx->d_phases = bot_upload(ctx, ph, ok);
     if (!ok) return;
@@ -1602,15 +1630,27 @@ void enqueue_vcycle(mgm_ctx* ctx, cudaStream_t st) {
         cfg.numAttrs = g_use_pdl ? 2 : 1;
         cfg.dynamicSmemBytes = ctx->bot_smem;
         const PfList pf = pf_take(ctx, ctx->pf_l0only ? Regions{} : ctx->bot_pf, !ctx->pf_l0only, ctx->pf_bot_budget);
-        if (!g_dry)
+        auto bottom = [&](int q0, int nph, int arm0, int arm1, PfList pfl) {
+            if (g_dry) return;
+            const BPhase* ph = (const BPhase*)ctx->d_phases + q0;
             note_launch(ctx->d_trace
-                            ? cudaLaunchKernelEx(&cfg, k_vcycle_bottom_t<true>, (const BPhase*)ctx->d_phases,
-                                                 ctx->nphases, ctx->d_trace + 256, pf, ctx->bot_arm0, ctx->bot_arm1)
-                            : cudaLaunchKernelEx(&cfg, k_vcycle_bottom_t<false>, (const BPhase*)ctx->d_phases,
-                                                 ctx->nphases, (unsigned long long*)nullptr, pf, ctx->bot_arm0,
-                                                 ctx->bot_arm1),
+                            ? cudaLaunchKernelEx(&cfg, k_vcycle_bottom_t<true>, ph, nph, ctx->d_trace + 256, pfl, arm0,
+                                                 arm1)
+                            : cudaLaunchKernelEx(&cfg, k_vcycle_bottom_t<false>, ph, nph,
+                                                 (unsigned long long*)nullptr, pfl, arm0, arm1),
                         ctx->bot_cluster, BOT_THREADS, ctx->bot_smem);
-        ctx->vcycle_kernels++;
+            ctx->vcycle_kernels++;
+        };
+        if (ctx->bot_split > 0) {  // down half, grid-wide coarse GEMV, up half
+            bottom(0, ctx->bot_split, ctx->bot_arm0, ctx->bot_arm1, pf);
+            const int m = ctx->nc;
+            launch(ctx->pdl, k_dense_gemv, (unsigned)((m + 3) / 4), 128, 0, st, m, ctx->bot_ainv,
+                   (const double*)lv[p - 1].f, lv[p - 1].u);
+            if (!g_dry) ctx->vcycle_kernels++;
+            bottom(ctx->bot_split, ctx->nphases - ctx->bot_split, ctx->bot_arm0b, ctx->bot_arm1b, PfList{nullptr, 0, 0});
+        } else {
+            bottom(0, ctx->nphases, ctx->bot_arm0, ctx->bot_arm1, pf);
+        }
     } else {
         enqueue_coarse(ctx, lv[p - 1].f, lv[p - 1].u, st);                 // line 10
     }

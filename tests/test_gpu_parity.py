@@ -296,13 +296,15 @@ def test_error_paths():
 
 @pytest.mark.parametrize("name", ["cfg1", "torus20000", "gfd9000"])
 @pytest.mark.parametrize("knobs", [{}, {"MGM_BOT_MAX": "100000000", "MGM_BOT_LOCAL": "0"},
-                                   {"MGM_BOT_MAX": "100000000", "MGM_BOT_LOCAL": "100000000"}])
+                                   {"MGM_BOT_MAX": "100000000", "MGM_BOT_LOCAL": "100000000"},
+                                   {"MGM_BOT_MAX": "100000000", "MGM_BOT_GEMV_MIN": "1"}])
 def test_bottom_kernel_equals_kernel_path(name, knobs, monkeypatch):
     """The one-kernel cluster bottom of the V-cycle (bottom_kernel.cuh, levels J..p-1) computes
     the same V-cycle as one kernel per colour / operator (MGM_BOT_MAX=0), to rounding: the
     coarsest solve uses the explicit inverse instead of the LU substitution (O13),
     and row sums are split over threads differently.  Variants: the default split, everything
-    below level 0 in cluster phases, and everything below level 0 on one CTA."""
+    below level 0 in cluster phases, everything below level 0 on one CTA, and the coarse
+    solve as a grid-wide GEMV between two launches (the path for large coarsest levels)."""
     import torch
     from paper_2204_06154_b200 import MGM
 
