@@ -90,6 +90,8 @@ struct Level {
     i32* slw = nullptr;                 // per slice: slots read by a sweep from a zero guess (pack_sell)
     uint8_t* nlow = nullptr;            // per row: its earlier-colour entries (slots 1..nlow)
     i32* sluw = nullptr;                // per slice: first later-colour slot of its rows (min 1 + nlow)
+    i32* l2m = nullptr;                 // lib row -> Morton index (residual written in Morton order)
+    i32* rcol_m = nullptr;              // R_j columns as fine Morton indices (same values / layout as rcol)
     std::vector<i64> lower_per_colour;  // per colour: stored entries such a sweep reads (diag + earlier colours)
     int tpr = 1, rtpr = 1;  // threads per row for L_j (colour sweeps) and R_j kernels
     int stpr = 1;           // threads per row for full-level SpMV / residual on L_j
@@ -160,6 +162,8 @@ struct mgm_ctx {
     cudaGraphExec_t vgraph0 = nullptr;  // the same V-cycle from a zero guess on level 0 (Krylov preconditioner)
     bool vc_zero_guess = false;         // set while enqueueing vgraph0
     bool no_zg = false;                 // MGM_NO_ZG: no zero-guess sweeps (comparison)
+    i64 morton_t_min = 8388608;         // levels with at least this many rows write the residual in
+                                        // Morton order (MGM_MORTON_T_MIN)
     i64 upper_res_min = 131072;         // levels with at least this many rows use the later-colour
                                         // residual after a zero-guess sweep (MGM_UPPER_RES_MIN)
     bool pdl = false;  // set while enqueueing the V-cycle (PDL launches)
@@ -437,7 +441,7 @@ void setup_bottom(mgm_ctx* ctx, const std::vector<double>& LU, const std::vector
     size_t table = 0;
     for (int j = 1; j < p; ++j) {
         if (ctx->lv[j].n > bmax) continue;
-        i64 nph = 3, vb = 0;
+        i64 nph = 3 + 2 * (p - j) + 2, vb = 0;  // (+ the STORE / LOAD phases of a split bottom)
         for (int q = j; q < p; ++q) {
             vb += ctx->lv[q].n * (i64)sizeof(double);
             if (q + 1 < p) nph += (i64)(ctx->lp.nu1 + ctx->lp.nu2) * ctx->lv[q].ncol + 3;
@@ -1070,6 +1074,16 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
             std::vector<double> rval;
             pack_sell(R, lib2mor[j + 1], mor2lib[j], false, rptr, rcol, rval, nullptr);
             L.r_stored = (i64)rval.size();
+            {  // the same R with Morton columns (same entry order, so the same sums)
+                std::vector<i32> ident(n), l2m(n);
+                for (i64 r = 0; r < n; ++r) ident[(size_t)r] = (i32)r;
+                for (i64 r = 0; r < n; ++r) l2m[(size_t)r] = (i32)lib2mor[j][(size_t)r];
+                std::vector<i64> rptr2;
+                std::vector<i32> rcol2;
+                std::vector<double> rval2;
+                pack_sell(R, lib2mor[j + 1], ident, false, rptr2, rcol2, rval2, nullptr);
+                if ((s = upload(ctx, &L.rcol_m, rcol2)) || (s = upload(ctx, &L.l2m, l2m))) return s;
+            }
             {
                 i64 nn = Lm[j + 1].nrows;
                 double wavg = (double)L.r_stored / (double)std::max<i64>(1, (nn + 31) / 32 * 32);
@@ -1277,12 +1291,13 @@ void launch_gs(bool pdl, bool poisson, int tpr, int r0, int r1, int span, const 
 // (MODE 2 reads the level's later-colour slot tables g_sluw / g_nlow, set by enqueue_residual)
 static thread_local const int* g_sluw = nullptr;
 static thread_local const uint8_t* g_nlow = nullptr;
+static thread_local const int* g_yperm = nullptr;  // residual output permutation (enqueue_residual)
 template <int MODE, bool P, int TPR>
 void spmv_launch_t(bool pdl, i64 r0, i64 r1, i64 nl, const i64* sptr, const i32* scol, const double* sval,
                    const double* x, const double* f, double* y, const double* c, cudaStream_t st, PfList pf) {
     launch(pdl, k_sell_spmv<MODE, P, TPR, CHUNK>, blocks_for((r1 - (r0 & ~31)) * TPR, 256), 256, 0, st, (int)r0,
            (int)r1, (int)nl, sptr, scol, sval, x, f, y, c, pf, MODE == 2 ? g_sluw : (const int*)nullptr,
-           MODE == 2 ? g_nlow : (const uint8_t*)nullptr);
+           MODE == 2 ? g_nlow : (const uint8_t*)nullptr, MODE != 0 ? g_yperm : (const int*)nullptr);
 }
 template <int MODE, bool P>
 void spmv_launch_p(bool pdl, int tpr, i64 r0, i64 r1, i64 nl, const i64* sptr, const i32* scol, const double* sval,
@@ -1487,9 +1502,13 @@ void enqueue_spmv(mgm_ctx* ctx, int j, const double* x, double* y, cudaStream_t 
 
 // t = f - L u (level j), Poisson: t[n] = f[n] - c.u.  after_zg: u is the result of ONE forward
 // sweep from a zero guess, so t = -(later-colour part of L) u (k_sell_spmv MODE 2)
+// morton_t: write t in the level's Morton order (the restriction then gathers with Morton
+// columns, a few sectors per coarse row instead of one per fine entry; not on split levels)
 void enqueue_residual(mgm_ctx* ctx, int j, const double* f, const double* u, double* t, cudaStream_t st,
-                      bool after_zg = false) {
+                      bool after_zg = false, bool morton_t = false) {
     Level& L = ctx->lv[j];
+    g_yperm = (morton_t && L.l2m) ? L.l2m : nullptr;
+    struct ResetP { ~ResetP() { g_yperm = nullptr; } } resetp_;
     // (bandwidth-bound levels only: on the small latency-bound levels the extra per-row table
     // loads cost more than the skipped entries save -- cfg3 L2/L3 17 -> 23 us)
     const int mode = (after_zg && L.sluw && !ctx->poisson && !ctx->no_zg && L.n >= ctx->upper_res_min) ? 2 : 1;
@@ -1507,14 +1526,15 @@ void enqueue_residual(mgm_ctx* ctx, int j, const double* f, const double* u, dou
 }
 
 // y (next level) = R_j x
-void enqueue_restrict(mgm_ctx* ctx, int j, const double* x, double* y, cudaStream_t st) {
+void enqueue_restrict(mgm_ctx* ctx, int j, const double* x, double* y, cudaStream_t st, bool morton_x = false) {
     Level& L = ctx->lv[j];
     Level& Ln = ctx->lv[j + 1];
+    const i32* rcol = (morton_x && L.rcol_m) ? L.rcol_m : L.rcol;
     for_my_pieces(ctx, j, 0, Ln.n, [&](i64 a, i64 b) {
         Regions rg;
         if (!ctx->pf_l0only) pf_sell(rg, L.h_rptr, L.rcol, L.rval, a, b);
         const PfList pf = pf_take(ctx, rg, !ctx->pf_l0only);
-        launch_spmv(ctx->pdl, 0, false, L.rtpr, a, b, Ln.n, L.rptr, L.rcol, L.rval, x, nullptr, y, nullptr, st, pf);
+        launch_spmv(ctx->pdl, 0, false, L.rtpr, a, b, Ln.n, L.rptr, rcol, L.rval, x, nullptr, y, nullptr, st, pf);
         ctx->vcycle_kernels++;
     });
     dist_exchange(ctx, j, y, 0, Ln.n, st);
@@ -1546,6 +1566,11 @@ void enqueue_interp_correct(mgm_ctx* ctx, int j, const double* ec, double* e, cu
 
 void enqueue_coarse(mgm_ctx* ctx, const double* r, double* e, cudaStream_t st) {
     const int m = ctx->nc;
+    if (m >= 1024 && ctx->ainv) {  // large coarsest: grid-wide GEMV with the explicit inverse (O13)
+        launch(ctx->pdl, k_dense_gemv, (unsigned)((m + 3) / 4), 128, 0, st, m, (const double*)ctx->ainv, r, e);
+        ctx->vcycle_kernels++;
+        return;
+    }
     const int in_smem = (size_t)(m + m * m) * sizeof(double) <= 200 * 1024 ? 1 : 0;
     const size_t smem = sizeof(double) * (m + (in_smem ? (size_t)m * m : 0));
     set_max_dyn_smem((const void*)k_coarse_solve);
@@ -1598,9 +1623,12 @@ void enqueue_vcycle(mgm_ctx* ctx, cudaStream_t st) {
     // the diagonal and earlier-colour entries (k_gs_colour ZG)
     for (int s = 0; s < nu1; ++s) enqueue_sweep(ctx, 0, pre_b, st, s == 0 && ctx->vc_zero_guess);  // line 4
     stamp(ctx, "presmooth", 0, st);
-    enqueue_residual(ctx, 0, lv[0].f, lv[0].u, lv[0].t, st, ctx->vc_zero_guess && nu1 == 1);  // line 5
+    // residual in Morton order for the restriction's gathers: levels whose t does not stay in L2
+    // (cfg3: restrict L0 30.4 -> 26.7 us but residual 80 -> 85 us, no net gain)
+    const bool mt0 = !dist_level(ctx, 0) && lv[0].n >= ctx->morton_t_min;
+    enqueue_residual(ctx, 0, lv[0].f, lv[0].u, lv[0].t, st, ctx->vc_zero_guess && nu1 == 1, mt0);  // line 5
     stamp(ctx, "residual", 0, st);
-    enqueue_restrict(ctx, 0, lv[0].t, lv[1].f, st);
+    enqueue_restrict(ctx, 0, lv[0].t, lv[1].f, st, mt0);
     stamp(ctx, "restrict", 0, st);
     for (int j = 1; j < D; ++j) {                                         // lines 6-9
         // e_j = 0 then presmooth; the first forward sweep from the zero guess writes every row
@@ -1609,8 +1637,9 @@ void enqueue_vcycle(mgm_ctx* ctx, cudaStream_t st) {
         if (!zg) enqueue_zero(ctx, lv[j].u, lv[j].n + pad, st);
         for (int s = 0; s < nu1; ++s) enqueue_sweep(ctx, j, pre_b, st, s == 0 && zg);
         stamp(ctx, "zero+presmooth", j, st);
-        enqueue_residual(ctx, j, lv[j].f, lv[j].u, lv[j].t, st, zg && nu1 == 1);
-        enqueue_restrict(ctx, j, lv[j].t, lv[j + 1].f, st);
+        const bool mt = !dist_level(ctx, j) && lv[j].n >= ctx->morton_t_min;
+        enqueue_residual(ctx, j, lv[j].f, lv[j].u, lv[j].t, st, zg && nu1 == 1, mt);
+        enqueue_restrict(ctx, j, lv[j].t, lv[j + 1].f, st, mt);
         stamp(ctx, "residual+restrict", j, st);
     }
     }
@@ -2439,6 +2468,7 @@ mgm_status mgm_setup(const double* points, const double* normals, int64_t n_poin
     if (const char* e = std::getenv("MGM_PF_CAP_MB")) ctx->pf_cap = (i64)std::max(0, std::atoi(e)) << 20;
     if (std::getenv("MGM_NO_ZG")) ctx->no_zg = true;
     if (const char* e = std::getenv("MGM_UPPER_RES_MIN")) ctx->upper_res_min = std::atoll(e);
+    if (const char* e = std::getenv("MGM_MORTON_T_MIN")) ctx->morton_t_min = std::atoll(e);
     if (std::getenv("MGM_PF_LATE")) ctx->pf_late = 1;
     if (std::getenv("MGM_PF_NOF")) ctx->pf_nof = 1;
     if (std::getenv("MGM_PF_L0ONLY")) ctx->pf_l0only = 1;
@@ -2608,7 +2638,7 @@ mgm_status mgm_destroy(mgm_ctx* ctx) {
     for (auto& L : ctx->lv) {
         for (void* ptr : {(void*)L.sptr, (void*)L.scol, (void*)L.sval, (void*)L.pcol, (void*)L.pval, (void*)L.rptr,
                           (void*)L.rcol, (void*)L.rval, (void*)L.u, (void*)L.f, (void*)L.t, (void*)L.c, (void*)L.slw,
-                          (void*)L.nlow, (void*)L.sluw})
+                          (void*)L.nlow, (void*)L.sluw, (void*)L.l2m, (void*)L.rcol_m})
             if (ptr) cudaFree(ptr);
     }
     for (void* ptr : {(void*)ctx->lu, (void*)ctx->piv, (void*)ctx->d_lib2orig, (void*)ctx->V, (void*)ctx->w,

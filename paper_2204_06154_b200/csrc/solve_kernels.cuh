@@ -265,7 +265,8 @@ __global__ void __launch_bounds__(256) k_sell_spmv(int r0, int r1, int nl, const
                                                    double* __restrict__ y,
                                                    const double* __restrict__ c, PfList pf,
                                                    const int* __restrict__ sluw = nullptr,
-                                                   const uint8_t* __restrict__ nlow = nullptr) {
+                                                   const uint8_t* __restrict__ nlow = nullptr,
+                                                   const int* __restrict__ yperm = nullptr) {
     pdl_trigger();
     l2_prefetch_share(pf);
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
@@ -273,9 +274,10 @@ __global__ void __launch_bounds__(256) k_sell_spmv(int r0, int r1, int nl, const
     const int part = g % TPR;
     const bool live = r >= r0 && r < r1;
     RowFrag<TPR, CH> fr;
-    int w = 0, k1 = part, lim = 0;
+    int w = 0, k1 = part, lim = 0, yr = r;
     int64_t base = 0;
     if (live) {
+        if (yperm) yr = yperm[r];  // output position (the residual in Morton order for the restriction)
         const int64_t s0 = sptr[r >> 5];
         w = (int)((sptr[(r >> 5) + 1] - s0) >> 5);
         base = s0 + (r & 31);
@@ -306,7 +308,7 @@ __global__ void __launch_bounds__(256) k_sell_spmv(int r0, int r1, int nl, const
     acc = group_sum<TPR>(acc);
     if (live && part == 0) {
         if (POISSON) acc += c[r] * x[nl];
-        y[r] = (MODE == 0) ? acc : (MODE == 1) ? f[r] - acc : -acc;
+        y[yr] = (MODE == 0) ? acc : (MODE == 1) ? f[r] - acc : -acc;
     }
 }
 

@@ -169,6 +169,7 @@ def test_later_colour_residual_all_levels(monkeypatch):
     from paper_2204_06154_b200 import MGM, mgm_apply
 
     monkeypatch.setenv("MGM_UPPER_RES_MIN", "0")
+    monkeypatch.setenv("MGM_MORTON_T_MIN", "0")   # (and the Morton-order residual for the restriction)
     P = pair("torus20000")
     m = MGM(P.w.points, P.w.normals, P.w.stencil, P.w.levels)
     n = P.ref.levels[0].N
