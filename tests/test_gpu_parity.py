@@ -184,6 +184,35 @@ def test_later_colour_residual_all_levels(monkeypatch):
     m.close()
 
 
+@pytest.mark.parametrize("bot_max", ["0", "100000000"])
+def test_large_coarsest_gemv(bot_max, monkeypatch):
+    """A coarsest level >= 1024 rows is solved by the grid-wide dense GEMV with the explicit
+    inverse (per-kernel path: enqueue_coarse; bottom kernel: split into two launches around
+    it).  Three-level hierarchy on the cfg1 sphere recipe at N = 16384 (coarsest 1024): V-cycle
+    vs the oracle's LU-based V-cycle to 1e-12 and the GMRES solve."""
+    import torch
+    from paper_2204_06154_b200 import MGM
+    import oracle as O
+
+    monkeypatch.setenv("MGM_BOT_MAX", bot_max)
+    w = MI.make_workload(1, n=16384)
+    lv = dict(w.levels, num_levels=3)
+    m = MGM(w.points, w.normals, w.stencil, lv)
+    ref = O.Oracle(w.points, w.normals, w.stencil, lv)
+    assert ref.levels[-1].N == 1024
+    n = len(w.points)
+    f = _rand(n, 70)
+    u0 = _rand(n, 71)
+    u = torch.from_numpy(u0.copy()).cuda()
+    m.vcycle(torch.from_numpy(f).cuda(), u)
+    assert relmax(u.cpu().numpy(), ref.vcycle(f, u0)) <= 1e-12
+    x, rep = m.solve(torch.from_numpy(w.rhs).cuda(), tol=1e-10)
+    xr, rr = ref.solve(w.rhs, tol=1e-10)
+    assert rep.converged and abs(rep.iterations - rr.iterations) <= 1
+    assert np.linalg.norm(x.cpu().numpy() - xr) / np.linalg.norm(xr) <= 1e-9
+    m.close()
+
+
 def test_device_gmres_equals_host_loop(monkeypatch):
     """The device-side GMRES (WHILE graph node per restart cycle, Givens on the device) and the
     host-driven loop run the same arithmetic: same iteration count, residual histories equal to
