@@ -162,8 +162,9 @@ struct mgm_ctx {
     cudaGraphExec_t vgraph0 = nullptr;  // the same V-cycle from a zero guess on level 0 (Krylov preconditioner)
     bool vc_zero_guess = false;         // set while enqueueing vgraph0
     bool no_zg = false;                 // MGM_NO_ZG: no zero-guess sweeps (comparison)
-    i64 morton_t_min = 8388608;         // levels with at least this many rows write the residual in
-                                        // Morton order (MGM_MORTON_T_MIN)
+    i64 morton_t_min = (i64)1 << 62;    // levels with at least this many rows write the residual in
+                                        // Morton order (MGM_MORTON_T_MIN; off: no gain measured at
+                                        // cfg3 or cfg5)
     i64 upper_res_min = 131072;         // levels with at least this many rows use the later-colour
                                         // residual after a zero-guess sweep (MGM_UPPER_RES_MIN)
     bool pdl = false;  // set while enqueueing the V-cycle (PDL launches)
@@ -1623,8 +1624,8 @@ void enqueue_vcycle(mgm_ctx* ctx, cudaStream_t st) {
     // the diagonal and earlier-colour entries (k_gs_colour ZG)
     for (int s = 0; s < nu1; ++s) enqueue_sweep(ctx, 0, pre_b, st, s == 0 && ctx->vc_zero_guess);  // line 4
     stamp(ctx, "presmooth", 0, st);
-    // residual in Morton order for the restriction's gathers: levels whose t does not stay in L2
-    // (cfg3: restrict L0 30.4 -> 26.7 us but residual 80 -> 85 us, no net gain)
+    // residual in Morton order for the restriction's gathers (opt-in: cfg3 restrict L0 30.4 ->
+    // 26.7 us but residual 80 -> 85 us; cfg5 solve 206.6 vs 205.2 ms without)
     const bool mt0 = !dist_level(ctx, 0) && lv[0].n >= ctx->morton_t_min;
     enqueue_residual(ctx, 0, lv[0].f, lv[0].u, lv[0].t, st, ctx->vc_zero_guess && nu1 == 1, mt0);  // line 5
     stamp(ctx, "residual", 0, st);
