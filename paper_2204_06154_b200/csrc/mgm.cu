@@ -2012,21 +2012,27 @@ static mgm_status build_gmres_graph(mgm_ctx* ctx) {
     cudaGraph_t body = cp.conditional.phGraph_out[0];
     CK(cudaStreamBeginCaptureToGraph(st, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
     g_launch_err.clear();
-    k_copy_col<<<RED_BLOCKS, 256, 0, st>>>(n, V, ld, kdev, ctx->lv[0].f);  // f_0 = V_k
+    // every node with programmatic serialisation (PDL): each kernel waits for its predecessor
+    // with griddepcontrol.wait, and its launch overlaps the predecessor's tail
+    launch(true, k_copy_col, RED_BLOCKS, 256, 0, st, n, (const double*)V, ld, kdev, ctx->lv[0].f);  // f_0 = V_k
     const bool zg = zg_capable(ctx);
     if (!zg) cudaMemsetAsync(ctx->lv[0].u, 0, sizeof(double) * n, st);
     ctx->vc_zero_guess = zg;
     enqueue_vcycle(ctx, st);                                              // u = M V_k
     ctx->vc_zero_guess = false;
+    ctx->pdl = true;
     enqueue_apply_A(ctx, ctx->lv[0].u, w, st);                            // w = A M V_k
+    ctx->pdl = false;
     // CGS2: h1 = V^T w; w -= V h1; h2 = V^T w (h1 += h2); w -= V h2, ||w||^2
-    k_multidot_fin<<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, V, ld, 0, w, ctx->partials, ctx->tickets, h1,
-                                                       (double*)nullptr, kdev);
-    k_multiaxpy<<<RED_BLOCKS * 2, 256, 0, st>>>(n, V, ld, 0, h1, w, kdev);
-    k_multidot_fin<<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, V, ld, 0, w, ctx->partials, ctx->tickets, h2, h1, kdev);
-    k_multiaxpy_norm<<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, V, ld, 0, h2, w, ctx->partials, ctx->tickets, nr, kdev);
-    k_scale_col<<<RED_BLOCKS, 256, 0, st>>>(n, w, nr, V, ld, kdev);         // V_{k+1}
-    k_gmres_givens<<<1, 32, 0, st>>>(G, h1, nr, cond);
+    launch(true, k_multidot_fin, RED_BLOCKS, RED_THREADS, 0, st, n, (const double*)V, ld, 0, (const double*)w,
+           ctx->partials, ctx->tickets, h1, (double*)nullptr, kdev);
+    launch(true, k_multiaxpy, RED_BLOCKS * 2, 256, 0, st, n, (const double*)V, ld, 0, (const double*)h1, w, kdev);
+    launch(true, k_multidot_fin, RED_BLOCKS, RED_THREADS, 0, st, n, (const double*)V, ld, 0, (const double*)w,
+           ctx->partials, ctx->tickets, h2, h1, kdev);
+    launch(true, k_multiaxpy_norm, RED_BLOCKS, RED_THREADS, 0, st, n, (const double*)V, ld, 0, (const double*)h2, w,
+           ctx->partials, ctx->tickets, nr, kdev);
+    launch(true, k_scale_col, RED_BLOCKS, 256, 0, st, n, (const double*)w, (const double*)nr, V, ld, kdev);  // V_{k+1}
+    launch(true, k_gmres_givens, 1, 32, 0, st, G, (const double*)h1, (const double*)nr, cond);
     cudaGraph_t cap = nullptr;
     const cudaError_t ce = cudaStreamEndCapture(st, &cap);
     if (ce != cudaSuccess || !g_launch_err.empty()) {

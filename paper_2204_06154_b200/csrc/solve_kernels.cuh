@@ -504,6 +504,8 @@ __global__ void __launch_bounds__(RED_THREADS) k_multidot_fin(int64_t n, const d
                                                               int k1, const double* __restrict__ w,
                                                               double* __restrict__ partials, unsigned* ticket,
                                                               double* out, double* acc, const int* kdev = nullptr) {
+    pdl_trigger();  // (no-ops unless launched with programmatic serialisation: gmres_dev's graph)
+    pdl_wait();
     if (kdev) k1 = *kdev + 1;  // device-side GMRES: the Arnoldi step lives in device memory
     __shared__ double red[RED_THREADS / 32][MD_GROUP];
     const int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
@@ -541,6 +543,8 @@ __global__ void __launch_bounds__(RED_THREADS) k_multiaxpy_norm(int64_t n, const
                                                                 int k1, const double* __restrict__ h,
                                                                 double* __restrict__ w, double* __restrict__ partials,
                                                                 unsigned* ticket, double* nrm2, const int* kdev = nullptr) {
+    pdl_trigger();
+    pdl_wait();
     if (kdev) k1 = *kdev + 1;
     __shared__ double hs[256];
     __shared__ double red[RED_THREADS / 32];
@@ -580,6 +584,8 @@ __global__ void k_reduce_partials(const double* __restrict__ partials, int nblk,
 __global__ void __launch_bounds__(256) k_multiaxpy(int64_t n, const double* __restrict__ V,
                                                    int64_t ld, int k1, const double* __restrict__ h,
                                                    double* __restrict__ w, const int* kdev = nullptr) {
+    pdl_trigger();
+    pdl_wait();
     if (kdev) k1 = *kdev + 1;
     __shared__ double hs[256];
     for (int j = threadIdx.x; j < k1; j += blockDim.x) hs[j] = h[j];
@@ -626,6 +632,8 @@ __device__ __forceinline__ double* gmd_hist(const GmresDev& G) { return gmd_g(G)
 // dst = V_k (k = gi[0]): the Arnoldi vector to precondition
 __global__ void k_copy_col(int64_t n, const double* __restrict__ V, int64_t ld, const int* __restrict__ kdev,
                            double* __restrict__ dst) {
+    pdl_trigger();
+    pdl_wait();
     const double* src = V + (int64_t)(*kdev) * ld;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         dst[i] = src[i];
@@ -633,6 +641,8 @@ __global__ void k_copy_col(int64_t n, const double* __restrict__ V, int64_t ld, 
 // V_{k+1} = w / sqrt(*nrm2)
 __global__ void k_scale_col(int64_t n, const double* __restrict__ w, const double* __restrict__ nrm2, double* V,
                             int64_t ld, const int* __restrict__ kdev) {
+    pdl_trigger();
+    pdl_wait();
     const double inv = 1.0 / sqrt(*nrm2);
     double* dst = V + (int64_t)(*kdev + 1) * ld;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -642,6 +652,8 @@ __global__ void k_scale_col(int64_t n, const double* __restrict__ w, const doubl
 // host loop), the relative residual history, and the loop condition.
 __global__ void k_gmres_givens(GmresDev G, const double* __restrict__ h, const double* __restrict__ nrm2,
                                cudaGraphConditionalHandle cond) {
+    pdl_trigger();
+    pdl_wait();
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     const int m = G.m;
     const int k = G.gi[0], k1 = k + 1;
