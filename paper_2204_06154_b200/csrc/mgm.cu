@@ -162,6 +162,7 @@ struct mgm_ctx {
     cudaGraphExec_t vgraph0 = nullptr;  // the same V-cycle from a zero guess on level 0 (Krylov preconditioner)
     bool vc_zero_guess = false;         // set while enqueueing vgraph0
     bool no_zg = false;                 // MGM_NO_ZG: no zero-guess sweeps (comparison)
+    bool no_c0_fuse = false;            // MGM_NO_C0_FUSE: colour 0 not fused into the restriction
     i64 morton_t_min = (i64)1 << 62;    // levels with at least this many rows write the residual in
                                         // Morton order (MGM_MORTON_T_MIN; off: no gain measured at
                                         // cfg3 or cfg5)
@@ -1293,12 +1294,14 @@ void launch_gs(bool pdl, bool poisson, int tpr, int r0, int r1, int span, const 
 static thread_local const int* g_sluw = nullptr;
 static thread_local const uint8_t* g_nlow = nullptr;
 static thread_local const int* g_yperm = nullptr;  // residual output permutation (enqueue_residual)
+static thread_local C0Fuse g_c0 = C0Fuse{nullptr, nullptr, nullptr, 0};  // restriction + colour 0 (enqueue_restrict)
 template <int MODE, bool P, int TPR>
 void spmv_launch_t(bool pdl, i64 r0, i64 r1, i64 nl, const i64* sptr, const i32* scol, const double* sval,
                    const double* x, const double* f, double* y, const double* c, cudaStream_t st, PfList pf) {
     launch(pdl, k_sell_spmv<MODE, P, TPR, CHUNK>, blocks_for((r1 - (r0 & ~31)) * TPR, 256), 256, 0, st, (int)r0,
            (int)r1, (int)nl, sptr, scol, sval, x, f, y, c, pf, MODE == 2 ? g_sluw : (const int*)nullptr,
-           MODE == 2 ? g_nlow : (const uint8_t*)nullptr, MODE != 0 ? g_yperm : (const int*)nullptr);
+           MODE == 2 ? g_nlow : (const uint8_t*)nullptr, MODE != 0 ? g_yperm : (const int*)nullptr,
+           MODE == 0 ? g_c0 : C0Fuse{nullptr, nullptr, nullptr, 0});
 }
 template <int MODE, bool P>
 void spmv_launch_p(bool pdl, int tpr, i64 r0, i64 r1, i64 nl, const i64* sptr, const i32* scol, const double* sval,
@@ -1422,7 +1425,7 @@ static PfList pf_take(mgm_ctx* ctx, const Regions& regs, bool issuer = true, i64
 
 bool timing_on(const mgm_ctx* ctx);
 // zg: first forward sweep from a zero guess (k_gs_colour ZG; shifted problems only)
-void enqueue_sweep(mgm_ctx* ctx, int j, bool backward, cudaStream_t st, bool zg = false) {
+void enqueue_sweep(mgm_ctx* ctx, int j, bool backward, cudaStream_t st, bool zg = false, bool skip_c0 = false) {
     Level& L = ctx->lv[j];
     zg = zg && !backward && !ctx->poisson && L.slw;
     if (L.swB > 0 && !timing_on(ctx) && !zg) {  // one persistent kernel for the whole sweep
@@ -1447,7 +1450,7 @@ void enqueue_sweep(mgm_ctx* ctx, int j, bool backward, cudaStream_t st, bool zg 
     if (j == 0) timer_begin(ctx, tcls, st);
     double bytes = 0.0;
     int nl = 0;
-    for (int q = 0; q < L.ncol; ++q) {
+    for (int q = (skip_c0 && zg) ? 1 : 0; q < L.ncol; ++q) {  // (colour 0 done by the restriction)
         int c = backward ? L.ncol - 1 - q : q;
         const i64 c0 = L.coff[c], c1 = L.coff[c + 1];
         if (c1 <= c0) continue;
@@ -1527,9 +1530,14 @@ void enqueue_residual(mgm_ctx* ctx, int j, const double* f, const double* u, dou
 }
 
 // y (next level) = R_j x
-void enqueue_restrict(mgm_ctx* ctx, int j, const double* x, double* y, cudaStream_t st, bool morton_x = false) {
+// fuse_c0: also set colour 0 of level j+1's presmooth from zero (u = f / a_rr), which the
+// following sweep then skips (undistributed, shifted problems)
+void enqueue_restrict(mgm_ctx* ctx, int j, const double* x, double* y, cudaStream_t st, bool morton_x = false,
+                      bool fuse_c0 = false) {
     Level& L = ctx->lv[j];
     Level& Ln = ctx->lv[j + 1];
+    if (fuse_c0) g_c0 = C0Fuse{Ln.u, Ln.sptr, Ln.sval, (int)Ln.coff[1]};
+    struct ResetC0 { ~ResetC0() { g_c0 = C0Fuse{nullptr, nullptr, nullptr, 0}; } } resetc0_;
     const i32* rcol = (morton_x && L.rcol_m) ? L.rcol_m : L.rcol;
     for_my_pieces(ctx, j, 0, Ln.n, [&](i64 a, i64 b) {
         Regions rg;
@@ -1629,18 +1637,24 @@ void enqueue_vcycle(mgm_ctx* ctx, cudaStream_t st) {
     const bool mt0 = !dist_level(ctx, 0) && lv[0].n >= ctx->morton_t_min;
     enqueue_residual(ctx, 0, lv[0].f, lv[0].u, lv[0].t, st, ctx->vc_zero_guess && nu1 == 1, mt0);  // line 5
     stamp(ctx, "residual", 0, st);
-    enqueue_restrict(ctx, 0, lv[0].t, lv[1].f, st, mt0);
+    // levels whose first presmooth colour (from zero) is fused into the restriction before them
+    auto zg_level = [&](int j) { return nu1 >= 1 && !pre_b && !ctx->poisson && lv[j].slw && !ctx->no_zg; };
+    auto c0_fused = [&](int j) {
+        return j < D && zg_level(j) && !dist_level(ctx, j) && !dist_level(ctx, j - 1) && lv[j].ncol > 1 &&
+               lv[j].swB == 0 && !ctx->no_c0_fuse;
+    };
+    enqueue_restrict(ctx, 0, lv[0].t, lv[1].f, st, mt0, c0_fused(1));
     stamp(ctx, "restrict", 0, st);
     for (int j = 1; j < D; ++j) {                                         // lines 6-9
         // e_j = 0 then presmooth; the first forward sweep from the zero guess writes every row
         // and reads only earlier-colour values, so the zero fill is not needed
-        const bool zg = nu1 >= 1 && !pre_b && !ctx->poisson && lv[j].slw && !ctx->no_zg;
+        const bool zg = zg_level(j);
         if (!zg) enqueue_zero(ctx, lv[j].u, lv[j].n + pad, st);
-        for (int s = 0; s < nu1; ++s) enqueue_sweep(ctx, j, pre_b, st, s == 0 && zg);
+        for (int s = 0; s < nu1; ++s) enqueue_sweep(ctx, j, pre_b, st, s == 0 && zg, s == 0 && c0_fused(j));
         stamp(ctx, "zero+presmooth", j, st);
         const bool mt = !dist_level(ctx, j) && lv[j].n >= ctx->morton_t_min;
         enqueue_residual(ctx, j, lv[j].f, lv[j].u, lv[j].t, st, zg && nu1 == 1, mt);
-        enqueue_restrict(ctx, j, lv[j].t, lv[j + 1].f, st, mt);
+        enqueue_restrict(ctx, j, lv[j].t, lv[j + 1].f, st, mt, c0_fused(j + 1));
         stamp(ctx, "residual+restrict", j, st);
     }
     }
@@ -2474,6 +2488,7 @@ mgm_status mgm_setup(const double* points, const double* normals, int64_t n_poin
     if (const char* e = std::getenv("MGM_PF_DIST")) ctx->pf_dist = std::max(0, std::atoi(e));
     if (const char* e = std::getenv("MGM_PF_CAP_MB")) ctx->pf_cap = (i64)std::max(0, std::atoi(e)) << 20;
     if (std::getenv("MGM_NO_ZG")) ctx->no_zg = true;
+    if (std::getenv("MGM_NO_C0_FUSE")) ctx->no_c0_fuse = true;
     if (const char* e = std::getenv("MGM_UPPER_RES_MIN")) ctx->upper_res_min = std::atoll(e);
     if (const char* e = std::getenv("MGM_MORTON_T_MIN")) ctx->morton_t_min = std::atoll(e);
     if (std::getenv("MGM_PF_LATE")) ctx->pf_late = 1;

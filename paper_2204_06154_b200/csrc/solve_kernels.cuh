@@ -256,6 +256,16 @@ __global__ void __launch_bounds__(256) k_gs_colour_pipe(int r0, int r1, int rows
 // later] rows (from sluw[slice] = 1 + the slice's smallest earlier count, masked below
 // 1 + nlow[r]); equal to f - L u up to rounding.  Poisson: border term
 // c_i * x[nl] (nl = the level's row count; the multiplier sits after the rows).
+// Restriction fused with colour 0 of the next level's presmooth from zero (MODE 0): for the
+// coarse rows r < c0_end (lib order: colour 0 first) also u[r] = f[r] / a_rr -- exactly what
+// the zero-guess colour kernel computes for colour 0 (no earlier colours to gather).
+struct C0Fuse {
+    double* u;
+    const int64_t* sptr;
+    const double* sval;
+    int c0_end;
+};
+
 template <int MODE, bool POISSON, int TPR, int CH>
 __global__ void __launch_bounds__(256) k_sell_spmv(int r0, int r1, int nl, const int64_t* __restrict__ sptr,
                                                    const int* __restrict__ scol,
@@ -266,7 +276,8 @@ __global__ void __launch_bounds__(256) k_sell_spmv(int r0, int r1, int nl, const
                                                    const double* __restrict__ c, PfList pf,
                                                    const int* __restrict__ sluw = nullptr,
                                                    const uint8_t* __restrict__ nlow = nullptr,
-                                                   const int* __restrict__ yperm = nullptr) {
+                                                   const int* __restrict__ yperm = nullptr,
+                                                   C0Fuse c0 = C0Fuse{nullptr, nullptr, nullptr, 0}) {
     pdl_trigger();
     l2_prefetch_share(pf);
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
@@ -309,6 +320,7 @@ __global__ void __launch_bounds__(256) k_sell_spmv(int r0, int r1, int nl, const
     if (live && part == 0) {
         if (POISSON) acc += c[r] * x[nl];
         y[yr] = (MODE == 0) ? acc : (MODE == 1) ? f[r] - acc : -acc;
+        if (MODE == 0 && c0.u && r < c0.c0_end) c0.u[r] = 0.0 + (acc - 0.0) / c0.sval[c0.sptr[r >> 5] + (r & 31)];
     }
 }
 

@@ -18,7 +18,7 @@ w = MI.make_workload(cfg, n=n)
 variants = json.loads(os.environ.get("VARIANTS", "[{}]"))
 f = torch.from_numpy(np.random.default_rng(0).uniform(-1, 1, len(w.points))).cuda()
 for var in variants:
-    for k in ("MGM_BOT_MAX", "MGM_BOT_LOCAL", "MGM_NO_PDL", "MGM_L0_TPR", "MGM_LJ_TPR", "MGM_L0_STPR", "MGM_LJ_STPR", "MGM_GS_BLOCK_SMALL", "MGM_GS_BLOCK_L0", "MGM_BOT_CS", "MGM_NO_PIPE", "MGM_PIPE_CTAS", "MGM_RTPR", "MGM_BOT_TPR_MAX", "MGM_PF_DIST", "MGM_PF_CAP_MB", "MGM_PF_BOT_MB", "MGM_PF_LATE", "MGM_PF_NOF", "MGM_PF_L0ONLY", "MGM_MORTON_T_MIN", "MGM_UPPER_RES_MIN", "MGM_NO_ZG", "MGM_BOT_GEMV_MIN"):
+    for k in ("MGM_BOT_MAX", "MGM_BOT_LOCAL", "MGM_NO_PDL", "MGM_L0_TPR", "MGM_LJ_TPR", "MGM_L0_STPR", "MGM_LJ_STPR", "MGM_GS_BLOCK_SMALL", "MGM_GS_BLOCK_L0", "MGM_BOT_CS", "MGM_NO_PIPE", "MGM_PIPE_CTAS", "MGM_RTPR", "MGM_BOT_TPR_MAX", "MGM_PF_DIST", "MGM_PF_CAP_MB", "MGM_PF_BOT_MB", "MGM_PF_LATE", "MGM_PF_NOF", "MGM_PF_L0ONLY", "MGM_MORTON_T_MIN", "MGM_UPPER_RES_MIN", "MGM_NO_ZG", "MGM_BOT_GEMV_MIN", "MGM_NO_C0_FUSE"):
         os.environ.pop(k, None)
     os.environ.update(var)
     m = MGM(w.points, w.normals, w.stencil, w.levels)
