@@ -1607,6 +1607,7 @@ void stamp(mgm_ctx* ctx, const char* label, int level, cudaStream_t st) {
     ctx->ntrace++;
 }
 
+bool c0_fused_l0(const mgm_ctx* ctx);
 // Alg. 3 on level-0 buffers lv[0].f (rhs) and lv[0].u (guess in, result out), lib order.
 void enqueue_vcycle(mgm_ctx* ctx, cudaStream_t st) {
     ctx->ntrace = 0;
@@ -1630,7 +1631,8 @@ void enqueue_vcycle(mgm_ctx* ctx, cudaStream_t st) {
     if (!bottom_only) {
     // level 0 from a zero guess (preconditioner applications): the first sweep reads only
     // the diagonal and earlier-colour entries (k_gs_colour ZG)
-    for (int s = 0; s < nu1; ++s) enqueue_sweep(ctx, 0, pre_b, st, s == 0 && ctx->vc_zero_guess);  // line 4
+    for (int s = 0; s < nu1; ++s)  // line 4 (colour 0 from zero: done with the input copy, c0_fused_l0)
+        enqueue_sweep(ctx, 0, pre_b, st, s == 0 && ctx->vc_zero_guess, s == 0 && ctx->vc_zero_guess && c0_fused_l0(ctx));
     stamp(ctx, "presmooth", 0, st);
     // residual in Morton order for the restriction's gathers (opt-in: cfg3 restrict L0 30.4 ->
     // 26.7 us but residual 80 -> 85 us; cfg5 solve 206.6 vs 205.2 ms without)
@@ -1844,9 +1846,21 @@ void enqueue_dot(mgm_ctx* ctx, i64 n, const double* a, const double* b, double* 
 void enqueue_apply_A(mgm_ctx* ctx, const double* x, double* y, cudaStream_t st) { enqueue_spmv(ctx, 0, x, y, st); }
 
 // z = M(v): one V-cycle from zero, result left in lv[0].u
+// colour 0 of the level-0 presmooth from the zero guess done while copying the input (the
+// zero-guess V-cycle graph then starts at colour 1)
+bool c0_fused_l0(const mgm_ctx* ctx) {
+    return zg_capable(ctx) && !dist_level(ctx, 0) && ctx->lv[0].ncol > 1 && ctx->lv[0].swB == 0 && !ctx->no_c0_fuse;
+}
+C0Fuse c0_l0(mgm_ctx* ctx) {
+    return c0_fused_l0(ctx) ? C0Fuse{ctx->lv[0].u, ctx->lv[0].sptr, ctx->lv[0].sval, (int)ctx->lv[0].coff[1]}
+                            : C0Fuse{nullptr, nullptr, nullptr, 0};
+}
 mgm_status enqueue_precond(mgm_ctx* ctx, const double* v, cudaStream_t st) {
     i64 n = ctx->N + (ctx->poisson ? 1 : 0);
-    CK(cudaMemcpyAsync(ctx->lv[0].f, v, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+    if (c0_fused_l0(ctx))
+        k_copy_col<<<RED_BLOCKS, 256, 0, st>>>(n, v, 0, (const int*)nullptr, ctx->lv[0].f, c0_l0(ctx));
+    else
+        CK(cudaMemcpyAsync(ctx->lv[0].f, v, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
     if (!zg_capable(ctx)) CK(cudaMemsetAsync(ctx->lv[0].u, 0, sizeof(double) * n, st));
     return run_vcycle(ctx, st, true);  // M v from the zero guess
 }
@@ -2028,7 +2042,8 @@ static mgm_status build_gmres_graph(mgm_ctx* ctx) {
     g_launch_err.clear();
     // every node with programmatic serialisation (PDL): each kernel waits for its predecessor
     // with griddepcontrol.wait, and its launch overlaps the predecessor's tail
-    launch(true, k_copy_col, RED_BLOCKS, 256, 0, st, n, (const double*)V, ld, kdev, ctx->lv[0].f);  // f_0 = V_k
+    launch(true, k_copy_col, RED_BLOCKS, 256, 0, st, n, (const double*)V, ld, kdev, ctx->lv[0].f,
+           c0_l0(ctx));  // f_0 = V_k (and colour 0 of the presmooth)
     const bool zg = zg_capable(ctx);
     if (!zg) cudaMemsetAsync(ctx->lv[0].u, 0, sizeof(double) * n, st);
     ctx->vc_zero_guess = zg;

@@ -641,14 +641,19 @@ __device__ __forceinline__ double* gmd_sn(const GmresDev& G) { return gmd_cs(G) 
 __device__ __forceinline__ double* gmd_g(const GmresDev& G) { return gmd_sn(G) + G.m; }
 __device__ __forceinline__ double* gmd_hist(const GmresDev& G) { return gmd_g(G) + G.m + 1; }
 
-// dst = V_k (k = gi[0]): the Arnoldi vector to precondition
+// dst = V_k (k = gi[0]): the Arnoldi vector to precondition.  With c0.u: also colour 0 of the
+// level-0 presmooth from the zero guess (u = f / a_rr for rows < c0_end; C0Fuse), which the
+// zero-guess V-cycle graph then skips.
 __global__ void k_copy_col(int64_t n, const double* __restrict__ V, int64_t ld, const int* __restrict__ kdev,
-                           double* __restrict__ dst) {
+                           double* __restrict__ dst, C0Fuse c0) {
     pdl_trigger();
     pdl_wait();
-    const double* src = V + (int64_t)(*kdev) * ld;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        dst[i] = src[i];
+    const double* src = kdev ? V + (int64_t)(*kdev) * ld : V;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const double v = src[i];
+        dst[i] = v;
+        if (c0.u && i < c0.c0_end) c0.u[i] = 0.0 + (v - 0.0) / c0.sval[c0.sptr[i >> 5] + (i & 31)];
+    }
 }
 // V_{k+1} = w / sqrt(*nrm2)
 __global__ void k_scale_col(int64_t n, const double* __restrict__ w, const double* __restrict__ nrm2, double* V,
