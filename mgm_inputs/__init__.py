@@ -317,9 +317,11 @@ def make_workload(cfg: int, n: int | None = None, method: str = "rbffd") -> Work
         _, rng_rhs = _rngs(2)
         f = _trig_rhs(rng_rhs, x)
         st = dict(method=0, poly_degree=4, phs_k=3, stencil_n=50, problem=1, mu=1.0)
-        # BASELINE cfg4 names no GMRES restart (cfg1/cfg5 say GMRES(50)); restarted GMRES(50)
-        # stagnates near 1e-8 on this problem (oracle, N = 262144), GMRES(128) converges
-        lv = dict(num_levels=level_count(n), interp_m=6, nu1=1, nu2=1, restart=128)
+        # BASELINE cfg4 names neither the GMRES restart nor the sweeps (cfg1/cfg5 say GMRES(50),
+        # cfg2 says 2 pre-/2 post-sweeps): restarted GMRES(50) stagnates near 1e-8 on this
+        # problem (oracle, N = 262144) and V(1,1) needs 86 GMRES(128) iterations there,
+        # V(2,2) 51 -- GMRES(128) with V(2,2)
+        lv = dict(num_levels=level_count(n), interp_m=6, nu1=2, nu2=2, restart=128)
         return Workload("cfg4-quartic-poisson", x, nrm, f, None, st, lv)
     if cfg == 5:
         n = n or 16777216
