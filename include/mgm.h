@@ -27,6 +27,7 @@
 #ifndef MGM_H
 #define MGM_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -53,7 +54,11 @@ typedef struct {
     int poly_degree;  /* ell: degree of the tangent-plane polynomials, 0..8          */
     int phs_k;        /* k: PHS kernel r^(2k+1), 1 <= k <= ell (k=0 has no Laplacian) */
     int stencil_n;    /* n: stencil size incl. the centre, nearest in R^3; <= 96      */
-    double gfd_alpha; /* alpha of the GFD Gaussian weight                            */
+    double gfd_alpha; /* alpha of the GFD Gaussian weight exactly as written at P:185-187,
+                         w_i = exp(-alpha |x_1 - x_i|^2 / (rho_1^2 + rho_i^2)), rho_k the radius
+                         of point k's own projected stencil.  NOTE (O5): the paper's
+                         Table 1 value alpha = 4 reproduces its Table 3 iteration counts only
+                         when 16 (= 4 x 4) is passed here; the cfg2-GFD workload passes 16.    */
     int problem;      /* 0 = shifted (L = I - mu D), 1 = Poisson (L = D, mean-zero border)   */
     double mu;        /* mu > 0 of the shifted problem                                 */
 } mgm_stencil_params;
@@ -80,8 +85,21 @@ typedef struct {
     double solve_ms;           /* device time of this solve (CUDA events on the stream)                 */
 } mgm_report;
 
+/* Device memory of a ctx: every device allocation the ctx makes (hierarchy, workspaces,
+ * setup scratch) calls alloc(bytes, user) and later release(ptr, user) on the ctx's device;
+ * alloc returns NULL on failure (-> MGM_ERR_OOM), pointers must be 256-byte aligned.
+ * Passing NULL to mgm_setup (or alloc == NULL) uses cudaMalloc / cudaFree.  The callbacks
+ * are called from the thread that calls into the library, inside mgm_* calls only.  The
+ * Python binding passes PyTorch's caching allocator (paper_2204_06154_b200.torch_allocator). */
+typedef struct {
+    void* (*alloc)(size_t bytes, void* user);
+    void (*release)(void* ptr, void* user);
+    void* user;
+} mgm_allocator;
+
 /* Build the hierarchy (Alg. 2) on the current CUDA device.
  * points, normals: host, n_points x 3 row-major fp64 (normals unit length).  Copied.
+ * allocator: host struct (copied) or NULL.
  * On success *out receives a new ctx (free with mgm_destroy).  Errors: MGM_ERR_ARG,
  * MGM_ERR_INPUT (index = point), MGM_ERR_UNISOLVENT (index = centre, original order),
  * MGM_ERR_SINGULAR, MGM_ERR_CUDA, MGM_ERR_OOM.  If out is non-NULL and the failure happened
@@ -89,7 +107,7 @@ typedef struct {
  * mgm_last_error, then mgm_destroy). */
 mgm_status mgm_setup(const double* points, const double* normals, int64_t n_points,
                      const mgm_stencil_params* stencil, const mgm_level_params* levels,
-                     void* cuda_stream, mgm_ctx** out);
+                     const mgm_allocator* allocator, void* cuda_stream, mgm_ctx** out);
 
 /* One V(nu1,nu2)-cycle (Alg. 3): u <- MGM(f, u).
  * f_dev, u_dev: device, n_points fp64, original order; u_dev is the initial guess on entry
@@ -106,16 +124,20 @@ mgm_status mgm_vcycle(mgm_ctx* ctx, const double* f_dev, double* u_dev, void* cu
  *             preconditioner applications (two per step) and report.history holds the
  *             relative residual after every half step; on a rho/omega breakdown it restarts
  *             once from the current iterate, then returns converged = 0.
- * rhs_dev, x_dev: device, n_points fp64, original order; x_dev is ignored on entry (zero
- * initial guess) and receives the solution.  rhs = 0 gives x = 0 with 0 iterations.
- * Non-convergence within maxit is NOT an error (converged = 0).  report may be NULL. */
-mgm_status mgm_solve(mgm_ctx* ctx, const double* rhs_dev, double* x_dev, double tol, int maxit,
-                     int krylov, mgm_report* report, void* cuda_stream);
+ * rhs_dev, x_dev: device, n_points fp64, original order (multi-GPU: the rank's local block in
+ * mgm_local_rows order).  x0_dev: the initial guess (device, same layout; may alias x_dev) or
+ * NULL for x0 = 0 -- the paper's applications warm-start from the previous time step
+ * (P:711).  GMRES then starts from r0 = rhs - L x0, BiCGSTAB likewise, standalone MGM from
+ * u = x0; the stopping test stays ||rhs - L x|| / ||rhs|| <= tol.  x_dev receives the
+ * solution.  rhs = 0 gives x = 0 with 0 iterations (whatever x0).  Non-convergence within
+ * maxit is NOT an error (converged = 0).  report may be NULL. */
+mgm_status mgm_solve(mgm_ctx* ctx, const double* rhs_dev, const double* x0_dev, double* x_dev, double tol,
+                     int maxit, int krylov, mgm_report* report, void* cuda_stream);
 
-/* Same as mgm_solve with HOST vectors (pinned or pageable): copies rhs in and x out on the
- * stream inside the call (the end-to-end path). */
-mgm_status mgm_solve_host(mgm_ctx* ctx, const double* rhs_host, double* x_host, double tol,
-                          int maxit, int krylov, mgm_report* report, void* cuda_stream);
+/* Same as mgm_solve with HOST vectors (pinned or pageable): copies rhs (and x0) in and x out
+ * on the stream inside the call (the end-to-end path). */
+mgm_status mgm_solve_host(mgm_ctx* ctx, const double* rhs_host, const double* x0_host, double* x_host,
+                          double tol, int maxit, int krylov, mgm_report* report, void* cuda_stream);
 
 mgm_status mgm_destroy(mgm_ctx* ctx);
 

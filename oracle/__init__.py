@@ -557,15 +557,16 @@ class Oracle:
             rep.lam = float(x[-1])
         return x, rep
 
-    def standalone(self, f, tol=1e-10, maxit=200):
-        """MGM as a standalone solver (O16): u <- V-cycle(f, u) from u = 0."""
+    def standalone(self, f, tol=1e-10, maxit=200, x0=None):
+        """MGM as a standalone solver (O16): u <- V-cycle(f, u) from u = 0 (or from the
+        initial guess x0, the applications' warm start from the previous step)."""
         f = np.ascontiguousarray(f, dtype=np.float64)
-        u = np.zeros_like(f)
+        u = np.zeros_like(f) if x0 is None else np.array(x0, dtype=np.float64)
         rep = Report()
         fn = float(np.linalg.norm(f))
         if fn == 0.0:
             rep.converged, rep.final_rel_residual = True, 0.0
-            return u, rep
+            return np.zeros_like(f), rep
         for it in range(1, maxit + 1):
             u = self.vcycle_level_order(f, u)
             rel = float(np.linalg.norm(f - self.apply_A(u))) / fn
@@ -579,23 +580,24 @@ class Oracle:
             rep.lam = float(u[-1])
         return u, rep
 
-    def bicgstab(self, b, tol=1e-10, maxit=500):
+    def bicgstab(self, b, tol=1e-10, maxit=500, x0=None):
         """MGM-preconditioned BiCGSTAB on the fine operator, level order."""
-        x, rep = bicgstab(self.apply_A, self.precondition, b, tol=tol, maxit=maxit)
+        x, rep = bicgstab(self.apply_A, self.precondition, b, tol=tol, maxit=maxit, x0=x0)
         if self.poisson:
             rep.lam = float(x[-1])
         return x, rep
 
-    def solve(self, rhs, tol=1e-10, maxit=500, krylov=1):
+    def solve(self, rhs, tol=1e-10, maxit=500, krylov=1, x0=None):
         """Public solve on original-order vectors (mirrors mgm_solve: krylov 0 standalone,
-        1 GMRES, 2 BiCGSTAB)."""
+        1 GMRES, 2 BiCGSTAB; x0 the initial guess or None for 0)."""
         b = self.to_level(rhs)
+        g = None if x0 is None else self.to_level(x0)
         if krylov == 1:
-            x, rep = self.gmres(b, tol=tol, maxit=maxit)
+            x, rep = self.gmres(b, tol=tol, maxit=maxit, x0=g)
         elif krylov == 2:
-            x, rep = self.bicgstab(b, tol=tol, maxit=maxit)
+            x, rep = self.bicgstab(b, tol=tol, maxit=maxit, x0=g)
         else:
-            x, rep = self.standalone(b, tol=tol, maxit=maxit)
+            x, rep = self.standalone(b, tol=tol, maxit=maxit, x0=g)
         return self.from_level(x), rep
 
 

@@ -14,7 +14,8 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler",
                   "-ffp-contract=off", "-Xptxas", "-v"]
 SOURCES = [
-    ("host_setup.cpp", ["g++", "-O3", "-ffp-contract=off", "-fPIC", "-std=c++17", "-pthread"]),
+    ("host_setup.cpp", ["g++", "-O3", "-ffp-contract=off", "-fPIC", "-std=c++17", "-pthread",
+                        "-I/usr/local/cuda/include"]),
     ("setup_kernels.cu", [NVCC] + NVFLAGS + ["-fmad=false"]),
     ("mgm.cu", [NVCC] + NVFLAGS),
 ]

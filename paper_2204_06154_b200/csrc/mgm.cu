@@ -19,7 +19,6 @@
 #include "mgm_internal.h"
 #include "solve_kernels.cuh"
 #include "bottom_kernel.cuh"
-#include "sweep_kernel.cuh"
 #include "batch_kernels.cuh"
 
 using namespace mgm;
@@ -96,7 +95,6 @@ struct Level {
     int tpr = 1, rtpr = 1;  // threads per row for L_j (colour sweeps) and R_j kernels
     int stpr = 1;           // threads per row for full-level SpMV / residual on L_j
     int gs_block = 256;     // threads per block of the colour kernels
-    int pipe_ctas = 0;      // > 0: colours with >= pipe_ctas*128 rows use k_gs_colour_pipe on this many CTAs
     int uniform_w = 0;      // > 0: every SELL slice has this width
     // interpolation P_j (ELL width pm, slot-major) and restriction R_j (SELL-32, next level rows)
     int pm = 0;
@@ -118,12 +116,6 @@ struct Level {
     std::vector<i32> colour_lib;
     std::vector<double> c_lib;
     std::vector<i64> lib2mor;  // Morton index of each lib row
-    // one-kernel sweep with CTA-to-CTA dependencies (sweep_kernel.cuh); swB = 0: off
-    int swB = 0;
-    int* sw_cstart = nullptr;
-    int* sw_nbr_ptr = nullptr;
-    int* sw_nbr = nullptr;
-    unsigned* sw_prog = nullptr;
 };
 
 struct KernelTimer {
@@ -138,6 +130,7 @@ struct KernelTimer {
 }  // namespace
 
 struct mgm_ctx {
+    mgm_allocator alloc{};  // device allocator (mgm_setup; alloc == NULL: cudaMalloc)
     mgm_stencil_params sp{};
     mgm_level_params lp{};
     i64 N = 0;
@@ -219,6 +212,7 @@ struct mgm_ctx {
     double* w = nullptr;
     double* xs = nullptr;    // solution accumulator (lib order)
     double* b = nullptr;     // rhs (lib order)
+    bool warm = false;       // xs holds an initial guess x0 on entry of the solver (mgm_solve x0)
     double* partials = nullptr;
     unsigned* tickets = nullptr;  // last-block counters of the fused reductions (reset by the finisher)
     double* dh = nullptr;    // device scratch: h1[128], h2[128], nrm2, misc
@@ -238,6 +232,32 @@ struct mgm_ctx {
     int64_t err_index = -1;
 };
 
+// ---------------------------------------------------------------------------------------
+// Device allocations through the ctx's allocator (mgm_setup's mgm_allocator; NULL = the CUDA
+// runtime).  Thread-local: every ABI entry point installs its ctx's allocator (AllocScope).
+// ---------------------------------------------------------------------------------------
+static thread_local const mgm_allocator* g_alloc = nullptr;
+cudaError_t mgm::dev_malloc(void** p, size_t bytes) {
+    if (g_alloc && g_alloc->alloc) {
+        *p = g_alloc->alloc(bytes, g_alloc->user);
+        return *p ? cudaSuccess : cudaErrorMemoryAllocation;
+    }
+    return cudaMalloc(p, bytes);
+}
+void mgm::dev_free(void* p) {
+    if (!p) return;
+    if (g_alloc && g_alloc->alloc) {
+        if (g_alloc->release) g_alloc->release(p, g_alloc->user);
+        return;
+    }
+    cudaFree(p);
+}
+struct AllocScope {
+    const mgm_allocator* prev;
+    explicit AllocScope(const mgm_ctx* ctx) : prev(g_alloc) { g_alloc = ctx ? &ctx->alloc : nullptr; }
+    ~AllocScope() { g_alloc = prev; }
+};
+
 #define CK(call)                                                                           \
     do {                                                                                   \
         cudaError_t e_ = (call);                                                           \
@@ -249,7 +269,7 @@ struct mgm_ctx {
 
 template <class T>
 static cudaError_t dalloc(T** p, i64 count) {
-    return cudaMalloc((void**)p, sizeof(T) * (size_t)std::max<i64>(count, 1));
+    return dev_malloc((void**)p, sizeof(T) * (size_t)std::max<i64>(count, 1));
 }
 
 static unsigned blocks_for(i64 n, int threads) { return (unsigned)std::max<i64>(1, (n + threads - 1) / threads); }
@@ -409,7 +429,7 @@ mgm_status fail(mgm_ctx* ctx, mgm_status s, const std::string& msg, int64_t idx)
 template <class T>
 static T* bot_upload(mgm_ctx* ctx, const std::vector<T>& v, bool& ok) {
     T* d = nullptr;
-    if (cudaMalloc((void**)&d, sizeof(T) * std::max<size_t>(1, v.size())) != cudaSuccess) { ok = false; return nullptr; }
+    if (dev_malloc((void**)&d, sizeof(T) * std::max<size_t>(1, v.size())) != cudaSuccess) { ok = false; return nullptr; }
     ctx->bot_mem.push_back(d);
     ctx->bot_pf.push_back(PfRegion{(const char*)d, (int64_t)(sizeof(T) * v.size())});
     if (!v.empty() && cudaMemcpy(d, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice) != cudaSuccess) ok = false;
@@ -665,77 +685,6 @@ void setup_bottom(mgm_ctx* ctx, const std::vector<double>& LU, const std::vector
     ctx->botJ = J;
 }
 
-// Build the CTA-dependency sweep (sweep_kernel.cuh) for level j: B Morton-block owners,
-// per-colour row ranges, symmetric neighbour lists, progress counters.  Off for Poisson
-// problems (border terms) or with MGM_NO_SWEEP.
-template <int TPR>
-static int sweep_max_blocks() {
-    int dev = 0, nsm = 0, per = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_gs_sweep<TPR, 16>, SW_THREADS, 0) != cudaSuccess) {
-        cudaGetLastError();
-        return 0;
-    }
-    return per * nsm;
-}
-
-void setup_sweep(mgm_ctx* ctx, int j) {
-    Level& L = ctx->lv[j];
-    L.swB = 0;
-    // opt-in (MGM_SWEEP=1): measured slower than one kernel per colour (profiles/r01_notes.md)
-    if (ctx->poisson || !std::getenv("MGM_SWEEP") || std::getenv("MGM_NO_SWEEP") || L.ncol <= 1) return;
-    i64 rows_min = 16;
-    if (const char* e = std::getenv("MGM_SWEEP_ROWS")) rows_min = std::max<i64>(1, std::atoll(e));
-    const int bmax = L.tpr == 1 ? sweep_max_blocks<1>() : L.tpr == 2 ? sweep_max_blocks<2>() : sweep_max_blocks<4>();
-    if (bmax <= 0) return;
-    const i64 n = L.n;
-    const int B = (int)std::max<i64>(1, std::min<i64>(bmax, n / ((i64)L.ncol * rows_min)));
-    std::vector<i64> mstart(B + 1);
-    for (int b = 0; b <= B; ++b) mstart[b] = (i64)b * n / B;
-    std::vector<int> owner_m(n);
-    for (int b = 0; b < B; ++b)
-        for (i64 m = mstart[b]; m < mstart[b + 1]; ++m) owner_m[m] = b;
-    std::vector<int> cstart((size_t)L.ncol * (B + 1));
-    for (int c = 0; c < L.ncol; ++c) {
-        const i64 a0 = L.coff[c], a1 = L.coff[c + 1];
-        for (int b = 0; b <= B; ++b) {
-            // first row of colour c with Morton index >= mstart[b] (Morton-sorted inside a colour)
-            i64 lo = a0, hi = a1;
-            while (lo < hi) {
-                const i64 mid = (lo + hi) / 2;
-                if (L.lib2mor[mid] < mstart[b]) lo = mid + 1; else hi = mid;
-            }
-            cstart[(size_t)c * (B + 1) + b] = (int)lo;
-        }
-    }
-    std::vector<std::vector<int>> nb(B);
-    for (i64 r = 0; r < n; ++r) {
-        const int ob = owner_m[L.lib2mor[r]];
-        for (i64 t = L.L_lib.ptr[r]; t < L.L_lib.ptr[r + 1]; ++t) {
-            const int oc = owner_m[L.lib2mor[L.L_lib.col[t]]];
-            if (oc != ob) {
-                nb[ob].push_back(oc);
-                nb[oc].push_back(ob);
-            }
-        }
-    }
-    std::vector<int> nptr(B + 1, 0), nidx;
-    for (int b = 0; b < B; ++b) {
-        std::sort(nb[b].begin(), nb[b].end());
-        nb[b].erase(std::unique(nb[b].begin(), nb[b].end()), nb[b].end());
-        nidx.insert(nidx.end(), nb[b].begin(), nb[b].end());
-        nptr[b + 1] = (int)nidx.size();
-    }
-    bool ok = true;
-    L.sw_cstart = bot_upload(ctx, cstart, ok);
-    L.sw_nbr_ptr = bot_upload(ctx, nptr, ok);
-    L.sw_nbr = bot_upload(ctx, nidx, ok);
-    L.sw_prog = bot_upload(ctx, std::vector<unsigned>((size_t)B * SW_PROG_STRIDE, 0u), ok);
-    if (!ok) return;
-    L.swB = B;
-}
-
 // Setup phase timer (MGM_SETUP_TIMING=1 prints host wall time per phase to stderr).
 struct SetupTimer {
     bool on = std::getenv("MGM_SETUP_TIMING") != nullptr;
@@ -820,10 +769,10 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
     CK(cudaMemcpyAsync(W.data(), dW, sizeof(double) * N * ns, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(&hfail, dfail, sizeof(i64), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    cudaFree(dW);
-    cudaFree(dS);
-    cudaFree(dN);
-    if (drho) cudaFree(drho);
+    dev_free(dW);
+    dev_free(dS);
+    dev_free(dN);
+    if (drho) dev_free(drho);
     if (hfail != INT64_MAX)
         return fail(ctx, MGM_ERR_UNISOLVENT, sp.method == 0 ? "RBF-FD stencil not unisolvent" : "GFD stencil rank deficient",
                     perm[hfail]);
@@ -904,10 +853,10 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
         CK(cudaMemcpyAsync(pc.data(), dcnt, sizeof(i32) * nf, cudaMemcpyDeviceToHost, st));
         CK(cudaMemcpyAsync(&hfail, dfail, sizeof(i64), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
-        cudaFree(dPw);
-        cudaFree(dI);
-        cudaFree(dcnt);
-        cudaFree(dXf);
+        dev_free(dPw);
+        dev_free(dI);
+        dev_free(dcnt);
+        dev_free(dXf);
         dXf = dXc;
         if (hfail != INT64_MAX) return fail(ctx, MGM_ERR_SINGULAR, "singular transfer system", idsl[j][hfail]);
         HostCSR& P = Pm[j];
@@ -942,8 +891,8 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
         free_dev_csr(dC);
         tm.mark("Galerkin RAP", j);
     }
-    cudaFree(dXf);
-    cudaFree(dfail);
+    dev_free(dXf);
+    dev_free(dfail);
     // ---- colouring (O11) and lib orders
     ctx->lv.assign(p, Level());
     std::vector<std::vector<i64>> lib2mor(p);
@@ -1008,13 +957,7 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
             // 112.8 -> 87.6 us per sweep with 8 instead of 4)
             if (L.ncol > 0 && (double)n / L.ncol * L.tpr < 16384.0 && L.tpr < 8) L.tpr *= 2;
             L.stpr = 1;
-            {   // streamed colour kernel for large colours: opt-in (MGM_PIPE=1), measured slower
-                // than the one-wave kernel (level-0 sweep 174 us vs 122 us, profiles/r01_notes.md)
-                int dev = 0, nsm = 148;
-                cudaGetDevice(&dev);
-                cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-                L.pipe_ctas = (std::getenv("MGM_PIPE") && !std::getenv("MGM_NO_PIPE")) ? nsm : 0;
-                if (const char* e = std::getenv("MGM_PIPE_CTAS")) L.pipe_ctas = std::atoi(e);
+            {
                 const i64 ns = (n + 31) / 32;
                 bool uni = ns > 0;
                 for (i64 q = 0; q < ns && uni; ++q) uni = sptr[q + 1] - sptr[q] == sptr[1] - sptr[0];
@@ -1108,7 +1051,6 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
         CK(cudaMemsetAsync(L.t, 0, sizeof(double) * vn, st));
     }
     tm.mark("pack + upload");
-    for (int j = 0; j + 1 < p; ++j) setup_sweep(ctx, j);
     // ---- Poisson border vectors c_{j+1} = P_j^T c_j, Morton order then lib
     if (ctx->poisson) {
         std::vector<double> cm(N, 1.0);
@@ -1428,22 +1370,6 @@ bool timing_on(const mgm_ctx* ctx);
 void enqueue_sweep(mgm_ctx* ctx, int j, bool backward, cudaStream_t st, bool zg = false, bool skip_c0 = false) {
     Level& L = ctx->lv[j];
     zg = zg && !backward && !ctx->poisson && L.slw;
-    if (L.swB > 0 && !timing_on(ctx) && !zg) {  // one persistent kernel for the whole sweep
-        SweepParams P{};
-        P.n = (int)L.n;
-        P.ncol = L.ncol;
-        P.nsweep = 1;
-        P.backward = backward ? 1 : 0;
-        P.sptr = L.sptr; P.scol = L.scol; P.sval = L.sval;
-        P.f = L.f; P.u = L.u;
-        P.cstart = L.sw_cstart; P.nbr_ptr = L.sw_nbr_ptr; P.nbr = L.sw_nbr; P.prog = L.sw_prog;
-        // no PDL: every CTA must be co-resident, so the predecessor must have drained
-        if (L.tpr == 1) launch(false, k_gs_sweep<1, 16>, L.swB, SW_THREADS, 0, st, P);
-        else if (L.tpr == 2) launch(false, k_gs_sweep<2, 16>, L.swB, SW_THREADS, 0, st, P);
-        else launch(false, k_gs_sweep<4, 16>, L.swB, SW_THREADS, 0, st, P);
-        ctx->vcycle_kernels++;
-        return;
-    }
     // timing class 0: CUDA events around the whole level-0 sweep (the colour kernels keep
     // their PDL overlap inside it); launches and algorithmic bytes are summed over colours
     const int tcls = zg ? 3 : 0;  // zero-guess level-0 sweeps are their own timing class
@@ -1456,13 +1382,7 @@ void enqueue_sweep(mgm_ctx* ctx, int j, bool backward, cudaStream_t st, bool zg 
         if (c1 <= c0) continue;
         for_my_pieces(ctx, j, c0, c1, [&](i64 a, i64 b) {
             if (b <= a) return;
-            if (L.pipe_ctas > 0 && !ctx->poisson && !zg && b - a >= (i64)L.pipe_ctas * 128) {
-                // large colour: streamed kernel, one CTA per SM (k_gs_colour_pipe)
-                const int rpc = (int)((b - a + L.pipe_ctas - 1) / L.pipe_ctas);
-                launch(ctx->pdl, k_gs_colour_pipe<2, CHUNK>, (unsigned)((b - a + rpc - 1) / rpc), 256, 0, st, (int)a,
-                       (int)b, rpc, L.uniform_w, (const i64*)L.sptr, (const i32*)L.scol, (const double*)L.sval,
-                       (const double*)L.f, L.u);
-            } else {
+            {
                 Regions rg;
                 if (!ctx->pf_l0only || j == 0) {
                     pf_sell(rg, L.h_sptr, L.scol, L.sval, a, b);
@@ -1643,7 +1563,7 @@ void enqueue_vcycle(mgm_ctx* ctx, cudaStream_t st) {
     auto zg_level = [&](int j) { return nu1 >= 1 && !pre_b && !ctx->poisson && lv[j].slw && !ctx->no_zg; };
     auto c0_fused = [&](int j) {
         return j < D && zg_level(j) && !dist_level(ctx, j) && !dist_level(ctx, j - 1) && lv[j].ncol > 1 &&
-               lv[j].swB == 0 && !ctx->no_c0_fuse;
+               !ctx->no_c0_fuse;
     };
     enqueue_restrict(ctx, 0, lv[0].t, lv[1].f, st, mt0, c0_fused(1));
     stamp(ctx, "restrict", 0, st);
@@ -1739,7 +1659,7 @@ mgm_status pf_prepare(mgm_ctx* ctx, cudaStream_t st) {
     if (!same) {
         if (ctx->d_pf) ctx->pf_old.push_back(ctx->d_pf);
         ctx->d_pf = nullptr;
-        CK(cudaMalloc((void**)&ctx->d_pf, sizeof(PfRegion) * std::max<size_t>(1, flat.size())));
+        CK(dev_malloc((void**)&ctx->d_pf, sizeof(PfRegion) * std::max<size_t>(1, flat.size())));
         if (!flat.empty())
             CK(cudaMemcpy(ctx->d_pf, flat.data(), sizeof(PfRegion) * flat.size(), cudaMemcpyHostToDevice));
         ctx->pf_flat = flat;
@@ -1815,7 +1735,7 @@ mgm_status ensure_krylov(mgm_ctx* ctx) {
     CK(dalloc(&ctx->xs, ctx->ld));
     CK(dalloc(&ctx->b, ctx->ld));
     CK(dalloc(&ctx->partials, (i64)RED_BLOCKS * 256));
-    CK(cudaMalloc((void**)&ctx->tickets, 64 * sizeof(unsigned)));
+    CK(dev_malloc((void**)&ctx->tickets, 64 * sizeof(unsigned)));
     CK(cudaMemset(ctx->tickets, 0, 64 * sizeof(unsigned)));
     CK(dalloc(&ctx->dh, 1024));
     CK(cudaMallocHost((void**)&ctx->hh, sizeof(double) * 1024));
@@ -1849,7 +1769,7 @@ void enqueue_apply_A(mgm_ctx* ctx, const double* x, double* y, cudaStream_t st) 
 // colour 0 of the level-0 presmooth from the zero guess done while copying the input (the
 // zero-guess V-cycle graph then starts at colour 1)
 bool c0_fused_l0(const mgm_ctx* ctx) {
-    return zg_capable(ctx) && !dist_level(ctx, 0) && ctx->lv[0].ncol > 1 && ctx->lv[0].swB == 0 && !ctx->no_c0_fuse;
+    return zg_capable(ctx) && !dist_level(ctx, 0) && ctx->lv[0].ncol > 1 && !ctx->no_c0_fuse;
 }
 C0Fuse c0_l0(mgm_ctx* ctx) {
     return c0_fused_l0(ctx) ? C0Fuse{ctx->lv[0].u, ctx->lv[0].sptr, ctx->lv[0].sval, (int)ctx->lv[0].coff[1]}
@@ -1877,19 +1797,20 @@ mgm_status gmres_lib(mgm_ctx* ctx, double tol, int maxit, mgm_report* rep, cudaS
     double* h2 = ctx->dh + 256;
     double* nr = ctx->dh + 512;
     mgm_status s;
-    CK(cudaMemsetAsync(ctx->xs, 0, sizeof(double) * n, st));
+    if (!ctx->warm) CK(cudaMemsetAsync(ctx->xs, 0, sizeof(double) * n, st));
     enqueue_dot(ctx, n, ctx->b, ctx->b, nr, st);
     CK(cudaMemcpyAsync(ctx->hh, nr, sizeof(double), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     const double bnorm = std::sqrt(ctx->hh[0]);
     int its = 0, hist_n = 0;
     bool converged = false;
-    if (bnorm == 0.0) {
+    if (bnorm == 0.0) {  // x = 0 solves A x = 0 (whatever x0)
+        CK(cudaMemsetAsync(ctx->xs, 0, sizeof(double) * n, st));
         if (rep) { rep->iterations = 0; rep->converged = 1; rep->final_rel_residual = 0.0; }
         return MGM_OK;
     }
     std::vector<double> H((size_t)(m + 1) * m), cs(m), sn(m), g(m + 1), y(m);
-    bool first = true;
+    bool first = !ctx->warm;  // r0 = b - A x0 (x0 = 0: r0 = b, no SpMV)
     while (true) {
         // r = b - A x ; beta
         if (first) {
@@ -2085,14 +2006,15 @@ mgm_status gmres_dev(mgm_ctx* ctx, double tol, int maxit, mgm_report* rep, cudaS
     double* nr = ctx->dh + 512;
     mgm_status s;
     if ((s = build_gmres_graph(ctx))) return s;
-    CK(cudaMemsetAsync(ctx->xs, 0, sizeof(double) * n, st));
+    if (!ctx->warm) CK(cudaMemsetAsync(ctx->xs, 0, sizeof(double) * n, st));
     enqueue_dot(ctx, n, ctx->b, ctx->b, nr, st);
     CK(cudaMemcpyAsync(ctx->hh, nr, sizeof(double), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     const double bnorm = std::sqrt(ctx->hh[0]);
     int its = 0, hist_n = 0;
     bool converged = false;
-    if (bnorm == 0.0) {
+    if (bnorm == 0.0) {  // x = 0 solves A x = 0 (whatever x0)
+        CK(cudaMemsetAsync(ctx->xs, 0, sizeof(double) * n, st));
         if (rep) { rep->iterations = 0; rep->converged = 1; rep->final_rel_residual = 0.0; }
         return MGM_OK;
     }
@@ -2102,7 +2024,7 @@ mgm_status gmres_dev(mgm_ctx* ctx, double tol, int maxit, mgm_report* rep, cudaS
     double* gg = Hh + (size_t)(m + 1) * m + 2 * (size_t)m;
     double* hist = gg + (m + 1);
     std::vector<double> y(m);
-    bool first = true;
+    bool first = !ctx->warm;  // r0 = b - A x0 (x0 = 0: r0 = b, no SpMV)
     while (true) {
         if (first) {  // r = b - A x ; beta
             CK(cudaMemcpyAsync(w, ctx->b, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
@@ -2195,20 +2117,26 @@ mgm_status bicgstab_lib(mgm_ctx* ctx, double tol, int maxit, mgm_report* rep, cu
         CK(cudaStreamSynchronize(st));
         return MGM_OK;
     };
-    CK(cudaMemsetAsync(ctx->xs, 0, sizeof(double) * n, st));
+    if (!ctx->warm) CK(cudaMemsetAsync(ctx->xs, 0, sizeof(double) * n, st));
     enqueue_dot(ctx, n, ctx->b, ctx->b, dd, st);
     if ((s = fetch(1))) return s;
     const double bnorm = std::sqrt(hh[0]);
     int its = 0, hist_n = 0, restarts = 0;
     bool converged = false;
-    if (bnorm == 0.0) {
+    if (bnorm == 0.0) {  // x = 0 solves A x = 0 (whatever x0)
+        CK(cudaMemsetAsync(ctx->xs, 0, sizeof(double) * n, st));
         if (rep) { rep->iterations = 0; rep->converged = 1; rep->final_rel_residual = 0.0; rep->lambda = 0.0; }
         return MGM_OK;
     }
     auto record = [&](double rel) {
         if (rep && rep->history && hist_n < rep->history_cap) rep->history[hist_n++] = rel;
     };
-    CK(cudaMemcpyAsync(r, ctx->b, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));  // r = b - A 0
+    if (ctx->warm) {  // r = b - A x0
+        enqueue_apply_A(ctx, ctx->xs, r, st);
+        k_axpby<<<nb, nt, 0, st>>>(n, 1.0, ctx->b, -1.0, r, r);
+    } else {
+        CK(cudaMemcpyAsync(r, ctx->b, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));  // r = b - A 0
+    }
     while (true) {
         CK(cudaMemcpyAsync(rh, r, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
         CK(cudaMemsetAsync(p, 0, sizeof(double) * n, st));
@@ -2355,7 +2283,7 @@ static void enqueue_vcycle_bk(mgm_ctx* ctx, int K, cudaStream_t st) {
 static mgm_status ensure_batch(mgm_ctx* ctx, int K) {
     if (ctx->bK >= K) return MGM_OK;
     for (auto* q : {&ctx->bu, &ctx->bf, &ctx->bt})
-        for (double* ptr : *q) cudaFree(ptr);
+        for (double* ptr : *q) dev_free(ptr);
     ctx->bu.assign(ctx->p, nullptr);
     ctx->bf.assign(ctx->p, nullptr);
     ctx->bt.assign(ctx->p, nullptr);
@@ -2364,7 +2292,7 @@ static mgm_status ensure_batch(mgm_ctx* ctx, int K) {
         CK(dalloc(&ctx->bf[j], ctx->lv[j].n * K));
         CK(dalloc(&ctx->bt[j], ctx->lv[j].n * K));
     }
-    if (ctx->bres) cudaFree(ctx->bres);
+    if (ctx->bres) dev_free(ctx->bres);
     CK(dalloc(&ctx->bres, ctx->N * K));
     for (auto& gx : ctx->bgraph)
         if (gx) { cudaGraphExecDestroy(gx); gx = nullptr; }
@@ -2414,7 +2342,10 @@ mgm_status standalone_lib(mgm_ctx* ctx, double tol, int maxit, mgm_report* rep, 
     CK(cudaMemcpyAsync(ctx->hh, nr, sizeof(double), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     const double fn = std::sqrt(ctx->hh[0]);
-    CK(cudaMemsetAsync(ctx->lv[0].u, 0, sizeof(double) * n, st));
+    if (ctx->warm && fn != 0.0)  // u starts at x0 (the applications' warm start)
+        CK(cudaMemcpyAsync(ctx->lv[0].u, ctx->xs, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+    else
+        CK(cudaMemsetAsync(ctx->lv[0].u, 0, sizeof(double) * n, st));
     CK(cudaMemsetAsync(ctx->xs, 0, sizeof(double) * n, st));
     if (fn == 0.0) {
         if (rep) { rep->iterations = 0; rep->converged = 1; rep->final_rel_residual = 0.0; }
@@ -2466,8 +2397,8 @@ mgm_status check_ctx(mgm_ctx* ctx) {
 extern "C" {
 
 mgm_status mgm_setup(const double* points, const double* normals, int64_t n_points,
-                     const mgm_stencil_params* stencil, const mgm_level_params* levels, void* cuda_stream,
-                     mgm_ctx** out) {
+                     const mgm_stencil_params* stencil, const mgm_level_params* levels,
+                     const mgm_allocator* allocator, void* cuda_stream, mgm_ctx** out) {
     g_setup_error.clear();
     g_setup_index = -1;
     if (out) *out = nullptr;
@@ -2491,7 +2422,13 @@ mgm_status mgm_setup(const double* points, const double* normals, int64_t n_poin
         return MGM_ERR_ARG;
     }
     auto t0 = std::chrono::steady_clock::now();
+    if (allocator && allocator->alloc && !allocator->release) {
+        g_setup_error = "allocator without a release function";
+        return MGM_ERR_ARG;
+    }
     mgm_ctx* ctx = new mgm_ctx();
+    if (allocator) ctx->alloc = *allocator;
+    AllocScope as_(ctx);
     ctx->sp = sp;
     ctx->lp = lp;
     ctx->N = n_points;
@@ -2544,6 +2481,7 @@ static mgm_status batch_check(mgm_ctx* ctx, int K) {
 }
 
 mgm_status mgm_vcycle_batch(mgm_ctx* ctx, int K, const double* f_dev, double* u_dev, void* cuda_stream) {
+    AllocScope as_(ctx);
     if (K == 1) return mgm_vcycle(ctx, f_dev, u_dev, cuda_stream);
     mgm_status s = batch_check(ctx, K);
     if (s) return s;
@@ -2561,7 +2499,8 @@ mgm_status mgm_vcycle_batch(mgm_ctx* ctx, int K, const double* f_dev, double* u_
 
 mgm_status mgm_solve_batch(mgm_ctx* ctx, int K, const double* rhs_dev, double* x_dev, double tol, int maxit,
                            mgm_report* reports, void* cuda_stream) {
-    if (K == 1) return mgm_solve(ctx, rhs_dev, x_dev, tol, maxit, 0, reports, cuda_stream);
+    AllocScope as_(ctx);
+    if (K == 1) return mgm_solve(ctx, rhs_dev, nullptr, x_dev, tol, maxit, 0, reports, cuda_stream);
     mgm_status s = batch_check(ctx, K);
     if (s) return s;
     if (!rhs_dev || !x_dev || !(tol >= 0) || maxit < 0) return MGM_ERR_ARG;
@@ -2638,6 +2577,7 @@ mgm_status mgm_nccl_unique_id(void* id128) {
 }
 
 mgm_status mgm_dist_attach(mgm_ctx* ctx, int rank, int nranks, const void* id128) {
+    AllocScope as_(ctx);
     if (!ctx || ctx->lv.empty() || nranks < 1 || rank < 0 || rank >= nranks || !id128) return MGM_ERR_ARG;
     if (ctx->poisson && nranks > 1) {
         ctx->err = "multi-GPU solve supports the shifted problem only";
@@ -2669,6 +2609,7 @@ mgm_status mgm_dist_attach(mgm_ctx* ctx, int rank, int nranks, const void* id128
 }
 
 mgm_status mgm_destroy(mgm_ctx* ctx) {
+    AllocScope as_(ctx);
     if (!ctx) return MGM_OK;
     cudaSetDevice(ctx->device);
     if (ctx->st) cudaStreamSynchronize(ctx->st);
@@ -2676,30 +2617,30 @@ mgm_status mgm_destroy(mgm_ctx* ctx) {
         for (void* ptr : {(void*)L.sptr, (void*)L.scol, (void*)L.sval, (void*)L.pcol, (void*)L.pval, (void*)L.rptr,
                           (void*)L.rcol, (void*)L.rval, (void*)L.u, (void*)L.f, (void*)L.t, (void*)L.c, (void*)L.slw,
                           (void*)L.nlow, (void*)L.sluw, (void*)L.l2m, (void*)L.rcol_m})
-            if (ptr) cudaFree(ptr);
+            if (ptr) dev_free(ptr);
     }
     for (void* ptr : {(void*)ctx->lu, (void*)ctx->piv, (void*)ctx->d_lib2orig, (void*)ctx->V, (void*)ctx->w,
                       (void*)ctx->xs, (void*)ctx->b, (void*)ctx->partials, (void*)ctx->dh, (void*)ctx->tickets})
-        if (ptr) cudaFree(ptr);
+        if (ptr) dev_free(ptr);
     if (ctx->hh) cudaFreeHost(ctx->hh);
     if (ctx->ggraph) cudaGraphExecDestroy(ctx->ggraph);
-    if (ctx->g_i) cudaFree(ctx->g_i);
-    if (ctx->g_d) cudaFree(ctx->g_d);
+    if (ctx->g_i) dev_free(ctx->g_i);
+    if (ctx->g_d) dev_free(ctx->g_d);
     if (ctx->g_h) cudaFreeHost(ctx->g_h);
     if (ctx->g_hi) cudaFreeHost(ctx->g_hi);
-    for (void* q : ctx->bot_mem) cudaFree(q);
-    if (ctx->d_pf) cudaFree(ctx->d_pf);
-    for (void* q : ctx->pf_old) cudaFree(q);
-    if (ctx->d_trace) cudaFree(ctx->d_trace);
+    for (void* q : ctx->bot_mem) dev_free(q);
+    if (ctx->d_pf) dev_free(ctx->d_pf);
+    for (void* q : ctx->pf_old) dev_free(q);
+    if (ctx->d_trace) dev_free(ctx->d_trace);
     if (ctx->vgraph) cudaGraphExecDestroy(ctx->vgraph);
     if (ctx->vgraph0) cudaGraphExecDestroy(ctx->vgraph0);
     if (ctx->comm) nccl().CommDestroy(ctx->comm);
     for (auto* q : {&ctx->bu, &ctx->bf, &ctx->bt})
-        for (double* ptr : *q) cudaFree(ptr);
+        for (double* ptr : *q) dev_free(ptr);
     for (auto& gx : ctx->bgraph)
         if (gx) cudaGraphExecDestroy(gx);
-    if (ctx->bres) cudaFree(ctx->bres);
-    if (ctx->ainv) cudaFree(ctx->ainv);
+    if (ctx->bres) dev_free(ctx->bres);
+    if (ctx->ainv) dev_free(ctx->ainv);
     for (auto& T : ctx->timer)
         for (auto e : T.ev) cudaEventDestroy(e);
     if (ctx->st) cudaStreamDestroy(ctx->st);
@@ -2717,6 +2658,7 @@ const char* mgm_last_error(const mgm_ctx* ctx, int64_t* failing_index) {
 }
 
 mgm_status mgm_vcycle(mgm_ctx* ctx, const double* f_dev, double* u_dev, void* cuda_stream) {
+    AllocScope as_(ctx);
     mgm_status s = check_ctx(ctx);
     if (s) return s;
     if (!f_dev || !u_dev) return MGM_ERR_ARG;
@@ -2740,8 +2682,9 @@ mgm_status mgm_vcycle(mgm_ctx* ctx, const double* f_dev, double* u_dev, void* cu
     return MGM_OK;
 }
 
-static mgm_status solve_impl(mgm_ctx* ctx, const double* rhs, double* x, bool host, double tol, int maxit,
-                             int krylov, mgm_report* rep, cudaStream_t st) {
+static mgm_status solve_impl(mgm_ctx* ctx, const double* rhs, const double* x0, double* x, bool host, double tol,
+                             int maxit, int krylov, mgm_report* rep, cudaStream_t st) {
+    AllocScope as_(ctx);
     mgm_status s = check_ctx(ctx);
     if (s) return s;
     if (!rhs || !x || !(tol >= 0) || maxit < 0 || krylov < 0 || krylov > 2) return MGM_ERR_ARG;
@@ -2758,6 +2701,17 @@ static mgm_status solve_impl(mgm_ctx* ctx, const double* rhs, double* x, bool ho
     }
     k_gather<<<blocks_for(N, 256), 256, 0, st>>>((int)N, ctx->d_lib2orig, rhs_dev, ctx->b);
     if (ctx->poisson) CK(cudaMemsetAsync(ctx->b + N, 0, sizeof(double), st));
+    ctx->warm = x0 != nullptr;
+    struct ResetW { mgm_ctx* c; ~ResetW() { c->warm = false; } } resetw_{ctx};
+    if (x0) {  // x0 -> lib order (xs); Poisson: the multiplier starts at 0
+        const double* x0_dev = x0;
+        if (host) {  // (x0 may alias x; rhs already sits in w, so x0 goes through lv[0].t)
+            CK(cudaMemcpyAsync(ctx->lv[0].t, x0, sizeof(double) * N, cudaMemcpyHostToDevice, st));
+            x0_dev = ctx->lv[0].t;
+        }
+        k_gather<<<blocks_for(N, 256), 256, 0, st>>>((int)N, ctx->d_lib2orig, x0_dev, ctx->xs);
+        if (ctx->poisson) CK(cudaMemsetAsync(ctx->xs + N, 0, sizeof(double), st));
+    }
     s = krylov == 1 ? (gmres_dev_ok(ctx) ? gmres_dev(ctx, tol, maxit, rep, st) : gmres_lib(ctx, tol, maxit, rep, st))
         : krylov == 2 ? bicgstab_lib(ctx, tol, maxit, rep, st)
                       : standalone_lib(ctx, tol, maxit, rep, st);
@@ -2782,14 +2736,14 @@ static mgm_status solve_impl(mgm_ctx* ctx, const double* rhs, double* x, bool ho
     return MGM_OK;
 }
 
-mgm_status mgm_solve(mgm_ctx* ctx, const double* rhs_dev, double* x_dev, double tol, int maxit, int krylov,
-                     mgm_report* report, void* cuda_stream) {
-    return solve_impl(ctx, rhs_dev, x_dev, false, tol, maxit, krylov, report, (cudaStream_t)cuda_stream);
+mgm_status mgm_solve(mgm_ctx* ctx, const double* rhs_dev, const double* x0_dev, double* x_dev, double tol,
+                     int maxit, int krylov, mgm_report* report, void* cuda_stream) {
+    return solve_impl(ctx, rhs_dev, x0_dev, x_dev, false, tol, maxit, krylov, report, (cudaStream_t)cuda_stream);
 }
 
-mgm_status mgm_solve_host(mgm_ctx* ctx, const double* rhs_host, double* x_host, double tol, int maxit, int krylov,
-                          mgm_report* report, void* cuda_stream) {
-    return solve_impl(ctx, rhs_host, x_host, true, tol, maxit, krylov, report, (cudaStream_t)cuda_stream);
+mgm_status mgm_solve_host(mgm_ctx* ctx, const double* rhs_host, const double* x0_host, double* x_host, double tol,
+                          int maxit, int krylov, mgm_report* report, void* cuda_stream) {
+    return solve_impl(ctx, rhs_host, x0_host, x_host, true, tol, maxit, krylov, report, (cudaStream_t)cuda_stream);
 }
 
 mgm_status mgm_num_levels(const mgm_ctx* ctx, int* p) {
@@ -2843,6 +2797,7 @@ mgm_status mgm_export_weights(const mgm_ctx* ctx, double* w, int64_t* sten) {
 
 mgm_status mgm_apply(mgm_ctx* ctx, int level, int op, const double* x, const double* f, double* y,
                      void* cuda_stream) {
+    AllocScope as_(ctx);
     mgm_status s = check_ctx(ctx);
     if (s) return s;
     if (level < 0 || level >= ctx->p || !x || !y) return MGM_ERR_ARG;

@@ -1,5 +1,7 @@
 // Internal declarations of libmgm (not part of the ABI).
 #pragma once
+#include <cuda_runtime.h>
+
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -8,6 +10,12 @@ namespace mgm {
 
 using i64 = int64_t;
 using i32 = int32_t;
+
+// Device memory of a ctx (setup scratch included) goes through the allocator passed to
+// mgm_setup (include/mgm.h mgm_allocator; NULL = cudaMalloc / cudaFree).  The current
+// allocator is thread-local: every ABI entry point installs its ctx's (AllocScope).
+cudaError_t dev_malloc(void** p, size_t bytes);
+void dev_free(void* p);
 
 // Host CSR (int64 row pointer, int32 columns ascending within a row).
 struct HostCSR {

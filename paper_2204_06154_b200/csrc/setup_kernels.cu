@@ -591,8 +591,8 @@ int spgemm_device(const DevCSR& A, const DevCSR& B, DevCSR& C, void* stream, std
     i64 n = A.nrows;
     i64* d_cnt = nullptr;
     unsigned char* d_skip = nullptr;
-    cudaError_t e = cudaMalloc(&d_cnt, sizeof(i64) * (n + 1));
-    if (e == cudaSuccess) e = cudaMalloc(&d_skip, std::max<i64>(1, n));
+    cudaError_t e = dev_malloc((void**)&d_cnt, sizeof(i64) * (n + 1));
+    if (e == cudaSuccess) e = dev_malloc((void**)&d_skip, std::max<i64>(1, n));
     if (e != cudaSuccess) { err = "cudaMalloc"; return (int)e; }
     k_row_products<<<(unsigned)std::min<i64>((n + 255) / 256, 148 * 16), 256, 0, st>>>(A.ptr, A.col, B.ptr, n, d_cnt);
     std::vector<i64> cnt(n), aptr(n + 1);
@@ -638,10 +638,10 @@ int spgemm_device(const DevCSR& A, const DevCSR& B, DevCSR& C, void* stream, std
     std::vector<i64> ptr(n + 1, 0);
     for (i64 r = 0; r < n; ++r) ptr[r + 1] = ptr[r] + cnt[r];
     C.nnz = ptr[n];
-    e = cudaMalloc(&C.ptr, sizeof(i64) * (n + 1));
-    if (e == cudaSuccess) e = cudaMalloc(&C.col, sizeof(i32) * std::max<i64>(1, C.nnz));
-    if (e == cudaSuccess) e = cudaMalloc(&C.val, sizeof(double) * std::max<i64>(1, C.nnz));
-    if (e != cudaSuccess) { cudaFree(d_cnt); cudaFree(d_skip); err = "cudaMalloc (SpGEMM output)"; return (int)e; }
+    e = dev_malloc((void**)&C.ptr, sizeof(i64) * (n + 1));
+    if (e == cudaSuccess) e = dev_malloc((void**)&C.col, sizeof(i32) * std::max<i64>(1, C.nnz));
+    if (e == cudaSuccess) e = dev_malloc((void**)&C.val, sizeof(double) * std::max<i64>(1, C.nnz));
+    if (e != cudaSuccess) { dev_free(d_cnt); dev_free(d_skip); err = "cudaMalloc (SpGEMM output)"; return (int)e; }
     cudaMemcpyAsync(C.ptr, ptr.data(), sizeof(i64) * (n + 1), cudaMemcpyHostToDevice, st);
     k_spgemm_rows<true><<<grid, threads, smem, st>>>(n, A.ptr, A.col, A.val, B.ptr, B.col, B.val, n2, nullptr,
                                                      C.ptr, C.col, C.val, d_skip);
@@ -651,16 +651,16 @@ int spgemm_device(const DevCSR& A, const DevCSR& B, DevCSR& C, void* stream, std
         cudaMemcpyAsync(C.val + o, lvals[q].data(), sizeof(double) * lvals[q].size(), cudaMemcpyHostToDevice, st);
     }
     e = cudaStreamSynchronize(st);
-    cudaFree(d_cnt);
-    cudaFree(d_skip);
+    dev_free(d_cnt);
+    dev_free(d_skip);
     if (e != cudaSuccess) { err = "SpGEMM kernel"; return (int)e; }
     return (int)cudaGetLastError();
 }
 
 void free_dev_csr(DevCSR& M) {
-    if (M.ptr) cudaFree(M.ptr);
-    if (M.col) cudaFree(M.col);
-    if (M.val) cudaFree(M.val);
+    if (M.ptr) dev_free(M.ptr);
+    if (M.col) dev_free(M.col);
+    if (M.val) dev_free(M.val);
     M = DevCSR();
 }
 
@@ -669,9 +669,9 @@ int upload_csr(const HostCSR& H, DevCSR& D, void* stream) {
     D.nrows = H.nrows;
     D.ncols = H.ncols;
     D.nnz = H.nnz();
-    cudaError_t e = cudaMalloc(&D.ptr, sizeof(i64) * (H.nrows + 1));
-    if (e == cudaSuccess) e = cudaMalloc(&D.col, sizeof(i32) * std::max<i64>(1, D.nnz));
-    if (e == cudaSuccess) e = cudaMalloc(&D.val, sizeof(double) * std::max<i64>(1, D.nnz));
+    cudaError_t e = dev_malloc((void**)&D.ptr, sizeof(i64) * (H.nrows + 1));
+    if (e == cudaSuccess) e = dev_malloc((void**)&D.col, sizeof(i32) * std::max<i64>(1, D.nnz));
+    if (e == cudaSuccess) e = dev_malloc((void**)&D.val, sizeof(double) * std::max<i64>(1, D.nnz));
     if (e != cudaSuccess) return (int)e;
     cudaMemcpyAsync(D.ptr, H.ptr.data(), sizeof(i64) * (H.nrows + 1), cudaMemcpyHostToDevice, st);
     cudaMemcpyAsync(D.col, H.col.data(), sizeof(i32) * D.nnz, cudaMemcpyHostToDevice, st);

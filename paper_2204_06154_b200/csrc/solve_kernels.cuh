@@ -173,81 +173,6 @@ __global__ void __launch_bounds__(256) k_gs_colour(int r0, int r1, int Wu, const
     }
 }
 
-// One colour of the sweep on a LARGE level, streamed: one CTA per SM takes a contiguous
-// block of the colour's rows and walks it in passes of blockDim/TPR rows, with the operator
-// rows of pass p+1 loaded (double buffer in registers) while pass p gathers and updates.
-// The CTA uses under half an SM's registers, so the NEXT colour's CTAs (PDL: launched when
-// this grid triggers at its start) are co-resident and load their first pass before their
-// griddepcontrol.wait -- the colour-to-colour handoff no longer starts from cold.  (The
-// one-wave k_gs_colour holds the whole colour in registers, so no next-colour CTA fits.)
-// Wu > 0: every SELL slice has width Wu (level 0: the stencil size), so the slice offset is
-// computed instead of loaded.  Same per-row arithmetic as k_gs_colour.
-template <int TPR, int CH>
-__global__ void __launch_bounds__(256) k_gs_colour_pipe(int r0, int r1, int rows_per_cta, int Wu,
-                                                        const int64_t* __restrict__ sptr,
-                                                        const int* __restrict__ scol,
-                                                        const double* __restrict__ sval,
-                                                        const double* __restrict__ f, double* u) {
-    pdl_trigger();
-    const int c0 = r0 + blockIdx.x * rows_per_cta;
-    const int c1 = min(r1, c0 + rows_per_cta);
-    const int part = threadIdx.x % TPR;
-    const int per_pass = blockDim.x / TPR;
-    auto slot = [&](int r, int& w, int64_t& base) {
-        if (Wu > 0) {
-            w = Wu;
-            base = (int64_t)(r >> 5) * 32 * Wu + (r & 31);
-        } else {
-            const int64_t s0 = sptr[r >> 5];
-            w = (int)((sptr[(r >> 5) + 1] - s0) >> 5);
-            base = s0 + (r & 31);
-        }
-    };
-    RowFrag<TPR, CH> fa, fb;
-    int wa = 0, wb = 0;
-    int64_t ba = 0, bb = 0;
-    double da = 1.0, db = 1.0;
-    int ra = c0 + (int)threadIdx.x / TPR;
-    if (ra < c1) {
-        slot(ra, wa, ba);
-        fa.load(sval + ba, scol + ba, wa, part);
-        da = ld_stream_f64(sval + ba);
-    } else {
-        fa.load(sval, scol, 0, 0);
-    }
-    pdl_wait();
-    for (int pb = c0; pb < c1; pb += per_pass) {
-        const int rn = ra + per_pass;  // next pass
-        if (rn < c1) {
-            slot(rn, wb, bb);
-            fb.load(sval + bb, scol + bb, wb, part);
-            db = ld_stream_f64(sval + bb);
-        } else {
-            wb = 0;
-            fb.load(sval, scol, 0, 0);
-        }
-        const bool live = ra < c1;
-        double fr_v = 0.0, ur = 0.0;
-        if (live && part == 0) {
-            fr_v = f[ra];
-            ur = u[ra];
-        }
-        double acc = fa.dot(u, 0.0);
-        for (int k0 = part + TPR * CH; k0 < wa; k0 += TPR * CH) {
-            RowFrag<TPR, CH> t;
-            t.load(sval + ba, scol + ba, wa, k0);
-            acc = t.dot(u, acc);
-        }
-        acc = group_sum<TPR>(acc);
-        if (live && part == 0) u[ra] = ur + (fr_v - acc) / da;
-        fa = fb;
-        wa = wb;
-        ba = bb;
-        da = db;
-        ra = rn;
-    }
-}
-
 // y = L x  (MODE 0),  y = f - L x  (MODE 1) on the rows [r0, r1).
 // MODE 2: the residual right after a forward Gauss-Seidel sweep from a ZERO guess,
 // y = f - L u = -sum_{later colours} a_ij u_j: the sweep made every row's residual zero when
@@ -580,16 +505,6 @@ __global__ void __launch_bounds__(RED_THREADS) k_multiaxpy_norm(int64_t n, const
         partials[blockIdx.x] = t;
     }
     finish_partials(partials, 1, ticket, nrm2, nullptr);
-}
-
-// out[j] = scale * sum_b partials[b*k1 + j] (+ out0[j] if accumulate)
-__global__ void k_reduce_partials(const double* __restrict__ partials, int nblk, int k1,
-                                  double* __restrict__ out) {
-    for (int j = threadIdx.x; j < k1; j += blockDim.x) {
-        double t = 0.0;
-        for (int b = 0; b < nblk; ++b) t += partials[(int64_t)b * k1 + j];
-        out[j] = t;
-    }
 }
 
 // w[i] -= sum_j V_j[i] * h[j]

@@ -47,6 +47,15 @@ class Report(ctypes.Structure):
 
 
 _vp = ctypes.c_void_p
+ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p)
+RELEASE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p)
+
+
+class Allocator(ctypes.Structure):
+    """mgm_allocator: device allocations of a ctx (include/mgm.h)."""
+    _fields_ = [("alloc", ALLOC_FN), ("release", RELEASE_FN), ("user", ctypes.c_void_p)]
+
+
 _i64 = ctypes.c_int64
 _i64p = ctypes.POINTER(ctypes.c_int64)
 _i32p = ctypes.POINTER(ctypes.c_int32)
@@ -54,11 +63,11 @@ _f64p = ctypes.POINTER(ctypes.c_double)
 
 _SIGS = {
     "mgm_setup": ([_f64p, _f64p, _i64, ctypes.POINTER(StencilParams), ctypes.POINTER(LevelParams),
-                   _vp, ctypes.POINTER(_vp)], ctypes.c_int),
+                   ctypes.POINTER(Allocator), _vp, ctypes.POINTER(_vp)], ctypes.c_int),
     "mgm_vcycle": ([_vp, _vp, _vp, _vp], ctypes.c_int),
-    "mgm_solve": ([_vp, _vp, _vp, ctypes.c_double, ctypes.c_int, ctypes.c_int,
+    "mgm_solve": ([_vp, _vp, _vp, _vp, ctypes.c_double, ctypes.c_int, ctypes.c_int,
                    ctypes.POINTER(Report), _vp], ctypes.c_int),
-    "mgm_solve_host": ([_vp, _vp, _vp, ctypes.c_double, ctypes.c_int, ctypes.c_int,
+    "mgm_solve_host": ([_vp, _vp, _vp, _vp, ctypes.c_double, ctypes.c_int, ctypes.c_int,
                         ctypes.POINTER(Report), _vp], ctypes.c_int),
     "mgm_destroy": ([_vp], ctypes.c_int),
     "mgm_nccl_unique_id": ([_vp], ctypes.c_int),
@@ -135,9 +144,33 @@ def _stream_ptr(stream):
     return stream.cuda_stream
 
 
+def torch_allocator():
+    """An mgm_allocator that takes the ctx's device memory from PyTorch's caching allocator
+    (marshalling only: the callbacks forward to torch.cuda.caching_allocator_alloc/_delete).
+    Keep the returned object alive as long as the ctx."""
+    import torch
+
+    dev = torch.cuda.current_device()
+
+    def _alloc(nbytes, user):
+        try:
+            return torch.cuda.caching_allocator_alloc(max(int(nbytes), 1), device=dev)
+        except Exception:
+            return None
+
+    def _release(ptr, user):
+        torch.cuda.caching_allocator_delete(ptr)
+
+    a = Allocator(ALLOC_FN(_alloc), RELEASE_FN(_release), None)
+    a._keep = (_alloc, _release)
+    return a
+
+
 # ---------------------------------------------------------------- ABI-named functions
-def mgm_setup(points: np.ndarray, normals: np.ndarray, stencil: dict, levels: dict, stream=None):
-    """Returns an opaque ctx handle (c_void_p).  Raises MGMError on failure."""
+def mgm_setup(points: np.ndarray, normals: np.ndarray, stencil: dict, levels: dict, stream=None,
+              allocator: Allocator | None = None):
+    """Returns an opaque ctx handle (c_void_p).  Raises MGMError on failure.  allocator: an
+    :class:`Allocator` (e.g. :func:`torch_allocator`) or None for cudaMalloc."""
     lib = load_library()
     pts = np.ascontiguousarray(points, dtype=np.float64)
     nrm = np.ascontiguousarray(normals, dtype=np.float64)
@@ -152,8 +185,8 @@ def mgm_setup(points: np.ndarray, normals: np.ndarray, stencil: dict, levels: di
                      restart=levels.get("restart", 50))
     ctx = _vp()
     st = lib.mgm_setup(_ptr(pts, _f64p), _ptr(nrm, _f64p), len(pts), ctypes.byref(sp),
-                       ctypes.byref(lp), _vp(_stream_ptr(stream) if stream is not None else 0),
-                       ctypes.byref(ctx))
+                       ctypes.byref(lp), ctypes.byref(allocator) if allocator is not None else None,
+                       _vp(_stream_ptr(stream) if stream is not None else 0), ctypes.byref(ctx))
     if st != MGM_OK:
         idx = _i64(-1)
         msg = lib.mgm_last_error(None, ctypes.byref(idx)).decode()
@@ -189,22 +222,27 @@ def _report(rep, hist):
                        list(hist[:n]), rep.lambda_, rep.setup_ms, rep.solve_ms)
 
 
-def mgm_solve(ctx, rhs, x, tol=1e-10, maxit=500, krylov=1, stream=None, history_cap=1024):
+def mgm_solve(ctx, rhs, x, tol=1e-10, maxit=500, krylov=1, stream=None, history_cap=1024, x0=None):
+    """x0: initial guess (torch CUDA tensor, may be x itself) or None for x0 = 0."""
     hist = np.zeros(history_cap)
     rep = Report(history=_ptr(hist, _f64p), history_cap=history_cap)
-    _check(load_library().mgm_solve(ctx, _vp(rhs.data_ptr()), _vp(x.data_ptr()), tol, maxit, krylov,
-                                    ctypes.byref(rep), _vp(_stream_ptr(stream))), ctx)
+    _check(load_library().mgm_solve(ctx, _vp(rhs.data_ptr()), _vp(x0.data_ptr()) if x0 is not None else None,
+                                    _vp(x.data_ptr()), tol, maxit, krylov, ctypes.byref(rep),
+                                    _vp(_stream_ptr(stream))), ctx)
     return _report(rep, hist)
 
 
 def mgm_solve_host(ctx, rhs: np.ndarray, x: np.ndarray, tol=1e-10, maxit=500, krylov=1,
-                   stream=None, history_cap=1024):
-    """rhs / x: host arrays (numpy, or pinned torch CPU tensors via .numpy())."""
+                   stream=None, history_cap=1024, x0: np.ndarray | None = None):
+    """rhs / x / x0: host arrays (numpy, or pinned torch CPU tensors via .numpy())."""
     hist = np.zeros(history_cap)
     rep = Report(history=_ptr(hist, _f64p), history_cap=history_cap)
     assert rhs.dtype == np.float64 and x.dtype == np.float64 and x.flags.c_contiguous
-    _check(load_library().mgm_solve_host(ctx, _vp(rhs.ctypes.data), _vp(x.ctypes.data), tol, maxit,
-                                         krylov, ctypes.byref(rep), _vp(_stream_ptr(stream))), ctx)
+    if x0 is not None:
+        assert x0.dtype == np.float64 and x0.flags.c_contiguous
+    _check(load_library().mgm_solve_host(ctx, _vp(rhs.ctypes.data), _vp(x0.ctypes.data) if x0 is not None else None,
+                                         _vp(x.ctypes.data), tol, maxit, krylov, ctypes.byref(rep),
+                                         _vp(_stream_ptr(stream))), ctx)
     return _report(rep, hist)
 
 
@@ -383,14 +421,15 @@ def mgm_host_colouring(ptr, col):
 class MGM:
     """Owns one libmgm context.  Vectors are torch CUDA float64 tensors in original order."""
 
-    def __init__(self, points, normals, stencil: dict, levels: dict):
+    def __init__(self, points, normals, stencil: dict, levels: dict, torch_memory: bool = False):
         import torch
 
         if not torch.cuda.is_available():
             raise RuntimeError("libmgm needs a CUDA device")
         self.n = len(points)
         self.stencil, self.levels = dict(stencil), dict(levels)
-        self.ctx = mgm_setup(points, normals, stencil, levels)
+        self._alloc = torch_allocator() if torch_memory else None
+        self.ctx = mgm_setup(points, normals, stencil, levels, allocator=self._alloc)
         self.p = mgm_num_levels(self.ctx)
 
     def close(self):
@@ -408,12 +447,12 @@ class MGM:
         mgm_vcycle(self.ctx, f, u, stream)
         return u
 
-    def solve(self, rhs, x=None, tol=1e-10, maxit=500, krylov=1, stream=None):
+    def solve(self, rhs, x=None, tol=1e-10, maxit=500, krylov=1, stream=None, x0=None):
         import torch
 
         if x is None:
             x = torch.empty_like(rhs)
-        rep = mgm_solve(self.ctx, rhs, x, tol, maxit, krylov, stream)
+        rep = mgm_solve(self.ctx, rhs, x, tol, maxit, krylov, stream, x0=x0)
         return x, rep
 
     def level_info(self):

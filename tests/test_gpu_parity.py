@@ -283,6 +283,62 @@ def test_solve(name, krylov):
         assert abs(xg.sum()) <= 1e-8 * len(xg)
 
 
+@pytest.mark.parametrize("name", ["cfg1", "torus20000", "poisson6000"])
+@pytest.mark.parametrize("krylov", [1, 0, 2])
+def test_warm_start_x0(name, krylov):
+    """mgm_solve with an initial guess x0 (the applications' warm start from the previous
+    step): GPU vs oracle from the same x0 -- iterations within +-1 (+-2 BiCGSTAB),
+    solutions to 1e-9; x0 may alias x; the host path takes x0 too."""
+    import torch
+    from paper_2204_06154_b200 import mgm_solve_host
+
+    P = pair(name)
+    if krylov == 0 and name == "poisson6000":
+        pytest.skip("standalone MGM converges slowly on this cloud (P:411)")
+    rhs = P.w.rhs
+    xr0, _ = P.ref.solve(rhs, tol=1e-6, krylov=1)
+    x0 = 0.9 * xr0 + 0.01 * _rand(len(rhs), 77)           # a nearby previous-step solution
+    xr, rr = P.ref.solve(rhs, tol=1e-10, krylov=krylov, maxit=300, x0=x0)
+    x = torch.from_numpy(x0.copy()).cuda()
+    _, rep = P.gpu.solve(torch.from_numpy(rhs).cuda(), x, tol=1e-10, krylov=krylov, maxit=300, x0=x)
+    assert rep.converged and rr.converged and rep.final_rel_residual <= 1e-10
+    assert abs(rep.iterations - rr.iterations) <= (2 if krylov == 2 else 1), (rep.iterations, rr.iterations)
+    xg = x.cpu().numpy()
+    assert np.linalg.norm(xg - xr) / np.linalg.norm(xr) <= 1e-9
+    if krylov == 1:
+        _, cold = P.ref.solve(rhs, tol=1e-10, krylov=1)
+        assert rr.iterations < cold.iterations            # the warm start pays
+        xh = np.empty(len(rhs))
+        reph = mgm_solve_host(P.gpu.ctx, np.ascontiguousarray(rhs), xh, tol=1e-10, x0=np.ascontiguousarray(x0))
+        assert reph.iterations == rep.iterations and np.array_equal(xh, xg)
+
+
+def test_torch_allocator():
+    """mgm_setup with an allocator hook (PyTorch's caching allocator): same V-cycle and solve,
+    bitwise, as the cudaMalloc ctx; the memory shows up in torch's allocator statistics."""
+    import torch
+    from paper_2204_06154_b200 import MGM
+
+    P = pair("torus20000")
+    before = torch.cuda.memory_allocated()
+    m2 = MGM(P.w.points, P.w.normals, P.w.stencil, P.w.levels, torch_memory=True)
+    assert torch.cuda.memory_allocated() - before > 10 * 2 ** 20
+    n = len(P.w.points)
+    f = torch.from_numpy(_rand(n, 3)).cuda()
+    u1 = torch.from_numpy(_rand(n, 4)).cuda()
+    u2 = u1.clone()
+    P.gpu.vcycle(f, u1)
+    m2.vcycle(f, u2)
+    assert torch.equal(u1, u2)
+    rhs = torch.from_numpy(P.w.rhs).cuda()
+    x1, r1 = P.gpu.solve(rhs, tol=1e-10)
+    x2, r2 = m2.solve(rhs, tol=1e-10)
+    assert r1.iterations == r2.iterations and torch.equal(x1, x2)
+    held = torch.cuda.memory_allocated()
+    m2.close()
+    assert held - torch.cuda.memory_allocated() > 10 * 2 ** 20     # released through the hook
+
+
 def test_zero_rhs_and_host_path():
     import torch
     from paper_2204_06154_b200 import mgm_solve_host

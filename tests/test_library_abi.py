@@ -35,7 +35,7 @@ def test_setup_rejects_null_arguments():
 
     lib = P.load_library()
     ctx = ctypes.c_void_p()
-    st = lib.mgm_setup(None, None, 0, None, None, None, ctypes.byref(ctx))
+    st = lib.mgm_setup(None, None, 0, None, None, None, None, ctypes.byref(ctx))
     assert st == P.mgm.MGM_ERR_ARG and not ctx.value
     assert lib.mgm_vcycle(None, None, None, None) == P.mgm.MGM_ERR_ARG
 
