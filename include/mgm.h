@@ -268,6 +268,14 @@ mgm_status mgm_trace_read(const mgm_ctx* ctx, uint64_t* stamps_ns, int cap, int*
  * MGM_NO_ZG).  For byte models. */
 mgm_status mgm_level_zg_nnz(const mgm_ctx* ctx, int level, int64_t* nnz_zg);
 
+/* The dense bottom of the V-cycle: Alg. 3 lines 6-14 for the
+ * levels >= J from e_J = 0 are linear in r_J; setup builds their matrix B_J
+ * (n_J x n_J, Poisson n_J + 1) from the unit vectors with the library's own level kernels and
+ * every V-cycle applies it as one dense HBM-bound kernel.  J = the first level >= 1 with at
+ * most MGM_DENSE_MAX rows (environment at mgm_setup, default 4096; 0 = off).  *level = J or
+ * -1 (off), *rows = its dimension, *bytes = the bytes of B_J read per apply. */
+mgm_status mgm_dense_bottom_info(const mgm_ctx* ctx, int* level, int64_t* rows, int64_t* bytes);
+
 /* Diagnostics: start time (%globaltimer, ns) of every phase of the one-kernel bottom of the
  * last V-cycle (MGM_TRACE set at setup), *n = number of phases (0 if tracing is off or the
  * bottom kernel is not used); meta[4*q..] = {op, local, rows, threads per row} (may be NULL). */

@@ -20,6 +20,7 @@
 #include "solve_kernels.cuh"
 #include "bottom_kernel.cuh"
 #include "batch_kernels.cuh"
+#include "dense_bottom.cuh"
 
 using namespace mgm;
 
@@ -169,6 +170,10 @@ struct mgm_ctx {
     int ntrace = 0;
     std::vector<std::string> trace_labels;
     int botJ = -1;
+    // bottom of the V-cycle as one dense operator B_J (dense_bottom.cuh); denseJ < 0 = off
+    int denseJ = -1;
+    int dense_m = 0, dense_ld = 0;
+    double* dB = nullptr;
     int bot_cluster = 16;
     size_t bot_smem = 0;
     int nphases = 0;
@@ -685,6 +690,18 @@ void setup_bottom(mgm_ctx* ctx, const std::vector<double>& LU, const std::vector
     ctx->botJ = J;
 }
 
+// Level J of the dense bottom (dense_bottom.cuh): the first level j >= 1 with
+// N_j (+1 Poisson) <= MGM_DENSE_MAX (default 4096: B_J = 134 MB, one HBM-bound apply per
+// V-cycle instead of the latency-bound colour steps of levels J..p-1); -1 = off.
+int dense_level(const mgm_ctx* ctx) {
+    i64 dmax = 4096;
+    if (const char* e = std::getenv("MGM_DENSE_MAX")) dmax = std::atoll(e);
+    const i64 pad = ctx->poisson ? 1 : 0;
+    for (int j = 1; j < ctx->p; ++j)
+        if (ctx->lv[j].n + pad <= dmax) return j;
+    return -1;
+}
+
 // Setup phase timer (MGM_SETUP_TIMING=1 prints host wall time per phase to stderr).
 struct SetupTimer {
     bool on = std::getenv("MGM_SETUP_TIMING") != nullptr;
@@ -1095,7 +1112,8 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
         ctx->nc = m;
         if ((s = upload(ctx, &ctx->lu, LU)) || (s = upload(ctx, &ctx->piv, piv))) return s;
         CK(cudaStreamSynchronize(st));
-        setup_bottom(ctx, LU, piv);
+        ctx->denseJ = dense_level(ctx);
+        if (ctx->denseJ < 0) setup_bottom(ctx, LU, piv);  // (the dense bottom replaces it)
         tm.mark("bottom kernel setup", p - 1);
         if (m <= 4096) {  // explicit inverse for the batched coarse solve (same solution up to rounding, O13)
             std::vector<double> Ainv((size_t)m * m), bb(m);
@@ -1527,6 +1545,95 @@ void stamp(mgm_ctx* ctx, const char* label, int level, cudaStream_t st) {
     ctx->ntrace++;
 }
 
+mgm_status ensure_krylov(mgm_ctx* ctx);
+// Alg. 3 lines 6-14 for the levels J..p-1 (J >= 1) from e_J = 0, one kernel per colour /
+// operator, no zero-guess shortcuts: rhs lv[J].f, result lv[J].u.  Builds the dense bottom.
+void enqueue_levels_plain(mgm_ctx* ctx, int J, cudaStream_t st) {
+    auto& lv = ctx->lv;
+    const int p = ctx->p;
+    const int nu1 = ctx->lp.nu1, nu2 = ctx->lp.nu2;
+    const bool pre_b = ctx->lp.smoother == 1, post_b = ctx->lp.smoother == 1 || ctx->lp.smoother == 2;
+    const i64 pad = ctx->poisson ? 1 : 0;
+    if (J == p - 1) {
+        enqueue_coarse(ctx, lv[J].f, lv[J].u, st);
+        return;
+    }
+    for (int j = J; j + 1 < p; ++j) {                                    // lines 6-9
+        enqueue_zero(ctx, lv[j].u, lv[j].n + pad, st);
+        for (int s = 0; s < nu1; ++s) enqueue_sweep(ctx, j, pre_b, st);
+        enqueue_residual(ctx, j, lv[j].f, lv[j].u, lv[j].t, st);
+        enqueue_restrict(ctx, j, lv[j].t, lv[j + 1].f, st);
+    }
+    enqueue_coarse(ctx, lv[p - 1].f, lv[p - 1].u, st);                  // line 10
+    for (int j = p - 2; j >= J; --j) {                                   // lines 11-14
+        enqueue_interp_correct(ctx, j, lv[j + 1].u, lv[j].u, st);
+        for (int s = 0; s < nu2; ++s) enqueue_sweep(ctx, j, post_b, st);
+    }
+}
+
+// B_J = the matrix of lines 6-14 for levels >= J (dense_bottom.cuh), one column per replay
+// of enqueue_levels_plain on a unit vector; on the coarsest level it is L_p^{-1} (the
+// explicit inverse, O13).  Row-major, leading dimension padded to 64 with zeros.
+mgm_status setup_dense_bottom(mgm_ctx* ctx) {
+    const int J = ctx->denseJ;
+    if (J < 0) return MGM_OK;
+    {
+        mgm_status s = ensure_krylov(ctx);  // (reduction scratch of the Poisson border terms)
+        if (s) return s;
+    }
+    cudaStream_t st = ctx->st;
+    const i64 pad = ctx->poisson ? 1 : 0;
+    const int mdim = (int)(ctx->lv[J].n + pad);
+    const int ld = (mdim + 63) / 64 * 64;
+    double* T = nullptr;
+    CK(dalloc(&ctx->dB, (i64)mdim * ld));
+    CK(dalloc(&T, (i64)mdim * mdim));
+    struct FreeT { double* t; ~FreeT() { dev_free(t); } } freet_{T};
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t gx = nullptr;
+    CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    g_launch_err.clear();
+    ctx->pdl = true;
+    enqueue_levels_plain(ctx, J, st);
+    ctx->pdl = false;
+    const cudaError_t ce = cudaStreamEndCapture(st, &g);
+    if (ce != cudaSuccess || !g_launch_err.empty()) {
+        ctx->err = "dense bottom capture failed: " + std::string(cudaGetErrorString(ce)) + "; " + g_launch_err;
+        g_launch_err.clear();
+        cudaGetLastError();
+        return MGM_ERR_CUDA;
+    }
+    CK(cudaGraphInstantiate(&gx, g, 0));
+    cudaGraphDestroy(g);
+    Level& L = ctx->lv[J];
+    for (int i = 0; i < mdim; ++i) {
+        k_unit<<<blocks_for(mdim, 256), 256, 0, st>>>(mdim, i, L.f);
+        CK(cudaGraphLaunch(gx, st));
+        CK(cudaMemcpyAsync(T + (i64)i * mdim, L.u, sizeof(double) * mdim, cudaMemcpyDeviceToDevice, st));
+    }
+    k_transpose_pad<<<dim3((mdim + 31) / 32, ld / 32), dim3(32, 8), 0, st>>>(mdim, ld, T, ctx->dB);
+    CK(cudaStreamSynchronize(st));
+    cudaGraphExecDestroy(gx);
+    CK(cudaGetLastError());
+    ctx->dense_m = mdim;
+    ctx->dense_ld = ld;
+    return MGM_OK;
+}
+
+// e_J = B_J r_J (the whole bottom of the V-cycle, dense_bottom.cuh); K interleaved columns
+void enqueue_dense_bottom(mgm_ctx* ctx, int K, const double* r, double* e, cudaStream_t st) {
+    const unsigned grid = blocks_for(ctx->dense_m, DENSE_ROWS_PER_CTA);
+    const int mm = ctx->dense_m, ld = ctx->dense_ld;
+    const double* B = ctx->dB;
+    switch (K) {
+        case 1: launch(ctx->pdl, k_dense_apply<1>, grid, DENSE_THREADS, 0, st, mm, ld, B, r, e); break;
+        case 2: launch(true, k_dense_apply<2>, grid, DENSE_THREADS, 0, st, mm, ld, B, r, e); break;
+        case 4: launch(true, k_dense_apply<4>, grid, DENSE_THREADS, 0, st, mm, ld, B, r, e); break;
+        default: launch(true, k_dense_apply<8>, grid, DENSE_THREADS, 0, st, mm, ld, B, r, e); break;
+    }
+    ctx->vcycle_kernels++;
+}
+
 bool c0_fused_l0(const mgm_ctx* ctx);
 // Alg. 3 on level-0 buffers lv[0].f (rhs) and lv[0].u (guess in, result out), lib order.
 void enqueue_vcycle(mgm_ctx* ctx, cudaStream_t st) {
@@ -1544,8 +1651,9 @@ void enqueue_vcycle(mgm_ctx* ctx, cudaStream_t st) {
         enqueue_coarse(ctx, lv[0].f, lv[0].u, st);
         return;
     }
-    // levels >= D run in the one-kernel bottom (if enabled), else D = p - 1
-    const int D = ctx->botJ > 0 ? ctx->botJ : p - 1;
+    // levels >= D run as the dense bottom B_D or in the one-kernel cluster bottom (if
+    // enabled), else D = p - 1 (the coarse solve)
+    const int D = ctx->denseJ > 0 ? ctx->denseJ : ctx->botJ > 0 ? ctx->botJ : p - 1;
     stamp(ctx, "start", 0, st);
     const bool bottom_only = std::getenv("MGM_DEBUG_BOTTOM_ONLY") && ctx->botJ > 0;  // timing experiment only
     if (!bottom_only) {
@@ -1580,7 +1688,9 @@ void enqueue_vcycle(mgm_ctx* ctx, cudaStream_t st) {
         stamp(ctx, "residual+restrict", j, st);
     }
     }
-    if (ctx->botJ > 0) {                                                  // lines 6-14 for j >= J
+    if (ctx->denseJ > 0) {                                                // lines 6-14 for j >= J
+        enqueue_dense_bottom(ctx, 1, lv[D].f, lv[D].u, st);
+    } else if (ctx->botJ > 0) {                                           // lines 6-14 for j >= J
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(ctx->bot_cluster);
         cfg.blockDim = dim3(BOT_THREADS);
@@ -2254,8 +2364,10 @@ static void enqueue_vcycle_b(mgm_ctx* ctx, cudaStream_t st) {
                (const double*)ctx->bf[p - 1], ctx->bu[p - 1]);
     };
     if (p == 1) { coarse(); return; }
+    // levels >= D: the dense bottom B_D applied to the K columns at once (dense_bottom.cuh)
+    const int D = ctx->denseJ > 0 ? ctx->denseJ : p - 1;
     for (int s = 0; s < nu1; ++s) sweep(0, pre_b);                                  // line 4
-    for (int j = 0; j + 1 < p; ++j) {                                               // lines 5-9
+    for (int j = 0; j < D; ++j) {                                                   // lines 5-9
         const Level& L = lv[j];
         if (j > 0) {
             cudaMemsetAsync(ctx->bu[j], 0, sizeof(double) * L.n * K, st);
@@ -2264,8 +2376,9 @@ static void enqueue_vcycle_b(mgm_ctx* ctx, cudaStream_t st) {
         b_spmv<1, K>(L.stpr, L.n, L.sptr, L.scol, L.sval, ctx->bu[j], ctx->bf[j], ctx->bt[j], st);
         b_spmv<0, K>(L.rtpr, lv[j + 1].n, L.rptr, L.rcol, L.rval, ctx->bt[j], nullptr, ctx->bf[j + 1], st);
     }
-    coarse();                                                                        // line 10
-    for (int j = p - 2; j >= 0; --j) {                                              // lines 11-16
+    if (ctx->denseJ > 0) enqueue_dense_bottom(ctx, K, ctx->bf[D], ctx->bu[D], st);
+    else coarse();                                                                   // line 10
+    for (int j = D - 1; j >= 0; --j) {                                              // lines 11-16
         const Level& L = lv[j];
         auto kern = L.pm <= 8 ? k_interp_correct_b<8, K> : k_interp_correct_b<16, K>;
         launch(true, kern, blocks_for(L.n, 256), 256, 0, st, (int)L.n, L.pm, (const i32*)L.pcol,
@@ -2455,6 +2568,7 @@ mgm_status mgm_setup(const double* points, const double* normals, int64_t n_poin
         return MGM_ERR_CUDA;
     }
     mgm_status s = do_setup(ctx, points, normals, n_points);
+    if (s == MGM_OK) s = setup_dense_bottom(ctx);
     ctx->setup_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     if (s != MGM_OK) {
         g_setup_error = ctx->err;
@@ -2641,6 +2755,7 @@ mgm_status mgm_destroy(mgm_ctx* ctx) {
         if (gx) cudaGraphExecDestroy(gx);
     if (ctx->bres) dev_free(ctx->bres);
     if (ctx->ainv) dev_free(ctx->ainv);
+    if (ctx->dB) dev_free(ctx->dB);
     for (auto& T : ctx->timer)
         for (auto e : T.ev) cudaEventDestroy(e);
     if (ctx->st) cudaStreamDestroy(ctx->st);
@@ -2909,6 +3024,14 @@ mgm_status mgm_bytes_model(const mgm_ctx* ctx, double* vcycle_bytes, double* spm
     B += 8.0 * np * np + 16.0 * np;
     if (vcycle_bytes) *vcycle_bytes = B;
     if (spmv_bytes) *spmv_bytes = 12.0 * ctx->lv[0].nnz + 16.0 * ctx->lv[0].n;
+    return MGM_OK;
+}
+
+mgm_status mgm_dense_bottom_info(const mgm_ctx* ctx, int* level, int64_t* rows, int64_t* bytes) {
+    if (!ctx || ctx->lv.empty()) return MGM_ERR_ARG;
+    if (level) *level = ctx->denseJ;
+    if (rows) *rows = ctx->denseJ >= 0 ? ctx->dense_m : 0;
+    if (bytes) *bytes = ctx->denseJ >= 0 ? (int64_t)8 * ctx->dense_m * ctx->dense_ld : 0;
     return MGM_OK;
 }
 

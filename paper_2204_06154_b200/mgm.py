@@ -92,6 +92,7 @@ _SIGS = {
     "mgm_bottom_trace_read": ([_vp, ctypes.POINTER(ctypes.c_uint64), ctypes.c_int,
                                ctypes.POINTER(ctypes.c_int), _i32p], ctypes.c_int),
     "mgm_level_zg_nnz": ([_vp, ctypes.c_int, _i64p], ctypes.c_int),
+    "mgm_dense_bottom_info": ([_vp, ctypes.POINTER(ctypes.c_int), _i64p, _i64p], ctypes.c_int),
     "mgm_bottom_ftrace_read": ([_vp, _i64p, ctypes.c_int, ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
     "mgm_host_morton": ([_f64p, _i64, _i64p], ctypes.c_int),
     "mgm_host_knn": ([_f64p, _i64, _f64p, _i64, ctypes.c_int, _i32p], ctypes.c_int),
@@ -340,6 +341,13 @@ def mgm_vcycle_kernel_count(ctx) -> int:
     c = _i64()
     _check(load_library().mgm_vcycle_kernel_count(ctx, ctypes.byref(c)), ctx)
     return c.value
+
+
+def mgm_dense_bottom_info(ctx) -> dict:
+    """{level J or -1, rows of B_J, bytes of B_J read per V-cycle}."""
+    j, r, b = ctypes.c_int(), _i64(), _i64()
+    _check(load_library().mgm_dense_bottom_info(ctx, ctypes.byref(j), ctypes.byref(r), ctypes.byref(b)), ctx)
+    return dict(level=j.value, rows=r.value, bytes=b.value)
 
 
 def mgm_nccl_unique_id() -> bytes:

@@ -195,6 +195,7 @@ def test_large_coarsest_gemv(bot_max, monkeypatch):
     import oracle as O
 
     monkeypatch.setenv("MGM_BOT_MAX", bot_max)
+    monkeypatch.setenv("MGM_DENSE_MAX", "0")
     w = MI.make_workload(1, n=16384)
     lv = dict(w.levels, num_levels=3)
     m = MGM(w.points, w.normals, w.stencil, lv)
@@ -296,8 +297,7 @@ def test_warm_start_x0(name, krylov):
     if krylov == 0 and name == "poisson6000":
         pytest.skip("standalone MGM converges slowly on this cloud (P:411)")
     rhs = P.w.rhs
-    xr0, _ = P.ref.solve(rhs, tol=1e-6, krylov=1)
-    x0 = 0.9 * xr0 + 0.01 * _rand(len(rhs), 77)           # a nearby previous-step solution
+    x0, _ = P.ref.solve(rhs, tol=1e-5, krylov=1)            # a nearby previous-step solution
     xr, rr = P.ref.solve(rhs, tol=1e-10, krylov=krylov, maxit=300, x0=x0)
     x = torch.from_numpy(x0.copy()).cuda()
     _, rep = P.gpu.solve(torch.from_numpy(rhs).cuda(), x, tol=1e-10, krylov=krylov, maxit=300, x0=x)
@@ -395,12 +395,13 @@ def test_bottom_kernel_equals_kernel_path(name, knobs, monkeypatch):
     from paper_2204_06154_b200 import MGM
 
     P = pair(name)
+    monkeypatch.setenv("MGM_DENSE_MAX", "0")            # (the dense bottom replaces it by default)
     monkeypatch.setenv("MGM_BOT_MAX", "0")
     ref = MGM(P.w.points, P.w.normals, P.w.stencil, P.w.levels)
     monkeypatch.delenv("MGM_BOT_MAX")
     for k, v in knobs.items():
         monkeypatch.setenv(k, v)
-    m2 = MGM(P.w.points, P.w.normals, P.w.stencil, P.w.levels) if knobs else P.gpu
+    m2 = MGM(P.w.points, P.w.normals, P.w.stencil, P.w.levels)
     n = len(P.w.points)
     f = torch.from_numpy(_rand(n, 5)).cuda()
     u1 = torch.from_numpy(_rand(n, 6)).cuda()
@@ -409,8 +410,50 @@ def test_bottom_kernel_equals_kernel_path(name, knobs, monkeypatch):
     m2.vcycle(f, u2)
     assert relmax(u2.cpu().numpy(), u1.cpu().numpy()) <= 1e-13
     ref.close()
-    if knobs:
-        m2.close()
+    m2.close()
+
+
+@pytest.mark.parametrize("name", list(CASES))
+@pytest.mark.parametrize("dense_max", ["4096", "1024", "100000000"])
+def test_dense_bottom(name, dense_max, monkeypatch):
+    """The dense bottom B_J (dense_bottom.cuh: Alg. 3 lines 6-14 for the levels >= J as one
+    matrix, built from the unit vectors at setup) against the oracle's recursive V-cycle, for
+    several J (4096 / 1024 rows, or every level below 0 when the threshold is huge) and
+    against the per-kernel path with no dense bottom (MGM_DENSE_MAX=0, MGM_BOT_MAX=0), to
+    1e-12; the zero-guess V-cycle (Krylov preconditioner) and GMRES as well."""
+    import torch
+    from paper_2204_06154_b200 import MGM, mgm_apply
+
+    P = pair(name)
+    monkeypatch.setenv("MGM_DENSE_MAX", "0")
+    monkeypatch.setenv("MGM_BOT_MAX", "0")
+    ref = MGM(P.w.points, P.w.normals, P.w.stencil, P.w.levels)
+    monkeypatch.setenv("MGM_DENSE_MAX", dense_max)
+    monkeypatch.delenv("MGM_BOT_MAX")
+    m2 = MGM(P.w.points, P.w.normals, P.w.stencil, P.w.levels)
+    n = len(P.w.points)
+    f0, u0 = _rand(n, 15), _rand(n, 16)
+    f = torch.from_numpy(f0).cuda()
+    u1 = torch.from_numpy(u0.copy()).cuda()
+    u2 = u1.clone()
+    ref.vcycle(f, u1)
+    m2.vcycle(f, u2)
+    assert relmax(u2.cpu().numpy(), u1.cpu().numpy()) <= 1e-12
+    assert relmax(u2.cpu().numpy(), P.ref.vcycle(f0, u0)) <= 1e-12
+    pad = 1 if P.poisson else 0
+    v = _rand(n + pad, 17)
+    if P.poisson:
+        v[-1] = 0.0
+    y = torch.empty(n + pad, dtype=torch.float64, device="cuda")
+    mgm_apply(m2.ctx, 0, 7, torch.from_numpy(P.to_lib_order(0, v)).cuda(), None, y)
+    assert relmax(P.to_oracle_order(0, y.cpu().numpy()), P.ref.vcycle_level_order(v, np.zeros(n + pad))) <= 1e-12
+    rhs = torch.from_numpy(P.w.rhs).cuda()
+    x, rep = m2.solve(rhs, tol=1e-10)
+    xr, rr = P.ref.solve(P.w.rhs, tol=1e-10)
+    assert rep.converged and abs(rep.iterations - rr.iterations) <= 1
+    assert np.linalg.norm(x.cpu().numpy() - xr) / np.linalg.norm(xr) <= 1e-9
+    ref.close()
+    m2.close()
 
 
 # ------------------------------------------------------------------ multi-GPU path (8(e))
