@@ -2550,7 +2550,6 @@ mgm_status mgm_setup(const double* points, const double* normals, int64_t n_poin
     ctx->nthreads = std::max(1, std::min(64, (int)std::thread::hardware_concurrency()));
     if (const char* e = std::getenv("MGM_DIST_LEVELS")) ctx->dist_levels = std::max(0, std::atoi(e));
     if (const char* e = std::getenv("MGM_DIST_FAKE_RANKS")) ctx->fake_ranks = ctx->poisson ? 0 : std::max(0, std::atoi(e));
-    if (const char* e = std::getenv("MGM_PF_DIST")) ctx->pf_dist = std::max(0, std::atoi(e));
     if (const char* e = std::getenv("MGM_PF_CAP_MB")) ctx->pf_cap = (i64)std::max(0, std::atoi(e)) << 20;
     if (std::getenv("MGM_NO_ZG")) ctx->no_zg = true;
     if (std::getenv("MGM_NO_C0_FUSE")) ctx->no_c0_fuse = true;
