@@ -161,28 +161,54 @@ mgm_status mgm_solve_batch(mgm_ctx* ctx, int K, const double* rhs_dev, double* x
 
 /* ---- multi-GPU ----------------------------------
  * One process per GPU.  Every rank calls mgm_setup with the SAME cloud and parameters (the
- * setup is deterministic, so all ranks hold identical hierarchies), then mgm_dist_attach.
- * From then on mgm_vcycle / mgm_solve are collective: on levels 0 .. D-1 (D from the
- * environment variable MGM_DIST_LEVELS at mgm_setup, default 1) every operator application
- * of Alg. 3 and of the Krylov loop (each colour of the Gauss-Seidel sweep, the residual,
- * the restriction, the interpolation, the GMRES SpMV) is split into nranks contiguous row
- * pieces (a colour's rows are in Morton order, so each piece is a Morton block of that
- * colour); each rank computes its piece and the pieces are exchanged with in-place NCCL
- * broadcasts (one grouped call per application), captured in the V-cycle's CUDA graph.
- * Levels >= D are computed redundantly on every rank.  Krylov inner products: each rank
- * reduces its own piece, then ncclAllReduce(sum).  Vectors stay replicated, so every
- * rank's result is the same; the V-cycle is bitwise the single-GPU one, the GMRES
- * iterates agree with it to rounding (the inner products are summed in another order).
- * Shifted problems only (MGM_ERR_ARG for the Poisson problem with nranks > 1).
+ * setup is deterministic, so every rank builds the same hierarchy), then mgm_dist_attach.
+ * The attach partitions the hierarchy: rank q owns the points whose level-0 Morton index lies
+ * in [floor(qN/P), floor((q+1)N/P)) -- on every level a coarse point stays with the owner of
+ * its level-0 point, so each level is split into Morton row blocks -- and keeps, on the
+ * distributed levels 0..D-1, only its own rows of L_j, P_j, R_j plus GHOST copies of the rows
+ * its operators read (the undistributed device arrays are freed).  D: the levels with at
+ * least MGM_DIST_MIN_ROWS rows per rank (environment at attach, default 16384; MGM_DIST_LEVELS
+ * forces D), never the V-cycle's bottom; levels >= D (and the dense bottom) run redundantly on
+ * every rank after an all-gather of the restricted residual.  Halos of ghost values only:
+ * after every colour of a Gauss-Seidel sweep (that colour's values), after interpolation +
+ * correction and before a restriction or SpMV (all ghosts); NCCL grouped send/receive,
+ * captured in the V-cycle's CUDA graph; Krylov inner products (and the Poisson border dots):
+ * rank-local reduction + ncclAllReduce.  Every local operator row keeps the undistributed
+ * row's entries and threads in the same order, so a V-cycle of the shifted problem is bitwise
+ * the single-GPU one; Krylov iterates agree with it to rounding (the inner products are
+ * summed in another order).  Shifted and Poisson problems.
+ * From then on mgm_vcycle / mgm_solve are collective (every rank calls them) and take the
+ * rank's LOCAL vectors: n_local entries in the order mgm_local_rows returns.  Not available
+ * on an attached ctx: the batched solves, mgm_apply, mgm_export_level of a distributed level.
  *
  * mgm_nccl_unique_id: rank 0 creates the 128-byte NCCL id (host buffer id128); the caller
  * broadcasts it to the other ranks (e.g. torch.distributed).  MGM_ERR_NCCL if
  * libnccl.so.2 cannot be loaded.
  * mgm_dist_attach: rank in [0, nranks); id128 = that id (host, 128 bytes, copied).  The
  * communicator is created on the ctx's device and destroyed by mgm_destroy.  Errors:
- * MGM_ERR_ARG (bad rank / already attached / Poisson), MGM_ERR_NCCL. */
+ * MGM_ERR_ARG (bad rank / already attached / a one-level hierarchy), MGM_ERR_NCCL. */
 mgm_status mgm_nccl_unique_id(void* id128);
 mgm_status mgm_dist_attach(mgm_ctx* ctx, int rank, int nranks, const void* id128);
+
+/* The rows this rank owns: *n_local = their count, original_ids[n_local] (host, may be NULL)
+ * = their original point indices, in the order of the rank's local vectors (the rank's
+ * level-0 points in Morton order).  Unattached ctx: all n_points rows, identity order. */
+mgm_status mgm_local_rows(const mgm_ctx* ctx, int64_t* n_local, int64_t* original_ids);
+
+/* Distribution diagnostics: *dist_levels = D (0 unattached), *ghosts = ghost rows of this rank
+ * over the distributed levels, *halo_values_per_vcycle = ghost values this rank receives in
+ * one V-cycle (x 8 bytes = its halo volume). */
+mgm_status mgm_dist_info(const mgm_ctx* ctx, int* dist_levels, int64_t* ghosts, int64_t* halo_values_per_vcycle);
+
+/* Test hook: R "fake" ranks on ONE GPU in one process.  mgm_fake_group_create makes a group of
+ * nranks; each rank's ctx (its own mgm_setup) attaches with mgm_dist_attach_fake and is then
+ * driven by its own host thread, calling the same collective entry points as with NCCL.  The
+ * transport copies between the ranks' device buffers (CUDA events + a host barrier) instead
+ * of NCCL: the distributed code path is otherwise unchanged.  V-cycles run eagerly (no CUDA
+ * graph).  Destroy the group after every ctx attached to it. */
+mgm_status mgm_fake_group_create(int nranks, void** group);
+mgm_status mgm_fake_group_destroy(void* group);
+mgm_status mgm_dist_attach_fake(mgm_ctx* ctx, int rank, void* group);
 
 /* Message of the last failure on this ctx (or of the last failed mgm_setup on this thread
  * when ctx is NULL); *failing_index (if non-NULL) receives the index or -1. */
@@ -304,6 +330,25 @@ mgm_status mgm_host_wse(const double* points, int64_t n, int64_t nt, int64_t* ke
  * CSR pattern ptr[n+1], col[ptr[n]]; colour[n] out; *n_colours out. */
 mgm_status mgm_host_colouring(int64_t n, const int64_t* ptr, const int32_t* col, int32_t* colour,
                               int* n_colours);
+
+/* Partition tables of one level for `rank` of `nranks` (the host code mgm_dist_attach runs;
+ * DESIGN.md "Multi-GPU").  Rows are the level's lib order (colour-major: ascending rows =
+ * ascending colours); owner[n] = owning rank of each row.  L_ptr/L_col: pattern of L_j;
+ * P_ptr/P_col (n rows -> nc coarse, owner_c[nc]): P_j, whose transpose R_j reads this level
+ * (NULL if none); Pf_ptr/Pf_col (nf fine rows -> n, owner_f[nf]): P_{j-1}, which reads this level
+ * (NULL on level 0).  Outputs (host, caller-allocated; any may be NULL): rows[n] owned rows
+ * (ascending, *n_rows); ghosts[n] ghost rows sorted by (owner, row) (*n_ghosts); peers[nranks]
+ * (*n_peers); send_rows[n] per peer concatenated (rows the peer reads that this rank owns);
+ * send_off / recv_off [nranks + 1] per-peer offsets into send_rows / ghosts;
+ * send_coff / recv_coff [nranks * (ncol + 1)] per peer the absolute offset of each colour's
+ * slice.  No GPU needed. */
+mgm_status mgm_host_partition_level(int64_t n, const int64_t* L_ptr, const int32_t* L_col, const int32_t* colour,
+                                    int ncol, const int32_t* owner, int64_t nc, const int64_t* P_ptr,
+                                    const int32_t* P_col, const int32_t* owner_c, int64_t nf, const int64_t* Pf_ptr,
+                                    const int32_t* Pf_col, const int32_t* owner_f, int nranks, int rank,
+                                    int64_t* n_rows, int64_t* rows, int64_t* n_ghosts, int64_t* ghosts, int* n_peers,
+                                    int32_t* peers, int64_t* send_rows, int64_t* send_off, int64_t* recv_off,
+                                    int64_t* send_coff, int64_t* recv_coff);
 
 #ifdef __cplusplus
 }

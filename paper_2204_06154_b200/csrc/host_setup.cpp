@@ -382,6 +382,80 @@ void wse_eliminate(const double* pts, i64 n, i64 nt, const std::vector<double>& 
 }
 
 // ---------------------------------------------------------------------------------------
+// ---------------------------------------------------------------------------------------
+// Partition tables of one level for every rank (mgm_internal.h PartTables).
+// ---------------------------------------------------------------------------------------
+void partition_level(const HostCSR& L, const std::vector<int>& owner, const std::vector<i32>& colour, int ncol,
+                     const HostCSR* Pj, const std::vector<int>* owner_c, const HostCSR* Pf,
+                     const std::vector<int>* owner_f, int nranks, std::vector<PartTables>& out) {
+    const i64 n = L.nrows;
+    std::vector<std::vector<i64>> need(nranks);  // non-owned rows each rank reads
+    for (i64 r = 0; r < n; ++r) {
+        const int q = owner[r];
+        for (i64 t = L.ptr[r]; t < L.ptr[r + 1]; ++t)
+            if (owner[L.col[t]] != q) need[q].push_back(L.col[t]);
+    }
+    if (Pj && owner_c)  // R_j = P_j^T: coarse row c (owned by owner_c[c]) reads fine rows r with P_j[r][c] != 0
+        for (i64 r = 0; r < n; ++r)
+            for (i64 t = Pj->ptr[r]; t < Pj->ptr[r + 1]; ++t) {
+                const int q = (*owner_c)[Pj->col[t]];
+                if (owner[r] != q) need[q].push_back(r);
+            }
+    if (Pf && owner_f)  // P_{j-1}: fine row f (owned by owner_f[f]) reads this level's rows
+        for (i64 f = 0; f < Pf->nrows; ++f) {
+            const int q = (*owner_f)[f];
+            for (i64 t = Pf->ptr[f]; t < Pf->ptr[f + 1]; ++t)
+                if (owner[Pf->col[t]] != q) need[q].push_back(Pf->col[t]);
+        }
+    out.assign(nranks, PartTables());
+    for (int q = 0; q < nranks; ++q) {
+        auto& g = need[q];
+        std::sort(g.begin(), g.end());
+        g.erase(std::unique(g.begin(), g.end()), g.end());
+        std::stable_sort(g.begin(), g.end(), [&](i64 a, i64 b) { return owner[a] < owner[b]; });
+        out[q].ghosts = g;
+    }
+    for (i64 r = 0; r < n; ++r) out[owner[r]].rows.push_back(r);
+    // send lists: rank q sends to p the rows of need[p] that q owns (need[p] is sorted by
+    // (owner, row), so they are one contiguous run); colour slices by scanning colours
+    for (int q = 0; q < nranks; ++q) {
+        PartTables& T = out[q];
+        T.send_off.assign(1, 0);
+        T.recv_off.assign(1, 0);
+        for (int p = 0; p < nranks; ++p) {
+            if (p == q) continue;
+            const auto& gp = out[p].ghosts;
+            auto lo = std::lower_bound(gp.begin(), gp.end(), q, [&](i64 a, int v) { return owner[a] < v; });
+            auto hi = std::upper_bound(gp.begin(), gp.end(), q, [&](int v, i64 a) { return v < owner[a]; });
+            const auto& gq = T.ghosts;
+            auto lo2 = std::lower_bound(gq.begin(), gq.end(), p, [&](i64 a, int v) { return owner[a] < v; });
+            auto hi2 = std::upper_bound(gq.begin(), gq.end(), p, [&](int v, i64 a) { return v < owner[a]; });
+            if (lo == hi && lo2 == hi2) continue;
+            T.peers.push_back(p);
+            const i64 s0 = (i64)T.send_rows.size();
+            T.send_rows.insert(T.send_rows.end(), lo, hi);
+            T.send_off.push_back((i64)T.send_rows.size());
+            const i64 g0 = (i64)(lo2 - gq.begin()), g1 = (i64)(hi2 - gq.begin());
+            T.recv_off.push_back(g1);
+            // colour slices (rows ascending = colours ascending in lib order)
+            auto slices = [&](const std::vector<i64>& v, i64 a, i64 b, std::vector<i64>& coff) {
+                i64 k = a;
+                for (int c = 0; c <= ncol; ++c) {
+                    while (k < b && colour[v[(size_t)k]] < c) ++k;
+                    coff.push_back(k);
+                }
+                coff.back() = b;
+            };
+            slices(T.send_rows, s0, (i64)T.send_rows.size(), T.send_coff);
+            slices(gq, g0, g1, T.recv_coff);
+            (void)g0;
+        }
+        // recv_off[0] must be the first peer's ghost start: ghosts are sorted by owner and every
+        // owner != q in them is a peer, so the segments tile [0, nghost)
+        if (!T.peers.empty()) T.recv_off[0] = 0;
+    }
+}
+
 HostCSR transpose(const HostCSR& A) {
     HostCSR T;
     T.nrows = A.ncols;

@@ -7,6 +7,8 @@
 
 #include <algorithm>
 #include <chrono>
+#include <condition_variable>
+#include <mutex>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -39,6 +41,8 @@ struct NcclApi {
         nullptr;
     ncclResult_t (*GroupStart)() = nullptr;
     ncclResult_t (*GroupEnd)() = nullptr;
+    ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
 NcclApi& nccl() {
@@ -56,21 +60,192 @@ NcclApi& nccl() {
             api.GroupStart = (decltype(api.GroupStart))dlsym(h, "ncclGroupStart");
             api.GroupEnd = (decltype(api.GroupEnd))dlsym(h, "ncclGroupEnd");
             api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
+            api.Send = (decltype(api.Send))dlsym(h, "ncclSend");
+            api.Recv = (decltype(api.Recv))dlsym(h, "ncclRecv");
             api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.Broadcast && api.AllReduce &&
-                     api.GroupStart && api.GroupEnd && api.GetErrorString;
+                     api.GroupStart && api.GroupEnd && api.GetErrorString && api.Send && api.Recv;
         }
     }
     return api;
 }
-void nccl_group_start() { nccl().GroupStart(); }
-void nccl_group_end() { nccl().GroupEnd(); }
-void nccl_bcast(double* p, size_t n, int root, ncclComm_t comm, cudaStream_t st) {
-    nccl().Broadcast(p, p, n, ncclFloat64, root, comm, st);
-}
-void nccl_allreduce_sum(double* p, size_t n, ncclComm_t comm, cudaStream_t st) {
-    nccl().AllReduce(p, p, n, ncclFloat64, ncclSum, comm, st);
-}
 }  // namespace
+
+// ---------------------------------------------------------------------------------------
+// Transport of the distributed solve: grouped halo
+// send/receive of ghost values, sum-allreduce of Krylov scalars, all-gather of the first
+// replicated level.  NcclTransport: one process per GPU (ncclSend/ncclRecv in a group,
+// ncclAllReduce, ncclBroadcast per root), capturable in the V-cycle's CUDA graph.
+// FakeTransport: R ranks on ONE GPU inside one process, each driven by its own host thread
+// (test hook, mgm_fake_group_create): the same collective calls, implemented with device
+// copies between the ranks' buffers ordered by CUDA events and a host barrier -- the
+// distributed code path itself is unchanged.  Eager only (not capturable).
+// ---------------------------------------------------------------------------------------
+namespace mgm {
+struct Xfer {
+    int peer;
+    const double* send;
+    i64 ns;
+    double* recv;
+    i64 nr;
+};
+struct Transport {
+    int rank = 0, nranks = 1;
+    virtual ~Transport() {}
+    virtual bool exchange(const std::vector<Xfer>& x, cudaStream_t st) = 0;
+    virtual bool allreduce_sum(double* buf, i64 n, cudaStream_t st) = 0;
+    // out[off[q] .. off[q+1]) <- rank q's `mine` (n = off[rank+1] - off[rank] on this rank)
+    virtual bool allgatherv(const double* mine, double* out, const std::vector<i64>& off, cudaStream_t st) = 0;
+    virtual bool capturable() const = 0;
+};
+
+struct NcclTransport : Transport {
+    ncclComm_t comm = nullptr;
+    bool exchange(const std::vector<Xfer>& x, cudaStream_t st) override {
+        if (x.empty()) return true;
+        bool ok = nccl().GroupStart() == ncclSuccess;
+        for (const Xfer& e : x) {
+            if (e.ns > 0) ok &= nccl().Send(e.send, (size_t)e.ns, ncclFloat64, e.peer, comm, st) == ncclSuccess;
+            if (e.nr > 0) ok &= nccl().Recv(e.recv, (size_t)e.nr, ncclFloat64, e.peer, comm, st) == ncclSuccess;
+        }
+        ok &= nccl().GroupEnd() == ncclSuccess;
+        return ok;
+    }
+    bool allreduce_sum(double* buf, i64 n, cudaStream_t st) override {
+        return nccl().AllReduce(buf, buf, (size_t)n, ncclFloat64, ncclSum, comm, st) == ncclSuccess;
+    }
+    bool allgatherv(const double* mine, double* out, const std::vector<i64>& off, cudaStream_t st) override {
+        bool ok = nccl().GroupStart() == ncclSuccess;
+        for (int q = 0; q < nranks; ++q) {
+            const i64 c = off[q + 1] - off[q];
+            if (c > 0)
+                ok &= nccl().Broadcast(q == rank ? mine : out + off[q], out + off[q], (size_t)c, ncclFloat64, q, comm,
+                                       st) == ncclSuccess;
+        }
+        ok &= nccl().GroupEnd() == ncclSuccess;
+        return ok;
+    }
+    bool capturable() const override { return true; }
+    ~NcclTransport() override {
+        if (comm) nccl().CommDestroy(comm);
+    }
+};
+
+// in-process group of R fake ranks (one host thread each, same GPU)
+struct FakeGroup {
+    int R = 0;
+    std::mutex mu;
+    std::condition_variable cv;
+    int arrived = 0;
+    long generation = 0;
+    // posted by each rank for the current collective
+    std::vector<std::vector<Xfer>> posted;   // [rank] its sends (peer, ptr, count)
+    std::vector<cudaEvent_t> ready, done;    // [rank]
+    std::vector<const double*> gather_src;   // [rank]
+    std::vector<double*> reduce_buf;         // [rank]
+    explicit FakeGroup(int r) : R(r), posted(r), ready(r), done(r), gather_src(r), reduce_buf(r) {
+        for (int q = 0; q < R; ++q) {
+            cudaEventCreateWithFlags(&ready[q], cudaEventDisableTiming);
+            cudaEventCreateWithFlags(&done[q], cudaEventDisableTiming);
+        }
+    }
+    ~FakeGroup() {
+        for (int q = 0; q < R; ++q) {
+            cudaEventDestroy(ready[q]);
+            cudaEventDestroy(done[q]);
+        }
+    }
+    void barrier() {
+        std::unique_lock<std::mutex> lk(mu);
+        const long g = generation;
+        if (++arrived == R) {
+            arrived = 0;
+            ++generation;
+            cv.notify_all();
+        } else {
+            cv.wait(lk, [&] { return generation != g; });
+        }
+    }
+};
+
+__global__ void k_sum_ranks(i64 n, int R, double* const* bufs, double* out) {
+    for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int q = 0; q < R; ++q) s += bufs[q][i];
+        out[i] = s;
+    }
+}
+
+struct FakeTransport : Transport {
+    FakeGroup* g = nullptr;
+    double* scratch = nullptr;  // this rank's copy for the allreduce
+    i64 scratch_n = 0;
+    double** d_bufs = nullptr;  // device table of the ranks' scratch pointers
+    // every rank posts, then waits for the others' data to be ready and copies what it receives;
+    // then waits until every rank has consumed its sends (so the send buffers may be reused)
+    bool exchange(const std::vector<Xfer>& x, cudaStream_t st) override {
+        g->posted[rank] = x;
+        cudaEventRecord(g->ready[rank], st);
+        g->barrier();
+        for (const Xfer& e : x) {
+            if (e.nr <= 0) continue;
+            const Xfer* s = nullptr;
+            for (const Xfer& f : g->posted[e.peer])
+                if (f.peer == rank) s = &f;
+            if (!s || s->ns != e.nr) return false;
+            cudaStreamWaitEvent(st, g->ready[e.peer], 0);
+            cudaMemcpyAsync(e.recv, s->send, sizeof(double) * e.nr, cudaMemcpyDeviceToDevice, st);
+        }
+        cudaEventRecord(g->done[rank], st);
+        g->barrier();
+        for (const Xfer& e : x)
+            if (e.ns > 0) cudaStreamWaitEvent(st, g->done[e.peer], 0);
+        g->barrier();  // (events re-recorded by the next collective only after everyone waited)
+        return true;
+    }
+    bool allreduce_sum(double* buf, i64 n, cudaStream_t st) override {
+        if (n > scratch_n) {
+            if (scratch) dev_free(scratch);
+            if (dev_malloc((void**)&scratch, sizeof(double) * (size_t)n) != cudaSuccess) return false;
+            scratch_n = n;
+        }
+        if (!d_bufs && dev_malloc((void**)&d_bufs, sizeof(double*) * (size_t)nranks) != cudaSuccess) return false;
+        cudaMemcpyAsync(scratch, buf, sizeof(double) * n, cudaMemcpyDeviceToDevice, st);
+        g->reduce_buf[rank] = scratch;
+        cudaEventRecord(g->ready[rank], st);
+        g->barrier();
+        for (int q = 0; q < nranks; ++q) cudaStreamWaitEvent(st, g->ready[q], 0);
+        cudaMemcpyAsync(d_bufs, g->reduce_buf.data(), sizeof(double*) * nranks, cudaMemcpyHostToDevice, st);
+        k_sum_ranks<<<(unsigned)std::min<i64>(1024, (n + 255) / 256), 256, 0, st>>>(n, nranks, d_bufs, buf);
+        cudaEventRecord(g->done[rank], st);
+        cudaStreamSynchronize(st);  // (d_bufs is pageable-host sourced; keep the host table alive)
+        g->barrier();
+        for (int q = 0; q < nranks; ++q) cudaStreamWaitEvent(st, g->done[q], 0);
+        g->barrier();
+        return true;
+    }
+    bool allgatherv(const double* mine, double* out, const std::vector<i64>& off, cudaStream_t st) override {
+        g->gather_src[rank] = mine;
+        cudaEventRecord(g->ready[rank], st);
+        g->barrier();
+        for (int q = 0; q < nranks; ++q) {
+            const i64 c = off[q + 1] - off[q];
+            if (c <= 0) continue;
+            cudaStreamWaitEvent(st, g->ready[q], 0);
+            cudaMemcpyAsync(out + off[q], g->gather_src[q], sizeof(double) * c, cudaMemcpyDeviceToDevice, st);
+        }
+        cudaEventRecord(g->done[rank], st);
+        g->barrier();
+        for (int q = 0; q < nranks; ++q) cudaStreamWaitEvent(st, g->done[q], 0);
+        g->barrier();
+        return true;
+    }
+    bool capturable() const override { return false; }
+    ~FakeTransport() override {
+        if (scratch) dev_free(scratch);
+        if (d_bufs) dev_free(d_bufs);
+    }
+};
+}  // namespace mgm
 
 namespace {
 
@@ -117,6 +292,24 @@ struct Level {
     std::vector<i32> colour_lib;
     std::vector<double> c_lib;
     std::vector<i64> lib2mor;  // Morton index of each lib row
+    // ---- distributed level (mgm_dist_attach): this rank's rows only.
+    // Vectors u, t: [owned rows (n) | multiplier (Poisson) | ghosts (nghost)]; f: [owned | mult].
+    bool dist = false;
+    i64 nghost = 0, gbase = 0;           // ghost slot g lives at index gbase + g
+    std::vector<int> peers;              // PartTables
+    std::vector<i64> send_off, recv_off, send_coff, recv_coff;
+    i32* d_send_idx = nullptr;           // owned row of each send entry
+    i64* d_srange = nullptr;             // [ncol + 1][npeers][2] send ranges: all (key 0), colour c (key c + 1)
+    double* d_sendbuf = nullptr;
+    std::vector<int> tpr_col;            // threads per row of each colour (the undistributed launch's)
+    std::vector<i64> gcoff;              // the undistributed level's colour offsets
+    // on the last distributed level: my coarse rows of the first replicated level are restricted
+    // into d_stage_mine, all-gathered into d_stage_all, then permuted (d_stage_perm) into lib order
+    i64 nstage = 0;
+    std::vector<i64> stage_off;
+    double* d_stage_mine = nullptr;
+    double* d_stage_all = nullptr;
+    i32* d_stage_perm = nullptr;
 };
 
 struct KernelTimer {
@@ -184,32 +377,17 @@ struct mgm_ctx {
     BPhase* d_phases = nullptr;
     std::vector<void*> bot_mem;
     i64 vcycle_kernels = 0;
-    // L2 prefetch pacing of the V-cycle graph (solve_kernels.cuh l2_prefetch_share): the
-    // schedule's operator regions ("targets") are recorded by a dry enqueue pass; kernel t
-    // of the schedule then prefetches targets (t, t + pf_dist], the bottom kernel the
-    // up-path targets within pf_bot_budget bytes.  MGM_PF_DIST=0 turns it off.
-    int pf_mode = 0;  // 0 off, 1 record, 2 emit
-    int pf_dist = 0;  // off by default: measured slower
-    i64 pf_cap = (i64)24 << 20;         // bytes prefetched per target (its prefix)
-    i64 pf_bot_budget = (i64)48 << 20;  // bytes the bottom kernel prefetches for the up-path
-    std::vector<std::vector<PfRegion>> pf_tg;
-    std::vector<PfRegion> pf_flat;
-    std::vector<int> pf_off;
-    PfRegion* d_pf = nullptr;
-    std::vector<void*> pf_old;  // earlier tables (graphs may still reference them)
-    int pf_pos = 0, pf_last = 0;
-    int pf_late = 0, pf_nof = 0, pf_l0only = 0;  // experiments (MGM_PF_LATE / _NOF / _L0ONLY)
-    std::vector<PfRegion> bot_pf;  // the bottom kernel's operator arrays
     // batched (multi-RHS) V-cycles: per level interleaved [n_j][bK] buffers, graph per K
     int bK = 0;
     std::vector<double*> bu, bf, bt;
     cudaGraphExec_t bgraph[9] = {};
     double* bres = nullptr;  // residual (n x K)
-    // multi-GPU (mgm_dist_attach)
+    // multi-GPU (mgm_dist_attach / mgm_dist_attach_fake): levels 0..D-1 partitioned by Morton row
+    // blocks, D..p-1 replicated
     int rank = 0, nranks = 1;
-    ncclComm_t comm = nullptr;
-    int dist_levels = 1;   // levels 0..dist_levels-1 are split across ranks (MGM_DIST_LEVELS)
-    int fake_ranks = 0;    // MGM_DIST_FAKE_RANKS: split into pieces on one GPU (test hook)
+    Transport* tp = nullptr;
+    int D = 0;
+    std::vector<i64> local_ids;  // original ids of my level-0 rows, in my I/O (Morton) order
     // GMRES workspace
     int restart = 50;
     i64 ld = 0;
@@ -436,7 +614,6 @@ static T* bot_upload(mgm_ctx* ctx, const std::vector<T>& v, bool& ok) {
     T* d = nullptr;
     if (dev_malloc((void**)&d, sizeof(T) * std::max<size_t>(1, v.size())) != cudaSuccess) { ok = false; return nullptr; }
     ctx->bot_mem.push_back(d);
-    ctx->bot_pf.push_back(PfRegion{(const char*)d, (int64_t)(sizeof(T) * v.size())});
     if (!v.empty() && cudaMemcpy(d, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice) != cudaSuccess) ok = false;
     return d;
 }
@@ -1250,6 +1427,30 @@ void launch_gs(bool pdl, bool poisson, int tpr, int r0, int r1, int span, const 
         else gs_launch_t<false, 8>(pdl, r0, r1, span, L, st, pf, zg);
     }
 }
+// distributed levels: the threads per row the undistributed colour launch used (L.tpr_col), so
+// every row is summed by the same threads in the same order
+void launch_gs_fixed(bool pdl, bool poisson, int tpr, int r0, int r1, int span, const Level& L, cudaStream_t st,
+                     bool zg) {
+    const PfList pf{nullptr, 0, 0};
+    if (poisson) {
+        if (tpr == 1) gs_launch_t<true, 1>(pdl, r0, r1, span, L, st, pf, zg);
+        else if (tpr == 2) gs_launch_t<true, 2>(pdl, r0, r1, span, L, st, pf, zg);
+        else if (tpr == 4) gs_launch_t<true, 4>(pdl, r0, r1, span, L, st, pf, zg);
+        else gs_launch_t<true, 8>(pdl, r0, r1, span, L, st, pf, zg);
+    } else {
+        if (tpr == 1) gs_launch_t<false, 1>(pdl, r0, r1, span, L, st, pf, zg);
+        else if (tpr == 2) gs_launch_t<false, 2>(pdl, r0, r1, span, L, st, pf, zg);
+        else if (tpr == 4) gs_launch_t<false, 4>(pdl, r0, r1, span, L, st, pf, zg);
+        else gs_launch_t<false, 8>(pdl, r0, r1, span, L, st, pf, zg);
+    }
+}
+// the threads per row launch_gs picks for a colour of `span` rows
+static int gs_tpr_for(int tpr, i64 span, int block) {
+    while (tpr > 1 && span * tpr > gs_wave_threads(tpr, block) && span * (tpr / 2) <= gs_wave_threads(tpr / 2, block))
+        tpr /= 2;
+    return tpr;
+}
+
 // (MODE 2 reads the level's later-colour slot tables g_sluw / g_nlow, set by enqueue_residual)
 static thread_local const int* g_sluw = nullptr;
 static thread_local const uint8_t* g_nlow = nullptr;
@@ -1288,100 +1489,61 @@ void launch_spmv(bool pdl, int mode, bool poisson, int tpr, i64 r0, i64 r1, i64 
 }
 
 // ---------------------------------------------------------------------------------------
-// Multi-GPU (mgm_dist_attach): every rank holds the full hierarchy
-// and full vectors; on the distributed levels (j < dist_levels) each operator application
-// is split into nranks contiguous row pieces (a colour's rows are Morton-ordered, so a
-// piece is a Morton block of that colour), each rank computes its piece and the pieces are
-// exchanged with in-place NCCL broadcasts (one grouped call), after which every rank's
-// vector is bitwise what one GPU computes.  Krylov inner products: own piece + allreduce.
-// MGM_DIST_FAKE_RANKS=R (debug, 1 GPU): split into R pieces, all computed locally.
+// Multi-GPU (mgm_dist_attach): on the distributed
+// levels 0..D-1 each rank holds only its Morton block of rows plus ghost copies of the rows
+// its operators read (PartTables); every operator application runs on the owned rows with
+// the same per-row arithmetic as one GPU, and halos refresh the ghosts:
+//   * after each colour of a Gauss-Seidel sweep: that colour's values (one send / receive
+//     per peer, received straight into the ghost slots),
+//   * after interpolation + correction, before a restriction (t), before an SpMV: all ghosts.
+// The last distributed level restricts its share of the first replicated level D; the shares
+// are all-gathered; levels D..p-1 (incl. the dense bottom) run redundantly on every rank.
 // ---------------------------------------------------------------------------------------
-static void piece(i64 lo, i64 hi, int R, int q, i64& a, i64& b) {
-    const i64 len = hi - lo;
-    a = lo + len * q / R;
-    b = lo + len * (q + 1) / R;
-}
-// distributed once a communicator is attached (also with nranks = 1: one piece, the
-// broadcasts are then no-ops but the exchange path is exercised), or with fake ranks
-static bool dist_level(const mgm_ctx* ctx, int j) {
-    return (ctx->comm || ctx->fake_ranks > 1) && j < ctx->dist_levels;
-}
-static int dist_pieces(const mgm_ctx* ctx) { return ctx->comm ? ctx->nranks : ctx->fake_ranks; }
-// run f(a, b) on this rank's piece(s) of [lo, hi)
-template <class F>
-static void for_my_pieces(const mgm_ctx* ctx, int j, i64 lo, i64 hi, F f) {
-    if (!dist_level(ctx, j)) { f(lo, hi); return; }
-    const int R = dist_pieces(ctx);
-    for (int q = 0; q < R; ++q) {
-        if (ctx->comm && q != ctx->rank) continue;
-        i64 a, b;
-        piece(lo, hi, R, q, a, b);
-        f(a, b);
-    }
-}
-// exchange the pieces of y[lo, hi) after a distributed application
-static void dist_exchange(mgm_ctx* ctx, int j, double* y, i64 lo, i64 hi, cudaStream_t st) {
-    if (!dist_level(ctx, j) || !ctx->comm || g_dry) return;
-    nccl_group_start();
-    for (int q = 0; q < ctx->nranks; ++q) {
-        i64 a, b;
-        piece(lo, hi, ctx->nranks, q, a, b);
-        if (b > a) nccl_bcast(y + a, (size_t)(b - a), q, ctx->comm, st);
-    }
-    nccl_group_end();
-    ctx->vcycle_kernels++;
+static bool dist_level(const mgm_ctx* ctx, int j) { return ctx->tp && j < ctx->D; }
+static bool dist_on(const mgm_ctx* ctx) { return ctx->tp != nullptr; }
+
+// pack the send entries [range[2p], range[2p+1]) of every peer p (chunks CTAs per peer)
+__global__ void k_pack(int chunks, const i64* __restrict__ range, const i32* __restrict__ idx,
+                       const double* __restrict__ v, double* __restrict__ out) {
+    const int p = blockIdx.x / chunks, b = blockIdx.x % chunks;
+    const i64 lo = range[2 * p], hi = range[2 * p + 1];
+    for (i64 e = lo + (i64)b * blockDim.x + threadIdx.x; e < hi; e += (i64)chunks * blockDim.x) out[e] = v[idx[e]];
 }
 
-// ---------------------------------------------------------------------------------------
-// L2 prefetch pacing (solve_kernels.cuh l2_prefetch_share)
-// ---------------------------------------------------------------------------------------
-using Regions = std::vector<PfRegion>;
-static PfRegion pf_region(const void* p, i64 bytes) { return PfRegion{(const char*)p, (int64_t)bytes}; }
-// rows [a, b) of a SELL-32 operator: its value and column slices
-static void pf_sell(Regions& R, const std::vector<i64>& hptr, const i32* col, const double* val, i64 a, i64 b) {
-    if (hptr.empty() || b <= a) return;
-    const i64 s0 = hptr[(size_t)(a >> 5)], s1 = hptr[(size_t)std::min<i64>((b + 31) >> 5, (i64)hptr.size() - 1)];
-    R.push_back(pf_region(val + s0, 8 * (s1 - s0)));
-    R.push_back(pf_region(col + s0, 4 * (s1 - s0)));
-}
-// Register the next kernel of the schedule as a prefetch target with the given operator
-// regions and return what this kernel (if it can issue prefetches) should prefetch.
-static PfList pf_take(mgm_ctx* ctx, const Regions& regs, bool issuer = true, i64 budget = 0) {
-    if (ctx->pf_mode == 1) {
-        Regions capped;
-        i64 left = ctx->pf_cap;
-        for (const PfRegion& r : regs) {
-            if (left <= 0) break;
-            const uintptr_t p0 = (uintptr_t)r.p & ~(uintptr_t)15;
-            i64 b = std::min<i64>((i64)((uintptr_t)r.p - p0) + r.bytes, left);
-            b = (b + 15) & ~(i64)15;
-            if (b > 0) capped.push_back(PfRegion{(const char*)p0, (int64_t)b});
-            left -= b;
-        }
-        ctx->pf_tg.push_back(capped);
-        return PfList{nullptr, 0, 0};
+// halo of vector v on distributed level j: colour c's owned values (c < 0: every ghost)
+static void exch(mgm_ctx* ctx, int j, double* v, int c, cudaStream_t st) {
+    if (!dist_level(ctx, j) || g_dry) return;
+    Level& L = ctx->lv[j];
+    const int np = (int)L.peers.size();
+    if (np == 0) return;
+    const int nc1 = L.ncol + 1;
+    std::vector<Xfer> x((size_t)np);
+    i64 maxlen = 0;
+    for (int i = 0; i < np; ++i) {
+        const i64 s0 = c < 0 ? L.send_off[i] : L.send_coff[(size_t)i * nc1 + c];
+        const i64 s1 = c < 0 ? L.send_off[i + 1] : L.send_coff[(size_t)i * nc1 + c + 1];
+        const i64 r0 = c < 0 ? L.recv_off[i] : L.recv_coff[(size_t)i * nc1 + c];
+        const i64 r1 = c < 0 ? L.recv_off[i + 1] : L.recv_coff[(size_t)i * nc1 + c + 1];
+        maxlen = std::max(maxlen, s1 - s0);
+        x[(size_t)i] = Xfer{L.peers[(size_t)i], L.d_sendbuf + s0, s1 - s0, v + L.gbase + r0, r1 - r0};
     }
-    if (ctx->pf_mode != 2) return PfList{nullptr, 0, 0};
-    const int t = ctx->pf_pos++;
-    const int T = (int)ctx->pf_off.size() - 1;
-    if (!issuer || t + 1 >= T) return PfList{nullptr, 0, 0};
-    int hi = std::min(T - 1, t + ctx->pf_dist);
-    if (budget > 0) {  // as many following targets as fit the budget
-        i64 acc = 0;
-        hi = t;
-        while (hi + 1 < T) {
-            i64 tb = 0;
-            for (int q = ctx->pf_off[hi + 1]; q < ctx->pf_off[hi + 2]; ++q) tb += ctx->pf_flat[(size_t)q].bytes;
-            if (acc + tb > budget && hi > t) break;
-            acc += tb;
-            ++hi;
-        }
+    if (maxlen > 0) {
+        const int chunks = (int)std::min<i64>(32, (maxlen + 255) / 256);
+        launch(false, k_pack, (unsigned)(chunks * np), 256, 0, st, chunks,
+               (const i64*)(L.d_srange + (size_t)(c + 1) * 2 * np), (const i32*)L.d_send_idx, (const double*)v,
+               L.d_sendbuf);
     }
-    const int lo = std::max(ctx->pf_last + 1, t + 1);
-    if (hi < lo) return PfList{nullptr, 0, 0};
-    ctx->pf_last = hi;
-    return PfList{ctx->d_pf + ctx->pf_off[lo], ctx->pf_off[hi + 1] - ctx->pf_off[lo], ctx->pf_late};
+    if (!ctx->tp->exchange(x, st) && ctx->err.empty()) ctx->err = "halo exchange failed";
+    ctx->vcycle_kernels += 2;
 }
+
+// Krylov / border inner products: rows this rank contributes (the replicated Poisson
+// multiplier is counted once, by rank 0)
+static i64 dot_rows(const mgm_ctx* ctx) {
+    return ctx->lv[0].n + ((ctx->poisson && ctx->rank == 0) ? 1 : 0);
+}
+// rows of a level-0 vector (owned rows + multiplier; ghosts excluded)
+static i64 vec_rows(const mgm_ctx* ctx) { return ctx->lv[0].n + (ctx->poisson ? 1 : 0); }
 
 bool timing_on(const mgm_ctx* ctx);
 // zg: first forward sweep from a zero guess (k_gs_colour ZG; shifted problems only)
@@ -1395,34 +1557,39 @@ void enqueue_sweep(mgm_ctx* ctx, int j, bool backward, cudaStream_t st, bool zg 
     double bytes = 0.0;
     int nl = 0;
     for (int q = (skip_c0 && zg) ? 1 : 0; q < L.ncol; ++q) {  // (colour 0 done by the restriction)
-        int c = backward ? L.ncol - 1 - q : q;
+        const int c = backward ? L.ncol - 1 - q : q;
         const i64 c0 = L.coff[c], c1 = L.coff[c + 1];
-        if (c1 <= c0) continue;
-        for_my_pieces(ctx, j, c0, c1, [&](i64 a, i64 b) {
-            if (b <= a) return;
-            {
-                Regions rg;
-                if (!ctx->pf_l0only || j == 0) {
-                    pf_sell(rg, L.h_sptr, L.scol, L.sval, a, b);
-                    if (!ctx->pf_nof) rg.push_back(pf_region(L.f + a, 8 * (b - a)));
-                }
-                const PfList pf = pf_take(ctx, rg, !ctx->pf_l0only || j == 0);
-                launch_gs(ctx->pdl, ctx->poisson, L.tpr, (int)a, (int)b, (int)(b - (a & ~31)), L, st, pf, zg);
-            }
+        if (c1 > c0) {
+            if (L.dist)  // the undistributed launch's threads per row: same per-row arithmetic
+                launch_gs_fixed(ctx->pdl, ctx->poisson, L.tpr_col[(size_t)c], (int)c0, (int)c1,
+                                (int)(c1 - (c0 & ~31)), L, st, zg);
+            else
+                launch_gs(ctx->pdl, ctx->poisson, L.tpr, (int)c0, (int)c1, (int)(c1 - (c0 & ~31)), L, st,
+                          PfList{nullptr, 0, 0}, zg);
             // algorithmic bytes; a zero-guess sweep reads its stored entries and f, writes u
-            bytes += zg ? (12.0 * (double)L.lower_per_colour[c] * (double)(b - a) / (double)(c1 - c0) + 16.0 * (double)(b - a))
-                        : sweep_colour_bytes(L, b - a);
+            bytes += zg ? (12.0 * (double)L.lower_per_colour[c] + 16.0 * (double)(c1 - c0))
+                        : sweep_colour_bytes(L, c1 - c0);
             ++nl;
             ctx->vcycle_kernels++;
-        });
-        dist_exchange(ctx, j, L.u, c0, c1, st);
+        }
+        exch(ctx, j, L.u, c, st);  // (collective: every rank calls it, even with no rows of c)
     }
     if (j == 0) timer_end(ctx, tcls, st, bytes, nl);
 }
 
-// Poisson border row: y[n] = fs*f[n] + sign * (c . x)
-void enqueue_border_dot(mgm_ctx* ctx, const Level& L, const double* x, const double* f, double fs, double sign,
-                        double* y, cudaStream_t st) {
+// Poisson border row: y[n] = fs*f[n] + sign * (c . x)  (distributed: + allreduce of c . x)
+void enqueue_border_dot(mgm_ctx* ctx, int j, const double* x, const double* f, double fs, double sign, double* y,
+                        cudaStream_t st) {
+    const Level& L = ctx->lv[j];
+    if (dist_level(ctx, j)) {
+        double* s = ctx->dh + 600;
+        k_multidot_fin<<<RED_BLOCKS, RED_THREADS, 0, st>>>((i64)L.n, (const double*)L.c, (i64)0, 1, x, ctx->partials,
+                                                           ctx->tickets, s, (double*)nullptr);
+        if (!ctx->tp->allreduce_sum(s, 1, st) && ctx->err.empty()) ctx->err = "allreduce failed";
+        k_border_set<<<1, 32, 0, st>>>(s, fs, f, (int)L.n, sign, y);
+        ctx->vcycle_kernels += 3;
+        return;
+    }
     launch(ctx->pdl, k_multidot, RED_BLOCKS, RED_THREADS, 0, st, (i64)L.n, (const double*)L.c, (i64)0, 1, x,
            ctx->partials);
     launch(ctx->pdl, k_border_finish, 1, 32, 0, st, (const double*)ctx->partials, (int)RED_BLOCKS, fs, f, (int)L.n,
@@ -1430,85 +1597,76 @@ void enqueue_border_dot(mgm_ctx* ctx, const Level& L, const double* x, const dou
     ctx->vcycle_kernels += 2;
 }
 
-// y = L x (level j)
+// y = L x (level j); distributed: x must have its ghosts current (the callers exchange)
 void enqueue_spmv(mgm_ctx* ctx, int j, const double* x, double* y, cudaStream_t st) {
     Level& L = ctx->lv[j];
     if (j == 0) timer_begin(ctx, 1, st);
-    for_my_pieces(ctx, j, 0, L.n, [&](i64 a, i64 b) {
-        launch_spmv(ctx->pdl, 0, ctx->poisson, L.stpr, a, b, L.n, L.sptr, L.scol, L.sval, x, nullptr, y, L.c, st);
-    });
-    dist_exchange(ctx, j, y, 0, L.n, st);
+    launch_spmv(ctx->pdl, 0, ctx->poisson, L.stpr, 0, L.n, L.n, L.sptr, L.scol, L.sval, x, nullptr, y, L.c, st);
     if (j == 0) timer_end(ctx, 1, st, 12.0 * L.nnz + 16.0 * L.n);
-    if (ctx->poisson) enqueue_border_dot(ctx, L, x, nullptr, 0.0, 1.0, y, st);
+    if (ctx->poisson) enqueue_border_dot(ctx, j, x, nullptr, 0.0, 1.0, y, st);
 }
 
 // t = f - L u (level j), Poisson: t[n] = f[n] - c.u.  after_zg: u is the result of ONE forward
 // sweep from a zero guess, so t = -(later-colour part of L) u (k_sell_spmv MODE 2)
 // morton_t: write t in the level's Morton order (the restriction then gathers with Morton
-// columns, a few sectors per coarse row instead of one per fine entry; not on split levels)
+// columns, a few sectors per coarse row instead of one per fine entry; not on distributed levels)
 void enqueue_residual(mgm_ctx* ctx, int j, const double* f, const double* u, double* t, cudaStream_t st,
                       bool after_zg = false, bool morton_t = false) {
     Level& L = ctx->lv[j];
-    g_yperm = (morton_t && L.l2m) ? L.l2m : nullptr;
+    g_yperm = (morton_t && L.l2m && !L.dist) ? L.l2m : nullptr;
     struct ResetP { ~ResetP() { g_yperm = nullptr; } } resetp_;
     // (bandwidth-bound levels only: on the small latency-bound levels the extra per-row table
     // loads cost more than the skipped entries save -- cfg3 L2/L3 17 -> 23 us)
     const int mode = (after_zg && L.sluw && !ctx->poisson && !ctx->no_zg && L.n >= ctx->upper_res_min) ? 2 : 1;
     g_sluw = L.sluw;
     g_nlow = L.nlow;
-    for_my_pieces(ctx, j, 0, L.n, [&](i64 a, i64 b) {
-        Regions rg;
-        if (!ctx->pf_l0only) pf_sell(rg, L.h_sptr, L.scol, L.sval, a, b);
-        const PfList pf = pf_take(ctx, rg, !ctx->pf_l0only);
-        launch_spmv(ctx->pdl, mode, ctx->poisson, L.stpr, a, b, L.n, L.sptr, L.scol, L.sval, u, f, t, L.c, st, pf);
-        ctx->vcycle_kernels++;
-    });
-    dist_exchange(ctx, j, t, 0, L.n, st);
-    if (ctx->poisson) enqueue_border_dot(ctx, L, u, f, 1.0, -1.0, t, st);
+    launch_spmv(ctx->pdl, mode, ctx->poisson, L.stpr, 0, L.n, L.n, L.sptr, L.scol, L.sval, u, f, t, L.c, st);
+    ctx->vcycle_kernels++;
+    if (ctx->poisson) enqueue_border_dot(ctx, j, u, f, 1.0, -1.0, t, st);
 }
 
 // y (next level) = R_j x
 // fuse_c0: also set colour 0 of level j+1's presmooth from zero (u = f / a_rr), which the
 // following sweep then skips (undistributed, shifted problems)
-void enqueue_restrict(mgm_ctx* ctx, int j, const double* x, double* y, cudaStream_t st, bool morton_x = false,
+// Distributed level j: x's ghosts (the fine residual rows the restriction reads) are exchanged
+// first; if level j+1 is the first replicated level, this rank's coarse rows go to the staging
+// vector, which is all-gathered and permuted into y.
+void enqueue_restrict(mgm_ctx* ctx, int j, double* x, double* y, cudaStream_t st, bool morton_x = false,
                       bool fuse_c0 = false) {
     Level& L = ctx->lv[j];
     Level& Ln = ctx->lv[j + 1];
     if (fuse_c0) g_c0 = C0Fuse{Ln.u, Ln.sptr, Ln.sval, (int)Ln.coff[1]};
     struct ResetC0 { ~ResetC0() { g_c0 = C0Fuse{nullptr, nullptr, nullptr, 0}; } } resetc0_;
-    const i32* rcol = (morton_x && L.rcol_m) ? L.rcol_m : L.rcol;
-    for_my_pieces(ctx, j, 0, Ln.n, [&](i64 a, i64 b) {
-        Regions rg;
-        if (!ctx->pf_l0only) pf_sell(rg, L.h_rptr, L.rcol, L.rval, a, b);
-        const PfList pf = pf_take(ctx, rg, !ctx->pf_l0only);
-        launch_spmv(ctx->pdl, 0, false, L.rtpr, a, b, Ln.n, L.rptr, rcol, L.rval, x, nullptr, y, nullptr, st, pf);
-        ctx->vcycle_kernels++;
-    });
-    dist_exchange(ctx, j, y, 0, Ln.n, st);
+    const i32* rcol = (morton_x && L.rcol_m && !L.dist) ? L.rcol_m : L.rcol;
+    exch(ctx, j, x, -1, st);
+    const bool to_stage = L.dist && L.d_stage_all;
+    const i64 nrows = to_stage ? L.nstage : Ln.n;
+    double* out = to_stage ? L.d_stage_mine : y;
+    launch_spmv(ctx->pdl, 0, false, L.rtpr, 0, nrows, nrows, L.rptr, rcol, L.rval, x, nullptr, out, nullptr, st);
+    ctx->vcycle_kernels++;
+    if (to_stage) {
+        if (!ctx->tp->allgatherv(L.d_stage_mine, L.d_stage_all, L.stage_off, st) && ctx->err.empty())
+            ctx->err = "all-gather failed";
+        k_scatter<<<blocks_for(Ln.n, 256), 256, 0, st>>>((int)Ln.n, L.d_stage_perm, L.d_stage_all, y);
+        ctx->vcycle_kernels += 2;
+    }
     if (ctx->poisson) {
         launch(ctx->pdl, k_copy1, 1, 1, 0, st, (const double*)(x + L.n), y + Ln.n);
         ctx->vcycle_kernels++;
     }
 }
 
+// e_j += P_j e_{j+1}; distributed: the ghosts of e_j are refreshed afterwards
 void enqueue_interp_correct(mgm_ctx* ctx, int j, const double* ec, double* e, cudaStream_t st) {
     Level& L = ctx->lv[j];
     Level& Ln = ctx->lv[j + 1];
     auto kern = ctx->poisson ? (L.pm <= 8 ? k_interp_correct<true, 8> : k_interp_correct<true, 16>)
                              : (L.pm <= 8 ? k_interp_correct<false, 8> : k_interp_correct<false, 16>);
-    for_my_pieces(ctx, j, 0, L.n, [&](i64 a, i64 b) {
-        const i64 extra = (ctx->poisson && b == L.n) ? 1 : 0;  // multiplier thread
-        Regions rg;
-        for (int k = 0; k < L.pm && b > a && !ctx->pf_l0only; ++k) {  // slot-major [pm][n]
-            rg.push_back(pf_region(L.pval + (i64)k * L.n + a, 8 * (b - a)));
-            rg.push_back(pf_region(L.pcol + (i64)k * L.n + a, 4 * (b - a)));
-        }
-        const PfList pf = pf_take(ctx, rg, !ctx->pf_l0only);
-        launch(ctx->pdl, kern, blocks_for(b - a + extra, 256), 256, 0, st, (int)a, (int)b, (int)L.n, L.pm,
-               (const i32*)L.pcol, (const double*)L.pval, ec, e, (int)Ln.n, pf);
-        ctx->vcycle_kernels++;
-    });
-    dist_exchange(ctx, j, e, 0, L.n, st);
+    const i64 extra = ctx->poisson ? 1 : 0;  // multiplier thread
+    launch(ctx->pdl, kern, blocks_for(L.n + extra, 256), 256, 0, st, 0, (int)L.n, (int)L.n, L.pm, (const i32*)L.pcol,
+           (const double*)L.pval, ec, e, (int)Ln.n, PfList{nullptr, 0, 0});
+    ctx->vcycle_kernels++;
+    exch(ctx, j, e, -1, st);
 }
 
 void enqueue_coarse(mgm_ctx* ctx, const double* r, double* e, cudaStream_t st) {
@@ -1526,8 +1684,7 @@ void enqueue_coarse(mgm_ctx* ctx, const double* r, double* e, cudaStream_t st) {
 }
 
 void enqueue_zero(mgm_ctx* ctx, double* x, i64 n, cudaStream_t st) {
-    const PfList pf = pf_take(ctx, Regions{}, !ctx->pf_l0only);
-    launch(ctx->pdl, k_fill, blocks_for(n, 256), 256, 0, st, n, x, 0.0, pf);
+    launch(ctx->pdl, k_fill, blocks_for(n, 256), 256, 0, st, n, x, 0.0, PfList{nullptr, 0, 0});
     ctx->vcycle_kernels++;
 }
 
@@ -1679,7 +1836,7 @@ void enqueue_vcycle(mgm_ctx* ctx, cudaStream_t st) {
         // e_j = 0 then presmooth; the first forward sweep from the zero guess writes every row
         // and reads only earlier-colour values, so the zero fill is not needed
         const bool zg = zg_level(j);
-        if (!zg) enqueue_zero(ctx, lv[j].u, lv[j].n + pad, st);
+        if (!zg) enqueue_zero(ctx, lv[j].u, lv[j].n + pad + lv[j].nghost, st);  // (+ ghosts: distributed)
         for (int s = 0; s < nu1; ++s) enqueue_sweep(ctx, j, pre_b, st, s == 0 && zg, s == 0 && c0_fused(j));
         stamp(ctx, "zero+presmooth", j, st);
         const bool mt = !dist_level(ctx, j) && lv[j].n >= ctx->morton_t_min;
@@ -1705,7 +1862,7 @@ void enqueue_vcycle(mgm_ctx* ctx, cudaStream_t st) {
         cfg.attrs = at;
         cfg.numAttrs = g_use_pdl ? 2 : 1;
         cfg.dynamicSmemBytes = ctx->bot_smem;
-        const PfList pf = pf_take(ctx, ctx->pf_l0only ? Regions{} : ctx->bot_pf, !ctx->pf_l0only, ctx->pf_bot_budget);
+        const PfList pf{nullptr, 0, 0};
         auto bottom = [&](int q0, int nph, int arm0, int arm1, PfList pfl) {
             if (g_dry) return;
             const BPhase* ph = (const BPhase*)ctx->d_phases + q0;
@@ -1746,55 +1903,15 @@ void enqueue_vcycle(mgm_ctx* ctx, cudaStream_t st) {
 bool timing_on(const mgm_ctx* ctx) { return ctx->timer[0].on || ctx->timer[1].on || ctx->timer[3].on; }
 
 bool zg_capable(const mgm_ctx* ctx);
-// Record the V-cycle schedule's prefetch targets with a dry enqueue pass and upload the
-// region table (a new table only when the schedule changed: captured graphs keep theirs).
-mgm_status pf_prepare(mgm_ctx* ctx, cudaStream_t st) {
-    ctx->pf_mode = 0;
-    if (ctx->pf_dist <= 0) return MGM_OK;
-    ctx->pf_tg.clear();
-    ctx->pf_mode = 1;
-    g_dry = true;
-    enqueue_vcycle(ctx, st);
-    g_dry = false;
-    ctx->pf_mode = 0;
-    std::vector<PfRegion> flat;
-    std::vector<int> off{0};
-    for (const auto& t : ctx->pf_tg) {
-        flat.insert(flat.end(), t.begin(), t.end());
-        off.push_back((int)flat.size());
-    }
-    const bool same = ctx->d_pf && off == ctx->pf_off && flat.size() == ctx->pf_flat.size() &&
-                      std::equal(flat.begin(), flat.end(), ctx->pf_flat.begin(),
-                                 [](const PfRegion& a, const PfRegion& b) { return a.p == b.p && a.bytes == b.bytes; });
-    if (!same) {
-        if (ctx->d_pf) ctx->pf_old.push_back(ctx->d_pf);
-        ctx->d_pf = nullptr;
-        CK(dev_malloc((void**)&ctx->d_pf, sizeof(PfRegion) * std::max<size_t>(1, flat.size())));
-        if (!flat.empty())
-            CK(cudaMemcpy(ctx->d_pf, flat.data(), sizeof(PfRegion) * flat.size(), cudaMemcpyHostToDevice));
-        ctx->pf_flat = flat;
-        ctx->pf_off = off;
-    }
-    ctx->pf_mode = 2;
-    ctx->pf_pos = 0;
-    ctx->pf_last = 0;
-    return MGM_OK;
-}
-
 mgm_status build_graph(mgm_ctx* ctx, bool zero_guess = false) {
     cudaGraphExec_t& gx = zero_guess ? ctx->vgraph0 : ctx->vgraph;
     if (gx) return MGM_OK;
     ctx->vc_zero_guess = zero_guess && zg_capable(ctx);
     struct ResetZ { mgm_ctx* c; ~ResetZ() { c->vc_zero_guess = false; } } resetz_{ctx};
     cudaGraph_t g;
-    {
-        mgm_status ps = pf_prepare(ctx, ctx->st);
-        if (ps) return ps;
-    }
     CK(cudaStreamBeginCapture(ctx->st, cudaStreamCaptureModeThreadLocal));
     g_launch_err.clear();
     enqueue_vcycle(ctx, ctx->st);
-    ctx->pf_mode = 0;
     const cudaError_t ce = cudaStreamEndCapture(ctx->st, &g);
     if (ce != cudaSuccess || !g_launch_err.empty()) {
         ctx->err = "V-cycle capture failed: " + std::string(cudaGetErrorString(ce)) + "; first failed launch: " +
@@ -1816,14 +1933,10 @@ bool zg_capable(const mgm_ctx* ctx) {
 }
 mgm_status run_vcycle(mgm_ctx* ctx, cudaStream_t st, bool zero_guess = false) {
     zero_guess = zero_guess && zg_capable(ctx);
-    if (timing_on(ctx)) {
-        ctx->vc_zero_guess = zero_guess;
-        mgm_status ps = pf_prepare(ctx, st);
-        if (ps) { ctx->vc_zero_guess = false; return ps; }
+    if (timing_on(ctx) || (ctx->tp && !ctx->tp->capturable())) {  // eager: event timing / fake ranks
         ctx->vc_zero_guess = zero_guess;
         timer_begin(ctx, 2, st);
         enqueue_vcycle(ctx, st);
-        ctx->pf_mode = 0;
         ctx->vc_zero_guess = false;
         timer_end(ctx, 2, st, 0.0);
         return MGM_OK;
@@ -1857,23 +1970,37 @@ mgm_status ensure_krylov(mgm_ctx* ctx) {
 // in-kernel finish) and the pieces are summed with ncclAllReduce (identical on every rank).
 void enqueue_multidot(mgm_ctx* ctx, i64 n, const double* V, i64 ld, int k1, const double* w, double* out,
                       double* acc, cudaStream_t st) {
-    if (!ctx->comm) {
+    if (!dist_on(ctx)) {
         k_multidot_fin<<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, V, ld, k1, w, ctx->partials, ctx->tickets, out, acc);
         return;
     }
-    i64 a, b;
-    piece(0, n, ctx->nranks, ctx->rank, a, b);
-    k_multidot_fin<<<RED_BLOCKS, RED_THREADS, 0, st>>>(b - a, V + a, ld, k1, w + a, ctx->partials, ctx->tickets, out,
+    // distributed: this rank's rows (deterministic in-kernel finish), then a sum-allreduce
+    k_multidot_fin<<<RED_BLOCKS, RED_THREADS, 0, st>>>(dot_rows(ctx), V, ld, k1, w, ctx->partials, ctx->tickets, out,
                                                        nullptr);
-    nccl_allreduce_sum(out, (size_t)k1, ctx->comm, st);
+    if (!ctx->tp->allreduce_sum(out, k1, st) && ctx->err.empty()) ctx->err = "allreduce failed";
     if (acc) k_vadd<<<1, 128, 0, st>>>(k1, acc, out);
 }
 void enqueue_dot(mgm_ctx* ctx, i64 n, const double* a, const double* b, double* out, cudaStream_t st) {
     enqueue_multidot(ctx, n, a, 0, 1, b, out, nullptr, st);
 }
 
-// A x on level 0 (bordered in Poisson mode), n-vector incl. multiplier
-void enqueue_apply_A(mgm_ctx* ctx, const double* x, double* y, cudaStream_t st) { enqueue_spmv(ctx, 0, x, y, st); }
+// A x on level 0 (bordered in Poisson mode), n-vector incl. multiplier.  Distributed: x is
+// copied into the ghosted scratch lv[0].t (unless it is lv[0].u, which has ghost slots) and
+// its ghosts are refreshed before the SpMV.
+void enqueue_apply_A(mgm_ctx* ctx, const double* x, double* y, cudaStream_t st) {
+    if (!dist_on(ctx)) {
+        enqueue_spmv(ctx, 0, x, y, st);
+        return;
+    }
+    Level& L0 = ctx->lv[0];
+    double* xg = L0.u;
+    if (x != L0.u) {
+        xg = L0.t;
+        cudaMemcpyAsync(xg, x, sizeof(double) * vec_rows(ctx), cudaMemcpyDeviceToDevice, st);
+    }
+    exch(ctx, 0, xg, -1, st);
+    enqueue_spmv(ctx, 0, xg, y, st);
+}
 
 // z = M(v): one V-cycle from zero, result left in lv[0].u
 // colour 0 of the level-0 presmooth from the zero guess done while copying the input (the
@@ -1886,19 +2013,20 @@ C0Fuse c0_l0(mgm_ctx* ctx) {
                             : C0Fuse{nullptr, nullptr, nullptr, 0};
 }
 mgm_status enqueue_precond(mgm_ctx* ctx, const double* v, cudaStream_t st) {
-    i64 n = ctx->N + (ctx->poisson ? 1 : 0);
+    const i64 n = vec_rows(ctx);
     if (c0_fused_l0(ctx))
         k_copy_col<<<RED_BLOCKS, 256, 0, st>>>(n, v, 0, (const int*)nullptr, ctx->lv[0].f, c0_l0(ctx));
     else
         CK(cudaMemcpyAsync(ctx->lv[0].f, v, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
-    if (!zg_capable(ctx)) CK(cudaMemsetAsync(ctx->lv[0].u, 0, sizeof(double) * n, st));
+    if (!zg_capable(ctx))  // (ghost slots too: the first sweep reads them)
+        CK(cudaMemsetAsync(ctx->lv[0].u, 0, sizeof(double) * (n + ctx->lv[0].nghost), st));
     return run_vcycle(ctx, st, true);  // M v from the zero guess
 }
 
 // Right-preconditioned GMRES(restart) with CGS2 orthogonalisation (equal to MGS in exact
 // arithmetic; O15), Givens rotations on the host.  b, x in lib order (x = 0 on entry).
 mgm_status gmres_lib(mgm_ctx* ctx, double tol, int maxit, mgm_report* rep, cudaStream_t st) {
-    const i64 n = ctx->N + (ctx->poisson ? 1 : 0);
+    const i64 n = vec_rows(ctx);
     const int m = ctx->restart;
     const i64 ld = ctx->ld;
     double* V = ctx->V;
@@ -1955,10 +2083,10 @@ mgm_status gmres_lib(mgm_ctx* ctx, double tol, int maxit, mgm_report* rep, cudaS
             enqueue_multidot(ctx, n, V, ld, k1, w, h1, nullptr, st);
             k_multiaxpy<<<RED_BLOCKS * 2, 256, 0, st>>>(n, V, ld, k1, h1, w);
             enqueue_multidot(ctx, n, V, ld, k1, w, h2, h1, st);
-            if (!ctx->comm) {
+            if (!dist_on(ctx)) {
                 k_multiaxpy_norm<<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, V, ld, k1, h2, w, ctx->partials, ctx->tickets,
                                                                      nr);
-            } else {  // full (replicated) update, distributed norm
+            } else {  // local update, distributed norm
                 k_multiaxpy<<<RED_BLOCKS * 2, 256, 0, st>>>(n, V, ld, k1, h2, w);
                 enqueue_dot(ctx, n, w, w, nr, st);
             }
@@ -2010,7 +2138,7 @@ mgm_status gmres_lib(mgm_ctx* ctx, double tol, int maxit, mgm_report* rep, cudaS
     k_axpby<<<RED_BLOCKS, 256, 0, st>>>(n, 1.0, ctx->b, -1.0, w, w);
     enqueue_dot(ctx, n, w, w, nr, st);
     CK(cudaMemcpyAsync(ctx->hh, nr, sizeof(double), cudaMemcpyDeviceToHost, st));
-    if (ctx->poisson) CK(cudaMemcpyAsync(ctx->hh + 1, ctx->xs + ctx->N, sizeof(double), cudaMemcpyDeviceToHost, st));
+    if (ctx->poisson) CK(cudaMemcpyAsync(ctx->hh + 1, ctx->xs + ctx->lv[0].n, sizeof(double), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     if (rep) {
         rep->iterations = its;
@@ -2034,7 +2162,7 @@ static size_t gmres_dev_doubles(const mgm_ctx* ctx) {
     return 2 + (m + 1) * m + 2 * m + (m + 1) + (size_t)ctx->g_hist_cap;
 }
 static bool gmres_dev_ok(const mgm_ctx* ctx) {
-    return !ctx->poisson && !ctx->comm && !timing_on(ctx) && ctx->restart <= 128 && ctx->p >= 1 &&
+    return !ctx->poisson && !dist_on(ctx) && !timing_on(ctx) && ctx->restart <= 128 && ctx->p >= 1 &&
            std::getenv("MGM_HOST_GMRES") == nullptr;
 }
 static mgm_status build_gmres_graph(mgm_ctx* ctx) {
@@ -2209,7 +2337,7 @@ mgm_status gmres_dev(mgm_ctx* ctx, double tol, int maxit, mgm_report* rep, cudaS
 // in lib order (x = 0 on entry).  Workspace columns of V: r_hat, r, p, v, p_hat, s, t
 // (r_hat/r and s/t adjacent so that one multi-dot gives two inner products).
 mgm_status bicgstab_lib(mgm_ctx* ctx, double tol, int maxit, mgm_report* rep, cudaStream_t st) {
-    const i64 n = ctx->N + (ctx->poisson ? 1 : 0);
+    const i64 n = vec_rows(ctx);
     const i64 ld = ctx->ld;
     double* rh = ctx->V;
     double* r = ctx->V + ld;
@@ -2304,7 +2432,7 @@ mgm_status bicgstab_lib(mgm_ctx* ctx, double tol, int maxit, mgm_report* rep, cu
     k_axpby<<<nb, nt, 0, st>>>(n, 1.0, ctx->b, -1.0, ctx->w, ctx->w);
     enqueue_dot(ctx, n, ctx->w, ctx->w, dd, st);
     CK(cudaMemcpyAsync(hh, dd, sizeof(double), cudaMemcpyDeviceToHost, st));
-    if (ctx->poisson) CK(cudaMemcpyAsync(hh + 1, ctx->xs + ctx->N, sizeof(double), cudaMemcpyDeviceToHost, st));
+    if (ctx->poisson) CK(cudaMemcpyAsync(hh + 1, ctx->xs + ctx->lv[0].n, sizeof(double), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     if (rep) {
         rep->iterations = its;
@@ -2448,7 +2576,7 @@ static void enqueue_res_b(mgm_ctx* ctx, int K, cudaStream_t st) {  // bres = bf0
 }
 
 mgm_status standalone_lib(mgm_ctx* ctx, double tol, int maxit, mgm_report* rep, cudaStream_t st) {
-    const i64 n = ctx->N + (ctx->poisson ? 1 : 0);
+    const i64 n = vec_rows(ctx);
     double* nr = ctx->dh + 512;
     mgm_status s;
     enqueue_dot(ctx, n, ctx->b, ctx->b, nr, st);
@@ -2458,7 +2586,8 @@ mgm_status standalone_lib(mgm_ctx* ctx, double tol, int maxit, mgm_report* rep, 
     if (ctx->warm && fn != 0.0)  // u starts at x0 (the applications' warm start)
         CK(cudaMemcpyAsync(ctx->lv[0].u, ctx->xs, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
     else
-        CK(cudaMemsetAsync(ctx->lv[0].u, 0, sizeof(double) * n, st));
+        CK(cudaMemsetAsync(ctx->lv[0].u, 0, sizeof(double) * (n + ctx->lv[0].nghost), st));
+    exch(ctx, 0, ctx->lv[0].u, -1, st);  // (distributed: the first sweep reads the ghosts of x0)
     CK(cudaMemsetAsync(ctx->xs, 0, sizeof(double) * n, st));
     if (fn == 0.0) {
         if (rep) { rep->iterations = 0; rep->converged = 1; rep->final_rel_residual = 0.0; }
@@ -2484,7 +2613,7 @@ mgm_status standalone_lib(mgm_ctx* ctx, double tol, int maxit, mgm_report* rep, 
     }
     CK(cudaMemcpyAsync(ctx->xs, ctx->lv[0].u, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
     if (ctx->poisson) {
-        CK(cudaMemcpyAsync(ctx->hh + 1, ctx->xs + ctx->N, sizeof(double), cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(ctx->hh + 1, ctx->xs + ctx->lv[0].n, sizeof(double), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
     }
     if (rep) {
@@ -2503,6 +2632,335 @@ mgm_status check_ctx(mgm_ctx* ctx) {
 }
 
 }  // namespace
+
+// ---------------------------------------------------------------------------------------
+// Partition of the hierarchy (mgm_dist_attach): levels 0..D-1 become this rank's Morton
+// block + ghosts (PartTables, host_setup.cpp partition_level), built from the undistributed
+// structures every rank holds after the (deterministic, replicated) setup; the
+// undistributed device arrays of those levels are freed.  Every local operator row keeps
+// the undistributed row's entries in the same order, and each colour launch keeps its
+// threads per row, so the distributed V-cycle computes every row with the same arithmetic.
+// ---------------------------------------------------------------------------------------
+namespace {
+
+template <class T>
+std::vector<T> download(const T* d, i64 n) {
+    std::vector<T> h((size_t)std::max<i64>(n, 0));
+    if (n > 0) cudaMemcpy(h.data(), d, sizeof(T) * (size_t)n, cudaMemcpyDeviceToHost);
+    return h;
+}
+
+// first level of the replicated bottom: the dense bottom, the cluster bottom, or the coarsest
+int bottom_level(const mgm_ctx* ctx) {
+    return ctx->denseJ > 0 ? ctx->denseJ : ctx->botJ > 0 ? ctx->botJ : ctx->p - 1;
+}
+
+// distributed levels: 0 .. D-1 with at least MGM_DIST_MIN_ROWS (default 16384) rows per rank
+// (below that a level is cheaper redundant than exchanged), never the bottom
+int choose_D(const mgm_ctx* ctx, int nranks) {
+    const int top = bottom_level(ctx);
+    i64 min_rows = 16384;
+    if (const char* e = std::getenv("MGM_DIST_MIN_ROWS")) min_rows = std::max<i64>(1, std::atoll(e));
+    int D = 1;
+    while (D < top && ctx->lv[D].n / nranks >= min_rows) ++D;
+    if (const char* e = std::getenv("MGM_DIST_LEVELS")) D = std::max(1, std::min(top, std::atoi(e)));
+    return D;
+}
+
+void free_level_device(Level& L) {
+    for (void* ptr : {(void*)L.sptr, (void*)L.scol, (void*)L.sval, (void*)L.pcol, (void*)L.pval, (void*)L.rptr,
+                      (void*)L.rcol, (void*)L.rval, (void*)L.u, (void*)L.f, (void*)L.t, (void*)L.c, (void*)L.slw,
+                      (void*)L.nlow, (void*)L.sluw, (void*)L.l2m, (void*)L.rcol_m, (void*)L.d_send_idx,
+                      (void*)L.d_sendbuf, (void*)L.d_srange, (void*)L.d_stage_mine, (void*)L.d_stage_all,
+                      (void*)L.d_stage_perm})
+        if (ptr) dev_free(ptr);
+}
+
+}  // namespace
+
+mgm_status dist_partition(mgm_ctx* ctx) {
+    const int P = ctx->nranks, q = ctx->rank;
+    if (ctx->p < 2) {
+        ctx->err = "multi-GPU solve needs at least two levels";
+        return MGM_ERR_ARG;
+    }
+    const int D = choose_D(ctx, P);
+    const i64 N = ctx->N;
+    const i64 pad = ctx->poisson ? 1 : 0;
+    cudaStream_t st = ctx->st;
+    auto& lv = ctx->lv;
+    // ---- owners: rank r owns the level-0 Morton indices [floor(rN/P), floor((r+1)N/P)); a
+    // coarse point keeps the owner of its level-0 point (coarse sets inherit the order)
+    std::vector<i64> mstart(P + 1);
+    for (int r = 0; r <= P; ++r) mstart[(size_t)r] = (i64)((__int128)r * N / P);
+    auto owner_of_m = [&](i64 m) {
+        return (int)(std::upper_bound(mstart.begin(), mstart.end(), m) - mstart.begin()) - 1;
+    };
+    std::vector<i64> mor0((size_t)N);
+    for (i64 r = 0; r < N; ++r) mor0[(size_t)lv[0].ids[(size_t)r]] = lv[0].lib2mor[(size_t)r];
+    std::vector<std::vector<int>> owner((size_t)D + 1);
+    for (int j = 0; j <= D; ++j) {
+        owner[(size_t)j].resize((size_t)lv[j].n);
+        for (i64 r = 0; r < lv[j].n; ++r) owner[(size_t)j][(size_t)r] = owner_of_m(mor0[(size_t)lv[j].ids[(size_t)r]]);
+    }
+    // ---- partition tables (this rank's) of the distributed levels
+    std::vector<PartTables> T((size_t)D);
+    for (int j = 0; j < D; ++j) {
+        std::vector<PartTables> all;
+        partition_level(lv[j].L_lib, owner[(size_t)j], lv[j].colour_lib, lv[j].ncol, &lv[j].P_lib, &owner[(size_t)j + 1],
+                        j > 0 ? &lv[j - 1].P_lib : nullptr, j > 0 ? &owner[(size_t)j - 1] : nullptr, P, all);
+        T[(size_t)j] = std::move(all[(size_t)q]);
+    }
+    // global row -> local column index (owned: 0..n-1; ghost g: n + pad + g), per level
+    std::vector<std::vector<i64>> cmap((size_t)D);
+    for (int j = 0; j < D; ++j) {
+        auto& c = cmap[(size_t)j];
+        c.assign((size_t)lv[j].n, -1);
+        const i64 nl = (i64)T[(size_t)j].rows.size();
+        for (i64 k = 0; k < nl; ++k) c[(size_t)T[(size_t)j].rows[(size_t)k]] = k;
+        for (size_t g = 0; g < T[(size_t)j].ghosts.size(); ++g) c[(size_t)T[(size_t)j].ghosts[g]] = nl + pad + (i64)g;
+    }
+    mgm_status s;
+    std::vector<Level> loc((size_t)D);
+    for (int j = 0; j < D; ++j) {
+        const Level& G = lv[j];
+        const PartTables& Tj = T[(size_t)j];
+        Level& L = loc[(size_t)j];
+        const i64 nl = (i64)Tj.rows.size();
+        const auto& cm = cmap[(size_t)j];
+        auto col_of = [&](i64 g) -> i32 {
+            const i64 v = cm[(size_t)g];
+            return (i32)(v >= 0 ? v : 0);  // (every column read is owned or a ghost by construction)
+        };
+        L.dist = true;
+        L.n = nl;
+        L.ncol = G.ncol;
+        L.nghost = (i64)Tj.ghosts.size();
+        L.gbase = nl + pad;
+        L.tpr = G.tpr;
+        L.rtpr = G.rtpr;
+        L.stpr = G.stpr;
+        L.gs_block = G.gs_block;
+        L.pm = G.pm;
+        L.gcoff = G.coff;
+        L.coff.assign((size_t)G.ncol + 1, 0);
+        for (i64 r : Tj.rows) L.coff[(size_t)G.colour_lib[(size_t)r] + 1]++;
+        for (int c = 0; c < G.ncol; ++c) L.coff[(size_t)c + 1] += L.coff[(size_t)c];
+        L.tpr_col.resize((size_t)G.ncol);
+        for (int c = 0; c < G.ncol; ++c)
+            L.tpr_col[(size_t)c] =
+                gs_tpr_for(G.tpr, G.coff[(size_t)c + 1] - (G.coff[(size_t)c] & ~(i64)31), G.gs_block);
+        L.ids.resize((size_t)nl);
+        L.colour_lib.resize((size_t)nl);
+        for (i64 k = 0; k < nl; ++k) {
+            L.ids[(size_t)k] = G.ids[(size_t)Tj.rows[(size_t)k]];
+            L.colour_lib[(size_t)k] = G.colour_lib[(size_t)Tj.rows[(size_t)k]];
+        }
+        // -- L_j: the undistributed SELL rows (pack_sell order), columns remapped
+        {
+            const auto gcol = download(G.scol, G.sell_stored);
+            const auto gval = download(G.sval, G.sell_stored);
+            const std::vector<uint8_t> gnlow = G.nlow ? download(G.nlow, G.n) : std::vector<uint8_t>();
+            const i64 ns = (nl + 31) / 32;
+            std::vector<i64> sptr((size_t)ns + 1, 0);
+            auto rlen = [&](i64 k) { const i64 r = Tj.rows[(size_t)k]; return G.L_lib.ptr[(size_t)r + 1] - G.L_lib.ptr[(size_t)r]; };
+            for (i64 sl = 0; sl < ns; ++sl) {
+                i64 w = 1;
+                for (i64 k = sl * 32; k < std::min(nl, sl * 32 + 32); ++k) w = std::max(w, rlen(k));
+                sptr[(size_t)sl + 1] = sptr[(size_t)sl] + 32 * w;
+            }
+            std::vector<i32> scol((size_t)sptr[(size_t)ns], 0);
+            std::vector<double> sval((size_t)sptr[(size_t)ns], 0.0);
+            std::vector<i32> slw, sluw;
+            std::vector<uint8_t> nlow;
+            if (G.nlow) {
+                slw.assign((size_t)ns, 1);
+                sluw.assign((size_t)ns, 1 << 30);
+                nlow.assign((size_t)nl, 0);
+                L.lower_per_colour.assign((size_t)G.ncol, 0);
+            }
+            for (i64 k = 0; k < nl; ++k) {
+                const i64 r = Tj.rows[(size_t)k], gs = r >> 5, gl = r & 31;
+                const i64 sl = k >> 5, lane = k & 31, w = (sptr[(size_t)sl + 1] - sptr[(size_t)sl]) / 32;
+                const i64 len = rlen(k);
+                for (i64 e = 0; e < w; ++e) {
+                    const i64 o = sptr[(size_t)sl] + 32 * e + lane;
+                    if (e < len) {
+                        const i64 go = G.h_sptr[(size_t)gs] + 32 * e + gl;
+                        scol[(size_t)o] = col_of(gcol[(size_t)go]);
+                        sval[(size_t)o] = gval[(size_t)go];
+                    } else {
+                        scol[(size_t)o] = (i32)k;
+                        sval[(size_t)o] = 0.0;
+                    }
+                }
+                if (G.nlow) {
+                    const int nlw = gnlow[(size_t)r];
+                    nlow[(size_t)k] = (uint8_t)nlw;
+                    slw[(size_t)sl] = std::max<i32>(slw[(size_t)sl], 1 + nlw);
+                    sluw[(size_t)sl] = std::min<i32>(sluw[(size_t)sl], 1 + nlw);
+                    L.lower_per_colour[(size_t)L.colour_lib[(size_t)k]] += 1 + nlw;
+                }
+            }
+            L.nnz = 0;
+            for (i64 k = 0; k < nl; ++k) L.nnz += rlen(k);
+            L.sell_stored = sptr[(size_t)ns];
+            bool uni = ns > 0;
+            for (i64 sl = 0; sl < ns && uni; ++sl) uni = sptr[(size_t)sl + 1] - sptr[(size_t)sl] == sptr[1] - sptr[0];
+            L.uniform_w = uni ? (int)((sptr[1] - sptr[0]) / 32) : 0;
+            L.h_sptr = sptr;
+            if ((s = upload(ctx, &L.sptr, sptr)) || (s = upload(ctx, &L.scol, scol)) || (s = upload(ctx, &L.sval, sval)))
+                return s;
+            if (G.nlow && ((s = upload(ctx, &L.slw, slw)) || (s = upload(ctx, &L.nlow, nlow)) ||
+                           (s = upload(ctx, &L.sluw, sluw))))
+                return s;
+        }
+        // -- P_j (ELL [pm][n], fine rows = my rows) and R_j (SELL, my coarse rows)
+        const bool next_dist = j + 1 < D;
+        const Level& Gn = lv[j + 1];
+        auto ccol_of = [&](i64 g) -> i32 {
+            if (!next_dist) return (i32)g;  // replicated coarse level: global lib index
+            const i64 v = cmap[(size_t)j + 1][(size_t)g];
+            return (i32)(v >= 0 ? v : 0);
+        };
+        {
+            const int pm = G.pm;
+            std::vector<i32> pcol((size_t)pm * nl);
+            std::vector<double> pval((size_t)pm * nl, 0.0);
+            i64 pnnz = 0;
+            for (i64 k = 0; k < nl; ++k) {
+                const i64 r = Tj.rows[(size_t)k];
+                const i64 a = G.P_lib.ptr[(size_t)r], cnt = G.P_lib.ptr[(size_t)r + 1] - a;
+                pnnz += cnt;
+                for (int e = 0; e < pm; ++e) {
+                    pcol[(size_t)e * nl + k] = ccol_of(G.P_lib.col[(size_t)(a + (e < cnt ? e : 0))]);
+                    pval[(size_t)e * nl + k] = e < cnt ? G.P_lib.val[(size_t)(a + e)] : 0.0;
+                }
+            }
+            L.p_nnz = pnnz;
+            if ((s = upload(ctx, &L.pcol, pcol)) || (s = upload(ctx, &L.pval, pval))) return s;
+        }
+        {
+            // my coarse rows: owned rows of level j+1 (ascending lib index)
+            std::vector<i64> crow;
+            if (next_dist) crow = T[(size_t)j + 1].rows;
+            else
+                for (i64 c = 0; c < Gn.n; ++c)
+                    if (owner[(size_t)j + 1][(size_t)c] == q) crow.push_back(c);
+            std::vector<i64> rcnt((size_t)Gn.n, 0);
+            for (i32 c : G.P_lib.col) rcnt[(size_t)c]++;
+            const auto grcol = download(G.rcol, G.r_stored);
+            const auto grval = download(G.rval, G.r_stored);
+            const i64 nc = (i64)crow.size(), ns = (nc + 31) / 32;
+            std::vector<i64> rptr((size_t)ns + 1, 0);
+            for (i64 sl = 0; sl < ns; ++sl) {
+                i64 w = 1;
+                for (i64 k = sl * 32; k < std::min(nc, sl * 32 + 32); ++k) w = std::max(w, rcnt[(size_t)crow[(size_t)k]]);
+                rptr[(size_t)sl + 1] = rptr[(size_t)sl] + 32 * w;
+            }
+            std::vector<i32> rcol((size_t)rptr[(size_t)ns], 0);
+            std::vector<double> rval((size_t)rptr[(size_t)ns], 0.0);
+            for (i64 k = 0; k < nc; ++k) {
+                const i64 c = crow[(size_t)k], gs = c >> 5, gl = c & 31;
+                const i64 sl = k >> 5, lane = k & 31, w = (rptr[(size_t)sl + 1] - rptr[(size_t)sl]) / 32;
+                const i64 len = rcnt[(size_t)c];
+                i32 first = 0;
+                for (i64 e = 0; e < w; ++e) {
+                    const i64 o = rptr[(size_t)sl] + 32 * e + lane;
+                    if (e < len) {
+                        const i64 go = G.h_rptr[(size_t)gs] + 32 * e + gl;
+                        rcol[(size_t)o] = col_of(grcol[(size_t)go]);
+                        rval[(size_t)o] = grval[(size_t)go];
+                        if (e == 0) first = rcol[(size_t)o];
+                    } else {
+                        rcol[(size_t)o] = first;
+                        rval[(size_t)o] = 0.0;
+                    }
+                }
+            }
+            L.r_stored = rptr[(size_t)ns];
+            L.h_rptr = rptr;
+            if ((s = upload(ctx, &L.rptr, rptr)) || (s = upload(ctx, &L.rcol, rcol)) || (s = upload(ctx, &L.rval, rval)))
+                return s;
+            if (!next_dist) {  // all-gather of the first replicated level
+                L.nstage = nc;
+                L.stage_off.assign((size_t)P + 1, 0);
+                for (i64 c = 0; c < Gn.n; ++c) L.stage_off[(size_t)owner[(size_t)j + 1][(size_t)c] + 1]++;
+                for (int r = 0; r < P; ++r) L.stage_off[(size_t)r + 1] += L.stage_off[(size_t)r];
+                std::vector<i32> perm((size_t)Gn.n);
+                std::vector<i64> fill(L.stage_off.begin(), L.stage_off.end() - 1);
+                for (i64 c = 0; c < Gn.n; ++c) perm[(size_t)fill[(size_t)owner[(size_t)j + 1][(size_t)c]]++] = (i32)c;
+                if ((s = upload(ctx, &L.d_stage_perm, perm))) return s;
+                CK(dalloc(&L.d_stage_mine, std::max<i64>(nc, 1)));
+                CK(dalloc(&L.d_stage_all, Gn.n));
+            }
+        }
+        // -- Poisson border, vectors
+        if (ctx->poisson) {
+            L.c_lib.resize((size_t)nl);
+            for (i64 k = 0; k < nl; ++k) L.c_lib[(size_t)k] = G.c_lib[(size_t)Tj.rows[(size_t)k]];
+            if ((s = upload(ctx, &L.c, L.c_lib))) return s;
+        }
+        const i64 vn = nl + pad + L.nghost;
+        CK(dalloc(&L.u, vn));
+        CK(dalloc(&L.f, vn));
+        CK(dalloc(&L.t, vn));
+        CK(cudaMemsetAsync(L.u, 0, sizeof(double) * vn, st));
+        CK(cudaMemsetAsync(L.f, 0, sizeof(double) * vn, st));
+        CK(cudaMemsetAsync(L.t, 0, sizeof(double) * vn, st));
+        // -- halo tables
+        L.peers = Tj.peers;
+        L.send_off = Tj.send_off;
+        L.recv_off = Tj.recv_off;
+        L.send_coff = Tj.send_coff;
+        L.recv_coff = Tj.recv_coff;
+        {
+            std::vector<i32> sidx(Tj.send_rows.size());
+            for (size_t e = 0; e < sidx.size(); ++e) sidx[e] = (i32)cm[(size_t)Tj.send_rows[e]];
+            if ((s = upload(ctx, &L.d_send_idx, sidx))) return s;
+            CK(dalloc(&L.d_sendbuf, (i64)std::max<size_t>(1, sidx.size())));
+            const size_t np = L.peers.size(), nc1 = (size_t)G.ncol + 1;
+            std::vector<i64> rng(nc1 * np * 2);
+            for (size_t i = 0; i < np; ++i) {
+                rng[2 * i] = L.send_off[i];
+                rng[2 * i + 1] = L.send_off[i + 1];
+                for (size_t c = 0; c + 1 < nc1; ++c) {
+                    rng[(c + 1) * np * 2 + 2 * i] = L.send_coff[i * nc1 + c];
+                    rng[(c + 1) * np * 2 + 2 * i + 1] = L.send_coff[i * nc1 + c + 1];
+                }
+            }
+            if ((s = upload(ctx, &L.d_srange, rng))) return s;
+        }
+    }
+    // ---- level-0 I/O order: my level-0 points in Morton order
+    {
+        const PartTables& T0 = T[0];
+        const i64 nl = (i64)T0.rows.size(), m0 = mstart[(size_t)q];
+        ctx->local_ids.assign((size_t)nl, -1);
+        std::vector<i32> l2io((size_t)nl);
+        for (i64 k = 0; k < nl; ++k) {
+            const i64 r = T0.rows[(size_t)k];
+            const i64 io = lv[0].lib2mor[(size_t)r] - m0;
+            l2io[(size_t)k] = (i32)io;
+            ctx->local_ids[(size_t)io] = lv[0].ids[(size_t)r];
+        }
+        dev_free(ctx->d_lib2orig);
+        ctx->d_lib2orig = nullptr;
+        if ((s = upload(ctx, &ctx->d_lib2orig, l2io))) return s;
+    }
+    CK(cudaStreamSynchronize(st));
+    for (int j = 0; j < D; ++j) {
+        free_level_device(lv[j]);
+        lv[j] = std::move(loc[(size_t)j]);
+    }
+    ctx->D = D;
+    for (cudaGraphExec_t* gx : {&ctx->vgraph, &ctx->vgraph0, &ctx->ggraph})  // re-capture with the halos
+        if (*gx) {
+            cudaGraphExecDestroy(*gx);
+            *gx = nullptr;
+        }
+    return MGM_OK;
+}
 
 // =======================================================================================
 // C ABI
@@ -2548,17 +3006,10 @@ mgm_status mgm_setup(const double* points, const double* normals, int64_t n_poin
     ctx->poisson = sp.problem == 1;
     ctx->restart = lp.restart;
     ctx->nthreads = std::max(1, std::min(64, (int)std::thread::hardware_concurrency()));
-    if (const char* e = std::getenv("MGM_DIST_LEVELS")) ctx->dist_levels = std::max(0, std::atoi(e));
-    if (const char* e = std::getenv("MGM_DIST_FAKE_RANKS")) ctx->fake_ranks = ctx->poisson ? 0 : std::max(0, std::atoi(e));
-    if (const char* e = std::getenv("MGM_PF_CAP_MB")) ctx->pf_cap = (i64)std::max(0, std::atoi(e)) << 20;
     if (std::getenv("MGM_NO_ZG")) ctx->no_zg = true;
     if (std::getenv("MGM_NO_C0_FUSE")) ctx->no_c0_fuse = true;
     if (const char* e = std::getenv("MGM_UPPER_RES_MIN")) ctx->upper_res_min = std::atoll(e);
     if (const char* e = std::getenv("MGM_MORTON_T_MIN")) ctx->morton_t_min = std::atoll(e);
-    if (std::getenv("MGM_PF_LATE")) ctx->pf_late = 1;
-    if (std::getenv("MGM_PF_NOF")) ctx->pf_nof = 1;
-    if (std::getenv("MGM_PF_L0ONLY")) ctx->pf_l0only = 1;
-    if (const char* e = std::getenv("MGM_PF_BOT_MB")) ctx->pf_bot_budget = (i64)std::max(0, std::atoi(e)) << 20;
     cudaGetDevice(&ctx->device);
     (void)cuda_stream;
     if (cudaStreamCreateWithFlags(&ctx->st, cudaStreamNonBlocking) != cudaSuccess) {
@@ -2585,7 +3036,7 @@ static int batch_width(int K) { return K <= 2 ? 2 : K <= 4 ? 4 : 8; }
 static mgm_status batch_check(mgm_ctx* ctx, int K) {
     mgm_status s = check_ctx(ctx);
     if (s) return s;
-    if (K < 1 || K > 8 || ctx->poisson || !ctx->ainv || ctx->comm) {
+    if (K < 1 || K > 8 || ctx->poisson || !ctx->ainv || dist_on(ctx)) {
         ctx->err = "batched solves: 1 <= K <= 8, shifted problem, coarsest level <= 4096 rows, one GPU";
         return MGM_ERR_ARG;
     }
@@ -2692,11 +3143,7 @@ mgm_status mgm_nccl_unique_id(void* id128) {
 mgm_status mgm_dist_attach(mgm_ctx* ctx, int rank, int nranks, const void* id128) {
     AllocScope as_(ctx);
     if (!ctx || ctx->lv.empty() || nranks < 1 || rank < 0 || rank >= nranks || !id128) return MGM_ERR_ARG;
-    if (ctx->poisson && nranks > 1) {
-        ctx->err = "multi-GPU solve supports the shifted problem only";
-        return MGM_ERR_ARG;
-    }
-    if (ctx->comm) return MGM_ERR_ARG;
+    if (ctx->tp) return MGM_ERR_ARG;
     if (!nccl().ok) {
         ctx->err = "libnccl.so.2 not found";
         return MGM_ERR_NCCL;
@@ -2710,14 +3157,64 @@ mgm_status mgm_dist_attach(mgm_ctx* ctx, int rank, int nranks, const void* id128
         ctx->err = std::string("ncclCommInitRank: ") + nccl().GetErrorString(r);
         return MGM_ERR_NCCL;
     }
-    ctx->comm = comm;
+    auto* t = new NcclTransport();
+    t->comm = comm;
+    t->rank = rank;
+    t->nranks = nranks;
+    ctx->tp = t;
     ctx->rank = rank;
     ctx->nranks = nranks;
-    for (cudaGraphExec_t* gx : {&ctx->vgraph, &ctx->vgraph0, &ctx->ggraph})  // re-capture with the exchanges
-        if (*gx) {
-            cudaGraphExecDestroy(*gx);
-            *gx = nullptr;
-        }
+    return dist_partition(ctx);
+}
+
+mgm_status mgm_fake_group_create(int nranks, void** group) {
+    if (nranks < 1 || !group) return MGM_ERR_ARG;
+    *group = new FakeGroup(nranks);
+    return MGM_OK;
+}
+
+mgm_status mgm_fake_group_destroy(void* group) {
+    delete static_cast<FakeGroup*>(group);
+    return MGM_OK;
+}
+
+mgm_status mgm_dist_attach_fake(mgm_ctx* ctx, int rank, void* group) {
+    AllocScope as_(ctx);
+    auto* g = static_cast<FakeGroup*>(group);
+    if (!ctx || ctx->lv.empty() || !g || rank < 0 || rank >= g->R || ctx->tp) return MGM_ERR_ARG;
+    cudaSetDevice(ctx->device);
+    auto* t = new FakeTransport();
+    t->g = g;
+    t->rank = rank;
+    t->nranks = g->R;
+    ctx->tp = t;
+    ctx->rank = rank;
+    ctx->nranks = g->R;
+    return dist_partition(ctx);
+}
+
+mgm_status mgm_local_rows(const mgm_ctx* ctx, int64_t* n_local, int64_t* original_ids) {
+    if (!ctx || ctx->lv.empty()) return MGM_ERR_ARG;
+    const i64 n = ctx->tp ? (i64)ctx->local_ids.size() : ctx->N;
+    if (n_local) *n_local = n;
+    if (original_ids)
+        for (i64 k = 0; k < n; ++k) original_ids[k] = ctx->tp ? ctx->local_ids[(size_t)k] : k;
+    return MGM_OK;
+}
+
+mgm_status mgm_dist_info(const mgm_ctx* ctx, int* dist_levels, int64_t* ghosts, int64_t* halo_values_per_vcycle) {
+    if (!ctx || ctx->lv.empty()) return MGM_ERR_ARG;
+    if (dist_levels) *dist_levels = ctx->tp ? ctx->D : 0;
+    i64 g = 0, hv = 0;
+    for (int j = 0; j < (ctx->tp ? ctx->D : 0); ++j) {
+        const Level& L = ctx->lv[j];
+        g += L.nghost;
+        // received values per V-cycle: every colour of nu1 + nu2 sweeps once, plus the full
+        // halos after interpolation and before the restriction
+        hv += (i64)(ctx->lp.nu1 + ctx->lp.nu2) * L.nghost + 2 * L.nghost;
+    }
+    if (ghosts) *ghosts = g;
+    if (halo_values_per_vcycle) *halo_values_per_vcycle = hv;
     return MGM_OK;
 }
 
@@ -2726,12 +3223,7 @@ mgm_status mgm_destroy(mgm_ctx* ctx) {
     if (!ctx) return MGM_OK;
     cudaSetDevice(ctx->device);
     if (ctx->st) cudaStreamSynchronize(ctx->st);
-    for (auto& L : ctx->lv) {
-        for (void* ptr : {(void*)L.sptr, (void*)L.scol, (void*)L.sval, (void*)L.pcol, (void*)L.pval, (void*)L.rptr,
-                          (void*)L.rcol, (void*)L.rval, (void*)L.u, (void*)L.f, (void*)L.t, (void*)L.c, (void*)L.slw,
-                          (void*)L.nlow, (void*)L.sluw, (void*)L.l2m, (void*)L.rcol_m})
-            if (ptr) dev_free(ptr);
-    }
+    for (auto& L : ctx->lv) free_level_device(L);
     for (void* ptr : {(void*)ctx->lu, (void*)ctx->piv, (void*)ctx->d_lib2orig, (void*)ctx->V, (void*)ctx->w,
                       (void*)ctx->xs, (void*)ctx->b, (void*)ctx->partials, (void*)ctx->dh, (void*)ctx->tickets})
         if (ptr) dev_free(ptr);
@@ -2742,12 +3234,11 @@ mgm_status mgm_destroy(mgm_ctx* ctx) {
     if (ctx->g_h) cudaFreeHost(ctx->g_h);
     if (ctx->g_hi) cudaFreeHost(ctx->g_hi);
     for (void* q : ctx->bot_mem) dev_free(q);
-    if (ctx->d_pf) dev_free(ctx->d_pf);
-    for (void* q : ctx->pf_old) dev_free(q);
     if (ctx->d_trace) dev_free(ctx->d_trace);
     if (ctx->vgraph) cudaGraphExecDestroy(ctx->vgraph);
     if (ctx->vgraph0) cudaGraphExecDestroy(ctx->vgraph0);
-    if (ctx->comm) nccl().CommDestroy(ctx->comm);
+    delete ctx->tp;
+    ctx->tp = nullptr;
     for (auto* q : {&ctx->bu, &ctx->bf, &ctx->bt})
         for (double* ptr : *q) dev_free(ptr);
     for (auto& gx : ctx->bgraph)
@@ -2778,7 +3269,7 @@ mgm_status mgm_vcycle(mgm_ctx* ctx, const double* f_dev, double* u_dev, void* cu
     if (!f_dev || !u_dev) return MGM_ERR_ARG;
     if ((s = ensure_krylov(ctx))) return s;
     cudaStream_t st = (cudaStream_t)cuda_stream;
-    const i64 N = ctx->N;
+    const i64 N = ctx->lv[0].n;  // (multi-GPU: this rank's rows, mgm_local_rows order)
     Level& L0 = ctx->lv[0];
     k_gather<<<blocks_for(N, 256), 256, 0, st>>>((int)N, ctx->d_lib2orig, f_dev, L0.f);
     k_gather<<<blocks_for(N, 256), 256, 0, st>>>((int)N, ctx->d_lib2orig, u_dev, L0.u);
@@ -2786,6 +3277,7 @@ mgm_status mgm_vcycle(mgm_ctx* ctx, const double* f_dev, double* u_dev, void* cu
         CK(cudaMemsetAsync(L0.f + N, 0, sizeof(double), st));
         CK(cudaMemsetAsync(L0.u + N, 0, sizeof(double), st));
     }
+    exch(ctx, 0, L0.u, -1, st);  // (distributed: the presmooth reads the guess's ghosts)
     if ((s = run_vcycle(ctx, st))) return s;
     k_scatter<<<blocks_for(N, 256), 256, 0, st>>>((int)N, ctx->d_lib2orig, L0.u, u_dev);
     CK(cudaGetLastError());
@@ -2803,7 +3295,7 @@ static mgm_status solve_impl(mgm_ctx* ctx, const double* rhs, const double* x0, 
     if (s) return s;
     if (!rhs || !x || !(tol >= 0) || maxit < 0 || krylov < 0 || krylov > 2) return MGM_ERR_ARG;
     if ((s = ensure_krylov(ctx))) return s;
-    const i64 N = ctx->N;
+    const i64 N = ctx->lv[0].n;  // (multi-GPU: this rank's rows, mgm_local_rows order)
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
@@ -2915,6 +3407,10 @@ mgm_status mgm_apply(mgm_ctx* ctx, int level, int op, const double* x, const dou
     mgm_status s = check_ctx(ctx);
     if (s) return s;
     if (level < 0 || level >= ctx->p || !x || !y) return MGM_ERR_ARG;
+    if (dist_on(ctx)) {
+        ctx->err = "mgm_apply: test hook of the undistributed hierarchy";
+        return MGM_ERR_ARG;
+    }
     cudaStream_t st = (cudaStream_t)cuda_stream;
     Level& L = ctx->lv[level];
     const i64 pad = ctx->poisson ? 1 : 0;
@@ -2937,7 +3433,7 @@ mgm_status mgm_apply(mgm_ctx* ctx, int level, int op, const double* x, const dou
             break;
         case MGM_OP_RESTRICT:
             if (level == ctx->p - 1) return MGM_ERR_ARG;
-            enqueue_restrict(ctx, level, x, y, st);
+            enqueue_restrict(ctx, level, const_cast<double*>(x), y, st);  // (undistributed: x is only read)
             break;
         case MGM_OP_INTERP: {
             if (level == ctx->p - 1) return MGM_ERR_ARG;
@@ -3131,6 +3627,53 @@ mgm_status mgm_host_wse(const double* points, int64_t n, int64_t nt, int64_t* ke
     std::vector<i64> k;
     wse_eliminate(points, n, nt, nn2, k, nth);
     std::copy(k.begin(), k.end(), keep);
+    return MGM_OK;
+}
+
+mgm_status mgm_host_partition_level(int64_t n, const int64_t* L_ptr, const int32_t* L_col, const int32_t* colour,
+                                    int ncol, const int32_t* owner, int64_t nc, const int64_t* P_ptr,
+                                    const int32_t* P_col, const int32_t* owner_c, int64_t nf, const int64_t* Pf_ptr,
+                                    const int32_t* Pf_col, const int32_t* owner_f, int nranks, int rank,
+                                    int64_t* n_rows, int64_t* rows, int64_t* n_ghosts, int64_t* ghosts, int* n_peers,
+                                    int32_t* peers, int64_t* send_rows, int64_t* send_off, int64_t* recv_off,
+                                    int64_t* send_coff, int64_t* recv_coff) {
+    if (n < 1 || !L_ptr || !L_col || !colour || !owner || ncol < 1 || nranks < 1 || rank < 0 || rank >= nranks)
+        return MGM_ERR_ARG;
+    auto csr = [](int64_t nr, int64_t ncl, const int64_t* ptr, const int32_t* col) {
+        HostCSR A;
+        A.nrows = nr;
+        A.ncols = ncl;
+        A.ptr.assign(ptr, ptr + nr + 1);
+        A.col.assign(col, col + ptr[nr]);
+        return A;
+    };
+    const HostCSR L = csr(n, n, L_ptr, L_col);
+    HostCSR Pj, Pf;
+    std::vector<int> ow(owner, owner + n), owc, owf;
+    if (P_ptr && P_col && owner_c) {
+        Pj = csr(n, nc, P_ptr, P_col);
+        owc.assign(owner_c, owner_c + nc);
+    }
+    if (Pf_ptr && Pf_col && owner_f) {
+        Pf = csr(nf, n, Pf_ptr, Pf_col);
+        owf.assign(owner_f, owner_f + nf);
+    }
+    std::vector<i32> colv(colour, colour + n);
+    std::vector<PartTables> all;
+    partition_level(L, ow, colv, ncol, owc.empty() ? nullptr : &Pj, owc.empty() ? nullptr : &owc,
+                    owf.empty() ? nullptr : &Pf, owf.empty() ? nullptr : &owf, nranks, all);
+    const PartTables& T = all[(size_t)rank];
+    if (n_rows) *n_rows = (int64_t)T.rows.size();
+    if (rows) std::copy(T.rows.begin(), T.rows.end(), rows);
+    if (n_ghosts) *n_ghosts = (int64_t)T.ghosts.size();
+    if (ghosts) std::copy(T.ghosts.begin(), T.ghosts.end(), ghosts);
+    if (n_peers) *n_peers = (int)T.peers.size();
+    if (peers) std::copy(T.peers.begin(), T.peers.end(), peers);
+    if (send_rows) std::copy(T.send_rows.begin(), T.send_rows.end(), send_rows);
+    if (send_off) std::copy(T.send_off.begin(), T.send_off.end(), send_off);
+    if (recv_off) std::copy(T.recv_off.begin(), T.recv_off.end(), recv_off);
+    if (send_coff) std::copy(T.send_coff.begin(), T.send_coff.end(), send_coff);
+    if (recv_coff) std::copy(T.recv_coff.begin(), T.recv_coff.end(), recv_coff);
     return MGM_OK;
 }
 

@@ -55,6 +55,34 @@ HostCSR transpose(const HostCSR& A);
 i64 dense_lu_colmajor(std::vector<double>& A_rowmajor, int m, std::vector<double>& LU_colmajor,
                       std::vector<i32>& piv);
 
+// ---------------- distributed solve: partition of one level (host_setup.cpp) ------------
+// SURVEY 8(e) / DESIGN.md "Multi-GPU": rank q owns the rows with owner[r] == q (a Morton
+// block); its vectors hold [owned rows | (Poisson multiplier) | ghost rows].  A ghost is a
+// row another rank owns whose value one of q's operator applications reads:
+//   * columns of L_j in q's rows (Gauss-Seidel, residual, SpMV),
+//   * fine columns (level j) of R_j = P_j^T in the coarse rows q owns at level j+1,
+//   * coarse columns (level j) of P_{j-1} in the fine rows q owns at level j-1.
+// Ghosts are sorted by (owner, row); rows are in lib order (colour-major), so the ghosts a peer
+// sends for one colour are a contiguous slice of the segment from that peer -- a per-colour
+// halo is one send / one receive per peer, received straight into the ghost slots.
+struct PartTables {
+    std::vector<i64> rows;              // owned rows (ascending)
+    std::vector<i64> ghosts;            // ghost rows, sorted by (owner, row)
+    std::vector<int> peers;             // ranks q exchanges with (ascending)
+    std::vector<i64> send_rows;         // per peer (concatenated): owned rows that peer needs, ascending
+    std::vector<i64> send_off, recv_off;  // per peer: offsets into send_rows / ghost slots (npeers + 1)
+    std::vector<i64> send_coff, recv_coff;  // [npeers][ncol + 1]: absolute offsets of each colour's slice
+};
+// need[p] = rows of this level that rank p reads (owned or not), from the three operators
+// above; the helper collects them for every rank at once (O(nnz)).
+// L: this level's operator (lib order, n rows); owner[n]; colour[n] (ncol colours);
+// Rt: P_j (fine rows n -> coarse cols), owner_c[nc] of level j+1 rows (or NULL on the coarsest
+// distributed level's absent transfer); Pf: P_{j-1} (fine rows nf of level j-1 -> cols of this
+// level), owner_f[nf] (or NULL on level 0).
+void partition_level(const HostCSR& L, const std::vector<int>& owner, const std::vector<i32>& colour, int ncol,
+                     const HostCSR* Pj, const std::vector<int>* owner_c, const HostCSR* Pf,
+                     const std::vector<int>* owner_f, int nranks, std::vector<PartTables>& out);
+
 // ---------------- device setup kernels (setup_kernels.cu; -fmad=false) -----------------
 // All pointers device.  Return cudaError_t as int; *fail_dev = failing row or INT64_MAX.
 int launch_rbffd_weights(const double* pts, const double* nrm, const i32* sten, i64 n, int ns,

@@ -652,6 +652,11 @@ __global__ void k_axpbypz(int64_t n, double* x, double a, const double* __restri
 __global__ void k_vadd(int k1, double* __restrict__ h, const double* __restrict__ h2) {
     for (int j = threadIdx.x; j < k1; j += blockDim.x) h[j] += h2[j];
 }
+// y[n] = fs*f[n] + sign*s[0]  (border row of the Poisson system from an all-reduced dot s)
+__global__ void k_border_set(const double* __restrict__ s, double fs, const double* __restrict__ f, int n,
+                             double sign, double* __restrict__ y) {
+    if (threadIdx.x == 0) y[n] = (f ? fs * f[n] : 0.0) + sign * s[0];
+}
 // y[n] = f[n]*fs - sum   (border row of the Poisson system), single block finish
 __global__ void k_border_finish(const double* __restrict__ partials, int nblk, double fs,
                                 const double* __restrict__ f, int n, double sign,

@@ -75,6 +75,11 @@ _SIGS = {
     "mgm_solve_batch": ([_vp, ctypes.c_int, _vp, _vp, ctypes.c_double, ctypes.c_int,
                          ctypes.POINTER(Report), _vp], ctypes.c_int),
     "mgm_dist_attach": ([_vp, ctypes.c_int, ctypes.c_int, _vp], ctypes.c_int),
+    "mgm_local_rows": ([_vp, _i64p, _i64p], ctypes.c_int),
+    "mgm_dist_info": ([_vp, ctypes.POINTER(ctypes.c_int), _i64p, _i64p], ctypes.c_int),
+    "mgm_fake_group_create": ([ctypes.c_int, ctypes.POINTER(_vp)], ctypes.c_int),
+    "mgm_fake_group_destroy": ([_vp], ctypes.c_int),
+    "mgm_dist_attach_fake": ([_vp, ctypes.c_int, _vp], ctypes.c_int),
     "mgm_last_error": ([_vp, _i64p], ctypes.c_char_p),
     "mgm_num_levels": ([_vp, ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
     "mgm_level_info": ([_vp, ctypes.c_int, _i64p, _i64p, _i64p, ctypes.POINTER(ctypes.c_int),
@@ -98,6 +103,10 @@ _SIGS = {
     "mgm_host_knn": ([_f64p, _i64, _f64p, _i64, ctypes.c_int, _i32p], ctypes.c_int),
     "mgm_host_wse": ([_f64p, _i64, _i64, _i64p], ctypes.c_int),
     "mgm_host_colouring": ([_i64, _i64p, _i32p, _i32p, ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
+    "mgm_host_partition_level": ([_i64, _i64p, _i32p, _i32p, ctypes.c_int, _i32p, _i64, _i64p, _i32p, _i32p,
+                                  _i64, _i64p, _i32p, _i32p, ctypes.c_int, ctypes.c_int,
+                                  _i64p, _i64p, _i64p, _i64p, ctypes.POINTER(ctypes.c_int), _i32p, _i64p,
+                                  _i64p, _i64p, _i64p, _i64p], ctypes.c_int),
 }
 EXPORTED = tuple(_SIGS)
 
@@ -362,6 +371,35 @@ def mgm_dist_attach(ctx, rank: int, nranks: int, nccl_id: bytes):
     _check(load_library().mgm_dist_attach(ctx, rank, nranks, buf), ctx)
 
 
+def mgm_local_rows(ctx) -> np.ndarray:
+    """Original point ids of the rows this rank owns, in the order of its local vectors."""
+    n = _i64()
+    _check(load_library().mgm_local_rows(ctx, ctypes.byref(n), None), ctx)
+    ids = np.empty(n.value, dtype=np.int64)
+    _check(load_library().mgm_local_rows(ctx, ctypes.byref(n), _ptr(ids, _i64p)), ctx)
+    return ids
+
+
+def mgm_dist_info(ctx) -> dict:
+    d, g, h = ctypes.c_int(), _i64(), _i64()
+    _check(load_library().mgm_dist_info(ctx, ctypes.byref(d), ctypes.byref(g), ctypes.byref(h)), ctx)
+    return dict(dist_levels=d.value, ghosts=g.value, halo_values_per_vcycle=h.value)
+
+
+def mgm_fake_group_create(nranks: int):
+    g = _vp()
+    _check(load_library().mgm_fake_group_create(nranks, ctypes.byref(g)))
+    return g
+
+
+def mgm_fake_group_destroy(group):
+    load_library().mgm_fake_group_destroy(group)
+
+
+def mgm_dist_attach_fake(ctx, rank: int, group):
+    _check(load_library().mgm_dist_attach_fake(ctx, rank, group), ctx)
+
+
 def mgm_trace_read(ctx):
     """Stage stamps of the last V-cycle (MGM_TRACE set at setup): list of (label, ns)."""
     buf = (ctypes.c_uint64 * 256)()
@@ -425,6 +463,50 @@ def mgm_host_colouring(ptr, col):
     return c, nc.value
 
 
+def mgm_host_partition_level(L_ptr, L_col, colour, ncol, owner, nranks, rank, P=None, owner_c=None,
+                             Pf=None, owner_f=None):
+    """Partition tables of one level (the host code of mgm_dist_attach).  L_ptr/L_col: pattern
+    of L_j in lib order; P = (ptr, col, nc) of P_j with owner_c; Pf = (ptr, col, nf) of P_{j-1}
+    with owner_f.  Returns a dict of numpy arrays (see include/mgm.h)."""
+    i64a = lambda a: np.ascontiguousarray(a, dtype=np.int64)
+    i32a = lambda a: np.ascontiguousarray(a, dtype=np.int32)
+    n = len(L_ptr) - 1
+    Lp, Lc, col, ow = i64a(L_ptr), i32a(L_col), i32a(colour), i32a(owner)
+    args = [n, _ptr(Lp, _i64p), _ptr(Lc, _i32p), _ptr(col, _i32p), int(ncol), _ptr(ow, _i32p)]
+    keep = [Lp, Lc, col, ow]
+    if P is not None:
+        pp, pc, nc = i64a(P[0]), i32a(P[1]), int(P[2])
+        oc = i32a(owner_c)
+        keep += [pp, pc, oc]
+        args += [nc, _ptr(pp, _i64p), _ptr(pc, _i32p), _ptr(oc, _i32p)]
+    else:
+        args += [0, None, None, None]
+    if Pf is not None:
+        fp, fc, nf = i64a(Pf[0]), i32a(Pf[1]), int(Pf[2])
+        of = i32a(owner_f)
+        keep += [fp, fc, of]
+        args += [nf, _ptr(fp, _i64p), _ptr(fc, _i32p), _ptr(of, _i32p)]
+    else:
+        args += [0, None, None, None]
+    nr, ng, npr = _i64(), _i64(), ctypes.c_int()
+    rows = np.empty(n, dtype=np.int64)
+    ghosts = np.empty(n, dtype=np.int64)
+    peers = np.empty(nranks, dtype=np.int32)
+    send_rows = np.empty(n, dtype=np.int64)
+    soff = np.zeros(nranks + 1, dtype=np.int64)
+    roff = np.zeros(nranks + 1, dtype=np.int64)
+    scoff = np.zeros(nranks * (ncol + 1), dtype=np.int64)
+    rcoff = np.zeros(nranks * (ncol + 1), dtype=np.int64)
+    _check(load_library().mgm_host_partition_level(
+        *args, nranks, rank, ctypes.byref(nr), _ptr(rows, _i64p), ctypes.byref(ng), _ptr(ghosts, _i64p),
+        ctypes.byref(npr), _ptr(peers, _i32p), _ptr(send_rows, _i64p), _ptr(soff, _i64p), _ptr(roff, _i64p),
+        _ptr(scoff, _i64p), _ptr(rcoff, _i64p)))
+    k = npr.value
+    return dict(rows=rows[:nr.value], ghosts=ghosts[:ng.value], peers=peers[:k], send_rows=send_rows[:soff[k]],
+                send_off=soff[:k + 1], recv_off=roff[:k + 1], send_coff=scoff[:k * (ncol + 1)].reshape(k, ncol + 1),
+                recv_coff=rcoff[:k * (ncol + 1)].reshape(k, ncol + 1))
+
+
 # ---------------------------------------------------------------- convenience wrapper
 class MGM:
     """Owns one libmgm context.  Vectors are torch CUDA float64 tensors in original order."""
@@ -477,3 +559,9 @@ class MGM:
         dist.broadcast_object_list(obj, src=0, group=group)
         mgm_dist_attach(self.ctx, rank, nranks, obj[0])
         self.rank, self.nranks = rank, nranks
+        self.local_ids = mgm_local_rows(self.ctx)
+
+    def attach_fake(self, rank: int, group):
+        """Test hook: join an in-process group of fake ranks on one GPU (mgm_dist_attach_fake)."""
+        mgm_dist_attach_fake(self.ctx, rank, group)
+        self.local_ids = mgm_local_rows(self.ctx)

@@ -457,35 +457,130 @@ def test_dense_bottom(name, dense_max, monkeypatch):
 
 
 # ------------------------------------------------------------------ multi-GPU path (8(e))
-@pytest.mark.parametrize("name", ["torus20000", "gfd9000"])
-def test_dist_fake_ranks_bitwise(name, monkeypatch):
-    """MGM_DIST_FAKE_RANKS=R splits every level-0..2 operator application into R row pieces
-    (the multi-GPU decomposition) computed on one GPU: the V-cycle and the GMRES solve must be
-    bitwise identical to the unsplit path (each output row is computed by the same arithmetic)."""
+def _fake_ranks(w, R, fn, levels=None):
+    """R fake ranks on this GPU (mgm_fake_group_create / mgm_dist_attach_fake): R contexts,
+    each partitioned to its Morton block, each driven by its own host thread and CUDA stream
+    through the SAME collective entry points as with NCCL.  fn(rank, mgm) -> result."""
+    import threading
+
     import torch
-    from paper_2204_06154_b200 import MGM
+    from paper_2204_06154_b200 import MGM, mgm_fake_group_create, mgm_fake_group_destroy
+
+    ms = [MGM(w.points, w.normals, w.stencil, levels or w.levels) for _ in range(R)]
+    g = mgm_fake_group_create(R)
+    for q, m in enumerate(ms):
+        m.attach_fake(q, g)
+    out, errs = [None] * R, []
+
+    def run(q):
+        try:
+            torch.cuda.set_device(0)
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                out[q] = fn(q, ms[q])
+                s.synchronize()
+        except Exception as e:  # noqa: BLE001
+            errs.append(e)
+
+    th = [threading.Thread(target=run, args=(q,)) for q in range(R)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    alive = any(t.is_alive() for t in th)
+    if not alive:
+        for m in ms:
+            m.close()
+        mgm_fake_group_destroy(g)
+    assert not alive, "fake-rank threads hung"
+    if errs:
+        raise errs[0]
+    return out, [m.local_ids for m in ms] if not alive else None
+
+
+DIST_KNOBS = [{}, {"MGM_DIST_MIN_ROWS": "1"},
+              {"MGM_DIST_MIN_ROWS": "1", "MGM_DENSE_MAX": "0", "MGM_BOT_MAX": "0"}]
+
+
+@pytest.mark.parametrize("R", [2, 3])
+@pytest.mark.parametrize("knobs", range(len(DIST_KNOBS)))
+def test_dist_fake_ranks_vcycle_bitwise(R, knobs, monkeypatch):
+    """The partitioned V-cycle (Morton row blocks on every distributed level, ghost halos per
+    colour / per transfer, all-gather into the replicated bottom) is bitwise the single-GPU
+    V-cycle: every owned row is computed by the same arithmetic.  Variants: the default level
+    split, every level above the bottom distributed, and no dense / cluster bottom (every level
+    but the coarsest distributed); every rank's ghost tables are exercised."""
+    import torch
+    from paper_2204_06154_b200 import MGM, mgm_dist_info
+
+    P = pair("torus20000")
+    for k, v in DIST_KNOBS[knobs].items():
+        monkeypatch.setenv(k, v)
+    ref = MGM(P.w.points, P.w.normals, P.w.stencil, P.w.levels)
+    n = len(P.w.points)
+    f, u0 = _rand(n, 7), _rand(n, 8)
+    u1 = torch.from_numpy(u0.copy()).cuda()
+    ref.vcycle(torch.from_numpy(f).cuda(), u1)
+    u1 = u1.cpu().numpy()
+
+    def fn(q, m):
+        ids = m.local_ids
+        uq = torch.from_numpy(u0[ids].copy()).cuda()
+        m.vcycle(torch.from_numpy(f[ids].copy()).cuda(), uq)
+        m.vcycle(torch.from_numpy(f[ids].copy()).cuda(), uq)       # twice: stale-ghost check
+        return uq.cpu().numpy(), mgm_dist_info(m.ctx)
+
+    out, ids = _fake_ranks(P.w, R, fn)
+    ids_all = np.concatenate(ids)
+    assert np.array_equal(np.sort(ids_all), np.arange(n))          # the ranks' rows tile the cloud
+    u2 = np.empty(n)
+    for (uq, info), iq in zip(out, ids):
+        u2[iq] = uq
+        assert info["dist_levels"] >= 1 and info["ghosts"] > 0
+    ref.vcycle(torch.from_numpy(f).cuda(), u1g := torch.from_numpy(u1.copy()).cuda())
+    assert np.array_equal(u2, u1g.cpu().numpy())
+    ref.close()
+
+
+@pytest.mark.parametrize("name", ["torus20000", "poisson6000"])
+@pytest.mark.parametrize("krylov", [1, 0, 2])
+def test_dist_fake_ranks_solve(name, krylov, monkeypatch):
+    """Distributed MGM-GMRES / standalone / BiCGSTAB on 3 fake ranks against the oracle: the
+    Krylov inner products are rank-local sums + an all-reduce (another summation order), so
+    iterations within +-1 (+-2 BiCGSTAB) and solutions to 1e-9; Poisson: the border dots and
+    the multiplier too; also a warm start (x0)."""
+    import torch
 
     P = pair(name)
-    monkeypatch.setenv("MGM_DIST_FAKE_RANKS", "3")
-    monkeypatch.setenv("MGM_DIST_LEVELS", "3")
-    m2 = MGM(P.w.points, P.w.normals, P.w.stencil, P.w.levels)
-    n = len(P.w.points)
-    f = torch.from_numpy(_rand(n, 7)).cuda()
-    u1 = torch.from_numpy(_rand(n, 8)).cuda()
-    u2 = u1.clone()
-    P.gpu.vcycle(f, u1)
-    m2.vcycle(f, u2)
-    assert torch.equal(u1, u2)
-    rhs = torch.from_numpy(P.w.rhs).cuda()
-    x1, r1 = P.gpu.solve(rhs, tol=1e-10)
-    x2, r2 = m2.solve(rhs, tol=1e-10)
-    assert r1.iterations == r2.iterations and torch.equal(x1, x2)
-    m2.close()
+    if krylov == 0 and name == "poisson6000":
+        pytest.skip("standalone MGM converges slowly on this cloud (P:411)")
+    monkeypatch.setenv("MGM_DIST_MIN_ROWS", "1")
+    rhs = P.w.rhs
+    xr, rr = P.ref.solve(rhs, tol=1e-10, krylov=krylov, maxit=300)
+
+    def fn(q, m):
+        ids = m.local_ids
+        x, rep = m.solve(torch.from_numpy(rhs[ids].copy()).cuda(), tol=1e-10, krylov=krylov, maxit=300)
+        return x.cpu().numpy(), rep
+
+    out, ids = _fake_ranks(P.w, 3, fn)
+    x = np.empty(len(rhs))
+    for (xq, rep), iq in zip(out, ids):
+        x[iq] = xq
+        assert rep.converged and rep.final_rel_residual <= 1e-10
+        assert abs(rep.iterations - rr.iterations) <= (2 if krylov == 2 else 1), (rep.iterations, rr.iterations)
+        if P.poisson:
+            assert abs(rep.lam - rr.lam) <= 1e-8 * max(1.0, abs(rr.lam))
+    reps = [r for _, r in out]
+    assert len({r.iterations for r in reps}) == 1 and len({r.final_rel_residual for r in reps}) == 1
+    assert np.linalg.norm(x - xr) / np.linalg.norm(xr) <= 1e-9
 
 
 def test_dist_nccl_single_rank():
-    """The NCCL path (mgm_dist_attach, grouped in-place broadcasts captured in the V-cycle
-    graph, allreduce of the Krylov inner products) with one rank: same solve as without."""
+    """The NCCL transport (mgm_dist_attach over a torch.distributed process group, halos and
+    all-gathers captured in the V-cycle's CUDA graph, allreduce of the Krylov inner products)
+    with one rank: the V-cycle is bitwise the undistributed one, the solve the same to
+    rounding."""
     import os
     import socket
 
@@ -503,18 +598,21 @@ def test_dist_nccl_single_rank():
     try:
         m2 = MGM(P.w.points, P.w.normals, P.w.stencil, P.w.levels)
         m2.attach_dist()
+        assert np.array_equal(np.sort(m2.local_ids), np.arange(len(P.w.points)))
+        ids = m2.local_ids
         n = len(P.w.points)
-        f = torch.from_numpy(_rand(n, 9)).cuda()
-        u1 = torch.from_numpy(_rand(n, 10)).cuda()
-        u2 = u1.clone()
-        P.gpu.vcycle(f, u1)
-        m2.vcycle(f, u2)
-        assert torch.equal(u1, u2)
+        f, u0 = _rand(n, 9), _rand(n, 10)
+        u1 = torch.from_numpy(u0.copy()).cuda()
+        P.gpu.vcycle(torch.from_numpy(f).cuda(), u1)
+        u2 = torch.from_numpy(u0[ids].copy()).cuda()
+        m2.vcycle(torch.from_numpy(f[ids].copy()).cuda(), u2)
+        assert np.array_equal(u2.cpu().numpy(), u1.cpu().numpy()[ids])
         rhs = torch.from_numpy(P.w.rhs).cuda()
         x1, r1 = P.gpu.solve(rhs, tol=1e-10)
-        x2, r2 = m2.solve(rhs, tol=1e-10)
+        x2, r2 = m2.solve(torch.from_numpy(P.w.rhs[ids].copy()).cuda(), tol=1e-10)
         assert abs(r1.iterations - r2.iterations) <= 1
-        assert (x1 - x2).norm().item() <= 1e-12 * x1.norm().item()
+        x1 = x1.cpu().numpy()[ids]
+        assert np.linalg.norm(x1 - x2.cpu().numpy()) <= 1e-12 * np.linalg.norm(x1)
         m2.close()
     finally:
         dist.destroy_process_group()
