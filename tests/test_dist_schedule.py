@@ -104,6 +104,17 @@ def _exchange(v, T, colour=None):
         v[order[T["ghosts"][g0:g1]]] = buf.numpy()
 
 
+def _sweep_rows(OR, A, rows, f, u):
+    """the oracle's O12 row update (orc_gs_sweep) on the given rows only, in their order"""
+    import ctypes
+
+    fail = ctypes.c_int64(-1)
+    rc = OR.lib().orc_gs_sweep(ctypes.c_int64(len(rows)), OR._p(A.ptr, OR.i64p), OR._p(A.idx, OR.i64p),
+                               OR._p(A.val, OR.f64p), OR._p(rows, OR.i64p), ctypes.c_int(0), OR._p(f, OR.f64p),
+                               OR._p(u, OR.f64p), None, ctypes.c_double(0.0), ctypes.byref(fail))
+    assert rc == 0
+
+
 def dist_vcycle(O, f, u, rank, nranks, D):
     """Alg. 3 with levels 0..D-1 partitioned (owned rows + ghosts, NaN elsewhere), levels >= D
     replicated (the oracle's routines on full vectors)."""
@@ -128,7 +139,7 @@ def dist_vcycle(O, f, u, rank, nranks, D):
         for c in range(lv.ncolours):
             rows = np.sort(mine[j][lv.colour[mine[j]] == c])
             if len(rows):
-                OR.gs_sweep(lv.L, np.ascontiguousarray(rows, dtype=np.int64), fj, uj)
+                _sweep_rows(OR, lv.L, np.ascontiguousarray(rows, dtype=np.int64), fj, uj)
             _exchange(uj, T[j], c)
 
     def own(vals, j):  # keep only this rank's rows of a full-length result
@@ -192,6 +203,7 @@ def dist_vcycle(O, f, u, rank, nranks, D):
 def _worker(rank, port, result_q, D):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    import traceback
     try:
         import oracle as O
 
@@ -207,6 +219,9 @@ def _worker(rank, port, result_q, D):
         counts = torch.tensor([len(rows)])
         dist.all_reduce(counts)
         result_q.put((rank, bool(ok), int(counts.item()), n, float(np.nanmax(np.abs(um - ref[rows])))))
+    except Exception:
+        result_q.put((rank, False, -1, -1, traceback.format_exc()))
+        raise
     finally:
         dist.destroy_process_group()
 
