@@ -288,9 +288,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--oracle-worker", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--no-stages", action="store_true", help="skip the traced per-stage V-cycle breakdown")
-    ap.add_argument("--parallel", choices=["replicas", "dist"], default="replicas",
-                    help="N>1: independent replicas of the solve (weak scaling) or one solve "
-                         "split across the ranks (mgm_dist_attach, strong scaling)")
+    ap.add_argument("--parallel", choices=["replicas", "dist"], default="dist",
+                    help="N>1: one solve partitioned across the ranks (mgm_dist_attach: Morton row "
+                         "blocks + ghost halos, strong scaling; the default) or independent replicas")
     args = ap.parse_args()
     if args.oracle_worker:
         return oracle_worker(args.steps, args.warmup, args.n)
@@ -318,10 +318,16 @@ def main():
     m = MGM(w.points, w.normals, w.stencil, w.levels)
     setup_s = time.perf_counter() - t0
     dist_mode = ws > 1 and args.parallel == "dist"
-    if dist_mode:
+    dinfo = None
+    ids = np.arange(N)
+    if dist_mode:  # this rank's Morton block: its rows of every vector (mgm_local_rows order)
+        from paper_2204_06154_b200 import mgm_dist_info
         m.attach_dist()
+        ids = m.local_ids
+        dinfo = mgm_dist_info(m.ctx)
+    NL = len(ids)
     st = torch.cuda.current_stream()
-    rhs = torch.from_numpy(w.rhs).cuda()
+    rhs = torch.from_numpy(np.ascontiguousarray(w.rhs[ids])).cuda()
     x = torch.empty_like(rhs)
 
     def barrier():
@@ -358,8 +364,8 @@ def main():
     assert rep.converged and rep.final_rel_residual <= 1e-10, rep
 
     # ---- end to end through the public API with pinned host buffers
-    rhs_h = torch.from_numpy(w.rhs).pin_memory()
-    x_h = torch.empty(N, dtype=torch.float64).pin_memory()
+    rhs_h = torch.from_numpy(np.ascontiguousarray(w.rhs[ids])).pin_memory()
+    x_h = torch.empty(NL, dtype=torch.float64).pin_memory()
     rn, xn = rhs_h.numpy(), x_h.numpy()
     mgm_solve_host(m.ctx, rn, xn, tol=1e-10)
     barrier()
@@ -419,7 +425,7 @@ def main():
 
     # ---- V-cycle throughput (graph-replayed V-cycles on device vectors)
     bm = mgm_bytes_model(m.ctx)
-    f = torch.from_numpy(np.random.default_rng(0).uniform(-1, 1, N)).cuda()
+    f = torch.from_numpy(np.ascontiguousarray(np.random.default_rng(0).uniform(-1, 1, N)[ids])).cuda()
     u = torch.zeros_like(f)
     for _ in range(5):
         m.vcycle(f, u)
@@ -476,7 +482,7 @@ def main():
 
     if rank == 0:
         cpu = None
-        if not args.no_cpu_baseline and args.cfg == 3:
+        if not args.no_cpu_baseline and args.cfg == 3 and ws == 1:
             _, cpu = oracle_full(1, 0, args.n)
         line = {
             "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": ws, "steps": args.steps,
@@ -487,12 +493,14 @@ def main():
                        "nnz": [lv["nnz"] for lv in levels],
                        "colours": [lv["colours"] for lv in levels],
                        "gmres_iterations": its[-1], "restart": w.levels.get("restart", 50), "tol": 1e-10,
-                       "parallelism": (f"dist{ws} (level-0 row pieces + NCCL)" if dist_mode else
+                       "parallelism": (f"dist{ws}: Morton row blocks on levels 0..{dinfo['dist_levels'] - 1} "
+                                       f"+ ghost halos (NCCL), replicated bottom" if dist_mode else
                                        f"replicas{ws}" if ws > 1 else "single GPU"),
+                       "dist_rank0": dinfo,
                        "l2": "inputs larger than L2 (hierarchy %.2f GB)" %
                              (sum(lv["stored_bytes"] for lv in levels) / 1e9),
                        "setup_s": round(setup_s, 2)},
-            "vcycle": {"ms": vc_ms, "alg_bytes": bm["vcycle_bytes"], "GBps": vc_gbs,
+            "vcycle": {"ms": vc_ms, "alg_bytes_rank0": bm["vcycle_bytes"], "GBps_rank0": vc_gbs,
                        "frac_of_measured_hbm": vc_gbs / hbm, "vcycles_per_s": 1e3 / vc_ms,
                        "Mrows_per_s": N * 1e-3 / vc_ms, "kernels": vk},
             "roofline": {"bound": "hbm", "kernel": "k_gs_colour (level-0 multicolour GS, one launch per colour)",
@@ -511,7 +519,7 @@ def main():
             "multi_rhs": multi,
             "roofline_bottom": bottom,
             "e2e": {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": 8 * N,
-                    "d2h_bytes_per_step": 8 * N},
+                    "d2h_bytes_per_step": 8 * N, "note": "all ranks together (each copies its own rows)"},
             "gpu_launches": per_step * args.steps,
             "clocks": clocks,
             "cpu_baseline": cpu,
