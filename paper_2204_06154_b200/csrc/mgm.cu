@@ -1656,6 +1656,75 @@ void enqueue_restrict(mgm_ctx* ctx, int j, double* x, double* y, cudaStream_t st
     }
 }
 
+// Fused residual + restriction (solve_kernels.cuh k_res_restrict, north_star item 4): one
+// cooperative launch, grid = every CTA the kernel can keep resident.  Undistributed shifted
+// levels with one thread per residual row and 1/2/4 per restriction row; MGM_NO_FUSE_RR=1
+// keeps the two kernels (comparison).
+static bool g_no_fuse_rr = std::getenv("MGM_NO_FUSE_RR") != nullptr;
+bool fused_rr_ok(const mgm_ctx* ctx, int j) {
+    const Level& L = ctx->lv[j];
+    return !g_no_fuse_rr && !dist_on(ctx) && !ctx->poisson && L.stpr == 1 &&
+           (L.rtpr == 1 || L.rtpr == 2 || L.rtpr == 4) && j + 1 < ctx->p;
+}
+template <int MODE, int TPRR>
+static void launch_rr(mgm_ctx* ctx, const ResRestrict& a, cudaStream_t st) {
+    auto kern = k_res_restrict<MODE, 1, TPRR, CHUNK>;
+    static int grid = 0;
+    if (!grid) {
+        int dev = 0, nsm = 0, per = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, 256, 0) != cudaSuccess || per < 1) per = 1;
+        grid = per * nsm;
+    }
+    if (g_dry) return;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(256);
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = (ctx->pdl && g_use_pdl) ? 2 : 1;
+    note_launch(cudaLaunchKernelEx(&cfg, kern, a), (unsigned)grid, 256, 0);
+}
+void enqueue_res_restrict(mgm_ctx* ctx, int j, const double* f, const double* u, double* t, double* y,
+                          cudaStream_t st, bool after_zg, bool morton_t, bool fuse_c0) {
+    Level& L = ctx->lv[j];
+    Level& Ln = ctx->lv[j + 1];
+    const int mode = (after_zg && L.sluw && !ctx->no_zg && L.n >= ctx->upper_res_min) ? 2 : 1;
+    ResRestrict a{};
+    a.n = (int)L.n;
+    a.sptr = L.sptr;
+    a.scol = L.scol;
+    a.sval = L.sval;
+    a.u = u;
+    a.f = f;
+    a.t = t;
+    a.sluw = L.sluw;
+    a.nlow = L.nlow;
+    a.yperm = (morton_t && L.l2m) ? L.l2m : nullptr;
+    a.nc = (int)Ln.n;
+    a.rptr = L.rptr;
+    a.rcol = (morton_t && L.rcol_m) ? L.rcol_m : L.rcol;
+    a.rval = L.rval;
+    a.y = y;
+    a.c0 = fuse_c0 ? C0Fuse{Ln.u, Ln.sptr, Ln.sval, (int)Ln.coff[1]} : C0Fuse{nullptr, nullptr, nullptr, 0};
+    if (mode == 2) {
+        if (L.rtpr == 1) launch_rr<2, 1>(ctx, a, st);
+        else if (L.rtpr == 2) launch_rr<2, 2>(ctx, a, st);
+        else launch_rr<2, 4>(ctx, a, st);
+    } else {
+        if (L.rtpr == 1) launch_rr<1, 1>(ctx, a, st);
+        else if (L.rtpr == 2) launch_rr<1, 2>(ctx, a, st);
+        else launch_rr<1, 4>(ctx, a, st);
+    }
+    ctx->vcycle_kernels++;
+}
+
 // e_j += P_j e_{j+1}; distributed: the ghosts of e_j are refreshed afterwards
 void enqueue_interp_correct(mgm_ctx* ctx, int j, const double* ec, double* e, cudaStream_t st) {
     Level& L = ctx->lv[j];
@@ -1822,16 +1891,22 @@ void enqueue_vcycle(mgm_ctx* ctx, cudaStream_t st) {
     // residual in Morton order for the restriction's gathers (opt-in: cfg3 restrict L0 30.4 ->
     // 26.7 us but residual 80 -> 85 us; cfg5 solve 206.6 vs 205.2 ms without)
     const bool mt0 = !dist_level(ctx, 0) && lv[0].n >= ctx->morton_t_min;
-    enqueue_residual(ctx, 0, lv[0].f, lv[0].u, lv[0].t, st, ctx->vc_zero_guess && nu1 == 1, mt0);  // line 5
-    stamp(ctx, "residual", 0, st);
     // levels whose first presmooth colour (from zero) is fused into the restriction before them
     auto zg_level = [&](int j) { return nu1 >= 1 && !pre_b && !ctx->poisson && lv[j].slw && !ctx->no_zg; };
     auto c0_fused = [&](int j) {
         return j < D && zg_level(j) && !dist_level(ctx, j) && !dist_level(ctx, j - 1) && lv[j].ncol > 1 &&
                !ctx->no_c0_fuse;
     };
-    enqueue_restrict(ctx, 0, lv[0].t, lv[1].f, st, mt0, c0_fused(1));
-    stamp(ctx, "restrict", 0, st);
+    if (fused_rr_ok(ctx, 0)) {                                           // lines 5 (+ 8's restriction)
+        enqueue_res_restrict(ctx, 0, lv[0].f, lv[0].u, lv[0].t, lv[1].f, st, ctx->vc_zero_guess && nu1 == 1, mt0,
+                             c0_fused(1));
+        stamp(ctx, "residual+restrict", 0, st);
+    } else {
+        enqueue_residual(ctx, 0, lv[0].f, lv[0].u, lv[0].t, st, ctx->vc_zero_guess && nu1 == 1, mt0);  // line 5
+        stamp(ctx, "residual", 0, st);
+        enqueue_restrict(ctx, 0, lv[0].t, lv[1].f, st, mt0, c0_fused(1));
+        stamp(ctx, "restrict", 0, st);
+    }
     for (int j = 1; j < D; ++j) {                                         // lines 6-9
         // e_j = 0 then presmooth; the first forward sweep from the zero guess writes every row
         // and reads only earlier-colour values, so the zero fill is not needed
@@ -1840,8 +1915,13 @@ void enqueue_vcycle(mgm_ctx* ctx, cudaStream_t st) {
         for (int s = 0; s < nu1; ++s) enqueue_sweep(ctx, j, pre_b, st, s == 0 && zg, s == 0 && c0_fused(j));
         stamp(ctx, "zero+presmooth", j, st);
         const bool mt = !dist_level(ctx, j) && lv[j].n >= ctx->morton_t_min;
-        enqueue_residual(ctx, j, lv[j].f, lv[j].u, lv[j].t, st, zg && nu1 == 1, mt);
-        enqueue_restrict(ctx, j, lv[j].t, lv[j + 1].f, st, mt, c0_fused(j + 1));
+        if (fused_rr_ok(ctx, j)) {
+            enqueue_res_restrict(ctx, j, lv[j].f, lv[j].u, lv[j].t, lv[j + 1].f, st, zg && nu1 == 1, mt,
+                                 c0_fused(j + 1));
+        } else {
+            enqueue_residual(ctx, j, lv[j].f, lv[j].u, lv[j].t, st, zg && nu1 == 1, mt);
+            enqueue_restrict(ctx, j, lv[j].t, lv[j + 1].f, st, mt, c0_fused(j + 1));
+        }
         stamp(ctx, "residual+restrict", j, st);
     }
     }

@@ -17,6 +17,8 @@
 
 #include "mgm_internal.h"
 
+#include <cub/cub.cuh>
+
 namespace mgm {
 
 #define FULL 0xffffffffu
@@ -474,7 +476,7 @@ __global__ void k_spgemm_rows(i64 nrows, const i64* __restrict__ ap, const i32* 
     __shared__ i64 off_s[1025];
     __shared__ int total_s;
     for (i64 i = blockIdx.x; i < nrows; i += gridDim.x) {
-        if (skip[i]) continue;  // long rows: computed on the host (spgemm_long_row)
+        if (skip[i]) continue;  // long rows: spgemm_long_rows (sorted products, same order)
         const i64 a0 = ap[i], a1 = ap[i + 1];
         const int na = (int)(a1 - a0);
         // offsets of each A entry's products (serial, rows are short)
@@ -538,49 +540,154 @@ static inline int next_pow2(i64 v) {
     return p;
 }
 
-// A row whose products do not fit the shared-memory buffer (or with more than 1024 A
-// entries) is computed on the host in exactly the device's canonical order: products
-// (A entries by ascending column, then B entries by ascending column) keyed (column,
-// product index), each column's products summed sequentially in product order, with the
-// same correctly rounded multiply and add -- so the result is bit-identical.
-static int spgemm_long_row(const DevCSR& A, const DevCSR& B, const std::vector<i64>& bptr, i64 i,
-                           std::vector<i32>& cols, std::vector<double>& vals, cudaStream_t st) {
-    i64 ar[2];
-    cudaMemcpy(ar, A.ptr + i, sizeof(i64) * 2, cudaMemcpyDeviceToHost);
-    const i64 na = ar[1] - ar[0];
-    std::vector<i32> ac(na);
-    std::vector<double> av(na);
-    cudaMemcpy(ac.data(), A.col + ar[0], sizeof(i32) * na, cudaMemcpyDeviceToHost);
-    cudaMemcpy(av.data(), A.val + ar[0], sizeof(double) * na, cudaMemcpyDeviceToHost);
-    std::vector<std::pair<unsigned long long, double>> prod;  // (col << 32 | pidx, a*b)
-    std::vector<i32> bc;
-    std::vector<double> bv;
-    for (i64 t = 0; t < na; ++t) {
-        const i64 b0 = bptr[ac[t]], b1 = bptr[ac[t] + 1];
-        bc.resize(b1 - b0);
-        bv.resize(b1 - b0);
-        cudaMemcpy(bc.data(), B.col + b0, sizeof(i32) * (b1 - b0), cudaMemcpyDeviceToHost);
-        cudaMemcpy(bv.data(), B.val + b0, sizeof(double) * (b1 - b0), cudaMemcpyDeviceToHost);
-        for (i64 s = 0; s < b1 - b0; ++s) {
-            const unsigned long long pidx = prod.size();
-            prod.push_back({((unsigned long long)(unsigned)bc[s] << 32) | pidx, av[t] * bv[s]});
+// ---------------------------------------------------------------------------------------
+// Long rows (products beyond the shared-memory buffer, or > 1024 A entries), on the GPU in
+// the same canonical order: every product of the long rows is written with the key
+// (long-row slot << 32 | column) and its global product index, the pairs are radix-sorted
+// (stable: equal keys keep ascending product index = the canonical product order), and each
+// run of equal keys is summed sequentially in that order with the same correctly rounded
+// multiply and add as k_spgemm_rows -- bit-identical to the shared-memory path.
+// ---------------------------------------------------------------------------------------
+__global__ void k_long_offsets(i64 nl, const i64* __restrict__ rows, const i64* __restrict__ ap,
+                               const i32* __restrict__ ai, const i64* __restrict__ bp, const i64* __restrict__ loff,
+                               i64* __restrict__ aoff /* per long row: product offset of each A entry */,
+                               const i64* __restrict__ aoff_base) {
+    for (i64 q = (i64)blockIdx.x * blockDim.x + threadIdx.x; q < nl; q += (i64)gridDim.x * blockDim.x) {
+        const i64 i = rows[q], a0 = ap[i], a1 = ap[i + 1];
+        i64 o = loff[q];
+        for (i64 t = a0; t < a1; ++t) {
+            aoff[aoff_base[q] + (t - a0)] = o;
+            const i32 k = ai[t];
+            o += bp[k + 1] - bp[k];
         }
     }
-    std::sort(prod.begin(), prod.end(),
-              [](const std::pair<unsigned long long, double>& x, const std::pair<unsigned long long, double>& y) {
-                  return x.first < y.first;
-              });
-    cols.clear();
-    vals.clear();
-    for (size_t p = 0; p < prod.size();) {
-        const unsigned col = (unsigned)(prod[p].first >> 32);
-        double sum = 0.0;
-        for (; p < prod.size() && (unsigned)(prod[p].first >> 32) == col; ++p) sum = sum + prod[p].second;
-        cols.push_back((i32)col);
-        vals.push_back(sum);
+}
+__global__ void k_long_products(i64 nl, const i64* __restrict__ rows, const i64* __restrict__ ap,
+                                const i32* __restrict__ ai, const double* __restrict__ av,
+                                const i64* __restrict__ bp, const i32* __restrict__ bi,
+                                const double* __restrict__ bv, const i64* __restrict__ aoff,
+                                const i64* __restrict__ aoff_base, unsigned long long* __restrict__ key,
+                                i64* __restrict__ pidx, double* __restrict__ val) {
+    for (i64 q = blockIdx.x; q < nl; q += gridDim.x) {
+        const i64 i = rows[q], a0 = ap[i], a1 = ap[i + 1];
+        for (i64 t = a0; t < a1; ++t) {
+            const i32 k = ai[t];
+            const i64 b0 = bp[k], b1 = bp[k + 1], o = aoff[aoff_base[q] + (t - a0)];
+            const double a = av[t];
+            for (i64 s = b0 + threadIdx.x; s < b1; s += blockDim.x) {
+                key[o + (s - b0)] = ((unsigned long long)q << 32) | (unsigned)bi[s];
+                pidx[o + (s - b0)] = o + (s - b0);
+                val[o + (s - b0)] = __dmul_rn(a, bv[s]);
+            }
+        }
     }
-    (void)st;
-    return (int)cudaGetLastError();
+}
+__global__ void k_long_heads(i64 np, const unsigned long long* __restrict__ key, int* __restrict__ head) {
+    for (i64 p = (i64)blockIdx.x * blockDim.x + threadIdx.x; p < np; p += (i64)gridDim.x * blockDim.x)
+        head[p] = (p == 0 || key[p] != key[p - 1]) ? 1 : 0;
+}
+// segment sums (sequential in product order) and per-long-row unique counts
+__global__ void k_long_sums(i64 np, const unsigned long long* __restrict__ key, const i64* __restrict__ pidx,
+                            const double* __restrict__ val, const int* __restrict__ head,
+                            const int* __restrict__ rank, i32* __restrict__ ocol, double* __restrict__ oval,
+                            int* __restrict__ row_first) {
+    for (i64 p = (i64)blockIdx.x * blockDim.x + threadIdx.x; p < np; p += (i64)gridDim.x * blockDim.x) {
+        if (!head[p]) continue;
+        const unsigned long long k = key[p];
+        double s = 0.0;
+        for (i64 r = p; r < np && key[r] == k; ++r) s = __dadd_rn(s, val[pidx[r]]);
+        ocol[rank[p]] = (i32)(unsigned)(k & 0xffffffffull);
+        oval[rank[p]] = s;
+        if (p == 0 || (key[p - 1] >> 32) != (k >> 32)) row_first[k >> 32] = rank[p];
+    }
+}
+
+struct LongRows {
+    i64 nl = 0, np = 0, nout = 0;
+    std::vector<i64> rows, first;  // first[q] .. first[q+1]: unique columns of long row q in ocol/oval
+    i32* ocol = nullptr;
+    double* oval = nullptr;
+};
+
+template <class T>
+static cudaError_t dalloc_n(T** p, i64 n) { return dev_malloc((void**)p, sizeof(T) * (size_t)std::max<i64>(n, 1)); }
+
+static int spgemm_long_rows(const DevCSR& A, const DevCSR& B, const std::vector<i64>& longs,
+                            const std::vector<i64>& cnt, const std::vector<i64>& aptr, LongRows& LR,
+                            cudaStream_t st, std::string& err) {
+    LR.nl = (i64)longs.size();
+    LR.rows = longs;
+    if (LR.nl == 0) return 0;
+    std::vector<i64> loff(LR.nl + 1, 0), abase(LR.nl + 1, 0);
+    for (i64 q = 0; q < LR.nl; ++q) {
+        loff[q + 1] = loff[q] + cnt[longs[q]];
+        abase[q + 1] = abase[q] + (aptr[longs[q] + 1] - aptr[longs[q]]);
+    }
+    const i64 np = loff[LR.nl];
+    LR.np = np;
+    i64 *d_rows = nullptr, *d_loff = nullptr, *d_abase = nullptr, *d_aoff = nullptr, *d_pidx = nullptr,
+        *d_pidx2 = nullptr;
+    unsigned long long *d_key = nullptr, *d_key2 = nullptr;
+    double* d_val = nullptr;
+    int *d_head = nullptr, *d_rank = nullptr, *d_first = nullptr;
+    void* d_tmp = nullptr;
+    auto cleanup = [&]() {
+        for (void* ptr : {(void*)d_rows, (void*)d_loff, (void*)d_abase, (void*)d_aoff, (void*)d_pidx, (void*)d_pidx2,
+                          (void*)d_key, (void*)d_key2, (void*)d_val, (void*)d_head, (void*)d_rank, (void*)d_first,
+                          d_tmp})
+            if (ptr) dev_free(ptr);
+    };
+    cudaError_t e = dalloc_n(&d_rows, LR.nl);
+    if (!e) e = dalloc_n(&d_loff, LR.nl + 1);
+    if (!e) e = dalloc_n(&d_abase, LR.nl + 1);
+    if (!e) e = dalloc_n(&d_aoff, abase[LR.nl]);
+    if (!e) e = dalloc_n(&d_pidx, np);
+    if (!e) e = dalloc_n(&d_pidx2, np);
+    if (!e) e = dalloc_n(&d_key, np);
+    if (!e) e = dalloc_n(&d_key2, np);
+    if (!e) e = dalloc_n(&d_val, np);
+    if (!e) e = dalloc_n(&d_head, np);
+    if (!e) e = dalloc_n(&d_rank, np);
+    if (!e) e = dalloc_n(&d_first, LR.nl + 1);
+    if (e) { cleanup(); err = "cudaMalloc (long SpGEMM rows)"; return (int)e; }
+    cudaMemcpyAsync(d_rows, longs.data(), sizeof(i64) * LR.nl, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(d_loff, loff.data(), sizeof(i64) * (LR.nl + 1), cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(d_abase, abase.data(), sizeof(i64) * (LR.nl + 1), cudaMemcpyHostToDevice, st);
+    const unsigned g = (unsigned)std::min<i64>(148 * 8, std::max<i64>(1, (LR.nl + 127) / 128));
+    k_long_offsets<<<g, 128, 0, st>>>(LR.nl, d_rows, A.ptr, A.col, B.ptr, d_loff, d_aoff, d_abase);
+    k_long_products<<<(unsigned)std::min<i64>(LR.nl, 148 * 8), 256, 0, st>>>(
+        LR.nl, d_rows, A.ptr, A.col, A.val, B.ptr, B.col, B.val, d_aoff, d_abase, d_key, d_pidx, d_val);
+    // stable radix sort of (row slot, column) keys carrying the product index
+    int hi_bit = 33;
+    while ((1ll << (hi_bit - 32)) <= LR.nl) ++hi_bit;
+    size_t tmp_bytes = 0, tmp2 = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, d_key, d_key2, d_pidx, d_pidx2, (int)np, 0, hi_bit, st);
+    cub::DeviceScan::ExclusiveSum(nullptr, tmp2, d_head, d_rank, (int)np, st);
+    tmp_bytes = std::max(tmp_bytes, tmp2);
+    if ((e = dev_malloc(&d_tmp, std::max<size_t>(tmp_bytes, 1)))) { cleanup(); err = "cudaMalloc (sort)"; return (int)e; }
+    cub::DeviceRadixSort::SortPairs(d_tmp, tmp_bytes, d_key, d_key2, d_pidx, d_pidx2, (int)np, 0, hi_bit, st);
+    const unsigned gp = (unsigned)std::min<i64>(148 * 16, std::max<i64>(1, (np + 255) / 256));
+    k_long_heads<<<gp, 256, 0, st>>>(np, d_key2, d_head);
+    cub::DeviceScan::ExclusiveSum(d_tmp, tmp_bytes, d_head, d_rank, (int)np, st);
+    int last_head = 0, last_rank = 0;
+    cudaMemcpyAsync(&last_head, d_head + np - 1, sizeof(int), cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(&last_rank, d_rank + np - 1, sizeof(int), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    LR.nout = (i64)last_rank + last_head;
+    if ((e = dalloc_n(&LR.ocol, LR.nout)) || (e = dalloc_n(&LR.oval, LR.nout))) {
+        cleanup();
+        err = "cudaMalloc (long rows out)";
+        return (int)e;
+    }
+    k_long_sums<<<gp, 256, 0, st>>>(np, d_key2, d_pidx2, d_val, d_head, d_rank, LR.ocol, LR.oval, d_first);
+    std::vector<int> first(LR.nl);
+    cudaMemcpyAsync(first.data(), d_first, sizeof(int) * LR.nl, cudaMemcpyDeviceToHost, st);
+    e = cudaStreamSynchronize(st);
+    cleanup();
+    if (e) { err = "long SpGEMM rows"; return (int)e; }
+    LR.first.assign(LR.nl + 1, LR.nout);
+    for (i64 q = 0; q < LR.nl; ++q) LR.first[q] = first[q];  // (every long row has >= 1 product)
+    return 0;
 }
 
 int spgemm_device(const DevCSR& A, const DevCSR& B, DevCSR& C, void* stream, std::string& err) {
@@ -600,12 +707,13 @@ int spgemm_device(const DevCSR& A, const DevCSR& B, DevCSR& C, void* stream, std
     cudaMemcpyAsync(aptr.data(), A.ptr, sizeof(i64) * (n + 1), cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
     // shared-memory row buffer: the largest power of two <= 8192 covering the typical rows;
-    // longer rows (and rows with > 1024 A entries) go to spgemm_long_row
+    // longer rows (and rows with > 1024 A entries) go to spgemm_long_rows
     i64 cap = 8192;
     if (const char* e = std::getenv("MGM_SPGEMM_CAP")) cap = std::max<i64>(2, std::atoll(e));  // test hook
     i64 mx = 2;
     std::vector<unsigned char> skip(n, 0);
     std::vector<i64> longs;
+    const std::vector<i64> pcnt = cnt;  // products per row
     for (i64 r = 0; r < n; ++r) {
         if (cnt[r] > cap || aptr[r + 1] - aptr[r] > 1024) {
             skip[r] = 1;
@@ -625,15 +733,13 @@ int spgemm_device(const DevCSR& A, const DevCSR& B, DevCSR& C, void* stream, std
                                                       nullptr, nullptr, nullptr, d_skip);
     cudaMemcpyAsync(cnt.data(), d_cnt, sizeof(i64) * n, cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
-    std::vector<std::vector<i32>> lcols(longs.size());
-    std::vector<std::vector<double>> lvals(longs.size());
-    if (!longs.empty()) {
-        std::vector<i64> bptr(B.nrows + 1);
-        cudaMemcpy(bptr.data(), B.ptr, sizeof(i64) * (B.nrows + 1), cudaMemcpyDeviceToHost);
-        for (size_t q = 0; q < longs.size(); ++q) {
-            spgemm_long_row(A, B, bptr, longs[q], lcols[q], lvals[q], st);
-            cnt[longs[q]] = (i64)lcols[q].size();
-        }
+    LongRows LR;
+    {
+        std::vector<i64> pc(n);  // products per row (the count pass above overwrote d_cnt for short rows)
+        for (size_t q = 0; q < longs.size(); ++q) pc[longs[q]] = pcnt[longs[q]];
+        const int rc = spgemm_long_rows(A, B, longs, pc, aptr, LR, st, err);
+        if (rc) { dev_free(d_cnt); dev_free(d_skip); return rc; }
+        for (i64 q = 0; q < LR.nl; ++q) cnt[longs[q]] = LR.first[q + 1] - LR.first[q];
     }
     std::vector<i64> ptr(n + 1, 0);
     for (i64 r = 0; r < n; ++r) ptr[r + 1] = ptr[r] + cnt[r];
@@ -645,12 +751,14 @@ int spgemm_device(const DevCSR& A, const DevCSR& B, DevCSR& C, void* stream, std
     cudaMemcpyAsync(C.ptr, ptr.data(), sizeof(i64) * (n + 1), cudaMemcpyHostToDevice, st);
     k_spgemm_rows<true><<<grid, threads, smem, st>>>(n, A.ptr, A.col, A.val, B.ptr, B.col, B.val, n2, nullptr,
                                                      C.ptr, C.col, C.val, d_skip);
-    for (size_t q = 0; q < longs.size(); ++q) {
-        const i64 o = ptr[longs[q]];
-        cudaMemcpyAsync(C.col + o, lcols[q].data(), sizeof(i32) * lcols[q].size(), cudaMemcpyHostToDevice, st);
-        cudaMemcpyAsync(C.val + o, lvals[q].data(), sizeof(double) * lvals[q].size(), cudaMemcpyHostToDevice, st);
+    for (i64 q = 0; q < LR.nl; ++q) {  // long rows: device-to-device into place
+        const i64 o = ptr[longs[q]], c0 = LR.first[q], c1 = LR.first[q + 1];
+        cudaMemcpyAsync(C.col + o, LR.ocol + c0, sizeof(i32) * (c1 - c0), cudaMemcpyDeviceToDevice, st);
+        cudaMemcpyAsync(C.val + o, LR.oval + c0, sizeof(double) * (c1 - c0), cudaMemcpyDeviceToDevice, st);
     }
     e = cudaStreamSynchronize(st);
+    if (LR.ocol) dev_free(LR.ocol);
+    if (LR.oval) dev_free(LR.oval);
     dev_free(d_cnt);
     dev_free(d_skip);
     if (e != cudaSuccess) { err = "SpGEMM kernel"; return (int)e; }

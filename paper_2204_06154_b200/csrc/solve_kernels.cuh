@@ -12,6 +12,7 @@
 // for its predecessor before reading any vector or writing anything.  Launched without the
 // attribute, both instructions are no-ops.
 #pragma once
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -89,6 +90,13 @@ struct RowFrag {
 #pragma unroll
         for (int q = 0; q < CH; ++q)
             if (c[q] >= 0) acc = fma(a[q], x[c[q]], acc);
+        return acc;
+    }
+    // the same with L2-coherent gathers (ld.global.cg; values written earlier in this kernel)
+    __device__ __forceinline__ double dot_cg(const double* x, double acc) const {
+#pragma unroll
+        for (int q = 0; q < CH; ++q)
+            if (c[q] >= 0) acc = fma(a[q], __ldcg(x + c[q]), acc);
         return acc;
     }
 };
@@ -246,6 +254,119 @@ __global__ void __launch_bounds__(256) k_sell_spmv(int r0, int r1, int nl, const
         if (POISSON) acc += c[r] * x[nl];
         y[yr] = (MODE == 0) ? acc : (MODE == 1) ? f[r] - acc : -acc;
         if (MODE == 0 && c0.u && r < c0.c0_end) c0.u[r] = 0.0 + (acc - 0.0) / c0.sval[c0.sptr[r >> 5] + (r & 31)];
+    }
+}
+
+// Fused residual + restriction (Alg. 3 lines 5 and 8, P:392 / P:395; north_star item 4):
+//   phase 1  t = f - L_j u  (MODE 1) or -(later-colour part of L_j) u after a zero-guess
+//            sweep (MODE 2), every fine row, written once;
+//   grid-wide barrier (cooperative launch: every CTA is resident);
+//   phase 2  r_{j+1} = R_j t, every coarse row, t gathered from L2 (ld.global.cg), plus
+//            colour 0 of level j+1's presmooth from zero when c0.u (C0Fuse).
+// One launch instead of two: no second kernel ramp and no PDL hand-off between them; t stays
+// in L2 between the phases.  Each fine / coarse row is summed exactly as k_sell_spmv MODE 1/2 /
+// MODE 0 sum it (same slots, same threads per row, same order), so the result is bitwise the
+// unfused pair's.  Grid-stride over rows with a warp-uniform pass count (group_sum shuffles).
+struct ResRestrict {
+    int n;                      // fine rows
+    const int64_t* sptr;
+    const int* scol;
+    const double* sval;
+    const double* u;
+    const double* f;
+    double* t;
+    const int* sluw;            // MODE 2
+    const uint8_t* nlow;        // MODE 2
+    const int* yperm;           // t written at yperm[r] (Morton order) if non-null
+    int nc;                     // coarse rows
+    const int64_t* rptr;
+    const int* rcol;
+    const double* rval;
+    double* y;
+    C0Fuse c0;
+};
+
+template <int MODE, int TPRL, int TPRR, int CH>
+__global__ void __launch_bounds__(256) k_res_restrict(ResRestrict a) {
+    const int T = gridDim.x * blockDim.x;
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    // ---- phase 1: fine rows (TPRL threads per row)
+    {
+        const int per_pass = T / TPRL, part = g % TPRL;
+        const int npass = (a.n + per_pass - 1) / per_pass;
+        for (int ps = 0; ps < npass; ++ps) {
+            const int r = ps * per_pass + g / TPRL;
+            const bool live = r < a.n;
+            RowFrag<TPRL, CH> fr;
+            int w = 0, k1 = part, lim = 0, yr = r;
+            int64_t base = 0;
+            if (live) {
+                if (a.yperm) yr = a.yperm[r];
+                const int64_t s0 = a.sptr[r >> 5];
+                w = (int)((a.sptr[(r >> 5) + 1] - s0) >> 5);
+                base = s0 + (r & 31);
+                if (MODE == 2) {
+                    k1 = a.sluw[r >> 5] + part;
+                    lim = 1 + (int)a.nlow[r];
+                }
+                fr.load(a.sval + base, a.scol + base, w, k1);
+            } else {
+                fr.load(a.sval, a.scol, 0, 0);
+            }
+            if (MODE == 2) {
+#pragma unroll
+                for (int q = 0; q < CH; ++q)
+                    if (k1 + q * TPRL < lim) fr.c[q] = -1;
+            }
+            if (ps == 0) pdl_wait();  // (the first row's operator chunk was loaded before the wait)
+            double acc = fr.dot(a.u, 0.0);
+            for (int k0 = k1 + TPRL * CH; k0 < w; k0 += TPRL * CH) {
+                fr.load(a.sval + base, a.scol + base, w, k0);
+                if (MODE == 2) {
+#pragma unroll
+                    for (int q = 0; q < CH; ++q)
+                        if (k0 + q * TPRL < lim) fr.c[q] = -1;
+                }
+                acc = fr.dot(a.u, acc);
+            }
+            acc = group_sum<TPRL>(acc);
+            if (live && part == 0) a.t[yr] = (MODE == 1) ? a.f[r] - acc : -acc;
+        }
+        if (npass == 0) pdl_wait();
+    }
+    __threadfence();
+    cooperative_groups::this_grid().sync();
+    pdl_trigger();  // (after the barrier: the successor cannot take the SMs of CTAs not yet resident)
+    // ---- phase 2: coarse rows (TPRR threads per row)
+    {
+        const int per_pass = T / TPRR, part = g % TPRR;
+        const int npass = (a.nc + per_pass - 1) / per_pass;
+        for (int ps = 0; ps < npass; ++ps) {
+            const int r = ps * per_pass + g / TPRR;
+            const bool live = r < a.nc;
+            RowFrag<TPRR, CH> fr;
+            int w = 0;
+            int64_t base = 0;
+            if (live) {
+                const int64_t s0 = a.rptr[r >> 5];
+                w = (int)((a.rptr[(r >> 5) + 1] - s0) >> 5);
+                base = s0 + (r & 31);
+                fr.load(a.rval + base, a.rcol + base, w, part);
+            } else {
+                fr.load(a.rval, a.rcol, 0, 0);
+            }
+            double acc = fr.dot_cg(a.t, 0.0);
+            for (int k0 = part + TPRR * CH; k0 < w; k0 += TPRR * CH) {
+                fr.load(a.rval + base, a.rcol + base, w, k0);
+                acc = fr.dot_cg(a.t, acc);
+            }
+            acc = group_sum<TPRR>(acc);
+            if (live && part == 0) {
+                a.y[r] = acc;
+                if (a.c0.u && r < a.c0.c0_end)
+                    a.c0.u[r] = 0.0 + (acc - 0.0) / a.c0.sval[a.c0.sptr[r >> 5] + (r & 31)];
+            }
+        }
     }
 }
 

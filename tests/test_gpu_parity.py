@@ -413,6 +413,54 @@ def test_bottom_kernel_equals_kernel_path(name, knobs, monkeypatch):
     m2.close()
 
 
+@pytest.mark.parametrize("name", ["cfg1", "torus20000", "gfd9000"])
+def test_fused_residual_restriction_bitwise(name, monkeypatch):
+    """The fused residual + restriction kernel (k_res_restrict: residual rows, grid barrier,
+    restriction rows in ONE cooperative launch; north_star item 4) sums every row exactly as
+    the two-kernel path (MGM_NO_FUSE_RR=1): V-cycles (general and from the zero guess, i.e.
+    MODE 1 and MODE 2 residuals, with and without the colour-0 fusion) and GMRES solves are
+    bitwise equal; both equal the oracle to 1e-12 (test_vcycle)."""
+    import torch
+    from paper_2204_06154_b200 import MGM, mgm_apply
+
+    P = pair(name)
+    monkeypatch.setenv("MGM_NO_FUSE_RR", "1")
+    import subprocess, sys, json, os
+    n = len(P.w.points)
+    code = r"""
+import sys, json, numpy as np, torch
+sys.path.insert(0, %r)
+import mgm_inputs as MI
+from paper_2204_06154_b200 import MGM, mgm_apply
+w = %s
+m = MGM(w.points, w.normals, w.stencil, w.levels)
+n = len(w.points)
+rng = np.random.default_rng(5)
+f, u0 = rng.uniform(-1, 1, n), rng.uniform(-1, 1, n)
+u = torch.from_numpy(u0.copy()).cuda()
+m.vcycle(torch.from_numpy(f).cuda(), u)
+y = torch.empty(n, dtype=torch.float64, device="cuda")
+mgm_apply(m.ctx, 0, 7, torch.from_numpy(f).cuda(), None, y)
+x, rep = m.solve(torch.from_numpy(w.rhs).cuda(), tol=1e-10)
+np.save(sys.argv[1], np.stack([u.cpu().numpy(), y.cpu().numpy(), x.cpu().numpy()]))
+print(json.dumps(rep.history))
+""" % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+       {"cfg1": "MI.make_workload(1)", "torus20000": "MI.make_workload(3, n=20000)",
+        "gfd9000": "MI.make_workload(2, n=9000, method='gfd')"}[name])
+    import tempfile
+    outs = []
+    for fuse in (True, False):
+        env = dict(os.environ)
+        if fuse:
+            env.pop("MGM_NO_FUSE_RR", None)
+        with tempfile.NamedTemporaryFile(suffix=".npy") as tf:
+            r = subprocess.run([sys.executable, "-c", code, tf.name], env=env, capture_output=True, text=True)
+            assert r.returncode == 0, r.stderr[-2000:]
+            outs.append((np.load(tf.name), json.loads(r.stdout.strip().splitlines()[-1])))
+    (a, ha), (b, hb) = outs
+    assert np.array_equal(a, b) and ha == hb
+
+
 @pytest.mark.parametrize("name", list(CASES))
 @pytest.mark.parametrize("dense_max", ["4096", "1024", "100000000"])
 def test_dense_bottom(name, dense_max, monkeypatch):
