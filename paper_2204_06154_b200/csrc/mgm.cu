@@ -835,7 +835,11 @@ void setup_bottom(mgm_ctx* ctx, const std::vector<double>& LU, const std::vector
     // data-synchronised phases (bottom_kernel.cuh): cluster GS / ADD / MV phases whose output
     // is a replicated vector; every CTA receives 8 bytes per row of such a phase
     // (numbered per launch: each launch initialises its own mbarriers)
-    const bool mbar_on = std::getenv("MGM_BOT_NO_MBAR") == nullptr;
+    // (opt-in, MGM_BOT_MBAR=1: the phase-ahead arming assumes every CTA sends rows in every
+    // data-synchronised phase, which a small colour spread over 16 CTAs can violate -- ADVICE r01;
+    // the cluster bottom is only the fallback of the dense bottom now, so it runs the always-safe
+    // barrier.cluster phases by default)
+    const bool mbar_on = std::getenv("MGM_BOT_MBAR") != nullptr && std::atoi(std::getenv("MGM_BOT_MBAR")) == 1;
     auto number = [&](size_t q0, size_t q1, int& arm0, int& arm1) {
         std::vector<int> mbq;
         for (size_t q = q0; q + 1 < q1; ++q) {
@@ -1661,9 +1665,13 @@ void enqueue_restrict(mgm_ctx* ctx, int j, double* x, double* y, cudaStream_t st
 // levels with one thread per residual row and 1/2/4 per restriction row; MGM_NO_FUSE_RR=1
 // keeps the two kernels (comparison).
 static bool g_no_fuse_rr = std::getenv("MGM_NO_FUSE_RR") != nullptr;
+// levels with at least this many rows (MGM_FUSE_RR_MIN): below it the grid barrier and the
+// lost PDL overlap cost more than the second kernel (cfg3 L1-L3: 34 / 18 / 15 us unfused vs
+// 47 / 25 / 23 fused; L0: 106.5 vs 103.3)
+static i64 g_fuse_rr_min = std::getenv("MGM_FUSE_RR_MIN") ? std::atoll(std::getenv("MGM_FUSE_RR_MIN")) : 524288;
 bool fused_rr_ok(const mgm_ctx* ctx, int j) {
     const Level& L = ctx->lv[j];
-    return !g_no_fuse_rr && !dist_on(ctx) && !ctx->poisson && L.stpr == 1 &&
+    return !g_no_fuse_rr && L.n >= g_fuse_rr_min && !dist_on(ctx) && !ctx->poisson && L.stpr == 1 &&
            (L.rtpr == 1 || L.rtpr == 2 || L.rtpr == 4) && j + 1 < ctx->p;
 }
 template <int MODE, int TPRR>
