@@ -474,6 +474,14 @@ def main():
     if not args.no_stages and ws == 1:
         stages, bottom = stage_breakdown(w, f, hbm)
 
+    comm = None
+    if dist_mode:  # communication-only replay of one V-cycle's halos + one allreduce (max over ranks)
+        from paper_2204_06154_b200 import mgm_dist_comm_time
+        c = mgm_dist_comm_time(m.ctx, 20)
+        t = torch.tensor([c["halo_ms_per_vcycle"], c["allreduce_us"], vc_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        comm = {"halo_ms_per_vcycle": float(t[0]), "allreduce16_us": float(t[1]),
+                "vcycle_ms": float(t[2]), "note": "device times, max over ranks"}
     vk = mgm_vcycle_kernel_count(m.ctx)
     # kernels per solve: per Arnoldi step the V-cycle graph (vk) + SpMV + 5 CGS2 kernels;
     # start: dot + scale; end: lincomb + V-cycle + axpby, true residual SpMV + axpby + dot
@@ -496,7 +504,7 @@ def main():
                        "parallelism": (f"dist{ws}: Morton row blocks on levels 0..{dinfo['dist_levels'] - 1} "
                                        f"+ ghost halos (NCCL), replicated bottom" if dist_mode else
                                        f"replicas{ws}" if ws > 1 else "single GPU"),
-                       "dist_rank0": dinfo,
+                       "dist_rank0": dinfo, "comm": comm,
                        "l2": "inputs larger than L2 (hierarchy %.2f GB)" %
                              (sum(lv["stored_bytes"] for lv in levels) / 1e9),
                        "setup_s": round(setup_s, 2)},

@@ -200,6 +200,14 @@ mgm_status mgm_local_rows(const mgm_ctx* ctx, int64_t* n_local, int64_t* origina
  * one V-cycle (x 8 bytes = its halo volume). */
 mgm_status mgm_dist_info(const mgm_ctx* ctx, int* dist_levels, int64_t* ghosts, int64_t* halo_values_per_vcycle);
 
+/* Communication-only timing (collective): replays the halo exchanges and the all-gather of one
+ * V-cycle in their V-cycle order without any compute, `reps` times, on the stream; then
+ * `reps` sum-allreduces of 16 doubles (one Krylov multi-dot).  *halo_ms_per_vcycle and
+ * *allreduce_us are this rank's device times (CUDA events); take the max over ranks.
+ * MGM_ERR_ARG on an unattached ctx. */
+mgm_status mgm_dist_comm_time(mgm_ctx* ctx, int reps, double* halo_ms_per_vcycle, double* allreduce_us,
+                              void* cuda_stream);
+
 /* Test hook: R "fake" ranks on ONE GPU in one process.  mgm_fake_group_create makes a group of
  * nranks; each rank's ctx (its own mgm_setup) attaches with mgm_dist_attach_fake and is then
  * driven by its own host thread, calling the same collective entry points as with NCCL.  The

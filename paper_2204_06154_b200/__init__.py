@@ -9,7 +9,7 @@ from .mgm import (MGM, MGMError, load_library, mgm_setup, mgm_vcycle, mgm_solve,
                   mgm_export_weights, mgm_apply, mgm_timing_enable, mgm_timing_read,
                   mgm_bytes_model, mgm_vcycle_kernel_count, mgm_trace_read, mgm_bottom_trace_read, mgm_bottom_ftrace_read,
                   mgm_nccl_unique_id, mgm_dist_attach, mgm_vcycle_batch, mgm_solve_batch,
-                  mgm_dense_bottom_info, torch_allocator, mgm_local_rows, mgm_dist_info,
+                  mgm_dense_bottom_info, torch_allocator, mgm_local_rows, mgm_dist_info, mgm_dist_comm_time,
                   mgm_fake_group_create, mgm_fake_group_destroy, mgm_dist_attach_fake, EXPORTED, LIB_PATH)
 
 load_library()
@@ -17,6 +17,6 @@ load_library()
 __all__ = ["MGM", "MGMError", "load_library", "mgm_setup", "mgm_vcycle", "mgm_solve",
            "mgm_solve_host", "mgm_destroy", "mgm_num_levels", "mgm_level_info",
            "mgm_export_level", "mgm_export_weights", "mgm_apply", "mgm_timing_enable",
-           "mgm_timing_read", "mgm_bytes_model", "mgm_vcycle_kernel_count", "mgm_trace_read", "mgm_bottom_trace_read", "mgm_bottom_ftrace_read", "mgm_nccl_unique_id", "mgm_dist_attach", "mgm_vcycle_batch", "mgm_solve_batch", "mgm_dense_bottom_info", "torch_allocator", "mgm_local_rows", "mgm_dist_info",
+           "mgm_timing_read", "mgm_bytes_model", "mgm_vcycle_kernel_count", "mgm_trace_read", "mgm_bottom_trace_read", "mgm_bottom_ftrace_read", "mgm_nccl_unique_id", "mgm_dist_attach", "mgm_vcycle_batch", "mgm_solve_batch", "mgm_dense_bottom_info", "torch_allocator", "mgm_local_rows", "mgm_dist_info", "mgm_dist_comm_time",
            "mgm_fake_group_create", "mgm_fake_group_destroy", "mgm_dist_attach_fake", "EXPORTED",
            "LIB_PATH"]

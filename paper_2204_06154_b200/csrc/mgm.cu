@@ -3281,6 +3281,52 @@ mgm_status mgm_dist_attach_fake(mgm_ctx* ctx, int rank, void* group) {
     return dist_partition(ctx);
 }
 
+mgm_status mgm_dist_comm_time(mgm_ctx* ctx, int reps, double* halo_ms_per_vcycle, double* allreduce_us,
+                              void* cuda_stream) {
+    AllocScope as_(ctx);
+    mgm_status s = check_ctx(ctx);
+    if (s) return s;
+    if (!ctx->tp || reps < 1) return MGM_ERR_ARG;
+    if ((s = ensure_krylov(ctx))) return s;
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    auto schedule = [&]() {  // the halos and the all-gather of one V-cycle, in order, no compute
+        for (int j = 0; j < ctx->D; ++j) {
+            Level& L = ctx->lv[j];
+            for (int s2 = 0; s2 < ctx->lp.nu1; ++s2)
+                for (int c = 0; c < L.ncol; ++c) exch(ctx, j, L.u, c, st);
+            exch(ctx, j, L.t, -1, st);
+            if (L.d_stage_all) ctx->tp->allgatherv(L.d_stage_mine, L.d_stage_all, L.stage_off, st);
+        }
+        for (int j = ctx->D - 1; j >= 0; --j) {
+            Level& L = ctx->lv[j];
+            exch(ctx, j, L.u, -1, st);
+            for (int s2 = 0; s2 < ctx->lp.nu2; ++s2)
+                for (int c = 0; c < L.ncol; ++c) exch(ctx, j, L.u, c, st);
+        }
+    };
+    schedule();  // warm-up
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, st);
+    for (int r = 0; r < reps; ++r) schedule();
+    cudaEventRecord(e1, st);
+    CK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (halo_ms_per_vcycle) *halo_ms_per_vcycle = ms / reps;
+    double* buf = ctx->dh + 700;
+    cudaEventRecord(e0, st);
+    for (int r = 0; r < reps; ++r) ctx->tp->allreduce_sum(buf, 16, st);
+    cudaEventRecord(e1, st);
+    CK(cudaEventSynchronize(e1));
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (allreduce_us) *allreduce_us = 1e3 * ms / reps;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return MGM_OK;
+}
+
 mgm_status mgm_local_rows(const mgm_ctx* ctx, int64_t* n_local, int64_t* original_ids) {
     if (!ctx || ctx->lv.empty()) return MGM_ERR_ARG;
     const i64 n = ctx->tp ? (i64)ctx->local_ids.size() : ctx->N;

@@ -76,6 +76,7 @@ _SIGS = {
                          ctypes.POINTER(Report), _vp], ctypes.c_int),
     "mgm_dist_attach": ([_vp, ctypes.c_int, ctypes.c_int, _vp], ctypes.c_int),
     "mgm_local_rows": ([_vp, _i64p, _i64p], ctypes.c_int),
+    "mgm_dist_comm_time": ([_vp, ctypes.c_int, _f64p, _f64p, _vp], ctypes.c_int),
     "mgm_dist_info": ([_vp, ctypes.POINTER(ctypes.c_int), _i64p, _i64p], ctypes.c_int),
     "mgm_fake_group_create": ([ctypes.c_int, ctypes.POINTER(_vp)], ctypes.c_int),
     "mgm_fake_group_destroy": ([_vp], ctypes.c_int),
@@ -384,6 +385,15 @@ def mgm_dist_info(ctx) -> dict:
     d, g, h = ctypes.c_int(), _i64(), _i64()
     _check(load_library().mgm_dist_info(ctx, ctypes.byref(d), ctypes.byref(g), ctypes.byref(h)), ctx)
     return dict(dist_levels=d.value, ghosts=g.value, halo_values_per_vcycle=h.value)
+
+
+def mgm_dist_comm_time(ctx, reps: int = 20, stream=None) -> dict:
+    """Collective: device time of one V-cycle's halos + all-gather (no compute) and of one
+    16-double allreduce, this rank."""
+    h, a = ctypes.c_double(), ctypes.c_double()
+    _check(load_library().mgm_dist_comm_time(ctx, reps, ctypes.byref(h), ctypes.byref(a),
+                                             _vp(_stream_ptr(stream))), ctx)
+    return dict(halo_ms_per_vcycle=h.value, allreduce_us=a.value)
 
 
 def mgm_fake_group_create(nranks: int):

@@ -576,6 +576,9 @@ def test_dist_fake_ranks_vcycle_bitwise(R, knobs, monkeypatch):
         uq = torch.from_numpy(u0[ids].copy()).cuda()
         m.vcycle(torch.from_numpy(f[ids].copy()).cuda(), uq)
         m.vcycle(torch.from_numpy(f[ids].copy()).cuda(), uq)       # twice: stale-ghost check
+        from paper_2204_06154_b200 import mgm_dist_comm_time
+        ct = mgm_dist_comm_time(m.ctx, 2)                          # (collective, communication only)
+        assert ct["halo_ms_per_vcycle"] > 0 and ct["allreduce_us"] > 0
         return uq.cpu().numpy(), mgm_dist_info(m.ctx)
 
     out, ids = _fake_ranks(P.w, R, fn)

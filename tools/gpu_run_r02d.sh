@@ -11,3 +11,5 @@ MGM_BENCH_PROFILE=1 ncu --profile-from-start off --cache-control none --replay-m
     --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
     --log-file gpurun_out/r02_insitu_dram.csv python bench.py $ARGS > gpurun_out/ncu_insitu.log 2>&1
 echo done
+python tools/ab_solve.py --cfg 5 --n 4194304 MGM_TRACE=1 MGM_TRACE=1,MGM_NO_FUSE_RR=1 > gpurun_out/ab_cfg5_4m.log 2>&1
+echo done2
