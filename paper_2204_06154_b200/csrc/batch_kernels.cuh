@@ -13,6 +13,24 @@
 
 namespace mgm {
 
+// acc[k] += a * xr[k], k < K, the K contiguous values gathered as 16-byte pairs (K even;
+// interleaved [row][K] vectors are 16-byte aligned for even K)
+template <int K>
+__device__ __forceinline__ void gather_fma(double a, const double* xr, double* acc) {
+    if (K % 2 == 0) {
+        const double2* x2 = reinterpret_cast<const double2*>(xr);
+#pragma unroll
+        for (int k2 = 0; k2 < K / 2; ++k2) {
+            const double2 v = x2[k2];
+            acc[2 * k2] = fma(a, v.x, acc[2 * k2]);
+            acc[2 * k2 + 1] = fma(a, v.y, acc[2 * k2 + 1]);
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < K; ++k) acc[k] = fma(a, xr[k], acc[k]);
+    }
+}
+
 // One colour of a Gauss-Seidel sweep for K right-hand sides (cf. k_gs_colour).
 template <int TPR, int CH, int K>
 __global__ void __launch_bounds__(256) k_gs_colour_b(int r0, int r1, int Wu, const int64_t* __restrict__ sptr,
@@ -60,11 +78,7 @@ __global__ void __launch_bounds__(256) k_gs_colour_b(int r0, int r1, int Wu, con
         if (k0 != part) fr.load(sval + base, scol + base, w, k0);
 #pragma unroll
         for (int q = 0; q < CH; ++q)
-            if (fr.c[q] >= 0) {
-                const double* xr = u + (int64_t)fr.c[q] * K;
-#pragma unroll
-                for (int k = 0; k < K; ++k) acc[k] = fma(fr.a[q], xr[k], acc[k]);
-            }
+            if (fr.c[q] >= 0) gather_fma<K>(fr.a[q], u + (int64_t)fr.c[q] * K, acc);
         if (k0 + TPR * CH >= w) break;
     }
 #pragma unroll
@@ -105,11 +119,7 @@ __global__ void __launch_bounds__(256) k_sell_spmv_b(int r0, int r1, const int64
         if (k0 != part) fr.load(sval + base, scol + base, w, k0);
 #pragma unroll
         for (int q = 0; q < CH; ++q)
-            if (fr.c[q] >= 0) {
-                const double* xr = x + (int64_t)fr.c[q] * K;
-#pragma unroll
-                for (int k = 0; k < K; ++k) acc[k] = fma(fr.a[q], xr[k], acc[k]);
-            }
+            if (fr.c[q] >= 0) gather_fma<K>(fr.a[q], x + (int64_t)fr.c[q] * K, acc);
         if (k0 + TPR * CH >= w) break;
     }
 #pragma unroll

@@ -43,7 +43,7 @@ __global__ void __launch_bounds__(DENSE_THREADS) k_dense_apply(int m, int ld, co
                                                                const double* __restrict__ X, double* __restrict__ Y) {
     constexpr int CR = 4096 / K;  // X rows per staged chunk (32 KB)
     constexpr int U = 8;          // double2 loads in flight per lane
-    __shared__ double xs[CR * K];
+    __shared__ __align__(16) double xs[CR * K];
     pdl_trigger();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int row = blockIdx.x * DENSE_ROWS_PER_CTA + warp;
@@ -82,10 +82,23 @@ __global__ void __launch_bounds__(DENSE_THREADS) k_dense_apply(int m, int ld, co
             for (int q = 0; q < U; ++q) {
                 const int c = 2 * (lane + 32 * (q0 + q));
                 if (c < cn) {
+                    if (K == 1) {
+                        const double2 x2 = *reinterpret_cast<const double2*>(xs + c);
+                        acc[0] = fma(v[q].x, x2.x, acc[0]);
+                        acc[0] = fma(v[q].y, x2.y, acc[0]);
+                    } else {  // (K even: the K values of a column are 16-byte pairs in shared memory)
 #pragma unroll
-                    for (int k = 0; k < K; ++k) {
-                        acc[k] = fma(v[q].x, xs[c * K + k], acc[k]);
-                        acc[k] = fma(v[q].y, xs[(c + 1) * K + k], acc[k]);
+                        for (int k2 = 0; k2 < K / 2; ++k2) {
+                            const double2 a2 = *reinterpret_cast<const double2*>(xs + c * K + 2 * k2);
+                            acc[2 * k2] = fma(v[q].x, a2.x, acc[2 * k2]);
+                            acc[2 * k2 + 1] = fma(v[q].x, a2.y, acc[2 * k2 + 1]);
+                        }
+#pragma unroll
+                        for (int k2 = 0; k2 < K / 2; ++k2) {
+                            const double2 b2 = *reinterpret_cast<const double2*>(xs + (c + 1) * K + 2 * k2);
+                            acc[2 * k2] = fma(v[q].y, b2.x, acc[2 * k2]);
+                            acc[2 * k2 + 1] = fma(v[q].y, b2.y, acc[2 * k2 + 1]);
+                        }
                     }
                 }
             }

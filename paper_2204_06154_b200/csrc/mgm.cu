@@ -2537,6 +2537,28 @@ mgm_status bicgstab_lib(mgm_ctx* ctx, double tol, int maxit, mgm_report* rep, cu
 // one pass over every operator; vectors interleaved [row][K] in lib order; the small levels
 // run the per-kernel path (the one-kernel bottom holds a single right-hand side).
 // ---------------------------------------------------------------------------------------
+// threads per row cap of the batched colour kernels (MGM_BATCH_TPR_CAP; experiment)
+static int g_batch_tpr_cap = std::getenv("MGM_BATCH_TPR_CAP") ? std::max(1, std::atoi(std::getenv("MGM_BATCH_TPR_CAP"))) : 8;
+// threads one wave of batched colour kernels can hold (all SMs, register-limited occupancy)
+template <int K>
+static i64 gs_wave_threads_b(int tpr, int block) {
+    static i64 cache[4][4] = {};
+    const int ti = tpr == 1 ? 0 : tpr == 2 ? 1 : tpr == 4 ? 2 : 3;
+    const int bi = block == 64 ? 0 : block == 128 ? 1 : block == 256 ? 2 : 3;
+    if (cache[ti][bi]) return cache[ti][bi];
+    int dev = 0, nsm = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const void* k = tpr == 1 ? (const void*)k_gs_colour_b<1, CHUNK, K>
+                  : tpr == 2 ? (const void*)k_gs_colour_b<2, CHUNK, K>
+                  : tpr == 4 ? (const void*)k_gs_colour_b<4, CHUNK, K>
+                             : (const void*)k_gs_colour_b<8, CHUNK, K>;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, block, 0) != cudaSuccess) {
+        cudaGetLastError();
+        per = 1;
+    }
+    return cache[ti][bi] = (i64)per * nsm * block;
+}
 template <int K>
 static void b_gs(mgm_ctx* ctx, const Level& L, int j, int r0, int r1, cudaStream_t st) {
     const int span = r1 - (r0 & ~31);
@@ -2545,9 +2567,14 @@ static void b_gs(mgm_ctx* ctx, const Level& L, int j, int r0, int r1, cudaStream
         launch(true, kern, blocks_for((i64)span * tpr, bs), bs, 0, st, r0, r1, L.uniform_w, (const i64*)L.sptr,
                (const i32*)L.scol, (const double*)L.sval, (const double*)ctx->bf[j], ctx->bu[j]);
     };
-    if (L.tpr == 1) go(k_gs_colour_b<1, CHUNK, K>, 1);
-    else if (L.tpr == 2) go(k_gs_colour_b<2, CHUNK, K>, 2);
-    else if (L.tpr == 4) go(k_gs_colour_b<4, CHUNK, K>, 4);
+    // a colour just above one (register-limited) wave: halve the threads per row (cf. launch_gs)
+    int tpr = std::min(L.tpr, g_batch_tpr_cap);
+    while (tpr > 1 && (i64)span * tpr > gs_wave_threads_b<K>(tpr, bs) &&
+           (i64)span * (tpr / 2) <= gs_wave_threads_b<K>(tpr / 2, bs))
+        tpr /= 2;
+    if (tpr == 1) go(k_gs_colour_b<1, CHUNK, K>, 1);
+    else if (tpr == 2) go(k_gs_colour_b<2, CHUNK, K>, 2);
+    else if (tpr == 4) go(k_gs_colour_b<4, CHUNK, K>, 4);
     else go(k_gs_colour_b<8, CHUNK, K>, 8);
 }
 template <int MODE, int K>

@@ -148,7 +148,10 @@ __global__ void __launch_bounds__(256) k_gs_colour(int r0, int r1, int Wu, const
             w = slw[r >> 5];
             lim = 1 + (int)nlow[r];
         }
-        fr.load(sval + base, scol + base, w, part);
+        // ZG: only this row's own diagonal + earlier-colour slots are fetched (the slice's
+        // wider rows' later slots would be masked anyway; in situ the ZG kernels read 1.6x
+        // their algorithmic bytes when the whole slice width was fetched)
+        fr.load(sval + base, scol + base, ZG ? lim : w, part);
         if (ZG) {
 #pragma unroll
             for (int q = 0; q < CH; ++q)  // the diagonal (u_i not yet written, term 0) and later colours
