@@ -463,7 +463,7 @@ def main():
     alg_per_launch = tk["alg_bytes"] / max(1, tk["launches"])
     traffic = None
     try:  # dram bytes per launch of the same kernel from one ncu --set full capture (profiles/)
-        prof = json.load(open(os.path.join(ROOT, "profiles", "r01_ncu_gs_colour_l0.json")))
+        prof = json.load(open(os.path.join(ROOT, "profiles", "r02_ncu_gs_colour_l0.json")))
         traffic = prof["dram_bytes_per_launch"]
     except Exception:
         pass

@@ -480,10 +480,17 @@ static void note_launch(cudaError_t e, unsigned grid, unsigned block, size_t sme
 static bool g_use_pdl = std::getenv("MGM_NO_PDL") == nullptr;
 // dry enqueue pass (L2 prefetch target recording): nothing is launched or recorded
 static thread_local bool g_dry = false;
+// set by every communication call (halo, all-gather, allreduce): the kernel launched next waits
+// for it fully (no programmatic dependency on a communication node)
+static thread_local bool g_after_comm = false;
 template <typename... KArgs, typename... Args>
 static void launch(bool pdl, void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t st,
                    Args... args) {
     if (g_dry) return;
+    if (g_after_comm) {
+        pdl = false;
+        g_after_comm = false;
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(block);
@@ -1538,6 +1545,7 @@ static void exch(mgm_ctx* ctx, int j, double* v, int c, cudaStream_t st) {
                L.d_sendbuf);
     }
     if (!ctx->tp->exchange(x, st) && ctx->err.empty()) ctx->err = "halo exchange failed";
+    g_after_comm = true;
     ctx->vcycle_kernels += 2;
 }
 
@@ -1590,6 +1598,7 @@ void enqueue_border_dot(mgm_ctx* ctx, int j, const double* x, const double* f, d
         k_multidot_fin<<<RED_BLOCKS, RED_THREADS, 0, st>>>((i64)L.n, (const double*)L.c, (i64)0, 1, x, ctx->partials,
                                                            ctx->tickets, s, (double*)nullptr);
         if (!ctx->tp->allreduce_sum(s, 1, st) && ctx->err.empty()) ctx->err = "allreduce failed";
+        g_after_comm = true;
         k_border_set<<<1, 32, 0, st>>>(s, fs, f, (int)L.n, sign, y);
         ctx->vcycle_kernels += 3;
         return;
@@ -1651,6 +1660,7 @@ void enqueue_restrict(mgm_ctx* ctx, int j, double* x, double* y, cudaStream_t st
     if (to_stage) {
         if (!ctx->tp->allgatherv(L.d_stage_mine, L.d_stage_all, L.stage_off, st) && ctx->err.empty())
             ctx->err = "all-gather failed";
+        g_after_comm = true;
         k_scatter<<<blocks_for(Ln.n, 256), 256, 0, st>>>((int)Ln.n, L.d_stage_perm, L.d_stage_all, y);
         ctx->vcycle_kernels += 2;
     }
