@@ -491,7 +491,7 @@ def main():
     if rank == 0:
         cpu = None
         if not args.no_cpu_baseline and args.cfg == 3 and ws == 1:
-            _, cpu = oracle_full(1, 0, args.n)
+            _, cpu = oracle_full(3, 0, args.n)  # median of 3 solves, one pinned core
         line = {
             "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
