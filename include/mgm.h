@@ -181,6 +181,14 @@ mgm_status mgm_solve_batch(mgm_ctx* ctx, int K, const double* rhs_dev, double* x
  * rank's LOCAL vectors: n_local entries in the order mgm_local_rows returns.  Not available
  * on an attached ctx: the batched solves, mgm_apply, mgm_export_level of a distributed level.
  *
+ * Peer-store halos (MGM_P2P=1 in the environment at attach): instead of pack + NCCL send /
+ * receive, one kernel per halo stores every boundary value straight into the peer's ghost slot
+ * (peer memory mapped with cudaIpcOpenMemHandle, handles all-gathered over NCCL) and its last
+ * CTA publishes a per-peer push count (st.release.sys into the peer's flag array); a one-CTA
+ * kernel then waits (ld.acquire.sys) for the counts it expects from its peers.  Requires the
+ * default allocator (no mgm_allocator) and at most 16 peers per level.  With fake ranks the
+ * same stores run, ordered by the group instead of the flags.
+ *
  * mgm_nccl_unique_id: rank 0 creates the 128-byte NCCL id (host buffer id128); the caller
  * broadcasts it to the other ranks (e.g. torch.distributed).  MGM_ERR_NCCL if
  * libnccl.so.2 cannot be loaded.

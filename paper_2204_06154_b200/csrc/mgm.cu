@@ -42,6 +42,7 @@ struct NcclApi {
     ncclResult_t (*GroupStart)() = nullptr;
     ncclResult_t (*GroupEnd)() = nullptr;
     ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
@@ -61,6 +62,7 @@ NcclApi& nccl() {
             api.GroupEnd = (decltype(api.GroupEnd))dlsym(h, "ncclGroupEnd");
             api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
             api.Send = (decltype(api.Send))dlsym(h, "ncclSend");
+            api.AllGather = (decltype(api.AllGather))dlsym(h, "ncclAllGather");
             api.Recv = (decltype(api.Recv))dlsym(h, "ncclRecv");
             api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.Broadcast && api.AllReduce &&
                      api.GroupStart && api.GroupEnd && api.GetErrorString && api.Send && api.Recv;
@@ -142,7 +144,8 @@ struct FakeGroup {
     std::vector<cudaEvent_t> ready, done;    // [rank]
     std::vector<const double*> gather_src;   // [rank]
     std::vector<double*> reduce_buf;         // [rank]
-    explicit FakeGroup(int r) : R(r), posted(r), ready(r), done(r), gather_src(r), reduce_buf(r) {
+    std::vector<std::vector<double*>> bases; // [rank] the u / t pointers of its distributed levels (peer stores)
+    explicit FakeGroup(int r) : R(r), posted(r), ready(r), done(r), gather_src(r), reduce_buf(r), bases(r) {
         for (int q = 0; q < R; ++q) {
             cudaEventCreateWithFlags(&ready[q], cudaEventDisableTiming);
             cudaEventCreateWithFlags(&done[q], cudaEventDisableTiming);
@@ -240,6 +243,20 @@ struct FakeTransport : Transport {
         return true;
     }
     bool capturable() const override { return false; }
+    // run f(stream) on every rank after all ranks' earlier work and before their later work
+    // (the fake-rank stand-in for the peer-store flags)
+    template <class F>
+    bool ordered(F f, cudaStream_t st) {
+        cudaEventRecord(g->ready[rank], st);
+        g->barrier();
+        for (int q = 0; q < nranks; ++q) cudaStreamWaitEvent(st, g->ready[q], 0);
+        f(st);
+        cudaEventRecord(g->done[rank], st);
+        g->barrier();
+        for (int q = 0; q < nranks; ++q) cudaStreamWaitEvent(st, g->done[q], 0);
+        g->barrier();
+        return true;
+    }
     ~FakeTransport() override {
         if (scratch) dev_free(scratch);
         if (d_bufs) dev_free(d_bufs);
@@ -300,6 +317,11 @@ struct Level {
     std::vector<i64> send_off, recv_off, send_coff, recv_coff;
     i32* d_send_idx = nullptr;           // owned row of each send entry
     i64* d_srange = nullptr;             // [ncol + 1][npeers][2] send ranges: all (key 0), colour c (key c + 1)
+    // peer-store halos (MGM_P2P=1): the slot each send entry lands in, in the peer's vector
+    std::vector<i64> h_rslot;
+    i64* d_rslot = nullptr;
+    double* peer_u[16] = {};             // the peers' u / t of this level (mapped peer memory)
+    double* peer_t[16] = {};
     double* d_sendbuf = nullptr;
     std::vector<int> tpr_col;            // threads per row of each colour (the undistributed launch's)
     std::vector<i64> gcoff;              // the undistributed level's colour offsets
@@ -387,6 +409,14 @@ struct mgm_ctx {
     int rank = 0, nranks = 1;
     Transport* tp = nullptr;
     int D = 0;
+    // peer-store halos (MGM_P2P=1 at attach): pushes into the peers' ghost slots + flags
+    bool p2p = false;
+    unsigned long long* p2p_flags = nullptr;   // [nranks] written by the peers (IPC-exported)
+    unsigned long long* p2p_sent = nullptr;    // [nranks] my pushes to each peer
+    unsigned long long* p2p_expect = nullptr;  // [nranks] pushes I have waited for, per peer
+    unsigned long long* peer_flags[64] = {};   // peer r's flag array (mapped), indexed by rank
+    unsigned* p2p_ticket = nullptr;
+    std::vector<void*> ipc_opened;
     std::vector<i64> local_ids;  // original ids of my level-0 rows, in my I/O (Morton) order
     // GMRES workspace
     int restart = 50;
@@ -1521,12 +1551,67 @@ __global__ void k_pack(int chunks, const i64* __restrict__ range, const i32* __r
     for (i64 e = lo + (i64)b * blockDim.x + threadIdx.x; e < hi; e += (i64)chunks * blockDim.x) out[e] = v[idx[e]];
 }
 
+// Peer-store halos (MGM_P2P=1; SURVEY 8(e) "B200-native mitigations"): instead of pack + NCCL,
+// one kernel stores every send entry straight into the peer's ghost slot (mapped peer memory
+// over NVLink: cudaIpc), then its last CTA publishes, per peer, the number of pushes it has
+// made to that peer (st.release.sys into the peer's flag array); the consumer side runs a
+// one-CTA kernel that waits (ld.acquire.sys) until every peer's count reaches the number of
+// exchanges it expects from that peer.  Per-pair counters: ranks need not agree on anything
+// but the (symmetric) sequence of exchanges between each pair.  In a fake-rank group the
+// flags are replaced by the group's event/barrier ordering (no kernel waits on another).
+struct PeerPtrs {
+    double* p[16];
+};
+struct P2PSignal {
+    unsigned long long* flag[16];  // &peer_flags[me] on each peer
+    int rank[16];                  // peer ranks
+    unsigned long long* sent;      // [nranks], this rank's push counters
+    unsigned* ticket;
+    int npeers;
+};
+__global__ void k_push(int chunks, const i64* __restrict__ range, const i32* __restrict__ idx,
+                       const i64* __restrict__ rslot, const double* __restrict__ v, PeerPtrs dst, P2PSignal sig) {
+    const int p = blockIdx.x / chunks, b = blockIdx.x % chunks;
+    const i64 lo = range[2 * p], hi = range[2 * p + 1];
+    double* d = dst.p[p];
+    for (i64 e = lo + (i64)b * blockDim.x + threadIdx.x; e < hi; e += (i64)chunks * blockDim.x) d[rslot[e]] = v[idx[e]];
+    if (!sig.sent) return;  // (fake ranks: the group orders the pushes)
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0 && atomicAdd(sig.ticket, 1u) == gridDim.x - 1) {
+        *sig.ticket = 0u;
+        __threadfence_system();
+        for (int i = 0; i < sig.npeers; ++i) {
+            const unsigned long long s = ++sig.sent[sig.rank[i]];
+            asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(sig.flag[i]), "l"(s) : "memory");
+        }
+    }
+}
+__global__ void k_wait_peers(P2PSignal sig, const unsigned long long* flags, unsigned long long* expect) {
+    if (threadIdx.x < sig.npeers) {
+        const int r = sig.rank[threadIdx.x];
+        const unsigned long long e = ++expect[r];
+        unsigned long long got;
+        do {
+            asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(got) : "l"(flags + r) : "memory");
+            if (got < e) __nanosleep(64);
+        } while (got < e);
+    }
+    __syncthreads();
+}
+
+static void exch_p2p(mgm_ctx* ctx, int j, double* v, int c, cudaStream_t st);
+
 // halo of vector v on distributed level j: colour c's owned values (c < 0: every ghost)
 static void exch(mgm_ctx* ctx, int j, double* v, int c, cudaStream_t st) {
     if (!dist_level(ctx, j) || g_dry) return;
     Level& L = ctx->lv[j];
     const int np = (int)L.peers.size();
     if (np == 0) return;
+    if (ctx->p2p) {
+        exch_p2p(ctx, j, v, c, st);
+        return;
+    }
     const int nc1 = L.ncol + 1;
     std::vector<Xfer> x((size_t)np);
     i64 maxlen = 0;
@@ -1545,6 +1630,44 @@ static void exch(mgm_ctx* ctx, int j, double* v, int c, cudaStream_t st) {
                L.d_sendbuf);
     }
     if (!ctx->tp->exchange(x, st) && ctx->err.empty()) ctx->err = "halo exchange failed";
+    g_after_comm = true;
+    ctx->vcycle_kernels += 2;
+}
+
+static void exch_p2p(mgm_ctx* ctx, int j, double* v, int c, cudaStream_t st) {
+    Level& L = ctx->lv[j];
+    const int np = (int)L.peers.size();
+    const int nc1 = L.ncol + 1;
+    i64 maxlen = 0;
+    for (int i = 0; i < np; ++i) {
+        const i64 s0 = c < 0 ? L.send_off[i] : L.send_coff[(size_t)i * nc1 + c];
+        const i64 s1 = c < 0 ? L.send_off[i + 1] : L.send_coff[(size_t)i * nc1 + c + 1];
+        maxlen = std::max(maxlen, s1 - s0);
+    }
+    const bool is_u = v == L.u;
+    PeerPtrs dst{};
+    for (int i = 0; i < np; ++i) dst.p[i] = is_u ? L.peer_u[i] : L.peer_t[i];
+    P2PSignal sig{};
+    sig.npeers = np;
+    for (int i = 0; i < np; ++i) {
+        sig.rank[i] = L.peers[(size_t)i];
+        sig.flag[i] = ctx->peer_flags[L.peers[(size_t)i]] ? ctx->peer_flags[L.peers[(size_t)i]] + ctx->rank : nullptr;
+    }
+    const int chunks = (int)std::max<i64>(1, std::min<i64>(32, (maxlen + 255) / 256));
+    const i64* rng = L.d_srange + (size_t)(c + 1) * 2 * np;
+    if (!ctx->tp->capturable()) {  // fake ranks: the group orders the pushes (no flags)
+        auto push = [&](cudaStream_t s2) {
+            launch(false, k_push, (unsigned)(chunks * np), 256, 0, s2, chunks, rng, (const i32*)L.d_send_idx,
+                   (const i64*)L.d_rslot, (const double*)v, dst, P2PSignal{});
+        };
+        if (!static_cast<FakeTransport*>(ctx->tp)->ordered(push, st) && ctx->err.empty()) ctx->err = "p2p halo failed";
+    } else {
+        sig.sent = ctx->p2p_sent;
+        sig.ticket = ctx->p2p_ticket;
+        launch(false, k_push, (unsigned)(chunks * np), 256, 0, st, chunks, rng, (const i32*)L.d_send_idx,
+               (const i64*)L.d_rslot, (const double*)v, dst, sig);
+        launch(false, k_wait_peers, 1u, 32u, 0, st, sig, (const unsigned long long*)ctx->p2p_flags, ctx->p2p_expect);
+    }
     g_after_comm = true;
     ctx->vcycle_kernels += 2;
 }
@@ -2797,7 +2920,7 @@ void free_level_device(Level& L) {
                       (void*)L.rcol, (void*)L.rval, (void*)L.u, (void*)L.f, (void*)L.t, (void*)L.c, (void*)L.slw,
                       (void*)L.nlow, (void*)L.sluw, (void*)L.l2m, (void*)L.rcol_m, (void*)L.d_send_idx,
                       (void*)L.d_sendbuf, (void*)L.d_srange, (void*)L.d_stage_mine, (void*)L.d_stage_all,
-                      (void*)L.d_stage_perm})
+                      (void*)L.d_stage_perm, (void*)L.d_rslot})
         if (ptr) dev_free(ptr);
 }
 
@@ -2830,10 +2953,22 @@ mgm_status dist_partition(mgm_ctx* ctx) {
     }
     // ---- partition tables (this rank's) of the distributed levels
     std::vector<PartTables> T((size_t)D);
+    std::vector<std::vector<i64>> rslot((size_t)D);
     for (int j = 0; j < D; ++j) {
         std::vector<PartTables> all;
         partition_level(lv[j].L_lib, owner[(size_t)j], lv[j].colour_lib, lv[j].ncol, &lv[j].P_lib, &owner[(size_t)j + 1],
                         j > 0 ? &lv[j - 1].P_lib : nullptr, j > 0 ? &owner[(size_t)j - 1] : nullptr, P, all);
+        {  // peer-store slots: where each of my send entries lands in the peer's vector
+            const PartTables& Tq = all[(size_t)q];
+            auto& rs = rslot[(size_t)j];
+            rs.assign(Tq.send_rows.size(), 0);
+            for (size_t i = 0; i < Tq.peers.size(); ++i) {
+                const PartTables& Tp = all[(size_t)Tq.peers[i]];
+                const size_t k = (size_t)(std::find(Tp.peers.begin(), Tp.peers.end(), q) - Tp.peers.begin());
+                const i64 base = (i64)Tp.rows.size() + pad + Tp.recv_off[k];
+                for (i64 e = Tq.send_off[i]; e < Tq.send_off[i + 1]; ++e) rs[(size_t)e] = base + (e - Tq.send_off[i]);
+            }
+        }
         T[(size_t)j] = std::move(all[(size_t)q]);
     }
     // global row -> local column index (owned: 0..n-1; ghost g: n + pad + g), per level
@@ -3035,6 +3170,7 @@ mgm_status dist_partition(mgm_ctx* ctx) {
         CK(cudaMemsetAsync(L.t, 0, sizeof(double) * vn, st));
         // -- halo tables
         L.peers = Tj.peers;
+        L.h_rslot = rslot[(size_t)j];
         L.send_off = Tj.send_off;
         L.recv_off = Tj.recv_off;
         L.send_coff = Tj.send_coff;
@@ -3084,6 +3220,93 @@ mgm_status dist_partition(mgm_ctx* ctx) {
             cudaGraphExecDestroy(*gx);
             *gx = nullptr;
         }
+    return MGM_OK;
+}
+
+// Peer-store halos (MGM_P2P=1 at attach): slot tables on the device, counters, and the peers'
+// u / t / flag pointers -- opened with cudaIpcOpenMemHandle (handles all-gathered over NCCL),
+// or taken from the group table for fake ranks.
+mgm_status p2p_setup(mgm_ctx* ctx) {
+    const int P = ctx->nranks, q = ctx->rank;
+    const bool fake = !ctx->tp->capturable();
+    if (!fake && ctx->alloc.alloc) {
+        ctx->err = "peer-store halos need cudaMalloc memory (no allocator hook)";
+        return MGM_ERR_ARG;
+    }
+    if (P > 64) return MGM_ERR_ARG;
+    for (int j = 0; j < ctx->D; ++j)
+        if (ctx->lv[j].peers.size() > 16) {
+            ctx->err = "peer-store halos: more than 16 peers on a level";
+            return MGM_ERR_ARG;
+        }
+    mgm_status s;
+    CK(dalloc(&ctx->p2p_flags, P));
+    CK(dalloc(&ctx->p2p_sent, P));
+    CK(dalloc(&ctx->p2p_expect, P));
+    CK(dalloc(&ctx->p2p_ticket, 1));
+    CK(cudaMemset(ctx->p2p_flags, 0, sizeof(unsigned long long) * P));
+    CK(cudaMemset(ctx->p2p_sent, 0, sizeof(unsigned long long) * P));
+    CK(cudaMemset(ctx->p2p_expect, 0, sizeof(unsigned long long) * P));
+    CK(cudaMemset(ctx->p2p_ticket, 0, sizeof(unsigned)));
+    for (int j = 0; j < ctx->D; ++j)
+        if ((s = upload(ctx, &ctx->lv[j].d_rslot, ctx->lv[j].h_rslot))) return s;
+    // my pointers: u, t of every distributed level, then the flag array
+    std::vector<void*> mine;
+    for (int j = 0; j < ctx->D; ++j) {
+        mine.push_back(ctx->lv[j].u);
+        mine.push_back(ctx->lv[j].t);
+    }
+    mine.push_back(ctx->p2p_flags);
+    const size_t nptr = mine.size();
+    std::vector<std::vector<void*>> theirs((size_t)P, std::vector<void*>(nptr, nullptr));
+    if (fake) {
+        auto* ft = static_cast<FakeTransport*>(ctx->tp);
+        std::vector<double*> b;
+        for (void* x : mine) b.push_back((double*)x);
+        ft->g->bases[(size_t)q] = b;
+        ft->g->barrier();
+        for (int r = 0; r < P; ++r)
+            for (size_t k = 0; k < nptr; ++k) theirs[(size_t)r][k] = ft->g->bases[(size_t)r][k];
+        ft->g->barrier();
+    } else {
+        if (!nccl().AllGather) return MGM_ERR_NCCL;
+        const size_t hb = sizeof(cudaIpcMemHandle_t);
+        std::vector<char> h(nptr * hb);
+        for (size_t k = 0; k < nptr; ++k) CK(cudaIpcGetMemHandle((cudaIpcMemHandle_t*)(h.data() + k * hb), mine[k]));
+        char *d_mine = nullptr, *d_all = nullptr;
+        CK(cudaMalloc((void**)&d_mine, h.size()));
+        CK(cudaMalloc((void**)&d_all, h.size() * P));
+        CK(cudaMemcpy(d_mine, h.data(), h.size(), cudaMemcpyHostToDevice));
+        auto* nt = static_cast<NcclTransport*>(ctx->tp);
+        if (nccl().AllGather(d_mine, d_all, h.size(), ncclChar, nt->comm, ctx->st) != ncclSuccess) return MGM_ERR_NCCL;
+        std::vector<char> all(h.size() * P);
+        CK(cudaStreamSynchronize(ctx->st));
+        CK(cudaMemcpy(all.data(), d_all, all.size(), cudaMemcpyDeviceToHost));
+        cudaFree(d_mine);
+        cudaFree(d_all);
+        for (int r = 0; r < P; ++r) {
+            if (r == q) continue;
+            for (size_t k = 0; k < nptr; ++k) {
+                cudaIpcMemHandle_t hh;
+                std::memcpy(&hh, all.data() + (size_t)r * h.size() + k * hb, hb);
+                void* ptr = nullptr;
+                CK(cudaIpcOpenMemHandle(&ptr, hh, cudaIpcMemLazyEnablePeerAccess));
+                ctx->ipc_opened.push_back(ptr);
+                theirs[(size_t)r][k] = ptr;
+            }
+        }
+    }
+    for (int j = 0; j < ctx->D; ++j) {
+        Level& L = ctx->lv[j];
+        for (size_t i = 0; i < L.peers.size(); ++i) {
+            L.peer_u[i] = (double*)theirs[(size_t)L.peers[i]][2 * (size_t)j];
+            L.peer_t[i] = (double*)theirs[(size_t)L.peers[i]][2 * (size_t)j + 1];
+        }
+    }
+    for (int r = 0; r < P; ++r)
+        ctx->peer_flags[r] = r == q ? nullptr : (unsigned long long*)theirs[(size_t)r][nptr - 1];
+    ctx->p2p = true;
+    CK(cudaDeviceSynchronize());
     return MGM_OK;
 }
 
@@ -3289,7 +3512,9 @@ mgm_status mgm_dist_attach(mgm_ctx* ctx, int rank, int nranks, const void* id128
     ctx->tp = t;
     ctx->rank = rank;
     ctx->nranks = nranks;
-    return dist_partition(ctx);
+    mgm_status s = dist_partition(ctx);
+    if (s == MGM_OK && std::getenv("MGM_P2P") && std::atoi(std::getenv("MGM_P2P")) == 1) s = p2p_setup(ctx);
+    return s;
 }
 
 mgm_status mgm_fake_group_create(int nranks, void** group) {
@@ -3315,7 +3540,9 @@ mgm_status mgm_dist_attach_fake(mgm_ctx* ctx, int rank, void* group) {
     ctx->tp = t;
     ctx->rank = rank;
     ctx->nranks = g->R;
-    return dist_partition(ctx);
+    mgm_status s = dist_partition(ctx);
+    if (s == MGM_OK && std::getenv("MGM_P2P") && std::atoi(std::getenv("MGM_P2P")) == 1) s = p2p_setup(ctx);
+    return s;
 }
 
 mgm_status mgm_dist_comm_time(mgm_ctx* ctx, int reps, double* halo_ms_per_vcycle, double* allreduce_us,
@@ -3408,6 +3635,9 @@ mgm_status mgm_destroy(mgm_ctx* ctx) {
     if (ctx->d_trace) dev_free(ctx->d_trace);
     if (ctx->vgraph) cudaGraphExecDestroy(ctx->vgraph);
     if (ctx->vgraph0) cudaGraphExecDestroy(ctx->vgraph0);
+    for (void* ptr : ctx->ipc_opened) cudaIpcCloseMemHandle(ptr);
+    for (void* ptr : {(void*)ctx->p2p_flags, (void*)ctx->p2p_sent, (void*)ctx->p2p_expect, (void*)ctx->p2p_ticket})
+        if (ptr) dev_free(ptr);
     delete ctx->tp;
     ctx->tp = nullptr;
     for (auto* q : {&ctx->bu, &ctx->bf, &ctx->bt})

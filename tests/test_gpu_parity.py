@@ -550,9 +550,10 @@ DIST_KNOBS = [{}, {"MGM_DIST_MIN_ROWS": "1"},
               {"MGM_DIST_MIN_ROWS": "1", "MGM_DENSE_MAX": "0", "MGM_BOT_MAX": "0"}]
 
 
+@pytest.mark.parametrize("p2p", ["0", "1"])
 @pytest.mark.parametrize("R", [2, 3])
 @pytest.mark.parametrize("knobs", range(len(DIST_KNOBS)))
-def test_dist_fake_ranks_vcycle_bitwise(R, knobs, monkeypatch):
+def test_dist_fake_ranks_vcycle_bitwise(R, knobs, p2p, monkeypatch):
     """The partitioned V-cycle (Morton row blocks on every distributed level, ghost halos per
     colour / per transfer, all-gather into the replicated bottom) is bitwise the single-GPU
     V-cycle: every owned row is computed by the same arithmetic.  Variants: the default level
@@ -564,6 +565,7 @@ def test_dist_fake_ranks_vcycle_bitwise(R, knobs, monkeypatch):
     P = pair("torus20000")
     for k, v in DIST_KNOBS[knobs].items():
         monkeypatch.setenv(k, v)
+    monkeypatch.setenv("MGM_P2P", p2p)   # 1: peer-store halos (remote stores into the ghost slots)
     ref = MGM(P.w.points, P.w.normals, P.w.stencil, P.w.levels)
     n = len(P.w.points)
     f, u0 = _rand(n, 7), _rand(n, 8)
@@ -593,9 +595,10 @@ def test_dist_fake_ranks_vcycle_bitwise(R, knobs, monkeypatch):
     ref.close()
 
 
+@pytest.mark.parametrize("p2p", ["0", "1"])
 @pytest.mark.parametrize("name", ["torus20000", "poisson6000"])
 @pytest.mark.parametrize("krylov", [1, 0, 2])
-def test_dist_fake_ranks_solve(name, krylov, monkeypatch):
+def test_dist_fake_ranks_solve(name, krylov, p2p, monkeypatch):
     """Distributed MGM-GMRES / standalone / BiCGSTAB on 3 fake ranks against the oracle: the
     Krylov inner products are rank-local sums + an all-reduce (another summation order), so
     iterations within +-1 (+-2 BiCGSTAB) and solutions to 1e-9; Poisson: the border dots and
@@ -606,6 +609,7 @@ def test_dist_fake_ranks_solve(name, krylov, monkeypatch):
     if krylov == 0 and name == "poisson6000":
         pytest.skip("standalone MGM converges slowly on this cloud (P:411)")
     monkeypatch.setenv("MGM_DIST_MIN_ROWS", "1")
+    monkeypatch.setenv("MGM_P2P", p2p)
     rhs = P.w.rhs
     xr, rr = P.ref.solve(rhs, tol=1e-10, krylov=krylov, maxit=300)
 
