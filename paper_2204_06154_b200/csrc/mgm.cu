@@ -2725,6 +2725,8 @@ template <int K>
 static void enqueue_vcycle_b(mgm_ctx* ctx, cudaStream_t st) {
     auto& lv = ctx->lv;
     const int p = ctx->p;
+    ctx->ntrace = 0;
+    ctx->trace_labels.clear();
     const int nu1 = ctx->lp.nu1, nu2 = ctx->lp.nu2;
     const bool pre_b = ctx->lp.smoother == 1, post_b = ctx->lp.smoother == 1 || ctx->lp.smoother == 2;
     auto sweep = [&](int j, bool backward) {
@@ -2742,24 +2744,30 @@ static void enqueue_vcycle_b(mgm_ctx* ctx, cudaStream_t st) {
     if (p == 1) { coarse(); return; }
     // levels >= D: the dense bottom B_D applied to the K columns at once (dense_bottom.cuh)
     const int D = ctx->denseJ > 0 ? ctx->denseJ : p - 1;
+    stamp(ctx, "start", 0, st);
     for (int s = 0; s < nu1; ++s) sweep(0, pre_b);                                  // line 4
+    stamp(ctx, "presmooth", 0, st);
     for (int j = 0; j < D; ++j) {                                                   // lines 5-9
         const Level& L = lv[j];
         if (j > 0) {
             cudaMemsetAsync(ctx->bu[j], 0, sizeof(double) * L.n * K, st);
             for (int s = 0; s < nu1; ++s) sweep(j, pre_b);
         }
+        if (j > 0) stamp(ctx, "zero+presmooth", j, st);
         b_spmv<1, K>(L.stpr, L.n, L.sptr, L.scol, L.sval, ctx->bu[j], ctx->bf[j], ctx->bt[j], st);
         b_spmv<0, K>(L.rtpr, lv[j + 1].n, L.rptr, L.rcol, L.rval, ctx->bt[j], nullptr, ctx->bf[j + 1], st);
+        stamp(ctx, "residual+restrict", j, st);
     }
     if (ctx->denseJ > 0) enqueue_dense_bottom(ctx, K, ctx->bf[D], ctx->bu[D], st);
     else coarse();                                                                   // line 10
+    stamp(ctx, "bottom", D, st);
     for (int j = D - 1; j >= 0; --j) {                                              // lines 11-16
         const Level& L = lv[j];
         auto kern = L.pm <= 8 ? k_interp_correct_b<8, K> : k_interp_correct_b<16, K>;
         launch(true, kern, blocks_for(L.n, 256), 256, 0, st, (int)L.n, L.pm, (const i32*)L.pcol,
                (const double*)L.pval, (const double*)ctx->bu[j + 1], ctx->bu[j]);
         for (int s = 0; s < nu2; ++s) sweep(j, post_b);
+        stamp(ctx, "interp+postsmooth", j, st);
     }
 }
 static void enqueue_vcycle_bk(mgm_ctx* ctx, int K, cudaStream_t st) {

@@ -516,13 +516,12 @@ def _fake_ranks(w, R, fn, levels=None):
 
     ms = [MGM(w.points, w.normals, w.stencil, levels or w.levels) for _ in range(R)]
     g = mgm_fake_group_create(R)
-    for q, m in enumerate(ms):
-        m.attach_fake(q, g)
     out, errs = [None] * R, []
 
     def run(q):
         try:
             torch.cuda.set_device(0)
+            ms[q].attach_fake(q, g)          # (collective with peer-store halos: every thread attaches)
             s = torch.cuda.Stream()
             with torch.cuda.stream(s):
                 out[q] = fn(q, ms[q])
@@ -530,11 +529,11 @@ def _fake_ranks(w, R, fn, levels=None):
         except Exception as e:  # noqa: BLE001
             errs.append(e)
 
-    th = [threading.Thread(target=run, args=(q,)) for q in range(R)]
+    th = [threading.Thread(target=run, args=(q,), daemon=True) for q in range(R)]
     for t in th:
         t.start()
     for t in th:
-        t.join(timeout=600)
+        t.join(timeout=300)
     alive = any(t.is_alive() for t in th)
     if not alive:
         for m in ms:
