@@ -1994,9 +1994,12 @@ void enqueue_dense_bottom(mgm_ctx* ctx, int K, const double* r, double* e, cudaS
     const double* B = ctx->dB;
     switch (K) {
         case 1: launch(ctx->pdl, k_dense_apply<1>, grid, DENSE_THREADS, 0, st, mm, ld, B, r, e); break;
-        case 2: launch(true, k_dense_apply<2>, grid, DENSE_THREADS, 0, st, mm, ld, B, r, e); break;
-        case 4: launch(true, k_dense_apply<4>, grid, DENSE_THREADS, 0, st, mm, ld, B, r, e); break;
-        default: launch(true, k_dense_apply<8>, grid, DENSE_THREADS, 0, st, mm, ld, B, r, e); break;
+        case 2: launch(true, k_dense_apply_multi<2, 4>, blocks_for(mm, 4 * DENSE_ROWS_PER_CTA), DENSE_THREADS, 0, st,
+                       mm, ld, B, r, e); break;
+        case 4: launch(true, k_dense_apply_multi<4, 4>, blocks_for(mm, 4 * DENSE_ROWS_PER_CTA), DENSE_THREADS, 0, st,
+                       mm, ld, B, r, e); break;
+        default: launch(true, k_dense_apply_multi<8, 4>, blocks_for(mm, 4 * DENSE_ROWS_PER_CTA), DENSE_THREADS, 0, st,
+                        mm, ld, B, r, e); break;
     }
     ctx->vcycle_kernels++;
 }
