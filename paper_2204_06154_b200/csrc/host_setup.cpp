@@ -607,6 +607,41 @@ int greedy_colouring(const HostCSR& A, std::vector<i32>& colour, int passes) {
     return ncol;
 }
 
+static int lu_threads() {
+    return std::max(1, std::min(64, (int)std::thread::hardware_concurrency()));
+}
+
+// Explicit inverse from the LU factors (column-major, pivots): column i solves P A x = e_i by
+// forward (unit lower, ascending k) and backward substitution (x_r = (b_r - sum_{c > r,
+// ascending} U_rc x_c) / U_rr), the same operations per column as the single-threaded loop it
+// replaces; U is transposed to row-major first so the backward sums read contiguously, and
+// the columns run on threads.  Ainv row-major.
+void dense_inverse(const std::vector<double>& LU, const std::vector<i32>& piv, int m, std::vector<double>& Ainv,
+                   int nthreads) {
+    std::vector<double> U((size_t)m * m);  // row-major copy: U[r*m + c] = LU(r, c)
+    for (int c = 0; c < m; ++c)
+        for (int r = 0; r < m; ++r) U[(size_t)r * m + c] = LU[(size_t)c * m + r];
+    Ainv.assign((size_t)m * m, 0.0);
+    parallel_for(m, m >= 256 ? nthreads : 1, [&](i64 a, i64 b) {
+        std::vector<double> bb(m);
+        for (i64 i = a; i < b; ++i) {
+            std::fill(bb.begin(), bb.end(), 0.0);
+            bb[(size_t)i] = 1.0;
+            for (int k = 0; k < m; ++k)
+                if (piv[k] != k) std::swap(bb[k], bb[piv[k]]);
+            for (int k = 0; k < m; ++k)
+                for (int r = k + 1; r < m; ++r) bb[r] -= LU[(size_t)k * m + r] * bb[k];
+            for (int r = m - 1; r >= 0; --r) {
+                double acc = bb[r];
+                const double* ur = U.data() + (size_t)r * m;
+                for (int c = r + 1; c < m; ++c) acc -= ur[c] * bb[c];
+                bb[r] = acc / ur[r];
+            }
+            for (int r = 0; r < m; ++r) Ainv[(size_t)r * m + i] = bb[r];
+        }
+    });
+}
+
 // Dense LU with partial pivoting (O13); ties -> lowest row.  Row-major in, column-major out.
 i64 dense_lu_colmajor(std::vector<double>& A, int m, std::vector<double>& LU, std::vector<i32>& piv) {
     double amax = 0.0;
@@ -622,10 +657,22 @@ i64 dense_lu_colmajor(std::vector<double>& A, int m, std::vector<double>& LU, st
         if (p != k)
             for (int j = 0; j < m; ++j) std::swap(A[(i64)k * m + j], A[(i64)p * m + j]);
         double d = A[(i64)k * m + k];
-        for (int i = k + 1; i < m; ++i) {
-            double l = A[(i64)i * m + k] / d;
-            A[(i64)i * m + k] = l;
-            for (int j = k + 1; j < m; ++j) A[(i64)i * m + j] = A[(i64)i * m + j] - l * A[(i64)k * m + j];
+        // rows below the pivot are independent: threads over rows (large coarsest levels)
+        auto rows = [&](i64 a, i64 b) {
+            for (i64 i = k + 1 + a; i < k + 1 + b; ++i) {
+                double l = A[i * m + k] / d;
+                A[i * m + k] = l;
+                for (int j = k + 1; j < m; ++j) A[i * m + j] = A[i * m + j] - l * A[(i64)k * m + j];
+            }
+        };
+        const i64 nr = m - k - 1;
+        const int nt = (nr >= 256 && m >= 1024) ? std::min<i64>(lu_threads(), nr / 64) : 1;
+        if (nt > 1) {
+            std::vector<std::thread> th;
+            for (int t = 0; t < nt; ++t) th.emplace_back([&, t] { rows(nr * t / nt, nr * (t + 1) / nt); });
+            for (auto& x : th) x.join();
+        } else {
+            rows(0, nr);
         }
     }
     LU.resize((size_t)m * m);

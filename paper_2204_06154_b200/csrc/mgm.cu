@@ -762,21 +762,8 @@ void setup_bottom(mgm_ctx* ctx, const std::vector<double>& LU, const std::vector
     const int m = ctx->nc;
     Ell EC;
     {
-        std::vector<double> Ainv((size_t)m * m), b(m);
-        for (int i = 0; i < m; ++i) {
-            std::fill(b.begin(), b.end(), 0.0);
-            b[i] = 1.0;
-            for (int k = 0; k < m; ++k)
-                if (piv[k] != k) std::swap(b[k], b[piv[k]]);
-            for (int k = 0; k < m; ++k)
-                for (int r = k + 1; r < m; ++r) b[r] -= LU[(size_t)k * m + r] * b[k];
-            for (int r = m - 1; r >= 0; --r) {
-                double acc = b[r];
-                for (int c = r + 1; c < m; ++c) acc -= LU[(size_t)c * m + r] * b[c];
-                b[r] = acc / LU[(size_t)r * m + r];
-            }
-            for (int r = 0; r < m; ++r) Ainv[(size_t)r * m + i] = b[r];
-        }
+        std::vector<double> Ainv;
+        dense_inverse(LU, piv, m, Ainv, ctx->nthreads);
         std::vector<int> ccol((size_t)m * m);
         for (int r = 0; r < m; ++r)
             for (int c = 0; c < m; ++c) ccol[(size_t)r * m + c] = c;
@@ -1028,21 +1015,27 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
         A.ptr.resize(N + 1);
         A.col.resize((size_t)N * ns);
         A.val.resize((size_t)N * ns);
-        std::vector<int> ord(ns);
-        for (i64 i = 0; i < N; ++i) {
-            A.ptr[i] = i * ns;
-            for (int j = 0; j < ns; ++j) ord[j] = j;
-            std::sort(ord.begin(), ord.end(), [&](int a, int b) { return sten[i * ns + a] < sten[i * ns + b]; });
-            for (int j = 0; j < ns; ++j) {
-                int q = ord[j];
-                double wv = W[i * ns + q];
-                double v;
-                if (sp.problem == 0) v = (q == 0) ? 1.0 - sp.mu * wv : -(sp.mu * wv);
-                else v = wv;
-                A.col[i * ns + j] = sten[i * ns + q];
-                A.val[i * ns + j] = v;
-            }
-        }
+        std::vector<std::thread> th;  // rows are independent: threads over row ranges
+        const int nt = std::max(1, std::min(nth, (int)(N / 65536) + 1));
+        for (int t = 0; t < nt; ++t)
+            th.emplace_back([&, t] {
+                std::vector<int> ord(ns);
+                for (i64 i = N * t / nt; i < N * (t + 1) / nt; ++i) {
+                    A.ptr[i] = i * ns;
+                    for (int j = 0; j < ns; ++j) ord[j] = j;
+                    std::sort(ord.begin(), ord.end(), [&](int a, int b) { return sten[i * ns + a] < sten[i * ns + b]; });
+                    for (int j = 0; j < ns; ++j) {
+                        int q = ord[j];
+                        double wv = W[i * ns + q];
+                        double v;
+                        if (sp.problem == 0) v = (q == 0) ? 1.0 - sp.mu * wv : -(sp.mu * wv);
+                        else v = wv;
+                        A.col[i * ns + j] = sten[i * ns + q];
+                        A.val[i * ns + j] = v;
+                    }
+                }
+            });
+        for (auto& t : th) t.join();
         A.ptr[N] = N * ns;
     }
     tm.mark("assemble L1");
@@ -1133,6 +1126,14 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
     std::vector<std::vector<i64>> lib2mor(p);
     std::vector<std::vector<i32>> mor2lib(p);
     std::vector<std::vector<i32>> colour_mor(p);
+    {  // the levels' colourings are independent: one thread per level
+        std::vector<std::thread> th;
+        std::vector<int> nc(p, 0);
+        for (int j = 0; j + 1 < p; ++j)
+            th.emplace_back([&, j] { nc[j] = greedy_colouring(Lm[j], colour_mor[j], colour_passes()); });
+        for (auto& t : th) t.join();
+        for (int j = 0; j + 1 < p; ++j) ctx->lv[j].ncol = nc[j];
+    }
     for (int j = 0; j < p; ++j) {
         Level& L = ctx->lv[j];
         i64 n = Lm[j].nrows;
@@ -1140,7 +1141,6 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
         lib2mor[j].resize(n);
         mor2lib[j].resize(n);
         if (j + 1 < p) {
-            L.ncol = greedy_colouring(Lm[j], colour_mor[j], colour_passes());
             L.coff.assign(L.ncol + 1, 0);
             for (i64 i = 0; i < n; ++i) L.coff[colour_mor[j][i] + 1]++;
             for (int c = 0; c < L.ncol; ++c) L.coff[c + 1] += L.coff[c];
@@ -1334,21 +1334,8 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
         if (ctx->denseJ < 0) setup_bottom(ctx, LU, piv);  // (the dense bottom replaces it)
         tm.mark("bottom kernel setup", p - 1);
         if (m <= 4096) {  // explicit inverse for the batched coarse solve (same solution up to rounding, O13)
-            std::vector<double> Ainv((size_t)m * m), bb(m);
-            for (int i = 0; i < m; ++i) {
-                std::fill(bb.begin(), bb.end(), 0.0);
-                bb[i] = 1.0;
-                for (int k = 0; k < m; ++k)
-                    if (piv[k] != k) std::swap(bb[k], bb[piv[k]]);
-                for (int k = 0; k < m; ++k)
-                    for (int r = k + 1; r < m; ++r) bb[r] -= LU[(size_t)k * m + r] * bb[k];
-                for (int r = m - 1; r >= 0; --r) {
-                    double acc = bb[r];
-                    for (int c = r + 1; c < m; ++c) acc -= LU[(size_t)c * m + r] * bb[c];
-                    bb[r] = acc / LU[(size_t)r * m + r];
-                }
-                for (int r = 0; r < m; ++r) Ainv[(size_t)r * m + i] = bb[r];
-            }
+            std::vector<double> Ainv;
+            dense_inverse(LU, piv, m, Ainv, nth);
             if ((s = upload(ctx, &ctx->ainv, Ainv))) return s;
             tm.mark("coarse inverse", p - 1);
         }

@@ -54,6 +54,9 @@ HostCSR transpose(const HostCSR& A);
 // solve.  Returns -1 on success or the failing pivot column.
 i64 dense_lu_colmajor(std::vector<double>& A_rowmajor, int m, std::vector<double>& LU_colmajor,
                       std::vector<i32>& piv);
+// Explicit inverse (row-major) from those factors, columns on `nthreads` threads.
+void dense_inverse(const std::vector<double>& LU, const std::vector<i32>& piv, int m, std::vector<double>& Ainv,
+                   int nthreads);
 
 // ---------------- distributed solve: partition of one level (host_setup.cpp) ------------
 // SURVEY 8(e) / DESIGN.md "Multi-GPU": rank q owns the rows with owner[r] == q (a Morton
