@@ -492,117 +492,199 @@ int colour_passes() {
 // its neighbours in sym(pattern) minus the diagonal), ties by larger degree (distinct
 // neighbours) then lower index, with the smallest colour unused by its neighbours.  Returns
 // the colour count, or -1 if a colour index would reach 256 (the caller falls back).
-// neighbours of each vertex in sym(pattern(A)) minus the diagonal: sorted, deduplicated
-static void sym_adjacency(const HostCSR& A, std::vector<i64>& np, std::vector<i64>& nb) {
-    const HostCSR T = transpose(A);
-    const i64 n = A.nrows;
-    np.assign(n + 1, 0);
-    nb.clear();
-    nb.reserve((size_t)(A.nnz() + T.nnz()));
-    for (i64 i = 0; i < n; ++i) {
-        const size_t o0 = nb.size();
-        for (i64 t = A.ptr[i]; t < A.ptr[i + 1]; ++t)
-            if (A.col[t] != i) nb.push_back(A.col[t]);
-        for (i64 t = T.ptr[i]; t < T.ptr[i + 1]; ++t)
-            if (T.col[t] != i) nb.push_back(T.col[t]);
-        std::sort(nb.begin() + (i64)o0, nb.end());
-        nb.erase(std::unique(nb.begin() + (i64)o0, nb.end()), nb.end());
-        np[i + 1] = (i64)nb.size();
+// neighbours of each vertex in sym(pattern(A)) minus the diagonal: sorted, deduplicated.
+// Pattern transpose, then each row's union sorted in its own slot (threads over rows) and
+// compacted.
+static int col_threads() { return std::max(1, std::min(64, (int)std::thread::hardware_concurrency())); }
+
+static void sym_adjacency(const HostCSR& A, std::vector<i64>& np, std::vector<i32>& nb) {
+    const i64 n = A.nrows, nnz = A.nnz();
+    std::vector<i64> tp(n + 1, 0);
+    for (i64 t = 0; t < nnz; ++t) tp[A.col[t] + 1]++;
+    for (i64 r = 0; r < n; ++r) tp[r + 1] += tp[r];
+    std::vector<i32> tc((size_t)nnz);
+    {
+        std::vector<i64> fill(tp.begin(), tp.end() - 1);
+        for (i64 i = 0; i < n; ++i)
+            for (i64 t = A.ptr[i]; t < A.ptr[i + 1]; ++t) tc[(size_t)fill[A.col[t]]++] = (i32)i;
     }
+    std::vector<i32> tmp((size_t)(2 * nnz));
+    std::vector<i64> cnt(n + 1, 0);
+    const int nt = col_threads();
+    parallel_for(n, nt, [&](i64 b, i64 e) {
+        for (i64 i = b; i < e; ++i) {
+            i32* o = tmp.data() + A.ptr[i] + tp[i];
+            i32* q = o;
+            for (i64 t = A.ptr[i]; t < A.ptr[i + 1]; ++t)
+                if (A.col[t] != i) *q++ = A.col[t];
+            for (i64 t = tp[i]; t < tp[i + 1]; ++t)
+                if (tc[t] != i) *q++ = tc[t];
+            std::sort(o, q);
+            cnt[i + 1] = std::unique(o, q) - o;
+        }
+    });
+    np.assign(n + 1, 0);
+    for (i64 i = 0; i < n; ++i) np[i + 1] = np[i] + cnt[i + 1];
+    nb.resize((size_t)np[n]);
+    parallel_for(n, nt, [&](i64 b, i64 e) {
+        for (i64 i = b; i < e; ++i)
+            std::copy(tmp.data() + A.ptr[i] + tp[i], tmp.data() + A.ptr[i] + tp[i] + cnt[i + 1], nb.data() + np[i]);
+    });
 }
 
-static int dsatur_colouring(i64 n, const std::vector<i64>& np, const std::vector<i64>& nb, std::vector<i32>& colour) {
-    struct Ent { i32 sat, deg; i64 v; };
-    auto less = [](const Ent& x, const Ent& y) {  // x has lower priority than y
-        if (x.sat != y.sat) return x.sat < y.sat;
-        if (x.deg != y.deg) return x.deg < y.deg;
-        return x.v > y.v;
+// The priority order (sat, deg, lower index) is total, so which vertex is taken next does not
+// depend on the queue's layout.  Vertices with sat = 0 sit in one array sorted by priority;
+// a vertex whose sat becomes >= 1 (it then outranks every sat = 0 vertex) enters an indexed
+// max-heap, where later sat increments sift it up in place.  next(): the heap's top while the
+// heap is non-empty, else the array's next uncoloured sat = 0 vertex.  The heap holds only
+// the colouring front, each vertex once.
+static int dsatur_colouring(i64 n, const std::vector<i64>& np, const std::vector<i32>& nb, std::vector<i32>& colour) {
+    std::vector<i32> sat(n, 0);
+    auto deg = [&](i64 v) { return np[v + 1] - np[v]; };
+    auto before = [&](i64 x, i64 y) {  // x has higher priority than y
+        if (sat[x] != sat[y]) return sat[x] > sat[y];
+        if (deg(x) != deg(y)) return deg(x) > deg(y);
+        return x < y;
     };
-    std::vector<Ent> h;
-    h.reserve((size_t)(n + np[n] + 1));
-    auto push = [&](Ent e) {
-        size_t k = h.size();
-        h.push_back(e);
-        while (k > 0 && less(h[(k - 1) / 2], h[k])) { std::swap(h[k], h[(k - 1) / 2]); k = (k - 1) / 2; }
+    std::vector<i64> a((size_t)n);
+    for (i64 i = 0; i < n; ++i) a[(size_t)i] = i;
+    std::sort(a.begin(), a.end(), before);  // all sat = 0 here
+    size_t ac = 0;
+    std::vector<i64> h, pos(n, -1);
+    auto up = [&](i64 k) {
+        const i64 v = h[k];
+        while (k > 0 && before(v, h[(k - 1) / 2])) {
+            h[k] = h[(k - 1) / 2];
+            pos[h[k]] = k;
+            k = (k - 1) / 2;
+        }
+        h[k] = v;
+        pos[v] = k;
     };
     auto pop = [&]() {
-        Ent top = h[0];
-        h[0] = h.back();
+        const i64 top = h[0], v = h.back();
         h.pop_back();
-        for (size_t k = 0;;) {
-            size_t l = 2 * k + 1, r = l + 1, m = k;
-            if (l < h.size() && less(h[m], h[l])) m = l;
-            if (r < h.size() && less(h[m], h[r])) m = r;
-            if (m == k) break;
-            std::swap(h[k], h[m]);
-            k = m;
+        pos[top] = -1;
+        if (h.empty()) return top;
+        const i64 m = (i64)h.size();
+        i64 k = 0;
+        for (;;) {
+            i64 l = 2 * k + 1, r = l + 1, c = k;
+            i64 best = v;
+            if (l < m && before(h[l], best)) { c = l; best = h[l]; }
+            if (r < m && before(h[r], best)) { c = r; best = h[r]; }
+            if (c == k) break;
+            h[k] = h[c];
+            pos[h[k]] = k;
+            k = c;
         }
+        h[k] = v;
+        pos[v] = k;
         return top;
     };
     std::vector<uint64_t> bits((size_t)n * 4, 0);
-    std::vector<i32> sat(n, 0);
     colour.assign(n, -1);
-    for (i64 i = 0; i < n; ++i) push(Ent{0, (i32)(np[i + 1] - np[i]), i});
     int maxc = 0;
-    for (i64 done = 0; done < n;) {
-        const Ent top = pop();
-        const i64 v = top.v;
-        if (colour[v] >= 0 || top.sat != sat[v]) continue;  // stale entry
+    for (i64 done = 0; done < n; ++done) {
+        i64 v;
+        if (!h.empty()) {
+            v = pop();
+        } else {
+            while (colour[a[ac]] >= 0 || sat[a[ac]] != 0) ++ac;
+            v = a[ac++];
+        }
         int c = 0;
         while (c < 256 && (bits[(size_t)v * 4 + (c >> 6)] >> (c & 63) & 1ull)) ++c;
         if (c >= 256) return -1;
         colour[v] = c;
         maxc = std::max(maxc, c + 1);
-        ++done;
         for (i64 t = np[v]; t < np[v + 1]; ++t) {
             const i64 w = nb[t];
             uint64_t& word = bits[(size_t)w * 4 + (c >> 6)];
             if (colour[w] >= 0 || (word >> (c & 63) & 1ull)) continue;
             word |= 1ull << (c & 63);
             sat[w]++;
-            push(Ent{sat[w], (i32)(np[w + 1] - np[w]), w});
+            if (pos[w] < 0) {
+                h.push_back(w);
+                up((i64)h.size() - 1);
+            } else {
+                up(pos[w]);
+            }
         }
     }
     return maxc;
 }
 
+// smallest colour not used by an already coloured neighbour of i (stamp: per-caller scratch)
+static inline i32 first_free(i64 i, i64 q, const std::vector<i64>& np, const std::vector<i32>& nb,
+                             const std::vector<i32>& colour, std::vector<i64>& stamp) {
+    for (i64 t = np[i]; t < np[i + 1]; ++t) {
+        const i32 c = colour[nb[t]];
+        if (c < 0) continue;
+        if ((size_t)c >= stamp.size()) stamp.resize(2 * c + 2, -1);
+        stamp[c] = q;
+    }
+    i32 c = 0;
+    while ((size_t)c < stamp.size() && stamp[c] == q) ++c;
+    return c;
+}
+
+// Iterated-greedy passes visit the previous colour classes one after another; a class is an
+// independent set of sym(pattern), so no vertex of a class sees another of the same class,
+// and the class's vertices are coloured on threads with the result of the sequential visit.
 int greedy_colouring(const HostCSR& A, std::vector<i32>& colour, int passes) {
     const i64 n = A.nrows;
-    std::vector<i64> np, nb;  // the symmetric adjacency, built once for every pass
+    std::vector<i64> np;
+    std::vector<i32> nb;  // the symmetric adjacency, built once for every pass
     sym_adjacency(A, np, nb);
-    std::vector<i64> stamp(256, -1), order(n);
-    for (i64 i = 0; i < n; ++i) order[i] = i;
     int ncol = 0;
     // first colouring: DSATUR (or greedy in Morton order if DSATUR needs >= 256 colours;
     // passes < 0: plain greedy in Morton order only)
     const int pass0 = (passes >= 0 && (ncol = dsatur_colouring(n, np, nb, colour)) > 0) ? 1 : 0;
-    if (pass0 == 0) ncol = 0;
-    for (int pass = pass0; pass <= std::max(passes, 0); ++pass) {
-        if (pass > 0) {  // descending previous colour, ascending index within a colour
-            std::vector<i64> cnt(ncol + 1, 0);
-            for (i64 i = 0; i < n; ++i) cnt[ncol - colour[i]]++;
-            for (int c = 0; c < ncol; ++c) cnt[c + 1] += cnt[c];
-            for (i64 i = 0; i < n; ++i) order[cnt[ncol - 1 - colour[i]]++] = i;
-        }
+    if (pass0 == 0) {
         colour.assign(n, -1);
-        std::fill(stamp.begin(), stamp.end(), -1);
+        std::vector<i64> stamp(256, -1);
         ncol = 0;
-        for (i64 q = 0; q < n; ++q) {
-            const i64 i = order[q];
-            auto mark = [&](i32 j) {
-                if (j == (i32)i) return;
-                i32 c = colour[j];
-                if (c < 0) return;
-                if ((size_t)c >= stamp.size()) stamp.resize(2 * c + 2, -1);
-                stamp[c] = q;
-            };
-            for (i64 t = np[i]; t < np[i + 1]; ++t) mark((i32)nb[t]);
-            i32 c = 0;
-            while ((size_t)c < stamp.size() && stamp[c] == q) ++c;
-            colour[i] = c;
-            ncol = std::max(ncol, c + 1);
-            if ((size_t)ncol >= stamp.size()) stamp.resize(2 * ncol + 2, -1);
+        for (i64 i = 0; i < n; ++i) {
+            colour[i] = first_free(i, i, np, nb, colour, stamp);
+            ncol = std::max(ncol, colour[i] + 1);
         }
+    }
+    const int nt = col_threads();
+    std::vector<i64> order(n);
+    for (int pass = 1; pass <= std::max(passes, 0); ++pass) {
+        // descending previous colour, ascending index within a colour
+        std::vector<i64> cnt(ncol + 1, 0);
+        for (i64 i = 0; i < n; ++i) cnt[ncol - colour[i]]++;
+        for (int c = 0; c < ncol; ++c) cnt[c + 1] += cnt[c];
+        const std::vector<i64> cls(cnt.begin(), cnt.end());  // class k: order[cls[k] .. cls[k+1])
+        for (i64 i = 0; i < n; ++i) order[cnt[ncol - 1 - colour[i]]++] = i;
+        colour.assign(n, -1);
+        int nc = 0;
+        for (int k = 0; k < ncol; ++k) {
+            const i64 b0 = cls[k], len = cls[k + 1] - cls[k];
+            const int ntk = len >= 8192 ? nt : 1;
+            std::vector<int> tmax(std::max(ntk, 1), 0);
+            std::vector<std::thread> th;
+            auto run = [&](int t) {
+                std::vector<i64> stamp(256, -1);
+                int m = 0;
+                for (i64 q = b0 + len * t / ntk; q < b0 + len * (t + 1) / ntk; ++q) {
+                    const i64 i = order[q];
+                    colour[i] = first_free(i, q, np, nb, colour, stamp);
+                    m = std::max(m, colour[i] + 1);
+                }
+                tmax[t] = m;
+            };
+            if (ntk > 1) {
+                for (int t = 0; t < ntk; ++t) th.emplace_back(run, t);
+                for (auto& x : th) x.join();
+            } else {
+                run(0);
+            }
+            for (int m : tmax) nc = std::max(nc, m);
+        }
+        ncol = nc;
     }
     return ncol;
 }
