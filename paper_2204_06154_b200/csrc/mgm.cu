@@ -545,86 +545,107 @@ namespace {
 // column, and slw[s] = 1 + the largest earlier-colour count of slice s: a Gauss-Seidel sweep
 // from a zero guess reads only those first slw slots (the later-colour values are still 0).
 // lib_csr keeps the plain order (diagonal first, ascending column).
+static int host_threads() { return std::max(1, std::min(64, (int)std::thread::hardware_concurrency())); }
+
 void pack_sell(const HostCSR& A, const std::vector<i64>& row_lib2mor, const std::vector<i32>& col_mor2lib,
                bool diag_first, std::vector<i64>& sptr, std::vector<i32>& scol, std::vector<double>& sval,
                HostCSR* lib_csr, const std::vector<i32>* colour_lib = nullptr, std::vector<i32>* slw = nullptr,
                std::vector<i64>* lower_per_colour = nullptr, std::vector<uint8_t>* nlow_row = nullptr,
                std::vector<i32>* sluw = nullptr) {
-    i64 n = (i64)row_lib2mor.size();
-    i64 ns = (n + 31) / 32;
+    // slices are independent once sptr is known: both passes run on threads over slices
+    const i64 n = (i64)row_lib2mor.size();
+    const i64 ns = (n + 31) / 32;
+    const int nt = ns >= 2048 ? host_threads() : 1;
+    auto par = [&](auto&& f) {  // f(t, s0, s1) over slice ranges
+        if (nt <= 1) { f(0, (i64)0, ns); return; }
+        std::vector<std::thread> th;
+        for (int t = 0; t < nt; ++t) th.emplace_back([&, t] { f(t, ns * t / nt, ns * (t + 1) / nt); });
+        for (auto& x : th) x.join();
+    };
+    auto rlen = [&](i64 r) { return A.ptr[row_lib2mor[r] + 1] - A.ptr[row_lib2mor[r]]; };
     sptr.assign(ns + 1, 0);
-    for (i64 s = 0; s < ns; ++s) {
-        i64 w = 0;
-        for (i64 r = s * 32; r < std::min(n, s * 32 + 32); ++r) {
-            i64 mr = row_lib2mor[r];
-            w = std::max(w, A.ptr[mr + 1] - A.ptr[mr]);
+    par([&](int, i64 s0, i64 s1) {
+        for (i64 s = s0; s < s1; ++s) {
+            i64 w = 0;
+            for (i64 r = s * 32; r < std::min(n, s * 32 + 32); ++r) w = std::max(w, rlen(r));
+            sptr[s + 1] = 32 * std::max<i64>(w, 1);
         }
-        sptr[s + 1] = sptr[s] + 32 * std::max<i64>(w, 1);
-    }
-    scol.assign(sptr[ns], 0);
-    sval.assign(sptr[ns], 0.0);
+    });
+    for (i64 s = 0; s < ns; ++s) sptr[s + 1] += sptr[s];
+    scol.resize(sptr[ns]);
+    sval.resize(sptr[ns]);
     if (lib_csr) {
         lib_csr->nrows = n;
         lib_csr->ncols = (i64)col_mor2lib.size();
         lib_csr->ptr.assign(n + 1, 0);
-        lib_csr->col.clear();
-        lib_csr->val.clear();
+        for (i64 r = 0; r < n; ++r) lib_csr->ptr[r + 1] = lib_csr->ptr[r] + rlen(r);
+        lib_csr->col.resize(lib_csr->ptr[n]);
+        lib_csr->val.resize(lib_csr->ptr[n]);
     }
-    std::vector<std::pair<i32, double>> row, srow;
     if (slw) slw->assign(ns, 1);
     if (nlow_row) nlow_row->assign(n, 0);
     if (sluw) sluw->assign(ns, 1 << 30);
+    i32 nc = 0;
     if (lower_per_colour && colour_lib) {
-        i32 nc = 0;
         for (i32 c : *colour_lib) nc = std::max(nc, c + 1);
         lower_per_colour->assign(nc, 0);
     }
-    for (i64 r = 0; r < n; ++r) {
-        i64 mr = row_lib2mor[r];
-        row.clear();
-        if (diag_first)
-            for (i64 t = A.ptr[mr]; t < A.ptr[mr + 1]; ++t)
-                if (A.col[t] == (i32)mr) row.push_back({A.col[t], A.val[t]});
-        for (i64 t = A.ptr[mr]; t < A.ptr[mr + 1]; ++t)
-            if (!diag_first || A.col[t] != (i32)mr) row.push_back({A.col[t], A.val[t]});
-        i64 s = r / 32, lane = r % 32;
-        i64 w = (sptr[s + 1] - sptr[s]) / 32;
-        srow = row;
-        if (colour_lib && diag_first && !row.empty()) {  // [diag | earlier colours | later colours]
-            const i32 cr = (*colour_lib)[r];
-            i64 o = 1;
-            for (size_t k = 1; k < row.size(); ++k)
-                if ((*colour_lib)[col_mor2lib[row[k].first]] < cr) srow[o++] = row[k];
-            const i64 nlow = o - 1;
-            for (size_t k = 1; k < row.size(); ++k)
-                if ((*colour_lib)[col_mor2lib[row[k].first]] >= cr) srow[o++] = row[k];
-            if (slw) (*slw)[s] = std::max<i32>((*slw)[s], (i32)(1 + nlow));
-            if (nlow_row) (*nlow_row)[r] = (uint8_t)std::min<i64>(nlow, 255);
-            if (sluw) (*sluw)[s] = std::min<i32>((*sluw)[s], (i32)(1 + nlow));
-            if (lower_per_colour) (*lower_per_colour)[cr] += 1 + nlow;
-        }
-        for (i64 k = 0; k < w; ++k) {
-            i64 o = sptr[s] + 32 * k + lane;
-            if (k < (i64)srow.size()) {
-                scol[o] = col_mor2lib[srow[k].first];
-                sval[o] = srow[k].second;
-            } else {
-                scol[o] = diag_first ? (i32)r : (row.empty() ? 0 : col_mor2lib[row[0].first]);
-                sval[o] = 0.0;
+    std::vector<std::vector<i64>> lpc(nt, std::vector<i64>(nc, 0));
+    par([&](int t, i64 s0, i64 s1) {
+        std::vector<std::pair<i32, double>> row, srow;
+        for (i64 r = s0 * 32; r < std::min(n, s1 * 32); ++r) {
+            i64 mr = row_lib2mor[r];
+            row.clear();
+            if (diag_first)
+                for (i64 q = A.ptr[mr]; q < A.ptr[mr + 1]; ++q)
+                    if (A.col[q] == (i32)mr) row.push_back({A.col[q], A.val[q]});
+            for (i64 q = A.ptr[mr]; q < A.ptr[mr + 1]; ++q)
+                if (!diag_first || A.col[q] != (i32)mr) row.push_back({A.col[q], A.val[q]});
+            i64 s = r / 32, lane = r % 32;
+            i64 w = (sptr[s + 1] - sptr[s]) / 32;
+            srow = row;
+            if (colour_lib && diag_first && !row.empty()) {  // [diag | earlier colours | later colours]
+                const i32 cr = (*colour_lib)[r];
+                i64 o = 1;
+                for (size_t k = 1; k < row.size(); ++k)
+                    if ((*colour_lib)[col_mor2lib[row[k].first]] < cr) srow[o++] = row[k];
+                const i64 nlow = o - 1;
+                for (size_t k = 1; k < row.size(); ++k)
+                    if ((*colour_lib)[col_mor2lib[row[k].first]] >= cr) srow[o++] = row[k];
+                if (slw) (*slw)[s] = std::max<i32>((*slw)[s], (i32)(1 + nlow));
+                if (nlow_row) (*nlow_row)[r] = (uint8_t)std::min<i64>(nlow, 255);
+                if (sluw) (*sluw)[s] = std::min<i32>((*sluw)[s], (i32)(1 + nlow));
+                if (lower_per_colour) lpc[t][cr] += 1 + nlow;
+            }
+            for (i64 k = 0; k < w; ++k) {
+                i64 o = sptr[s] + 32 * k + lane;
+                if (k < (i64)srow.size()) {
+                    scol[o] = col_mor2lib[srow[k].first];
+                    sval[o] = srow[k].second;
+                } else {
+                    scol[o] = diag_first ? (i32)r : (row.empty() ? 0 : col_mor2lib[row[0].first]);
+                    sval[o] = 0.0;
+                }
+            }
+            if (lib_csr) {
+                i64 o = lib_csr->ptr[r];
+                for (auto& e : row) {
+                    lib_csr->col[o] = col_mor2lib[e.first];
+                    lib_csr->val[o++] = e.second;
+                }
             }
         }
-        if (lib_csr) {
-            for (auto& e : row) {
-                lib_csr->col.push_back(col_mor2lib[e.first]);
-                lib_csr->val.push_back(e.second);
-            }
-            lib_csr->ptr[r + 1] = (i64)lib_csr->col.size();
-        }
-    }
+    });
+    if (lower_per_colour && colour_lib)
+        for (int t = 0; t < nt; ++t)
+            for (i32 c = 0; c < nc; ++c) (*lower_per_colour)[c] += lpc[t][c];
     // padded slice rows beyond n point at row 0
     for (i64 r = n; r < ns * 32; ++r) {
         i64 s = r / 32, lane = r % 32;
-        for (i64 k = 0; k < (sptr[s + 1] - sptr[s]) / 32; ++k) scol[sptr[s] + 32 * k + lane] = 0;
+        for (i64 k = 0; k < (sptr[s + 1] - sptr[s]) / 32; ++k) {
+            scol[sptr[s] + 32 * k + lane] = 0;
+            sval[sptr[s] + 32 * k + lane] = 0.0;
+        }
     }
 }
 
@@ -1229,23 +1250,35 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
             L.P_lib.nrows = n;
             L.P_lib.ncols = Lm[j + 1].nrows;
             L.P_lib.ptr.assign(n + 1, 0);
-            for (i64 r = 0; r < n; ++r) {
-                i64 mr = lib2mor[j][r];
-                i64 a = P.ptr[mr], cnt = P.ptr[mr + 1] - a;
-                for (int k = 0; k < m; ++k) {
-                    if (k < cnt) {
-                        pcol[(size_t)k * n + r] = mor2lib[j + 1][P.col[a + k]];
-                        pval[(size_t)k * n + r] = P.val[a + k];
-                    } else {
-                        pcol[(size_t)k * n + r] = mor2lib[j + 1][P.col[a]];
-                        pval[(size_t)k * n + r] = 0.0;
+            for (i64 r = 0; r < n; ++r)
+                L.P_lib.ptr[r + 1] = L.P_lib.ptr[r] + P.ptr[lib2mor[j][r] + 1] - P.ptr[lib2mor[j][r]];
+            L.P_lib.col.resize(L.P_lib.ptr[n]);
+            L.P_lib.val.resize(L.P_lib.ptr[n]);
+            auto prow = [&](i64 r0, i64 r1) {
+                for (i64 r = r0; r < r1; ++r) {
+                    i64 mr = lib2mor[j][r];
+                    i64 a = P.ptr[mr], cnt = P.ptr[mr + 1] - a;
+                    for (int k = 0; k < m; ++k) {
+                        if (k < cnt) {
+                            pcol[(size_t)k * n + r] = mor2lib[j + 1][P.col[a + k]];
+                            pval[(size_t)k * n + r] = P.val[a + k];
+                        } else {
+                            pcol[(size_t)k * n + r] = mor2lib[j + 1][P.col[a]];
+                            pval[(size_t)k * n + r] = 0.0;
+                        }
+                    }
+                    for (i64 k = 0; k < cnt; ++k) {
+                        L.P_lib.col[L.P_lib.ptr[r] + k] = mor2lib[j + 1][P.col[a + k]];
+                        L.P_lib.val[L.P_lib.ptr[r] + k] = P.val[a + k];
                     }
                 }
-                for (i64 k = 0; k < cnt; ++k) {
-                    L.P_lib.col.push_back(mor2lib[j + 1][P.col[a + k]]);
-                    L.P_lib.val.push_back(P.val[a + k]);
-                }
-                L.P_lib.ptr[r + 1] = (i64)L.P_lib.col.size();
+            };
+            {
+                const int nt = n >= 65536 ? host_threads() : 1;
+                std::vector<std::thread> th;
+                for (int t = 1; t < nt; ++t) th.emplace_back(prow, n * t / nt, n * (t + 1) / nt);
+                prow(0, nt > 1 ? n / nt : n);
+                for (auto& x : th) x.join();
             }
             if ((s = upload(ctx, &L.pcol, pcol)) || (s = upload(ctx, &L.pval, pval))) return s;
             HostCSR R = transpose(P);
