@@ -247,116 +247,250 @@ i64 nearest_other(const double* pts, i64 n, std::vector<double>& nn2, int nthrea
 // One elimination pass with weight radius R; false if it would have to eliminate a point of
 // zero weight (no live neighbour within R: index ties would then decide and wipe out the
 // lowest-index region), in which case the caller enlarges R.
+// Neighbours within R on a hashed grid of cells of side >= 2R (only occupied cells stored):
+// points sorted by cell key (LSD radix), cell key -> run of points by open addressing.  The
+// neighbour set {j != i : d(i, j) < R} does not depend on the grid, and the weights are
+// integers, so neither does anything below.
+struct CellHash {
+    double lo[3], cell;
+    i64 dims[3];
+    std::vector<uint64_t> key;  // sorted occupied cell keys
+    std::vector<i64> start;     // run of cell q: items[start[q] .. start[q+1])
+    std::vector<i32> items;
+    std::vector<i64> slot;      // open addressing: index into key, -1 empty
+    uint64_t mask;
+    static uint64_t mix(uint64_t k) {
+        k ^= k >> 33; k *= 0xff51afd7ed558ccdull; k ^= k >> 33; k *= 0xc4ceb9fe1a85ec53ull; k ^= k >> 33;
+        return k;
+    }
+    void coords(const double* x, i64* c) const {
+        for (int a = 0; a < 3; ++a) {
+            i64 v = (i64)std::floor((x[a] - lo[a]) / cell);
+            c[a] = std::min<i64>(std::max<i64>(v, 0), dims[a] - 1);
+        }
+    }
+    void build(const double* p, i64 n, double R) {
+        double hi[3];
+        for (int a = 0; a < 3; ++a) lo[a] = hi[a] = p[a];
+        for (i64 i = 0; i < n; ++i)
+            for (int a = 0; a < 3; ++a) {
+                lo[a] = std::min(lo[a], p[3 * i + a]);
+                hi[a] = std::max(hi[a], p[3 * i + a]);
+            }
+        cell = R > 0 ? 2.0 * R * (1.0 + 1e-6) : 1.0;
+        for (;;) {  // cells only grow (any side >= R is correct); keep keys below 2^60
+            double tot = 1.0;
+            for (int a = 0; a < 3; ++a) tot *= std::floor((hi[a] - lo[a]) / cell) + 1.0;
+            if (tot < 1e18) break;
+            cell *= 2.0;
+        }
+        for (int a = 0; a < 3; ++a) dims[a] = (i64)std::floor((hi[a] - lo[a]) / cell) + 1;
+        std::vector<uint64_t> k0(n), k1(n);
+        std::vector<i32> i0(n), i1(n);
+        uint64_t kmax = 0;
+        for (i64 i = 0; i < n; ++i) {
+            i64 c[3];
+            coords(p + 3 * i, c);
+            k0[i] = (uint64_t)((c[2] * dims[1] + c[1]) * dims[0] + c[0]);
+            i0[i] = (i32)i;
+            kmax = std::max(kmax, k0[i]);
+        }
+        for (int sh = 0; sh < 64 && (kmax >> sh) != 0; sh += 16) {  // stable LSD radix, 16-bit digits
+            std::vector<i64> cnt(65537, 0);
+            for (i64 i = 0; i < n; ++i) cnt[((k0[i] >> sh) & 0xffff) + 1]++;
+            for (int d = 0; d < 65536; ++d) cnt[d + 1] += cnt[d];
+            for (i64 i = 0; i < n; ++i) {
+                const i64 o = cnt[(k0[i] >> sh) & 0xffff]++;
+                k1[o] = k0[i];
+                i1[o] = i0[i];
+            }
+            k0.swap(k1);
+            i0.swap(i1);
+        }
+        items = std::move(i0);
+        key.clear();
+        start.clear();
+        for (i64 i = 0; i < n; ++i)
+            if (i == 0 || k0[i] != k0[i - 1]) {
+                key.push_back(k0[i]);
+                start.push_back(i);
+            }
+        start.push_back(n);
+        uint64_t cap = 16;
+        while (cap < 2 * key.size()) cap <<= 1;
+        mask = cap - 1;
+        slot.assign(cap, -1);
+        for (size_t q = 0; q < key.size(); ++q) {
+            uint64_t h = mix(key[q]) & mask;
+            while (slot[h] >= 0) h = (h + 1) & mask;
+            slot[h] = (i64)q;
+        }
+    }
+    i64 find(uint64_t k) const {  // index into key, or -1
+        for (uint64_t h = mix(k) & mask;; h = (h + 1) & mask) {
+            const i64 q = slot[h];
+            if (q < 0) return -1;
+            if (key[q] == k) return q;
+        }
+    }
+    template <class F>
+    void near(const double* x, F&& f) const {
+        // cell side >= 2R (1 + 1e-6): the ball of radius R around x lies in x's cell and, per
+        // axis, the neighbour on the side of the nearer face -- a 2 x 2 x 2 block
+        i64 c[3], o[3];
+        coords(x, c);
+        for (int a = 0; a < 3; ++a) {
+            const double f = (x[a] - lo[a]) - (double)c[a] * cell;
+            o[a] = f < 0.5 * cell ? c[a] - 1 : c[a] + 1;
+        }
+        for (int m = 0; m < 8; ++m) {
+            const i64 zz = (m & 4) ? o[2] : c[2], yy = (m & 2) ? o[1] : c[1], xx = (m & 1) ? o[0] : c[0];
+            if (zz < 0 || zz >= dims[2] || yy < 0 || yy >= dims[1] || xx < 0 || xx >= dims[0]) continue;
+            const i64 q = find((uint64_t)((zz * dims[1] + yy) * dims[0] + xx));
+            if (q < 0) continue;
+            for (i64 t = start[q]; t < start[q + 1]; ++t) f(items[t]);
+        }
+    }
+};
+
+// One elimination pass with weight radius R; false if it would have to eliminate a point of
+// zero weight (no live neighbour within R: index ties would then decide and wipe out the
+// lowest-index region), in which case the caller enlarges R.
 static bool wse_pass(const double* pts, i64 n, i64 nt, double R, std::vector<i64>& keep, int nthreads) {
     keep.clear();
-    Grid g;
-    g.build(pts, n, std::max(R, default_cell(pts, n, 8)));
-    // neighbour lists per thread chunk, then concatenated (CSR)
-    int nt_threads = std::max(1, nthreads);
-    std::vector<std::vector<i32>> nj(nt_threads);
+    CellHash g;
+    g.build(pts, n, R);
     using wse_w = i64;  // O8: fixed-point weights, 2^40 per unit
-    std::vector<std::vector<wse_w>> nw(nt_threads);
-    std::vector<i64> cnt(n, 0);
-    i64 chunk = (n + nt_threads - 1) / nt_threads;
-    std::vector<std::thread> th;
-    for (int t = 0; t < nt_threads; ++t) {
-        i64 b = t * chunk, e = std::min(n, b + chunk);
-        if (b >= e) break;
-        th.emplace_back([&, t, b, e] {
-            for (i64 i = b; i < e; ++i) {
-                i64 c[3];
-                g.coords(pts + 3 * i, c);
-                for (i64 z = c[2] - 1; z <= c[2] + 1; ++z) {
-                    if (z < 0 || z >= g.dims[2]) continue;
-                    for (i64 y = c[1] - 1; y <= c[1] + 1; ++y) {
-                        if (y < 0 || y >= g.dims[1]) continue;
-                        for (i64 x = c[0] - 1; x <= c[0] + 1; ++x) {
-                            if (x < 0 || x >= g.dims[0]) continue;
-                            i64 cell = (z * g.dims[1] + y) * g.dims[0] + x;
-                            for (i64 q = g.start[cell]; q < g.start[cell + 1]; ++q) {
-                                i32 j = g.items[q];
-                                if (j == (i32)i) continue;
-                                double d = std::sqrt(dist2(pts + 3 * i, pts + 3 * (i64)j));
-                                if (!(d < R)) continue;
-                                double u = 1.0 - d / R;
-                                double u2 = u * u;
-                                double u4 = u2 * u2;
-                                double u8 = u4 * u4;
-                                wse_w W = (wse_w)std::floor(u8 * 1099511627776.0 + 0.5);  // 2^40
-                                nj[t].push_back(j);
-                                nw[t].push_back(W);
-                                cnt[i]++;
-                            }
-                        }
-                    }
-                }
-            }
-        });
-    }
-    for (auto& x : th) x.join();
+    // neighbour CSR: per-thread lists over contiguous point ranges, then concatenated
+    const int T = n >= 4096 ? std::max(1, nthreads) : 1;
+    const double R2far = R * R * (1.0 + 1e-6);
+    std::vector<std::vector<i32>> nj(T);
+    std::vector<std::vector<wse_w>> nw(T);
     std::vector<i64> ptr(n + 1, 0);
-    for (i64 i = 0; i < n; ++i) ptr[i + 1] = ptr[i] + cnt[i];
+    {
+        std::vector<std::thread> th;
+        for (int t = 0; t < T; ++t)
+            th.emplace_back([&, t] {
+                for (i64 i = n * t / T; i < n * (t + 1) / T; ++i) {
+                    const size_t c0 = nj[t].size();
+                    g.near(pts + 3 * i, [&](i32 j) {
+                        if (j == (i32)i) return;
+                        const double d2 = dist2(pts + 3 * i, pts + 3 * (i64)j);
+                        if (d2 > R2far) return;  // sqrt(d2) > R for certain
+                        double d = std::sqrt(d2);
+                        if (!(d < R)) return;
+                        double u = 1.0 - d / R;
+                        double u2 = u * u;
+                        double u4 = u2 * u2;
+                        double u8 = u4 * u4;
+                        nj[t].push_back(j);
+                        nw[t].push_back((wse_w)std::floor(u8 * 1099511627776.0 + 0.5));  // 2^40
+                    });
+                    ptr[i + 1] = (i64)(nj[t].size() - c0);
+                }
+            });
+        for (auto& x : th) x.join();
+    }
+    for (i64 i = 0; i < n; ++i) ptr[i + 1] += ptr[i];
     std::vector<i32> adj(ptr[n]);
     std::vector<wse_w> adjw(ptr[n]);
     {
-        i64 o = 0;
-        for (int t = 0; t < (int)nj.size(); ++t) {
-            std::copy(nj[t].begin(), nj[t].end(), adj.begin() + o);
-            std::copy(nw[t].begin(), nw[t].end(), adjw.begin() + o);
-            o += (i64)nj[t].size();
-        }
+        std::vector<std::thread> th;
+        for (int t = 0; t < T; ++t)
+            th.emplace_back([&, t] {
+                const i64 o = ptr[n * t / T];
+                std::copy(nj[t].begin(), nj[t].end(), adj.begin() + o);
+                std::copy(nw[t].begin(), nw[t].end(), adjw.begin() + o);
+            });
+        for (auto& x : th) x.join();
     }
     std::vector<wse_w> weight(n, 0);
     for (i64 i = 0; i < n; ++i)
         for (i64 t = ptr[i]; t < ptr[i + 1]; ++t) weight[i] += adjw[t];
 
-    // indexed max-heap: priority (weight desc, index asc)
-    std::vector<i32> heap(n), pos(n);
-    auto higher = [&](i32 a, i32 b) {
-        return weight[a] > weight[b] || (weight[a] == weight[b] && a < b);
-    };
-    for (i64 i = 0; i < n; ++i) { heap[i] = (i32)i; pos[i] = (i32)i; }
-    i64 hs = n;
-    auto sift_down = [&](i64 p) {
-        for (;;) {
-            i64 l = 2 * p + 1, r = l + 1, best = p;
-            if (l < hs && higher(heap[l], heap[best])) best = l;
-            if (r < hs && higher(heap[r], heap[best])) best = r;
-            if (best == p) return;
-            std::swap(heap[p], heap[best]);
-            pos[heap[p]] = (i32)p;
-            pos[heap[best]] = (i32)best;
-            p = best;
-        }
-    };
-    auto sift_up = [&](i64 p) {
-        while (p > 0) {
-            i64 q = (p - 1) / 2;
-            if (!higher(heap[p], heap[q])) return;
-            std::swap(heap[p], heap[q]);
-            pos[heap[p]] = (i32)p;
-            pos[heap[q]] = (i32)q;
-            p = q;
-        }
-    };
-    for (i64 p = n / 2 - 1; p >= 0; --p) sift_down(p);
+    // The elimination takes the live point of highest priority (weight desc, index asc) and
+    // lowers its live neighbours' weights.  The popped priorities are strictly decreasing (the
+    // top never rises: every other weight only falls), so the points eliminated are the
+    // n - nt of highest priority at their pop, and a point whose priority beats every live
+    // neighbour's pops with exactly that priority (no neighbour can pop before it).  So all
+    // such local maxima are popped together, round after round (integer weights: the
+    // neighbour updates commute), until no live point has positive weight; then the n - nt
+    // highest pop priorities are selected.  The pass is degenerate (false) exactly when the
+    // sequential loop would have met a zero-weight top: fewer than n - nt positive pops.
+    const i64 ne = n - nt;
     std::vector<uint8_t> dead(n, 0);
-    for (i64 it = 0; it < n - nt; ++it) {
-        i32 a = heap[0];
-        if (weight[a] == 0) return false;  // degenerate: R too small for this cloud (O8)
-        dead[a] = 1;
-        heap[0] = heap[hs - 1];
-        pos[heap[0]] = 0;
-        --hs;
-        if (hs > 0) sift_down(0);
-        for (i64 t = ptr[a]; t < ptr[a + 1]; ++t) {
-            i32 j = adj[t];
-            if (dead[j]) continue;
-            weight[j] -= adjw[t];
-            sift_down(pos[j]);
-            (void)sift_up;
-        }
+    std::vector<i64> stamp(n, -1);  // round in which a point was last queued
+    std::vector<i32> cand;
+    cand.reserve(n);
+    for (i64 i = 0; i < n; ++i)
+        if (weight[i] > 0) cand.push_back((i32)i);
+    struct Pop { wse_w w; i32 v; };
+    std::vector<Pop> pops;
+    pops.reserve(n);
+    const int NT = std::max(1, nthreads);
+    auto run = [&](i64 m, auto&& f) {  // f(t, b, e) over [0, m)
+        const int k = m >= 16384 ? NT : 1;
+        if (k == 1) { f(0, (i64)0, m); return; }
+        std::vector<std::thread> th;
+        for (int t = 0; t < k; ++t) th.emplace_back([&, t] { f(t, m * t / k, m * (t + 1) / k); });
+        for (auto& x : th) x.join();
+    };
+    std::vector<std::vector<i32>> tl(NT);
+    for (i64 round = 0; !cand.empty(); ++round) {
+        // 1. local maxima among the candidates (read-only)
+        for (auto& v : tl) v.clear();
+        run((i64)cand.size(), [&](int t, i64 b, i64 e) {
+            for (i64 q = b; q < e; ++q) {
+                const i32 x = cand[q];
+                const wse_w wx = weight[x];
+                if (dead[x] || wx <= 0) continue;
+                bool top = true;
+                for (i64 r = ptr[x]; r < ptr[x + 1] && top; ++r) {
+                    const i32 y = adj[r];
+                    if (!dead[y] && (weight[y] > wx || (weight[y] == wx && y < x))) top = false;
+                }
+                if (top) tl[t].push_back(x);
+            }
+        });
+        const size_t p0 = pops.size();
+        for (auto& v : tl)
+            for (i32 x : v) pops.push_back(Pop{weight[x], x});
+        const i64 np_ = (i64)(pops.size() - p0);
+        // 2. pop them, 3. lower their live neighbours' weights (exact integer updates)
+        for (size_t q = p0; q < pops.size(); ++q) dead[pops[q].v] = 1;
+        run(np_, [&](int, i64 b, i64 e) {
+            for (i64 q = b; q < e; ++q) {
+                const i32 x = pops[p0 + q].v;
+                for (i64 r = ptr[x]; r < ptr[x + 1]; ++r)
+                    if (!dead[adj[r]]) __atomic_fetch_sub(&weight[adj[r]], adjw[r], __ATOMIC_RELAXED);
+            }
+        });
+        // 4. next candidates: live points within two hops of a popped point (only their
+        //    neighbourhoods changed)
+        for (auto& v : tl) v.clear();
+        run(np_, [&](int t, i64 b, i64 e) {
+            auto queue = [&](i32 y) {
+                if (!dead[y] && __atomic_exchange_n(&stamp[y], round, __ATOMIC_RELAXED) != round) tl[t].push_back(y);
+            };
+            for (i64 q = b; q < e; ++q) {
+                const i32 x = pops[p0 + q].v;
+                for (i64 r = ptr[x]; r < ptr[x + 1]; ++r) {
+                    const i32 y = adj[r];
+                    if (dead[y]) continue;
+                    queue(y);
+                    for (i64 r2 = ptr[y]; r2 < ptr[y + 1]; ++r2) queue(adj[r2]);
+                }
+            }
+        });
+        cand.clear();
+        for (auto& v : tl) cand.insert(cand.end(), v.begin(), v.end());
     }
+    if ((i64)pops.size() < ne) return false;  // degenerate: R too small for this cloud (O8)
+    std::nth_element(pops.begin(), pops.begin() + (ne - 1), pops.end(), [](const Pop& x, const Pop& y) {
+        return x.w > y.w || (x.w == y.w && x.v < y.v);
+    });
+    std::fill(dead.begin(), dead.end(), 0);
+    for (i64 q = 0; q < ne; ++q) dead[pops[q].v] = 1;
     keep.reserve(nt);
     for (i64 i = 0; i < n; ++i)
         if (!dead[i]) keep.push_back(i);

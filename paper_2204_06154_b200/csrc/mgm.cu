@@ -1023,11 +1023,20 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
     // export copy of weights in original order
     ctx->w_orig.assign((size_t)N * ns, 0.0);
     ctx->sten_orig.assign((size_t)N * ns, 0);
-    for (i64 k = 0; k < N; ++k)
-        for (int j = 0; j < ns; ++j) {
-            ctx->w_orig[perm[k] * ns + j] = W[k * ns + j];
-            ctx->sten_orig[perm[k] * ns + j] = perm[sten[k * ns + j]];
-        }
+    {  // row k goes to row perm[k]: distinct rows, threads over k
+        auto cp = [&](i64 k0, i64 k1) {
+            for (i64 k = k0; k < k1; ++k)
+                for (int j = 0; j < ns; ++j) {
+                    ctx->w_orig[perm[k] * ns + j] = W[k * ns + j];
+                    ctx->sten_orig[perm[k] * ns + j] = perm[sten[k * ns + j]];
+                }
+        };
+        const int nt = N >= 65536 ? host_threads() : 1;
+        std::vector<std::thread> th;
+        for (int t = 1; t < nt; ++t) th.emplace_back(cp, N * t / nt, N * (t + 1) / nt);
+        cp(0, N / nt);
+        for (auto& x : th) x.join();
+    }
     // ---- L_1, Morton order CSR with ascending columns
     std::vector<HostCSR> Lm(p), Pm(p);
     {
