@@ -63,7 +63,25 @@ bool morton_order(const double* pts, i64 n, std::vector<i64>& perm) {
         }
         keys[i] = {(spread3(q[0]) << 2) | (spread3(q[1]) << 1) | spread3(q[2]), i};
     }
-    std::sort(keys.begin(), keys.end());
+    {  // chunks sorted on threads, then merged pairwise (keys are distinct: same order)
+        const int T = n >= (1 << 18) ? std::max(1, std::min(16, (int)std::thread::hardware_concurrency())) : 1;
+        std::vector<i64> b(T + 1);
+        for (int t = 0; t <= T; ++t) b[t] = n * t / T;
+        std::vector<std::thread> th;
+        for (int t = 0; t < T; ++t) th.emplace_back([&, t] { std::sort(keys.begin() + b[t], keys.begin() + b[t + 1]); });
+        for (auto& x : th) x.join();
+        std::vector<std::pair<uint64_t, i64>> tmp(T > 1 ? n : 0);
+        for (int w = 1; w < T; w *= 2) {
+            th.clear();
+            for (int t = 0; t < T; t += 2 * w)
+                th.emplace_back([&, t] {
+                    const i64 lo = b[t], mid = b[std::min(T, t + w)], hi = b[std::min(T, t + 2 * w)];
+                    std::merge(keys.begin() + lo, keys.begin() + mid, keys.begin() + mid, keys.begin() + hi, tmp.begin() + lo);
+                });
+            for (auto& x : th) x.join();
+            keys.swap(tmp);
+        }
+    }
     perm.resize(n);
     for (i64 i = 0; i < n; ++i) perm[i] = keys[i].second;
     return true;
@@ -178,6 +196,13 @@ void knn_grid(const double* pts, i64 n, const double* qry, i64 nq, int k, std::v
     out.assign((size_t)nq * k, -1);
     Grid g;
     g.build(pts, n, default_cell(pts, n, k));
+    {  // surface clouds fill few cells of the box: shrink the cells towards ~k/2 points per
+       // occupied cell (the result does not depend on the cell size)
+        i64 occ = 0;
+        for (size_t c = 0; c + 1 < g.start.size(); ++c) occ += g.start[c + 1] > g.start[c];
+        const double per = (double)n / (double)std::max<i64>(occ, 1);
+        if (per > 2.0 * k) g.build(pts, n, g.cell * std::sqrt(0.5 * k / per));
+    }
     parallel_for(nq, nthreads, [&](i64 b, i64 e) {
         std::vector<double> bd(k);
         std::vector<i32> bj(k);

@@ -1121,16 +1121,27 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
         P.nrows = nf;
         P.ncols = ncs;
         P.ptr.assign(nf + 1, 0);
-        std::vector<int> ord(m);
-        for (i64 i = 0; i < nf; ++i) {
-            int c = pc[i];
-            for (int t = 0; t < c; ++t) ord[t] = t;
-            std::sort(ord.begin(), ord.begin() + c, [&](int a, int b) { return ist[i * m + a] < ist[i * m + b]; });
-            for (int t = 0; t < c; ++t) {
-                P.col.push_back(ist[i * m + ord[t]]);
-                P.val.push_back(Pw[i * m + ord[t]]);
-            }
-            P.ptr[i + 1] = (i64)P.col.size();
+        for (i64 i = 0; i < nf; ++i) P.ptr[i + 1] = P.ptr[i] + pc[i];
+        P.col.resize(P.ptr[nf]);
+        P.val.resize(P.ptr[nf]);
+        {  // rows sorted by column, independent: threads over rows
+            auto rows = [&](i64 r0, i64 r1) {
+                std::vector<int> ord(m);
+                for (i64 i = r0; i < r1; ++i) {
+                    int c = pc[i];
+                    for (int t = 0; t < c; ++t) ord[t] = t;
+                    std::sort(ord.begin(), ord.begin() + c, [&](int a, int b) { return ist[i * m + a] < ist[i * m + b]; });
+                    for (int t = 0; t < c; ++t) {
+                        P.col[P.ptr[i] + t] = ist[i * m + ord[t]];
+                        P.val[P.ptr[i] + t] = Pw[i * m + ord[t]];
+                    }
+                }
+            };
+            const int nt = nf >= 65536 ? host_threads() : 1;
+            std::vector<std::thread> th;
+            for (int t = 1; t < nt; ++t) th.emplace_back(rows, nf * t / nt, nf * (t + 1) / nt);
+            rows(0, nf / nt);
+            for (auto& x : th) x.join();
         }
         tm.mark("interp weights", j);
         HostCSR R = transpose(P);  // P:370, exact
