@@ -363,8 +363,11 @@ struct mgm_ctx {
     // level-0 permutation (lib row -> original index)
     i32* d_lib2orig = nullptr;
     // fine weights (export)
-    std::vector<double> w_orig;
-    std::vector<i64> sten_orig;
+    // fine-level weights and stencils in Morton order, exported in original order on demand
+    std::vector<double> w_mor;
+    std::vector<i32> sten_mor;
+    std::vector<i64> perm0;
+    int ns0 = 0;
     // streams / graph
     cudaStream_t st = nullptr;
     cudaGraphExec_t vgraph = nullptr;
@@ -1021,24 +1024,26 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
                     perm[hfail]);
     tm.mark("fine weights (GPU)");
     // export copy of weights in original order
-    ctx->w_orig.assign((size_t)N * ns, 0.0);
-    ctx->sten_orig.assign((size_t)N * ns, 0);
-    {  // row k goes to row perm[k]: distinct rows, threads over k
-        auto cp = [&](i64 k0, i64 k1) {
-            for (i64 k = k0; k < k1; ++k)
-                for (int j = 0; j < ns; ++j) {
-                    ctx->w_orig[perm[k] * ns + j] = W[k * ns + j];
-                    ctx->sten_orig[perm[k] * ns + j] = perm[sten[k * ns + j]];
-                }
-        };
-        const int nt = N >= 65536 ? host_threads() : 1;
-        std::vector<std::thread> th;
-        for (int t = 1; t < nt; ++t) th.emplace_back(cp, N * t / nt, N * (t + 1) / nt);
-        cp(0, N / nt);
-        for (auto& x : th) x.join();
-    }
     // ---- L_1, Morton order CSR with ascending columns
     std::vector<HostCSR> Lm(p), Pm(p);
+    // colourings (O11) run on background threads, each started as soon as its level's
+    // operator is final (L_1 after assembly, L_{j+1} after its Galerkin product), so they
+    // overlap the rest of the level loop; joined before the lib orders are built (and on
+    // every early return)
+    std::vector<std::vector<i32>> colour_mor(p);
+    std::vector<int> ncol_j(p, 0);
+    struct Joiner {
+        std::vector<std::thread> th;
+        ~Joiner() { join(); }
+        void join() {
+            for (auto& t : th)
+                if (t.joinable()) t.join();
+        }
+    } colour_th;
+    auto start_colouring = [&](int j) {
+        if (j + 1 < p)
+            colour_th.th.emplace_back([&, j] { ncol_j[j] = greedy_colouring(Lm[j], colour_mor[j], colour_passes()); });
+    };
     {
         HostCSR& A = Lm[0];
         A.nrows = A.ncols = N;
@@ -1068,6 +1073,11 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
         for (auto& t : th) t.join();
         A.ptr[N] = N * ns;
     }
+    start_colouring(0);
+    ctx->w_mor = std::move(W);
+    ctx->sten_mor = std::move(sten);
+    ctx->perm0 = perm;
+    ctx->ns0 = ns;
     tm.mark("assemble L1");
     // ---- level loop (Alg. 2 lines 5-12)
     std::vector<std::vector<double>> Xl(p);
@@ -1158,6 +1168,7 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
         free_dev_csr(dR);
         free_dev_csr(dLP);
         free_dev_csr(dC);
+        start_colouring(j + 1);
         tm.mark("Galerkin RAP", j);
     }
     dev_free(dXf);
@@ -1166,15 +1177,8 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
     ctx->lv.assign(p, Level());
     std::vector<std::vector<i64>> lib2mor(p);
     std::vector<std::vector<i32>> mor2lib(p);
-    std::vector<std::vector<i32>> colour_mor(p);
-    {  // the levels' colourings are independent: one thread per level
-        std::vector<std::thread> th;
-        std::vector<int> nc(p, 0);
-        for (int j = 0; j + 1 < p; ++j)
-            th.emplace_back([&, j] { nc[j] = greedy_colouring(Lm[j], colour_mor[j], colour_passes()); });
-        for (auto& t : th) t.join();
-        for (int j = 0; j + 1 < p; ++j) ctx->lv[j].ncol = nc[j];
-    }
+    colour_th.join();
+    for (int j = 0; j + 1 < p; ++j) ctx->lv[j].ncol = ncol_j[j];
     for (int j = 0; j < p; ++j) {
         Level& L = ctx->lv[j];
         i64 n = Lm[j].nrows;
@@ -1260,6 +1264,7 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
         }
         if ((s = upload(ctx, &L.sptr, sptr)) || (s = upload(ctx, &L.scol, scol)) || (s = upload(ctx, &L.sval, sval))) return s;
         L.h_sptr = sptr;
+        tm.mark("pack L (SELL)", j);
         if (j + 1 < p) {
             const HostCSR& P = Pm[j];
             const int m = lp.interp_m;
@@ -1301,6 +1306,7 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
                 for (auto& x : th) x.join();
             }
             if ((s = upload(ctx, &L.pcol, pcol)) || (s = upload(ctx, &L.pval, pval))) return s;
+            tm.mark("pack P", j);
             HostCSR R = transpose(P);
             std::vector<i64> rptr;
             std::vector<i32> rcol;
@@ -1329,6 +1335,7 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
             L.h_rptr = rptr;
             if ((s = upload(ctx, &L.rptr, rptr)) || (s = upload(ctx, &L.rcol, rcol)) || (s = upload(ctx, &L.rval, rval)))
                 return s;
+            tm.mark("pack R", j);
         }
         i64 vn = n + (ctx->poisson ? 1 : 0);
         CK(dalloc(&L.u, vn));
@@ -1338,7 +1345,7 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
         CK(cudaMemsetAsync(L.f, 0, sizeof(double) * vn, st));
         CK(cudaMemsetAsync(L.t, 0, sizeof(double) * vn, st));
     }
-    tm.mark("pack + upload");
+    tm.mark("pack vectors");
     // ---- Poisson border vectors c_{j+1} = P_j^T c_j, Morton order then lib
     if (ctx->poisson) {
         std::vector<double> cm(N, 1.0);
@@ -3417,7 +3424,11 @@ mgm_status mgm_setup(const double* points, const double* normals, int64_t n_poin
         return MGM_ERR_CUDA;
     }
     mgm_status s = do_setup(ctx, points, normals, n_points);
-    if (s == MGM_OK) s = setup_dense_bottom(ctx);
+    if (s == MGM_OK) {
+        SetupTimer tm;
+        s = setup_dense_bottom(ctx);
+        tm.mark("dense bottom B_J", ctx->denseJ);
+    }
     ctx->setup_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     if (s != MGM_OK) {
         g_setup_error = ctx->err;
@@ -3848,8 +3859,13 @@ mgm_status mgm_export_level(const mgm_ctx* ctx, int level, int64_t* ids, int64_t
 
 mgm_status mgm_export_weights(const mgm_ctx* ctx, double* w, int64_t* sten) {
     if (!ctx || ctx->lv.empty()) return MGM_ERR_ARG;
-    if (w) std::copy(ctx->w_orig.begin(), ctx->w_orig.end(), w);
-    if (sten) std::copy(ctx->sten_orig.begin(), ctx->sten_orig.end(), sten);
+    const i64 N = (i64)ctx->perm0.size(), ns = ctx->ns0;
+    const std::vector<i64>& perm = ctx->perm0;
+    for (i64 k = 0; k < N; ++k)  // Morton row k is original row perm[k]
+        for (i64 j = 0; j < ns; ++j) {
+            if (w) w[perm[k] * ns + j] = ctx->w_mor[k * ns + j];
+            if (sten) sten[perm[k] * ns + j] = perm[ctx->sten_mor[k * ns + j]];
+        }
     return MGM_OK;
 }
 

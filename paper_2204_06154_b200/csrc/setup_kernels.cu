@@ -460,6 +460,43 @@ __device__ void block_bitonic_sort(unsigned long long* keys, int n2) {
     }
 }
 
+// flag[0 .. total) in {0, 1} -> flag[p] = flag[p] ? (number of ones before p) : -1 and
+// flag[total] = number of ones: contiguous runs per thread, block scan of the run sums.
+// blockDim.x a multiple of 32, <= 1024.
+__device__ void block_rank_flags(int* flag, int total) {
+    __shared__ int wsum[32];
+    const int nthr = blockDim.x, per = (total + nthr - 1) / nthr;
+    const int b = threadIdx.x * per, e = min(total, b + per);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int s = 0;
+    for (int p = b; p < e; ++p) s += flag[p];
+    int incl = s;
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+    }
+    if (lane == 31) wsum[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+        const int v = lane < (nthr >> 5) ? wsum[lane] : 0;
+        int vi = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int u = __shfl_up_sync(0xffffffffu, vi, o);
+            if (lane >= o) vi += u;
+        }
+        if (lane < (nthr >> 5)) wsum[lane] = vi - v;
+    }
+    __syncthreads();
+    int run = wsum[w] + incl - s;
+    for (int p = b; p < e; ++p) {
+        const int f = flag[p];
+        flag[p] = f ? run : -1;
+        run += f;
+    }
+    if (threadIdx.x == nthr - 1) flag[total] = run;
+    __syncthreads();
+}
+
 // numeric == false: write the unique-column count of each row to cnt.
 // numeric == true : write columns/values at cptr[i].
 template <bool NUMERIC>
@@ -479,16 +516,29 @@ __global__ void k_spgemm_rows(i64 nrows, const i64* __restrict__ ap, const i32* 
         if (skip[i]) continue;  // long rows: spgemm_long_rows (sorted products, same order)
         const i64 a0 = ap[i], a1 = ap[i + 1];
         const int na = (int)(a1 - a0);
-        // offsets of each A entry's products (serial, rows are short)
-        if (threadIdx.x == 0) {
-            i64 o = 0;
-            for (int t = 0; t < na; ++t) {
-                off_s[t] = o;
-                i32 k = ai[a0 + t];
-                o += bp[k + 1] - bp[k];
+        // offsets of each A entry's products: warp 0, shuffle scan over chunks of 32 entries
+        if (threadIdx.x < 32) {
+            const int lane = threadIdx.x;
+            i64 carry = 0;
+            for (int base = 0; base < na; base += 32) {
+                const int t = base + lane;
+                i64 len = 0;
+                if (t < na) {
+                    const i32 k = ai[a0 + t];
+                    len = bp[k + 1] - bp[k];
+                }
+                i64 inc = len;
+                for (int o = 1; o < 32; o <<= 1) {
+                    const i64 v = __shfl_up_sync(0xffffffffu, inc, o);
+                    if (lane >= o) inc += v;
+                }
+                if (t < na) off_s[t] = carry + inc - len;
+                carry += __shfl_sync(0xffffffffu, inc, 31);
             }
-            off_s[na] = o;
-            total_s = (int)o;
+            if (lane == 0) {
+                off_s[na] = carry;
+                total_s = (int)carry;
+            }
         }
         __syncthreads();
         const int total = total_s;
@@ -509,12 +559,7 @@ __global__ void k_spgemm_rows(i64 nrows, const i64* __restrict__ ap, const i32* 
         for (int p = threadIdx.x; p < total; p += blockDim.x)
             flag[p] = (p == 0 || (keys[p] >> 32) != (keys[p - 1] >> 32)) ? 1 : 0;
         __syncthreads();
-        if (threadIdx.x == 0) {
-            int s = 0;
-            for (int p = 0; p < total; ++p) { int f = flag[p]; flag[p] = f ? s : -1; s += f; }
-            flag[total] = s;
-        }
-        __syncthreads();
+        block_rank_flags(flag, total);
         if (!NUMERIC) {
             if (threadIdx.x == 0) cnt[i] = flag[total];
         } else {
