@@ -1985,6 +1985,7 @@ void enqueue_levels_plain(mgm_ctx* ctx, int J, cudaStream_t st) {
     }
 }
 
+mgm_status build_dense_columns_b(mgm_ctx* ctx, int J, int mdim, double* T, cudaStream_t st);
 // B_J = the matrix of lines 6-14 for levels >= J (dense_bottom.cuh), one column per replay
 // of enqueue_levels_plain on a unit vector; on the coarsest level it is L_p^{-1} (the
 // explicit inverse, O13).  Row-major, leading dimension padded to 64 with zeros.
@@ -2003,6 +2004,17 @@ mgm_status setup_dense_bottom(mgm_ctx* ctx) {
     CK(dalloc(&ctx->dB, (i64)mdim * ld));
     CK(dalloc(&T, (i64)mdim * mdim));
     struct FreeT { double* t; ~FreeT() { dev_free(t); } } freet_{T};
+    if (!ctx->poisson && ctx->bK == 0 && J < ctx->p - 1 && ctx->ainv && !std::getenv("MGM_DENSE_BUILD_SINGLE")) {
+        // 8 unit vectors per replay through the batched level kernels (non-Poisson)
+        mgm_status s = build_dense_columns_b(ctx, J, mdim, T, st);
+        if (s) return s;
+        k_transpose_pad<<<dim3((mdim + 31) / 32, ld / 32), dim3(32, 8), 0, st>>>(mdim, ld, T, ctx->dB);
+        CK(cudaStreamSynchronize(st));
+        CK(cudaGetLastError());
+        ctx->dense_m = mdim;
+        ctx->dense_ld = ld;
+        return MGM_OK;
+    }
     cudaGraph_t g = nullptr;
     cudaGraphExec_t gx = nullptr;
     CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
@@ -2827,6 +2839,99 @@ static void enqueue_vcycle_bk(mgm_ctx* ctx, int K, cudaStream_t st) {
         default: enqueue_vcycle_b<8>(ctx, st); break;
     }
 }
+// Alg. 3 lines 6-14 for the levels J..p-1 from e_J = 0 on K interleaved columns (the batched
+// kernels of enqueue_vcycle_b): the dense bottom's build, K unit vectors per replay.
+template <int K>
+static void enqueue_levels_plain_b(mgm_ctx* ctx, int J, cudaStream_t st) {
+    auto& lv = ctx->lv;
+    const int p = ctx->p;
+    const int nu1 = ctx->lp.nu1, nu2 = ctx->lp.nu2;
+    const bool pre_b = ctx->lp.smoother == 1, post_b = ctx->lp.smoother == 1 || ctx->lp.smoother == 2;
+    auto sweep = [&](int j, bool backward) {
+        const Level& L = lv[j];
+        for (int q = 0; q < L.ncol; ++q) {
+            const int c = backward ? L.ncol - 1 - q : q;
+            if (L.coff[c + 1] > L.coff[c]) b_gs<K>(ctx, L, j, (int)L.coff[c], (int)L.coff[c + 1], st);
+        }
+    };
+    auto coarse = [&]() {
+        const int m = ctx->nc;
+        launch(true, k_dense_mv_b<K>, blocks_for((i64)m * K, 256), 256, 0, st, m, (const double*)ctx->ainv,
+               (const double*)ctx->bf[p - 1], ctx->bu[p - 1]);
+    };
+    for (int j = J; j + 1 < p; ++j) {                                               // lines 6-9
+        const Level& L = lv[j];
+        cudaMemsetAsync(ctx->bu[j], 0, sizeof(double) * L.n * K, st);
+        for (int s = 0; s < nu1; ++s) sweep(j, pre_b);
+        b_spmv<1, K>(L.stpr, L.n, L.sptr, L.scol, L.sval, ctx->bu[j], ctx->bf[j], ctx->bt[j], st);
+        b_spmv<0, K>(L.rtpr, lv[j + 1].n, L.rptr, L.rcol, L.rval, ctx->bt[j], nullptr, ctx->bf[j + 1], st);
+    }
+    coarse();                                                                        // line 10
+    for (int j = p - 2; j >= J; --j) {                                              // lines 11-14
+        const Level& L = lv[j];
+        auto kern = L.pm <= 8 ? k_interp_correct_b<8, K> : k_interp_correct_b<16, K>;
+        launch(true, kern, blocks_for(L.n, 256), 256, 0, st, (int)L.n, L.pm, (const i32*)L.pcol,
+               (const double*)L.pval, (const double*)ctx->bu[j + 1], ctx->bu[j]);
+        for (int s = 0; s < nu2; ++s) sweep(j, post_b);
+    }
+}
+template <int K>
+__global__ void k_unit_b(int n, int i0, double* __restrict__ f) {  // f[r][c] = (r == i0 + c)
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n * K; q += gridDim.x * blockDim.x)
+        f[q] = q / K == i0 + q % K ? 1.0 : 0.0;
+}
+template <int K>
+__global__ void k_take_b(int n, int i0, const double* __restrict__ u, double* __restrict__ T) {
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n * K; q += gridDim.x * blockDim.x) {
+        const int r = q / K, c = q % K;
+        if (i0 + c < n) T[(i64)(i0 + c) * n + r] = u[q];
+    }
+}
+mgm_status build_dense_columns_b(mgm_ctx* ctx, int J, int mdim, double* T, cudaStream_t st) {
+    constexpr int K = 8;
+    const int p = ctx->p;
+    if (ctx->bK != 0 || J >= p - 1 || !ctx->ainv) return MGM_ERR_ARG;
+    ctx->bu.assign(p, nullptr);
+    ctx->bf.assign(p, nullptr);
+    ctx->bt.assign(p, nullptr);
+    struct Release {
+        mgm_ctx* c;
+        ~Release() {
+            for (auto* q : {&c->bu, &c->bf, &c->bt}) {
+                for (double* ptr : *q) dev_free(ptr);
+                q->clear();
+            }
+        }
+    } release_{ctx};
+    for (int j = J; j < p; ++j) {
+        CK(dalloc(&ctx->bu[j], ctx->lv[j].n * K));
+        CK(dalloc(&ctx->bf[j], ctx->lv[j].n * K));
+        CK(dalloc(&ctx->bt[j], ctx->lv[j].n * K));
+    }
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t gx = nullptr;
+    CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    g_launch_err.clear();
+    enqueue_levels_plain_b<K>(ctx, J, st);
+    const cudaError_t ce = cudaStreamEndCapture(st, &g);
+    if (ce != cudaSuccess || !g_launch_err.empty()) {
+        ctx->err = "dense bottom capture failed: " + std::string(cudaGetErrorString(ce)) + "; " + g_launch_err;
+        g_launch_err.clear();
+        cudaGetLastError();
+        return MGM_ERR_CUDA;
+    }
+    CK(cudaGraphInstantiate(&gx, g, 0));
+    cudaGraphDestroy(g);
+    for (int i0 = 0; i0 < mdim; i0 += K) {
+        k_unit_b<K><<<blocks_for((i64)mdim * K, 256), 256, 0, st>>>(mdim, i0, ctx->bf[J]);
+        CK(cudaGraphLaunch(gx, st));
+        k_take_b<K><<<blocks_for((i64)mdim * K, 256), 256, 0, st>>>(mdim, i0, ctx->bu[J], T);
+    }
+    CK(cudaStreamSynchronize(st));
+    cudaGraphExecDestroy(gx);
+    return MGM_OK;
+}
+
 static mgm_status ensure_batch(mgm_ctx* ctx, int K) {
     if (ctx->bK >= K) return MGM_OK;
     for (auto* q : {&ctx->bu, &ctx->bf, &ctx->bt})

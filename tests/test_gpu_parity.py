@@ -504,6 +504,35 @@ def test_dense_bottom(name, dense_max, monkeypatch):
     m2.close()
 
 
+@pytest.mark.parametrize("name", list(CASES))
+def test_dense_bottom_batched_build(name, monkeypatch):
+    """B_J built 8 unit vectors per replay through the batched level kernels (the default,
+    non-Poisson) against one unit vector per replay of the single-column kernels
+    (MGM_DENSE_BUILD_SINGLE=1): the V-cycles agree to 1e-13."""
+    import torch
+    from paper_2204_06154_b200 import MGM
+
+    P = pair(name)
+    if P.poisson:
+        pytest.skip("Poisson builds B_J with the single-column kernels")
+    monkeypatch.setenv("MGM_DENSE_MAX", "100000000")
+    monkeypatch.setenv("MGM_DENSE_BUILD_SINGLE", "1")
+    m1 = MGM(P.w.points, P.w.normals, P.w.stencil, P.w.levels)
+    monkeypatch.delenv("MGM_DENSE_BUILD_SINGLE")
+    m2 = MGM(P.w.points, P.w.normals, P.w.stencil, P.w.levels)
+    n = len(P.w.points)
+    f0, u0 = _rand(n, 25), _rand(n, 26)
+    f = torch.from_numpy(f0).cuda()
+    u1 = torch.from_numpy(u0.copy()).cuda()
+    u2 = u1.clone()
+    m1.vcycle(f, u1)
+    m2.vcycle(f, u2)
+    assert relmax(u2.cpu().numpy(), u1.cpu().numpy()) <= 1e-13
+    assert relmax(u2.cpu().numpy(), P.ref.vcycle(f0, u0)) <= 1e-12
+    m1.close()
+    m2.close()
+
+
 # ------------------------------------------------------------------ multi-GPU path (8(e))
 def _fake_ranks(w, R, fn, levels=None):
     """R fake ranks on this GPU (mgm_fake_group_create / mgm_dist_attach_fake): R contexts,
