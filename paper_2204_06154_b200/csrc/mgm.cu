@@ -548,10 +548,27 @@ namespace {
 // column, and slw[s] = 1 + the largest earlier-colour count of slice s: a Gauss-Seidel sweep
 // from a zero guess reads only those first slw slots (the later-colour values are still 0).
 // lib_csr keeps the plain order (diagonal first, ascending column).
+// host vectors whose resize() leaves new elements uninitialised (every element is written
+// afterwards): no sequential zero fill of the large packed arrays
+template <class T>
+struct NoInit : std::allocator<T> {
+    template <class U>
+    struct rebind { using other = NoInit<U>; };
+    NoInit() = default;
+    template <class U>
+    NoInit(const NoInit<U>&) noexcept {}
+    template <class U>
+    void construct(U* p) noexcept { ::new ((void*)p) U; }
+    template <class U, class... Args>
+    void construct(U* p, Args&&... a) { ::new ((void*)p) U(std::forward<Args>(a)...); }
+};
+template <class T>
+using hvec = std::vector<T, NoInit<T>>;
+
 static int host_threads() { return std::max(1, std::min(64, (int)std::thread::hardware_concurrency())); }
 
 void pack_sell(const HostCSR& A, const std::vector<i64>& row_lib2mor, const std::vector<i32>& col_mor2lib,
-               bool diag_first, std::vector<i64>& sptr, std::vector<i32>& scol, std::vector<double>& sval,
+               bool diag_first, std::vector<i64>& sptr, hvec<i32>& scol, hvec<double>& sval,
                HostCSR* lib_csr, const std::vector<i32>* colour_lib = nullptr, std::vector<i32>* slw = nullptr,
                std::vector<i64>* lower_per_colour = nullptr, std::vector<uint8_t>* nlow_row = nullptr,
                std::vector<i32>* sluw = nullptr) {
@@ -652,8 +669,8 @@ void pack_sell(const HostCSR& A, const std::vector<i64>& row_lib2mor, const std:
     }
 }
 
-template <class T>
-mgm_status upload(mgm_ctx* ctx, T** dst, const std::vector<T>& src) {
+template <class T, class A>
+mgm_status upload(mgm_ctx* ctx, T** dst, const std::vector<T, A>& src) {
     CK(dalloc(dst, (i64)src.size()));
     if (!src.empty()) CK(cudaMemcpyAsync(*dst, src.data(), sizeof(T) * src.size(), cudaMemcpyHostToDevice, ctx->st));
     return MGM_OK;
@@ -1213,8 +1230,8 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
         i64 n = L.n;
         L.nnz = Lm[j].nnz();
         std::vector<i64> sptr;
-        std::vector<i32> scol;
-        std::vector<double> sval;
+        hvec<i32> scol;
+        hvec<double> sval;
         std::vector<i32> slw, sluw;
         std::vector<uint8_t> nlow;
         bool coloured = L.ncol > 0 && j + 1 < p;
@@ -1309,8 +1326,8 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
             tm.mark("pack P", j);
             HostCSR R = transpose(P);
             std::vector<i64> rptr;
-            std::vector<i32> rcol;
-            std::vector<double> rval;
+            hvec<i32> rcol;
+            hvec<double> rval;
             pack_sell(R, lib2mor[j + 1], mor2lib[j], false, rptr, rcol, rval, nullptr);
             L.r_stored = (i64)rval.size();
             {  // the same R with Morton columns (same entry order, so the same sums)
@@ -1318,8 +1335,8 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
                 for (i64 r = 0; r < n; ++r) ident[(size_t)r] = (i32)r;
                 for (i64 r = 0; r < n; ++r) l2m[(size_t)r] = (i32)lib2mor[j][(size_t)r];
                 std::vector<i64> rptr2;
-                std::vector<i32> rcol2;
-                std::vector<double> rval2;
+                hvec<i32> rcol2;
+                hvec<double> rval2;
                 pack_sell(R, lib2mor[j + 1], ident, false, rptr2, rcol2, rval2, nullptr);
                 if ((s = upload(ctx, &L.rcol_m, rcol2)) || (s = upload(ctx, &L.l2m, l2m))) return s;
             }
@@ -2888,47 +2905,67 @@ __global__ void k_take_b(int n, int i0, const double* __restrict__ u, double* __
     }
 }
 mgm_status build_dense_columns_b(mgm_ctx* ctx, int J, int mdim, double* T, cudaStream_t st) {
-    constexpr int K = 8;
+    // S independent buffer sets, each with its own captured graph, replayed on S streams
+    // (the small levels' kernels are latency-bound: the replays overlap)
+    constexpr int K = 8, S = 4;
     const int p = ctx->p;
     if (ctx->bK != 0 || J >= p - 1 || !ctx->ainv) return MGM_ERR_ARG;
-    ctx->bu.assign(p, nullptr);
-    ctx->bf.assign(p, nullptr);
-    ctx->bt.assign(p, nullptr);
+    struct Set {
+        std::vector<double*> bu, bf, bt;
+        cudaGraphExec_t gx = nullptr;
+        cudaStream_t s = nullptr;
+    };
+    std::vector<Set> sets(S);
     struct Release {
         mgm_ctx* c;
+        std::vector<Set>& v;
         ~Release() {
-            for (auto* q : {&c->bu, &c->bf, &c->bt}) {
-                for (double* ptr : *q) dev_free(ptr);
-                q->clear();
+            for (auto& q : v) {
+                for (auto* w : {&q.bu, &q.bf, &q.bt})
+                    for (double* ptr : *w) dev_free(ptr);
+                if (q.gx) cudaGraphExecDestroy(q.gx);
+                if (q.s) cudaStreamDestroy(q.s);
             }
+            c->bu.clear();
+            c->bf.clear();
+            c->bt.clear();
         }
-    } release_{ctx};
-    for (int j = J; j < p; ++j) {
-        CK(dalloc(&ctx->bu[j], ctx->lv[j].n * K));
-        CK(dalloc(&ctx->bf[j], ctx->lv[j].n * K));
-        CK(dalloc(&ctx->bt[j], ctx->lv[j].n * K));
-    }
-    cudaGraph_t g = nullptr;
-    cudaGraphExec_t gx = nullptr;
-    CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-    g_launch_err.clear();
-    enqueue_levels_plain_b<K>(ctx, J, st);
-    const cudaError_t ce = cudaStreamEndCapture(st, &g);
-    if (ce != cudaSuccess || !g_launch_err.empty()) {
-        ctx->err = "dense bottom capture failed: " + std::string(cudaGetErrorString(ce)) + "; " + g_launch_err;
+    } release_{ctx, sets};
+    for (auto& q : sets) {
+        q.bu.assign(p, nullptr);
+        q.bf.assign(p, nullptr);
+        q.bt.assign(p, nullptr);
+        for (int j = J; j < p; ++j) {
+            CK(dalloc(&q.bu[j], ctx->lv[j].n * K));
+            CK(dalloc(&q.bf[j], ctx->lv[j].n * K));
+            CK(dalloc(&q.bt[j], ctx->lv[j].n * K));
+        }
+        CK(cudaStreamCreateWithFlags(&q.s, cudaStreamNonBlocking));
+        ctx->bu = q.bu;
+        ctx->bf = q.bf;
+        ctx->bt = q.bt;
+        cudaGraph_t g = nullptr;
+        CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
         g_launch_err.clear();
-        cudaGetLastError();
-        return MGM_ERR_CUDA;
+        enqueue_levels_plain_b<K>(ctx, J, st);
+        const cudaError_t ce = cudaStreamEndCapture(st, &g);
+        if (ce != cudaSuccess || !g_launch_err.empty()) {
+            ctx->err = "dense bottom capture failed: " + std::string(cudaGetErrorString(ce)) + "; " + g_launch_err;
+            g_launch_err.clear();
+            cudaGetLastError();
+            return MGM_ERR_CUDA;
+        }
+        CK(cudaGraphInstantiate(&q.gx, g, 0));
+        cudaGraphDestroy(g);
     }
-    CK(cudaGraphInstantiate(&gx, g, 0));
-    cudaGraphDestroy(g);
-    for (int i0 = 0; i0 < mdim; i0 += K) {
-        k_unit_b<K><<<blocks_for((i64)mdim * K, 256), 256, 0, st>>>(mdim, i0, ctx->bf[J]);
-        CK(cudaGraphLaunch(gx, st));
-        k_take_b<K><<<blocks_for((i64)mdim * K, 256), 256, 0, st>>>(mdim, i0, ctx->bu[J], T);
+    CK(cudaStreamSynchronize(st));  // (T allocated and zero state before the side streams)
+    for (int i0 = 0, b = 0; i0 < mdim; i0 += K, b = (b + 1) % S) {
+        Set& q = sets[b];
+        k_unit_b<K><<<blocks_for((i64)mdim * K, 256), 256, 0, q.s>>>(mdim, i0, q.bf[J]);
+        CK(cudaGraphLaunch(q.gx, q.s));
+        k_take_b<K><<<blocks_for((i64)mdim * K, 256), 256, 0, q.s>>>(mdim, i0, q.bu[J], T);
     }
-    CK(cudaStreamSynchronize(st));
-    cudaGraphExecDestroy(gx);
+    for (auto& q : sets) CK(cudaStreamSynchronize(q.s));
     return MGM_OK;
 }
 
