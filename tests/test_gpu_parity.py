@@ -268,9 +268,9 @@ def test_solve(name, krylov):
     import torch
 
     P = pair(name)
-    if krylov == 0 and name in ("gfd9000", "poisson6000"):
+    if krylov == 0 and name == "poisson6000":
         pytest.skip("standalone MGM converges slowly here (P:411: 'may converge slowly ... "
-                    "on more irregular point clouds'); the GMRES case covers the cycle")
+                    "on more irregular point clouds'); test_standalone_fixed_cycles covers it")
     rhs = P.w.rhs
     x, rep = P.gpu.solve(torch.from_numpy(rhs).cuda(), tol=1e-10, krylov=krylov, maxit=300)
     xr, rr = P.ref.solve(rhs, tol=1e-10, krylov=krylov, maxit=300)
@@ -286,9 +286,10 @@ def test_solve(name, krylov):
 
 @pytest.mark.parametrize("name", ["gfd9000", "poisson6000"])
 def test_standalone_fixed_cycles(name):
-    """Standalone MGM on the clouds where it converges too slowly for the 1e-10 solve
-    test: a fixed number of cycles (tolerance out of reach) on both sides -- same cycle
-    count, iterate to 1e-9 relative, relative residual to 1e-6 relative."""
+    """Standalone MGM for a fixed number of cycles (tolerance out of reach) on both
+    sides -- the Poisson cloud converges too slowly for the 1e-10 solve test: same cycle
+    count, iterate to 1e-9 relative, every residual of the history above the rounding floor
+    (1e-11) to 1e-6 relative."""
     import torch
 
     P = pair(name)
@@ -300,7 +301,10 @@ def test_standalone_fixed_cycles(name):
     assert rep.iterations == rr.iterations == cycles
     xg = x.cpu().numpy()
     assert np.linalg.norm(xg - xr) / np.linalg.norm(xr) <= 1e-9
-    assert abs(rep.final_rel_residual - rr.final_rel_residual) <= 1e-6 * rr.final_rel_residual
+    hg, hr = np.array(rep.history, dtype=float), np.array(rr.history, dtype=float)
+    assert len(hg) == len(hr) == cycles
+    above = hr > 1e-11
+    assert above[0] and np.all(np.abs(hg[above] - hr[above]) <= 1e-6 * hr[above])
     if P.poisson:
         assert abs(rep.lam - rr.lam) <= 1e-8 * max(1.0, abs(rr.lam))
 
