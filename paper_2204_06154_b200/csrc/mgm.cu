@@ -1102,8 +1102,92 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
     Xl[0] = X;
     idsl[0] = perm;
     double* dXf = dX;
+    // Galerkin products on their own thread and stream, pipelined against the point
+    // hierarchy: RAP_j needs L_j (the previous product) and P_j (this loop), while WSE and the
+    // transfers of the next levels need only the points.
+    struct RapPipe {
+        std::mutex mu;
+        std::condition_variable cv;
+        int ready = -1;  // highest j whose P_j is final
+        bool abort = false;
+        mgm_status status = MGM_OK;
+        std::string err;
+        i64 err_j = -1;
+        std::thread th;
+        void publish(int j) {
+            {
+                std::lock_guard<std::mutex> lk(mu);
+                ready = j;
+            }
+            cv.notify_all();
+        }
+        void stop() {
+            {
+                std::lock_guard<std::mutex> lk(mu);
+                abort = true;
+            }
+            cv.notify_all();
+            if (th.joinable()) th.join();
+        }
+        ~RapPipe() { stop(); }
+    } rap;
+    rap.th = std::thread([&] {
+        AllocScope as_(ctx);
+        cudaStream_t rs = nullptr;
+        if (cudaStreamCreateWithFlags(&rs, cudaStreamNonBlocking) != cudaSuccess) {
+            rap.status = MGM_ERR_CUDA;
+            rap.err = "cannot create the Galerkin stream";
+            return;
+        }
+        SetupTimer rtm;
+        for (int j = 0; j + 1 < p; ++j) {
+            {
+                std::unique_lock<std::mutex> lk(rap.mu);
+                rap.cv.wait(lk, [&] { return rap.ready >= j || rap.abort; });
+                if (rap.ready < j) break;
+            }
+            rtm.t0 = std::chrono::steady_clock::now();
+            const HostCSR& P = Pm[j];
+            HostCSR R = transpose(P);  // P:370, exact
+            // Galerkin L_{j+1} = R (L P) on the GPU
+            DevCSR dL, dP, dR, dLP, dC;
+            auto release = [&] {
+                free_dev_csr(dL);
+                free_dev_csr(dP);
+                free_dev_csr(dR);
+                free_dev_csr(dLP);
+                free_dev_csr(dC);
+            };
+            std::string e1;
+            mgm_status st_ = MGM_OK;
+            if (upload_csr(Lm[j], dL, rs) || upload_csr(P, dP, rs) || upload_csr(R, dR, rs)) {
+                st_ = MGM_ERR_OOM;
+                e1 = "upload for SpGEMM";
+            } else if (spgemm_device(dL, dP, dLP, rs, e1)) {
+                st_ = MGM_ERR_CUDA;
+                e1 = "SpGEMM L*P: " + e1;
+            } else if (spgemm_device(dR, dLP, dC, rs, e1)) {
+                st_ = MGM_ERR_CUDA;
+                e1 = "SpGEMM R*(LP): " + e1;
+            } else if (download_csr(dC, Lm[j + 1], rs)) {
+                st_ = MGM_ERR_CUDA;
+                e1 = "download Galerkin";
+            }
+            release();
+            if (st_ != MGM_OK) {
+                rap.status = st_;
+                rap.err = e1;
+                rap.err_j = j;
+                break;
+            }
+            start_colouring(j + 1);
+            rtm.mark("Galerkin RAP", j);
+        }
+        cudaStreamSynchronize(rs);
+        cudaStreamDestroy(rs);
+    });
     for (int j = 0; j + 1 < p; ++j) {
-        i64 nf = Lm[j].nrows, ncs = nf / lp.coarsen_factor;
+        i64 nf = (i64)Xl[j].size() / 3, ncs = nf / lp.coarsen_factor;
         // WSE, host
         std::vector<double> nn2;
         nearest_other(Xl[j].data(), nf, nn2, nth);
@@ -1171,23 +1255,11 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
             for (auto& x : th) x.join();
         }
         tm.mark("interp weights", j);
-        HostCSR R = transpose(P);  // P:370, exact
-        // Galerkin L_{j+1} = R (L P) on the GPU
-        DevCSR dL, dP, dR, dLP, dC;
-        if (upload_csr(Lm[j], dL, st) || upload_csr(P, dP, st) || upload_csr(R, dR, st))
-            return fail(ctx, MGM_ERR_OOM, "upload for SpGEMM", j);
-        std::string e1;
-        if (spgemm_device(dL, dP, dLP, st, e1)) return fail(ctx, MGM_ERR_CUDA, "SpGEMM L*P: " + e1, j);
-        if (spgemm_device(dR, dLP, dC, st, e1)) return fail(ctx, MGM_ERR_CUDA, "SpGEMM R*(LP): " + e1, j);
-        if (download_csr(dC, Lm[j + 1], st)) return fail(ctx, MGM_ERR_CUDA, "download Galerkin", j);
-        free_dev_csr(dL);
-        free_dev_csr(dP);
-        free_dev_csr(dR);
-        free_dev_csr(dLP);
-        free_dev_csr(dC);
-        start_colouring(j + 1);
-        tm.mark("Galerkin RAP", j);
+        rap.publish(j);
     }
+    rap.stop();
+    if (rap.status != MGM_OK) return fail(ctx, rap.status, rap.err, rap.err_j);
+    tm.mark("Galerkin pipeline wait");
     dev_free(dXf);
     dev_free(dfail);
     // ---- colouring (O11) and lib orders
