@@ -979,10 +979,10 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
             X[3 * k + a] = points[3 * perm[k] + a];
             NR[3 * k + a] = normals[3 * perm[k] + a];
         }
-    // duplicates
+    // duplicates (the nearest-other distances are level 0's WSE input too)
+    std::vector<double> nn2_0;
     {
-        std::vector<double> nn2;
-        i64 dup = nearest_other(X.data(), N, nn2, nth);
+        i64 dup = nearest_other(X.data(), N, nn2_0, nth);
         if (dup >= 0) return fail(ctx, MGM_ERR_INPUT, "duplicate points", perm[dup]);
     }
     tm.mark("morton+duplicates");
@@ -1005,6 +1005,31 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
     std::vector<i32> sten;
     knn_grid(X.data(), N, X.data(), N, ns, sten, nth);
     tm.mark("fine kNN");
+    HostCSR pat0;  // pattern of L_1: row i's columns are its stencil
+    pat0.nrows = pat0.ncols = N;
+    pat0.ptr.resize(N + 1);
+    for (i64 i = 0; i <= N; ++i) pat0.ptr[i] = i * ns;
+    pat0.col = sten;
+    std::vector<HostCSR> Lm(p), Pm(p);
+    // colourings (O11) run on background threads, each started as soon as its level's
+    // pattern is final (L_1's is the stencil lists, right after the kNN; L_{j+1}'s after its
+    // Galerkin product), so they overlap the rest of the setup; joined before the lib orders
+    // are built (and on every early return).  A colouring reads only the pattern.
+    std::vector<std::vector<i32>> colour_mor(p);
+    std::vector<int> ncol_j(p, 0);
+    struct Joiner {
+        std::vector<std::thread> th;
+        ~Joiner() { join(); }
+        void join() {
+            for (auto& t : th)
+                if (t.joinable()) t.join();
+        }
+    } colour_th;
+    auto start_colouring = [&](int j, const HostCSR* A) {
+        if (j + 1 < p)
+            colour_th.th.emplace_back([&, j, A] { ncol_j[j] = greedy_colouring(*A, colour_mor[j], colour_passes()); });
+    };
+    start_colouring(0, &pat0);
     double *dX = nullptr, *dN = nullptr, *dW = nullptr, *drho = nullptr;
     i32* dS = nullptr;
     i64* dfail = nullptr;
@@ -1042,25 +1067,6 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
     tm.mark("fine weights (GPU)");
     // export copy of weights in original order
     // ---- L_1, Morton order CSR with ascending columns
-    std::vector<HostCSR> Lm(p), Pm(p);
-    // colourings (O11) run on background threads, each started as soon as its level's
-    // operator is final (L_1 after assembly, L_{j+1} after its Galerkin product), so they
-    // overlap the rest of the level loop; joined before the lib orders are built (and on
-    // every early return)
-    std::vector<std::vector<i32>> colour_mor(p);
-    std::vector<int> ncol_j(p, 0);
-    struct Joiner {
-        std::vector<std::thread> th;
-        ~Joiner() { join(); }
-        void join() {
-            for (auto& t : th)
-                if (t.joinable()) t.join();
-        }
-    } colour_th;
-    auto start_colouring = [&](int j) {
-        if (j + 1 < p)
-            colour_th.th.emplace_back([&, j] { ncol_j[j] = greedy_colouring(Lm[j], colour_mor[j], colour_passes()); });
-    };
     {
         HostCSR& A = Lm[0];
         A.nrows = A.ncols = N;
@@ -1090,7 +1096,6 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
         for (auto& t : th) t.join();
         A.ptr[N] = N * ns;
     }
-    start_colouring(0);
     ctx->w_mor = std::move(W);
     ctx->sten_mor = std::move(sten);
     ctx->perm0 = perm;
@@ -1180,7 +1185,7 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
                 rap.err_j = j;
                 break;
             }
-            start_colouring(j + 1);
+            start_colouring(j + 1, &Lm[j + 1]);
             rtm.mark("Galerkin RAP", j);
         }
         cudaStreamSynchronize(rs);
@@ -1190,7 +1195,10 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
         i64 nf = (i64)Xl[j].size() / 3, ncs = nf / lp.coarsen_factor;
         // WSE, host
         std::vector<double> nn2;
-        nearest_other(Xl[j].data(), nf, nn2, nth);
+        if (j == 0)
+            nn2.swap(nn2_0);
+        else
+            nearest_other(Xl[j].data(), nf, nn2, nth);
         std::vector<i64> keep;
         wse_eliminate(Xl[j].data(), nf, ncs, nn2, keep, nth);
         tm.mark("WSE", j);
