@@ -1017,17 +1017,75 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
     // are built (and on every early return).  A colouring reads only the pattern.
     std::vector<std::vector<i32>> colour_mor(p);
     std::vector<int> ncol_j(p, 0);
+    // ... and each thread then builds its level's lib order and packs L_j's SELL arrays
+    // (host), once L_j's values are final (level 0: after the assembly below)
+    struct LevelPack {
+        bool done = false;
+        std::vector<i64> coff, lib2mor;
+        std::vector<i32> mor2lib, colour_lib;
+        std::vector<i64> sptr, lower_per_colour;
+        hvec<i32> scol;
+        hvec<double> sval;
+        std::vector<i32> slw, sluw;
+        std::vector<uint8_t> nlow;
+        HostCSR L_lib;
+    };
+    std::vector<LevelPack> pk(p);
+    struct Gate {  // opened when L_1's values are assembled; aborted on an early return
+        std::mutex mu;
+        std::condition_variable cv;
+        bool open = false, abort = false;
+        void set(bool ab) {
+            {
+                std::lock_guard<std::mutex> lk(mu);
+                (ab ? abort : open) = true;
+            }
+            cv.notify_all();
+        }
+        bool wait() {
+            std::unique_lock<std::mutex> lk(mu);
+            cv.wait(lk, [&] { return open || abort; });
+            return open;
+        }
+    } l0_values;
     struct Joiner {
+        Gate* g;
         std::vector<std::thread> th;
-        ~Joiner() { join(); }
+        ~Joiner() {
+            g->set(true);
+            join();
+        }
         void join() {
             for (auto& t : th)
                 if (t.joinable()) t.join();
         }
-    } colour_th;
+    } colour_th{&l0_values, {}};
     auto start_colouring = [&](int j, const HostCSR* A) {
-        if (j + 1 < p)
-            colour_th.th.emplace_back([&, j, A] { ncol_j[j] = greedy_colouring(*A, colour_mor[j], colour_passes()); });
+        if (j + 1 >= p) return;
+        colour_th.th.emplace_back([&, j, A] {
+            const int nc = greedy_colouring(*A, colour_mor[j], colour_passes());
+            ncol_j[j] = nc;
+            LevelPack& q = pk[j];
+            const std::vector<i32>& cm = colour_mor[j];
+            const i64 n = A->nrows;
+            q.coff.assign(nc + 1, 0);  // lib order: colours ascending, Morton order within
+            for (i64 i = 0; i < n; ++i) q.coff[cm[i] + 1]++;
+            for (int c = 0; c < nc; ++c) q.coff[c + 1] += q.coff[c];
+            q.lib2mor.resize(n);
+            q.mor2lib.resize(n);
+            std::vector<i64> fillp(q.coff.begin(), q.coff.end() - 1);
+            for (i64 i = 0; i < n; ++i) q.lib2mor[fillp[cm[i]]++] = i;
+            for (i64 r = 0; r < n; ++r) q.mor2lib[q.lib2mor[r]] = (i32)r;
+            q.colour_lib.resize(n);
+            for (i64 r = 0; r < n; ++r) q.colour_lib[r] = cm[q.lib2mor[r]];
+            if (j == 0 && !l0_values.wait()) return;
+            const bool coloured = nc > 0;
+            pack_sell(Lm[j], q.lib2mor, q.mor2lib, true, q.sptr, q.scol, q.sval, &q.L_lib,
+                      coloured ? &q.colour_lib : nullptr, coloured ? &q.slw : nullptr,
+                      coloured ? &q.lower_per_colour : nullptr, coloured ? &q.nlow : nullptr,
+                      coloured ? &q.sluw : nullptr);
+            q.done = true;
+        });
     };
     start_colouring(0, &pat0);
     double *dX = nullptr, *dN = nullptr, *dW = nullptr, *drho = nullptr;
@@ -1096,6 +1154,7 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
         for (auto& t : th) t.join();
         A.ptr[N] = N * ns;
     }
+    l0_values.set(false);
     ctx->w_mor = std::move(W);
     ctx->sten_mor = std::move(sten);
     ctx->perm0 = perm;
@@ -1275,32 +1334,31 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
     std::vector<std::vector<i64>> lib2mor(p);
     std::vector<std::vector<i32>> mor2lib(p);
     colour_th.join();
-    for (int j = 0; j + 1 < p; ++j) ctx->lv[j].ncol = ncol_j[j];
+    for (int j = 0; j + 1 < p; ++j) {
+        if (!pk[j].done) return fail(ctx, MGM_ERR_ARG, "colouring thread did not finish", j);
+        ctx->lv[j].ncol = ncol_j[j];
+    }
     for (int j = 0; j < p; ++j) {
         Level& L = ctx->lv[j];
         i64 n = Lm[j].nrows;
         L.n = n;
-        lib2mor[j].resize(n);
-        mor2lib[j].resize(n);
         if (j + 1 < p) {
-            L.coff.assign(L.ncol + 1, 0);
-            for (i64 i = 0; i < n; ++i) L.coff[colour_mor[j][i] + 1]++;
-            for (int c = 0; c < L.ncol; ++c) L.coff[c + 1] += L.coff[c];
-            std::vector<i64> fillp(L.coff.begin(), L.coff.end() - 1);
-            for (i64 i = 0; i < n; ++i) lib2mor[j][fillp[colour_mor[j][i]]++] = i;
+            L.coff = std::move(pk[j].coff);
+            lib2mor[j] = std::move(pk[j].lib2mor);
+            mor2lib[j] = std::move(pk[j].mor2lib);
+            L.colour_lib = std::move(pk[j].colour_lib);
         } else {
             L.ncol = 0;
             colour_mor[j].assign(n, 0);
+            lib2mor[j].resize(n);
+            mor2lib[j].resize(n);
             for (i64 i = 0; i < n; ++i) lib2mor[j][i] = i;
+            for (i64 r = 0; r < n; ++r) mor2lib[j][lib2mor[j][r]] = (i32)r;
+            L.colour_lib.assign(n, 0);
         }
-        for (i64 r = 0; r < n; ++r) mor2lib[j][lib2mor[j][r]] = (i32)r;
         L.lib2mor = lib2mor[j];
         L.ids.resize(n);
-        L.colour_lib.resize(n);
-        for (i64 r = 0; r < n; ++r) {
-            L.ids[r] = idsl[j][lib2mor[j][r]];
-            L.colour_lib[r] = colour_mor[j][lib2mor[j][r]];
-        }
+        for (i64 r = 0; r < n; ++r) L.ids[r] = idsl[j][lib2mor[j][r]];
     }
     tm.mark("colouring");
     // ---- pack solve-phase layout
@@ -1315,10 +1373,19 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
         std::vector<i32> slw, sluw;
         std::vector<uint8_t> nlow;
         bool coloured = L.ncol > 0 && j + 1 < p;
-        pack_sell(Lm[j], lib2mor[j], mor2lib[j], true, sptr, scol, sval, &L.L_lib,
-                  coloured ? &L.colour_lib : nullptr, coloured ? &slw : nullptr,
-                  coloured ? &L.lower_per_colour : nullptr, coloured ? &nlow : nullptr,
-                  coloured ? &sluw : nullptr);
+        if (j + 1 < p) {  // packed by the level's colouring thread
+            LevelPack& q = pk[j];
+            sptr = std::move(q.sptr);
+            scol = std::move(q.scol);
+            sval = std::move(q.sval);
+            slw = std::move(q.slw);
+            sluw = std::move(q.sluw);
+            nlow = std::move(q.nlow);
+            L.L_lib = std::move(q.L_lib);
+            L.lower_per_colour = std::move(q.lower_per_colour);
+        } else {
+            pack_sell(Lm[j], lib2mor[j], mor2lib[j], true, sptr, scol, sval, &L.L_lib);
+        }
         for (i64 r = 0; r < n && coloured; ++r)
             if (nlow[(size_t)r] == 255) coloured = false;  // (no zero-guess sweeps for such rows)
         if (coloured && ((s = upload(ctx, &L.slw, slw)) || (s = upload(ctx, &L.nlow, nlow)) ||
