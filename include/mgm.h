@@ -340,6 +340,11 @@ mgm_status mgm_host_morton(const double* points, int64_t n, int64_t* perm);
  * out[nq * k] int32 indices into points. */
 mgm_status mgm_host_knn(const double* points, int64_t n, const double* queries, int64_t nq,
                         int k, int32_t* out);
+/* The same kNN lists computed on the GPU (the path mgm_setup takes for k <= 64): host
+ * arrays in and out, copied through device buffers on the current device.  MGM_ERR_ARG for
+ * k < 1, k > n or k > 64; MGM_ERR_CUDA on a CUDA error. */
+mgm_status mgm_device_knn(const double* points, int64_t n, const double* queries, int64_t nq,
+                          int k, int32_t* out);
 /* Weighted sample elimination of n points down to nt (O8). keep[nt] ascending. */
 mgm_status mgm_host_wse(const double* points, int64_t n, int64_t nt, int64_t* keep);
 /* Greedy colouring (O11) of sym(pattern) minus the diagonal, vertices in index order.

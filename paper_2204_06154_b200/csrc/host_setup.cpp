@@ -248,7 +248,7 @@ void knn_grid(const double* pts, i64 n, const double* qry, i64 nq, int k, std::v
                     }
                 }
             }
-            for (int t = 0; t < k; ++t) out[(size_t)q * k + t] = best.j[t];
+            for (int t = 0; t < k; ++t) out[(size_t)q * k + t] = t < best.count ? best.j[t] : -1;
         }
     });
 }

@@ -1002,8 +1002,21 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
     ctx->p = p;
     // ---- fine stencils and weights on the GPU
     const int ns = sp.stencil_n;
-    std::vector<i32> sten;
-    knn_grid(X.data(), N, X.data(), N, ns, sten, nth);
+    double *dX = nullptr, *dN = nullptr, *dW = nullptr, *drho = nullptr;
+    i32* dS = nullptr;
+    i64* dfail = nullptr;
+    CK(dalloc(&dX, 3 * N));
+    CK(dalloc(&dS, N * ns));
+    CK(cudaMemcpyAsync(dX, X.data(), sizeof(double) * 3 * N, cudaMemcpyHostToDevice, st));
+    std::vector<i32> sten((size_t)N * ns);
+    if (knn_device(X.data(), dX, N, dX, N, ns, dS, st) == 0) {  // O2 stencils on the GPU
+        CK(cudaMemcpyAsync(sten.data(), dS, sizeof(i32) * N * ns, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+    } else {  // (k > 64)
+        cudaGetLastError();
+        knn_grid(X.data(), N, X.data(), N, ns, sten, nth);
+        CK(cudaMemcpyAsync(dS, sten.data(), sizeof(i32) * N * ns, cudaMemcpyHostToDevice, st));
+    }
     tm.mark("fine kNN");
     HostCSR pat0;  // pattern of L_1: row i's columns are its stencil
     pat0.nrows = pat0.ncols = N;
@@ -1088,17 +1101,10 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
         });
     };
     start_colouring(0, &pat0);
-    double *dX = nullptr, *dN = nullptr, *dW = nullptr, *drho = nullptr;
-    i32* dS = nullptr;
-    i64* dfail = nullptr;
-    CK(dalloc(&dX, 3 * N));
     CK(dalloc(&dN, 3 * N));
     CK(dalloc(&dW, N * ns));
-    CK(dalloc(&dS, N * ns));
     CK(dalloc(&dfail, 1));
-    CK(cudaMemcpyAsync(dX, X.data(), sizeof(double) * 3 * N, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(dN, NR.data(), sizeof(double) * 3 * N, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(dS, sten.data(), sizeof(i32) * N * ns, cudaMemcpyHostToDevice, st));
     i64 none = INT64_MAX;
     CK(cudaMemcpyAsync(dfail, &none, sizeof(i64), cudaMemcpyHostToDevice, st));
     int rc;
@@ -1269,9 +1275,6 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
         }
         // interpolation stencils (m nearest coarse points, O2) and weights on the GPU
         const int m = lp.interp_m;
-        std::vector<i32> ist;
-        knn_grid(Xl[j + 1].data(), ncs, Xl[j].data(), nf, m, ist, nth);
-        tm.mark("interp kNN", j);
         double *dXc = nullptr, *dPw = nullptr;
         i32 *dI = nullptr, *dcnt = nullptr;
         CK(dalloc(&dXc, 3 * ncs));
@@ -1279,7 +1282,15 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
         CK(dalloc(&dI, nf * m));
         CK(dalloc(&dcnt, nf));
         CK(cudaMemcpyAsync(dXc, Xl[j + 1].data(), sizeof(double) * 3 * ncs, cudaMemcpyHostToDevice, st));
-        CK(cudaMemcpyAsync(dI, ist.data(), sizeof(i32) * nf * m, cudaMemcpyHostToDevice, st));
+        std::vector<i32> ist((size_t)nf * m);
+        if (knn_device(Xl[j + 1].data(), dXc, ncs, dXf, nf, m, dI, st) == 0) {
+            CK(cudaMemcpyAsync(ist.data(), dI, sizeof(i32) * nf * m, cudaMemcpyDeviceToHost, st));
+        } else {  // (m > 64)
+            cudaGetLastError();
+            knn_grid(Xl[j + 1].data(), ncs, Xl[j].data(), nf, m, ist, nth);
+            CK(cudaMemcpyAsync(dI, ist.data(), sizeof(i32) * nf * m, cudaMemcpyHostToDevice, st));
+        }
+        tm.mark("interp kNN", j);
         CK(cudaMemcpyAsync(dfail, &none, sizeof(i64), cudaMemcpyHostToDevice, st));
         rc = launch_interp_weights(dXf, nf, dXc, dI, m, dPw, dcnt, dfail, st);
         if (rc) return fail(ctx, MGM_ERR_CUDA, "interp kernel", -1);
@@ -4373,6 +4384,34 @@ mgm_status mgm_host_knn(const double* points, int64_t n, const double* queries, 
     std::vector<i32> o;
     knn_grid(points, n, queries, nq, k, o, std::max(1, (int)std::thread::hardware_concurrency()));
     std::copy(o.begin(), o.end(), out);
+    return MGM_OK;
+}
+
+mgm_status mgm_device_knn(const double* points, int64_t n, const double* queries, int64_t nq, int k,
+                          int32_t* out) {
+    if (!points || !queries || !out || k < 1 || k > n || k > 64 || nq < 0) return MGM_ERR_ARG;
+    if (nq == 0) return MGM_OK;
+    double *dp = nullptr, *dq = nullptr;
+    i32* dout = nullptr;
+    struct Free {
+        double** a;
+        double** b;
+        i32** c;
+        ~Free() {
+            cudaFree(*a);
+            cudaFree(*b);
+            cudaFree(*c);
+        }
+    } free_{&dp, &dq, &dout};
+    if (cudaMalloc(&dp, sizeof(double) * 3 * n) != cudaSuccess || cudaMalloc(&dq, sizeof(double) * 3 * nq) != cudaSuccess ||
+        cudaMalloc(&dout, sizeof(i32) * nq * k) != cudaSuccess)
+        return MGM_ERR_CUDA;
+    cudaStream_t st = nullptr;
+    if (cudaMemcpy(dp, points, sizeof(double) * 3 * n, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(dq, queries, sizeof(double) * 3 * nq, cudaMemcpyHostToDevice) != cudaSuccess)
+        return MGM_ERR_CUDA;
+    if (knn_device(points, dp, n, dq, nq, k, dout, st) != 0) return MGM_ERR_CUDA;
+    if (cudaMemcpy(out, dout, sizeof(i32) * nq * k, cudaMemcpyDeviceToHost) != cudaSuccess) return MGM_ERR_CUDA;
     return MGM_OK;
 }
 

@@ -98,6 +98,11 @@ int launch_gfd_weights(const double* pts, const double* nrm, const i32* sten, i6
 int launch_interp_weights(const double* fine, i64 nf, const double* coarse, const i32* sten,
                           int m, double* w, i32* cnt, i64* fail_dev, void* stream);
 
+// Exact kNN on the device (same lists as knn_grid; k <= 64).  h_pts: the same points on the
+// host (bounding box); d_out[nq * k].  Synchronises the stream.
+int knn_device(const double* h_pts, const double* d_pts, i64 n, const double* d_qry, i64 nq, int k, i32* d_out,
+               void* stream);
+
 // Device SpGEMM C = A B (CSR, columns ascending).  Symbolic pattern kept in full; values
 // summed in canonical order (O10), bit-identical to a sequential loop.
 struct DevCSR {

@@ -735,6 +735,214 @@ static int spgemm_long_rows(const DevCSR& A, const DevCSR& B, const std::vector<
     return 0;
 }
 
+// ---------------------------------------------------------------------------------------
+// Exact grid kNN on the device (O2; the same lists as host_setup.cpp knn_grid: the k
+// smallest (squared distance, index) pairs, ascending).  A dense cell table over the
+// bounding box (cells grown until it holds at most 4n + 64 cells, then shrunk towards ~k/2
+// points per occupied cell); one thread per query expands Chebyshev shells of cells and
+// stops once the k-th best squared distance is below the squared distance to every
+// unvisited cell (1e-9 relative margin).  The result does not depend on the cell size.
+// ---------------------------------------------------------------------------------------
+struct DevGrid {
+    double lo[3], cell;
+    i64 dims[3];
+};
+
+__device__ __forceinline__ void grid_coords(const DevGrid& g, const double* x, i64* c) {
+    for (int a = 0; a < 3; ++a) {
+        const i64 v = (i64)floor((x[a] - g.lo[a]) / g.cell);
+        c[a] = min(max(v, (i64)0), g.dims[a] - 1);
+    }
+}
+
+__global__ void k_grid_count(DevGrid g, const double* __restrict__ pts, i64 n, i64* __restrict__ cid,
+                             int* __restrict__ cnt) {
+    for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
+        i64 c[3];
+        grid_coords(g, pts + 3 * i, c);
+        const i64 id = (c[2] * g.dims[1] + c[1]) * g.dims[0] + c[0];
+        cid[i] = id;
+        atomicAdd(&cnt[id], 1);
+    }
+}
+
+__global__ void k_grid_fill(i64 n, const i64* __restrict__ cid, int* __restrict__ fill, i32* __restrict__ items) {
+    for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
+        items[atomicAdd(&fill[cid[i]], 1)] = (i32)i;
+}
+
+__global__ void k_count_occupied(i64 total, const int* __restrict__ cnt, unsigned long long* __restrict__ occ) {
+    unsigned long long c = 0;
+    for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < total; i += (i64)gridDim.x * blockDim.x)
+        c += cnt[i] > 0;
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_down_sync(FULL, c, o);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(occ, c);
+}
+
+template <int KMAX>
+__global__ void __launch_bounds__(128) k_knn(DevGrid g, const double* __restrict__ pts, const int* __restrict__ start,
+                                             const i32* __restrict__ items, const double* __restrict__ qry, i64 nq,
+                                             int k, i32* __restrict__ out) {
+    double bd[KMAX];
+    int bj[KMAX];
+    const i64 maxr = max(g.dims[0], max(g.dims[1], g.dims[2]));
+    for (i64 qi = blockIdx.x * (i64)blockDim.x + threadIdx.x; qi < nq; qi += (i64)gridDim.x * blockDim.x) {
+        const double x[3] = {qry[3 * qi], qry[3 * qi + 1], qry[3 * qi + 2]};
+        int count = 0;
+        i64 c[3];
+        grid_coords(g, x, c);
+        for (i64 r = 0; r <= maxr; ++r) {
+            for (i64 z = c[2] - r; z <= c[2] + r; ++z) {
+                if (z < 0 || z >= g.dims[2]) continue;
+                const bool zface = (z == c[2] - r || z == c[2] + r);
+                for (i64 y = c[1] - r; y <= c[1] + r; ++y) {
+                    if (y < 0 || y >= g.dims[1]) continue;
+                    const bool yface = zface || (y == c[1] - r || y == c[1] + r);
+                    for (i64 xx = c[0] - r; xx <= c[0] + r; ++xx) {
+                        if (xx < 0 || xx >= g.dims[0]) continue;
+                        if (!yface && xx != c[0] - r && xx != c[0] + r) {
+                            xx = c[0] + r - 1;  // skip the interior run of this row
+                            continue;
+                        }
+                        const i64 cell = (z * g.dims[1] + y) * g.dims[0] + xx;
+                        for (int t = start[cell]; t < start[cell + 1]; ++t) {
+                            const i32 j = items[t];
+                            const double* yv = pts + 3 * (i64)j;
+                            const double dx = yv[0] - x[0], dy = yv[1] - x[1], dz = yv[2] - x[2];
+                            const double dd = (dx * dx + dy * dy) + dz * dz;  // O2 (no FMA: -fmad=false)
+                            if (count == k && (dd > bd[k - 1] || (dd == bd[k - 1] && j > bj[k - 1]))) continue;
+                            int p = count < k ? count++ : k - 1;
+                            while (p > 0 && (bd[p - 1] > dd || (bd[p - 1] == dd && bj[p - 1] > j))) {
+                                bd[p] = bd[p - 1];
+                                bj[p] = bj[p - 1];
+                                --p;
+                            }
+                            bd[p] = dd;
+                            bj[p] = j;
+                        }
+                    }
+                }
+            }
+            if (count == k) {
+                double dmin = INFINITY;
+                bool all = true;
+                for (int a = 0; a < 3; ++a) {
+                    const double lo_face = g.lo[a] + (double)(c[a] - r) * g.cell;
+                    const double hi_face = g.lo[a] + (double)(c[a] + r + 1) * g.cell;
+                    if (c[a] - r > 0) { dmin = fmin(dmin, x[a] - lo_face); all = false; }
+                    if (c[a] + r + 1 < g.dims[a]) { dmin = fmin(dmin, hi_face - x[a]); all = false; }
+                }
+                if (all) break;
+                if (dmin > 0) {
+                    const double b2 = dmin * dmin * (1.0 - 1e-9);
+                    if (bd[k - 1] < b2) break;
+                }
+            }
+        }
+        for (int t = 0; t < k; ++t) out[qi * k + t] = t < count ? bj[t] : -1;
+    }
+}
+
+int knn_device(const double* h_pts, const double* d_pts, i64 n, const double* d_qry, i64 nq, int k, i32* d_out,
+               void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (k < 1 || k > 64 || n < 1) return (int)cudaErrorInvalidValue;
+    DevGrid g;
+    double hi[3];
+    for (int a = 0; a < 3; ++a) g.lo[a] = hi[a] = h_pts[a];
+    for (i64 i = 0; i < n; ++i)
+        for (int a = 0; a < 3; ++a) {
+            g.lo[a] = std::min(g.lo[a], h_pts[3 * i + a]);
+            hi[a] = std::max(hi[a], h_pts[3 * i + a]);
+        }
+    double cell;
+    {  // volumetric start: ~k/4 points per cell of the box
+        const double ext = std::max(hi[0] - g.lo[0], std::max(hi[1] - g.lo[1], hi[2] - g.lo[2]));
+        double vol = 1.0;
+        for (int a = 0; a < 3; ++a) vol *= std::max(hi[a] - g.lo[a], 1e-3 * ext);
+        cell = std::cbrt(vol * std::max(1, k / 4) / (double)n);
+        if (!(cell > 0)) cell = 1.0;
+    }
+    i64* cid = nullptr;
+    int *cnt = nullptr, *fill = nullptr;
+    i32* items = nullptr;
+    unsigned long long* occ = nullptr;
+    void* tmp = nullptr;
+    size_t tmp_bytes = 0;
+    i64 cap = 0;
+    auto release = [&] {
+        dev_free(cid);
+        dev_free(cnt);
+        dev_free(fill);
+        dev_free(items);
+        dev_free(occ);
+        dev_free(tmp);
+    };
+    cudaError_t e = dev_malloc((void**)&cid, sizeof(i64) * n);
+    if (e == cudaSuccess) e = dev_malloc((void**)&items, sizeof(i32) * n);
+    if (e == cudaSuccess) e = dev_malloc((void**)&occ, sizeof(unsigned long long));
+    if (e != cudaSuccess) { release(); return (int)e; }
+    const unsigned nb = (unsigned)std::min<i64>((n + 255) / 256, 148 * 16);
+    for (int pass = 0; pass < 2; ++pass) {
+        g.cell = cell;
+        i64 total = 1;
+        auto dims_for = [&] {
+            total = 1;
+            for (int a = 0; a < 3; ++a) {
+                g.dims[a] = std::max<i64>(1, (i64)std::floor((hi[a] - g.lo[a]) / g.cell) + 1);
+                total *= g.dims[a];
+            }
+        };
+        dims_for();
+        while (total > 4 * n + 64) {  // bounded dense table (cells only grow)
+            g.cell *= 1.26;
+            dims_for();
+        }
+        if (total + 1 > cap) {
+            dev_free(cnt);
+            dev_free(fill);
+            dev_free(tmp);
+            cnt = fill = nullptr;
+            tmp = nullptr;
+            cap = total + 1;
+            e = dev_malloc((void**)&cnt, sizeof(int) * cap);
+            if (e == cudaSuccess) e = dev_malloc((void**)&fill, sizeof(int) * cap);
+            tmp_bytes = 0;
+            cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, cnt, fill, (int)cap, st);
+            if (e == cudaSuccess) e = dev_malloc(&tmp, std::max<size_t>(tmp_bytes, 16));
+            if (e != cudaSuccess) { release(); return (int)e; }
+        }
+        cudaMemsetAsync(cnt, 0, sizeof(int) * (total + 1), st);
+        k_grid_count<<<nb, 256, 0, st>>>(g, d_pts, n, cid, cnt);
+        if (pass == 0) {  // surface clouds fill few cells of the box: shrink the cells
+            cudaMemsetAsync(occ, 0, sizeof(unsigned long long), st);
+            k_count_occupied<<<(unsigned)std::min<i64>((total + 255) / 256, 148 * 16), 256, 0, st>>>(total, cnt, occ);
+            unsigned long long h_occ = 1;
+            cudaMemcpyAsync(&h_occ, occ, sizeof(h_occ), cudaMemcpyDeviceToHost, st);
+            e = cudaStreamSynchronize(st);
+            if (e != cudaSuccess) { release(); return (int)e; }
+            const double per = (double)n / (double)std::max<unsigned long long>(h_occ, 1);
+            if (per > 2.0 * k) {
+                cell = g.cell * std::sqrt(0.5 * k / per);
+                continue;
+            }
+        }
+        size_t tb = tmp_bytes;
+        cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, fill, (int)(total + 1), st);
+        cudaMemcpyAsync(cnt, fill, sizeof(int) * (total + 1), cudaMemcpyDeviceToDevice, st);  // cnt := start
+        k_grid_fill<<<nb, 256, 0, st>>>(n, cid, fill, items);
+        const unsigned qb = (unsigned)std::max<i64>(1, std::min<i64>((nq + 127) / 128, 148 * 64));
+        if (k <= 16) k_knn<16><<<qb, 128, 0, st>>>(g, d_pts, cnt, items, d_qry, nq, k, d_out);
+        else if (k <= 32) k_knn<32><<<qb, 128, 0, st>>>(g, d_pts, cnt, items, d_qry, nq, k, d_out);
+        else k_knn<64><<<qb, 128, 0, st>>>(g, d_pts, cnt, items, d_qry, nq, k, d_out);
+        break;
+    }
+    e = cudaStreamSynchronize(st);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    release();
+    return (int)e;
+}
+
 int spgemm_device(const DevCSR& A, const DevCSR& B, DevCSR& C, void* stream, std::string& err) {
     cudaStream_t st = (cudaStream_t)stream;
     C = DevCSR();

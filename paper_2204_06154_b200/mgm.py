@@ -102,6 +102,7 @@ _SIGS = {
     "mgm_bottom_ftrace_read": ([_vp, _i64p, ctypes.c_int, ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
     "mgm_host_morton": ([_f64p, _i64, _i64p], ctypes.c_int),
     "mgm_host_knn": ([_f64p, _i64, _f64p, _i64, ctypes.c_int, _i32p], ctypes.c_int),
+    "mgm_device_knn": ([_f64p, _i64, _f64p, _i64, ctypes.c_int, _i32p], ctypes.c_int),
     "mgm_host_wse": ([_f64p, _i64, _i64, _i64p], ctypes.c_int),
     "mgm_host_colouring": ([_i64, _i64p, _i32p, _i32p, ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
     "mgm_host_partition_level": ([_i64, _i64p, _i32p, _i32p, ctypes.c_int, _i32p, _i64, _i64p, _i32p, _i32p,
@@ -452,6 +453,16 @@ def mgm_host_knn(points, queries, k):
     out = np.empty((len(q), k), dtype=np.int32)
     _check(load_library().mgm_host_knn(_ptr(pts, _f64p), len(pts), _ptr(q, _f64p), len(q), k,
                                        _ptr(out, _i32p)))
+    return out
+
+
+def mgm_device_knn(points, queries, k):
+    """The kNN lists of mgm_host_knn computed by the GPU path of mgm_setup (k <= 64)."""
+    pts = np.ascontiguousarray(points, dtype=np.float64)
+    q = np.ascontiguousarray(queries, dtype=np.float64)
+    out = np.empty((len(q), k), dtype=np.int32)
+    _check(load_library().mgm_device_knn(_ptr(pts, _f64p), len(pts), _ptr(q, _f64p), len(q), k,
+                                         _ptr(out, _i32p)))
     return out
 
 

@@ -79,6 +79,32 @@ def test_fine_weights(name):
     assert (np.abs(wg - wo) / rowscale).max() <= 1e-10
 
 
+@pytest.mark.parametrize("case", ["sphere", "torus", "grid_ties", "coarse_queries"])
+def test_device_knn_equals_oracle(case):
+    """The GPU kNN (mgm_setup's O2 path) against the oracle's kNN lists, exactly: jittered
+    sphere and torus clouds, a lattice full of exact distance ties, coarse points queried
+    by fine ones (the interpolation stencils), k = 2 .. 50."""
+    import mgm_inputs as MI
+    import oracle as O
+    from paper_2204_06154_b200.mgm import mgm_device_knn
+
+    if case == "sphere":
+        x, _ = MI.fibonacci_sphere(20000, jitter=0.2, seed=2)
+        pairs = [(x, x, k) for k in (2, 15, 30, 50)]
+    elif case == "torus":
+        x, _ = MI.torus_cloud(12000, seed=3)
+        pairs = [(x, x, 30)]
+    elif case == "grid_ties":
+        g = np.stack(np.meshgrid(np.arange(14.), np.arange(13.), np.arange(3.), indexing="ij"), -1)
+        g = g.reshape(-1, 3)
+        pairs = [(g, g, 19), (g, g, 7)]
+    else:
+        x, _ = MI.fibonacci_sphere(16000, jitter=0.1, seed=5)
+        pairs = [(x[::4].copy(), x, 6), (x[::4].copy(), x, 12)]
+    for pts, q, k in pairs:
+        assert np.array_equal(mgm_device_knn(pts, q, k).astype(np.int64), O.knn(pts, q, k)), (case, k)
+
+
 def _rand(n, seed):
     return np.random.default_rng(seed).uniform(-1.0, 1.0, n)
 
