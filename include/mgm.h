@@ -152,12 +152,15 @@ mgm_status mgm_destroy(mgm_ctx* ctx);
  * f_dev, u_dev, rhs_dev, x_dev: device, K column-major vectors of n_points fp64 in
  * original order (column k at ptr + k*n_points).
  * mgm_vcycle_batch: one V-cycle per column (u in: guess, out: result).
- * mgm_solve_batch: standalone MGM on every column from x = 0 until every column's
- * ||f - L x|| / ||f|| <= tol or maxit; reports[K] (may be NULL): iterations = the first
- * cycle at which that column met tol, final_rel_residual after the last cycle. */
+ * mgm_solve_batch: from x = 0 on every column, krylov = 0: standalone MGM until
+ * every column's ||f - L x|| / ||f|| <= tol or maxit; reports[K] (may be NULL): iterations =
+ * the first cycle at which that column met tol, final_rel_residual after the last cycle.
+ * krylov = 1: K independent MGM-GMRES(restart) processes (right preconditioning, CGS2, as
+ * mgm_solve) sharing each batched V-cycle and SpMV; a column that meets tol stops
+ * iterating (its own count in reports[k].iterations, true final residual). */
 mgm_status mgm_vcycle_batch(mgm_ctx* ctx, int K, const double* f_dev, double* u_dev, void* cuda_stream);
 mgm_status mgm_solve_batch(mgm_ctx* ctx, int K, const double* rhs_dev, double* x_dev, double tol, int maxit,
-                           mgm_report* reports, void* cuda_stream);
+                           int krylov, mgm_report* reports, void* cuda_stream);
 
 /* ---- multi-GPU ----------------------------------
  * One process per GPU.  Every rank calls mgm_setup with the SAME cloud and parameters (the

@@ -31,11 +31,14 @@ __device__ __forceinline__ void gather_fma(double a, const double* xr, double* a
     }
 }
 
-// One colour of a Gauss-Seidel sweep for K right-hand sides (cf. k_gs_colour).
-template <int TPR, int CH, int K>
+// One colour of a Gauss-Seidel sweep for K right-hand sides (cf. k_gs_colour).  ZG: the
+// sweep starts from u = 0 (the first presmooth of a coarse level): only the diagonal and the
+// earlier-colour slots are read, as in k_gs_colour<..., ZG> (slw, nlow from pack_sell).
+template <int TPR, int CH, int K, bool ZG = false>
 __global__ void __launch_bounds__(256) k_gs_colour_b(int r0, int r1, int Wu, const int64_t* __restrict__ sptr,
                                                      const int* __restrict__ scol, const double* __restrict__ sval,
-                                                     const double* __restrict__ f, double* u) {
+                                                     const double* __restrict__ f, double* u,
+                                                     const int* __restrict__ slw, const uint8_t* __restrict__ nlow) {
     pdl_trigger();
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
     const int r = (r0 & ~31) + g / TPR;
@@ -54,7 +57,18 @@ __global__ void __launch_bounds__(256) k_gs_colour_b(int r0, int r1, int Wu, con
             w = (int)((sptr[(r >> 5) + 1] - s0) >> 5);
             base = s0 + (r & 31);
         }
-        fr.load(sval + base, scol + base, w, part);
+        int lim = 0;
+        if (ZG) {
+            w = slw[r >> 5];
+            lim = 1 + (int)nlow[r];
+        }
+        fr.load(sval + base, scol + base, ZG ? lim : w, part);
+        if (ZG) {
+#pragma unroll
+            for (int q = 0; q < CH; ++q)  // the diagonal (u_i = 0, term 0) and later colours
+                if (part + q * TPR == 0 || part + q * TPR >= lim) fr.c[q] = -1;
+            w = lim;
+        }
         d = ld_stream_f64(sval + base);
     } else {
         fr.load(sval, scol, 0, 0);
@@ -71,7 +85,7 @@ __global__ void __launch_bounds__(256) k_gs_colour_b(int r0, int r1, int Wu, con
 #pragma unroll
         for (int k = 0; k < K; ++k) {
             fv[k] = f[(int64_t)r * K + k];
-            uv[k] = u[(int64_t)r * K + k];
+            uv[k] = ZG ? 0.0 : u[(int64_t)r * K + k];
         }
     }
     for (int k0 = part;; k0 += TPR * CH) {
@@ -193,6 +207,24 @@ __global__ void k_scatter_b(int n, int K, int KK, const int* __restrict__ idx, c
         const int64_t r = t / KK, k = t % KK;
         if (k < K) out[k * n + idx[r]] = in[t];
     }
+}
+
+// y[r][k] = (acc ? y[r][k] : 0) + sgn * sum_{j < nv} c[j*K + k] V_j[r][k]   (V_j = V + j*stride)
+template <int K>
+__global__ void k_blincomb(int64_t n, int nv, const double* __restrict__ V, int64_t stride,
+                           const double* __restrict__ c, double sgn, int acc, double* y) {
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n * K; t += (int64_t)gridDim.x * blockDim.x) {
+        const int k = (int)(t % K);
+        double s = acc ? y[t] : 0.0;
+        for (int j = 0; j < nv; ++j) s = fma(sgn * c[j * K + k], V[j * stride + t], s);
+        y[t] = s;
+    }
+}
+// y[r][k] = x[r][k] * c[k]
+template <int K>
+__global__ void k_bscale(int64_t n, const double* __restrict__ x, const double* __restrict__ c, double* __restrict__ y) {
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n * K; t += (int64_t)gridDim.x * blockDim.x)
+        y[t] = x[t] * c[t % K];
 }
 
 // out[k] = sum_r a[r*K+k] b[r*K+k], deterministic (block partials in fixed order, last-block finish)

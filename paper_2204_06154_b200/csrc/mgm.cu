@@ -407,6 +407,9 @@ struct mgm_ctx {
     std::vector<double*> bu, bf, bt;
     cudaGraphExec_t bgraph[9] = {};
     double* bres = nullptr;  // residual (n x K)
+    // batched GMRES: basis (restart + 1) x n x K, w, x, b (n x K); dots (device) + pinned mirror
+    double *bV = nullptr, *bw = nullptr, *bx = nullptr, *bb = nullptr, *bdh = nullptr, *bhh = nullptr;
+    int bgK = 0;
     // multi-GPU (mgm_dist_attach / mgm_dist_attach_fake): levels 0..D-1 partitioned by Morton row
     // blocks, D..p-1 replicated
     int rank = 0, nranks = 1;
@@ -460,8 +463,28 @@ cudaError_t mgm::dev_malloc(void** p, size_t bytes) {
     }
     return cudaMalloc(p, bytes);
 }
+// Setup defers cudaFree to its end: cudaFree synchronises the whole device, which would
+// stall the setup's concurrent threads (Galerkin stream, colouring) on each other's work.
+struct DeferFree {
+    std::mutex mu;
+    std::vector<void*> ptrs;
+    ~DeferFree() {
+        for (void* q : ptrs) cudaFree(q);
+    }
+};
+static thread_local DeferFree* g_defer = nullptr;
+struct DeferScope {
+    DeferFree* prev;
+    explicit DeferScope(DeferFree* d) : prev(g_defer) { g_defer = d; }
+    ~DeferScope() { g_defer = prev; }
+};
 void mgm::dev_free(void* p) {
     if (!p) return;
+    if (g_defer && !(g_alloc && g_alloc->alloc)) {
+        std::lock_guard<std::mutex> lk(g_defer->mu);
+        g_defer->ptrs.push_back(p);
+        return;
+    }
     if (g_alloc && g_alloc->alloc) {
         if (g_alloc->release) g_alloc->release(p, g_alloc->user);
         return;
@@ -962,6 +985,8 @@ struct SetupTimer {
 };
 
 mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i64 N) {
+    DeferFree deferred;  // (destroyed last: after every setup thread has been joined)
+    DeferScope defer_(&deferred);
     SetupTimer tm;
     const auto& sp = ctx->sp;
     const auto& lp = ctx->lp;
@@ -1203,6 +1228,7 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
     } rap;
     rap.th = std::thread([&] {
         AllocScope as_(ctx);
+        DeferScope defer_(&deferred);
         cudaStream_t rs = nullptr;
         if (cudaStreamCreateWithFlags(&rs, cudaStreamNonBlocking) != cudaSuccess) {
             rap.status = MGM_ERR_CUDA;
@@ -2930,22 +2956,30 @@ static i64 gs_wave_threads_b(int tpr, int block) {
     return cache[ti][bi] = (i64)per * nsm * block;
 }
 template <int K>
-static void b_gs(mgm_ctx* ctx, const Level& L, int j, int r0, int r1, cudaStream_t st) {
+static void b_gs(mgm_ctx* ctx, const Level& L, int j, int r0, int r1, cudaStream_t st, bool zg = false) {
     const int span = r1 - (r0 & ~31);
     const int bs = L.gs_block;
     auto go = [&](auto kern, int tpr) {
         launch(true, kern, blocks_for((i64)span * tpr, bs), bs, 0, st, r0, r1, L.uniform_w, (const i64*)L.sptr,
-               (const i32*)L.scol, (const double*)L.sval, (const double*)ctx->bf[j], ctx->bu[j]);
+               (const i32*)L.scol, (const double*)L.sval, (const double*)ctx->bf[j], ctx->bu[j],
+               (const i32*)L.slw, (const uint8_t*)L.nlow);
     };
     // a colour just above one (register-limited) wave: halve the threads per row (cf. launch_gs)
     int tpr = std::min(L.tpr, g_batch_tpr_cap);
     while (tpr > 1 && (i64)span * tpr > gs_wave_threads_b<K>(tpr, bs) &&
            (i64)span * (tpr / 2) <= gs_wave_threads_b<K>(tpr / 2, bs))
         tpr /= 2;
-    if (tpr == 1) go(k_gs_colour_b<1, CHUNK, K>, 1);
-    else if (tpr == 2) go(k_gs_colour_b<2, CHUNK, K>, 2);
-    else if (tpr == 4) go(k_gs_colour_b<4, CHUNK, K>, 4);
-    else go(k_gs_colour_b<8, CHUNK, K>, 8);
+    if (zg) {
+        if (tpr == 1) go(k_gs_colour_b<1, CHUNK, K, true>, 1);
+        else if (tpr == 2) go(k_gs_colour_b<2, CHUNK, K, true>, 2);
+        else if (tpr == 4) go(k_gs_colour_b<4, CHUNK, K, true>, 4);
+        else go(k_gs_colour_b<8, CHUNK, K, true>, 8);
+    } else {
+        if (tpr == 1) go(k_gs_colour_b<1, CHUNK, K>, 1);
+        else if (tpr == 2) go(k_gs_colour_b<2, CHUNK, K>, 2);
+        else if (tpr == 4) go(k_gs_colour_b<4, CHUNK, K>, 4);
+        else go(k_gs_colour_b<8, CHUNK, K>, 8);
+    }
 }
 template <int MODE, int K>
 static void b_spmv(int tpr, i64 r1, const i64* sptr, const i32* scol, const double* sval, const double* x,
@@ -2966,13 +3000,15 @@ static void enqueue_vcycle_b(mgm_ctx* ctx, cudaStream_t st) {
     ctx->trace_labels.clear();
     const int nu1 = ctx->lp.nu1, nu2 = ctx->lp.nu2;
     const bool pre_b = ctx->lp.smoother == 1, post_b = ctx->lp.smoother == 1 || ctx->lp.smoother == 2;
-    auto sweep = [&](int j, bool backward) {
+    auto sweep = [&](int j, bool backward, bool zg = false) {
         const Level& L = lv[j];
         for (int q = 0; q < L.ncol; ++q) {
             const int c = backward ? L.ncol - 1 - q : q;
-            if (L.coff[c + 1] > L.coff[c]) b_gs<K>(ctx, L, j, (int)L.coff[c], (int)L.coff[c + 1], st);
+            if (L.coff[c + 1] > L.coff[c]) b_gs<K>(ctx, L, j, (int)L.coff[c], (int)L.coff[c + 1], st, zg);
         }
     };
+    // the first presmooth of a coarse level starts from zero: zero-guess colour kernels
+    auto zg_ok = [&](int j) { return !pre_b && !ctx->poisson && lv[j].slw && lv[j].nlow && !ctx->no_zg; };
     auto coarse = [&]() {
         const int m = ctx->nc;
         launch(true, k_dense_mv_b<K>, blocks_for((i64)m * K, 256), 256, 0, st, m, (const double*)ctx->ainv,
@@ -2988,7 +3024,7 @@ static void enqueue_vcycle_b(mgm_ctx* ctx, cudaStream_t st) {
         const Level& L = lv[j];
         if (j > 0) {
             cudaMemsetAsync(ctx->bu[j], 0, sizeof(double) * L.n * K, st);
-            for (int s = 0; s < nu1; ++s) sweep(j, pre_b);
+            for (int s = 0; s < nu1; ++s) sweep(j, pre_b, s == 0 && zg_ok(j));
         }
         if (j > 0) stamp(ctx, "zero+presmooth", j, st);
         b_spmv<1, K>(L.stpr, L.n, L.sptr, L.scol, L.sval, ctx->bu[j], ctx->bf[j], ctx->bt[j], st);
@@ -3771,13 +3807,232 @@ mgm_status mgm_vcycle_batch(mgm_ctx* ctx, int K, const double* f_dev, double* u_
     return MGM_OK;
 }
 
+}  // extern "C"
+
+// K independent right-preconditioned GMRES(restart) processes (CGS2, as gmres_lib) sharing
+// every operator pass: one batched V-cycle (from zero) and one batched SpMV per Arnoldi step
+// for all K columns; Givens rotations per column on the host.  A column that met tol (or
+// broke down) is frozen: its further basis vectors are zero and its update uses the steps it
+// took, so each column follows its own single-RHS iteration.  bf[0] holds b, x -> bx.
+template <int K>
+static mgm_status gmres_batch(mgm_ctx* ctx, int Kreal, double tol, int maxit, mgm_report* reports, cudaStream_t st) {
+    const i64 N = ctx->N;
+    const int m = ctx->restart;
+    const Level& L0 = ctx->lv[0];
+    if (ctx->bgK < K) {
+        for (double** q : {&ctx->bV, &ctx->bw, &ctx->bx, &ctx->bb, &ctx->bdh})
+            if (*q) { dev_free(*q); *q = nullptr; }
+        if (ctx->bhh) { cudaFreeHost(ctx->bhh); ctx->bhh = nullptr; }
+        CK(dalloc(&ctx->bV, (i64)(m + 1) * N * K));
+        CK(dalloc(&ctx->bw, N * K));
+        CK(dalloc(&ctx->bx, N * K));
+        CK(dalloc(&ctx->bb, N * K));
+        CK(dalloc(&ctx->bdh, (i64)(2 * (m + 1) + 4) * K));
+        CK(cudaMallocHost((void**)&ctx->bhh, sizeof(double) * (3 * (m + 1) + 4) * K));
+        ctx->bgK = K;
+    }
+    const i64 nk = N * K;
+    const unsigned nb = blocks_for(nk, 256);
+    double *V = ctx->bV, *w = ctx->bw, *x = ctx->bx, *b = ctx->bb;
+    double *h1 = ctx->bdh, *h2 = ctx->bdh + (i64)(m + 1) * K, *nr = ctx->bdh + (i64)2 * (m + 1) * K;
+    double* coef = nr + K;  // (K scale factors; reused for the y coefficients below: m * K)
+    double* hh = ctx->bhh;
+    mgm_status s;
+    CK(cudaMemcpyAsync(b, ctx->bf[0], sizeof(double) * nk, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemsetAsync(x, 0, sizeof(double) * nk, st));
+    enqueue_bdot(ctx, K, N, b, b, nr, st);
+    CK(cudaMemcpyAsync(hh, nr, sizeof(double) * K, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    std::vector<double> bnorm(K), H((size_t)K * (m + 1) * m), cs((size_t)K * m), sn((size_t)K * m),
+        g((size_t)K * (m + 1)), y((size_t)m * K), sc(K), rel(K, 0.0);
+    std::vector<int> its(K, 0), kdone(K, 0), hist(K, 0);
+    std::vector<char> conv(K, 0), active(K, 0);
+    for (int c = 0; c < K; ++c) {
+        bnorm[c] = std::sqrt(hh[c]);
+        if (c >= Kreal || bnorm[c] == 0.0) conv[c] = 1;  // (padding columns are zero)
+    }
+    auto Hc = [&](int c, int i, int k) -> double& { return H[((size_t)c * (m + 1) + i) * m + k]; };
+    // pinned mirror: h1 | h2 | norms (read back), then two upload areas: y (m K) and K scalars
+    // (each area is rewritten only after a stream synchronisation or in the other area)
+    double* up_y = hh + (size_t)(2 * (m + 1) + 1) * K;
+    double* up_k = up_y + (size_t)(m + 1) * K;
+    auto upload_coef = [&](const std::vector<double>& v, double* dst) -> mgm_status {
+        double* src = v.size() > (size_t)K ? up_y : up_k;
+        std::copy(v.begin(), v.end(), src);
+        CK(cudaMemcpyAsync(dst, src, sizeof(double) * v.size(), cudaMemcpyHostToDevice, st));
+        return MGM_OK;
+    };
+    bool first = true;
+    int cycles_its = 0;  // Arnoldi steps taken (shared by all columns)
+    while (true) {
+        // r = b - A x ; beta per column
+        if (first)
+            CK(cudaMemcpyAsync(w, b, sizeof(double) * nk, cudaMemcpyDeviceToDevice, st));
+        else
+            b_spmv<1, K>(L0.stpr, N, L0.sptr, L0.scol, L0.sval, x, b, w, st);
+        first = false;
+        enqueue_bdot(ctx, K, N, w, w, nr, st);
+        CK(cudaMemcpyAsync(hh, nr, sizeof(double) * K, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        bool any = false;
+        for (int c = 0; c < K; ++c) {
+            const double beta = std::sqrt(hh[c]);
+            active[c] = !conv[c] && its[c] < maxit && !(beta / bnorm[c] <= tol);
+            if (!conv[c] && beta / bnorm[c] <= tol) conv[c] = 1;
+            sc[c] = active[c] ? 1.0 / beta : 0.0;
+            std::fill(g.begin() + (size_t)c * (m + 1), g.begin() + (size_t)(c + 1) * (m + 1), 0.0);
+            g[(size_t)c * (m + 1)] = beta;
+            kdone[c] = 0;
+            any = any || active[c];
+        }
+        if (!any) break;
+        std::fill(H.begin(), H.end(), 0.0);
+        if ((s = upload_coef(sc, coef))) return s;
+        launch(false, k_bscale<K>, nb, 256, 0, st, nk, (const double*)w, (const double*)coef, V);
+        for (int k = 0; k < m; ++k) {
+            // z = M^{-1} v_k (batched V-cycle from zero), w = A z
+            CK(cudaMemcpyAsync(ctx->bf[0], V + (i64)k * nk, sizeof(double) * nk, cudaMemcpyDeviceToDevice, st));
+            CK(cudaMemsetAsync(ctx->bu[0], 0, sizeof(double) * nk, st));
+            if ((s = run_vcycle_b(ctx, K, st))) return s;
+            b_spmv<0, K>(L0.stpr, N, L0.sptr, L0.scol, L0.sval, ctx->bu[0], nullptr, w, st);
+            ++cycles_its;
+            const int k1 = k + 1;
+            // CGS2 per column: h1 = V^T w; w -= V h1; h2 = V^T w; w -= V h2; h = h1 + h2
+            for (int j = 0; j < k1; ++j) enqueue_bdot(ctx, K, N, V + (i64)j * nk, w, h1 + (i64)j * K, st);
+            launch(false, k_blincomb<K>, nb, 256, 0, st, nk, k1, (const double*)V, nk, (const double*)h1, -1.0, 1, w);
+            for (int j = 0; j < k1; ++j) enqueue_bdot(ctx, K, N, V + (i64)j * nk, w, h2 + (i64)j * K, st);
+            launch(false, k_blincomb<K>, nb, 256, 0, st, nk, k1, (const double*)V, nk, (const double*)h2, -1.0, 1, w);
+            enqueue_bdot(ctx, K, N, w, w, nr, st);
+            CK(cudaMemcpyAsync(hh, h1, sizeof(double) * k1 * K, cudaMemcpyDeviceToHost, st));
+            CK(cudaMemcpyAsync(hh + (m + 1) * K, h2, sizeof(double) * k1 * K, cudaMemcpyDeviceToHost, st));
+            CK(cudaMemcpyAsync(hh + 2 * (m + 1) * K, nr, sizeof(double) * K, cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            bool still = false;
+            for (int c = 0; c < K; ++c) {
+                if (!active[c]) {
+                    sc[c] = 0.0;
+                    continue;
+                }
+                for (int i = 0; i < k1; ++i) Hc(c, i, k) = hh[(size_t)i * K + c] + hh[(size_t)(m + 1) * K + (size_t)i * K + c];
+                const double hk1 = std::sqrt(hh[(size_t)2 * (m + 1) * K + c]);
+                Hc(c, k1, k) = hk1;
+                double* csc = cs.data() + (size_t)c * m;
+                double* snc = sn.data() + (size_t)c * m;
+                double* gc = g.data() + (size_t)c * (m + 1);
+                for (int i = 0; i < k; ++i) {
+                    const double t = csc[i] * Hc(c, i, k) + snc[i] * Hc(c, i + 1, k);
+                    Hc(c, i + 1, k) = -snc[i] * Hc(c, i, k) + csc[i] * Hc(c, i + 1, k);
+                    Hc(c, i, k) = t;
+                }
+                const double den = std::hypot(Hc(c, k, k), hk1);
+                csc[k] = Hc(c, k, k) / den;
+                snc[k] = hk1 / den;
+                Hc(c, k, k) = den;
+                Hc(c, k1, k) = 0.0;
+                gc[k1] = -snc[k] * gc[k];
+                gc[k] = csc[k] * gc[k];
+                rel[c] = std::fabs(gc[k1]) / bnorm[c];
+                ++its[c];
+                kdone[c] = k1;
+                if (reports && reports[c].history && hist[c] < reports[c].history_cap) reports[c].history[hist[c]++] = rel[c];
+                if (!std::isfinite(rel[c])) return fail(ctx, MGM_ERR_BREAKDOWN, "non-finite GMRES residual", c);
+                if (rel[c] <= tol || its[c] >= maxit || hk1 == 0.0) {
+                    active[c] = 0;  // frozen: further basis vectors of this column are zero
+                    if (rel[c] <= tol) conv[c] = 1;
+                    sc[c] = 0.0;
+                } else {
+                    sc[c] = 1.0 / hk1;
+                    still = true;
+                }
+            }
+            if (!still || k1 == m) break;
+            if ((s = upload_coef(sc, coef))) return s;
+            launch(false, k_bscale<K>, nb, 256, 0, st, nk, (const double*)w, (const double*)coef, V + (i64)k1 * nk);
+        }
+        // x += M^{-1} V y per column (y = 0 beyond the column's own steps)
+        int kmax = 0;
+        std::fill(y.begin(), y.end(), 0.0);
+        for (int c = 0; c < K; ++c) {
+            const int kd = kdone[c];
+            kmax = std::max(kmax, kd);
+            std::vector<double> yc(kd);
+            for (int i = kd - 1; i >= 0; --i) {
+                double sacc = g[(size_t)c * (m + 1) + i];
+                for (int j2 = i + 1; j2 < kd; ++j2) sacc -= Hc(c, i, j2) * yc[j2];
+                yc[i] = sacc / Hc(c, i, i);
+            }
+            for (int i = 0; i < kd; ++i) y[(size_t)i * K + c] = yc[i];
+        }
+        if (kmax > 0) {
+            std::vector<double> yv(y.begin(), y.begin() + (size_t)kmax * K);
+            if ((s = upload_coef(yv, h1))) return s;
+            launch(false, k_blincomb<K>, nb, 256, 0, st, nk, kmax, (const double*)V, nk, (const double*)h1, 1.0, 0,
+                   ctx->bf[0]);
+            CK(cudaMemsetAsync(ctx->bu[0], 0, sizeof(double) * nk, st));
+            if ((s = run_vcycle_b(ctx, K, st))) return s;
+            std::vector<double> one(K, 1.0);
+            if ((s = upload_coef(one, coef))) return s;
+            launch(false, k_blincomb<K>, nb, 256, 0, st, nk, 1, (const double*)ctx->bu[0], nk, (const double*)coef,
+                   1.0, 1, x);
+        }
+        bool left = false;
+        for (int c = 0; c < K; ++c) left = left || (!conv[c] && its[c] < maxit);
+        if (!left) break;
+    }
+    // true residuals
+    b_spmv<1, K>(L0.stpr, N, L0.sptr, L0.scol, L0.sval, x, b, w, st);
+    enqueue_bdot(ctx, K, N, w, w, nr, st);
+    CK(cudaMemcpyAsync(hh, nr, sizeof(double) * K, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (reports)
+        for (int c = 0; c < Kreal; ++c) {
+            reports[c].iterations = its[c];
+            reports[c].converged = conv[c];
+            reports[c].final_rel_residual = bnorm[c] > 0.0 ? std::sqrt(hh[c]) / bnorm[c] : 0.0;
+            reports[c].lambda = 0.0;
+        }
+    (void)cycles_its;
+    return MGM_OK;
+}
+
+extern "C" {
+
 mgm_status mgm_solve_batch(mgm_ctx* ctx, int K, const double* rhs_dev, double* x_dev, double tol, int maxit,
-                           mgm_report* reports, void* cuda_stream) {
+                           int krylov, mgm_report* reports, void* cuda_stream) {
     AllocScope as_(ctx);
-    if (K == 1) return mgm_solve(ctx, rhs_dev, nullptr, x_dev, tol, maxit, 0, reports, cuda_stream);
+    if (krylov != 0 && krylov != 1) return MGM_ERR_ARG;
+    if (K == 1) return mgm_solve(ctx, rhs_dev, nullptr, x_dev, tol, maxit, krylov, reports, cuda_stream);
     mgm_status s = batch_check(ctx, K);
     if (s) return s;
     if (!rhs_dev || !x_dev || !(tol >= 0) || maxit < 0) return MGM_ERR_ARG;
+    if (krylov == 1) {
+        cudaStream_t st = (cudaStream_t)cuda_stream;
+        const i64 N = ctx->N;
+        const int KK = batch_width(K);
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        cudaEventRecord(e0, st);
+        k_gather_b<<<blocks_for(N * KK, 256), 256, 0, st>>>((int)N, K, KK, ctx->d_lib2orig, rhs_dev, ctx->bf[0]);
+        s = KK == 2 ? gmres_batch<2>(ctx, K, tol, maxit, reports, st)
+          : KK == 4 ? gmres_batch<4>(ctx, K, tol, maxit, reports, st)
+                    : gmres_batch<8>(ctx, K, tol, maxit, reports, st);
+        if (s) return s;
+        k_scatter_b<<<blocks_for(N * KK, 256), 256, 0, st>>>((int)N, K, KK, ctx->d_lib2orig, ctx->bx, x_dev);
+        cudaEventRecord(e1, st);
+        CK(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        if (reports)
+            for (int k = 0; k < K; ++k) {
+                reports[k].solve_ms = ms;
+                reports[k].setup_ms = ctx->setup_ms;
+            }
+        CK(cudaGetLastError());
+        return MGM_OK;
+    }
     cudaStream_t st = (cudaStream_t)cuda_stream;
     const i64 N = ctx->N;
     const int KK = batch_width(K);
@@ -4007,6 +4262,9 @@ mgm_status mgm_destroy(mgm_ctx* ctx) {
     for (auto& gx : ctx->bgraph)
         if (gx) cudaGraphExecDestroy(gx);
     if (ctx->bres) dev_free(ctx->bres);
+    for (double* ptr : {ctx->bV, ctx->bw, ctx->bx, ctx->bb, ctx->bdh})
+        if (ptr) dev_free(ptr);
+    if (ctx->bhh) cudaFreeHost(ctx->bhh);
     if (ctx->ainv) dev_free(ctx->ainv);
     if (ctx->dB) dev_free(ctx->dB);
     for (auto& T : ctx->timer)

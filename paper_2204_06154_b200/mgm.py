@@ -72,7 +72,7 @@ _SIGS = {
     "mgm_destroy": ([_vp], ctypes.c_int),
     "mgm_nccl_unique_id": ([_vp], ctypes.c_int),
     "mgm_vcycle_batch": ([_vp, ctypes.c_int, _vp, _vp, _vp], ctypes.c_int),
-    "mgm_solve_batch": ([_vp, ctypes.c_int, _vp, _vp, ctypes.c_double, ctypes.c_int,
+    "mgm_solve_batch": ([_vp, ctypes.c_int, _vp, _vp, ctypes.c_double, ctypes.c_int, ctypes.c_int,
                          ctypes.POINTER(Report), _vp], ctypes.c_int),
     "mgm_dist_attach": ([_vp, ctypes.c_int, ctypes.c_int, _vp], ctypes.c_int),
     "mgm_local_rows": ([_vp, _i64p, _i64p], ctypes.c_int),
@@ -265,15 +265,16 @@ def mgm_vcycle_batch(ctx, K: int, f, u, stream=None):
                                            _vp(_stream_ptr(stream))), ctx)
 
 
-def mgm_solve_batch(ctx, K: int, rhs, x, tol=1e-10, maxit=500, stream=None, history_cap=512):
-    """Standalone MGM on K right-hand sides at once: rhs, x (K, N) CUDA float64 tensors."""
+def mgm_solve_batch(ctx, K: int, rhs, x, tol=1e-10, maxit=500, stream=None, history_cap=512, krylov=0):
+    """K right-hand sides at once (rhs, x: (K, N) CUDA float64 tensors): standalone MGM
+    (krylov=0) or K MGM-GMRES processes sharing every operator pass (krylov=1)."""
     assert rhs.is_contiguous() and x.is_contiguous() and rhs.shape == x.shape and rhs.shape[0] == K
     hists = [np.zeros(history_cap) for _ in range(K)]
     reps = (Report * K)()
     for k in range(K):
         reps[k].history = _ptr(hists[k], _f64p)
         reps[k].history_cap = history_cap
-    _check(load_library().mgm_solve_batch(ctx, K, _vp(rhs.data_ptr()), _vp(x.data_ptr()), tol, maxit,
+    _check(load_library().mgm_solve_batch(ctx, K, _vp(rhs.data_ptr()), _vp(x.data_ptr()), tol, maxit, krylov,
                                           reps, _vp(_stream_ptr(stream))), ctx)
     return [_report(reps[k], hists[k]) for k in range(K)]
 

@@ -976,6 +976,32 @@ def test_vcycle_batch_matches_oracle(K):
         assert relmax(ug[k], P.ref.vcycle(F[k], U[k])) <= 1e-12, k
 
 
+@pytest.mark.parametrize("name,K", [("cfg1", 4), ("cfg1", 3), ("torus20000", 8)])
+def test_solve_batch_gmres_matches_oracle(name, K):
+    """K MGM-GMRES processes sharing every batched operator pass (mgm_solve_batch, krylov=1):
+    every column converges like its own oracle GMRES solve (iterations within +-1, solutions
+    to 1e-9, true final residual <= 1e-10); an all-zero column returns x = 0 with 0
+    iterations; K = 3 pads to width 4."""
+    import torch
+    from paper_2204_06154_b200 import mgm_solve_batch
+
+    P = pair(name)
+    n = len(P.w.points)
+    cols = [P.w.rhs] + [_rand(n, 30 + k) for k in range(K - 1)]
+    cols[1] = np.zeros(n)
+    R = np.stack(cols)
+    x = torch.zeros(K, n, dtype=torch.float64, device="cuda")
+    reps = mgm_solve_batch(P.gpu.ctx, K, torch.from_numpy(R).cuda(), x, tol=1e-10, maxit=200, krylov=1)
+    xg = x.cpu().numpy()
+    assert not xg[1].any() and reps[1].converged and reps[1].iterations == 0
+    for k in [0] + list(range(2, K)):
+        xr, rr = P.ref.solve(R[k], tol=1e-10, krylov=1, maxit=200)
+        assert reps[k].converged and rr.converged
+        assert abs(reps[k].iterations - rr.iterations) <= 1, (k, reps[k].iterations, rr.iterations)
+        assert reps[k].final_rel_residual <= 1e-10
+        assert np.linalg.norm(xg[k] - xr) / np.linalg.norm(xr) <= 1e-9
+
+
 def test_solve_batch_matches_oracle():
     """Batched standalone MGM: every column converges like its own oracle solve (iterations
     within +-1, solutions to 1e-9); an all-zero column returns x = 0."""
