@@ -406,6 +406,7 @@ struct mgm_ctx {
     int bK = 0;
     std::vector<double*> bu, bf, bt;
     cudaGraphExec_t bgraph[9] = {};
+    cudaGraphExec_t bgraph_zg[9] = {};  // from a zero level-0 guess (batched GMRES)
     double* bres = nullptr;  // residual (n x K)
     // batched GMRES: basis (restart + 1) x n x K, w, x, b (n x K); dots (device) + pinned mirror
     double *bV = nullptr, *bw = nullptr, *bx = nullptr, *bb = nullptr, *bdh = nullptr, *bhh = nullptr;
@@ -2993,7 +2994,7 @@ static void b_spmv(int tpr, i64 r1, const i64* sptr, const i32* scol, const doub
     else go(k_sell_spmv_b<MODE, 8, CHUNK, K>, 8);
 }
 template <int K>
-static void enqueue_vcycle_b(mgm_ctx* ctx, cudaStream_t st) {
+static void enqueue_vcycle_b(mgm_ctx* ctx, cudaStream_t st, bool zero0) {
     auto& lv = ctx->lv;
     const int p = ctx->p;
     ctx->ntrace = 0;
@@ -3018,7 +3019,7 @@ static void enqueue_vcycle_b(mgm_ctx* ctx, cudaStream_t st) {
     // levels >= D: the dense bottom B_D applied to the K columns at once (dense_bottom.cuh)
     const int D = ctx->denseJ > 0 ? ctx->denseJ : p - 1;
     stamp(ctx, "start", 0, st);
-    for (int s = 0; s < nu1; ++s) sweep(0, pre_b);                                  // line 4
+    for (int s = 0; s < nu1; ++s) sweep(0, pre_b, zero0 && s == 0 && zg_ok(0));   // line 4
     stamp(ctx, "presmooth", 0, st);
     for (int j = 0; j < D; ++j) {                                                   // lines 5-9
         const Level& L = lv[j];
@@ -3043,11 +3044,11 @@ static void enqueue_vcycle_b(mgm_ctx* ctx, cudaStream_t st) {
         stamp(ctx, "interp+postsmooth", j, st);
     }
 }
-static void enqueue_vcycle_bk(mgm_ctx* ctx, int K, cudaStream_t st) {
+static void enqueue_vcycle_bk(mgm_ctx* ctx, int K, cudaStream_t st, bool zero0) {
     switch (K) {
-        case 2: enqueue_vcycle_b<2>(ctx, st); break;
-        case 4: enqueue_vcycle_b<4>(ctx, st); break;
-        default: enqueue_vcycle_b<8>(ctx, st); break;
+        case 2: enqueue_vcycle_b<2>(ctx, st, zero0); break;
+        case 4: enqueue_vcycle_b<4>(ctx, st, zero0); break;
+        default: enqueue_vcycle_b<8>(ctx, st, zero0); break;
     }
 }
 // Alg. 3 lines 6-14 for the levels J..p-1 from e_J = 0 on K interleaved columns (the batched
@@ -3179,15 +3180,19 @@ static mgm_status ensure_batch(mgm_ctx* ctx, int K) {
     CK(dalloc(&ctx->bres, ctx->N * K));
     for (auto& gx : ctx->bgraph)
         if (gx) { cudaGraphExecDestroy(gx); gx = nullptr; }
+    for (auto& gx : ctx->bgraph_zg)
+        if (gx) { cudaGraphExecDestroy(gx); gx = nullptr; }
     ctx->bK = K;
     return MGM_OK;
 }
-static mgm_status run_vcycle_b(mgm_ctx* ctx, int K, cudaStream_t st) {
-    if (!ctx->bgraph[K]) {
+// zero0: the level-0 guess is zero (Krylov preconditioning): zero-guess first presmooth
+static mgm_status run_vcycle_b(mgm_ctx* ctx, int K, cudaStream_t st, bool zero0 = false) {
+    cudaGraphExec_t& gx = zero0 ? ctx->bgraph_zg[K] : ctx->bgraph[K];
+    if (!gx) {
         cudaGraph_t g;
         CK(cudaStreamBeginCapture(ctx->st, cudaStreamCaptureModeThreadLocal));
         g_launch_err.clear();
-        enqueue_vcycle_bk(ctx, K, ctx->st);
+        enqueue_vcycle_bk(ctx, K, ctx->st, zero0);
         const cudaError_t ce = cudaStreamEndCapture(ctx->st, &g);
         if (ce != cudaSuccess || !g_launch_err.empty()) {
             ctx->err = "batched V-cycle capture failed: " + std::string(cudaGetErrorString(ce)) + "; " + g_launch_err;
@@ -3195,10 +3200,10 @@ static mgm_status run_vcycle_b(mgm_ctx* ctx, int K, cudaStream_t st) {
             cudaGetLastError();
             return MGM_ERR_CUDA;
         }
-        CK(cudaGraphInstantiate(&ctx->bgraph[K], g, 0));
+        CK(cudaGraphInstantiate(&gx, g, 0));
         cudaGraphDestroy(g);
     }
-    CK(cudaGraphLaunch(ctx->bgraph[K], st));
+    CK(cudaGraphLaunch(gx, st));
     return MGM_OK;
 }
 static void enqueue_bdot(mgm_ctx* ctx, int K, i64 n, const double* a, const double* b, double* out, cudaStream_t st) {
@@ -3888,20 +3893,19 @@ static mgm_status gmres_batch(mgm_ctx* ctx, int Kreal, double tol, int maxit, mg
         if (!any) break;
         std::fill(H.begin(), H.end(), 0.0);
         if ((s = upload_coef(sc, coef))) return s;
-        launch(false, k_bscale<K>, nb, 256, 0, st, nk, (const double*)w, (const double*)coef, V);
+        launch(false, k_bscale<K>, nb, 256, 0, st, N, (const double*)w, (const double*)coef, V);
         for (int k = 0; k < m; ++k) {
             // z = M^{-1} v_k (batched V-cycle from zero), w = A z
             CK(cudaMemcpyAsync(ctx->bf[0], V + (i64)k * nk, sizeof(double) * nk, cudaMemcpyDeviceToDevice, st));
-            CK(cudaMemsetAsync(ctx->bu[0], 0, sizeof(double) * nk, st));
-            if ((s = run_vcycle_b(ctx, K, st))) return s;
+            if ((s = run_vcycle_b(ctx, K, st, true))) return s;
             b_spmv<0, K>(L0.stpr, N, L0.sptr, L0.scol, L0.sval, ctx->bu[0], nullptr, w, st);
             ++cycles_its;
             const int k1 = k + 1;
             // CGS2 per column: h1 = V^T w; w -= V h1; h2 = V^T w; w -= V h2; h = h1 + h2
             for (int j = 0; j < k1; ++j) enqueue_bdot(ctx, K, N, V + (i64)j * nk, w, h1 + (i64)j * K, st);
-            launch(false, k_blincomb<K>, nb, 256, 0, st, nk, k1, (const double*)V, nk, (const double*)h1, -1.0, 1, w);
+            launch(false, k_blincomb<K>, nb, 256, 0, st, N, k1, (const double*)V, nk, (const double*)h1, -1.0, 1, w);
             for (int j = 0; j < k1; ++j) enqueue_bdot(ctx, K, N, V + (i64)j * nk, w, h2 + (i64)j * K, st);
-            launch(false, k_blincomb<K>, nb, 256, 0, st, nk, k1, (const double*)V, nk, (const double*)h2, -1.0, 1, w);
+            launch(false, k_blincomb<K>, nb, 256, 0, st, N, k1, (const double*)V, nk, (const double*)h2, -1.0, 1, w);
             enqueue_bdot(ctx, K, N, w, w, nr, st);
             CK(cudaMemcpyAsync(hh, h1, sizeof(double) * k1 * K, cudaMemcpyDeviceToHost, st));
             CK(cudaMemcpyAsync(hh + (m + 1) * K, h2, sizeof(double) * k1 * K, cudaMemcpyDeviceToHost, st));
@@ -3947,7 +3951,7 @@ static mgm_status gmres_batch(mgm_ctx* ctx, int Kreal, double tol, int maxit, mg
             }
             if (!still || k1 == m) break;
             if ((s = upload_coef(sc, coef))) return s;
-            launch(false, k_bscale<K>, nb, 256, 0, st, nk, (const double*)w, (const double*)coef, V + (i64)k1 * nk);
+            launch(false, k_bscale<K>, nb, 256, 0, st, N, (const double*)w, (const double*)coef, V + (i64)k1 * nk);
         }
         // x += M^{-1} V y per column (y = 0 beyond the column's own steps)
         int kmax = 0;
@@ -3966,13 +3970,12 @@ static mgm_status gmres_batch(mgm_ctx* ctx, int Kreal, double tol, int maxit, mg
         if (kmax > 0) {
             std::vector<double> yv(y.begin(), y.begin() + (size_t)kmax * K);
             if ((s = upload_coef(yv, h1))) return s;
-            launch(false, k_blincomb<K>, nb, 256, 0, st, nk, kmax, (const double*)V, nk, (const double*)h1, 1.0, 0,
+            launch(false, k_blincomb<K>, nb, 256, 0, st, N, kmax, (const double*)V, nk, (const double*)h1, 1.0, 0,
                    ctx->bf[0]);
-            CK(cudaMemsetAsync(ctx->bu[0], 0, sizeof(double) * nk, st));
-            if ((s = run_vcycle_b(ctx, K, st))) return s;
+            if ((s = run_vcycle_b(ctx, K, st, true))) return s;
             std::vector<double> one(K, 1.0);
             if ((s = upload_coef(one, coef))) return s;
-            launch(false, k_blincomb<K>, nb, 256, 0, st, nk, 1, (const double*)ctx->bu[0], nk, (const double*)coef,
+            launch(false, k_blincomb<K>, nb, 256, 0, st, N, 1, (const double*)ctx->bu[0], nk, (const double*)coef,
                    1.0, 1, x);
         }
         bool left = false;
@@ -4260,6 +4263,8 @@ mgm_status mgm_destroy(mgm_ctx* ctx) {
     for (auto* q : {&ctx->bu, &ctx->bf, &ctx->bt})
         for (double* ptr : *q) dev_free(ptr);
     for (auto& gx : ctx->bgraph)
+        if (gx) cudaGraphExecDestroy(gx);
+    for (auto& gx : ctx->bgraph_zg)
         if (gx) cudaGraphExecDestroy(gx);
     if (ctx->bres) dev_free(ctx->bres);
     for (double* ptr : {ctx->bV, ctx->bw, ctx->bx, ctx->bb, ctx->bdh})
