@@ -1665,25 +1665,11 @@ double sweep_colour_bytes(const Level& L, i64 rows) {
 
 // kernel variants by threads-per-row (chosen per level from the SELL width)
 constexpr int CHUNK = 16;
-// MGM_GS_STAGE=0: level-0 colour kernels without the shared-memory staging (experiment)
-static const bool g_gs_stage = !(std::getenv("MGM_GS_STAGE") && std::atoi(std::getenv("MGM_GS_STAGE")) == 0);
 template <bool P, int TPR>
 void gs_launch_t(bool pdl, int r0, int r1, int span, const Level& L, cudaStream_t st, PfList pf, bool zg) {
     // block size: colours too small to give every SM a 256-thread block use smaller blocks
     // (spreads the gathers over more SMs)
     const int bs = L.gs_block;
-    if (TPR == 1 && !P && !zg && g_gs_stage && L.uniform_w > CHUNK && L.uniform_w <= CHUNK + 48) {
-        // level 0: the rows' later slots staged in shared memory during the prologue
-        const size_t smem = (size_t)(L.uniform_w - CHUNK) * bs * 12;
-        static size_t smem_set = 0;
-        if (smem > smem_set) {
-            cudaFuncSetAttribute(k_gs_colour_st<CHUNK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            smem_set = smem;
-        }
-        launch(pdl, k_gs_colour_st<CHUNK>, blocks_for((i64)span, bs), bs, smem, st, r0, r1, L.uniform_w,
-               (const i32*)L.scol, (const double*)L.sval, (const double*)L.f, L.u);
-        return;
-    }
     if (zg && !P)
         launch(pdl, k_gs_colour<false, TPR, CHUNK, true>, blocks_for((i64)span * TPR, bs), bs, 0, st, r0, r1,
                L.uniform_w, L.sptr, L.scol, L.sval, L.f, L.u, L.c, (int)L.n, pf, (const int*)L.slw,

@@ -184,65 +184,6 @@ __global__ void __launch_bounds__(256) k_gs_colour(int r0, int r1, int Wu, const
     }
 }
 
-__device__ __forceinline__ void cp_async8(void* dst_smem, const void* src) {
-    const unsigned d = (unsigned)__cvta_generic_to_shared(dst_smem);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async4(void* dst_smem, const void* src) {
-    const unsigned d = (unsigned)__cvta_generic_to_shared(dst_smem);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
-
-// One colour of a full Gauss-Seidel sweep, one thread per row of a uniform-width level
-// (Wu > CH slots, level 0; shifted problems): the first CH slots are loaded into registers
-// as in k_gs_colour, and the slots CH..Wu-1 are copied into shared memory with cp.async in
-// the prologue -- before griddepcontrol.wait, since the operator does not depend on the
-// previous colour -- so after the wait only the gathers of u remain.  The same fma sequence
-// as k_gs_colour<false, 1, CH> (slots in order), so the same bits.
-template <int CH>
-__global__ void __launch_bounds__(256) k_gs_colour_st(int r0, int r1, int Wu, const int* __restrict__ scol,
-                                                      const double* __restrict__ sval, const double* __restrict__ f,
-                                                      double* u) {
-    extern __shared__ __align__(16) unsigned char st_smem[];
-    pdl_trigger();
-    const int tid = threadIdx.x, bd = blockDim.x;
-    const int r = (r0 & ~31) + blockIdx.x * bd + tid;
-    const bool live = (r >= r0 && r < r1);
-    const int nst = Wu - CH;
-    double* sv = (double*)st_smem;                 // [nst][bd]
-    int* sc = (int*)(sv + (size_t)nst * bd);       // [nst][bd]
-    RowFrag<1, CH> fr;
-    int64_t base = 0;
-    double d = 1.0;
-    if (live) {
-        base = (int64_t)(r >> 5) * 32 * Wu + (r & 31);
-        fr.load(sval + base, scol + base, Wu, 0);
-        for (int q = 0; q < nst; ++q) {
-            cp_async8(sv + (size_t)q * bd + tid, sval + base + 32 * (CH + q));
-            cp_async4(sc + (size_t)q * bd + tid, scol + base + 32 * (CH + q));
-        }
-        cp_async_commit();
-        d = ld_stream_f64(sval + base);
-    } else {
-        fr.load(sval, scol, 0, 0);
-    }
-    pdl_wait();
-    double fr_v = 0.0, ur = 0.0;
-    if (live) {
-        fr_v = f[r];
-        ur = u[r];
-    }
-    double acc = fr.dot(u, 0.0);
-    if (live) {
-        cp_async_wait_all();
-        for (int q = 0; q < nst; ++q) acc = fma(sv[(size_t)q * bd + tid], u[sc[(size_t)q * bd + tid]], acc);
-        const double res = fr_v - acc;
-        u[r] = ur + res / d;
-    }
-}
-
 // y = L x  (MODE 0),  y = f - L x  (MODE 1) on the rows [r0, r1).
 // MODE 2: the residual right after a forward Gauss-Seidel sweep from a ZERO guess,
 // y = f - L u = -sum_{later colours} a_ij u_j: the sweep made every row's residual zero when
