@@ -313,14 +313,6 @@ mgm_status mgm_trace_read(const mgm_ctx* ctx, uint64_t* stamps_ns, int cap, int*
  * MGM_NO_ZG).  For byte models. */
 mgm_status mgm_level_zg_nnz(const mgm_ctx* ctx, int level, int64_t* nnz_zg);
 
-/* CTAs of the one-launch sweep of level `level` (flow_kernel.cuh k_gs_flow: the whole
- * multicolour Gauss-Seidel sweep of P:285-291 in one cooperative launch, CTA b owning the
- * b-th Morton block of the level's rows and waiting only for its neighbour blocks between
- * colours), or 0 when the level runs one kernel per colour.  Chosen at mgm_setup: levels
- * with at least MGM_FLOW_MIN rows (default 524288), MGM_FLOW=0 disables.  Not used on
- * distributed levels.  *ctas receives the count; MGM_ERR_ARG on a bad level or NULL. */
-mgm_status mgm_level_flow_ctas(const mgm_ctx* ctx, int level, int* ctas);
-
 /* The dense bottom of the V-cycle: Alg. 3 lines 6-14 for the
  * levels >= J from e_J = 0 are linear in r_J; setup builds their matrix B_J
  * (n_J x n_J, Poisson n_J + 1) from the unit vectors with the library's own level kernels and

@@ -23,7 +23,6 @@
 #include "bottom_kernel.cuh"
 #include "batch_kernels.cuh"
 #include "dense_bottom.cuh"
-#include "flow_kernel.cuh"
 
 using namespace mgm;
 
@@ -333,13 +332,6 @@ struct Level {
     double* d_stage_mine = nullptr;
     double* d_stage_all = nullptr;
     i32* d_stage_perm = nullptr;
-    // ---- one-launch sweep (flow_kernel.cuh, MGM_FLOW): B CTAs own Morton blocks of rows
-    int flow_B = 0;                      // 0: per-colour kernels
-    int flow_pf = 2;                     // L2 prefetch distance (steps)
-    int* d_cst = nullptr;                // [ncol][B + 1] CTA b's rows of colour c
-    int* d_nbr_ptr = nullptr;            // [B + 1]
-    int* d_nbr = nullptr;                // neighbour CTAs
-    unsigned* d_prog = nullptr;          // [B * FLOW_PROG_STRIDE] progress counters
 };
 
 struct KernelTimer {
@@ -993,86 +985,6 @@ struct SetupTimer {
     }
 };
 
-// ---- one-launch sweeps (flow_kernel.cuh k_gs_flow; DESIGN.md section 6 "One-launch sweep").
-// MGM_FLOW=0 keeps one kernel per colour everywhere; MGM_FLOW_MIN: levels with at least this
-// many rows use the flow sweep (default: the bandwidth-bound levels); MGM_FLOW_CPS: CTAs per
-// SM (default: the kernel's occupancy); MGM_FLOW_PF: L2 prefetch distance in steps.
-static i64 env_i64(const char* k, i64 dflt) { return std::getenv(k) ? std::atoll(std::getenv(k)) : dflt; }
-template <bool P, int TPR, bool ZG>
-static const void* flow_kernel_ptr() {
-    return (const void*)k_gs_flow<P, TPR, 16, ZG>;
-}
-template <bool P>
-static const void* flow_kernel_sel(int tpr, bool zg) {
-    if (zg) return tpr == 1 ? flow_kernel_ptr<P, 1, true>() : tpr == 2 ? flow_kernel_ptr<P, 2, true>()
-                 : tpr == 4 ? flow_kernel_ptr<P, 4, true>() : flow_kernel_ptr<P, 8, true>();
-    return tpr == 1 ? flow_kernel_ptr<P, 1, false>() : tpr == 2 ? flow_kernel_ptr<P, 2, false>()
-         : tpr == 4 ? flow_kernel_ptr<P, 4, false>() : flow_kernel_ptr<P, 8, false>();
-}
-// CTAs of a flow launch on level j: every CTA must be co-resident (cooperative launch)
-static int flow_grid(bool poisson, int tpr) {
-    int dev = 0, nsm = 0, per = 1 << 20;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    for (bool zg : {false, true}) {
-        int q = 0;
-        const void* k = poisson ? flow_kernel_sel<true>(tpr, zg) : flow_kernel_sel<false>(tpr, zg);
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&q, k, FLOW_THREADS, 0) != cudaSuccess) {
-            cudaGetLastError();
-            q = 0;
-        }
-        per = std::min(per, q);
-    }
-    if (const char* e = std::getenv("MGM_FLOW_CPS")) per = std::min(per, std::max(1, std::atoi(e)));
-    return per * nsm;
-}
-mgm_status build_flow(mgm_ctx* ctx, int j) {
-    Level& L = ctx->lv[j];
-    L.flow_B = 0;
-    if (env_i64("MGM_FLOW", 1) == 0 || L.n < env_i64("MGM_FLOW_MIN", 524288) || L.ncol <= 0 ||
-        L.L_lib.nrows != L.n)
-        return MGM_OK;
-    L.flow_pf = (int)env_i64("MGM_FLOW_PF", 2);
-    const i64 n = L.n;
-    // lib order must be Morton-sorted inside every colour (pack order), so a CTA's rows of a
-    // colour are contiguous
-    for (int c = 0; c < L.ncol; ++c)
-        for (i64 r = L.coff[c] + 1; r < L.coff[c + 1]; ++r)
-            if (L.lib2mor[(size_t)r] <= L.lib2mor[(size_t)r - 1]) return MGM_OK;
-    const int B = flow_grid(ctx->poisson, L.tpr);
-    if (B <= 0) return MGM_OK;
-    auto owner = [&](i64 r) { return (int)((L.lib2mor[(size_t)r] * (i64)B) / n); };
-    std::vector<int> cst((size_t)L.ncol * (B + 1), 0);
-    for (int c = 0; c < L.ncol; ++c) {
-        int* cs = cst.data() + (size_t)c * (B + 1);
-        std::vector<i64> cnt(B + 1, 0);
-        for (i64 r = L.coff[c]; r < L.coff[c + 1]; ++r) cnt[owner(r) + 1]++;
-        cs[0] = (int)L.coff[c];
-        for (int b = 0; b < B; ++b) cs[b + 1] = cs[b] + (int)cnt[b + 1];
-    }
-    std::vector<std::vector<char>> adj(B, std::vector<char>(B, 0));
-    for (i64 r = 0; r < n; ++r) {
-        const int b = owner(r);
-        for (i64 q = L.L_lib.ptr[r]; q < L.L_lib.ptr[r + 1]; ++q) {
-            const int ob = owner(L.L_lib.col[q]);
-            if (ob != b) adj[b][ob] = adj[ob][b] = 1;
-        }
-    }
-    std::vector<int> nptr(B + 1, 0), nbr;
-    for (int b = 0; b < B; ++b) {
-        for (int o = 0; o < B; ++o)
-            if (adj[b][o]) nbr.push_back(o);
-        nptr[b + 1] = (int)nbr.size();
-    }
-    mgm_status s;
-    if ((s = upload(ctx, &L.d_cst, cst)) || (s = upload(ctx, &L.d_nbr_ptr, nptr)) || (s = upload(ctx, &L.d_nbr, nbr)))
-        return s;
-    CK(dalloc(&L.d_prog, (i64)B * FLOW_PROG_STRIDE));
-    CK(cudaMemset(L.d_prog, 0, sizeof(unsigned) * (size_t)B * FLOW_PROG_STRIDE));
-    L.flow_B = B;
-    return MGM_OK;
-}
-
 mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i64 N) {
     DeferFree deferred;  // (destroyed last: after every setup thread has been joined)
     DeferScope defer_(&deferred);
@@ -1691,10 +1603,6 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
         }
         cudaGetLastError();
     }
-    // ---- one-launch sweeps (flow_kernel.cuh): CTA ownership and neighbour tables
-    for (int j = 0; j + 1 < p; ++j)
-        if ((s = build_flow(ctx, j))) return s;
-    tm.mark("flow tables");
     // ---- level-0 permutation
     {
         std::vector<i32> l2o(N);
@@ -2021,65 +1929,6 @@ static i64 dot_rows(const mgm_ctx* ctx) {
 // rows of a level-0 vector (owned rows + multiplier; ghosts excluded)
 static i64 vec_rows(const mgm_ctx* ctx) { return ctx->lv[0].n + (ctx->poisson ? 1 : 0); }
 
-// One sweep of level j as one k_gs_flow launch (cooperative: all flow_B CTAs resident).
-template <bool P, int TPR, bool ZG>
-static void launch_flow_t(mgm_ctx* ctx, const FlowSweep& a, int B, cudaStream_t st) {
-    if (g_dry) return;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)B);
-    cfg.blockDim = dim3(FLOW_THREADS);
-    cfg.stream = st;
-    cudaLaunchAttribute at[2];
-    at[0].id = cudaLaunchAttributeCooperative;
-    at[0].val.cooperative = 1;
-    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[1].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = at;
-    bool pdl = ctx->pdl && g_use_pdl;
-    if (g_after_comm) {
-        pdl = false;
-        g_after_comm = false;
-    }
-    cfg.numAttrs = pdl ? 2 : 1;
-    note_launch(cudaLaunchKernelEx(&cfg, k_gs_flow<P, TPR, 16, ZG>, a), (unsigned)B, FLOW_THREADS, 0);
-}
-template <bool P, bool ZG>
-static void launch_flow_z(mgm_ctx* ctx, int tpr, const FlowSweep& a, int B, cudaStream_t st) {
-    if (tpr == 1) launch_flow_t<P, 1, ZG>(ctx, a, B, st);
-    else if (tpr == 2) launch_flow_t<P, 2, ZG>(ctx, a, B, st);
-    else if (tpr == 4) launch_flow_t<P, 4, ZG>(ctx, a, B, st);
-    else launch_flow_t<P, 8, ZG>(ctx, a, B, st);
-}
-static void enqueue_flow_sweep(mgm_ctx* ctx, Level& L, bool backward, bool zg, int s0, cudaStream_t st) {
-    FlowSweep a{};
-    a.n = (int)L.n;
-    a.ncol = L.ncol;
-    a.s0 = s0;
-    a.backward = backward ? 1 : 0;
-    a.Wu = L.uniform_w;
-    a.pf_dist = L.flow_pf;
-    a.sptr = L.sptr;
-    a.scol = L.scol;
-    a.sval = L.sval;
-    a.f = L.f;
-    a.u = L.u;
-    a.c = L.c;
-    a.cst = L.d_cst;
-    a.nbr_ptr = L.d_nbr_ptr;
-    a.nbr = L.d_nbr;
-    a.prog = L.d_prog;
-    a.slw = L.slw;
-    a.nlow = L.nlow;
-    if (ctx->poisson) {
-        if (zg) launch_flow_z<true, true>(ctx, L.tpr, a, L.flow_B, st);
-        else launch_flow_z<true, false>(ctx, L.tpr, a, L.flow_B, st);
-    } else {
-        if (zg) launch_flow_z<false, true>(ctx, L.tpr, a, L.flow_B, st);
-        else launch_flow_z<false, false>(ctx, L.tpr, a, L.flow_B, st);
-    }
-    ctx->vcycle_kernels++;
-}
-
 bool timing_on(const mgm_ctx* ctx);
 // zg: first forward sweep from a zero guess (k_gs_colour ZG; shifted problems only)
 void enqueue_sweep(mgm_ctx* ctx, int j, bool backward, cudaStream_t st, bool zg = false, bool skip_c0 = false) {
@@ -2091,18 +1940,6 @@ void enqueue_sweep(mgm_ctx* ctx, int j, bool backward, cudaStream_t st, bool zg 
     if (j == 0) timer_begin(ctx, tcls, st);
     double bytes = 0.0;
     int nl = 0;
-    if (L.flow_B > 0 && !L.dist && !dist_on(ctx)) {  // the whole sweep as one launch
-        const int s0 = (skip_c0 && zg) ? 1 : 0;
-        enqueue_flow_sweep(ctx, L, backward, zg, s0, st);
-        for (int q = s0; q < L.ncol; ++q) {
-            const int c = backward ? L.ncol - 1 - q : q;
-            const i64 c0 = L.coff[c], c1 = L.coff[c + 1];
-            bytes += zg ? (12.0 * (double)L.lower_per_colour[c] + 16.0 * (double)(c1 - c0))
-                        : sweep_colour_bytes(L, c1 - c0);
-        }
-        if (j == 0) timer_end(ctx, tcls, st, bytes, 1);
-        return;
-    }
     for (int q = (skip_c0 && zg) ? 1 : 0; q < L.ncol; ++q) {  // (colour 0 done by the restriction)
         const int c = backward ? L.ncol - 1 - q : q;
         const i64 c0 = L.coff[c], c1 = L.coff[c + 1];
@@ -3482,8 +3319,7 @@ void free_level_device(Level& L) {
                       (void*)L.rcol, (void*)L.rval, (void*)L.u, (void*)L.f, (void*)L.t, (void*)L.c, (void*)L.slw,
                       (void*)L.nlow, (void*)L.sluw, (void*)L.l2m, (void*)L.rcol_m, (void*)L.d_send_idx,
                       (void*)L.d_sendbuf, (void*)L.d_srange, (void*)L.d_stage_mine, (void*)L.d_stage_all,
-                      (void*)L.d_stage_perm, (void*)L.d_rslot, (void*)L.d_cst, (void*)L.d_nbr_ptr,
-                      (void*)L.d_nbr, (void*)L.d_prog})
+                      (void*)L.d_stage_perm, (void*)L.d_rslot})
         if (ptr) dev_free(ptr);
 }
 
@@ -4730,13 +4566,6 @@ mgm_status mgm_level_zg_nnz(const mgm_ctx* ctx, int level, int64_t* nnz_zg) {
     i64 s = 0;
     for (i64 v : ctx->lv[level].lower_per_colour) s += v;
     *nnz_zg = zg_capable(ctx) ? s : ctx->lv[level].nnz;
-    return MGM_OK;
-}
-
-mgm_status mgm_level_flow_ctas(const mgm_ctx* ctx, int level, int* ctas) {
-    if (!ctx || level < 0 || level >= ctx->p || !ctas) return MGM_ERR_ARG;
-    const Level& L = ctx->lv[level];
-    *ctas = (L.flow_B > 0 && !L.dist && !ctx->tp) ? L.flow_B : 0;
     return MGM_OK;
 }
 

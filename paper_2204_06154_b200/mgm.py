@@ -98,7 +98,6 @@ _SIGS = {
     "mgm_bottom_trace_read": ([_vp, ctypes.POINTER(ctypes.c_uint64), ctypes.c_int,
                                ctypes.POINTER(ctypes.c_int), _i32p], ctypes.c_int),
     "mgm_level_zg_nnz": ([_vp, ctypes.c_int, _i64p], ctypes.c_int),
-    "mgm_level_flow_ctas": ([_vp, ctypes.c_int, ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
     "mgm_dense_bottom_info": ([_vp, ctypes.POINTER(ctypes.c_int), _i64p, _i64p], ctypes.c_int),
     "mgm_bottom_ftrace_read": ([_vp, _i64p, ctypes.c_int, ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
     "mgm_host_morton": ([_f64p, _i64, _i64p], ctypes.c_int),
@@ -293,10 +292,8 @@ def mgm_level_info(ctx, level: int) -> dict:
                                          ctypes.byref(q), ctypes.byref(c), ctypes.byref(b)), ctx)
     zg = _i64()
     _check(load_library().mgm_level_zg_nnz(ctx, level, ctypes.byref(zg)), ctx)
-    fc = ctypes.c_int()
-    _check(load_library().mgm_level_flow_ctas(ctx, level, ctypes.byref(fc)), ctx)
     return dict(n=n.value, nnz=z.value, nnz_P=q.value, colours=c.value, stored_bytes=b.value,
-                nnz_zg=zg.value, flow_ctas=fc.value)
+                nnz_zg=zg.value)
 
 
 def mgm_export_level(ctx, level: int, poisson: bool = False) -> dict:

@@ -1020,111 +1020,3 @@ def test_solve_batch_matches_oracle():
         assert reps[k].converged and rr.converged
         assert abs(reps[k].iterations - rr.iterations) <= 1, (k, reps[k].iterations, rr.iterations)
         assert np.linalg.norm(xg[k] - xr) / np.linalg.norm(xr) <= 1e-9
-
-
-# ------------------------------------------------------------------ one-launch (flow) sweeps
-FLOW_KNOBS = [{"MGM_FLOW_MIN": "0"},                          # every coloured level, occupancy grid
-              {"MGM_FLOW_MIN": "0", "MGM_FLOW_CPS": "1", "MGM_FLOW_PF": "0"}]  # 148 CTAs, no L2 prefetch
-
-
-def _flow_ctx(name, knobs, monkeypatch, levels=None):
-    from paper_2204_06154_b200 import MGM, mgm_level_info
-    for k, v in knobs.items():
-        monkeypatch.setenv(k, v)
-    w = CASES[name]()
-    lv = levels if levels is not None else w.levels
-    g = MGM(w.points, w.normals, w.stencil, lv)
-    for j in range(g.p - 1):
-        assert mgm_level_info(g.ctx, j)["flow_ctas"] > 0, j   # the flow path is the one tested
-    return w, g
-
-
-@pytest.mark.parametrize("name", list(CASES))
-@pytest.mark.parametrize("knobs", range(len(FLOW_KNOBS)))
-def test_flow_sweep_matches_oracle(name, knobs, monkeypatch):
-    """The whole multicolour sweep as ONE launch ordered by CTA-to-CTA progress counters
-    (flow_kernel.cuh, O12) on every coloured level: one forward sweep, one sweep
-    from the zero guess, the V-cycle and MGM-GMRES against the oracle (1e-12 / +-1 iteration,
-    1e-9)."""
-    import torch
-    from paper_2204_06154_b200 import mgm_apply
-
-    P = pair(name)
-    w, g = _flow_ctx(name, FLOW_KNOBS[knobs], monkeypatch)
-    pad = 1 if P.poisson else 0
-    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
-    for j in range(P.ref.p - 1):
-        o = P.ref.levels[j]
-        n = o.N
-        x, f = _rand(n + pad, 60 + j), _rand(n + pad, 70 + j)
-        y = torch.empty(n + pad, dtype=torch.float64, device="cuda")
-        mgm_apply(g.ctx, j, 1, dev(P.to_lib_order(j, x)), dev(P.to_lib_order(j, f)), y)
-        u = x.copy()
-        P.ref._smooth(o, f, u, 1, False)
-        assert relmax(P.to_oracle_order(j, y.cpu().numpy()), u) <= 1e-12, ("sweep", j)
-        if not P.poisson:
-            mgm_apply(g.ctx, j, 6, dev(np.zeros(n)), dev(P.to_lib_order(j, f[:n])), y)
-            u = np.zeros(n)
-            P.ref._smooth(o, f[:n], u, 1, False)
-            yo = P.to_oracle_order(j, y.cpu().numpy())
-            assert np.isfinite(yo).all() and relmax(yo, u) <= 1e-12, ("zero-guess sweep", j)
-    n = P.ref.levels[0].N
-    f0, u0 = _rand(n + pad, 81), _rand(n + pad, 82)
-    uu = torch.from_numpy(u0.copy()).cuda()
-    g.vcycle(torch.from_numpy(f0).cuda(), uu)
-    assert relmax(uu.cpu().numpy(), P.ref.vcycle(f0, u0)) <= 1e-12
-    x, rep = g.solve(torch.from_numpy(w.rhs).cuda(), tol=1e-10)
-    xr, rr = P.ref.solve(w.rhs, tol=1e-10)
-    assert rep.converged and rr.converged
-    assert abs(rep.iterations - rr.iterations) <= 1
-    assert np.linalg.norm(x.cpu().numpy() - xr) / np.linalg.norm(xr) <= 1e-9
-    g.close()
-
-
-@pytest.mark.parametrize("name", ["cfg1", "torus20000", "gfd9000"])
-def test_flow_sweep_bitwise_equals_colour_kernels(name, monkeypatch):
-    """Same per-row arithmetic as the one-kernel-per-colour sweep: the V-cycle (from a random
-    guess and from zero) is bit-identical with MGM_FLOW=0 and with every level on the flow
-    path."""
-    import torch
-    from paper_2204_06154_b200 import MGM, mgm_apply
-
-    w = CASES[name]()
-    n = len(w.points)
-    f0, u0 = _rand(n, 91), _rand(n, 92)
-    outs = []
-    for knobs in ({"MGM_FLOW": "0"}, {"MGM_FLOW_MIN": "0"}):
-        for k in ("MGM_FLOW", "MGM_FLOW_MIN"):
-            monkeypatch.delenv(k, raising=False)
-        for k, v in knobs.items():
-            monkeypatch.setenv(k, v)
-        g = MGM(w.points, w.normals, w.stencil, w.levels)
-        uu = torch.from_numpy(u0.copy()).cuda()
-        g.vcycle(torch.from_numpy(f0).cuda(), uu)
-        y = torch.empty(n, dtype=torch.float64, device="cuda")
-        mgm_apply(g.ctx, 0, 7, torch.from_numpy(f0).cuda(), None, y)
-        outs.append((uu.cpu().numpy(), y.cpu().numpy()))
-        g.close()
-    assert np.array_equal(outs[0][0], outs[1][0])
-    assert np.array_equal(outs[0][1], outs[1][1])
-
-
-@pytest.mark.parametrize("smoother", [1, 2])
-def test_flow_sweep_backward_orders(smoother, monkeypatch):
-    """Backward colour order (smoother 1) and forward-pre / backward-post (smoother 2) through
-    the flow sweep: V-cycle to 1e-12 of the oracle on a ragged cloud (N = 1500)."""
-    import torch
-    import oracle as O
-    from paper_2204_06154_b200 import MGM
-
-    monkeypatch.setenv("MGM_FLOW_MIN", "0")
-    w = MI.make_workload(1, n=1500)
-    lv = dict(w.levels, num_levels=4, nu1=1, nu2=1, smoother=smoother)
-    g = MGM(w.points, w.normals, w.stencil, lv)
-    o = O.Oracle(w.points, w.normals, w.stencil, lv)
-    n = len(w.points)
-    f, u0 = _rand(n, 43), _rand(n, 44)
-    uf = torch.from_numpy(u0.copy()).cuda()
-    g.vcycle(torch.from_numpy(f).cuda(), uf)
-    assert relmax(uf.cpu().numpy(), o.vcycle(f, u0)) <= 1e-12
-    g.close()
