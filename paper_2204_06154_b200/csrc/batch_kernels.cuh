@@ -145,6 +145,188 @@ __global__ void __launch_bounds__(256) k_sell_spmv_b(int r0, int r1, const int64
     }
 }
 
+// ---- right-hand-side-split variants: KS = K/2 threads per (row, slot part), each owning the
+// pair of right-hand sides (2 kk, 2 kk + 1).  A gather of column j by the KS threads of a row
+// reads the K contiguous values of u[j][*] as ONE coalesced 16 * KS-byte segment (instead of
+// K/2 16-byte loads by one thread, each warp load touching 32 scattered lines); the operator
+// entry (same address for the KS threads) is one broadcast load.  Per (row, right-hand side)
+// the slots are summed in the same order by the same slot part as the unsplit kernels (TPR
+// parts, group sum over the parts), so the results are bitwise theirs.
+template <int TPR, int KS>
+__device__ __forceinline__ double part_sum(double v) {
+#pragma unroll
+    for (int o = (TPR * KS) >> 1; o >= KS; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+template <int TPR, int CH, int K, bool ZG = false>
+__global__ void __launch_bounds__(256) k_gs_colour_bs(int r0, int r1, int Wu, const int64_t* __restrict__ sptr,
+                                                      const int* __restrict__ scol, const double* __restrict__ sval,
+                                                      const double* __restrict__ f, double* u,
+                                                      const int* __restrict__ slw, const uint8_t* __restrict__ nlow) {
+    constexpr int KS = K / 2;
+    pdl_trigger();
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    const int r = (r0 & ~31) + g / (TPR * KS);
+    const int kk = g % KS, part = (g / KS) % TPR;
+    const bool live = (r >= r0 && r < r1);
+    RowFrag<TPR, CH> fr;
+    int w = 0;
+    int64_t base = 0;
+    double d = 1.0;
+    if (live) {
+        if (Wu > 0) {
+            w = Wu;
+            base = (int64_t)(r >> 5) * 32 * Wu + (r & 31);
+        } else {
+            const int64_t s0 = sptr[r >> 5];
+            w = (int)((sptr[(r >> 5) + 1] - s0) >> 5);
+            base = s0 + (r & 31);
+        }
+        int lim = 0;
+        if (ZG) {
+            w = slw[r >> 5];
+            lim = 1 + (int)nlow[r];
+        }
+        fr.load(sval + base, scol + base, ZG ? lim : w, part);
+        if (ZG) {
+#pragma unroll
+            for (int q = 0; q < CH; ++q)
+                if (part + q * TPR == 0 || part + q * TPR >= lim) fr.c[q] = -1;
+            w = lim;
+        }
+        d = ld_stream_f64(sval + base);
+    } else {
+        fr.load(sval, scol, 0, 0);
+    }
+    pdl_wait();
+    const double2* u2 = reinterpret_cast<const double2*>(u);
+    double2 fv = make_double2(0.0, 0.0), uv = make_double2(0.0, 0.0);
+    double a0 = 0.0, a1 = 0.0;
+    if (live && part == 0) {
+        fv = reinterpret_cast<const double2*>(f)[(int64_t)r * KS + kk];
+        if (!ZG) uv = u2[(int64_t)r * KS + kk];
+    }
+    for (int k0 = part;; k0 += TPR * CH) {
+        if (k0 != part) fr.load(sval + base, scol + base, w, k0);
+#pragma unroll
+        for (int q = 0; q < CH; ++q)
+            if (fr.c[q] >= 0) {
+                const double2 v = u2[(int64_t)fr.c[q] * KS + kk];
+                a0 = fma(fr.a[q], v.x, a0);
+                a1 = fma(fr.a[q], v.y, a1);
+            }
+        if (k0 + TPR * CH >= w) break;
+    }
+    a0 = part_sum<TPR, KS>(a0);
+    a1 = part_sum<TPR, KS>(a1);
+    if (live && part == 0)
+        reinterpret_cast<double2*>(u)[(int64_t)r * KS + kk] = make_double2(uv.x + (fv.x - a0) / d, uv.y + (fv.y - a1) / d);
+}
+// MODE 0: y = A x; MODE 1: y = f - A x; MODE 2: y = -(later-colour part of A) x, the residual
+// right after a forward sweep from a zero guess (k_sell_spmv MODE 2: from the slice's first
+// later-colour slot sluw, masked below the row's own 1 + nlow).  yperm: output row of each
+// input row (the residual written in Morton order for the restriction's Morton columns).
+template <int MODE, int TPR, int CH, int K>
+__global__ void __launch_bounds__(256) k_sell_spmv_bs(int r0, int r1, const int64_t* __restrict__ sptr,
+                                                      const int* __restrict__ scol, const double* __restrict__ sval,
+                                                      const double* __restrict__ x, const double* __restrict__ f,
+                                                      double* __restrict__ y, const int* __restrict__ sluw,
+                                                      const uint8_t* __restrict__ nlow, const int* __restrict__ yperm) {
+    constexpr int KS = K / 2;
+    pdl_trigger();
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    const int r = (r0 & ~31) + g / (TPR * KS);
+    const int kk = g % KS, part = (g / KS) % TPR;
+    const bool live = r >= r0 && r < r1;
+    RowFrag<TPR, CH> fr;
+    int w = 0, k1 = part, lim = 0, yr = r;
+    int64_t base = 0;
+    if (live) {
+        if (yperm) yr = yperm[r];
+        const int64_t s0 = sptr[r >> 5];
+        w = (int)((sptr[(r >> 5) + 1] - s0) >> 5);
+        base = s0 + (r & 31);
+        if (MODE == 2) {
+            k1 = sluw[r >> 5] + part;
+            lim = 1 + (int)nlow[r];
+        }
+        fr.load(sval + base, scol + base, w, k1);
+    } else {
+        fr.load(sval, scol, 0, 0);
+    }
+    if (MODE == 2) {
+#pragma unroll
+        for (int q = 0; q < CH; ++q)
+            if (k1 + q * TPR < lim) fr.c[q] = -1;
+    }
+    pdl_wait();
+    const double2* x2 = reinterpret_cast<const double2*>(x);
+    double a0 = 0.0, a1 = 0.0;
+    for (int k0 = k1;; k0 += TPR * CH) {
+        if (k0 != k1) {
+            fr.load(sval + base, scol + base, w, k0);
+            if (MODE == 2) {
+#pragma unroll
+                for (int q = 0; q < CH; ++q)
+                    if (k0 + q * TPR < lim) fr.c[q] = -1;
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < CH; ++q)
+            if (fr.c[q] >= 0) {
+                const double2 v = x2[(int64_t)fr.c[q] * KS + kk];
+                a0 = fma(fr.a[q], v.x, a0);
+                a1 = fma(fr.a[q], v.y, a1);
+            }
+        if (k0 + TPR * CH >= w) break;
+    }
+    a0 = part_sum<TPR, KS>(a0);
+    a1 = part_sum<TPR, KS>(a1);
+    if (live && part == 0) {
+        double2 o = make_double2(a0, a1);
+        if (MODE == 1) {
+            const double2 fv = reinterpret_cast<const double2*>(f)[(int64_t)r * KS + kk];
+            o = make_double2(fv.x - a0, fv.y - a1);
+        } else if (MODE == 2) {
+            o = make_double2(-a0, -a1);
+        }
+        reinterpret_cast<double2*>(y)[(int64_t)yr * KS + kk] = o;
+    }
+}
+template <int M, int K>
+__global__ void __launch_bounds__(256) k_interp_correct_bs(int n, int m, const int* __restrict__ pcol,
+                                                           const double* __restrict__ pval,
+                                                           const double* __restrict__ ec, double* __restrict__ e) {
+    constexpr int KS = K / 2;
+    pdl_trigger();
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    const int r = g / KS, kk = g % KS;
+    int cidx[M];
+    double a[M];
+#pragma unroll
+    for (int q = 0; q < M; ++q) {
+        const bool ok = r < n && q < m;
+        cidx[q] = ok ? ld_stream_i32(pcol + (int64_t)q * n + r) : -1;
+        a[q] = ok ? ld_stream_f64(pval + (int64_t)q * n + r) : 0.0;
+    }
+    pdl_wait();
+    if (r >= n) return;
+    const double2* ec2 = reinterpret_cast<const double2*>(ec);
+    double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+    for (int q = 0; q < M; ++q)
+        if (cidx[q] >= 0) {
+            const double2 v = ec2[(int64_t)cidx[q] * KS + kk];
+            a0 = fma(a[q], v.x, a0);
+            a1 = fma(a[q], v.y, a1);
+        }
+    double2* e2 = reinterpret_cast<double2*>(e);
+    double2 o = e2[(int64_t)r * KS + kk];
+    o.x += a0;
+    o.y += a1;
+    e2[(int64_t)r * KS + kk] = o;
+}
+
 // e += P ec for K right-hand sides (interpolate + correct), rows [0, n)
 template <int M, int K>
 __global__ void __launch_bounds__(256) k_interp_correct_b(int n, int m, const int* __restrict__ pcol,

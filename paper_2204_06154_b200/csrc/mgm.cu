@@ -2956,6 +2956,31 @@ static i64 gs_wave_threads_b(int tpr, int block) {
     }
     return cache[ti][bi] = (i64)per * nsm * block;
 }
+// batched levels with at least this many rows write the residual in Morton order
+// (MGM_BATCH_MORTON_T_MIN; off by default: cfg3 K = 8 residual+restrict L0 437 vs 413 us)
+static i64 g_batch_morton_min = std::getenv("MGM_BATCH_MORTON_T_MIN") ? std::atoll(std::getenv("MGM_BATCH_MORTON_T_MIN"))
+                                                                      : (i64)1 << 62;
+// MGM_BATCH_SPLIT=0: the unsplit batched kernels (one thread gathers all K values of a column)
+static bool g_batch_split = !(std::getenv("MGM_BATCH_SPLIT") && std::atoi(std::getenv("MGM_BATCH_SPLIT")) == 0);
+template <int K>
+static i64 gs_wave_threads_bs(int tpr, int block) {
+    static i64 cache[4][4] = {};
+    const int ti = tpr == 1 ? 0 : tpr == 2 ? 1 : tpr == 4 ? 2 : 3;
+    const int bi = block == 64 ? 0 : block == 128 ? 1 : block == 256 ? 2 : 3;
+    if (cache[ti][bi]) return cache[ti][bi];
+    int dev = 0, nsm = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const void* k = tpr == 1 ? (const void*)k_gs_colour_bs<1, CHUNK, K>
+                  : tpr == 2 ? (const void*)k_gs_colour_bs<2, CHUNK, K>
+                  : tpr == 4 ? (const void*)k_gs_colour_bs<4, CHUNK, K>
+                             : (const void*)k_gs_colour_bs<8, CHUNK, K>;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, block, 0) != cudaSuccess) {
+        cudaGetLastError();
+        per = 1;
+    }
+    return cache[ti][bi] = (i64)per * nsm * block;
+}
 template <int K>
 static void b_gs(mgm_ctx* ctx, const Level& L, int j, int r0, int r1, cudaStream_t st, bool zg = false) {
     const int span = r1 - (r0 & ~31);
@@ -2970,6 +2995,25 @@ static void b_gs(mgm_ctx* ctx, const Level& L, int j, int r0, int r1, cudaStream
     while (tpr > 1 && (i64)span * tpr > gs_wave_threads_b<K>(tpr, bs) &&
            (i64)span * (tpr / 2) <= gs_wave_threads_b<K>(tpr / 2, bs))
         tpr /= 2;
+    if (g_batch_split) {  // right-hand-side-split kernels: TPR * K/2 threads per row
+        int t = std::min(L.tpr, std::min(g_batch_tpr_cap, 64 / K));
+        while (t > 1 && (i64)span * t * (K / 2) > gs_wave_threads_bs<K>(t, bs) &&
+               (i64)span * (t / 2) * (K / 2) <= gs_wave_threads_bs<K>(t / 2, bs))
+            t /= 2;
+        auto gos = [&](auto kern, int tt) { go(kern, tt * (K / 2)); };
+        if (zg) {
+            if (t == 1) gos(k_gs_colour_bs<1, CHUNK, K, true>, 1);
+            else if (t == 2) gos(k_gs_colour_bs<2, CHUNK, K, true>, 2);
+            else if (t == 4) gos(k_gs_colour_bs<4, CHUNK, K, true>, 4);
+            else gos(k_gs_colour_bs<8, CHUNK, K, true>, 8);
+        } else {
+            if (t == 1) gos(k_gs_colour_bs<1, CHUNK, K>, 1);
+            else if (t == 2) gos(k_gs_colour_bs<2, CHUNK, K>, 2);
+            else if (t == 4) gos(k_gs_colour_bs<4, CHUNK, K>, 4);
+            else gos(k_gs_colour_bs<8, CHUNK, K>, 8);
+        }
+        return;
+    }
     if (zg) {
         if (tpr == 1) go(k_gs_colour_b<1, CHUNK, K, true>, 1);
         else if (tpr == 2) go(k_gs_colour_b<2, CHUNK, K, true>, 2);
@@ -2984,14 +3028,39 @@ static void b_gs(mgm_ctx* ctx, const Level& L, int j, int r0, int r1, cudaStream
 }
 template <int MODE, int K>
 static void b_spmv(int tpr, i64 r1, const i64* sptr, const i32* scol, const double* sval, const double* x,
-                   const double* f, double* y, cudaStream_t st) {
+                   const double* f, double* y, cudaStream_t st, const i32* sluw = nullptr,
+                   const uint8_t* nlow = nullptr, const i32* yperm = nullptr) {
     auto go = [&](auto kern, int t) {
         launch(true, kern, blocks_for(r1 * t, 256), 256, 0, st, 0, (int)r1, sptr, scol, sval, x, f, y);
     };
+    if (g_batch_split) {
+        tpr = std::min(tpr, 64 / K);
+        auto gos = [&](auto kern, int t) {
+            launch(true, kern, blocks_for(r1 * t * (K / 2), 256), 256, 0, st, 0, (int)r1, sptr, scol, sval, x, f, y,
+                   sluw, nlow, yperm);
+        };
+        if (tpr == 1) gos(k_sell_spmv_bs<MODE, 1, CHUNK, K>, 1);
+        else if (tpr == 2) gos(k_sell_spmv_bs<MODE, 2, CHUNK, K>, 2);
+        else if (tpr == 4) gos(k_sell_spmv_bs<MODE, 4, CHUNK, K>, 4);
+        else gos(k_sell_spmv_bs<MODE, 8, CHUNK, K>, 8);
+        return;
+    }
     if (tpr == 1) go(k_sell_spmv_b<MODE, 1, CHUNK, K>, 1);
     else if (tpr == 2) go(k_sell_spmv_b<MODE, 2, CHUNK, K>, 2);
     else if (tpr == 4) go(k_sell_spmv_b<MODE, 4, CHUNK, K>, 4);
     else go(k_sell_spmv_b<MODE, 8, CHUNK, K>, 8);
+}
+template <int K>
+static void b_interp(const Level& L, const double* ec, double* e, cudaStream_t st) {
+    if (g_batch_split) {
+        auto kern = L.pm <= 8 ? k_interp_correct_bs<8, K> : k_interp_correct_bs<16, K>;
+        launch(true, kern, blocks_for(L.n * (K / 2), 256), 256, 0, st, (int)L.n, L.pm, (const i32*)L.pcol,
+               (const double*)L.pval, ec, e);
+        return;
+    }
+    auto kern = L.pm <= 8 ? k_interp_correct_b<8, K> : k_interp_correct_b<16, K>;
+    launch(true, kern, blocks_for(L.n, 256), 256, 0, st, (int)L.n, L.pm, (const i32*)L.pcol, (const double*)L.pval, ec,
+           e);
 }
 template <int K>
 static void enqueue_vcycle_b(mgm_ctx* ctx, cudaStream_t st, bool zero0) {
@@ -3028,8 +3097,19 @@ static void enqueue_vcycle_b(mgm_ctx* ctx, cudaStream_t st, bool zero0) {
             for (int s = 0; s < nu1; ++s) sweep(j, pre_b, s == 0 && zg_ok(j));
         }
         if (j > 0) stamp(ctx, "zero+presmooth", j, st);
-        b_spmv<1, K>(L.stpr, L.n, L.sptr, L.scol, L.sval, ctx->bu[j], ctx->bf[j], ctx->bt[j], st);
-        b_spmv<0, K>(L.rtpr, lv[j + 1].n, L.rptr, L.rcol, L.rval, ctx->bt[j], nullptr, ctx->bf[j + 1], st);
+        // after exactly one presmooth from the zero guess: the later-colour residual (MODE 2);
+        // the residual in Morton order for the restriction's Morton columns (split kernels)
+        const bool after_zg = nu1 == 1 && zg_ok(j) && (j > 0 || zero0);
+        const bool m2 = g_batch_split && after_zg && L.sluw && L.n >= ctx->upper_res_min;
+        const bool mt = g_batch_split && L.l2m && L.rcol_m && L.n >= g_batch_morton_min;
+        if (m2)
+            b_spmv<2, K>(L.stpr, L.n, L.sptr, L.scol, L.sval, ctx->bu[j], ctx->bf[j], ctx->bt[j], st, L.sluw, L.nlow,
+                         mt ? L.l2m : nullptr);
+        else
+            b_spmv<1, K>(L.stpr, L.n, L.sptr, L.scol, L.sval, ctx->bu[j], ctx->bf[j], ctx->bt[j], st, nullptr, nullptr,
+                         mt ? L.l2m : nullptr);
+        b_spmv<0, K>(L.rtpr, lv[j + 1].n, L.rptr, mt ? L.rcol_m : L.rcol, L.rval, ctx->bt[j], nullptr, ctx->bf[j + 1],
+                     st);
         stamp(ctx, "residual+restrict", j, st);
     }
     if (ctx->denseJ > 0) enqueue_dense_bottom(ctx, K, ctx->bf[D], ctx->bu[D], st);
@@ -3037,9 +3117,7 @@ static void enqueue_vcycle_b(mgm_ctx* ctx, cudaStream_t st, bool zero0) {
     stamp(ctx, "bottom", D, st);
     for (int j = D - 1; j >= 0; --j) {                                              // lines 11-16
         const Level& L = lv[j];
-        auto kern = L.pm <= 8 ? k_interp_correct_b<8, K> : k_interp_correct_b<16, K>;
-        launch(true, kern, blocks_for(L.n, 256), 256, 0, st, (int)L.n, L.pm, (const i32*)L.pcol,
-               (const double*)L.pval, (const double*)ctx->bu[j + 1], ctx->bu[j]);
+        b_interp<K>(L, ctx->bu[j + 1], ctx->bu[j], st);
         for (int s = 0; s < nu2; ++s) sweep(j, post_b);
         stamp(ctx, "interp+postsmooth", j, st);
     }
@@ -3081,9 +3159,7 @@ static void enqueue_levels_plain_b(mgm_ctx* ctx, int J, cudaStream_t st) {
     coarse();                                                                        // line 10
     for (int j = p - 2; j >= J; --j) {                                              // lines 11-14
         const Level& L = lv[j];
-        auto kern = L.pm <= 8 ? k_interp_correct_b<8, K> : k_interp_correct_b<16, K>;
-        launch(true, kern, blocks_for(L.n, 256), 256, 0, st, (int)L.n, L.pm, (const i32*)L.pcol,
-               (const double*)L.pval, (const double*)ctx->bu[j + 1], ctx->bu[j]);
+        b_interp<K>(L, ctx->bu[j + 1], ctx->bu[j], st);
         for (int s = 0; s < nu2; ++s) sweep(j, post_b);
     }
 }
