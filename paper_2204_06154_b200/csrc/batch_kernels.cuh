@@ -13,145 +13,15 @@
 
 namespace mgm {
 
-// acc[k] += a * xr[k], k < K, the K contiguous values gathered as 16-byte pairs (K even;
-// interleaved [row][K] vectors are 16-byte aligned for even K)
-template <int K>
-__device__ __forceinline__ void gather_fma(double a, const double* xr, double* acc) {
-    if (K % 2 == 0) {
-        const double2* x2 = reinterpret_cast<const double2*>(xr);
-#pragma unroll
-        for (int k2 = 0; k2 < K / 2; ++k2) {
-            const double2 v = x2[k2];
-            acc[2 * k2] = fma(a, v.x, acc[2 * k2]);
-            acc[2 * k2 + 1] = fma(a, v.y, acc[2 * k2 + 1]);
-        }
-    } else {
-#pragma unroll
-        for (int k = 0; k < K; ++k) acc[k] = fma(a, xr[k], acc[k]);
-    }
-}
-
-// One colour of a Gauss-Seidel sweep for K right-hand sides (cf. k_gs_colour).  ZG: the
-// sweep starts from u = 0 (the first presmooth of a coarse level): only the diagonal and the
-// earlier-colour slots are read, as in k_gs_colour<..., ZG> (slw, nlow from pack_sell).
-template <int TPR, int CH, int K, bool ZG = false>
-__global__ void __launch_bounds__(256) k_gs_colour_b(int r0, int r1, int Wu, const int64_t* __restrict__ sptr,
-                                                     const int* __restrict__ scol, const double* __restrict__ sval,
-                                                     const double* __restrict__ f, double* u,
-                                                     const int* __restrict__ slw, const uint8_t* __restrict__ nlow) {
-    pdl_trigger();
-    const int g = blockIdx.x * blockDim.x + threadIdx.x;
-    const int r = (r0 & ~31) + g / TPR;
-    const int part = g % TPR;
-    const bool live = (r >= r0 && r < r1);
-    RowFrag<TPR, CH> fr;
-    int w = 0;
-    int64_t base = 0;
-    double d = 1.0;
-    if (live) {
-        if (Wu > 0) {
-            w = Wu;
-            base = (int64_t)(r >> 5) * 32 * Wu + (r & 31);
-        } else {
-            const int64_t s0 = sptr[r >> 5];
-            w = (int)((sptr[(r >> 5) + 1] - s0) >> 5);
-            base = s0 + (r & 31);
-        }
-        int lim = 0;
-        if (ZG) {
-            w = slw[r >> 5];
-            lim = 1 + (int)nlow[r];
-        }
-        fr.load(sval + base, scol + base, ZG ? lim : w, part);
-        if (ZG) {
-#pragma unroll
-            for (int q = 0; q < CH; ++q)  // the diagonal (u_i = 0, term 0) and later colours
-                if (part + q * TPR == 0 || part + q * TPR >= lim) fr.c[q] = -1;
-            w = lim;
-        }
-        d = ld_stream_f64(sval + base);
-    } else {
-        fr.load(sval, scol, 0, 0);
-    }
-    pdl_wait();
-    double fv[K], uv[K], acc[K];
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-        fv[k] = 0.0;
-        uv[k] = 0.0;
-        acc[k] = 0.0;
-    }
-    if (live && part == 0) {
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-            fv[k] = f[(int64_t)r * K + k];
-            uv[k] = ZG ? 0.0 : u[(int64_t)r * K + k];
-        }
-    }
-    for (int k0 = part;; k0 += TPR * CH) {
-        if (k0 != part) fr.load(sval + base, scol + base, w, k0);
-#pragma unroll
-        for (int q = 0; q < CH; ++q)
-            if (fr.c[q] >= 0) gather_fma<K>(fr.a[q], u + (int64_t)fr.c[q] * K, acc);
-        if (k0 + TPR * CH >= w) break;
-    }
-#pragma unroll
-    for (int k = 0; k < K; ++k) acc[k] = group_sum<TPR>(acc[k]);
-    if (live && part == 0) {
-#pragma unroll
-        for (int k = 0; k < K; ++k) u[(int64_t)r * K + k] = uv[k] + (fv[k] - acc[k]) / d;
-    }
-}
-
-// y = A x (MODE 0), y = f - A x (MODE 1) for K right-hand sides on the rows [r0, r1).
-template <int MODE, int TPR, int CH, int K>
-__global__ void __launch_bounds__(256) k_sell_spmv_b(int r0, int r1, const int64_t* __restrict__ sptr,
-                                                     const int* __restrict__ scol, const double* __restrict__ sval,
-                                                     const double* __restrict__ x, const double* __restrict__ f,
-                                                     double* __restrict__ y) {
-    pdl_trigger();
-    const int g = blockIdx.x * blockDim.x + threadIdx.x;
-    const int r = (r0 & ~31) + g / TPR;
-    const int part = g % TPR;
-    const bool live = r >= r0 && r < r1;
-    RowFrag<TPR, CH> fr;
-    int w = 0;
-    int64_t base = 0;
-    if (live) {
-        const int64_t s0 = sptr[r >> 5];
-        w = (int)((sptr[(r >> 5) + 1] - s0) >> 5);
-        base = s0 + (r & 31);
-        fr.load(sval + base, scol + base, w, part);
-    } else {
-        fr.load(sval, scol, 0, 0);
-    }
-    pdl_wait();
-    double acc[K];
-#pragma unroll
-    for (int k = 0; k < K; ++k) acc[k] = 0.0;
-    for (int k0 = part;; k0 += TPR * CH) {
-        if (k0 != part) fr.load(sval + base, scol + base, w, k0);
-#pragma unroll
-        for (int q = 0; q < CH; ++q)
-            if (fr.c[q] >= 0) gather_fma<K>(fr.a[q], x + (int64_t)fr.c[q] * K, acc);
-        if (k0 + TPR * CH >= w) break;
-    }
-#pragma unroll
-    for (int k = 0; k < K; ++k) acc[k] = group_sum<TPR>(acc[k]);
-    if (live && part == 0) {
-#pragma unroll
-        for (int k = 0; k < K; ++k)
-            y[(int64_t)r * K + k] = (MODE == 0) ? acc[k] : f[(int64_t)r * K + k] - acc[k];
-    }
-}
-
-// ---- right-hand-side-split variants: KS = K/2 threads per (row, slot part), each owning the
-// pair of right-hand sides (2 kk, 2 kk + 1).  A gather of column j by the KS threads of a row
+// ---- Colour sweep / SpMV / interpolation for K right-hand sides (K even), split over the
+// right-hand sides: KS = K/2 threads per (row, slot part), each owning the pair of
+// right-hand sides (2 kk, 2 kk + 1).  A gather of column j by the KS threads of a row
 // reads the K contiguous values of u[j][*] as ONE coalesced 16 * KS-byte segment (instead of
 // K/2 16-byte loads by one thread, each warp load touching 32 scattered lines); the operator
 // entry (same address for the KS threads) is one broadcast load.  Per (row, right-hand side)
-// the slots are summed in the same order by the same slot part as the unsplit kernels (TPR
-// parts, group sum over the parts), so the results are bitwise theirs.
+// the slots are summed exactly as the single-RHS kernels sum them with TPR threads per row
+// (TPR slot parts, then the group sum over the parts).  One thread gathering all K values of
+// a column (round 1) measured 3.88 ms per K = 8 V-cycle at cfg3 against 3.06 split.
 template <int TPR, int KS>
 __device__ __forceinline__ double part_sum(double v) {
 #pragma unroll
@@ -325,37 +195,6 @@ __global__ void __launch_bounds__(256) k_interp_correct_bs(int n, int m, const i
     o.x += a0;
     o.y += a1;
     e2[(int64_t)r * KS + kk] = o;
-}
-
-// e += P ec for K right-hand sides (interpolate + correct), rows [0, n)
-template <int M, int K>
-__global__ void __launch_bounds__(256) k_interp_correct_b(int n, int m, const int* __restrict__ pcol,
-                                                          const double* __restrict__ pval,
-                                                          const double* __restrict__ ec, double* __restrict__ e) {
-    pdl_trigger();
-    const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    int cidx[M];
-    double a[M];
-#pragma unroll
-    for (int q = 0; q < M; ++q) {
-        const bool ok = r < n && q < m;
-        cidx[q] = ok ? ld_stream_i32(pcol + (int64_t)q * n + r) : -1;
-        a[q] = ok ? ld_stream_f64(pval + (int64_t)q * n + r) : 0.0;
-    }
-    pdl_wait();
-    if (r >= n) return;
-    double acc[K];
-#pragma unroll
-    for (int k = 0; k < K; ++k) acc[k] = 0.0;
-#pragma unroll
-    for (int q = 0; q < M; ++q)
-        if (cidx[q] >= 0) {
-            const double* xr = ec + (int64_t)cidx[q] * K;
-#pragma unroll
-            for (int k = 0; k < K; ++k) acc[k] = fma(a[q], xr[k], acc[k]);
-        }
-#pragma unroll
-    for (int k = 0; k < K; ++k) e[(int64_t)r * K + k] += acc[k];
 }
 
 // coarsest level: y = A^{-1} x for K right-hand sides with the explicit inverse (row-major)

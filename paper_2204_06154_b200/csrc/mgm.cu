@@ -2936,32 +2936,10 @@ mgm_status bicgstab_lib(mgm_ctx* ctx, double tol, int maxit, mgm_report* rep, cu
 // ---------------------------------------------------------------------------------------
 // threads per row cap of the batched colour kernels (MGM_BATCH_TPR_CAP; experiment)
 static int g_batch_tpr_cap = std::getenv("MGM_BATCH_TPR_CAP") ? std::max(1, std::atoi(std::getenv("MGM_BATCH_TPR_CAP"))) : 8;
-// threads one wave of batched colour kernels can hold (all SMs, register-limited occupancy)
-template <int K>
-static i64 gs_wave_threads_b(int tpr, int block) {
-    static i64 cache[4][4] = {};
-    const int ti = tpr == 1 ? 0 : tpr == 2 ? 1 : tpr == 4 ? 2 : 3;
-    const int bi = block == 64 ? 0 : block == 128 ? 1 : block == 256 ? 2 : 3;
-    if (cache[ti][bi]) return cache[ti][bi];
-    int dev = 0, nsm = 0, per = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    const void* k = tpr == 1 ? (const void*)k_gs_colour_b<1, CHUNK, K>
-                  : tpr == 2 ? (const void*)k_gs_colour_b<2, CHUNK, K>
-                  : tpr == 4 ? (const void*)k_gs_colour_b<4, CHUNK, K>
-                             : (const void*)k_gs_colour_b<8, CHUNK, K>;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, block, 0) != cudaSuccess) {
-        cudaGetLastError();
-        per = 1;
-    }
-    return cache[ti][bi] = (i64)per * nsm * block;
-}
 // batched levels with at least this many rows write the residual in Morton order
 // (MGM_BATCH_MORTON_T_MIN; off by default: cfg3 K = 8 residual+restrict L0 437 vs 413 us)
 static i64 g_batch_morton_min = std::getenv("MGM_BATCH_MORTON_T_MIN") ? std::atoll(std::getenv("MGM_BATCH_MORTON_T_MIN"))
                                                                       : (i64)1 << 62;
-// MGM_BATCH_SPLIT=0: the unsplit batched kernels (one thread gathers all K values of a column)
-static bool g_batch_split = !(std::getenv("MGM_BATCH_SPLIT") && std::atoi(std::getenv("MGM_BATCH_SPLIT")) == 0);
 template <int K>
 static i64 gs_wave_threads_bs(int tpr, int block) {
     static i64 cache[4][4] = {};
@@ -2981,49 +2959,31 @@ static i64 gs_wave_threads_bs(int tpr, int block) {
     }
     return cache[ti][bi] = (i64)per * nsm * block;
 }
+// K right-hand sides (K even): TPR * K/2 threads per row (batch_kernels.cuh)
 template <int K>
 static void b_gs(mgm_ctx* ctx, const Level& L, int j, int r0, int r1, cudaStream_t st, bool zg = false) {
     const int span = r1 - (r0 & ~31);
     const int bs = L.gs_block;
-    auto go = [&](auto kern, int tpr) {
-        launch(true, kern, blocks_for((i64)span * tpr, bs), bs, 0, st, r0, r1, L.uniform_w, (const i64*)L.sptr,
-               (const i32*)L.scol, (const double*)L.sval, (const double*)ctx->bf[j], ctx->bu[j],
+    auto go = [&](auto kern, int t) {
+        launch(true, kern, blocks_for((i64)span * t * (K / 2), bs), bs, 0, st, r0, r1, L.uniform_w,
+               (const i64*)L.sptr, (const i32*)L.scol, (const double*)L.sval, (const double*)ctx->bf[j], ctx->bu[j],
                (const i32*)L.slw, (const uint8_t*)L.nlow);
     };
     // a colour just above one (register-limited) wave: halve the threads per row (cf. launch_gs)
-    int tpr = std::min(L.tpr, g_batch_tpr_cap);
-    while (tpr > 1 && (i64)span * tpr > gs_wave_threads_b<K>(tpr, bs) &&
-           (i64)span * (tpr / 2) <= gs_wave_threads_b<K>(tpr / 2, bs))
-        tpr /= 2;
-    if (g_batch_split) {  // right-hand-side-split kernels: TPR * K/2 threads per row
-        int t = std::min(L.tpr, std::min(g_batch_tpr_cap, 64 / K));
-        while (t > 1 && (i64)span * t * (K / 2) > gs_wave_threads_bs<K>(t, bs) &&
-               (i64)span * (t / 2) * (K / 2) <= gs_wave_threads_bs<K>(t / 2, bs))
-            t /= 2;
-        auto gos = [&](auto kern, int tt) { go(kern, tt * (K / 2)); };
-        if (zg) {
-            if (t == 1) gos(k_gs_colour_bs<1, CHUNK, K, true>, 1);
-            else if (t == 2) gos(k_gs_colour_bs<2, CHUNK, K, true>, 2);
-            else if (t == 4) gos(k_gs_colour_bs<4, CHUNK, K, true>, 4);
-            else gos(k_gs_colour_bs<8, CHUNK, K, true>, 8);
-        } else {
-            if (t == 1) gos(k_gs_colour_bs<1, CHUNK, K>, 1);
-            else if (t == 2) gos(k_gs_colour_bs<2, CHUNK, K>, 2);
-            else if (t == 4) gos(k_gs_colour_bs<4, CHUNK, K>, 4);
-            else gos(k_gs_colour_bs<8, CHUNK, K>, 8);
-        }
-        return;
-    }
+    int t = std::min(L.tpr, std::min(g_batch_tpr_cap, 64 / K));
+    while (t > 1 && (i64)span * t * (K / 2) > gs_wave_threads_bs<K>(t, bs) &&
+           (i64)span * (t / 2) * (K / 2) <= gs_wave_threads_bs<K>(t / 2, bs))
+        t /= 2;
     if (zg) {
-        if (tpr == 1) go(k_gs_colour_b<1, CHUNK, K, true>, 1);
-        else if (tpr == 2) go(k_gs_colour_b<2, CHUNK, K, true>, 2);
-        else if (tpr == 4) go(k_gs_colour_b<4, CHUNK, K, true>, 4);
-        else go(k_gs_colour_b<8, CHUNK, K, true>, 8);
+        if (t == 1) go(k_gs_colour_bs<1, CHUNK, K, true>, 1);
+        else if (t == 2) go(k_gs_colour_bs<2, CHUNK, K, true>, 2);
+        else if (t == 4) go(k_gs_colour_bs<4, CHUNK, K, true>, 4);
+        else go(k_gs_colour_bs<8, CHUNK, K, true>, 8);
     } else {
-        if (tpr == 1) go(k_gs_colour_b<1, CHUNK, K>, 1);
-        else if (tpr == 2) go(k_gs_colour_b<2, CHUNK, K>, 2);
-        else if (tpr == 4) go(k_gs_colour_b<4, CHUNK, K>, 4);
-        else go(k_gs_colour_b<8, CHUNK, K>, 8);
+        if (t == 1) go(k_gs_colour_bs<1, CHUNK, K>, 1);
+        else if (t == 2) go(k_gs_colour_bs<2, CHUNK, K>, 2);
+        else if (t == 4) go(k_gs_colour_bs<4, CHUNK, K>, 4);
+        else go(k_gs_colour_bs<8, CHUNK, K>, 8);
     }
 }
 template <int MODE, int K>
@@ -3031,36 +2991,20 @@ static void b_spmv(int tpr, i64 r1, const i64* sptr, const i32* scol, const doub
                    const double* f, double* y, cudaStream_t st, const i32* sluw = nullptr,
                    const uint8_t* nlow = nullptr, const i32* yperm = nullptr) {
     auto go = [&](auto kern, int t) {
-        launch(true, kern, blocks_for(r1 * t, 256), 256, 0, st, 0, (int)r1, sptr, scol, sval, x, f, y);
+        launch(true, kern, blocks_for(r1 * t * (K / 2), 256), 256, 0, st, 0, (int)r1, sptr, scol, sval, x, f, y, sluw,
+               nlow, yperm);
     };
-    if (g_batch_split) {
-        tpr = std::min(tpr, 64 / K);
-        auto gos = [&](auto kern, int t) {
-            launch(true, kern, blocks_for(r1 * t * (K / 2), 256), 256, 0, st, 0, (int)r1, sptr, scol, sval, x, f, y,
-                   sluw, nlow, yperm);
-        };
-        if (tpr == 1) gos(k_sell_spmv_bs<MODE, 1, CHUNK, K>, 1);
-        else if (tpr == 2) gos(k_sell_spmv_bs<MODE, 2, CHUNK, K>, 2);
-        else if (tpr == 4) gos(k_sell_spmv_bs<MODE, 4, CHUNK, K>, 4);
-        else gos(k_sell_spmv_bs<MODE, 8, CHUNK, K>, 8);
-        return;
-    }
-    if (tpr == 1) go(k_sell_spmv_b<MODE, 1, CHUNK, K>, 1);
-    else if (tpr == 2) go(k_sell_spmv_b<MODE, 2, CHUNK, K>, 2);
-    else if (tpr == 4) go(k_sell_spmv_b<MODE, 4, CHUNK, K>, 4);
-    else go(k_sell_spmv_b<MODE, 8, CHUNK, K>, 8);
+    tpr = std::min(tpr, 64 / K);
+    if (tpr == 1) go(k_sell_spmv_bs<MODE, 1, CHUNK, K>, 1);
+    else if (tpr == 2) go(k_sell_spmv_bs<MODE, 2, CHUNK, K>, 2);
+    else if (tpr == 4) go(k_sell_spmv_bs<MODE, 4, CHUNK, K>, 4);
+    else go(k_sell_spmv_bs<MODE, 8, CHUNK, K>, 8);
 }
 template <int K>
 static void b_interp(const Level& L, const double* ec, double* e, cudaStream_t st) {
-    if (g_batch_split) {
-        auto kern = L.pm <= 8 ? k_interp_correct_bs<8, K> : k_interp_correct_bs<16, K>;
-        launch(true, kern, blocks_for(L.n * (K / 2), 256), 256, 0, st, (int)L.n, L.pm, (const i32*)L.pcol,
-               (const double*)L.pval, ec, e);
-        return;
-    }
-    auto kern = L.pm <= 8 ? k_interp_correct_b<8, K> : k_interp_correct_b<16, K>;
-    launch(true, kern, blocks_for(L.n, 256), 256, 0, st, (int)L.n, L.pm, (const i32*)L.pcol, (const double*)L.pval, ec,
-           e);
+    auto kern = L.pm <= 8 ? k_interp_correct_bs<8, K> : k_interp_correct_bs<16, K>;
+    launch(true, kern, blocks_for(L.n * (K / 2), 256), 256, 0, st, (int)L.n, L.pm, (const i32*)L.pcol,
+           (const double*)L.pval, ec, e);
 }
 template <int K>
 static void enqueue_vcycle_b(mgm_ctx* ctx, cudaStream_t st, bool zero0) {
@@ -3100,8 +3044,8 @@ static void enqueue_vcycle_b(mgm_ctx* ctx, cudaStream_t st, bool zero0) {
         // after exactly one presmooth from the zero guess: the later-colour residual (MODE 2);
         // the residual in Morton order for the restriction's Morton columns (split kernels)
         const bool after_zg = nu1 == 1 && zg_ok(j) && (j > 0 || zero0);
-        const bool m2 = g_batch_split && after_zg && L.sluw && L.n >= ctx->upper_res_min;
-        const bool mt = g_batch_split && L.l2m && L.rcol_m && L.n >= g_batch_morton_min;
+        const bool m2 = after_zg && L.sluw && L.n >= ctx->upper_res_min;
+        const bool mt = L.l2m && L.rcol_m && L.n >= g_batch_morton_min;
         if (m2)
             b_spmv<2, K>(L.stpr, L.n, L.sptr, L.scol, L.sval, ctx->bu[j], ctx->bf[j], ctx->bt[j], st, L.sluw, L.nlow,
                          mt ? L.l2m : nullptr);
