@@ -210,7 +210,9 @@ def stage_breakdown(w, f, hbm):
             return 8.0 * lv[j]["n"] + sweep_b(j, nu1)
         if name == "residual+restrict":
             res = 12.0 * lv[j]["nnz"] + 24.0 * lv[j]["n"]
-            if lv[j]["nnz_zg"] < lv[j]["nnz"] and nu1 == 1 and lv[j]["n"] >= 131072:  # after the zero-guess sweep
+            # after the zero-guess sweep (coarse levels always start from zero; the traced level 0
+            # does not: the graph is the V-cycle from the caller's u, MODE 1)
+            if j > 0 and lv[j]["nnz_zg"] < lv[j]["nnz"] and nu1 == 1 and lv[j]["n"] >= 131072:
                 res = 12.0 * (lv[j]["nnz"] - lv[j]["nnz_zg"]) + 24.0 * lv[j]["n"]
             return res + 12.0 * lv[j]["nnz_P"] + 8.0 * lv[j]["n"] + 8.0 * lv[j + 1]["n"]
         if name == "interp":

@@ -2959,6 +2959,13 @@ static i64 gs_wave_threads_bs(int tpr, int block) {
     }
     return cache[ti][bi] = (i64)per * nsm * block;
 }
+// 8-slot register chunks in the batched kernels (fewer registers, more CTAs per SM) on the
+// bandwidth-bound levels; 16-slot chunks (fewer dependent operator loads) on the small K = 8
+// levels.  Measured at cfg3 (traced V-cycle, tools/batch_trace.py): K = 8 L0 presmooth 457 ->
+// 364 us, residual+restrict 414 -> 381, postsmooth 514 -> 420, but L3 postsmooth 78 -> 102;
+// K = 4 every level gains.  MGM_BATCH_CH8=0/1 forces either.
+static int g_batch_ch8_env = std::getenv("MGM_BATCH_CH8") ? std::atoi(std::getenv("MGM_BATCH_CH8")) : -1;
+static bool batch_ch8(int K, i64 n) { return g_batch_ch8_env >= 0 ? g_batch_ch8_env != 0 : (K == 4 || n >= 131072); }
 // K right-hand sides (K even): TPR * K/2 threads per row (batch_kernels.cuh)
 template <int K>
 static void b_gs(mgm_ctx* ctx, const Level& L, int j, int r0, int r1, cudaStream_t st, bool zg = false) {
@@ -2974,6 +2981,22 @@ static void b_gs(mgm_ctx* ctx, const Level& L, int j, int r0, int r1, cudaStream
     while (t > 1 && (i64)span * t * (K / 2) > gs_wave_threads_bs<K>(t, bs) &&
            (i64)span * (t / 2) * (K / 2) <= gs_wave_threads_bs<K>(t / 2, bs))
         t /= 2;
+    if constexpr (K >= 4) {
+        if (batch_ch8(K, L.n)) {
+            if (zg) {
+                if (t == 1) go(k_gs_colour_bs<1, 8, K, true>, 1);
+                else if (t == 2) go(k_gs_colour_bs<2, 8, K, true>, 2);
+                else if (t == 4) go(k_gs_colour_bs<4, 8, K, true>, 4);
+                else go(k_gs_colour_bs<8, 8, K, true>, 8);
+            } else {
+                if (t == 1) go(k_gs_colour_bs<1, 8, K>, 1);
+                else if (t == 2) go(k_gs_colour_bs<2, 8, K>, 2);
+                else if (t == 4) go(k_gs_colour_bs<4, 8, K>, 4);
+                else go(k_gs_colour_bs<8, 8, K>, 8);
+            }
+            return;
+        }
+    }
     if (zg) {
         if (t == 1) go(k_gs_colour_bs<1, CHUNK, K, true>, 1);
         else if (t == 2) go(k_gs_colour_bs<2, CHUNK, K, true>, 2);
@@ -2995,6 +3018,15 @@ static void b_spmv(int tpr, i64 r1, const i64* sptr, const i32* scol, const doub
                nlow, yperm);
     };
     tpr = std::min(tpr, 64 / K);
+    if constexpr (K >= 4) {
+        if (batch_ch8(K, r1)) {
+            if (tpr == 1) go(k_sell_spmv_bs<MODE, 1, 8, K>, 1);
+            else if (tpr == 2) go(k_sell_spmv_bs<MODE, 2, 8, K>, 2);
+            else if (tpr == 4) go(k_sell_spmv_bs<MODE, 4, 8, K>, 4);
+            else go(k_sell_spmv_bs<MODE, 8, 8, K>, 8);
+            return;
+        }
+    }
     if (tpr == 1) go(k_sell_spmv_bs<MODE, 1, CHUNK, K>, 1);
     else if (tpr == 2) go(k_sell_spmv_bs<MODE, 2, CHUNK, K>, 2);
     else if (tpr == 4) go(k_sell_spmv_bs<MODE, 4, CHUNK, K>, 4);
