@@ -171,6 +171,79 @@ __global__ void __launch_bounds__(DENSE_THREADS) k_dense_apply_multi(int m, int 
     }
 }
 
+// Split over the columns (the reduction dimension) for K > 1: CTA (x, y) computes rows
+// [32 x, 32 x + 32) over the column slice y of S (width cs, a multiple of 64) and writes the
+// partial sums P[y][row][k]; k_dense_sum adds the S partials in order y = 0..S-1
+// (deterministic).  Without the split the K = 8 apply ran 128 CTAs with ~16 KB of B in flight
+// per SM: latency-bound at ~1.3 TB/s (109 us for 134 MB).
+template <int K, int RPW>
+__global__ void __launch_bounds__(DENSE_THREADS) k_dense_apply_split(int m, int ld, int cs,
+                                                                     const double* __restrict__ B,
+                                                                     const double* __restrict__ X,
+                                                                     double* __restrict__ P) {
+    constexpr int CR = 4096 / K;
+    __shared__ __align__(16) double xs[CR * K];
+    pdl_trigger();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int row0 = (blockIdx.x * DENSE_ROWS_PER_CTA + warp) * RPW;
+    const int cb = blockIdx.y * cs, ce = min(ld, cb + cs);
+    double acc[RPW][K];
+#pragma unroll
+    for (int r = 0; r < RPW; ++r)
+#pragma unroll
+        for (int k = 0; k < K; ++k) acc[r][k] = 0.0;
+    pdl_wait();
+    for (int c0 = cb; c0 < ce; c0 += CR) {
+        const int cn = min(CR, ce - c0);
+        if (c0 > cb) __syncthreads();
+        for (int t = threadIdx.x; t < cn * K; t += DENSE_THREADS) {
+            const int i = c0 + t / K;
+            xs[t] = i < m ? X[(int64_t)c0 * K + t] : 0.0;
+        }
+        __syncthreads();
+        for (int c = 2 * lane; c < cn; c += 64) {
+            double2 v[RPW];
+#pragma unroll
+            for (int r = 0; r < RPW; ++r)
+                v[r] = (row0 + r < m) ? ld_stream_f64x2(B + (int64_t)(row0 + r) * ld + c0 + c) : make_double2(0.0, 0.0);
+#pragma unroll
+            for (int k2 = 0; k2 < K / 2; ++k2) {
+                const double2 a2 = *reinterpret_cast<const double2*>(xs + c * K + 2 * k2);
+                const double2 b2 = *reinterpret_cast<const double2*>(xs + (c + 1) * K + 2 * k2);
+#pragma unroll
+                for (int r = 0; r < RPW; ++r) {
+                    acc[r][2 * k2] = fma(v[r].x, a2.x, acc[r][2 * k2]);
+                    acc[r][2 * k2 + 1] = fma(v[r].x, a2.y, acc[r][2 * k2 + 1]);
+                    acc[r][2 * k2] = fma(v[r].y, b2.x, acc[r][2 * k2]);
+                    acc[r][2 * k2 + 1] = fma(v[r].y, b2.y, acc[r][2 * k2 + 1]);
+                }
+            }
+        }
+    }
+    double* Pq = P + (int64_t)blockIdx.y * m * K;
+#pragma unroll
+    for (int r = 0; r < RPW; ++r) {
+        if (row0 + r >= m) break;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            double s = acc[r][k];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+            if (lane == 0) Pq[(int64_t)(row0 + r) * K + k] = s;
+        }
+    }
+}
+// Y[t] = sum_{y < S} P[y][t], t < m K (fixed order)
+__global__ void k_dense_sum(int64_t mk, int S, const double* __restrict__ P, double* __restrict__ Y) {
+    pdl_trigger();
+    pdl_wait();
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < mk; t += (int64_t)gridDim.x * blockDim.x) {
+        double s = P[t];
+        for (int y = 1; y < S; ++y) s += P[(int64_t)y * mk + t];
+        Y[t] = s;
+    }
+}
+
 // e_J (n rows) <- unit vector e_i (setup of B_J, one column per replay)
 __global__ void k_unit(int n, int i, double* __restrict__ f) {
     for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) f[r] = r == i ? 1.0 : 0.0;

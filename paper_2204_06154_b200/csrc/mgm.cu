@@ -392,6 +392,7 @@ struct mgm_ctx {
     int denseJ = -1;
     int dense_m = 0, dense_ld = 0;
     double* dB = nullptr;
+    double* dP = nullptr;  // partial sums of the column-split multi-RHS dense apply [S][m][8]
     int bot_cluster = 16;
     size_t bot_smem = 0;
     int nphases = 0;
@@ -963,6 +964,8 @@ void setup_bottom(mgm_ctx* ctx, const std::vector<double>& LU, const std::vector
 // Level J of the dense bottom (dense_bottom.cuh): the first level j >= 1 with
 // N_j (+1 Poisson) <= MGM_DENSE_MAX (default 4096: B_J = 134 MB, one HBM-bound apply per
 // V-cycle instead of the latency-bound colour steps of levels J..p-1); -1 = off.
+// column slices of the multi-RHS dense apply (MGM_DENSE_SPLIT; 1 = one kernel, no partials)
+static int g_dense_split = std::getenv("MGM_DENSE_SPLIT") ? std::max(1, std::atoi(std::getenv("MGM_DENSE_SPLIT"))) : 4;
 int dense_level(const mgm_ctx* ctx) {
     i64 dmax = 4096;
     if (const char* e = std::getenv("MGM_DENSE_MAX")) dmax = std::atoll(e);
@@ -2215,6 +2218,7 @@ mgm_status setup_dense_bottom(mgm_ctx* ctx) {
         CK(cudaGetLastError());
         ctx->dense_m = mdim;
         ctx->dense_ld = ld;
+        if (g_dense_split > 1) CK(dalloc(&ctx->dP, (i64)g_dense_split * mdim * 8));
         return MGM_OK;
     }
     cudaGraph_t g = nullptr;
@@ -2245,6 +2249,7 @@ mgm_status setup_dense_bottom(mgm_ctx* ctx) {
     CK(cudaGetLastError());
     ctx->dense_m = mdim;
     ctx->dense_ld = ld;
+    if (g_dense_split > 1) CK(dalloc(&ctx->dP, (i64)g_dense_split * mdim * 8));
     return MGM_OK;
 }
 
@@ -2253,6 +2258,31 @@ void enqueue_dense_bottom(mgm_ctx* ctx, int K, const double* r, double* e, cudaS
     const unsigned grid = blocks_for(ctx->dense_m, DENSE_ROWS_PER_CTA);
     const int mm = ctx->dense_m, ld = ctx->dense_ld;
     const double* B = ctx->dB;
+    if (K > 1 && ctx->dP && g_dense_split > 1) {  // column-split apply + ordered sum of the partials
+        const int S = g_dense_split;
+        const int cs = (int)(((ld + S - 1) / S + 63) / 64 * 64);
+        const dim3 g2(blocks_for(mm, 4 * DENSE_ROWS_PER_CTA), (unsigned)((ld + cs - 1) / cs));
+        auto go = [&](auto kern) {
+            if (g_dry) return;
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = g2;
+            cfg.blockDim = dim3(DENSE_THREADS);
+            cfg.stream = st;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            at[0].val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = g_use_pdl ? 1 : 0;
+            note_launch(cudaLaunchKernelEx(&cfg, kern, mm, ld, cs, B, r, ctx->dP), g2.x * g2.y, DENSE_THREADS, 0);
+        };
+        if (K == 2) go(k_dense_apply_split<2, 4>);
+        else if (K == 4) go(k_dense_apply_split<4, 4>);
+        else go(k_dense_apply_split<8, 4>);
+        launch(true, k_dense_sum, blocks_for((i64)mm * K, 256), 256, 0, st, (int64_t)mm * K, (int)g2.y,
+               (const double*)ctx->dP, e);
+        ctx->vcycle_kernels += 2;
+        return;
+    }
     switch (K) {
         case 1: launch(ctx->pdl, k_dense_apply<1>, grid, DENSE_THREADS, 0, st, mm, ld, B, r, e); break;
         case 2: launch(true, k_dense_apply_multi<2, 4>, blocks_for(mm, 4 * DENSE_ROWS_PER_CTA), DENSE_THREADS, 0, st,
@@ -4324,6 +4354,7 @@ mgm_status mgm_destroy(mgm_ctx* ctx) {
     if (ctx->bhh) cudaFreeHost(ctx->bhh);
     if (ctx->ainv) dev_free(ctx->ainv);
     if (ctx->dB) dev_free(ctx->dB);
+    if (ctx->dP) dev_free(ctx->dP);
     for (auto& T : ctx->timer)
         for (auto e : T.ev) cudaEventDestroy(e);
     if (ctx->st) cudaStreamDestroy(ctx->st);
