@@ -3,6 +3,7 @@
 // and the C ABI declared in include/mgm.h.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <cusolverDn.h>
 #include <nccl.h>
 
 #include <algorithm>
@@ -66,6 +67,35 @@ NcclApi& nccl() {
             api.Recv = (decltype(api.Recv))dlsym(h, "ncclRecv");
             api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.Broadcast && api.AllReduce &&
                      api.GroupStart && api.GroupEnd && api.GetErrorString && api.Send && api.Recv;
+        }
+    }
+    return api;
+}
+// cuSOLVER (dense LU of the coarsest operator at setup), loaded at run time like NCCL.
+struct CusolverApi {
+    bool tried = false, ok = false;
+    cusolverStatus_t (*Create)(cusolverDnHandle_t*) = nullptr;
+    cusolverStatus_t (*Destroy)(cusolverDnHandle_t) = nullptr;
+    cusolverStatus_t (*SetStream)(cusolverDnHandle_t, cudaStream_t) = nullptr;
+    cusolverStatus_t (*GetrfBuf)(cusolverDnHandle_t, int, int, double*, int, int*) = nullptr;
+    cusolverStatus_t (*Getrf)(cusolverDnHandle_t, int, int, double*, int, double*, int*, int*) = nullptr;
+    cusolverStatus_t (*Getrs)(cusolverDnHandle_t, cublasOperation_t, int, int, const double*, int, const int*,
+                              double*, int, int*) = nullptr;
+};
+CusolverApi& cusolver() {
+    static CusolverApi api;
+    if (!api.tried) {
+        api.tried = true;
+        void* h = dlopen("libcusolver.so.11", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libcusolver.so", RTLD_NOW | RTLD_GLOBAL);
+        if (h) {
+            api.Create = (decltype(api.Create))dlsym(h, "cusolverDnCreate");
+            api.Destroy = (decltype(api.Destroy))dlsym(h, "cusolverDnDestroy");
+            api.SetStream = (decltype(api.SetStream))dlsym(h, "cusolverDnSetStream");
+            api.GetrfBuf = (decltype(api.GetrfBuf))dlsym(h, "cusolverDnDgetrf_bufferSize");
+            api.Getrf = (decltype(api.Getrf))dlsym(h, "cusolverDnDgetrf");
+            api.Getrs = (decltype(api.Getrs))dlsym(h, "cusolverDnDgetrs");
+            api.ok = api.Create && api.Destroy && api.SetStream && api.GetrfBuf && api.Getrf && api.Getrs;
         }
     }
     return api;
@@ -988,6 +1018,84 @@ struct SetupTimer {
     }
 };
 
+// Coarsest LU on the device (cuSOLVER): A row-major on the host -> ctx->lu (column-major
+// factors, unit L below the diagonal), ctx->piv (0-based row swaps, as dense_lu_colmajor),
+// and with want_inv the explicit inverse ctx->ainv (row-major) from getrs on A^T X = I
+// (X = A^-T column-major = A^-1 row-major).  *bad = the first pivot column with
+// |u_kk| <= 1e-14 max|a_ij| (dense_lu_colmajor's singularity test), else -1.
+__global__ void k_identity(int m, double* X) {
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < (int64_t)m * m;
+         t += (int64_t)gridDim.x * blockDim.x)
+        X[t] = (t / m == t % m) ? 1.0 : 0.0;
+}
+__global__ void k_piv0(int m, const int* __restrict__ ipiv1, int* __restrict__ piv0) {
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < m; k += gridDim.x * blockDim.x) piv0[k] = ipiv1[k] - 1;
+}
+mgm_status device_lu(mgm_ctx* ctx, const std::vector<double>& A, int m, bool want_inv, i64* bad) {
+    cudaStream_t st = ctx->st;
+    CusolverApi& cs = cusolver();
+    double amax = 0.0;
+    for (double v : A) amax = std::max(amax, std::fabs(v));
+    std::vector<double> Ac((size_t)m * m);  // column-major copy
+    {
+        auto cols = [&](i64 a, i64 b) {
+            for (i64 j = a; j < b; ++j)
+                for (int i = 0; i < m; ++i) Ac[(size_t)j * m + i] = A[(size_t)i * m + j];
+        };
+        const int nt = m >= 512 ? host_threads() : 1;
+        std::vector<std::thread> th;
+        for (int t = 1; t < nt; ++t) th.emplace_back(cols, (i64)m * t / nt, (i64)m * (t + 1) / nt);
+        cols(0, (i64)m / nt);
+        for (auto& x : th) x.join();
+    }
+    if (mgm_status s = upload(ctx, &ctx->lu, Ac)) return s;
+    cusolverDnHandle_t h = nullptr;
+    if (cs.Create(&h) != CUSOLVER_STATUS_SUCCESS) {
+        ctx->err = "cusolverDnCreate failed";
+        return MGM_ERR_CUDA;
+    }
+    struct HDel { CusolverApi& cs; cusolverDnHandle_t h; ~HDel() { cs.Destroy(h); } } hdel_{cs, h};
+    cs.SetStream(h, st);
+    int lwork = 0;
+    if (cs.GetrfBuf(h, m, m, ctx->lu, m, &lwork) != CUSOLVER_STATUS_SUCCESS) {
+        ctx->err = "cusolverDnDgetrf_bufferSize failed";
+        return MGM_ERR_CUDA;
+    }
+    double* work = nullptr;
+    int *ipiv = nullptr, *info = nullptr;
+    CK(dalloc(&work, std::max(lwork, 1)));
+    CK(dalloc(&ipiv, m));
+    CK(dalloc(&info, 1));
+    struct WDel { double* w; int* a; int* b; ~WDel() { dev_free(w); dev_free(a); dev_free(b); } } wdel_{work, ipiv, info};
+    if (cs.Getrf(h, m, m, ctx->lu, m, work, ipiv, info) != CUSOLVER_STATUS_SUCCESS) {
+        ctx->err = "cusolverDnDgetrf failed";
+        return MGM_ERR_CUDA;
+    }
+    std::vector<double> dg(m);
+    CK(cudaMemcpy2DAsync(dg.data(), sizeof(double), ctx->lu, sizeof(double) * (m + 1), sizeof(double), m,
+                         cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    *bad = -1;
+    for (int k = 0; k < m; ++k)
+        if (!(std::fabs(dg[k]) > 1e-14 * amax)) {
+            *bad = k;
+            return MGM_OK;
+        }
+    CK(dalloc(&ctx->piv, m));
+    k_piv0<<<blocks_for(m, 256), 256, 0, st>>>(m, ipiv, ctx->piv);
+    if (want_inv) {
+        CK(dalloc(&ctx->ainv, (i64)m * m));
+        k_identity<<<1184, 256, 0, st>>>(m, ctx->ainv);
+        if (cs.Getrs(h, CUBLAS_OP_T, m, m, ctx->lu, m, ipiv, ctx->ainv, m, info) != CUSOLVER_STATUS_SUCCESS) {
+            ctx->err = "cusolverDnDgetrs failed";
+            return MGM_ERR_CUDA;
+        }
+    }
+    CK(cudaStreamSynchronize(st));
+    CK(cudaGetLastError());
+    return MGM_OK;
+}
+
 mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i64 N) {
     DeferFree deferred;  // (destroyed last: after every setup thread has been joined)
     DeferScope defer_(&deferred);
@@ -1589,20 +1697,39 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
         std::vector<double> LU;
         std::vector<i32> piv;
         tm.mark("border vectors");
-        i64 bad = dense_lu_colmajor(A, m, LU, piv);
-        tm.mark("coarse LU", p - 1);
-        if (bad >= 0) return fail(ctx, MGM_ERR_SINGULAR, "singular coarsest operator", bad);
         ctx->nc = m;
-        if ((s = upload(ctx, &ctx->lu, LU)) || (s = upload(ctx, &ctx->piv, piv))) return s;
-        CK(cudaStreamSynchronize(st));
-        ctx->denseJ = dense_level(ctx);
-        if (ctx->denseJ < 0) setup_bottom(ctx, LU, piv);  // (the dense bottom replaces it)
-        tm.mark("bottom kernel setup", p - 1);
-        if (m <= 4096) {  // explicit inverse for the batched coarse solve (same solution up to rounding, O13)
-            std::vector<double> Ainv;
-            dense_inverse(LU, piv, m, Ainv, nth);
-            if ((s = upload(ctx, &ctx->ainv, Ainv))) return s;
-            tm.mark("coarse inverse", p - 1);
+        // large coarsest levels (MGM_DEVICE_LU_MIN, default 1024 rows): LU with partial
+        // pivoting and the explicit inverse on the GPU (cuSOLVER getrf / getrs; same pivot rule
+        // -- the first row of largest magnitude -- the sums in another order, O13)
+        const i64 dlu_min = std::getenv("MGM_DEVICE_LU_MIN") ? std::atoll(std::getenv("MGM_DEVICE_LU_MIN")) : 1024;
+        if (m >= dlu_min && cusolver().ok) {
+            i64 bad = -1;
+            if ((s = device_lu(ctx, A, m, m <= 4096, &bad))) return s;
+            tm.mark("coarse LU (device)", p - 1);
+            if (bad >= 0) return fail(ctx, MGM_ERR_SINGULAR, "singular coarsest operator", bad);
+            ctx->denseJ = dense_level(ctx);
+            if (ctx->denseJ < 0) {  // the cluster bottom takes host factors
+                LU.resize((size_t)m * m);
+                piv.resize(m);
+                CK(cudaMemcpy(LU.data(), ctx->lu, sizeof(double) * LU.size(), cudaMemcpyDeviceToHost));
+                CK(cudaMemcpy(piv.data(), ctx->piv, sizeof(i32) * m, cudaMemcpyDeviceToHost));
+                setup_bottom(ctx, LU, piv);
+            }
+        } else {
+            i64 bad = dense_lu_colmajor(A, m, LU, piv);
+            tm.mark("coarse LU", p - 1);
+            if (bad >= 0) return fail(ctx, MGM_ERR_SINGULAR, "singular coarsest operator", bad);
+            if ((s = upload(ctx, &ctx->lu, LU)) || (s = upload(ctx, &ctx->piv, piv))) return s;
+            CK(cudaStreamSynchronize(st));
+            ctx->denseJ = dense_level(ctx);
+            if (ctx->denseJ < 0) setup_bottom(ctx, LU, piv);  // (the dense bottom replaces it)
+            tm.mark("bottom kernel setup", p - 1);
+            if (m <= 4096) {  // explicit inverse for the batched coarse solve (same solution up to rounding, O13)
+                std::vector<double> Ainv;
+                dense_inverse(LU, piv, m, Ainv, nth);
+                if ((s = upload(ctx, &ctx->ainv, Ainv))) return s;
+                tm.mark("coarse inverse", p - 1);
+            }
         }
         cudaGetLastError();
     }

@@ -1020,3 +1020,35 @@ def test_solve_batch_matches_oracle():
         assert reps[k].converged and rr.converged
         assert abs(reps[k].iterations - rr.iterations) <= 1, (k, reps[k].iterations, rr.iterations)
         assert np.linalg.norm(xg[k] - xr) / np.linalg.norm(xr) <= 1e-9
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_device_coarse_lu(name, monkeypatch):
+    """The coarsest LU and explicit inverse on the GPU (cuSOLVER getrf / getrs, forced for
+    every size with MGM_DEVICE_LU_MIN=0; default: coarsest levels >= 1024 rows): the coarse
+    solve, the V-cycle and MGM-GMRES against the oracle's partial-pivoting LU (O13) --
+    1e-12 / +-1 iteration, 1e-9."""
+    import torch
+    from paper_2204_06154_b200 import MGM, mgm_apply
+
+    P = pair(name)
+    monkeypatch.setenv("MGM_DEVICE_LU_MIN", "0")
+    g = MGM(P.w.points, P.w.normals, P.w.stencil, P.w.levels)
+    pad = 1 if P.poisson else 0
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    jp = P.ref.p - 1
+    npd = P.ref.levels[jp].N + pad
+    r = _rand(npd, 97)
+    y = torch.empty(npd, dtype=torch.float64, device="cuda")
+    mgm_apply(g.ctx, jp, 5, dev(P.to_lib_order(jp, r)), None, y)
+    assert relmax(P.to_oracle_order(jp, y.cpu().numpy()), P.ref.coarse_solve(r)) <= 1e-12
+    n = len(P.w.points)
+    f, u0 = _rand(n, 95), _rand(n, 96)
+    uf = torch.from_numpy(u0.copy()).cuda()
+    g.vcycle(torch.from_numpy(f).cuda(), uf)
+    assert relmax(uf.cpu().numpy(), P.ref.vcycle(f, u0)) <= 1e-12
+    x, rep = g.solve(torch.from_numpy(P.w.rhs).cuda(), tol=1e-10)
+    xr, rr = P.ref.solve(P.w.rhs, tol=1e-10)
+    assert rep.converged and rr.converged and abs(rep.iterations - rr.iterations) <= 1
+    assert np.linalg.norm(x.cpu().numpy() - xr) / np.linalg.norm(xr) <= 1e-9
+    g.close()
