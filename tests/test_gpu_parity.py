@@ -1052,3 +1052,69 @@ def test_device_coarse_lu(name, monkeypatch):
     assert rep.converged and rr.converged and abs(rep.iterations - rr.iterations) <= 1
     assert np.linalg.norm(x.cpu().numpy() - xr) / np.linalg.norm(xr) <= 1e-9
     g.close()
+
+
+@pytest.mark.parametrize("method", ["rbffd", "gfd"])
+def test_full_size_cfg2_vs_oracle(method):
+    """BASELINE configs[1] at its FULL size (jittered sphere, N = 262,144, 7 levels; RBF-FD
+    l=3 n=30 with V(2,2), and the GFD variant l=2 n=20) in the launch configuration bench.py
+    times, against the oracle built from the same cloud: identical level sizes, nnz and colour
+    counts; the V-cycle from a random guess and from zero (the preconditioner) to 1e-12;
+    MGM-GMRES iterations +-1 and the solution to 1e-9."""
+    import torch
+    import oracle as O
+    from paper_2204_06154_b200 import MGM, mgm_level_info
+
+    w = MI.make_workload(2, method=method)
+    g = MGM(w.points, w.normals, w.stencil, w.levels)
+    ref = O.Oracle(w.points, w.normals, w.stencil, w.levels)
+    assert g.p == ref.p == 7
+    for j in range(g.p):
+        li = mgm_level_info(g.ctx, j)
+        assert li["n"] == ref.levels[j].N and li["nnz"] == ref.levels[j].L.nnz
+        if j + 1 < g.p:
+            assert li["colours"] == ref.levels[j].ncolours
+    n = len(w.points)
+    f, u0 = _rand(n, 31), _rand(n, 32)
+    uu = torch.from_numpy(u0.copy()).cuda()
+    g.vcycle(torch.from_numpy(f).cuda(), uu)
+    assert relmax(uu.cpu().numpy(), ref.vcycle(f, u0)) <= 1e-12
+    uz = torch.zeros(n, dtype=torch.float64, device="cuda")
+    g.vcycle(torch.from_numpy(f).cuda(), uz)
+    assert relmax(uz.cpu().numpy(), ref.vcycle(f, np.zeros(n))) <= 1e-12
+    x, rep = g.solve(torch.from_numpy(w.rhs).cuda(), tol=1e-10)
+    xr, rr = ref.solve(w.rhs, tol=1e-10)
+    assert rep.converged and rr.converged and abs(rep.iterations - rr.iterations) <= 1
+    assert np.linalg.norm(x.cpu().numpy() - xr) / np.linalg.norm(xr) <= 1e-9
+    g.close()
+
+
+def test_cfg4_poisson_65536_vs_oracle():
+    """BASELINE configs[3]'s recipe (quartic level set, pure Poisson with the bordered saddle
+    system P:300-355, RBF-FD l=4 r^7 n=50) at N = 65,536 -- the largest size at which the
+    method still converges in well under 100 GMRES iterations -- against the
+    oracle: level sizes, nnz and colours exact; the bordered V-cycle to 1e-12; MGM-GMRES
+    iterations +-1, solution (and multiplier) to 1e-9."""
+    import torch
+    import oracle as O
+    from paper_2204_06154_b200 import MGM, mgm_level_info
+
+    w = MI.make_workload(4, n=65536)
+    g = MGM(w.points, w.normals, w.stencil, w.levels)
+    ref = O.Oracle(w.points, w.normals, w.stencil, w.levels)
+    assert g.p == ref.p
+    for j in range(g.p):
+        li = mgm_level_info(g.ctx, j)
+        assert li["n"] == ref.levels[j].N and li["nnz"] == ref.levels[j].L.nnz
+        if j + 1 < g.p:
+            assert li["colours"] == ref.levels[j].ncolours
+    n = len(w.points)
+    f, u0 = _rand(n, 33), _rand(n, 34)
+    uu = torch.from_numpy(u0.copy()).cuda()
+    g.vcycle(torch.from_numpy(f).cuda(), uu)
+    assert relmax(uu.cpu().numpy(), ref.vcycle(f, u0)) <= 1e-12
+    x, rep = g.solve(torch.from_numpy(w.rhs).cuda(), tol=1e-10, maxit=300)
+    xr, rr = ref.solve(w.rhs, tol=1e-10, maxit=300)
+    assert rep.converged and rr.converged and abs(rep.iterations - rr.iterations) <= 1
+    assert np.linalg.norm(x.cpu().numpy() - xr) / np.linalg.norm(xr) <= 1e-9
+    g.close()
