@@ -422,6 +422,8 @@ struct mgm_ctx {
     int denseJ = -1;
     int dense_m = 0, dense_ld = 0;
     double* dB = nullptr;
+    double* d_dlt = nullptr;    // increments of the GMRES graph's last level-0 postsmooth (MODE 3)
+    double* dlt_out = nullptr;  // set while enqueueing that graph's V-cycle
     double* dP = nullptr;  // partial sums of the column-split multi-RHS dense apply [S][m][8]
     int bot_cluster = 16;
     size_t bot_smem = 0;
@@ -1795,6 +1797,8 @@ double sweep_colour_bytes(const Level& L, i64 rows) {
 
 // kernel variants by threads-per-row (chosen per level from the SELL width)
 constexpr int CHUNK = 16;
+// increments of the sweep being enqueued (enqueue_sweep with dlt; k_sell_spmv MODE 3)
+static thread_local double* g_dlt = nullptr;
 template <bool P, int TPR>
 void gs_launch_t(bool pdl, int r0, int r1, int span, const Level& L, cudaStream_t st, PfList pf, bool zg) {
     // block size: colours too small to give every SM a 256-thread block use smaller blocks
@@ -1803,10 +1807,10 @@ void gs_launch_t(bool pdl, int r0, int r1, int span, const Level& L, cudaStream_
     if (zg && !P)
         launch(pdl, k_gs_colour<false, TPR, CHUNK, true>, blocks_for((i64)span * TPR, bs), bs, 0, st, r0, r1,
                L.uniform_w, L.sptr, L.scol, L.sval, L.f, L.u, L.c, (int)L.n, pf, (const int*)L.slw,
-               (const uint8_t*)L.nlow);
+               (const uint8_t*)L.nlow, (double*)nullptr);
     else
         launch(pdl, k_gs_colour<P, TPR, CHUNK>, blocks_for((i64)span * TPR, bs), bs, 0, st, r0, r1, L.uniform_w, L.sptr,
-               L.scol, L.sval, L.f, L.u, L.c, (int)L.n, pf, (const int*)nullptr, (const uint8_t*)nullptr);
+               L.scol, L.sval, L.f, L.u, L.c, (int)L.n, pf, (const int*)nullptr, (const uint8_t*)nullptr, g_dlt);
 }
 // Threads one wave of colour kernels can hold (all SMs, register-limited occupancy).
 static i64 gs_wave_threads(int tpr, int block) {
@@ -1880,8 +1884,8 @@ template <int MODE, bool P, int TPR>
 void spmv_launch_t(bool pdl, i64 r0, i64 r1, i64 nl, const i64* sptr, const i32* scol, const double* sval,
                    const double* x, const double* f, double* y, const double* c, cudaStream_t st, PfList pf) {
     launch(pdl, k_sell_spmv<MODE, P, TPR, CHUNK>, blocks_for((r1 - (r0 & ~31)) * TPR, 256), 256, 0, st, (int)r0,
-           (int)r1, (int)nl, sptr, scol, sval, x, f, y, c, pf, MODE == 2 ? g_sluw : (const int*)nullptr,
-           MODE == 2 ? g_nlow : (const uint8_t*)nullptr, MODE != 0 ? g_yperm : (const int*)nullptr,
+           (int)r1, (int)nl, sptr, scol, sval, x, f, y, c, pf, MODE >= 2 ? g_sluw : (const int*)nullptr,
+           MODE >= 2 ? g_nlow : (const uint8_t*)nullptr, MODE != 0 ? g_yperm : (const int*)nullptr,
            MODE == 0 ? g_c0 : C0Fuse{nullptr, nullptr, nullptr, 0});
 }
 template <int MODE, bool P>
@@ -1899,6 +1903,8 @@ void launch_spmv(bool pdl, int mode, bool poisson, int tpr, i64 r0, i64 r1, i64 
     if (r1 <= r0) return;
     if (mode == 2) {  // residual after a zero-guess sweep (shifted problems)
         spmv_launch_p<2, false>(pdl, tpr, r0, r1, nl, sptr, scol, sval, x, f, y, c, st, pf);
+    } else if (mode == 3) {  // A u after a forward sweep that added x to u (shifted problems)
+        spmv_launch_p<3, false>(pdl, tpr, r0, r1, nl, sptr, scol, sval, x, f, y, c, st, pf);
     } else if (mode == 0) {
         if (poisson) spmv_launch_p<0, true>(pdl, tpr, r0, r1, nl, sptr, scol, sval, x, f, y, c, st, pf);
         else spmv_launch_p<0, false>(pdl, tpr, r0, r1, nl, sptr, scol, sval, x, f, y, c, st, pf);
@@ -2538,7 +2544,11 @@ void enqueue_vcycle(mgm_ctx* ctx, cudaStream_t st) {
     }
     enqueue_interp_correct(ctx, 0, lv[1].u, lv[0].u, st);                 // line 15
     stamp(ctx, "interp", 0, st);
-    for (int s = 0; s < nu2; ++s) enqueue_sweep(ctx, 0, post_b, st);      // line 16
+    for (int s = 0; s < nu2; ++s) {                                       // line 16
+        g_dlt = (s + 1 == nu2) ? ctx->dlt_out : nullptr;  // the last sweep's increments (MODE 3 A z)
+        enqueue_sweep(ctx, 0, post_b, st);
+        g_dlt = nullptr;
+    }
     stamp(ctx, "postsmooth", 0, st);
 }
 
@@ -2819,6 +2829,12 @@ static mgm_status build_gmres_graph(mgm_ctx* ctx) {
         CK(cudaMallocHost((void**)&ctx->g_h, sizeof(double) * gmres_dev_doubles(ctx)));
         CK(cudaMallocHost((void**)&ctx->g_hi, sizeof(int) * 8));
     }
+    // w = A z from the last level-0 postsmooth's increments (below); its buffer is allocated
+    // before the capture
+    const Level& L0 = ctx->lv[0];
+    const bool mode3 = !ctx->poisson && !dist_on(ctx) && ctx->p >= 2 && ctx->lp.nu2 >= 1 && ctx->lp.smoother == 0 &&
+                       L0.sluw && L0.nlow && !ctx->no_zg && std::getenv("MGM_NO_MODE3") == nullptr;
+    if (mode3 && !ctx->d_dlt) CK(dalloc(&ctx->d_dlt, n));
     GmresDev G{ctx->g_i, ctx->g_d, m, ctx->g_hist_cap};
     double* V = ctx->V;
     double* w = ctx->w;
@@ -2848,10 +2864,22 @@ static mgm_status build_gmres_graph(mgm_ctx* ctx) {
     const bool zg = zg_capable(ctx);
     if (!zg) cudaMemsetAsync(ctx->lv[0].u, 0, sizeof(double) * n, st);
     ctx->vc_zero_guess = zg;
+    // w = A z from the last level-0 postsmooth's increments d: A z = V_k + (later-colour part
+    // of L_1) d (k_sell_spmv MODE 3) -- half the operator bytes of the plain SpMV
+    ctx->dlt_out = mode3 ? ctx->d_dlt : nullptr;
     enqueue_vcycle(ctx, st);                                              // u = M V_k
+    ctx->dlt_out = nullptr;
     ctx->vc_zero_guess = false;
     ctx->pdl = true;
-    enqueue_apply_A(ctx, ctx->lv[0].u, w, st);                            // w = A M V_k
+    if (mode3) {                                                          // w = A M V_k
+        g_sluw = L0.sluw;
+        g_nlow = L0.nlow;
+        launch_spmv(true, 3, false, L0.stpr, 0, L0.n, L0.n, L0.sptr, L0.scol, L0.sval, ctx->d_dlt, L0.f, w, L0.c, st);
+        g_sluw = nullptr;
+        g_nlow = nullptr;
+    } else {
+        enqueue_apply_A(ctx, ctx->lv[0].u, w, st);
+    }
     ctx->pdl = false;
     // CGS2: h1 = V^T w; w -= V h1; h2 = V^T w (h1 += h2); w -= V h2, ||w||^2
     launch(true, k_multidot_fin, RED_BLOCKS, RED_THREADS, 0, st, n, (const double*)V, ld, 0, (const double*)w,
@@ -4481,6 +4509,7 @@ mgm_status mgm_destroy(mgm_ctx* ctx) {
     if (ctx->bhh) cudaFreeHost(ctx->bhh);
     if (ctx->ainv) dev_free(ctx->ainv);
     if (ctx->dB) dev_free(ctx->dB);
+    if (ctx->d_dlt) dev_free(ctx->d_dlt);
     if (ctx->dP) dev_free(ctx->dP);
     for (auto& T : ctx->timer)
         for (auto e : T.ev) cudaEventDestroy(e);

@@ -123,7 +123,8 @@ __global__ void __launch_bounds__(256) k_gs_colour(int r0, int r1, int Wu, const
                                                    const double* __restrict__ sval,
                                                    const double* __restrict__ f, double* u,
                                                    const double* __restrict__ c, int n, PfList pf,
-                                                   const int* __restrict__ slw, const uint8_t* __restrict__ nlow) {
+                                                   const int* __restrict__ slw, const uint8_t* __restrict__ nlow,
+                                                   double* __restrict__ dlt) {
     pdl_trigger();
     if (!pf.late) l2_prefetch_share(pf);
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
@@ -180,7 +181,9 @@ __global__ void __launch_bounds__(256) k_gs_colour(int r0, int r1, int Wu, const
     if (live && part == 0) {
         double res = fr_v - acc;
         if (POISSON) res -= cl;
-        u[r] = ur + res / d;
+        const double dl = res / d;
+        u[r] = ur + dl;
+        if (dlt) dlt[r] = dl;  // the sweep's increment (the residual identity of k_sell_spmv MODE 3)
     }
 }
 
@@ -192,6 +195,10 @@ __global__ void __launch_bounds__(256) k_gs_colour(int r0, int r1, int Wu, const
 // later] rows (from sluw[slice] = 1 + the slice's smallest earlier count, masked below
 // 1 + nlow[r]); equal to f - L u up to rounding.  Poisson: border term
 // c_i * x[nl] (nl = the level's row count; the multiplier sits after the rows).
+// MODE 3: A u right after a forward Gauss-Seidel sweep that added the increments d = x to u:
+// the sweep left every row's residual zero when it updated the row (with the earlier colours'
+// new and the later colours' old values), so (A u)_i = f_i + sum_{later colours} a_ij d_j --
+// the later-colour slots only, as MODE 2 (equal to A u up to rounding).
 // Restriction fused with colour 0 of the next level's presmooth from zero (MODE 0): for the
 // coarse rows r < c0_end (lib order: colour 0 first) also u[r] = f[r] / a_rr -- exactly what
 // the zero-guess colour kernel computes for colour 0 (no earlier colours to gather).
@@ -228,7 +235,7 @@ __global__ void __launch_bounds__(256) k_sell_spmv(int r0, int r1, int nl, const
         const int64_t s0 = sptr[r >> 5];
         w = (int)((sptr[(r >> 5) + 1] - s0) >> 5);
         base = s0 + (r & 31);
-        if (MODE == 2) {  // later-colour slots only: from the slice's first one, masked per row
+        if (MODE >= 2) {  // later-colour slots only: from the slice's first one, masked per row
             k1 = sluw[r >> 5] + part;
             lim = 1 + (int)nlow[r];
         }
@@ -236,7 +243,7 @@ __global__ void __launch_bounds__(256) k_sell_spmv(int r0, int r1, int nl, const
     } else {
         fr.load(sval, scol, 0, 0);
     }
-    if (MODE == 2) {
+    if (MODE >= 2) {
 #pragma unroll
         for (int q = 0; q < CH; ++q)
             if (k1 + q * TPR < lim) fr.c[q] = -1;
@@ -245,7 +252,7 @@ __global__ void __launch_bounds__(256) k_sell_spmv(int r0, int r1, int nl, const
     double acc = fr.dot(x, 0.0);
     for (int k0 = k1 + TPR * CH; k0 < w; k0 += TPR * CH) {
         fr.load(sval + base, scol + base, w, k0);
-        if (MODE == 2) {
+        if (MODE >= 2) {
 #pragma unroll
             for (int q = 0; q < CH; ++q)
                 if (k0 + q * TPR < lim) fr.c[q] = -1;
@@ -255,7 +262,7 @@ __global__ void __launch_bounds__(256) k_sell_spmv(int r0, int r1, int nl, const
     acc = group_sum<TPR>(acc);
     if (live && part == 0) {
         if (POISSON) acc += c[r] * x[nl];
-        y[yr] = (MODE == 0) ? acc : (MODE == 1) ? f[r] - acc : -acc;
+        y[yr] = (MODE == 0) ? acc : (MODE == 1) ? f[r] - acc : (MODE == 2) ? -acc : f[r] + acc;
         if (MODE == 0 && c0.u && r < c0.c0_end) c0.u[r] = 0.0 + (acc - 0.0) / c0.sval[c0.sptr[r >> 5] + (r & 31)];
     }
 }

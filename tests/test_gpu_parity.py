@@ -1118,3 +1118,31 @@ def test_cfg4_poisson_65536_vs_oracle():
     assert rep.converged and rr.converged and abs(rep.iterations - rr.iterations) <= 1
     assert np.linalg.norm(x.cpu().numpy() - xr) / np.linalg.norm(xr) <= 1e-9
     g.close()
+
+
+@pytest.mark.parametrize("name", ["cfg1", "torus20000", "gfd9000"])
+def test_gmres_sweep_residual_identity(name, monkeypatch):
+    """Inside the device GMRES, w = A M v_k comes from the last level-0 postsmooth's
+    increments d (a forward sweep leaves each row's residual zero when it updates the row, so
+    A z = v_k + (later-colour part of L_1) d; k_sell_spmv MODE 3) instead of a full SpMV:
+    the same iteration count and residual history to rounding as with the plain SpMV
+    (MGM_NO_MODE3=1), and both within +-1 iteration / 1e-9 of the oracle."""
+    import torch
+    from paper_2204_06154_b200 import MGM
+
+    P = pair(name)
+    rhs = torch.from_numpy(P.w.rhs).cuda()
+    out = []
+    for plain in (False, True):
+        if plain:
+            monkeypatch.setenv("MGM_NO_MODE3", "1")
+        m = MGM(P.w.points, P.w.normals, P.w.stencil, P.w.levels)
+        x, rep = m.solve(rhs, tol=1e-10)
+        out.append((x.cpu().numpy(), rep))
+        m.close()
+    (x3, r3), (xp, rp) = out
+    assert r3.converged and rp.converged and r3.iterations == rp.iterations
+    assert np.allclose(r3.history, rp.history, rtol=0, atol=1e-12 * rp.history[0])
+    xr, rr = P.ref.solve(P.w.rhs, tol=1e-10)
+    assert abs(r3.iterations - rr.iterations) <= 1
+    assert np.linalg.norm(x3 - xr) / np.linalg.norm(xr) <= 1e-9
