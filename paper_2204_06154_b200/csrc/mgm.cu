@@ -424,6 +424,7 @@ struct mgm_ctx {
     double* dB = nullptr;
     double* d_dlt = nullptr;    // increments of the GMRES graph's last level-0 postsmooth (MODE 3)
     double* dlt_out = nullptr;  // set while enqueueing that graph's V-cycle
+    bool vgraph_dlt = false;    // the general V-cycle graph writes d_dlt (standalone residual)
     double* dP = nullptr;  // partial sums of the column-split multi-RHS dense apply [S][m][8]
     int bot_cluster = 16;
     size_t bot_smem = 0;
@@ -2555,11 +2556,25 @@ void enqueue_vcycle(mgm_ctx* ctx, cudaStream_t st) {
 bool timing_on(const mgm_ctx* ctx) { return ctx->timer[0].on || ctx->timer[1].on || ctx->timer[3].on; }
 
 bool zg_capable(const mgm_ctx* ctx);
+// The last level-0 postsmooth of the V-cycle writes its increments d (k_gs_colour dlt): after
+// that forward sweep the residual is f - A u = -(later-colour part of L_1) d (k_sell_spmv
+// MODE 2 on d) and A u = f + (later-colour part) d (MODE 3) -- equal up to rounding, about half
+// the operator bytes of a full SpMV.  Shifted, undistributed, forward postsmoothing only.
+bool mode3_ok(const mgm_ctx* ctx) {
+    const Level& L0 = ctx->lv[0];
+    return !ctx->poisson && !dist_on(ctx) && ctx->p >= 2 && ctx->lp.nu2 >= 1 && ctx->lp.smoother == 0 && L0.sluw &&
+           L0.nlow && !ctx->no_zg && std::getenv("MGM_NO_MODE3") == nullptr;
+}
 mgm_status build_graph(mgm_ctx* ctx, bool zero_guess = false) {
     cudaGraphExec_t& gx = zero_guess ? ctx->vgraph0 : ctx->vgraph;
     if (gx) return MGM_OK;
     ctx->vc_zero_guess = zero_guess && zg_capable(ctx);
-    struct ResetZ { mgm_ctx* c; ~ResetZ() { c->vc_zero_guess = false; } } resetz_{ctx};
+    struct ResetZ { mgm_ctx* c; ~ResetZ() { c->vc_zero_guess = false; c->dlt_out = nullptr; } } resetz_{ctx};
+    // the general V-cycle (standalone MGM) leaves the last postsmooth's increments in d_dlt
+    const bool dl = !zero_guess && mode3_ok(ctx);
+    if (dl && !ctx->d_dlt) CK(dalloc(&ctx->d_dlt, ctx->lv[0].n));
+    ctx->dlt_out = dl ? ctx->d_dlt : nullptr;
+    if (!zero_guess) ctx->vgraph_dlt = dl;
     cudaGraph_t g;
     CK(cudaStreamBeginCapture(ctx->st, cudaStreamCaptureModeThreadLocal));
     g_launch_err.clear();
@@ -2832,8 +2847,7 @@ static mgm_status build_gmres_graph(mgm_ctx* ctx) {
     // w = A z from the last level-0 postsmooth's increments (below); its buffer is allocated
     // before the capture
     const Level& L0 = ctx->lv[0];
-    const bool mode3 = !ctx->poisson && !dist_on(ctx) && ctx->p >= 2 && ctx->lp.nu2 >= 1 && ctx->lp.smoother == 0 &&
-                       L0.sluw && L0.nlow && !ctx->no_zg && std::getenv("MGM_NO_MODE3") == nullptr;
+    const bool mode3 = mode3_ok(ctx);
     if (mode3 && !ctx->d_dlt) CK(dalloc(&ctx->d_dlt, n));
     GmresDev G{ctx->g_i, ctx->g_d, m, ctx->g_hist_cap};
     double* V = ctx->V;
@@ -3481,11 +3495,23 @@ mgm_status standalone_lib(mgm_ctx* ctx, double tol, int maxit, mgm_report* rep, 
     int it = 0, hist_n = 0;
     double rel = 1.0;
     bool conv = false;
+    // the residual from the last postsmooth's increments when the V-cycle graph records them
+    const bool from_dlt = !timing_on(ctx) && mode3_ok(ctx);
     while (it < maxit) {
         if ((s = run_vcycle(ctx, st))) return s;
         ++it;
-        enqueue_apply_A(ctx, ctx->lv[0].u, ctx->w, st);
-        k_axpby<<<RED_BLOCKS, 256, 0, st>>>(n, 1.0, ctx->b, -1.0, ctx->w, ctx->w);
+        if (from_dlt && ctx->vgraph_dlt) {  // r = f - A u = -(later-colour part of L_1) d
+            const Level& L0 = ctx->lv[0];
+            g_sluw = L0.sluw;
+            g_nlow = L0.nlow;
+            launch_spmv(false, 2, false, L0.stpr, 0, L0.n, L0.n, L0.sptr, L0.scol, L0.sval, ctx->d_dlt, nullptr, ctx->w,
+                        L0.c, st);
+            g_sluw = nullptr;
+            g_nlow = nullptr;
+        } else {
+            enqueue_apply_A(ctx, ctx->lv[0].u, ctx->w, st);
+            k_axpby<<<RED_BLOCKS, 256, 0, st>>>(n, 1.0, ctx->b, -1.0, ctx->w, ctx->w);
+        }
         enqueue_dot(ctx, n, ctx->w, ctx->w, nr, st);
         CK(cudaMemcpyAsync(ctx->hh, nr, sizeof(double), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
