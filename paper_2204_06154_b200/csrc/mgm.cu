@@ -425,6 +425,8 @@ struct mgm_ctx {
     double* d_dlt = nullptr;    // increments of the GMRES graph's last level-0 postsmooth (MODE 3)
     double* dlt_out = nullptr;  // set while enqueueing that graph's V-cycle
     bool vgraph_dlt = false;    // the general V-cycle graph writes d_dlt (standalone residual)
+    bool vgraph0_dlt = false;   // ... and the zero-guess one (A M v)
+    bool last_vc_dlt = false;   // the last run_vcycle left its increments in d_dlt
     double* dP = nullptr;  // partial sums of the column-split multi-RHS dense apply [S][m][8]
     int bot_cluster = 16;
     size_t bot_smem = 0;
@@ -2570,11 +2572,12 @@ mgm_status build_graph(mgm_ctx* ctx, bool zero_guess = false) {
     if (gx) return MGM_OK;
     ctx->vc_zero_guess = zero_guess && zg_capable(ctx);
     struct ResetZ { mgm_ctx* c; ~ResetZ() { c->vc_zero_guess = false; c->dlt_out = nullptr; } } resetz_{ctx};
-    // the general V-cycle (standalone MGM) leaves the last postsmooth's increments in d_dlt
-    const bool dl = !zero_guess && mode3_ok(ctx);
+    // both V-cycle graphs leave the last postsmooth's increments in d_dlt (standalone residual;
+    // A M v in BiCGSTAB and the host-loop GMRES)
+    const bool dl = mode3_ok(ctx);
     if (dl && !ctx->d_dlt) CK(dalloc(&ctx->d_dlt, ctx->lv[0].n));
     ctx->dlt_out = dl ? ctx->d_dlt : nullptr;
-    if (!zero_guess) ctx->vgraph_dlt = dl;
+    (zero_guess ? ctx->vgraph0_dlt : ctx->vgraph_dlt) = dl;
     cudaGraph_t g;
     CK(cudaStreamBeginCapture(ctx->st, cudaStreamCaptureModeThreadLocal));
     g_launch_err.clear();
@@ -2600,6 +2603,7 @@ bool zg_capable(const mgm_ctx* ctx) {
 }
 mgm_status run_vcycle(mgm_ctx* ctx, cudaStream_t st, bool zero_guess = false) {
     zero_guess = zero_guess && zg_capable(ctx);
+    ctx->last_vc_dlt = false;
     if (timing_on(ctx) || (ctx->tp && !ctx->tp->capturable())) {  // eager: event timing / fake ranks
         ctx->vc_zero_guess = zero_guess;
         timer_begin(ctx, 2, st);
@@ -2613,7 +2617,25 @@ mgm_status run_vcycle(mgm_ctx* ctx, cudaStream_t st, bool zero_guess = false) {
     timer_begin(ctx, 2, st);
     CK(cudaGraphLaunch(zero_guess ? ctx->vgraph0 : ctx->vgraph, st));
     timer_end(ctx, 2, st, 0.0);
+    ctx->last_vc_dlt = zero_guess ? ctx->vgraph0_dlt : ctx->vgraph_dlt;
     return MGM_OK;
+}
+
+void enqueue_apply_A(mgm_ctx* ctx, const double* x, double* y, cudaStream_t st);
+// y = A u right after run_vcycle on lv[0] (u = lv[0].u): from the last postsmooth's increments
+// when the graph recorded them (A u = f + (later-colour part of L_1) d, k_sell_spmv MODE 3),
+// else the plain SpMV
+void enqueue_apply_A_after_vcycle(mgm_ctx* ctx, double* y, cudaStream_t st) {
+    if (!ctx->last_vc_dlt) {
+        enqueue_apply_A(ctx, ctx->lv[0].u, y, st);
+        return;
+    }
+    const Level& L0 = ctx->lv[0];
+    g_sluw = L0.sluw;
+    g_nlow = L0.nlow;
+    launch_spmv(false, 3, false, L0.stpr, 0, L0.n, L0.n, L0.sptr, L0.scol, L0.sval, ctx->d_dlt, L0.f, y, L0.c, st);
+    g_sluw = nullptr;
+    g_nlow = nullptr;
 }
 
 mgm_status ensure_krylov(mgm_ctx* ctx) {
@@ -2741,7 +2763,7 @@ mgm_status gmres_lib(mgm_ctx* ctx, double tol, int maxit, mgm_report* rep, cudaS
         bool stop = false;
         for (int k = 0; k < m; ++k) {
             if ((s = enqueue_precond(ctx, V + (i64)k * ld, st))) return s;
-            enqueue_apply_A(ctx, ctx->lv[0].u, w, st);
+            enqueue_apply_A_after_vcycle(ctx, w, st);
             ++its;
             const int k1 = k + 1;
             // CGS2: h = V^T w; w -= V h; h2 = V^T w; w -= V h2; h += h2
@@ -3075,7 +3097,7 @@ mgm_status bicgstab_lib(mgm_ctx* ctx, double tol, int maxit, mgm_report* rep, cu
             if ((s = enqueue_precond(ctx, p, st))) return s;  // p_hat = M p
             ++its;
             CK(cudaMemcpyAsync(ph, ctx->lv[0].u, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
-            enqueue_apply_A(ctx, ph, v, st);
+            enqueue_apply_A_after_vcycle(ctx, v, st);
             enqueue_dot(ctx, n, rh, v, dd, st);
             if ((s = fetch(1))) return s;
             alpha = rho / hh[0];
@@ -3092,7 +3114,7 @@ mgm_status bicgstab_lib(mgm_ctx* ctx, double tol, int maxit, mgm_report* rep, cu
             }
             if ((s = enqueue_precond(ctx, sv, st))) return s;  // s_hat = M s (in lv[0].u)
             ++its;
-            enqueue_apply_A(ctx, ctx->lv[0].u, t, st);
+            enqueue_apply_A_after_vcycle(ctx, t, st);
             enqueue_multidot(ctx, n, sv, ld, 2, t, dd, nullptr, st);  // (s, t), (t, t)
             if ((s = fetch(2))) return s;
             omega = hh[1] > 0.0 ? hh[0] / hh[1] : 0.0;
@@ -3500,7 +3522,7 @@ mgm_status standalone_lib(mgm_ctx* ctx, double tol, int maxit, mgm_report* rep, 
     while (it < maxit) {
         if ((s = run_vcycle(ctx, st))) return s;
         ++it;
-        if (from_dlt && ctx->vgraph_dlt) {  // r = f - A u = -(later-colour part of L_1) d
+        if (from_dlt && ctx->last_vc_dlt) {  // r = f - A u = -(later-colour part of L_1) d
             const Level& L0 = ctx->lv[0];
             g_sluw = L0.sluw;
             g_nlow = L0.nlow;
