@@ -424,6 +424,8 @@ struct mgm_ctx {
     double* dB = nullptr;
     double* d_dlt = nullptr;    // increments of the GMRES graph's last level-0 postsmooth (MODE 3)
     double* dlt_out = nullptr;  // set while enqueueing that graph's V-cycle
+    double* d_dlt_pre = nullptr;    // increments of the general V-cycle's last level-0 presmooth
+    double* dlt_pre_out = nullptr;  // set while enqueueing the general V-cycle graph
     bool vgraph_dlt = false;    // the general V-cycle graph writes d_dlt (standalone residual)
     bool vgraph0_dlt = false;   // ... and the zero-guess one (A M v)
     bool last_vc_dlt = false;   // the last run_vcycle left its increments in d_dlt
@@ -2456,9 +2458,17 @@ void enqueue_vcycle(mgm_ctx* ctx, cudaStream_t st) {
     if (!bottom_only) {
     // level 0 from a zero guess (preconditioner applications): the first sweep reads only
     // the diagonal and earlier-colour entries (k_gs_colour ZG)
-    for (int s = 0; s < nu1; ++s)  // line 4 (colour 0 from zero: done with the input copy, c0_fused_l0)
+    for (int s = 0; s < nu1; ++s) {  // line 4 (colour 0 from zero: done with the input copy, c0_fused_l0)
+        g_dlt = (s + 1 == nu1) ? ctx->dlt_pre_out : nullptr;  // the last presmooth's increments
         enqueue_sweep(ctx, 0, pre_b, st, s == 0 && ctx->vc_zero_guess, s == 0 && ctx->vc_zero_guess && c0_fused_l0(ctx));
+        g_dlt = nullptr;
+    }
     stamp(ctx, "presmooth", 0, st);
+    // after a forward presmooth with increments d: t = f - L u = -(later-colour part of L) d
+    // (MODE 2 on d, as after a zero-guess sweep where d = u)
+    const bool res_d = ctx->dlt_pre_out != nullptr;
+    const double* ures = res_d ? ctx->dlt_pre_out : lv[0].u;
+    const bool res_m2 = res_d || (ctx->vc_zero_guess && nu1 == 1);
     // residual in Morton order for the restriction's gathers (opt-in: cfg3 restrict L0 30.4 ->
     // 26.7 us but residual 80 -> 85 us; cfg5 solve 206.6 vs 205.2 ms without)
     const bool mt0 = !dist_level(ctx, 0) && lv[0].n >= ctx->morton_t_min;
@@ -2469,11 +2479,10 @@ void enqueue_vcycle(mgm_ctx* ctx, cudaStream_t st) {
                !ctx->no_c0_fuse;
     };
     if (fused_rr_ok(ctx, 0)) {                                           // lines 5 (+ 8's restriction)
-        enqueue_res_restrict(ctx, 0, lv[0].f, lv[0].u, lv[0].t, lv[1].f, st, ctx->vc_zero_guess && nu1 == 1, mt0,
-                             c0_fused(1));
+        enqueue_res_restrict(ctx, 0, lv[0].f, ures, lv[0].t, lv[1].f, st, res_m2, mt0, c0_fused(1));
         stamp(ctx, "residual+restrict", 0, st);
     } else {
-        enqueue_residual(ctx, 0, lv[0].f, lv[0].u, lv[0].t, st, ctx->vc_zero_guess && nu1 == 1, mt0);  // line 5
+        enqueue_residual(ctx, 0, lv[0].f, ures, lv[0].t, st, res_m2, mt0);  // line 5
         stamp(ctx, "residual", 0, st);
         enqueue_restrict(ctx, 0, lv[0].t, lv[1].f, st, mt0, c0_fused(1));
         stamp(ctx, "restrict", 0, st);
@@ -2571,13 +2580,27 @@ mgm_status build_graph(mgm_ctx* ctx, bool zero_guess = false) {
     cudaGraphExec_t& gx = zero_guess ? ctx->vgraph0 : ctx->vgraph;
     if (gx) return MGM_OK;
     ctx->vc_zero_guess = zero_guess && zg_capable(ctx);
-    struct ResetZ { mgm_ctx* c; ~ResetZ() { c->vc_zero_guess = false; c->dlt_out = nullptr; } } resetz_{ctx};
+    struct ResetZ {
+        mgm_ctx* c;
+        ~ResetZ() {
+            c->vc_zero_guess = false;
+            c->dlt_out = nullptr;
+            c->dlt_pre_out = nullptr;
+        }
+    } resetz_{ctx};
     // both V-cycle graphs leave the last postsmooth's increments in d_dlt (standalone residual;
     // A M v in BiCGSTAB and the host-loop GMRES)
     const bool dl = mode3_ok(ctx);
     if (dl && !ctx->d_dlt) CK(dalloc(&ctx->d_dlt, ctx->lv[0].n));
     ctx->dlt_out = dl ? ctx->d_dlt : nullptr;
     (zero_guess ? ctx->vgraph0_dlt : ctx->vgraph_dlt) = dl;
+    // the general V-cycle: the level-0 residual from the last presmooth's increments
+    const Level& L0 = ctx->lv[0];
+    const bool dpre = !zero_guess && !ctx->poisson && !dist_on(ctx) && ctx->p >= 2 && ctx->lp.nu1 >= 1 &&
+                      ctx->lp.smoother != 1 && L0.sluw && L0.nlow && !ctx->no_zg && L0.n >= ctx->upper_res_min &&
+                      std::getenv("MGM_NO_MODE3") == nullptr;
+    if (dpre && !ctx->d_dlt_pre) CK(dalloc(&ctx->d_dlt_pre, L0.n));
+    ctx->dlt_pre_out = dpre ? ctx->d_dlt_pre : nullptr;
     cudaGraph_t g;
     CK(cudaStreamBeginCapture(ctx->st, cudaStreamCaptureModeThreadLocal));
     g_launch_err.clear();
@@ -4558,6 +4581,7 @@ mgm_status mgm_destroy(mgm_ctx* ctx) {
     if (ctx->ainv) dev_free(ctx->ainv);
     if (ctx->dB) dev_free(ctx->dB);
     if (ctx->d_dlt) dev_free(ctx->d_dlt);
+    if (ctx->d_dlt_pre) dev_free(ctx->d_dlt_pre);
     if (ctx->dP) dev_free(ctx->dP);
     for (auto& T : ctx->timer)
         for (auto e : T.ev) cudaEventDestroy(e);
