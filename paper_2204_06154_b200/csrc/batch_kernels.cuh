@@ -277,4 +277,56 @@ __global__ void __launch_bounds__(RED_THREADS) k_bdot_fin(int64_t n, const doubl
     finish_partials(partials, K, ticket, out, nullptr);
 }
 
+// out[j K + k] = sum_r V_j[r][k] w[r][k] for j < k1 (V_j = V + j stride): every basis vector of
+// a batched CGS2 pass in ONE launch (w read once per group of G vectors instead of once per
+// vector).  Same block chunks, per-thread order, warp / block / last-block sums as
+// k_bdot_fin<K> on (V_j, w), so each output is bitwise that kernel's.  partials holds
+// gridDim.x * k1 * K doubles.
+template <int K, int G>
+__global__ void __launch_bounds__(RED_THREADS) k_bmultidot_fin(int64_t n, const double* __restrict__ V, int64_t stride,
+                                                               int k1, const double* __restrict__ w,
+                                                               double* __restrict__ partials, unsigned* ticket,
+                                                               double* out) {
+    __shared__ double red[RED_THREADS / 32][G * K];
+    const int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
+    const int64_t b0 = blockIdx.x * chunk, b1 = min(n, b0 + chunk);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nout = k1 * K;
+    for (int g = 0; g < k1; g += G) {
+        const int gn = min(G, k1 - g);
+        double s[G][K];
+#pragma unroll
+        for (int q = 0; q < G; ++q)
+#pragma unroll
+            for (int k = 0; k < K; ++k) s[q][k] = 0.0;
+        for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
+            double wr[K];
+#pragma unroll
+            for (int k = 0; k < K; ++k) wr[k] = w[i * K + k];
+#pragma unroll
+            for (int q = 0; q < G; ++q)
+                if (q < gn) {
+                    const double* a = V + (int64_t)(g + q) * stride + i * K;
+#pragma unroll
+                    for (int k = 0; k < K; ++k) s[q][k] = fma(a[k], wr[k], s[q][k]);
+                }
+        }
+#pragma unroll
+        for (int q = 0; q < G; ++q)
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                const double t = warp_sum(s[q][k]);
+                if (lane == 0) red[warp][q * K + k] = t;
+            }
+        __syncthreads();
+        if (threadIdx.x < gn * K) {
+            double t = 0.0;
+            for (int ww = 0; ww < RED_THREADS / 32; ++ww) t += red[ww][threadIdx.x];
+            partials[(int64_t)blockIdx.x * nout + g * K + threadIdx.x] = t;
+        }
+        __syncthreads();
+    }
+    finish_partials(partials, nout, ticket, out, nullptr);
+}
+
 }  // namespace mgm

@@ -423,6 +423,7 @@ struct mgm_ctx {
     int dense_m = 0, dense_ld = 0;
     double* dB = nullptr;
     double* d_dlt = nullptr;    // increments of the GMRES graph's last level-0 postsmooth (MODE 3)
+    double* bpart = nullptr;    // block partials of the batched multi-dot [RED_BLOCKS][(restart + 1) 8]
     double* dlt_out = nullptr;  // set while enqueueing that graph's V-cycle
     double* d_dlt_pre = nullptr;    // increments of the general V-cycle's last level-0 presmooth
     double* dlt_pre_out = nullptr;  // set while enqueueing the general V-cycle graph
@@ -3509,6 +3510,18 @@ static void enqueue_bdot(mgm_ctx* ctx, int K, i64 n, const double* a, const doub
         default: k_bdot_fin<8><<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, a, b, ctx->partials, ctx->tickets, out); break;
     }
 }
+// out[j K + k] = V_j[:, k] . w[:, k] for j < k1, one launch (k_bmultidot_fin; partials in bpart)
+static void enqueue_bmultidot(mgm_ctx* ctx, int K, i64 n, const double* V, i64 stride, int k1, const double* w,
+                              double* out, cudaStream_t st) {
+    switch (K) {
+        case 2: k_bmultidot_fin<2, 8><<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, V, stride, k1, w, ctx->bpart, ctx->tickets,
+                                                                           out); break;
+        case 4: k_bmultidot_fin<4, 4><<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, V, stride, k1, w, ctx->bpart, ctx->tickets,
+                                                                           out); break;
+        default: k_bmultidot_fin<8, 2><<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, V, stride, k1, w, ctx->bpart, ctx->tickets,
+                                                                            out); break;
+    }
+}
 static void enqueue_res_b(mgm_ctx* ctx, int K, cudaStream_t st) {  // bres = bf0 - L_1 bu0
     const Level& L = ctx->lv[0];
     switch (K) {
@@ -4133,10 +4146,11 @@ static mgm_status gmres_batch(mgm_ctx* ctx, int Kreal, double tol, int maxit, mg
     const int m = ctx->restart;
     const Level& L0 = ctx->lv[0];
     if (ctx->bgK < K) {
-        for (double** q : {&ctx->bV, &ctx->bw, &ctx->bx, &ctx->bb, &ctx->bdh})
+        for (double** q : {&ctx->bV, &ctx->bw, &ctx->bx, &ctx->bb, &ctx->bdh, &ctx->bpart})
             if (*q) { dev_free(*q); *q = nullptr; }
         if (ctx->bhh) { cudaFreeHost(ctx->bhh); ctx->bhh = nullptr; }
         CK(dalloc(&ctx->bV, (i64)(m + 1) * N * K));
+        CK(dalloc(&ctx->bpart, (i64)RED_BLOCKS * (m + 1) * K));
         CK(dalloc(&ctx->bw, N * K));
         CK(dalloc(&ctx->bx, N * K));
         CK(dalloc(&ctx->bb, N * K));
@@ -4210,9 +4224,9 @@ static mgm_status gmres_batch(mgm_ctx* ctx, int Kreal, double tol, int maxit, mg
             ++cycles_its;
             const int k1 = k + 1;
             // CGS2 per column: h1 = V^T w; w -= V h1; h2 = V^T w; w -= V h2; h = h1 + h2
-            for (int j = 0; j < k1; ++j) enqueue_bdot(ctx, K, N, V + (i64)j * nk, w, h1 + (i64)j * K, st);
+            enqueue_bmultidot(ctx, K, N, V, nk, k1, w, h1, st);
             launch(false, k_blincomb<K>, nb, 256, 0, st, N, k1, (const double*)V, nk, (const double*)h1, -1.0, 1, w);
-            for (int j = 0; j < k1; ++j) enqueue_bdot(ctx, K, N, V + (i64)j * nk, w, h2 + (i64)j * K, st);
+            enqueue_bmultidot(ctx, K, N, V, nk, k1, w, h2, st);
             launch(false, k_blincomb<K>, nb, 256, 0, st, N, k1, (const double*)V, nk, (const double*)h2, -1.0, 1, w);
             enqueue_bdot(ctx, K, N, w, w, nr, st);
             CK(cudaMemcpyAsync(hh, h1, sizeof(double) * k1 * K, cudaMemcpyDeviceToHost, st));
@@ -4581,6 +4595,7 @@ mgm_status mgm_destroy(mgm_ctx* ctx) {
     if (ctx->ainv) dev_free(ctx->ainv);
     if (ctx->dB) dev_free(ctx->dB);
     if (ctx->d_dlt) dev_free(ctx->d_dlt);
+    if (ctx->bpart) dev_free(ctx->bpart);
     if (ctx->d_dlt_pre) dev_free(ctx->d_dlt_pre);
     if (ctx->dP) dev_free(ctx->dP);
     for (auto& T : ctx->timer)
