@@ -32,7 +32,8 @@ template <int TPR, int CH, int K, bool ZG = false>
 __global__ void __launch_bounds__(256) k_gs_colour_bs(int r0, int r1, int Wu, const int64_t* __restrict__ sptr,
                                                       const int* __restrict__ scol, const double* __restrict__ sval,
                                                       const double* __restrict__ f, double* u,
-                                                      const int* __restrict__ slw, const uint8_t* __restrict__ nlow) {
+                                                      const int* __restrict__ slw, const uint8_t* __restrict__ nlow,
+                                                      double* __restrict__ dlt) {
     constexpr int KS = K / 2;
     pdl_trigger();
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
@@ -90,9 +91,14 @@ __global__ void __launch_bounds__(256) k_gs_colour_bs(int r0, int r1, int Wu, co
     a0 = part_sum<TPR, KS>(a0);
     a1 = part_sum<TPR, KS>(a1);
     if (live && part == 0)
-        reinterpret_cast<double2*>(u)[(int64_t)r * KS + kk] = make_double2(uv.x + (fv.x - a0) / d, uv.y + (fv.y - a1) / d);
+    {
+        const double d0 = (fv.x - a0) / d, d1 = (fv.y - a1) / d;
+        reinterpret_cast<double2*>(u)[(int64_t)r * KS + kk] = make_double2(uv.x + d0, uv.y + d1);
+        if (dlt) reinterpret_cast<double2*>(dlt)[(int64_t)r * KS + kk] = make_double2(d0, d1);  // increments (MODE 3)
+    }
 }
-// MODE 0: y = A x; MODE 1: y = f - A x; MODE 2: y = -(later-colour part of A) x, the residual
+// MODE 0: y = A x; MODE 1: y = f - A x; MODE 3: y = f + (later-colour part of A) x (A u after
+// a forward sweep that added x to u); MODE 2: y = -(later-colour part of A) x, the residual
 // right after a forward sweep from a zero guess (k_sell_spmv MODE 2: from the slice's first
 // later-colour slot sluw, masked below the row's own 1 + nlow).  yperm: output row of each
 // input row (the residual written in Morton order for the restriction's Morton columns).
@@ -116,7 +122,7 @@ __global__ void __launch_bounds__(256) k_sell_spmv_bs(int r0, int r1, const int6
         const int64_t s0 = sptr[r >> 5];
         w = (int)((sptr[(r >> 5) + 1] - s0) >> 5);
         base = s0 + (r & 31);
-        if (MODE == 2) {
+        if (MODE >= 2) {
             k1 = sluw[r >> 5] + part;
             lim = 1 + (int)nlow[r];
         }
@@ -124,7 +130,7 @@ __global__ void __launch_bounds__(256) k_sell_spmv_bs(int r0, int r1, const int6
     } else {
         fr.load(sval, scol, 0, 0);
     }
-    if (MODE == 2) {
+    if (MODE >= 2) {
 #pragma unroll
         for (int q = 0; q < CH; ++q)
             if (k1 + q * TPR < lim) fr.c[q] = -1;
@@ -135,7 +141,7 @@ __global__ void __launch_bounds__(256) k_sell_spmv_bs(int r0, int r1, const int6
     for (int k0 = k1;; k0 += TPR * CH) {
         if (k0 != k1) {
             fr.load(sval + base, scol + base, w, k0);
-            if (MODE == 2) {
+            if (MODE >= 2) {
 #pragma unroll
                 for (int q = 0; q < CH; ++q)
                     if (k0 + q * TPR < lim) fr.c[q] = -1;
@@ -159,6 +165,9 @@ __global__ void __launch_bounds__(256) k_sell_spmv_bs(int r0, int r1, const int6
             o = make_double2(fv.x - a0, fv.y - a1);
         } else if (MODE == 2) {
             o = make_double2(-a0, -a1);
+        } else if (MODE == 3) {  // A u after a forward sweep that added x to u (k_sell_spmv MODE 3)
+            const double2 fv = reinterpret_cast<const double2*>(f)[(int64_t)r * KS + kk];
+            o = make_double2(fv.x + a0, fv.y + a1);
         }
         reinterpret_cast<double2*>(y)[(int64_t)yr * KS + kk] = o;
     }

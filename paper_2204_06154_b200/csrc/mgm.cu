@@ -424,6 +424,10 @@ struct mgm_ctx {
     double* dB = nullptr;
     double* d_dlt = nullptr;    // increments of the GMRES graph's last level-0 postsmooth (MODE 3)
     double* bpart = nullptr;    // block partials of the batched multi-dot [RED_BLOCKS][(restart + 1) 8]
+    double* bdlt = nullptr;     // K-wide increments of the batched zero-guess graph's last postsmooth
+    int bdlt_k = 0;
+    double* bdlt_out = nullptr;  // set while capturing that graph
+    bool bgraph_zg_dlt[9] = {};
     double* dlt_out = nullptr;  // set while enqueueing that graph's V-cycle
     double* d_dlt_pre = nullptr;    // increments of the general V-cycle's last level-0 presmooth
     double* dlt_pre_out = nullptr;  // set while enqueueing the general V-cycle graph
@@ -3211,6 +3215,8 @@ static i64 gs_wave_threads_bs(int tpr, int block) {
 // K = 4 every level gains.  MGM_BATCH_CH8=0/1 forces either.
 static int g_batch_ch8_env = std::getenv("MGM_BATCH_CH8") ? std::atoi(std::getenv("MGM_BATCH_CH8")) : -1;
 static bool batch_ch8(int K, i64 n) { return g_batch_ch8_env >= 0 ? g_batch_ch8_env != 0 : (K == 4 || n >= 131072); }
+// increments of the batched sweep being enqueued (the batched GMRES's A z, MODE 3)
+static thread_local double* g_bdlt = nullptr;
 // K right-hand sides (K even): TPR * K/2 threads per row (batch_kernels.cuh)
 template <int K>
 static void b_gs(mgm_ctx* ctx, const Level& L, int j, int r0, int r1, cudaStream_t st, bool zg = false) {
@@ -3219,7 +3225,7 @@ static void b_gs(mgm_ctx* ctx, const Level& L, int j, int r0, int r1, cudaStream
     auto go = [&](auto kern, int t) {
         launch(true, kern, blocks_for((i64)span * t * (K / 2), bs), bs, 0, st, r0, r1, L.uniform_w,
                (const i64*)L.sptr, (const i32*)L.scol, (const double*)L.sval, (const double*)ctx->bf[j], ctx->bu[j],
-               (const i32*)L.slw, (const uint8_t*)L.nlow);
+               (const i32*)L.slw, (const uint8_t*)L.nlow, zg ? (double*)nullptr : g_bdlt);
     };
     // a colour just above one (register-limited) wave: halve the threads per row (cf. launch_gs)
     int t = std::min(L.tpr, std::min(g_batch_tpr_cap, 64 / K));
@@ -3339,7 +3345,11 @@ static void enqueue_vcycle_b(mgm_ctx* ctx, cudaStream_t st, bool zero0) {
     for (int j = D - 1; j >= 0; --j) {                                              // lines 11-16
         const Level& L = lv[j];
         b_interp<K>(L, ctx->bu[j + 1], ctx->bu[j], st);
-        for (int s = 0; s < nu2; ++s) sweep(j, post_b);
+        for (int s = 0; s < nu2; ++s) {
+            g_bdlt = (j == 0 && s + 1 == nu2) ? ctx->bdlt_out : nullptr;  // last level-0 postsmooth: increments
+            sweep(j, post_b);
+            g_bdlt = nullptr;
+        }
         stamp(ctx, "interp+postsmooth", j, st);
     }
 }
@@ -3486,6 +3496,17 @@ static mgm_status ensure_batch(mgm_ctx* ctx, int K) {
 static mgm_status run_vcycle_b(mgm_ctx* ctx, int K, cudaStream_t st, bool zero0 = false) {
     cudaGraphExec_t& gx = zero0 ? ctx->bgraph_zg[K] : ctx->bgraph[K];
     if (!gx) {
+        // the zero-guess graph (batched GMRES) leaves its last postsmooth's increments in bdlt
+        const bool dl = zero0 && mode3_ok(ctx);
+        if (dl && ctx->bdlt_k < K) {
+            if (ctx->bdlt) dev_free(ctx->bdlt);
+            ctx->bdlt = nullptr;
+            CK(dalloc(&ctx->bdlt, ctx->N * K));
+            ctx->bdlt_k = K;
+        }
+        ctx->bdlt_out = dl ? ctx->bdlt : nullptr;
+        ctx->bgraph_zg_dlt[K] = dl;
+        struct ResetB { mgm_ctx* c; ~ResetB() { c->bdlt_out = nullptr; } } resetb_{ctx};
         cudaGraph_t g;
         CK(cudaStreamBeginCapture(ctx->st, cudaStreamCaptureModeThreadLocal));
         g_launch_err.clear();
@@ -4220,7 +4241,10 @@ static mgm_status gmres_batch(mgm_ctx* ctx, int Kreal, double tol, int maxit, mg
             // z = M^{-1} v_k (batched V-cycle from zero), w = A z
             CK(cudaMemcpyAsync(ctx->bf[0], V + (i64)k * nk, sizeof(double) * nk, cudaMemcpyDeviceToDevice, st));
             if ((s = run_vcycle_b(ctx, K, st, true))) return s;
-            b_spmv<0, K>(L0.stpr, N, L0.sptr, L0.scol, L0.sval, ctx->bu[0], nullptr, w, st);
+            if (ctx->bgraph_zg_dlt[K])  // A z = v_k + (later-colour part of L_1) d (MODE 3)
+                b_spmv<3, K>(L0.stpr, N, L0.sptr, L0.scol, L0.sval, ctx->bdlt, ctx->bf[0], w, st, L0.sluw, L0.nlow);
+            else
+                b_spmv<0, K>(L0.stpr, N, L0.sptr, L0.scol, L0.sval, ctx->bu[0], nullptr, w, st);
             ++cycles_its;
             const int k1 = k + 1;
             // CGS2 per column: h1 = V^T w; w -= V h1; h2 = V^T w; w -= V h2; h = h1 + h2
@@ -4596,6 +4620,7 @@ mgm_status mgm_destroy(mgm_ctx* ctx) {
     if (ctx->dB) dev_free(ctx->dB);
     if (ctx->d_dlt) dev_free(ctx->d_dlt);
     if (ctx->bpart) dev_free(ctx->bpart);
+    if (ctx->bdlt) dev_free(ctx->bdlt);
     if (ctx->d_dlt_pre) dev_free(ctx->d_dlt_pre);
     if (ctx->dP) dev_free(ctx->dP);
     for (auto& T : ctx->timer)
