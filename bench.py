@@ -195,12 +195,21 @@ def stage_breakdown(w, f, hbm):
     def sweep_b(j, nsw):
         return nsw * (12.0 * lv[j]["nnz"] + 24.0 * lv[j]["n"])
 
+    # level 0 of the traced (general) V-cycle: the last presmooth and postsmooth write their
+    # increments d (8 B/row each) and the residual reads the later-colour entries only, from d
+    # (libmgm dpre_ok / mode3_ok: shifted problem, forward sweeps, level >= 131072 rows)
+    smoother = w.levels.get("smoother", 0)
+    d0 = (os.environ.get("MGM_NO_MODE3") is None and w.stencil.get("problem", 0) == 0 and smoother == 0
+          and lv[0]["nnz_zg"] < lv[0]["nnz"] and lv[0]["n"] >= 131072 and len(lv) > 1)
+
     def bytes_of(lab):
         name, jl = lab.rsplit(" L", 1)
         j = int(jl)
         if name == "presmooth":
-            return sweep_b(j, nu1)
+            return sweep_b(j, nu1) + (8.0 * lv[j]["n"] if d0 and j == 0 else 0.0)
         if name == "residual":  # reads L, u, f; writes t (12 z + 24 N)
+            if d0 and j == 0:  # later-colour entries only, from the presmooth's increments
+                return 12.0 * (lv[j]["nnz"] - lv[j]["nnz_zg"]) + 24.0 * lv[j]["n"]
             return 12.0 * lv[j]["nnz"] + 24.0 * lv[j]["n"]
         if name == "restrict":
             return 12.0 * lv[j]["nnz_P"] + 8.0 * lv[j]["n"] + 8.0 * lv[j + 1]["n"]
@@ -210,9 +219,9 @@ def stage_breakdown(w, f, hbm):
             return 8.0 * lv[j]["n"] + sweep_b(j, nu1)
         if name == "residual+restrict":
             res = 12.0 * lv[j]["nnz"] + 24.0 * lv[j]["n"]
-            # after the zero-guess sweep (coarse levels always start from zero; the traced level 0
-            # does not: the graph is the V-cycle from the caller's u, MODE 1)
-            if j > 0 and lv[j]["nnz_zg"] < lv[j]["nnz"] and nu1 == 1 and lv[j]["n"] >= 131072:
+            # after the zero-guess sweep (coarse levels always start from zero) or, on level 0 of
+            # the traced general V-cycle, from the presmooth's increments d (d0)
+            if (d0 and j == 0) or (j > 0 and lv[j]["nnz_zg"] < lv[j]["nnz"] and nu1 == 1 and lv[j]["n"] >= 131072):
                 res = 12.0 * (lv[j]["nnz"] - lv[j]["nnz_zg"]) + 24.0 * lv[j]["n"]
             return res + 12.0 * lv[j]["nnz_P"] + 8.0 * lv[j]["n"] + 8.0 * lv[j + 1]["n"]
         if name == "interp":
@@ -220,7 +229,7 @@ def stage_breakdown(w, f, hbm):
         if name == "interp+postsmooth":
             return 12.0 * lv[j]["nnz_P"] + 8.0 * lv[j + 1]["n"] + 16.0 * lv[j]["n"] + sweep_b(j, nu2)
         if name == "postsmooth":
-            return sweep_b(j, nu2)
+            return sweep_b(j, nu2) + (8.0 * lv[j]["n"] if d0 and j == 0 else 0.0)
         if name == "bottom":  # levels j..p-1: sweeps, residuals, transfers, dense coarse solve
             b = 0.0
             for q in range(j, len(lv) - 1):

@@ -2581,6 +2581,12 @@ bool mode3_ok(const mgm_ctx* ctx) {
     return !ctx->poisson && !dist_on(ctx) && ctx->p >= 2 && ctx->lp.nu2 >= 1 && ctx->lp.smoother == 0 && L0.sluw &&
            L0.nlow && !ctx->no_zg && std::getenv("MGM_NO_MODE3") == nullptr;
 }
+// the general V-cycle's level-0 residual from the last presmooth's increments (MODE 2 on d)
+bool dpre_ok(const mgm_ctx* ctx) {
+    const Level& L0 = ctx->lv[0];
+    return !ctx->poisson && !dist_on(ctx) && ctx->p >= 2 && ctx->lp.nu1 >= 1 && ctx->lp.smoother != 1 && L0.sluw &&
+           L0.nlow && !ctx->no_zg && L0.n >= ctx->upper_res_min && std::getenv("MGM_NO_MODE3") == nullptr;
+}
 mgm_status build_graph(mgm_ctx* ctx, bool zero_guess = false) {
     cudaGraphExec_t& gx = zero_guess ? ctx->vgraph0 : ctx->vgraph;
     if (gx) return MGM_OK;
@@ -2601,9 +2607,7 @@ mgm_status build_graph(mgm_ctx* ctx, bool zero_guess = false) {
     (zero_guess ? ctx->vgraph0_dlt : ctx->vgraph_dlt) = dl;
     // the general V-cycle: the level-0 residual from the last presmooth's increments
     const Level& L0 = ctx->lv[0];
-    const bool dpre = !zero_guess && !ctx->poisson && !dist_on(ctx) && ctx->p >= 2 && ctx->lp.nu1 >= 1 &&
-                      ctx->lp.smoother != 1 && L0.sluw && L0.nlow && !ctx->no_zg && L0.n >= ctx->upper_res_min &&
-                      std::getenv("MGM_NO_MODE3") == nullptr;
+    const bool dpre = !zero_guess && dpre_ok(ctx);
     if (dpre && !ctx->d_dlt_pre) CK(dalloc(&ctx->d_dlt_pre, L0.n));
     ctx->dlt_pre_out = dpre ? ctx->d_dlt_pre : nullptr;
     cudaGraph_t g;
@@ -4896,6 +4900,13 @@ mgm_status mgm_bytes_model(const mgm_ctx* ctx, double* vcycle_bytes, double* spm
         }
         B += 12.0 * z + 16.0 * n + 12.0 * q + 8.0 * nn + 16.0 * n + bp * n;  // residual + restrict (unfused)
         B += 12.0 * q + 8.0 * nn + 16.0 * n;                        // interp + correct
+        if (j == 0 && dpre_ok(ctx)) {  // the general V-cycle (mgm_vcycle): the residual from the presmooth's
+            double low = 0.0;          // increments d (written: +8 n), later-colour entries only
+            for (i64 v : L.lower_per_colour) low += (double)v;
+            B -= (12.0 * z + 16.0 * n) - (12.0 * (z - low) + 8.0 * n);
+            B += 8.0 * n;
+        }
+        if (j == 0 && mode3_ok(ctx)) B += 8.0 * n;  // the last postsmooth writes its increments
     }
     const double np = (double)ctx->nc;
     B += 8.0 * np * np + 16.0 * np;
