@@ -428,6 +428,7 @@ struct mgm_ctx {
     int bdlt_k = 0;
     double* bdlt_out = nullptr;  // set while capturing that graph
     bool bgraph_zg_dlt[9] = {};
+    bool bgraph_dlt[9] = {};
     double* dlt_out = nullptr;  // set while enqueueing that graph's V-cycle
     double* d_dlt_pre = nullptr;    // increments of the general V-cycle's last level-0 presmooth
     double* dlt_pre_out = nullptr;  // set while enqueueing the general V-cycle graph
@@ -3500,8 +3501,9 @@ static mgm_status ensure_batch(mgm_ctx* ctx, int K) {
 static mgm_status run_vcycle_b(mgm_ctx* ctx, int K, cudaStream_t st, bool zero0 = false) {
     cudaGraphExec_t& gx = zero0 ? ctx->bgraph_zg[K] : ctx->bgraph[K];
     if (!gx) {
-        // the zero-guess graph (batched GMRES) leaves its last postsmooth's increments in bdlt
-        const bool dl = zero0 && mode3_ok(ctx);
+        // both batched graphs leave their last postsmooth's increments in bdlt (the batched GMRES's
+        // A z, the batched standalone residual)
+        const bool dl = mode3_ok(ctx);
         if (dl && ctx->bdlt_k < K) {
             if (ctx->bdlt) dev_free(ctx->bdlt);
             ctx->bdlt = nullptr;
@@ -3509,7 +3511,7 @@ static mgm_status run_vcycle_b(mgm_ctx* ctx, int K, cudaStream_t st, bool zero0 
             ctx->bdlt_k = K;
         }
         ctx->bdlt_out = dl ? ctx->bdlt : nullptr;
-        ctx->bgraph_zg_dlt[K] = dl;
+        (zero0 ? ctx->bgraph_zg_dlt : ctx->bgraph_dlt)[K] = dl;
         struct ResetB { mgm_ctx* c; ~ResetB() { c->bdlt_out = nullptr; } } resetb_{ctx};
         cudaGraph_t g;
         CK(cudaStreamBeginCapture(ctx->st, cudaStreamCaptureModeThreadLocal));
@@ -3549,6 +3551,14 @@ static void enqueue_bmultidot(mgm_ctx* ctx, int K, i64 n, const double* V, i64 s
 }
 static void enqueue_res_b(mgm_ctx* ctx, int K, cudaStream_t st) {  // bres = bf0 - L_1 bu0
     const Level& L = ctx->lv[0];
+    if (ctx->bgraph_dlt[K]) {  // after the general batched V-cycle: -(later-colour part of L_1) d
+        switch (K) {
+            case 2: b_spmv<2, 2>(L.stpr, L.n, L.sptr, L.scol, L.sval, ctx->bdlt, nullptr, ctx->bres, st, L.sluw, L.nlow); break;
+            case 4: b_spmv<2, 4>(L.stpr, L.n, L.sptr, L.scol, L.sval, ctx->bdlt, nullptr, ctx->bres, st, L.sluw, L.nlow); break;
+            default: b_spmv<2, 8>(L.stpr, L.n, L.sptr, L.scol, L.sval, ctx->bdlt, nullptr, ctx->bres, st, L.sluw, L.nlow); break;
+        }
+        return;
+    }
     switch (K) {
         case 2: b_spmv<1, 2>(L.stpr, L.n, L.sptr, L.scol, L.sval, ctx->bu[0], ctx->bf[0], ctx->bres, st); break;
         case 4: b_spmv<1, 4>(L.stpr, L.n, L.sptr, L.scol, L.sval, ctx->bu[0], ctx->bf[0], ctx->bres, st); break;
