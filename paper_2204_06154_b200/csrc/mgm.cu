@@ -473,6 +473,7 @@ struct mgm_ctx {
     int restart = 50;
     i64 ld = 0;
     double* V = nullptr;
+    double* Z = nullptr;  // device GMRES: z_k = M v_k of the current restart cycle (restart x ld)
     double* w = nullptr;
     double* xs = nullptr;    // solution accumulator (lib order)
     double* b = nullptr;     // rhs (lib order)
@@ -2887,6 +2888,8 @@ static bool gmres_dev_ok(const mgm_ctx* ctx) {
     return !ctx->poisson && !dist_on(ctx) && !timing_on(ctx) && ctx->restart <= 128 && ctx->p >= 1 &&
            std::getenv("MGM_HOST_GMRES") == nullptr;
 }
+// device GMRES keeps Z = M V (MGM_GMRES_NO_Z=1: x += M (V y) at the end of a restart cycle)
+static bool gmres_keep_z() { return std::getenv("MGM_GMRES_NO_Z") == nullptr; }
 static mgm_status build_gmres_graph(mgm_ctx* ctx) {
     if (ctx->ggraph) return MGM_OK;
     const i64 n = ctx->N;
@@ -2904,6 +2907,7 @@ static mgm_status build_gmres_graph(mgm_ctx* ctx) {
     const Level& L0 = ctx->lv[0];
     const bool mode3 = mode3_ok(ctx);
     if (mode3 && !ctx->d_dlt) CK(dalloc(&ctx->d_dlt, n));
+    if (gmres_keep_z() && !ctx->Z) CK(dalloc(&ctx->Z, (i64)m * ctx->ld));
     GmresDev G{ctx->g_i, ctx->g_d, m, ctx->g_hist_cap};
     double* V = ctx->V;
     double* w = ctx->w;
@@ -2940,6 +2944,8 @@ static mgm_status build_gmres_graph(mgm_ctx* ctx) {
     ctx->dlt_out = nullptr;
     ctx->vc_zero_guess = false;
     ctx->pdl = true;
+    if (ctx->Z)                                                           // Z_k = M V_k
+        launch(true, k_store_col, RED_BLOCKS, 256, 0, st, n, (const double*)ctx->lv[0].u, ctx->Z, ld, kdev);
     if (mode3) {                                                          // w = A M V_k
         g_sluw = L0.sluw;
         g_nlow = L0.nlow;
@@ -3047,9 +3053,14 @@ mgm_status gmres_dev(mgm_ctx* ctx, double tol, int maxit, mgm_report* rep, cudaS
             y[i] = sacc / Hh[(size_t)i * m + i];
         }
         CK(cudaMemcpyAsync(h1, y.data(), sizeof(double) * kdone, cudaMemcpyHostToDevice, st));
-        k_lincomb<<<RED_BLOCKS * 2, 256, 0, st>>>(n, V, ld, kdone, h1, w);
-        if ((s = enqueue_precond(ctx, w, st))) return s;
-        k_axpby<<<RED_BLOCKS, 256, 0, st>>>(n, 1.0, ctx->xs, 1.0, ctx->lv[0].u, ctx->xs);
+        if (ctx->Z) {  // x += Z y (z_j = M v_j kept by the graph)
+            k_lincomb<<<RED_BLOCKS * 2, 256, 0, st>>>(n, ctx->Z, ld, kdone, h1, w);
+            k_axpby<<<RED_BLOCKS, 256, 0, st>>>(n, 1.0, ctx->xs, 1.0, w, ctx->xs);
+        } else {       // x += M (V y)
+            k_lincomb<<<RED_BLOCKS * 2, 256, 0, st>>>(n, V, ld, kdone, h1, w);
+            if ((s = enqueue_precond(ctx, w, st))) return s;
+            k_axpby<<<RED_BLOCKS, 256, 0, st>>>(n, 1.0, ctx->xs, 1.0, ctx->lv[0].u, ctx->xs);
+        }
         if (stop == 1) {
             converged = std::fabs(gg[kdone]) / bnorm <= tol;
             break;
@@ -4633,6 +4644,7 @@ mgm_status mgm_destroy(mgm_ctx* ctx) {
     if (ctx->ainv) dev_free(ctx->ainv);
     if (ctx->dB) dev_free(ctx->dB);
     if (ctx->d_dlt) dev_free(ctx->d_dlt);
+    if (ctx->Z) dev_free(ctx->Z);
     if (ctx->bpart) dev_free(ctx->bpart);
     if (ctx->bdlt) dev_free(ctx->bdlt);
     if (ctx->d_dlt_pre) dev_free(ctx->d_dlt_pre);

@@ -711,6 +711,15 @@ __global__ void k_scale_col(int64_t n, const double* __restrict__ w, const doubl
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         dst[i] = w[i] * inv;
 }
+// Z[:, k] = z (k = *kdev): the device GMRES keeps z_k = M v_k, so the restart-cycle update is
+// x += Z y instead of x += M (V y) (M is linear: one V-cycle less per restart cycle)
+__global__ void k_store_col(int64_t n, const double* __restrict__ z, double* Z, int64_t ld, const int* __restrict__ kdev) {
+    pdl_trigger();
+    pdl_wait();
+    double* dst = Z + (int64_t)(*kdev) * ld;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = z[i];
+}
 // One Givens step of the Hessenberg least-squares problem (same operations as gmres_lib's
 // host loop), the relative residual history, and the loop condition.
 __global__ void k_gmres_givens(GmresDev G, const double* __restrict__ h, const double* __restrict__ nrm2,
