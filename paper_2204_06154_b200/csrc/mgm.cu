@@ -2748,10 +2748,13 @@ mgm_status enqueue_precond(mgm_ctx* ctx, const double* v, cudaStream_t st) {
 
 // Right-preconditioned GMRES(restart) with CGS2 orthogonalisation (equal to MGS in exact
 // arithmetic; O15), Givens rotations on the host.  b, x in lib order (x = 0 on entry).
+// GMRES keeps Z = M V (MGM_GMRES_NO_Z=1: x += M (V y) at the end of a restart cycle)
+static bool gmres_keep_z() { return std::getenv("MGM_GMRES_NO_Z") == nullptr; }
 mgm_status gmres_lib(mgm_ctx* ctx, double tol, int maxit, mgm_report* rep, cudaStream_t st) {
     const i64 n = vec_rows(ctx);
     const int m = ctx->restart;
     const i64 ld = ctx->ld;
+    if (gmres_keep_z() && !ctx->Z) CK(dalloc(&ctx->Z, (i64)m * ld));
     double* V = ctx->V;
     double* w = ctx->w;
     double* h1 = ctx->dh;
@@ -2797,6 +2800,8 @@ mgm_status gmres_lib(mgm_ctx* ctx, double tol, int maxit, mgm_report* rep, cudaS
         bool stop = false;
         for (int k = 0; k < m; ++k) {
             if ((s = enqueue_precond(ctx, V + (i64)k * ld, st))) return s;
+            if (ctx->Z)  // z_k = M v_k (x += Z y at the end of the cycle)
+                CK(cudaMemcpyAsync(ctx->Z + (i64)k * ld, ctx->lv[0].u, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
             enqueue_apply_A_after_vcycle(ctx, w, st);
             ++its;
             const int k1 = k + 1;
@@ -2848,9 +2853,14 @@ mgm_status gmres_lib(mgm_ctx* ctx, double tol, int maxit, mgm_report* rep, cudaS
             y[i] = sacc / H[(size_t)i * m + i];
         }
         CK(cudaMemcpyAsync(h1, y.data(), sizeof(double) * kdone, cudaMemcpyHostToDevice, st));
-        k_lincomb<<<RED_BLOCKS * 2, 256, 0, st>>>(n, V, ld, kdone, h1, w);
-        if ((s = enqueue_precond(ctx, w, st))) return s;
-        k_axpby<<<RED_BLOCKS, 256, 0, st>>>(n, 1.0, ctx->xs, 1.0, ctx->lv[0].u, ctx->xs);
+        if (ctx->Z) {  // x += Z y
+            k_lincomb<<<RED_BLOCKS * 2, 256, 0, st>>>(n, ctx->Z, ld, kdone, h1, w);
+            k_axpby<<<RED_BLOCKS, 256, 0, st>>>(n, 1.0, ctx->xs, 1.0, w, ctx->xs);
+        } else {       // x += M (V y)
+            k_lincomb<<<RED_BLOCKS * 2, 256, 0, st>>>(n, V, ld, kdone, h1, w);
+            if ((s = enqueue_precond(ctx, w, st))) return s;
+            k_axpby<<<RED_BLOCKS, 256, 0, st>>>(n, 1.0, ctx->xs, 1.0, ctx->lv[0].u, ctx->xs);
+        }
         if (stop) {
             converged = std::fabs(g[kdone]) / bnorm <= tol;
             break;
@@ -2888,8 +2898,6 @@ static bool gmres_dev_ok(const mgm_ctx* ctx) {
     return !ctx->poisson && !dist_on(ctx) && !timing_on(ctx) && ctx->restart <= 128 && ctx->p >= 1 &&
            std::getenv("MGM_HOST_GMRES") == nullptr;
 }
-// device GMRES keeps Z = M V (MGM_GMRES_NO_Z=1: x += M (V y) at the end of a restart cycle)
-static bool gmres_keep_z() { return std::getenv("MGM_GMRES_NO_Z") == nullptr; }
 static mgm_status build_gmres_graph(mgm_ctx* ctx) {
     if (ctx->ggraph) return MGM_OK;
     const i64 n = ctx->N;
