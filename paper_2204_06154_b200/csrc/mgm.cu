@@ -474,6 +474,7 @@ struct mgm_ctx {
     i64 ld = 0;
     double* V = nullptr;
     double* Z = nullptr;  // device GMRES: z_k = M v_k of the current restart cycle (restart x ld)
+    double* bZ = nullptr;  // batched GMRES: the same, K-wide (restart x N x K)
     double* w = nullptr;
     double* xs = nullptr;    // solution accumulator (lib order)
     double* b = nullptr;     // rhs (lib order)
@@ -4200,10 +4201,11 @@ static mgm_status gmres_batch(mgm_ctx* ctx, int Kreal, double tol, int maxit, mg
     const int m = ctx->restart;
     const Level& L0 = ctx->lv[0];
     if (ctx->bgK < K) {
-        for (double** q : {&ctx->bV, &ctx->bw, &ctx->bx, &ctx->bb, &ctx->bdh, &ctx->bpart})
+        for (double** q : {&ctx->bV, &ctx->bw, &ctx->bx, &ctx->bb, &ctx->bdh, &ctx->bpart, &ctx->bZ})
             if (*q) { dev_free(*q); *q = nullptr; }
         if (ctx->bhh) { cudaFreeHost(ctx->bhh); ctx->bhh = nullptr; }
         CK(dalloc(&ctx->bV, (i64)(m + 1) * N * K));
+        if (gmres_keep_z()) CK(dalloc(&ctx->bZ, (i64)m * N * K));
         CK(dalloc(&ctx->bpart, (i64)RED_BLOCKS * (m + 1) * K));
         CK(dalloc(&ctx->bw, N * K));
         CK(dalloc(&ctx->bx, N * K));
@@ -4274,6 +4276,8 @@ static mgm_status gmres_batch(mgm_ctx* ctx, int Kreal, double tol, int maxit, mg
             // z = M^{-1} v_k (batched V-cycle from zero), w = A z
             CK(cudaMemcpyAsync(ctx->bf[0], V + (i64)k * nk, sizeof(double) * nk, cudaMemcpyDeviceToDevice, st));
             if ((s = run_vcycle_b(ctx, K, st, true))) return s;
+            if (ctx->bZ)
+                CK(cudaMemcpyAsync(ctx->bZ + (i64)k * nk, ctx->bu[0], sizeof(double) * nk, cudaMemcpyDeviceToDevice, st));
             if (ctx->bgraph_zg_dlt[K])  // A z = v_k + (later-colour part of L_1) d (MODE 3)
                 b_spmv<3, K>(L0.stpr, N, L0.sptr, L0.scol, L0.sval, ctx->bdlt, ctx->bf[0], w, st, L0.sluw, L0.nlow);
             else
@@ -4349,13 +4353,18 @@ static mgm_status gmres_batch(mgm_ctx* ctx, int Kreal, double tol, int maxit, mg
         if (kmax > 0) {
             std::vector<double> yv(y.begin(), y.begin() + (size_t)kmax * K);
             if ((s = upload_coef(yv, h1))) return s;
-            launch(false, k_blincomb<K>, nb, 256, 0, st, N, kmax, (const double*)V, nk, (const double*)h1, 1.0, 0,
-                   ctx->bf[0]);
-            if ((s = run_vcycle_b(ctx, K, st, true))) return s;
-            std::vector<double> one(K, 1.0);
-            if ((s = upload_coef(one, coef))) return s;
-            launch(false, k_blincomb<K>, nb, 256, 0, st, N, 1, (const double*)ctx->bu[0], nk, (const double*)coef,
-                   1.0, 1, x);
+            if (ctx->bZ) {  // x += Z y (z_j = M v_j kept per step)
+                launch(false, k_blincomb<K>, nb, 256, 0, st, N, kmax, (const double*)ctx->bZ, nk, (const double*)h1,
+                       1.0, 1, x);
+            } else {
+                launch(false, k_blincomb<K>, nb, 256, 0, st, N, kmax, (const double*)V, nk, (const double*)h1, 1.0, 0,
+                       ctx->bf[0]);
+                if ((s = run_vcycle_b(ctx, K, st, true))) return s;
+                std::vector<double> one(K, 1.0);
+                if ((s = upload_coef(one, coef))) return s;
+                launch(false, k_blincomb<K>, nb, 256, 0, st, N, 1, (const double*)ctx->bu[0], nk, (const double*)coef,
+                       1.0, 1, x);
+            }
         }
         bool left = false;
         for (int c = 0; c < K; ++c) left = left || (!conv[c] && its[c] < maxit);
@@ -4653,6 +4662,7 @@ mgm_status mgm_destroy(mgm_ctx* ctx) {
     if (ctx->dB) dev_free(ctx->dB);
     if (ctx->d_dlt) dev_free(ctx->d_dlt);
     if (ctx->Z) dev_free(ctx->Z);
+    if (ctx->bZ) dev_free(ctx->bZ);
     if (ctx->bpart) dev_free(ctx->bpart);
     if (ctx->bdlt) dev_free(ctx->bdlt);
     if (ctx->d_dlt_pre) dev_free(ctx->d_dlt_pre);
