@@ -3016,19 +3016,20 @@ mgm_status gmres_dev(mgm_ctx* ctx, double tol, int maxit, mgm_report* rep, cudaS
     double* gg = Hh + (size_t)(m + 1) * m + 2 * (size_t)m;
     double* hist = gg + (m + 1);
     std::vector<double> y(m);
-    bool first = !ctx->warm;  // r0 = b - A x0 (x0 = 0: r0 = b, no SpMV)
+    bool first = !ctx->warm;  // r0 = b - A x0 (x0 = 0: r0 = b, no SpMV; ||r0||^2 is still in nr)
     while (true) {
+        double beta = bnorm;
         if (first) {  // r = b - A x ; beta
             CK(cudaMemcpyAsync(w, ctx->b, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
         } else {
             enqueue_apply_A(ctx, ctx->xs, w, st);
             k_axpby<<<RED_BLOCKS, 256, 0, st>>>(n, 1.0, ctx->b, -1.0, w, w);
+            enqueue_dot(ctx, n, w, w, nr, st);
+            CK(cudaMemcpyAsync(ctx->hh, nr, sizeof(double), cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            beta = std::sqrt(ctx->hh[0]);
         }
         first = false;
-        enqueue_dot(ctx, n, w, w, nr, st);
-        CK(cudaMemcpyAsync(ctx->hh, nr, sizeof(double), cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
-        const double beta = std::sqrt(ctx->hh[0]);
         if (beta / bnorm <= tol || its >= maxit) {
             converged = beta / bnorm <= tol;
             break;
