@@ -2810,8 +2810,13 @@ mgm_status gmres_lib(mgm_ctx* ctx, double tol, int maxit, mgm_report* rep, cudaS
             // CGS2 in 5 launches: h1 = V^T w; w -= V h1; h2 = V^T w (h1 += h2); w -= V h2 with
             // ||w||^2; v_{k+1} = w / ||w||.  Reductions finish in the last block (deterministic).
             enqueue_multidot(ctx, n, V, ld, k1, w, h1, nullptr, st);
-            k_multiaxpy<<<RED_BLOCKS * 2, 256, 0, st>>>(n, V, ld, k1, h1, w);
-            enqueue_multidot(ctx, n, V, ld, k1, w, h2, h1, st);
+            if (!dist_on(ctx)) {  // w -= V h1 and h2 = V^T w (h1 += h2) in one pass over V
+                k_multiaxpy_dot_fin<<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, V, ld, k1, h1, w, ctx->partials,
+                                                                        ctx->tickets, h2, h1);
+            } else {
+                k_multiaxpy<<<RED_BLOCKS * 2, 256, 0, st>>>(n, V, ld, k1, h1, w);
+                enqueue_multidot(ctx, n, V, ld, k1, w, h2, h1, st);
+            }
             if (!dist_on(ctx)) {
                 k_multiaxpy_norm<<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, V, ld, k1, h2, w, ctx->partials, ctx->tickets,
                                                                      nr);
@@ -2968,8 +2973,7 @@ static mgm_status build_gmres_graph(mgm_ctx* ctx) {
     // CGS2: h1 = V^T w; w -= V h1; h2 = V^T w (h1 += h2); w -= V h2, ||w||^2
     launch(true, k_multidot_fin, RED_BLOCKS, RED_THREADS, 0, st, n, (const double*)V, ld, 0, (const double*)w,
            ctx->partials, ctx->tickets, h1, (double*)nullptr, kdev);
-    launch(true, k_multiaxpy, RED_BLOCKS * 2, 256, 0, st, n, (const double*)V, ld, 0, (const double*)h1, w, kdev);
-    launch(true, k_multidot_fin, RED_BLOCKS, RED_THREADS, 0, st, n, (const double*)V, ld, 0, (const double*)w,
+    launch(true, k_multiaxpy_dot_fin, RED_BLOCKS, RED_THREADS, 0, st, n, (const double*)V, ld, 0, (const double*)h1, w,
            ctx->partials, ctx->tickets, h2, h1, kdev);
     launch(true, k_multiaxpy_norm, RED_BLOCKS, RED_THREADS, 0, st, n, (const double*)V, ld, 0, (const double*)h2, w,
            ctx->partials, ctx->tickets, nr, kdev);

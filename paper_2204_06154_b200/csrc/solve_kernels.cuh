@@ -606,6 +606,88 @@ __global__ void __launch_bounds__(RED_THREADS) k_multidot_fin(int64_t n, const d
     finish_partials(partials, k1, ticket, out, acc);
 }
 
+// CGS2's middle two passes in one launch: w -= V h1 (k_multiaxpy's per-row arithmetic), then
+// out[j] = V_j . w (k_multidot_fin's block chunks, per-thread order and finish; acc += out), on
+// each block's own rows -- no grid-wide dependency between the two, so one kernel.  For k1 <=
+// 16 a row's V entries are loaded once into registers and serve both; beyond, the block
+// re-reads its chunk for the dots.  Bitwise the unfused pair.
+__global__ void __launch_bounds__(RED_THREADS) k_multiaxpy_dot_fin(int64_t n, const double* __restrict__ V, int64_t ld,
+                                                                   int k1, const double* __restrict__ h,
+                                                                   double* __restrict__ w, double* __restrict__ partials,
+                                                                   unsigned* ticket, double* out, double* acc,
+                                                                   const int* kdev = nullptr) {
+    pdl_trigger();
+    pdl_wait();
+    if (kdev) k1 = *kdev + 1;
+    __shared__ double hs[256];
+    __shared__ double red[RED_THREADS / 32][MD_GROUP];
+    for (int j = threadIdx.x; j < k1; j += blockDim.x) hs[j] = h[j];
+    __syncthreads();
+    const int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
+    const int64_t b0 = blockIdx.x * chunk, b1 = min(n, b0 + chunk);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (k1 <= MD_GROUP) {
+        double s[MD_GROUP];
+#pragma unroll
+        for (int q = 0; q < MD_GROUP; ++q) s[q] = 0.0;
+        for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
+            double v[MD_GROUP];
+#pragma unroll
+            for (int q = 0; q < MD_GROUP; ++q) v[q] = (q < k1) ? V[(int64_t)q * ld + i] : 0.0;
+            double a = w[i];
+#pragma unroll
+            for (int q = 0; q < MD_GROUP; ++q)
+                if (q < k1) a -= v[q] * hs[q];
+            w[i] = a;
+#pragma unroll
+            for (int q = 0; q < MD_GROUP; ++q)
+                if (q < k1) s[q] = fma(v[q], a, s[q]);
+        }
+#pragma unroll
+        for (int q = 0; q < MD_GROUP; ++q) {
+            const double t = warp_sum(s[q]);
+            if (lane == 0) red[warp][q] = t;
+        }
+        __syncthreads();
+        if (threadIdx.x < k1) {
+            double t = 0.0;
+            for (int ww = 0; ww < RED_THREADS / 32; ++ww) t += red[ww][threadIdx.x];
+            partials[(int64_t)blockIdx.x * k1 + threadIdx.x] = t;
+        }
+    } else {
+        for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
+            double a = w[i];
+            for (int j = 0; j < k1; ++j) a -= V[(int64_t)j * ld + i] * hs[j];
+            w[i] = a;
+        }
+        for (int g = 0; g < k1; g += MD_GROUP) {  // (each thread re-reads only the rows it wrote)
+            const int gn = min(MD_GROUP, k1 - g);
+            double s[MD_GROUP];
+#pragma unroll
+            for (int q = 0; q < MD_GROUP; ++q) s[q] = 0.0;
+            for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
+                const double wi = w[i];
+#pragma unroll
+                for (int q = 0; q < MD_GROUP; ++q)
+                    if (q < gn) s[q] = fma(V[(int64_t)(g + q) * ld + i], wi, s[q]);
+            }
+#pragma unroll
+            for (int q = 0; q < MD_GROUP; ++q) {
+                const double t = warp_sum(s[q]);
+                if (lane == 0) red[warp][q] = t;
+            }
+            __syncthreads();
+            if (threadIdx.x < gn) {
+                double t = 0.0;
+                for (int ww = 0; ww < RED_THREADS / 32; ++ww) t += red[ww][threadIdx.x];
+                partials[(int64_t)blockIdx.x * k1 + g + threadIdx.x] = t;
+            }
+            __syncthreads();
+        }
+    }
+    finish_partials(partials, k1, ticket, out, acc);
+}
+
 // w[i] -= sum_j V_j[i] h[j]; nrm2[0] = ||w||^2 (block partials + last-block finish)
 __global__ void __launch_bounds__(RED_THREADS) k_multiaxpy_norm(int64_t n, const double* __restrict__ V, int64_t ld,
                                                                 int k1, const double* __restrict__ h,
