@@ -119,7 +119,9 @@ mgm_status mgm_vcycle(mgm_ctx* ctx, const double* f_dev, double* u_dev, void* cu
  *             preconditioner; on one GPU (shifted problems) each restart cycle
  *             runs as ONE CUDA-graph launch whose WHILE node iterates the Arnoldi steps with
  *             the Givens rotations on the device (MGM_HOST_GMRES=1: host-driven loop, same
- *             arithmetic up to rounding);  krylov = 0: standalone MGM;
+ *             arithmetic up to rounding); the preconditioned vectors z_k = M v_k are kept
+ *             (restart x N fp64 of device memory) and x += Z y ends a restart cycle;
+ *             krylov = 0: standalone MGM;
  * krylov = 2: right-preconditioned BiCGSTAB: report.iterations counts
  *             preconditioner applications (two per step) and report.history holds the
  *             relative residual after every half step; on a rho/omega breakdown it restarts
