@@ -1146,3 +1146,29 @@ def test_gmres_sweep_residual_identity(name, monkeypatch):
     xr, rr = P.ref.solve(P.w.rhs, tol=1e-10)
     assert abs(r3.iterations - rr.iterations) <= 1
     assert np.linalg.norm(x3 - xr) / np.linalg.norm(xr) <= 1e-9
+
+
+@pytest.mark.parametrize("name", ["cfg1", "torus20000", "poisson6000"])
+def test_gmres_z_basis_update(name, monkeypatch):
+    """x += Z y with the stored z_j = M v_j (the zero-guess V-cycle is linear) equals the
+    textbook x += M (V y) (MGM_GMRES_NO_Z=1): same iterations and residual history, solutions
+    to 1e-9 -- device GMRES and, for the Poisson case, the host-loop GMRES; restart = 5 so
+    several restart-cycle updates happen."""
+    import torch
+    from paper_2204_06154_b200 import MGM
+
+    P = pair(name)
+    lv = dict(P.w.levels, restart=5)
+    rhs = torch.from_numpy(P.w.rhs).cuda()
+    out = []
+    for noz in (False, True):
+        if noz:
+            monkeypatch.setenv("MGM_GMRES_NO_Z", "1")
+        m = MGM(P.w.points, P.w.normals, P.w.stencil, lv)
+        x, rep = m.solve(rhs, tol=1e-10, maxit=400)
+        out.append((x.cpu().numpy(), rep))
+        m.close()
+    (xz, rz), (xv, rv) = out
+    assert rz.converged and rv.converged and rz.iterations == rv.iterations > 5
+    assert np.allclose(rz.history, rv.history, rtol=0, atol=1e-9 * rv.history[0])
+    assert np.linalg.norm(xz - xv) / np.linalg.norm(xv) <= 1e-9
