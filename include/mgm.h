@@ -352,6 +352,11 @@ mgm_status mgm_device_knn(const double* points, int64_t n, const double* queries
                           int k, int32_t* out);
 /* Weighted sample elimination of n points down to nt (O8). keep[nt] ascending. */
 mgm_status mgm_host_wse(const double* points, int64_t n, int64_t nt, int64_t* keep);
+/* The same elimination on the GPU (the path mgm_setup takes unless MGM_HOST_WSE=1): host
+ * arrays in and out, copied through device buffers on the current device.  keep[nt]
+ * ascending, equal to mgm_host_wse's.  MGM_ERR_ARG for nt < 1 or nt > n; MGM_ERR_INPUT for
+ * duplicate points or no non-degenerate radius; MGM_ERR_CUDA on a CUDA error. */
+mgm_status mgm_device_wse(const double* points, int64_t n, int64_t nt, int64_t* keep);
 /* Greedy colouring (O11) of sym(pattern) minus the diagonal, vertices in index order.
  * CSR pattern ptr[n+1], col[ptr[n]]; colour[n] out; *n_colours out. */
 mgm_status mgm_host_colouring(int64_t n, const int64_t* ptr, const int32_t* col, int32_t* colour,

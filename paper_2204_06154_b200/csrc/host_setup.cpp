@@ -522,6 +522,16 @@ static bool wse_pass(const double* pts, i64 n, i64 nt, double R, std::vector<i64
     return true;
 }
 
+// O8: R = 2 r_max with r_max = r_h sqrt(N / N_t), r_h = half the median nearest-other distance
+double wse_initial_radius(const std::vector<double>& nn2, i64 n, i64 nt) {
+    std::vector<double> s(n);
+    for (i64 i = 0; i < n; ++i) s[i] = std::sqrt(nn2[i]);
+    std::nth_element(s.begin(), s.begin() + (n - 1) / 2, s.end());
+    double rh = 0.5 * s[(n - 1) / 2];
+    double rmax = rh * std::sqrt((double)n / (double)nt);
+    return 2.0 * rmax;
+}
+
 void wse_eliminate(const double* pts, i64 n, i64 nt, const std::vector<double>& nn2,
                    std::vector<i64>& keep, int nthreads) {
     keep.clear();
@@ -529,13 +539,8 @@ void wse_eliminate(const double* pts, i64 n, i64 nt, const std::vector<double>& 
         for (i64 i = 0; i < n; ++i) keep.push_back(i);
         return;
     }
-    std::vector<double> s(n);
-    for (i64 i = 0; i < n; ++i) s[i] = std::sqrt(nn2[i]);
-    std::nth_element(s.begin(), s.begin() + (n - 1) / 2, s.end());
-    double rh = 0.5 * s[(n - 1) / 2];
-    double rmax = rh * std::sqrt((double)n / (double)nt);
-    // O8: R = 2 r_max; a degenerate pass (zero-weight elimination) restarts with R *= 1.25
-    double R = 2.0 * rmax;
+    // O8: a degenerate pass (zero-weight elimination) restarts with R *= 1.25
+    double R = wse_initial_radius(nn2, n, nt);
     for (int attempt = 0; attempt < 16; ++attempt, R *= 1.25)
         if (wse_pass(pts, n, nt, R, keep, nthreads)) return;
 }

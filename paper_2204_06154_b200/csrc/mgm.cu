@@ -1132,8 +1132,10 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
             NR[3 * k + a] = normals[3 * perm[k] + a];
         }
     // duplicates (the nearest-other distances are level 0's WSE input too)
+    // (on the GPU after the upload below unless MGM_HOST_WSE=1 or N < 3)
+    const bool use_host_wse = std::getenv("MGM_HOST_WSE") && std::atoi(std::getenv("MGM_HOST_WSE")) != 0;
     std::vector<double> nn2_0;
-    {
+    if (use_host_wse || N < 3) {
         i64 dup = nearest_other(X.data(), N, nn2_0, nth);
         if (dup >= 0) return fail(ctx, MGM_ERR_INPUT, "duplicate points", perm[dup]);
     }
@@ -1160,6 +1162,17 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
     CK(dalloc(&dX, 3 * N));
     CK(dalloc(&dS, N * ns));
     CK(cudaMemcpyAsync(dX, X.data(), sizeof(double) * 3 * N, cudaMemcpyHostToDevice, st));
+    if (nn2_0.empty()) {
+        int e2 = 0;
+        i64 dup = nearest_other_device(X.data(), dX, N, nn2_0, st, &e2);
+        if (e2 || dup >= 0) {
+            dev_free(dX);
+            dev_free(dS);
+            if (e2) return fail(ctx, MGM_ERR_CUDA, "nearest-other kernels", -1);
+            return fail(ctx, MGM_ERR_INPUT, "duplicate points", perm[dup]);
+        }
+        tm.mark("duplicates (GPU)");
+    }
     std::vector<i32> sten((size_t)N * ns);
     if (knn_device(X.data(), dX, N, dX, N, ns, dS, st) == 0) {  // O2 stencils on the GPU
         CK(cudaMemcpyAsync(sten.data(), dS, sizeof(i32) * N * ns, cudaMemcpyDeviceToHost, st));
@@ -1411,14 +1424,26 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
     });
     for (int j = 0; j + 1 < p; ++j) {
         i64 nf = (i64)Xl[j].size() / 3, ncs = nf / lp.coarsen_factor;
-        // WSE, host
+        // WSE: rounds of local maxima on the GPU (wse_device; MGM_HOST_WSE=1: the
+        // host's threaded rounds -- the same survivors)
         std::vector<double> nn2;
-        if (j == 0)
+        if (j == 0) {
             nn2.swap(nn2_0);
-        else
+        } else if (use_host_wse || nf < 3) {
             nearest_other(Xl[j].data(), nf, nn2, nth);
+        } else {
+            int e2 = 0;
+            nearest_other_device(Xl[j].data(), dXf, nf, nn2, st, &e2);  // (coarse points: distinct)
+            if (e2) return fail(ctx, MGM_ERR_CUDA, "nearest-other kernels", -1);
+        }
         std::vector<i64> keep;
-        wse_eliminate(Xl[j].data(), nf, ncs, nn2, keep, nth);
+        if (use_host_wse) {
+            wse_eliminate(Xl[j].data(), nf, ncs, nn2, keep, nth);
+        } else {
+            rc = wse_device(dXf, Xl[j].data(), nf, ncs, nn2, keep, st);
+            if (rc) return fail(ctx, MGM_ERR_CUDA, "WSE kernels", -1);
+        }
+        if ((i64)keep.size() != ncs) return fail(ctx, MGM_ERR_INPUT, "WSE: no non-degenerate elimination radius", -1);
         tm.mark("WSE", j);
         Xl[j + 1].resize(3 * ncs);
         idsl[j + 1].resize(ncs);
@@ -5092,6 +5117,23 @@ mgm_status mgm_host_wse(const double* points, int64_t n, int64_t nt, int64_t* ke
     if (nearest_other(points, n, nn2, nth) >= 0) return MGM_ERR_INPUT;
     std::vector<i64> k;
     wse_eliminate(points, n, nt, nn2, k, nth);
+    std::copy(k.begin(), k.end(), keep);
+    return MGM_OK;
+}
+
+mgm_status mgm_device_wse(const double* points, int64_t n, int64_t nt, int64_t* keep) {
+    if (!points || !keep || nt < 1 || nt > n) return MGM_ERR_ARG;
+    int nth = std::max(1, (int)std::thread::hardware_concurrency());
+    std::vector<double> nn2;
+    if (nearest_other(points, n, nn2, nth) >= 0) return MGM_ERR_INPUT;
+    double* dp = nullptr;
+    if (cudaMalloc(&dp, sizeof(double) * 3 * n) != cudaSuccess) return MGM_ERR_CUDA;
+    std::vector<i64> k;
+    int rc = (int)cudaMemcpy(dp, points, sizeof(double) * 3 * n, cudaMemcpyHostToDevice);
+    if (!rc) rc = wse_device(dp, points, n, nt, nn2, k, nullptr);
+    cudaFree(dp);
+    if (rc) return MGM_ERR_CUDA;
+    if ((i64)k.size() != nt) return MGM_ERR_INPUT;
     std::copy(k.begin(), k.end(), keep);
     return MGM_OK;
 }

@@ -40,6 +40,7 @@ void knn_grid(const double* pts, i64 n, const double* qry, i64 nq, int k, std::v
 i64 nearest_other(const double* pts, i64 n, std::vector<double>& nn2, int nthreads);
 
 // Weighted sample elimination (O8): keep (size nt) = surviving indices, ascending.
+double wse_initial_radius(const std::vector<double>& nn2, i64 n, i64 nt);
 void wse_eliminate(const double* pts, i64 n, i64 nt, const std::vector<double>& nn2,
                    std::vector<i64>& keep, int nthreads);
 
@@ -102,6 +103,18 @@ int launch_interp_weights(const double* fine, i64 nf, const double* coarse, cons
 // host (bounding box); d_out[nq * k].  Synchronises the stream.
 int knn_device(const double* h_pts, const double* d_pts, i64 n, const double* d_qry, i64 nq, int k, i32* d_out,
                void* stream);
+
+// nearest_other on the device (the same nn2 bits; k = 3 lists from knn_device): the smallest
+// duplicate index or -1; *err a cudaError_t.
+i64 nearest_other_device(const double* h_pts, const double* d_pts, i64 n, std::vector<double>& nn2, void* stream,
+                         int* err);
+
+// Weighted sample elimination (O8) on the device: the same survivors as wse_eliminate (same
+// neighbour sets and fixed-point weights, the same rounds of local maxima, the same final
+// selection).  d_pts: the n points on the device; nn2: nearest-other squared distances (host).
+// keep: ascending survivor indices.  Synchronises the stream; returns a cudaError_t.
+int wse_device(const double* d_pts, const double* h_pts, i64 n, i64 nt, const std::vector<double>& nn2,
+               std::vector<i64>& keep, void* stream);
 
 // Device SpGEMM C = A B (CSR, columns ascending).  Symbolic pattern kept in full; values
 // summed in canonical order (O10), bit-identical to a sequential loop.

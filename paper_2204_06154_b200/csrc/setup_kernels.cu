@@ -5,6 +5,7 @@
 //   * batched GFD weights, one warp per stencil, Householder QR
 //   * batched PHS interpolation weights, one thread per fine point
 //   * SpGEMM for the Galerkin product, one CTA per output row, sort-based
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -940,6 +941,367 @@ int knn_device(const double* h_pts, const double* d_pts, i64 n, const double* d_
     e = cudaStreamSynchronize(st);
     if (e == cudaSuccess) e = cudaGetLastError();
     release();
+    return (int)e;
+}
+
+// Squared distance to the nearest other point (host_setup.cpp nearest_other, the same
+// arithmetic): from the 3 nearest (O2 order) of every point, the first entry that is not the
+// point itself.  dup: the smallest index with a zero distance (a duplicate), or n.
+__global__ void k_nearest_other(i64 n, const double* __restrict__ pts, const i32* __restrict__ nb,
+                                double* __restrict__ nn2, unsigned long long* __restrict__ dup) {
+    for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
+        const i32 j = nb[3 * i] == (i32)i ? nb[3 * i + 1] : nb[3 * i];
+        const double* x = pts + 3 * i;
+        const double* y = pts + 3 * (i64)j;
+        const double dx = y[0] - x[0], dy = y[1] - x[1], dz = y[2] - x[2];
+        const double d2 = (dx * dx + dy * dy) + dz * dz;
+        nn2[i] = d2;
+        if (d2 == 0.0) atomicMin(dup, (unsigned long long)i);
+    }
+}
+
+i64 nearest_other_device(const double* h_pts, const double* d_pts, i64 n, std::vector<double>& nn2, void* stream,
+                         int* err) {
+    cudaStream_t st = (cudaStream_t)stream;
+    *err = 0;
+    if (n < 3) { *err = (int)cudaErrorInvalidValue; return -1; }
+    i32* nb = nullptr;
+    double* d_nn2 = nullptr;
+    unsigned long long* d_dup = nullptr;
+    cudaError_t e = dev_malloc((void**)&nb, sizeof(i32) * 3 * n);
+    if (e == cudaSuccess) e = dev_malloc((void**)&d_nn2, sizeof(double) * n);
+    if (e == cudaSuccess) e = dev_malloc((void**)&d_dup, sizeof(unsigned long long));
+    unsigned long long h_dup = (unsigned long long)n;
+    if (e == cudaSuccess) e = (cudaError_t)knn_device(h_pts, d_pts, n, d_pts, n, 3, nb, stream);
+    if (e == cudaSuccess) {
+        cudaMemcpyAsync(d_dup, &h_dup, sizeof(h_dup), cudaMemcpyHostToDevice, st);
+        k_nearest_other<<<(unsigned)std::min<i64>((n + 255) / 256, 148 * 16), 256, 0, st>>>(n, d_pts, nb, d_nn2, d_dup);
+        nn2.resize(n);
+        cudaMemcpyAsync(nn2.data(), d_nn2, sizeof(double) * n, cudaMemcpyDeviceToHost, st);
+        cudaMemcpyAsync(&h_dup, d_dup, sizeof(h_dup), cudaMemcpyDeviceToHost, st);
+        e = cudaStreamSynchronize(st);
+    }
+    dev_free(nb);
+    dev_free(d_nn2);
+    dev_free(d_dup);
+    if (e != cudaSuccess) { *err = (int)e; return -1; }
+    return h_dup < (unsigned long long)n ? (i64)h_dup : -1;
+}
+
+// ---------------------------------------------------------------------------------------
+// Weighted sample elimination on the device (O8).  The same result as
+// host_setup.cpp's wse_pass, step for step:
+//   * neighbour sets {j != i : sqrt(d2) < R} with d2 = (dx^2 + dy^2) + dz^2 (-fmad=false: the
+//     host's rounding), W_ij = floor((1 - d/R)^8 2^40 + 0.5) as int64 and weight_i = sum_j W_ij
+//     (exact integers: the order of the neighbour lists does not matter);
+//   * rounds of local maxima: every live point of positive weight whose priority (weight
+//     desc, index asc) beats all its live neighbours' pops in this round with its current
+//     weight, then its live neighbours' weights drop by W (integer atomics commute);
+//   * the n - nt highest pop priorities are eliminated (stable radix sort, index order ties),
+//     or the pass is degenerate (fewer positive pops) and R grows by 1.25.
+// A dense cell table over the bounding box (cell side >= R, grown until it holds at most
+// 4n + 64 cells); one thread per point scans the cells that meet the box of half side R.
+// ---------------------------------------------------------------------------------------
+template <bool FILL>
+__global__ void __launch_bounds__(128) k_wse_nbrs(DevGrid g, const double* __restrict__ pts, const int* __restrict__ start,
+                                                  const i32* __restrict__ items, i64 n, double R,
+                                                  i64* __restrict__ cnt, const i64* __restrict__ ptr,
+                                                  i32* __restrict__ adj, i64* __restrict__ adjw,
+                                                  i64* __restrict__ weight) {
+    const double R2far = R * R * (1.0 + 1e-6);
+    const double Rm = R * (1.0 + 1e-6);
+    for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
+        const double x[3] = {pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]};
+        i64 lo[3], hi[3];
+        for (int a = 0; a < 3; ++a) {
+            lo[a] = max((i64)floor((x[a] - Rm - g.lo[a]) / g.cell), (i64)0);
+            hi[a] = min((i64)floor((x[a] + Rm - g.lo[a]) / g.cell), g.dims[a] - 1);
+        }
+        i64 c = 0, o = FILL ? ptr[i] : 0, wsum = 0;
+        for (i64 z = lo[2]; z <= hi[2]; ++z)
+            for (i64 y = lo[1]; y <= hi[1]; ++y)
+                for (i64 xx = lo[0]; xx <= hi[0]; ++xx) {
+                    const i64 cell = (z * g.dims[1] + y) * g.dims[0] + xx;
+                    for (int t = start[cell]; t < start[cell + 1]; ++t) {
+                        const i32 j = items[t];
+                        if (j == (i32)i) continue;
+                        const double* yv = pts + 3 * (i64)j;
+                        const double dx = yv[0] - x[0], dy = yv[1] - x[1], dz = yv[2] - x[2];
+                        const double d2 = (dx * dx + dy * dy) + dz * dz;
+                        if (d2 > R2far) continue;  // sqrt(d2) > R for certain
+                        const double d = sqrt(d2);
+                        if (!(d < R)) continue;
+                        if (FILL) {
+                            const double u = 1.0 - d / R;
+                            const double u2 = u * u;
+                            const double u4 = u2 * u2;
+                            const double u8 = u4 * u4;
+                            const i64 w = (i64)floor(u8 * 1099511627776.0 + 0.5);  // 2^40
+                            adj[o] = j;
+                            adjw[o] = w;
+                            ++o;
+                            wsum += w;
+                        } else {
+                            ++c;
+                        }
+                    }
+                }
+        if (FILL) weight[i] = wsum;
+        else cnt[i] = c;
+    }
+}
+
+// All rounds in one cooperative launch (grid barriers between the phases), the work of a
+// round limited to its candidates as in the host loop: round 0 every point of positive
+// weight, later rounds the live points within two hops of the previous round's pops (only
+// their neighbourhoods changed).  dead[x]: 0 live, r + 1 popped in round r (live at the start
+// of round r: 0 or > r).  Per round:
+//   A. each live candidate of positive weight that beats every live neighbour (weight desc,
+//      index asc) pops: dead = r + 1, popw = its weight, appended to pops;
+//   B. each pop lowers its live neighbours' weights by W (int64 atomics: the updates commute)
+//      and queues its live 1- and 2-hop neighbours (stamp: once per round) for round r + 1.
+// Ends after a round without pops; *total = the number of pops.
+struct WseRounds {
+    i64 n;
+    const i64* ptr;
+    const i32* adj;
+    const i64* adjw;
+    i64* weight;
+    int* dead;
+    int* stamp;
+    unsigned long long* popw;
+    i32* cand[2];
+    i32* pops;
+    unsigned long long* cnt;  // [0..1] candidates per parity, [2..3] pops per parity, [4] total
+};
+
+__global__ void __launch_bounds__(256) k_wse_rounds(WseRounds a) {
+    cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+    const i64 tid = blockIdx.x * (i64)blockDim.x + threadIdx.x, nth = (i64)gridDim.x * blockDim.x;
+    volatile unsigned long long* cnt = a.cnt;
+    for (int r = 0;; ++r) {
+        const int p = r & 1;
+        const i64 nc = (i64)cnt[p];
+        const i32* cand = a.cand[p];
+        if (tid == 0) cnt[p ^ 1] = 0;  // round r + 1's candidates (round r - 1 read them)
+        for (i64 q = tid; q < nc; q += nth) {
+            const i32 x = cand[q];
+            if (a.dead[x] != 0) continue;
+            const i64 wx = a.weight[x];
+            if (wx <= 0) continue;
+            bool top = true;
+            for (i64 t = a.ptr[x]; t < a.ptr[x + 1] && top; ++t) {
+                const i32 y = a.adj[t];
+                const int dy = *(volatile int*)&a.dead[y];
+                if (dy != 0 && dy <= r) continue;  // popped in an earlier round
+                const i64 wy = a.weight[y];
+                if (wy > wx || (wy == wx && y < x)) top = false;
+            }
+            if (top) {
+                a.dead[x] = r + 1;
+                a.popw[x] = (unsigned long long)wx;
+                a.pops[atomicAdd(&a.cnt[2 + p], 1ull)] = x;
+            }
+        }
+        grid.sync();
+        const i64 np = (i64)cnt[2 + p];
+        if (np == 0) break;
+        if (tid == 0) {
+            cnt[2 + (p ^ 1)] = 0;
+            cnt[4] += (unsigned long long)np;
+        }
+        i32* next = a.cand[p ^ 1];
+        auto queue = [&](i32 y) {
+            if (atomicExch(&a.stamp[y], r) != r) next[atomicAdd(&a.cnt[p ^ 1], 1ull)] = y;
+        };
+        for (i64 q = tid; q < np; q += nth) {
+            const i32 x = a.pops[q];
+            for (i64 t = a.ptr[x]; t < a.ptr[x + 1]; ++t) {
+                const i32 y = a.adj[t];
+                if (a.dead[y] != 0) continue;
+                atomicAdd((unsigned long long*)&a.weight[y], (unsigned long long)(-a.adjw[t]));
+                queue(y);
+                for (i64 t2 = a.ptr[y]; t2 < a.ptr[y + 1]; ++t2)
+                    if (a.dead[a.adj[t2]] == 0) queue(a.adj[t2]);
+            }
+        }
+        grid.sync();
+    }
+}
+
+__global__ void k_wse_cand0(i64 n, const i64* __restrict__ weight, i32* __restrict__ cand,
+                            unsigned long long* __restrict__ cnt) {
+    for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
+        if (weight[i] > 0) cand[atomicAdd(cnt, 1ull)] = (i32)i;
+}
+
+__global__ void k_iota_i32(i64 n, i32* __restrict__ v) {
+    for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) v[i] = (i32)i;
+}
+
+__global__ void k_wse_mark(i64 ne, const i32* __restrict__ order, uint8_t* __restrict__ elim) {
+    for (i64 q = blockIdx.x * (i64)blockDim.x + threadIdx.x; q < ne; q += (i64)gridDim.x * blockDim.x)
+        elim[order[q]] = 1;
+}
+
+int wse_device(const double* d_pts, const double* h_pts, i64 n, i64 nt, const std::vector<double>& nn2,
+               std::vector<i64>& keep, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    keep.clear();
+    if (nt >= n) {
+        for (i64 i = 0; i < n; ++i) keep.push_back(i);
+        return 0;
+    }
+    if (n >= ((i64)1 << 31)) return (int)cudaErrorInvalidValue;
+    const i64 ne = n - nt;
+    double lo3[3], hi3[3];
+    for (int a = 0; a < 3; ++a) lo3[a] = hi3[a] = h_pts[a];
+    for (i64 i = 0; i < n; ++i)
+        for (int a = 0; a < 3; ++a) {
+            lo3[a] = std::min(lo3[a], h_pts[3 * i + a]);
+            hi3[a] = std::max(hi3[a], h_pts[3 * i + a]);
+        }
+    i64 *cid = nullptr, *cnt = nullptr, *ptr = nullptr, *adjw = nullptr, *weight = nullptr;
+    int *gcnt = nullptr, *gfill = nullptr, *dead = nullptr;
+    i32 *items = nullptr, *adj = nullptr, *ord_in = nullptr, *ord_out = nullptr, *candA = nullptr, *candB = nullptr,
+        *pops = nullptr;
+    int* stamp = nullptr;
+    unsigned long long *popw = nullptr, *popw_out = nullptr, *npop = nullptr;
+    uint8_t* elim = nullptr;
+    void* tmp = nullptr;
+    size_t tmp_cap = 0;
+    auto release = [&] {
+        dev_free(cid); dev_free(cnt); dev_free(ptr); dev_free(adjw); dev_free(weight);
+        dev_free(gcnt); dev_free(gfill); dev_free(dead); dev_free(items); dev_free(adj);
+        dev_free(ord_in); dev_free(ord_out); dev_free(popw); dev_free(popw_out); dev_free(npop);
+        dev_free(elim); dev_free(tmp); dev_free(candA); dev_free(candB); dev_free(pops); dev_free(stamp);
+    };
+    auto need_tmp = [&](size_t b) -> cudaError_t {
+        if (b <= tmp_cap) return cudaSuccess;
+        dev_free(tmp);
+        tmp = nullptr;
+        tmp_cap = b;
+        return dev_malloc(&tmp, b);
+    };
+    cudaError_t e = dev_malloc((void**)&cid, sizeof(i64) * n);
+    if (e == cudaSuccess) e = dev_malloc((void**)&items, sizeof(i32) * n);
+    if (e == cudaSuccess) e = dev_malloc((void**)&cnt, sizeof(i64) * (n + 1));
+    if (e == cudaSuccess) e = dev_malloc((void**)&ptr, sizeof(i64) * (n + 1));
+    if (e == cudaSuccess) e = dev_malloc((void**)&weight, sizeof(i64) * n);
+    if (e == cudaSuccess) e = dev_malloc((void**)&dead, sizeof(int) * n);
+    if (e == cudaSuccess) e = dev_malloc((void**)&popw, sizeof(unsigned long long) * n);
+    if (e == cudaSuccess) e = dev_malloc((void**)&popw_out, sizeof(unsigned long long) * n);
+    if (e == cudaSuccess) e = dev_malloc((void**)&ord_in, sizeof(i32) * n);
+    if (e == cudaSuccess) e = dev_malloc((void**)&ord_out, sizeof(i32) * n);
+    if (e == cudaSuccess) e = dev_malloc((void**)&npop, sizeof(unsigned long long) * 5);
+    if (e == cudaSuccess) e = dev_malloc((void**)&elim, n);
+    if (e == cudaSuccess) e = dev_malloc((void**)&candA, sizeof(i32) * n);
+    if (e == cudaSuccess) e = dev_malloc((void**)&candB, sizeof(i32) * n);
+    if (e == cudaSuccess) e = dev_malloc((void**)&pops, sizeof(i32) * n);
+    if (e == cudaSuccess) e = dev_malloc((void**)&stamp, sizeof(int) * n);
+    if (e != cudaSuccess) { release(); return (int)e; }
+    const unsigned nb = (unsigned)std::min<i64>((n + 255) / 256, 148 * 16);
+    const unsigned nbq = (unsigned)std::min<i64>((n + 127) / 128, 148 * 64);
+    double R = wse_initial_radius(nn2, n, nt);
+    bool done = false;
+    for (int attempt = 0; attempt < 16 && !done; ++attempt, R *= 1.25) {
+        // cell table, side >= R
+        DevGrid g;
+        for (int a = 0; a < 3; ++a) g.lo[a] = lo3[a];
+        g.cell = R * (1.0 + 1e-6);
+        i64 total = 1;
+        for (;;) {
+            total = 1;
+            for (int a = 0; a < 3; ++a) {
+                g.dims[a] = std::max<i64>(1, (i64)std::floor((hi3[a] - g.lo[a]) / g.cell) + 1);
+                total *= g.dims[a];
+            }
+            if (total <= 4 * n + 64) break;
+            g.cell *= 1.26;
+        }
+        dev_free(gcnt);
+        dev_free(gfill);
+        gcnt = gfill = nullptr;
+        e = dev_malloc((void**)&gcnt, sizeof(int) * (total + 1));
+        if (e == cudaSuccess) e = dev_malloc((void**)&gfill, sizeof(int) * (total + 1));
+        size_t tb = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, tb, gcnt, gfill, (int)(total + 1), st);
+        if (e == cudaSuccess) e = need_tmp(std::max<size_t>(tb, 16));
+        if (e != cudaSuccess) { release(); return (int)e; }
+        cudaMemsetAsync(gcnt, 0, sizeof(int) * (total + 1), st);
+        k_grid_count<<<nb, 256, 0, st>>>(g, d_pts, n, cid, gcnt);
+        tb = tmp_cap;
+        cub::DeviceScan::ExclusiveSum(tmp, tb, gcnt, gfill, (int)(total + 1), st);
+        cudaMemcpyAsync(gcnt, gfill, sizeof(int) * (total + 1), cudaMemcpyDeviceToDevice, st);  // gcnt := start
+        k_grid_fill<<<nb, 256, 0, st>>>(n, cid, gfill, items);
+        // neighbour CSR
+        k_wse_nbrs<false><<<nbq, 128, 0, st>>>(g, d_pts, gcnt, items, n, R, cnt, nullptr, nullptr, nullptr, nullptr);
+        cudaMemsetAsync(cnt + n, 0, sizeof(i64), st);
+        tb = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, ptr, n + 1, st);
+        e = need_tmp(tb);
+        if (e != cudaSuccess) { release(); return (int)e; }
+        tb = tmp_cap;
+        cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, ptr, n + 1, st);
+        i64 nnz = 0;
+        cudaMemcpyAsync(&nnz, ptr + n, sizeof(i64), cudaMemcpyDeviceToHost, st);
+        e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) { release(); return (int)e; }
+        dev_free(adj);
+        dev_free(adjw);
+        adj = nullptr;
+        adjw = nullptr;
+        e = dev_malloc((void**)&adj, sizeof(i32) * std::max<i64>(nnz, 1));
+        if (e == cudaSuccess) e = dev_malloc((void**)&adjw, sizeof(i64) * std::max<i64>(nnz, 1));
+        if (e != cudaSuccess) { release(); return (int)e; }
+        k_wse_nbrs<true><<<nbq, 128, 0, st>>>(g, d_pts, gcnt, items, n, R, nullptr, ptr, adj, adjw, weight);
+        // rounds of local maxima until a round pops nothing (one cooperative launch)
+        cudaMemsetAsync(dead, 0, sizeof(int) * n, st);
+        cudaMemsetAsync(stamp, 0xff, sizeof(int) * n, st);  // -1
+        cudaMemsetAsync(popw, 0, sizeof(unsigned long long) * n, st);
+        cudaMemsetAsync(npop, 0, sizeof(unsigned long long) * 5, st);
+        k_wse_cand0<<<nb, 256, 0, st>>>(n, weight, candA, npop);
+        {
+            WseRounds wr{n, ptr, adj, adjw, weight, dead, stamp, popw, {candA, candB}, pops, npop};
+            int dev = 0, per_sm = 0, nsm = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_wse_rounds, 256, 0);
+            const i64 want = (n + 255) / 256;
+            const unsigned grid = (unsigned)std::max<i64>(1, std::min<i64>(want, (i64)std::max(per_sm, 1) * nsm));
+            void* args[] = {&wr};
+            e = cudaLaunchCooperativeKernel((const void*)k_wse_rounds, grid, 256, args, 0, st);
+            if (e != cudaSuccess) { release(); return (int)e; }
+        }
+        unsigned long long popped = 0;
+        cudaMemcpyAsync(&popped, npop + 4, sizeof(popped), cudaMemcpyDeviceToHost, st);
+        e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) { release(); return (int)e; }
+        if ((i64)popped < ne) continue;  // degenerate: R too small for this cloud (O8)
+        // the ne highest pop priorities (weight desc, index asc; unpopped points have key 0)
+        k_iota_i32<<<nb, 256, 0, st>>>(n, ord_in);
+        tb = 0;
+        cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, popw, popw_out, ord_in, ord_out, (int)n, 0, 64, st);
+        e = need_tmp(tb);
+        if (e != cudaSuccess) { release(); return (int)e; }
+        tb = tmp_cap;
+        cub::DeviceRadixSort::SortPairsDescending(tmp, tb, popw, popw_out, ord_in, ord_out, (int)n, 0, 64, st);
+        cudaMemsetAsync(elim, 0, n, st);
+        k_wse_mark<<<nb, 256, 0, st>>>(ne, ord_out, elim);
+        std::vector<uint8_t> h_elim(n);
+        cudaMemcpyAsync(h_elim.data(), elim, n, cudaMemcpyDeviceToHost, st);
+        e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) { release(); return (int)e; }
+        keep.reserve(nt);
+        for (i64 i = 0; i < n; ++i)
+            if (!h_elim[i]) keep.push_back(i);
+        done = true;
+    }
+    if (e == cudaSuccess) e = cudaGetLastError();
+    release();
+    if (e == cudaSuccess && !done) {  // 16 degenerate passes: the host loop's outcome (keep empty)
+        keep.clear();
+    }
     return (int)e;
 }
 

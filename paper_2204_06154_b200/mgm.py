@@ -104,6 +104,7 @@ _SIGS = {
     "mgm_host_knn": ([_f64p, _i64, _f64p, _i64, ctypes.c_int, _i32p], ctypes.c_int),
     "mgm_device_knn": ([_f64p, _i64, _f64p, _i64, ctypes.c_int, _i32p], ctypes.c_int),
     "mgm_host_wse": ([_f64p, _i64, _i64, _i64p], ctypes.c_int),
+    "mgm_device_wse": ([_f64p, _i64, _i64, _i64p], ctypes.c_int),
     "mgm_host_colouring": ([_i64, _i64p, _i32p, _i32p, ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
     "mgm_host_partition_level": ([_i64, _i64p, _i32p, _i32p, ctypes.c_int, _i32p, _i64, _i64p, _i32p, _i32p,
                                   _i64, _i64p, _i32p, _i32p, ctypes.c_int, ctypes.c_int,
@@ -471,6 +472,14 @@ def mgm_host_wse(points, nt):
     pts = np.ascontiguousarray(points, dtype=np.float64)
     keep = np.empty(nt, dtype=np.int64)
     _check(load_library().mgm_host_wse(_ptr(pts, _f64p), len(pts), nt, _ptr(keep, _i64p)))
+    return keep
+
+
+def mgm_device_wse(points, nt):
+    """The survivors of mgm_host_wse computed by the GPU path of mgm_setup."""
+    pts = np.ascontiguousarray(points, dtype=np.float64)
+    keep = np.empty(nt, dtype=np.int64)
+    _check(load_library().mgm_device_wse(_ptr(pts, _f64p), len(pts), nt, _ptr(keep, _i64p)))
     return keep
 
 

@@ -105,6 +105,35 @@ def test_device_knn_equals_oracle(case):
         assert np.array_equal(mgm_device_knn(pts, q, k).astype(np.int64), O.knn(pts, q, k)), (case, k)
 
 
+@pytest.mark.parametrize("case", ["sphere", "torus", "quartic_restart", "grid_ties", "torus_large"])
+def test_device_wse_equals_oracle(case):
+    """The GPU WSE (mgm_setup's S5 path: rounds of local maxima on the device) against the
+    oracle's sequential heap elimination (O8), exactly: jittered sphere, torus, the cfg4
+    quartic cloud whose median-spacing radius is degenerate (the R *= 1.25 restart runs), a
+    lattice full of exact weight ties; at 262,144 points against the host's threaded rounds."""
+    import mgm_inputs as MI
+    import oracle as O
+    from paper_2204_06154_b200.mgm import mgm_device_wse, mgm_host_wse
+
+    if case == "sphere":
+        x, _ = MI.fibonacci_sphere(20000, jitter=0.2, seed=2)
+    elif case == "torus":
+        x, _ = MI.torus_cloud(12000, seed=3)
+    elif case == "quartic_restart":
+        w = MI.make_workload(4, n=16384)
+        x = w.points[O.morton_perm(w.points)]
+    elif case == "grid_ties":
+        g = np.stack(np.meshgrid(np.arange(24.), np.arange(23.), np.arange(2.), indexing="ij"), -1)
+        x = g.reshape(-1, 3) * 0.5
+    else:
+        x, _ = MI.torus_cloud(262144, seed=7)
+        for nt in (len(x) // 4,):
+            assert np.array_equal(mgm_device_wse(x, nt), mgm_host_wse(x, nt))
+        return
+    for nt in (len(x) // 4, len(x) // 2, len(x) - 1):
+        assert np.array_equal(mgm_device_wse(x, nt), O.wse(x, nt)), (case, nt)
+
+
 def _rand(n, seed):
     return np.random.default_rng(seed).uniform(-1.0, 1.0, n)
 
