@@ -652,10 +652,6 @@ int colour_passes() {
     return e ? std::max(-1, std::atoi(e)) : 10;
 }
 
-// DSATUR (Brelaz): colour the uncoloured vertex of largest saturation (distinct colours among
-// its neighbours in sym(pattern) minus the diagonal), ties by larger degree (distinct
-// neighbours) then lower index, with the smallest colour unused by its neighbours.  Returns
-// the colour count, or -1 if a colour index would reach 256 (the caller falls back).
 // neighbours of each vertex in sym(pattern(A)) minus the diagonal: sorted, deduplicated.
 // Pattern transpose, then each row's union sorted in its own slot (threads over rows) and
 // compacted.
@@ -697,56 +693,60 @@ static void sym_adjacency(const HostCSR& A, std::vector<i64>& np, std::vector<i3
 }
 
 // The priority order (sat, deg, lower index) is total, so which vertex is taken next does not
-// depend on the queue's layout.  Vertices with sat = 0 sit in one array sorted by priority;
-// a vertex whose sat becomes >= 1 (it then outranks every sat = 0 vertex) enters an indexed
-// max-heap, where later sat increments sift it up in place.  next(): the heap's top while the
-// heap is non-empty, else the array's next uncoloured sat = 0 vertex.  The heap holds only
-// the colouring front, each vertex once.
-static int dsatur_colouring(i64 n, const std::vector<i64>& np, const std::vector<i32>& nb, std::vector<i32>& colour) {
-    std::vector<i32> sat(n, 0);
-    auto deg = [&](i64 v) { return np[v + 1] - np[v]; };
-    auto before = [&](i64 x, i64 y) {  // x has higher priority than y
-        if (sat[x] != sat[y]) return sat[x] > sat[y];
-        if (deg(x) != deg(y)) return deg(x) > deg(y);
-        return x < y;
-    };
-    std::vector<i64> a((size_t)n);
-    for (i64 i = 0; i < n; ++i) a[(size_t)i] = i;
-    std::sort(a.begin(), a.end(), before);  // all sat = 0 here
+// depend on the queue's layout.  It is packed into one 64-bit key per vertex,
+// sat << 56 | deg << 31 | (2^31 - 1 - index) (larger key = higher priority; deg < 2^25,
+// n < 2^31), so a comparison is one integer compare.  Vertices with sat = 0 sit in one array
+// sorted by priority; a vertex whose sat becomes >= 1 (it then outranks every sat = 0 vertex)
+// enters an indexed max-heap of keys, where later sat increments sift it up in place.
+// next(): the heap's top while the heap is non-empty, else the array's next uncoloured
+// sat = 0 vertex.  The heap holds only the colouring front, each vertex once.  W 64-bit words
+// of used-colour mask per vertex: W = 1 first (a colour index reaching 64 returns -1 and the
+// caller reruns with W = 4; the same choices either way).
+template <int W>
+static int dsatur_impl(i64 n, const std::vector<i64>& np, const std::vector<i32>& nb, std::vector<i32>& colour) {
+    constexpr int CMAX = 64 * W;
+    const uint64_t IMASK = 0x7fffffffull;
+    auto key0 = [&](i64 v) { return ((uint64_t)(np[v + 1] - np[v]) << 31) | (IMASK - (uint64_t)v); };
+    std::vector<uint64_t> a((size_t)n);
+    for (i64 i = 0; i < n; ++i) a[(size_t)i] = key0(i);
+    std::sort(a.begin(), a.end(), std::greater<uint64_t>());  // all sat = 0 here
     size_t ac = 0;
-    std::vector<i64> h, pos(n, -1);
-    auto up = [&](i64 k) {
-        const i64 v = h[k];
-        while (k > 0 && before(v, h[(k - 1) / 2])) {
+    std::vector<uint64_t> h;       // heap of keys
+    std::vector<i32> pos(n, -1);   // heap slot of a vertex, -1 if not in the heap
+    std::vector<uint8_t> sat(n, 0);
+    auto vert = [&](uint64_t k) { return (i64)(IMASK - (k & IMASK)); };
+    auto up = [&](i64 k, uint64_t key) {
+        while (k > 0 && key > h[(k - 1) / 2]) {
             h[k] = h[(k - 1) / 2];
-            pos[h[k]] = k;
+            pos[vert(h[k])] = (i32)k;
             k = (k - 1) / 2;
         }
-        h[k] = v;
-        pos[v] = k;
+        h[k] = key;
+        pos[vert(key)] = (i32)k;
     };
     auto pop = [&]() {
-        const i64 top = h[0], v = h.back();
+        const uint64_t top = h[0], last = h.back();
         h.pop_back();
-        pos[top] = -1;
-        if (h.empty()) return top;
+        pos[vert(top)] = -1;
+        if (h.empty()) return vert(top);
         const i64 m = (i64)h.size();
         i64 k = 0;
         for (;;) {
-            i64 l = 2 * k + 1, r = l + 1, c = k;
-            i64 best = v;
-            if (l < m && before(h[l], best)) { c = l; best = h[l]; }
-            if (r < m && before(h[r], best)) { c = r; best = h[r]; }
+            const i64 l = 2 * k + 1, r = l + 1;
+            i64 c = k;
+            uint64_t best = last;
+            if (l < m && h[l] > best) { c = l; best = h[l]; }
+            if (r < m && h[r] > best) { c = r; best = h[r]; }
             if (c == k) break;
             h[k] = h[c];
-            pos[h[k]] = k;
+            pos[vert(h[k])] = (i32)k;
             k = c;
         }
-        h[k] = v;
-        pos[v] = k;
-        return top;
+        h[k] = last;
+        pos[vert(last)] = (i32)k;
+        return vert(top);
     };
-    std::vector<uint64_t> bits((size_t)n * 4, 0);
+    std::vector<uint64_t> bits((size_t)n * W, 0);
     colour.assign(n, -1);
     int maxc = 0;
     for (i64 done = 0; done < n; ++done) {
@@ -754,29 +754,39 @@ static int dsatur_colouring(i64 n, const std::vector<i64>& np, const std::vector
         if (!h.empty()) {
             v = pop();
         } else {
-            while (colour[a[ac]] >= 0 || sat[a[ac]] != 0) ++ac;
-            v = a[ac++];
+            while (colour[vert(a[ac])] >= 0 || sat[vert(a[ac])] != 0) ++ac;
+            v = vert(a[ac++]);
         }
         int c = 0;
-        while (c < 256 && (bits[(size_t)v * 4 + (c >> 6)] >> (c & 63) & 1ull)) ++c;
-        if (c >= 256) return -1;
+        const uint64_t* bv = bits.data() + (size_t)v * W;
+        while (c < CMAX && (bv[c >> 6] >> (c & 63) & 1ull)) ++c;
+        if (c >= CMAX) return -1;
         colour[v] = c;
         maxc = std::max(maxc, c + 1);
+        const uint64_t cb = 1ull << (c & 63);
         for (i64 t = np[v]; t < np[v + 1]; ++t) {
             const i64 w = nb[t];
-            uint64_t& word = bits[(size_t)w * 4 + (c >> 6)];
-            if (colour[w] >= 0 || (word >> (c & 63) & 1ull)) continue;
-            word |= 1ull << (c & 63);
-            sat[w]++;
-            if (pos[w] < 0) {
-                h.push_back(w);
-                up((i64)h.size() - 1);
-            } else {
-                up(pos[w]);
-            }
+            uint64_t& word = bits[(size_t)w * W + (c >> 6)];
+            if ((word & cb) || colour[w] >= 0) continue;
+            word |= cb;
+            const int s1 = ++sat[w];
+            const uint64_t key = ((uint64_t)s1 << 56) | key0(w);
+            up(pos[w] < 0 ? (h.push_back(key), (i64)h.size() - 1) : (i64)pos[w], key);
         }
     }
     return maxc;
+}
+
+// DSATUR (Brelaz): colour the uncoloured vertex of largest saturation (distinct colours among
+// its neighbours in sym(pattern) minus the diagonal), ties by larger degree (distinct
+// neighbours) then lower index, with the smallest colour unused by its neighbours.  Returns
+// the colour count, or -1 if a colour index would reach 256 (the caller falls back).
+static int dsatur_colouring(i64 n, const std::vector<i64>& np, const std::vector<i32>& nb, std::vector<i32>& colour) {
+    if (n >= ((i64)1 << 31)) return -1;
+    for (i64 v = 0; v < n; ++v)
+        if (np[v + 1] - np[v] >= ((i64)1 << 25)) return -1;
+    const int c = dsatur_impl<1>(n, np, nb, colour);
+    return c > 0 ? c : dsatur_impl<4>(n, np, nb, colour);
 }
 
 // smallest colour not used by an already coloured neighbour of i (stamp: per-caller scratch)
