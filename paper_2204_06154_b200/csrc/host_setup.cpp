@@ -659,18 +659,25 @@ static int col_threads() { return std::max(1, std::min(64, (int)std::thread::har
 
 static void sym_adjacency(const HostCSR& A, std::vector<i64>& np, std::vector<i32>& nb) {
     const i64 n = A.nrows, nnz = A.nnz();
+    const int nt = col_threads();
+    // pattern transpose on threads (atomic counters: the order inside a transposed row is
+    // arbitrary, every row is sorted and deduplicated below)
     std::vector<i64> tp(n + 1, 0);
-    for (i64 t = 0; t < nnz; ++t) tp[A.col[t] + 1]++;
+    parallel_for(n, nt, [&](i64 b, i64 e) {
+        for (i64 t = A.ptr[b]; t < A.ptr[e]; ++t) __atomic_fetch_add(&tp[A.col[t] + 1], 1, __ATOMIC_RELAXED);
+    });
     for (i64 r = 0; r < n; ++r) tp[r + 1] += tp[r];
     std::vector<i32> tc((size_t)nnz);
     {
         std::vector<i64> fill(tp.begin(), tp.end() - 1);
-        for (i64 i = 0; i < n; ++i)
-            for (i64 t = A.ptr[i]; t < A.ptr[i + 1]; ++t) tc[(size_t)fill[A.col[t]]++] = (i32)i;
+        parallel_for(n, nt, [&](i64 b, i64 e) {
+            for (i64 i = b; i < e; ++i)
+                for (i64 t = A.ptr[i]; t < A.ptr[i + 1]; ++t)
+                    tc[(size_t)__atomic_fetch_add(&fill[A.col[t]], 1, __ATOMIC_RELAXED)] = (i32)i;
+        });
     }
     std::vector<i32> tmp((size_t)(2 * nnz));
     std::vector<i64> cnt(n + 1, 0);
-    const int nt = col_threads();
     parallel_for(n, nt, [&](i64 b, i64 e) {
         for (i64 i = b; i < e; ++i) {
             i32* o = tmp.data() + A.ptr[i] + tp[i];
