@@ -713,28 +713,42 @@ template <int W>
 static int dsatur_impl(i64 n, const std::vector<i64>& np, const std::vector<i32>& nb, std::vector<i32>& colour) {
     constexpr int CMAX = 64 * W;
     const uint64_t IMASK = 0x7fffffffull;
-    auto key0 = [&](i64 v) { return ((uint64_t)(np[v + 1] - np[v]) << 31) | (IMASK - (uint64_t)v); };
+    // one record per vertex (the fields the neighbour loop touches share a cache line):
+    // current key (sat in the top byte), used-colour mask, heap slot (-1: not in the heap),
+    // colour (-1: uncoloured)
+    struct alignas(W == 1 ? 32 : 64) VR {
+        uint64_t key;
+        uint64_t bits[W];
+        i32 pos;
+        i32 col;
+    };
+    std::vector<VR> vr((size_t)n);
+    for (i64 v = 0; v < n; ++v) {
+        VR& r = vr[(size_t)v];
+        r.key = ((uint64_t)(np[v + 1] - np[v]) << 31) | (IMASK - (uint64_t)v);
+        for (int q = 0; q < W; ++q) r.bits[q] = 0;
+        r.pos = -1;
+        r.col = -1;
+    }
     std::vector<uint64_t> a((size_t)n);
-    for (i64 i = 0; i < n; ++i) a[(size_t)i] = key0(i);
+    for (i64 i = 0; i < n; ++i) a[(size_t)i] = vr[(size_t)i].key;
     std::sort(a.begin(), a.end(), std::greater<uint64_t>());  // all sat = 0 here
     size_t ac = 0;
-    std::vector<uint64_t> h;       // heap of keys
-    std::vector<i32> pos(n, -1);   // heap slot of a vertex, -1 if not in the heap
-    std::vector<uint8_t> sat(n, 0);
+    std::vector<uint64_t> h;  // heap of keys
     auto vert = [&](uint64_t k) { return (i64)(IMASK - (k & IMASK)); };
     auto up = [&](i64 k, uint64_t key) {
         while (k > 0 && key > h[(k - 1) / 2]) {
             h[k] = h[(k - 1) / 2];
-            pos[vert(h[k])] = (i32)k;
+            vr[(size_t)vert(h[k])].pos = (i32)k;
             k = (k - 1) / 2;
         }
         h[k] = key;
-        pos[vert(key)] = (i32)k;
+        vr[(size_t)vert(key)].pos = (i32)k;
     };
     auto pop = [&]() {
         const uint64_t top = h[0], last = h.back();
         h.pop_back();
-        pos[vert(top)] = -1;
+        vr[(size_t)vert(top)].pos = -1;
         if (h.empty()) return vert(top);
         const i64 m = (i64)h.size();
         i64 k = 0;
@@ -746,41 +760,43 @@ static int dsatur_impl(i64 n, const std::vector<i64>& np, const std::vector<i32>
             if (r < m && h[r] > best) { c = r; best = h[r]; }
             if (c == k) break;
             h[k] = h[c];
-            pos[vert(h[k])] = (i32)k;
+            vr[(size_t)vert(h[k])].pos = (i32)k;
             k = c;
         }
         h[k] = last;
-        pos[vert(last)] = (i32)k;
+        vr[(size_t)vert(last)].pos = (i32)k;
         return vert(top);
     };
-    std::vector<uint64_t> bits((size_t)n * W, 0);
-    colour.assign(n, -1);
     int maxc = 0;
     for (i64 done = 0; done < n; ++done) {
         i64 v;
         if (!h.empty()) {
             v = pop();
         } else {
-            while (colour[vert(a[ac])] >= 0 || sat[vert(a[ac])] != 0) ++ac;
+            for (;; ++ac) {
+                const VR& r = vr[(size_t)vert(a[ac])];
+                if (r.col < 0 && (r.key >> 56) == 0) break;
+            }
             v = vert(a[ac++]);
         }
+        VR& rv = vr[(size_t)v];
         int c = 0;
-        const uint64_t* bv = bits.data() + (size_t)v * W;
-        while (c < CMAX && (bv[c >> 6] >> (c & 63) & 1ull)) ++c;
+        while (c < CMAX && (rv.bits[c >> 6] >> (c & 63) & 1ull)) ++c;
         if (c >= CMAX) return -1;
-        colour[v] = c;
+        rv.col = c;
         maxc = std::max(maxc, c + 1);
         const uint64_t cb = 1ull << (c & 63);
         for (i64 t = np[v]; t < np[v + 1]; ++t) {
-            const i64 w = nb[t];
-            uint64_t& word = bits[(size_t)w * W + (c >> 6)];
-            if ((word & cb) || colour[w] >= 0) continue;
+            VR& rw = vr[(size_t)nb[t]];
+            uint64_t& word = rw.bits[c >> 6];
+            if ((word & cb) || rw.col >= 0) continue;
             word |= cb;
-            const int s1 = ++sat[w];
-            const uint64_t key = ((uint64_t)s1 << 56) | key0(w);
-            up(pos[w] < 0 ? (h.push_back(key), (i64)h.size() - 1) : (i64)pos[w], key);
+            rw.key += 1ull << 56;  // sat + 1 (sat < 256: at most one per colour below CMAX)
+            up(rw.pos < 0 ? (h.push_back(rw.key), (i64)h.size() - 1) : (i64)rw.pos, rw.key);
         }
     }
+    colour.resize(n);
+    for (i64 v = 0; v < n; ++v) colour[v] = vr[(size_t)v].col;
     return maxc;
 }
 
