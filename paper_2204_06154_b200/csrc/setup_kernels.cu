@@ -1216,7 +1216,7 @@ int wse_device(const double* d_pts, const double* h_pts, i64 n, i64 nt, const st
                 g.dims[a] = std::max<i64>(1, (i64)std::floor((hi3[a] - g.lo[a]) / g.cell) + 1);
                 total *= g.dims[a];
             }
-            if (total <= 4 * n + 64) break;
+            if (total <= std::min<i64>(4 * n + 64, (i64)1 << 30)) break;  // (int cell offsets)
             g.cell *= 1.26;
         }
         dev_free(gcnt);

@@ -132,6 +132,15 @@ def test_device_wse_equals_oracle(case):
         return
     for nt in (len(x) // 4, len(x) // 2, len(x) - 1):
         assert np.array_equal(mgm_device_wse(x, nt), O.wse(x, nt)), (case, nt)
+    if case == "sphere":  # argument and input errors
+        from paper_2204_06154_b200 import MGMError
+        for bad in (0, len(x) + 1):
+            with pytest.raises(MGMError):
+                mgm_device_wse(x, bad)
+        y = x.copy()
+        y[7] = y[3]                                        # duplicate point
+        with pytest.raises(MGMError):
+            mgm_device_wse(y, len(y) // 4)
 
 
 def _rand(n, seed):
