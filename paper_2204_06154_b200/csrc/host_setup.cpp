@@ -5,6 +5,7 @@
 #include "mgm_internal.h"
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cmath>
 #include <cstring>
@@ -829,7 +830,7 @@ static inline i32 first_free(i64 i, i64 q, const std::vector<i64>& np, const std
 // Iterated-greedy passes visit the previous colour classes one after another; a class is an
 // independent set of sym(pattern), so no vertex of a class sees another of the same class,
 // and the class's vertices are coloured on threads with the result of the sequential visit.
-int greedy_colouring(const HostCSR& A, std::vector<i32>& colour, int passes) {
+int greedy_colouring(const HostCSR& A, std::vector<i32>& colour, int passes, int device) {
     const i64 n = A.nrows;
     std::vector<i64> np;
     std::vector<i32> nb;  // the symmetric adjacency, built once for every pass
@@ -848,6 +849,15 @@ int greedy_colouring(const HostCSR& A, std::vector<i32>& colour, int passes) {
         }
     }
     const int nt = col_threads();
+    if (device >= 0 && passes > 0 && ncol <= 255) {
+        const char* e = std::getenv("MGM_IG_DEVICE_MIN");
+        const i64 dmin = e ? std::atoll(e) : 65536;
+        if (n >= dmin) {
+            const int nc = ig_passes_device(n, np.data(), nb.data(), colour.data(), ncol, passes, device);
+            if (nc > 0) return nc;
+            std::fprintf(stderr, "[mgm] device colouring passes failed (%d); host passes\n", nc);
+        }
+    }
     std::vector<i64> order(n);
     for (int pass = 1; pass <= std::max(passes, 0); ++pass) {
         // descending previous colour, ascending index within a colour

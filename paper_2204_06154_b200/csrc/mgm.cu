@@ -1238,10 +1238,12 @@ mgm_status do_setup(mgm_ctx* ctx, const double* points, const double* normals, i
                 if (t.joinable()) t.join();
         }
     } colour_th{&l0_values, {}};
+    int setup_dev = 0;
+    cudaGetDevice(&setup_dev);
     auto start_colouring = [&](int j, const HostCSR* A) {
         if (j + 1 >= p) return;
         colour_th.th.emplace_back([&, j, A] {
-            const int nc = greedy_colouring(*A, colour_mor[j], colour_passes());
+            const int nc = greedy_colouring(*A, colour_mor[j], colour_passes(), setup_dev);
             ncol_j[j] = nc;
             LevelPack& q = pk[j];
             const std::vector<i32>& cm = colour_mor[j];

@@ -45,7 +45,12 @@ void wse_eliminate(const double* pts, i64 n, i64 nt, const std::vector<double>& 
                    std::vector<i64>& keep, int nthreads);
 
 // Greedy colouring (O11) of sym(pattern(A)) minus the diagonal in index order.
-int greedy_colouring(const HostCSR& A, std::vector<i32>& colour, int passes);
+// device >= 0: the iterated-greedy passes run on that GPU (ig_passes_device) for patterns of
+// at least MGM_IG_DEVICE_MIN (default 65536) rows -- the same colours.
+int greedy_colouring(const HostCSR& A, std::vector<i32>& colour, int passes, int device = -1);
+// Iterated-greedy passes on the device from a colouring with ncol <= 255 colours (host CSR
+// adjacency in, colours in/out): the new colour count, or -cudaError_t.
+int ig_passes_device(i64 n, const i64* np, const i32* nb, i32* colour, int ncol, int passes, int device);
 // O11 iterated-greedy passes: 10, or MGM_COLOUR_PASSES (experiments; the oracle must match)
 int colour_passes();
 

@@ -1305,6 +1305,115 @@ int wse_device(const double* d_pts, const double* h_pts, i64 n, i64 nt, const st
     return (int)e;
 }
 
+// ---------------------------------------------------------------------------------------
+// Iterated-greedy colouring passes on the device (O11; host_setup.cpp greedy_colouring):
+// each pass visits the previous colour classes by descending colour and gives every vertex
+// the smallest colour unused by its neighbours already coloured in this pass.  A class is an
+// independent set of sym(pattern), so its vertices are coloured by one launch with the
+// sequential visit's result.  Classes: stable 8-bit radix sort of (ncol - 1 - colour) with
+// the vertex indices (ascending within a class).  Plain cudaMalloc on a private stream: this
+// runs on the setup's background colouring threads.
+// ---------------------------------------------------------------------------------------
+__global__ void k_ig_keys(i64 n, const i32* __restrict__ colour, int ncol, uint8_t* __restrict__ key,
+                          i32* __restrict__ idx, int* __restrict__ cnt) {
+    for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
+        key[i] = (uint8_t)(ncol - 1 - colour[i]);
+        idx[i] = (i32)i;
+        atomicAdd(&cnt[colour[i]], 1);
+    }
+}
+
+__global__ void k_ig_class(i64 len, const i32* __restrict__ ord, const i64* __restrict__ np,
+                           const i32* __restrict__ nb, i32* colour, int* __restrict__ maxc) {
+    int m = 0;
+    for (i64 q = blockIdx.x * (i64)blockDim.x + threadIdx.x; q < len; q += (i64)gridDim.x * blockDim.x) {
+        const i32 i = ord[q];
+        uint64_t used[4] = {0, 0, 0, 0};
+        for (i64 t = np[i]; t < np[i + 1]; ++t) {
+            const int c = colour[nb[t]];
+            if (c >= 0) used[c >> 6] |= 1ull << (c & 63);
+        }
+        int c = 0;
+        for (int w = 0; w < 4; ++w)
+            if (~used[w]) {
+                c = 64 * w + __ffsll((long long)~used[w]) - 1;
+                break;
+            }
+        colour[i] = c;
+        m = max(m, c + 1);
+    }
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_down_sync(FULL, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(maxc, m);
+}
+
+int ig_passes_device(i64 n, const i64* h_np, const i32* h_nb, i32* h_colour, int ncol, int passes, int device) {
+    if (ncol < 1 || ncol > 255 || n >= ((i64)1 << 31)) return -(int)cudaErrorInvalidValue;
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) return -(int)e;
+    cudaStream_t st = nullptr;
+    e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return -(int)e;
+    const i64 nnz = h_np[n];
+    i64* np = nullptr;
+    i32 *nb = nullptr, *cp = nullptr, *cn = nullptr, *idx = nullptr, *ord = nullptr;
+    uint8_t *key = nullptr, *key2 = nullptr;
+    int* cnt = nullptr;  // [256] class sizes, [256] max colour
+    void* tmp = nullptr;
+    size_t tb = 0;
+    auto release = [&] {
+        cudaFree(np); cudaFree(nb); cudaFree(cp); cudaFree(cn); cudaFree(idx); cudaFree(ord);
+        cudaFree(key); cudaFree(key2); cudaFree(cnt); cudaFree(tmp);
+        cudaStreamDestroy(st);
+    };
+    e = cudaMalloc(&np, sizeof(i64) * (n + 1));
+    if (e == cudaSuccess) e = cudaMalloc(&nb, sizeof(i32) * std::max<i64>(nnz, 1));
+    if (e == cudaSuccess) e = cudaMalloc(&cp, sizeof(i32) * n);
+    if (e == cudaSuccess) e = cudaMalloc(&cn, sizeof(i32) * n);
+    if (e == cudaSuccess) e = cudaMalloc(&idx, sizeof(i32) * n);
+    if (e == cudaSuccess) e = cudaMalloc(&ord, sizeof(i32) * n);
+    if (e == cudaSuccess) e = cudaMalloc(&key, n);
+    if (e == cudaSuccess) e = cudaMalloc(&key2, n);
+    if (e == cudaSuccess) e = cudaMalloc(&cnt, sizeof(int) * 257);
+    if (e == cudaSuccess) cub::DeviceRadixSort::SortPairs(nullptr, tb, key, key2, idx, ord, (int)n, 0, 8, st);
+    if (e == cudaSuccess) e = cudaMalloc(&tmp, std::max<size_t>(tb, 16));
+    if (e != cudaSuccess) { release(); return -(int)e; }
+    cudaMemcpyAsync(np, h_np, sizeof(i64) * (n + 1), cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(nb, h_nb, sizeof(i32) * nnz, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(cp, h_colour, sizeof(i32) * n, cudaMemcpyHostToDevice, st);
+    const unsigned nb1 = (unsigned)std::min<i64>((n + 255) / 256, 148 * 16);
+    std::vector<int> h_cnt(257);
+    for (int pass = 1; pass <= passes; ++pass) {
+        cudaMemsetAsync(cnt, 0, sizeof(int) * 257, st);
+        k_ig_keys<<<nb1, 256, 0, st>>>(n, cp, ncol, key, idx, cnt);
+        size_t t2 = tb;
+        cub::DeviceRadixSort::SortPairs(tmp, t2, key, key2, idx, ord, (int)n, 0, 8, st);
+        cudaMemcpyAsync(h_cnt.data(), cnt, sizeof(int) * ncol, cudaMemcpyDeviceToHost, st);
+        cudaMemsetAsync(cn, 0xff, sizeof(i32) * n, st);  // -1: not yet coloured in this pass
+        e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) { release(); return -(int)e; }
+        i64 off = 0;
+        for (int k = 0; k < ncol; ++k) {  // class k = previous colour ncol - 1 - k
+            const i64 len = h_cnt[ncol - 1 - k];
+            if (len > 0) {
+                const unsigned g = (unsigned)std::min<i64>((len + 127) / 128, 148 * 16);
+                k_ig_class<<<g, 128, 0, st>>>(len, ord + off, np, nb, cn, cnt + 256);
+            }
+            off += len;
+        }
+        int nc = 0;
+        cudaMemcpyAsync(&nc, cnt + 256, sizeof(int), cudaMemcpyDeviceToHost, st);
+        e = cudaStreamSynchronize(st);
+        if (e == cudaSuccess) e = cudaGetLastError();
+        if (e != cudaSuccess) { release(); return -(int)e; }
+        std::swap(cp, cn);
+        ncol = nc;
+    }
+    e = cudaMemcpyAsync(h_colour, cp, sizeof(i32) * n, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    release();
+    return e == cudaSuccess ? ncol : -(int)e;
+}
+
 int spgemm_device(const DevCSR& A, const DevCSR& B, DevCSR& C, void* stream, std::string& err) {
     cudaStream_t st = (cudaStream_t)stream;
     C = DevCSR();

@@ -62,6 +62,25 @@ def test_structures_exact(name):
             assert relmax(g["border"], o.c[pos[g["ids"]]]) <= 1e-13
 
 
+@pytest.mark.parametrize("name", ["torus20000", "poisson6000"])
+def test_device_colouring_passes(name, monkeypatch):
+    """The iterated-greedy colouring passes on the GPU (ig_passes_device, forced on every level
+    with MGM_IG_DEVICE_MIN=0) give the oracle's colours (O11) on every level."""
+    from paper_2204_06154_b200 import MGM, mgm_export_level
+
+    monkeypatch.setenv("MGM_IG_DEVICE_MIN", "0")
+    P = pair(name)
+    w = CASES[name]()
+    g = MGM(w.points, w.normals, w.stencil, w.levels)
+    try:
+        for j in range(P.ref.p - 1):
+            d = mgm_export_level(g.ctx, j, P.poisson)
+            o = P.ref.levels[j]
+            assert np.array_equal(d["colour"], o.colour[P.oracle_pos(j)[d["ids"]]]), j
+    finally:
+        g.close()
+
+
 @pytest.mark.parametrize("name", list(CASES))
 def test_fine_weights(name):
     from paper_2204_06154_b200 import mgm_export_weights
