@@ -486,6 +486,27 @@ def test_error_paths():
         MGM(w.points, w.normals, dict(w.stencil, stencil_n=0), w.levels)
     with pytest.raises(MGMError):
         MGM(w.points, w.normals, w.stencil, dict(w.levels, num_levels=9))
+    bad = w.points.copy()
+    bad[17, 1] = np.nan                                    # non-finite coordinate: index = the point
+    with pytest.raises(MGMError) as e:
+        MGM(bad, w.normals, w.stencil, w.levels)
+    assert e.value.status == 8 and e.value.index == 17
+    nbad = w.normals.copy()
+    nbad[5, 2] = np.inf                                    # non-finite normal
+    with pytest.raises(MGMError) as e:
+        MGM(w.points, nbad, w.stencil, w.levels)
+    assert e.value.status == 8 and e.value.index == 5
+    with pytest.raises(MGMError):                          # fewer points than one stencil
+        k = w.stencil["stencil_n"] - 1
+        MGM(w.points[:k], w.normals[:k], w.stencil, dict(w.levels, num_levels=1))
+    with pytest.raises(MGMError):                          # empty cloud
+        MGM(w.points[:0], w.normals[:0], w.stencil, dict(w.levels, num_levels=1))
+    # after every failed setup the library still builds and solves (no sticky state)
+    m = MGM(w.points, w.normals, w.stencil, w.levels)
+    import torch
+    x, rep = m.solve(torch.from_numpy(w.rhs).cuda(), tol=1e-10)
+    assert rep.converged
+    m.close()
 
 
 @pytest.mark.parametrize("name", ["cfg1", "torus20000", "gfd9000"])
